@@ -33,6 +33,7 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -1806,6 +1807,25 @@ int orc_block_apply(orc_block* b, const double* x, double* y) {
   Vec xv(x, x + b->J.n_u() + b->J.n_phi());
   Vec yv = b->J.apply(xv);
   std::copy(yv.begin(), yv.end(), y);
+  return 0;
+}
+// SpMV of one block with `threads` OpenMP threads (row-parallel; each row summed sequentially,
+// so the result is independent of the thread count).  Used for the bounded CPU baseline.
+int orc_block_spmv_threads(orc_block* b, int which, const double* x, double* y, int threads) {
+  const Csr& A = blk_of(b, which);
+  threads = std::max(1, threads);
+  auto work = [&](i64 lo, i64 hi) {
+    for (i64 i = lo; i < hi; ++i) {
+      double s = 0.0;
+      for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) s += A.val[k] * x[A.col[k]];
+      y[i] = s;
+    }
+  };
+  std::vector<std::thread> pool;
+  const i64 chunk = (A.rows + threads - 1) / threads;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back(work, std::min(A.rows, t * chunk), std::min(A.rows, (t + 1) * chunk));
+  for (auto& th : pool) th.join();
   return 0;
 }
 // SpMV of one block (used for the bounded CPU-baseline sample)

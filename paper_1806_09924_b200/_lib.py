@@ -1,0 +1,136 @@
+"""Loader of libcrackfield_b200.so (the C ABI declared in include/crackfield_b200.h).
+
+The library is built in-tree by __graft_entry__.build() (nvcc, sm_100a).  There is no
+fallback: if the shared object is missing or no CUDA device is present, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcrackfield_b200.so")
+
+CF_OK = 0
+ERRORS = {1: ValueError, 2: RuntimeError, 3: RuntimeError, 4: RuntimeError, 5: MemoryError, 6: NotImplementedError}
+
+
+class CfError(RuntimeError):
+    pass
+
+
+class Material(C.Structure):
+    """model.hpp:14-30 (eps_mode 0 = tied, 1 = fixed; pressure_coupling 0 = extrapolated)."""
+    _fields_ = [("E", C.c_double), ("nu", C.c_double), ("G_c", C.c_double), ("pressure", C.c_double),
+                ("l0", C.c_double), ("kappa_factor", C.c_double), ("eps_mode", C.c_int),
+                ("c_eps", C.c_double), ("eps_fixed", C.c_double), ("pressure_coupling", C.c_int)]
+
+    def __init__(self, **kw):
+        d = dict(E=1.0, nu=0.2, G_c=1.0, pressure=1e-3, l0=1.0, kappa_factor=1e-12, eps_mode=0, c_eps=2.0,
+                 eps_fixed=0.0625, pressure_coupling=0)
+        d.update(kw)
+        super().__init__(**d)
+
+    def mu(self):
+        return self.E / (2.0 * (1.0 + self.nu))
+
+    def lam(self):
+        return self.E * self.nu / ((1.0 + self.nu) * (1.0 - 2.0 * self.nu))
+
+
+class Regularization(C.Structure):
+    """model.hpp:38-41."""
+    _fields_ = [("eps", C.c_double), ("kappa", C.c_double)]
+
+
+class AmgOptions(C.Structure):
+    """linsolve.hpp:51-60."""
+    _fields_ = [("strength_threshold", C.c_double), ("prolongation_omega", C.c_double),
+                ("jacobi_omega", C.c_double), ("smoothing_sweeps", C.c_int), ("coarse_size", C.c_int),
+                ("max_levels", C.c_int)]
+
+    def __init__(self, **kw):
+        d = dict(strength_threshold=0.02, prolongation_omega=2.0 / 3.0, jacobi_omega=2.0 / 3.0,
+                 smoothing_sweeps=1, coarse_size=64, max_levels=25)
+        d.update(kw)
+        super().__init__(**d)
+
+
+class GmresOptions(C.Structure):
+    """linsolve.hpp:32-36."""
+    _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int), ("restart", C.c_int)]
+
+    def __init__(self, **kw):
+        d = dict(rtol=1e-8, max_iter=1000, restart=100)
+        d.update(kw)
+        super().__init__(**d)
+
+
+class SolverOptions(C.Structure):
+    """solver.hpp:13-26 (prec_kind 0 exact, 1 amg, 2 diagonal)."""
+    _fields_ = [("newton_tol", C.c_double), ("newton_abs_floor", C.c_double), ("newton_max_iter", C.c_int),
+                ("active_set_c_scale", C.c_double), ("cycle_window", C.c_int), ("cycle_toggles", C.c_int),
+                ("damping", C.c_int), ("prec_kind", C.c_int), ("freeze_preconditioner", C.c_int),
+                ("log", C.c_int), ("gmres", GmresOptions), ("amg", AmgOptions)]
+
+    def __init__(self, **kw):
+        d = dict(newton_tol=1e-8, newton_abs_floor=1e-11, newton_max_iter=50, active_set_c_scale=100.0,
+                 cycle_window=8, cycle_toggles=3, damping=0, prec_kind=1, freeze_preconditioner=0, log=0,
+                 gmres=GmresOptions(), amg=AmgOptions())
+        d.update(kw)
+        super().__init__(**d)
+
+
+_lib = None
+
+# (name, restype, argtypes); the not-gpu test checks every symbol of include/crackfield_b200.h is here
+_P = C.c_void_p
+_D = C.c_double
+_I = C.c_int
+_L = C.c_int64
+_PD = C.POINTER(C.c_double)
+SIGNATURES = [
+    ("cf_last_error", C.c_char_p, []),
+    ("cf_version", _I, []),
+    ("cf_device_info", _I, [C.POINTER(_I), C.POINTER(_I), C.POINTER(_L)]),
+    ("cf_set_stream", _I, [_P]),
+    ("cf_synchronize", _I, []),
+    ("cf_kernel_launches", _L, []),
+    ("cf_problem_create_uniform", _I, [_I, _D, _I, _I, C.POINTER(_P)]),
+    ("cf_problem_destroy", _I, [_P]),
+    ("cf_problem_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_D)]),
+    ("cf_constraints_build", _I, [_P, _I, _L, _P, _P, C.POINTER(_P)]),
+    ("cf_constraints_destroy", _I, [_P]),
+    ("cf_constraints_distribute", _I, [_P, _P, _I]),
+    ("cf_assemble_residual", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, _P]),
+    ("cf_assemble_jacobian", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, C.POINTER(_P)]),
+    ("cf_block_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),
+    ("cf_block_export", _I, [_P, _I, _P, _P, _P]),
+    ("cf_block_apply", _I, [_P, _P, _P]),
+    ("cf_block_spmv", _I, [_P, _I, _P, _P]),
+    ("cf_block_destroy", _I, [_P]),
+]
+
+
+def load(path: str | None = None):
+    """Load the library and bind the C ABI.  Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(f"crackfield_b200: {path} is missing; run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def check(rc: int):
+    if rc != CF_OK:
+        msg = load().cf_last_error().decode()
+        raise ERRORS.get(rc, CfError)(msg)

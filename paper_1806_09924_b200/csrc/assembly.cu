@@ -1,0 +1,747 @@
+// K1 residual and K2 Jacobian assembly on a uniform Q1 grid.
+//
+// Reference: assemble_residual / assemble_jacobian (proj/src/model.cpp:127-322).  The
+// reference loops cells, builds element vectors/matrices, and scatters them through the
+// constraint set into triplets summed by setFromTriplets (duplicates summed in insertion =
+// cell order).  The B200 design is atomic-free and deterministic:
+//   * a cell-centric pass computes the per-cell quadrature-point state (or, for the residual,
+//     the element vector) once per cell and writes it to an HBM scratch array;
+//   * a vertex-centric pass owns its rows and gathers the contributions of its 2^d cells in
+//     the reference's cell order (root-lexicographic, then hierarchical z-order), so every
+//     entry is the same sequence of IEEE operations as the reference's: this file is compiled
+//     with -fmad=false and mirrors the reference's expression order term by term;
+//   * the CSR pattern is the geometric 3^d stencil minus constrained rows/columns, with a
+//     diagonal kept on constrained rows iff its summed value is non-zero (model.cpp:308-311);
+//     row pointers come from a count pass + device scan, so no triplets are materialised
+//     (the reference's triplet path would need ~65 GB at config 1).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "cf_types.hpp"
+
+namespace cfb {
+
+namespace {
+
+// ------------------------------------------------------------------ cell order
+// Reference active-cell order after uniform_refine (mesh.cpp:147-169, 209-215).
+__host__ __device__ inline i64 cell_key(const GridDesc& g, i64 cx, i64 cy, i64 cz) {
+  const i64 mask = (i64(1) << g.r) - 1;
+  const i64 rx = cx >> g.r, ry = cy >> g.r, rz = cz >> g.r;
+  const i64 lx = cx & mask, ly = cy & mask, lz = cz & mask;
+  i64 m = 0;
+  for (int j = 0; j < g.r; ++j) {
+    m |= ((lx >> j) & 1) << (g.d * j);
+    m |= ((ly >> j) & 1) << (g.d * j + 1);
+    if (g.d == 3) m |= ((lz >> j) & 1) << (g.d * j + 2);
+  }
+  const i64 root = rx + i64(g.n0) * (ry + i64(g.n0) * rz);
+  return (root << (g.d * g.r)) | m;
+}
+
+template <int D>
+struct CellList {
+  int n;
+  i64 cell[1 << D];
+  int kv[1 << D];  // local index of the row vertex in the cell
+  int kw[1 << D];  // local index of the column vertex (pair lists)
+};
+
+// Cells containing both v=(x,y,z) and w=v+delta, in reference order.
+template <int D>
+__device__ inline void common_cells(const GridDesc& g, i64 x, i64 y, i64 z, int dx, int dy, int dz,
+                                    CellList<D>& L) {
+  L.n = 0;
+  i64 key[1 << D];
+  const int del[3] = {dx, dy, dz};
+  const i64 vc[3] = {x, y, z};
+  for (int t = 0; t < (1 << D); ++t) {
+    bool ok = true;
+    i64 anc[3] = {0, 0, 0};
+    int kv = 0, kw = 0;
+    for (int a = 0; a < D; ++a) {
+      const int ta = (t >> a) & 1;  // 1: v is the high corner of the cell along axis a
+      const int la = ta + del[a];
+      anc[a] = vc[a] - ta;
+      if (la < 0 || la > 1 || anc[a] < 0 || anc[a] >= g.nc) ok = false;
+      kv |= ta << a;
+      kw |= la << a;
+    }
+    if (!ok) continue;
+    const i64 c = anc[0] + g.nc * (anc[1] + g.nc * anc[2]);
+    const i64 k = cell_key(g, anc[0], anc[1], anc[2]);
+    int p = L.n++;
+    while (p > 0 && key[p - 1] > k) {  // insertion sort by reference order
+      key[p] = key[p - 1];
+      L.cell[p] = L.cell[p - 1];
+      L.kv[p] = L.kv[p - 1];
+      L.kw[p] = L.kw[p - 1];
+      --p;
+    }
+    key[p] = k;
+    L.cell[p] = c;
+    L.kv[p] = kv;
+    L.kw[p] = kw;
+  }
+}
+
+template <int D>
+__device__ inline void vxyz(const GridDesc& g, i64 v, i64& x, i64& y, i64& z) {
+  x = v % g.nn;
+  y = (v / g.nn) % g.nn;
+  z = (D == 3) ? v / (g.nn * g.nn) : 0;
+}
+
+struct Coef {
+  double kap, eps, p, Gc, mu, lam;
+  int coupling;
+};
+
+// ------------------------------------------------------------------ K1a: element residuals
+// model.cpp:145-194, one thread per cell; writes ru/rphi of all 2^d local nodes.
+template <int D>
+__global__ void __launch_bounds__(128) k_cell_residual(GridDesc g, const Tables* __restrict__ T, Coef cf,
+                                                       const double* __restrict__ sol,
+                                                       const double* __restrict__ ptil,
+                                                       double* __restrict__ out) {
+  constexpr int NV = 1 << D, NQ = 1 << D;
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= g.ncells) return;
+  const i64 cx = c % g.nc, cy = (c / g.nc) % g.nc, cz = (D == 3) ? c / (g.nc * g.nc) : 0;
+  const i64 nu = g.n_u();
+  double uloc[NV][D], philoc[NV], ptloc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const i64 v = (cx + (k & 1)) + g.nn * ((cy + ((k >> 1) & 1)) + g.nn * (cz + ((k >> 2) & 1)));
+#pragma unroll
+    for (int a = 0; a < D; ++a) uloc[k][a] = sol[v * D + a];
+    philoc[k] = sol[nu + v];
+    ptloc[k] = ptil[v];
+  }
+  const double h = g.h;
+  double ru[NV * D], rphi[NV];
+#pragma unroll
+  for (int i = 0; i < NV * D; ++i) ru[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) rphi[i] = 0.0;
+  for (int q = 0; q < NQ; ++q) {
+    double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    double gphi[3] = {0, 0, 0};
+    double phi = 0.0, pt = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double sk = T->s[q][k];
+      phi += sk * philoc[k];
+      pt += sk * ptloc[k];
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        const double Gkb = T->G[q][k][b];
+        gphi[b] += philoc[k] * Gkb / h;
+#pragma unroll
+        for (int a = 0; a < D; ++a) gu[a][b] += uloc[k][a] * Gkb / h;
+      }
+    }
+    double e[3][3], sig[3][3];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
+    double tre = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) tre += e[a][a];
+    const double two_mu = 2.0 * cf.mu;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) sig[a][b] = two_mu * e[a][b];
+#pragma unroll
+    for (int a = 0; a < D; ++a) sig[a][a] += cf.lam * tre;
+    double sig_ee = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) sig_ee += sig[a][b] * e[a][b];
+    const double gcoef = (1.0 - cf.kap) * pt * pt + cf.kap;
+    const double pphi = (cf.coupling == 0) ? pt * pt : phi * phi;
+    const double w = T->w[q];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        double val = 0.0;
+#pragma unroll
+        for (int b = 0; b < D; ++b) val += gcoef * sig[a][b] * T->G[q][k][b] / h;
+        val += pphi * cf.p * T->G[q][k][a] / h;
+        ru[k * D + a] += w * val;
+      }
+      double vphi = ((1.0 - cf.kap) * phi * sig_ee + 2.0 * phi * cf.p * tre - cf.Gc / cf.eps * (1.0 - phi)) * T->s[q][k];
+#pragma unroll
+      for (int b = 0; b < D; ++b) vphi += cf.Gc * cf.eps * gphi[b] * T->G[q][k][b] / h;
+      rphi[k] += w * vphi;
+    }
+  }
+  double* o = out + c * (NV * (D + 1));
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) o[k * (D + 1) + a] = ru[k * D + a];
+    o[k * (D + 1) + D] = rphi[k];
+  }
+}
+
+// K1b: vertex gather with condensation (Scatter::vector_add, model.cpp:74-80; entry-free lines drop).
+template <int D>
+__global__ void k_vertex_residual(GridDesc g, const double* __restrict__ cellres,
+                                  const std::uint8_t* __restrict__ flag, double* __restrict__ R) {
+  constexpr int NV = 1 << D;
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= g.V) return;
+  i64 x, y, z;
+  vxyz<D>(g, v, x, y, z);
+  CellList<D> L;
+  common_cells<D>(g, x, y, z, 0, 0, 0, L);
+  double acc[D + 1];
+#pragma unroll
+  for (int a = 0; a <= D; ++a) acc[a] = 0.0;
+  for (int i = 0; i < L.n; ++i) {
+    const double* o = cellres + L.cell[i] * (NV * (D + 1)) + L.kv[i] * (D + 1);
+#pragma unroll
+    for (int a = 0; a <= D; ++a) acc[a] += o[a];
+  }
+  const i64 nu = g.n_u();
+#pragma unroll
+  for (int a = 0; a < D; ++a) R[v * D + a] = flag[v * D + a] ? 0.0 : acc[a];
+  R[nu + v] = flag[nu + v] ? 0.0 : acc[D];
+}
+
+// ------------------------------------------------------------------ K2a: quadrature-point state
+// model.cpp:242-266 per (cell, q): wg = w*gcoef, phi, tre, sig:e, sigma.
+template <int D>
+struct QS {
+  static constexpr int NS = 4 + D * D;
+};
+
+template <int D>
+__global__ void __launch_bounds__(128) k_cell_qpstate(GridDesc g, const Tables* __restrict__ T, Coef cf,
+                                                      const double* __restrict__ sol,
+                                                      const double* __restrict__ ptil,
+                                                      double* __restrict__ out) {
+  constexpr int NV = 1 << D, NQ = 1 << D, NS = QS<D>::NS;
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= g.ncells) return;
+  const i64 cx = c % g.nc, cy = (c / g.nc) % g.nc, cz = (D == 3) ? c / (g.nc * g.nc) : 0;
+  const i64 nu = g.n_u();
+  double uloc[NV][D], philoc[NV], ptloc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const i64 v = (cx + (k & 1)) + g.nn * ((cy + ((k >> 1) & 1)) + g.nn * (cz + ((k >> 2) & 1)));
+#pragma unroll
+    for (int a = 0; a < D; ++a) uloc[k][a] = sol[v * D + a];
+    philoc[k] = sol[nu + v];
+    ptloc[k] = ptil[v];
+  }
+  double* o = out + c * (NQ * NS);
+  for (int q = 0; q < NQ; ++q) {
+    double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    double phi = 0.0, pt = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double sk = T->s[q][k];
+      phi += sk * philoc[k];
+      pt += sk * ptloc[k];
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+#pragma unroll
+        for (int a = 0; a < D; ++a) gu[a][b] += uloc[k][a] * T->gp[q][k][b];
+    }
+    double e[3][3], sig[3][3];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
+    double tre = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) tre += e[a][a];
+    const double two_mu = 2.0 * cf.mu;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) sig[a][b] = two_mu * e[a][b];
+#pragma unroll
+    for (int a = 0; a < D; ++a) sig[a][a] += cf.lam * tre;
+    double sig_ee = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) sig_ee += sig[a][b] * e[a][b];
+    const double gcoef = (1.0 - cf.kap) * pt * pt + cf.kap;
+    const double w = T->w[q];
+    double* oq = o + q * NS;
+    oq[0] = w * gcoef;
+    oq[1] = phi;
+    oq[2] = tre;
+    oq[3] = sig_ee;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) oq[4 + a * D + b] = sig[a][b];
+  }
+}
+
+// Element-matrix entries coupling row vertex v (local k) and column vertex w (local l),
+// summed over their common cells in reference order (kuu/kpu/kpp of model.cpp:268-285).
+template <int D>
+struct PairBlocks {
+  double uu[D][D];
+  double pu[D];
+  double pp;
+};
+
+template <int D>
+__device__ inline void pair_blocks(const Tables* __restrict__ T, const Coef& cf, const double* __restrict__ qs,
+                                   const CellList<D>& L, bool need_u, bool need_p, PairBlocks<D>& out) {
+  constexpr int NQ = 1 << D, NS = QS<D>::NS;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+#pragma unroll
+    for (int b = 0; b < D; ++b) out.uu[a][b] = 0.0;
+    out.pu[a] = 0.0;
+  }
+  out.pp = 0.0;
+  const double c2k = 2.0 * (1.0 - cf.kap);
+  const double c2p = 2.0 * cf.p;
+  const double omk = 1.0 - cf.kap;
+  const double gce = cf.Gc / cf.eps;
+  const double gcx = cf.Gc * cf.eps;
+  for (int i = 0; i < L.n; ++i) {
+    const int k = L.kv[i], l = L.kw[i];
+    const double* cs = qs + L.cell[i] * (NQ * NS);
+    double bu[D][D], bp[D], bpp = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int b = 0; b < D; ++b) bu[a][b] = 0.0;
+      bp[a] = 0.0;
+    }
+    for (int q = 0; q < NQ; ++q) {
+      const double* st = cs + q * NS;
+      if (need_u) {
+        const double wg = st[0];
+        const double* vl = &T->val[q][k][l][0][0];
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) bu[a][b] += wg * vl[a * 3 + b];
+      }
+      if (need_p) {
+        const double w = T->w[q];
+        const double phi = st[1], tre = st[2], see = st[3];
+        const double sk = T->s[q][k], sl = T->s[q][l];
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          double sgl = 0.0;
+#pragma unroll
+          for (int c = 0; c < D; ++c) sgl += st[4 + b * D + c] * T->gp[q][l][c];
+          bp[b] += w * (c2k * phi * sgl + c2p * phi * T->gp[q][l][b]) * sk;
+        }
+        bpp += w * ((omk * see + c2p * tre + gce) * sl * sk + gcx * T->gg[q][k][l]);
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int b = 0; b < D; ++b) out.uu[a][b] += bu[a][b];
+      out.pu[a] += bp[a];
+    }
+    out.pp += bpp;
+  }
+}
+
+// K2 count pass: row lengths of the three blocks; constrained rows keep a diagonal iff its
+// summed value is non-zero (model.cpp:295,300,308-311).
+template <int D>
+__global__ void k_jac_count(GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
+                            const std::uint8_t* __restrict__ flag, i64* __restrict__ cnt_uu,
+                            i64* __restrict__ cnt_pu, i64* __restrict__ cnt_pp) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= g.V) return;
+  i64 x, y, z;
+  vxyz<D>(g, v, x, y, z);
+  const i64 nu = g.n_u();
+  i64 nfu = 0, nfp = 0;
+  const int zl = (D == 3) ? -1 : 0, zh = (D == 3) ? 1 : 0;
+  for (int dz = zl; dz <= zh; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const i64 X = x + dx, Y = y + dy, Z = z + dz;
+        if (X < 0 || Y < 0 || Z < 0 || X >= g.nn || Y >= g.nn || Z >= ((D == 3) ? g.nn : 1)) continue;
+        const i64 w = X + g.nn * (Y + g.nn * Z);
+#pragma unroll
+        for (int b = 0; b < D; ++b) nfu += flag[w * D + b] ? 0 : 1;
+        nfp += flag[nu + w] ? 0 : 1;
+      }
+  bool any_con = flag[nu + v] != 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) any_con |= flag[v * D + a] != 0;
+  PairBlocks<D> pb;
+  if (any_con) {
+    CellList<D> L;
+    common_cells<D>(g, x, y, z, 0, 0, 0, L);
+    pair_blocks<D>(T, cf, qs, L, true, true, pb);
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) cnt_uu[v * D + a] = flag[v * D + a] ? (pb.uu[a][a] != 0.0 ? 1 : 0) : nfu;
+  const bool pf = flag[nu + v] == 0;
+  cnt_pu[v] = pf ? nfu : 0;
+  cnt_pp[v] = pf ? nfp : (pb.pp != 0.0 ? 1 : 0);
+}
+
+// K2 fill pass: one thread per (row vertex v, stencil slot s) writes the columns and values
+// of the v-w coupling in all three blocks.
+template <int D>
+__global__ void __launch_bounds__(128) k_jac_fill(GridDesc g, const Tables* __restrict__ T, Coef cf,
+                                                  const double* __restrict__ qs,
+                                                  const std::uint8_t* __restrict__ flag,
+                                                  const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
+                                                  double* __restrict__ val_uu, const i64* __restrict__ ptr_pu,
+                                                  int* __restrict__ col_pu, double* __restrict__ val_pu,
+                                                  const i64* __restrict__ ptr_pp, int* __restrict__ col_pp,
+                                                  double* __restrict__ val_pp) {
+  constexpr int S = (D == 3) ? 27 : 9;
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= g.V * S) return;
+  const i64 v = t / S;
+  const int s = int(t % S);
+  const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
+  i64 x, y, z;
+  vxyz<D>(g, v, x, y, z);
+  const i64 X = x + dx, Y = y + dy, Z = z + dz;
+  if (X < 0 || Y < 0 || Z < 0 || X >= g.nn || Y >= g.nn || Z >= ((D == 3) ? g.nn : 1)) return;
+  const i64 w = X + g.nn * (Y + g.nn * Z);
+  const i64 nu = g.n_u();
+  bool rowfree_u[D], colfree_u[D];
+  bool any_row_u = false, any_col_u = false;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    rowfree_u[a] = flag[v * D + a] == 0;
+    colfree_u[a] = flag[w * D + a] == 0;
+    any_row_u |= rowfree_u[a];
+    any_col_u |= colfree_u[a];
+  }
+  const bool rowfree_p = flag[nu + v] == 0, colfree_p = flag[nu + w] == 0;
+  const bool center = (w == v);
+  bool any_con_row = !rowfree_p;
+#pragma unroll
+  for (int a = 0; a < D; ++a) any_con_row |= !rowfree_u[a];
+  const bool need_u = (any_row_u && any_col_u) || (center && any_con_row);
+  const bool need_p = (rowfree_p && (any_col_u || colfree_p)) || (center && !rowfree_p);
+  if (!need_u && !need_p) return;
+  // offsets of w's columns inside v's rows: free components of lower stencil slots
+  i64 off_u = 0, off_p = 0;
+  for (int s2 = 0; s2 < s; ++s2) {
+    const int ex = s2 % 3 - 1, ey = (s2 / 3) % 3 - 1, ez = (D == 3) ? s2 / 9 - 1 : 0;
+    const i64 X2 = x + ex, Y2 = y + ey, Z2 = z + ez;
+    if (X2 < 0 || Y2 < 0 || Z2 < 0 || X2 >= g.nn || Y2 >= g.nn || Z2 >= ((D == 3) ? g.nn : 1)) continue;
+    const i64 w2 = X2 + g.nn * (Y2 + g.nn * Z2);
+#pragma unroll
+    for (int b = 0; b < D; ++b) off_u += flag[w2 * D + b] ? 0 : 1;
+    off_p += flag[nu + w2] ? 0 : 1;
+  }
+  CellList<D> L;
+  common_cells<D>(g, x, y, z, dx, dy, dz, L);
+  PairBlocks<D> pb;
+  pair_blocks<D>(T, cf, qs, L, need_u, need_p, pb);
+  // M_uu rows (v, a)
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const i64 row = v * D + a;
+    if (rowfree_u[a]) {
+      i64 pos = ptr_uu[row] + off_u;
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        if (colfree_u[b]) {
+          col_uu[pos] = int(w * D + b);
+          val_uu[pos] = pb.uu[a][b];
+          ++pos;
+        }
+    } else if (center && ptr_uu[row + 1] > ptr_uu[row]) {
+      col_uu[ptr_uu[row]] = int(row);
+      val_uu[ptr_uu[row]] = pb.uu[a][a];
+    }
+  }
+  if (rowfree_p) {
+    i64 pos = ptr_pu[v] + off_u;
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+      if (colfree_u[b]) {
+        col_pu[pos] = int(w * D + b);
+        val_pu[pos] = pb.pu[b];
+        ++pos;
+      }
+    if (colfree_p) {
+      col_pp[ptr_pp[v] + off_p] = int(w);
+      val_pp[ptr_pp[v] + off_p] = pb.pp;
+    }
+  } else if (center && ptr_pp[v + 1] > ptr_pp[v]) {
+    col_pp[ptr_pp[v]] = int(v);
+    val_pp[ptr_pp[v]] = pb.pp;
+  }
+}
+
+__global__ void k_build_flags(GridDesc g, int clamp, std::uint8_t* flag) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= g.V) return;
+  const i64 x = v % g.nn, y = (v / g.nn) % g.nn, z = (g.d == 3) ? v / (g.nn * g.nn) : 0;
+  bool b = x == 0 || x == g.nc || y == 0 || y == g.nc;
+  if (g.d == 3) b = b || z == 0 || z == g.nc;
+  for (int a = 0; a < g.d; ++a) flag[v * g.d + a] = (clamp && b) ? 1 : 0;
+  flag[g.n_u() + v] = 0;
+}
+
+// fem.cpp:258-263: active entries on unconstrained dofs (Dirichlet wins)
+__global__ void k_apply_active(i64 n, const i64* __restrict__ dofs, const double* __restrict__ vals, i64 ntot,
+                               std::uint8_t* flag, double* inhom, int* bad) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const i64 dof = dofs[i];
+  if (dof < 0 || dof >= ntot) {
+    *bad = 1;
+    return;
+  }
+  if (flag[dof] == 1) return;  // Dirichlet (or a duplicate entry with the same value)
+  flag[dof] = 2;
+  inhom[dof] = vals[i];
+}
+
+__global__ void k_normalise_flags(i64 n, std::uint8_t* flag) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) flag[i] = 1;
+}
+
+__global__ void k_distribute(i64 n, const std::uint8_t* __restrict__ flag, const double* __restrict__ inhom,
+                             double* v, int homogeneous) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) v[i] = homogeneous ? 0.0 : inhom[i];
+}
+
+Coef make_coef(const Problem& P, const cf_material& m, const cf_regularization& reg) {
+  Coef c;
+  c.kap = reg.kappa;
+  c.eps = reg.eps;
+  c.p = m.pressure;
+  c.Gc = m.G_c;
+  c.mu = mat_mu(m);
+  c.lam = mat_lambda(m);
+  c.coupling = m.pressure_coupling;
+  (void)P;
+  return c;
+}
+
+template <class T>
+void exclusive_scan_inplace(T* data, i64 n) {  // n entries + 1 trailing zero -> offsets
+  size_t bytes = 0;
+  CF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, data, data, n + 1, stream()));
+  DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+  CF_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, data, data, n + 1, stream()));
+  count_launch();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+void validate_material(const cf_material& m) {
+  if (!(m.E > 0.0)) fail(CF_ERR_INVALID_ARGUMENT, "Material: E must be positive");
+  if (!(m.nu >= 0.0 && m.nu < 0.5)) fail(CF_ERR_INVALID_ARGUMENT, "Material: nu must be in [0, 0.5)");
+  if (!(m.G_c > 0.0)) fail(CF_ERR_INVALID_ARGUMENT, "Material: G_c must be positive");
+}
+
+Problem* make_problem(int d, double K, int n0, int r) {
+  if (d != 2 && d != 3) fail(CF_ERR_INVALID_ARGUMENT, "DomainSpec: dimension must be 2 or 3");
+  if (!(K > 0.0)) fail(CF_ERR_INVALID_ARGUMENT, "DomainSpec: half_width must be positive");
+  if (n0 < 1 || n0 > 16) fail(CF_ERR_INVALID_ARGUMENT, "DomainSpec: initial_cells_per_side must be in [1,16]");
+  if (r < 0) fail(CF_ERR_INVALID_ARGUMENT, "uniform_refine: times must be >= 0");
+  if (r > 16) fail(CF_ERR_NUMERICAL, "Mesh: refinement depth exceeds integer coordinate resolution");
+  ensure_device();
+  auto* P = new Problem;
+  GridDesc& g = P->g;
+  g.d = d;
+  g.r = r;
+  g.n0 = n0;
+  g.K = K;
+  g.nc = i64(n0) << r;
+  g.nn = g.nc + 1;
+  g.V = (d == 3) ? g.nn * g.nn * g.nn : g.nn * g.nn;
+  g.ncells = (d == 3) ? g.nc * g.nc * g.nc : g.nc * g.nc;
+  if (g.V * (d + 1) >= (i64(1) << 31)) fail(CF_ERR_UNSUPPORTED, "problem exceeds int32 column indices");
+  g.unit = 2.0 * K / (n0 * double(i64(1) << 16));  // mesh.cpp:20
+  g.h = 2.0 * K / (n0 * double(i64(1) << r));      // mesh.hpp:65-67
+  g.detJ = std::pow(g.h, d);                        // model.cpp:148
+  P->tab.alloc(1);
+  return P;
+}
+
+// q1_shape / cell_rule (fem.cpp:53-96) and the elasticity integrand table (model.cpp:270-276).
+void build_tables(Problem& P, double mu, double lam) {
+  if (P.val_ready && P.mu == mu && P.lam == lam) return;
+  const int d = P.g.d, nv = 1 << d, nq = 1 << d;
+  Tables& T = P.host_tab;
+  std::memset(&T, 0, sizeof(T));
+  const double a1 = 1.0 / std::sqrt(3.0);
+  const double x1[2] = {-a1, a1}, w1[2] = {1.0, 1.0};
+  for (int q = 0; q < nq; ++q) {
+    int rem = q;
+    double wt = 1.0;
+    double xi[3] = {0, 0, 0};
+    for (int a = 0; a < d; ++a) {
+      const int i = rem % 2;
+      rem /= 2;
+      xi[a] = 0.5 * (x1[i] + 1.0);
+      wt *= 0.5 * w1[i];
+    }
+    T.w[q] = wt * P.g.detJ;
+    for (int k = 0; k < nv; ++k) {
+      double v = 1.0;
+      for (int a = 0; a < d; ++a) v *= (k & (1 << a)) ? xi[a] : 1.0 - xi[a];
+      T.s[q][k] = v;
+      for (int a = 0; a < d; ++a) {
+        double gr = (k & (1 << a)) ? 1.0 : -1.0;
+        for (int b = 0; b < d; ++b) {
+          if (b == a) continue;
+          gr *= (k & (1 << b)) ? xi[b] : 1.0 - xi[b];
+        }
+        T.G[q][k][a] = gr;
+        T.gp[q][k][a] = gr / P.g.h;
+      }
+    }
+    for (int k = 0; k < nv; ++k)
+      for (int l = 0; l < nv; ++l) {
+        double gg = 0.0;
+        for (int b = 0; b < d; ++b) gg += T.gp[q][k][b] * T.gp[q][l][b];
+        T.gg[q][k][l] = gg;
+        for (int a = 0; a < d; ++a)
+          for (int b = 0; b < d; ++b)
+            T.val[q][k][l][a][b] =
+                mu * ((a == b ? gg : 0.0) + T.gp[q][l][a] * T.gp[q][k][b]) + lam * T.gp[q][l][b] * T.gp[q][k][a];
+      }
+  }
+  CF_CUDA(cudaMemcpyAsync(P.tab.p, &T, sizeof(Tables), cudaMemcpyHostToDevice, stream()));
+  P.mu = mu;
+  P.lam = lam;
+  P.val_ready = true;
+}
+
+std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64 n_active, const i64* dofs_dev,
+                                               const double* vals_dev) {
+  auto c = std::make_unique<Constraints>();
+  c->prob = &P;
+  const i64 nt = P.g.n_total();
+  c->flag.alloc(nt);
+  c->inhom.alloc(nt);
+  c->inhom.zero();
+  k_build_flags<<<grid_for(P.g.V, 256), 256, 0, stream()>>>(P.g, clamp ? 1 : 0, c->flag.p);
+  CF_LAUNCHED();
+  if (n_active > 0) {
+    DevBuf<int> bad(1);
+    bad.zero();
+    k_apply_active<<<grid_for(n_active, 256), 256, 0, stream()>>>(n_active, dofs_dev, vals_dev, nt, c->flag.p,
+                                                                   c->inhom.p, bad.p);
+    CF_LAUNCHED();
+    k_normalise_flags<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, c->flag.p);
+    CF_LAUNCHED();
+    int hb = 0;
+    CF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    if (hb) fail(CF_ERR_INVALID_ARGUMENT, "build_constraints: active dof out of range");
+  }
+  return c;
+}
+
+void distribute(const Constraints& c, double* v, bool homogeneous) {
+  const i64 nt = c.prob->g.n_total();
+  k_distribute<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, c.flag.p, c.inhom.p, v, homogeneous ? 1 : 0);
+  CF_LAUNCHED();
+}
+
+void assemble_residual(Problem& P, const Constraints& cs, const cf_material& m, const cf_regularization& reg,
+                       const double* x, const double* pt, double* R) {
+  build_tables(P, mat_mu(m), mat_lambda(m));
+  const Coef cf = make_coef(P, m, reg);
+  const GridDesc& g = P.g;
+  const int nv = 1 << g.d;
+  DevBuf<double> cellres(g.ncells * nv * (g.d + 1));
+  if (g.d == 2) {
+    k_cell_residual<2><<<grid_for(g.ncells, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p);
+    CF_LAUNCHED();
+    k_vertex_residual<2><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R);
+    CF_LAUNCHED();
+  } else {
+    k_cell_residual<3><<<grid_for(g.ncells, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p);
+    CF_LAUNCHED();
+    k_vertex_residual<3><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R);
+    CF_LAUNCHED();
+  }
+}
+
+template <int D>
+static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, const double* x, const double* pt,
+                          BlockSystem& J) {
+  const GridDesc& g = P.g;
+  constexpr int NQ = 1 << D, NS = QS<D>::NS, S = (D == 3) ? 27 : 9;
+  DevBuf<double> qs(g.ncells * NQ * NS);
+  k_cell_qpstate<D><<<grid_for(g.ncells, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p);
+  CF_LAUNCHED();
+  const i64 nu = g.n_u(), np = g.V;
+  J.uu.rows = J.uu.cols = nu;
+  J.pu.rows = np;
+  J.pu.cols = nu;
+  J.pp.rows = J.pp.cols = np;
+  J.uu.ptr.alloc(nu + 1);
+  J.pu.ptr.alloc(np + 1);
+  J.pp.ptr.alloc(np + 1);
+  CF_CUDA(cudaMemsetAsync(J.uu.ptr.p + nu, 0, sizeof(i64), stream()));
+  CF_CUDA(cudaMemsetAsync(J.pu.ptr.p + np, 0, sizeof(i64), stream()));
+  CF_CUDA(cudaMemsetAsync(J.pp.ptr.p + np, 0, sizeof(i64), stream()));
+  k_jac_count<D><<<grid_for(g.V, 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu.ptr.p, J.pu.ptr.p,
+                                                           J.pp.ptr.p);
+  CF_LAUNCHED();
+  exclusive_scan_inplace(J.uu.ptr.p, nu);
+  exclusive_scan_inplace(J.pu.ptr.p, np);
+  exclusive_scan_inplace(J.pp.ptr.p, np);
+  i64 nnz[3];
+  CF_CUDA(cudaMemcpyAsync(&nnz[0], J.uu.ptr.p + nu, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaMemcpyAsync(&nnz[1], J.pu.ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaMemcpyAsync(&nnz[2], J.pp.ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  J.uu.nnz = nnz[0];
+  J.pu.nnz = nnz[1];
+  J.pp.nnz = nnz[2];
+  J.uu.col.alloc(nnz[0]);
+  J.uu.val.alloc(nnz[0]);
+  J.pu.col.alloc(nnz[1]);
+  J.pu.val.alloc(nnz[1]);
+  J.pp.col.alloc(nnz[2]);
+  J.pp.val.alloc(nnz[2]);
+  k_jac_fill<D><<<grid_for(g.V * S, 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu.ptr.p,
+                                                              J.uu.col.p, J.uu.val.p, J.pu.ptr.p, J.pu.col.p,
+                                                              J.pu.val.p, J.pp.ptr.p, J.pp.col.p, J.pp.val.p);
+  CF_LAUNCHED();
+}
+
+std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& cs, const cf_material& m,
+                                               const cf_regularization& reg, const double* x, const double* pt) {
+  build_tables(P, mat_mu(m), mat_lambda(m));
+  const Coef cf = make_coef(P, m, reg);
+  auto J = std::make_unique<BlockSystem>();
+  J->d = P.g.d;
+  J->nu = P.g.n_u();
+  J->np = P.g.V;
+  if (P.g.d == 2)
+    jacobian_impl<2>(P, cs, cf, x, pt, *J);
+  else
+    jacobian_impl<3>(P, cs, cf, x, pt, *J);
+  return J;
+}
+
+}  // namespace cfb

@@ -1,0 +1,132 @@
+// Shared runtime pieces of the crackfield_b200 library: errors, the library stream, a
+// stream-ordered device buffer and launch accounting.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "crackfield_b200.h"
+
+namespace cfb {
+
+using i64 = std::int64_t;
+
+// Exception carrying a CF_ERR_* code; converted to a status at the C ABI.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "%s: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+    fail(e == cudaErrorMemoryAllocation ? CF_ERR_OUT_OF_MEMORY : CF_ERR_CUDA, buf);
+  }
+}
+#define CF_CUDA(x) ::cfb::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Library-wide state: the stream all device work is ordered on, the device's SM count and the
+// kernel-launch counter (bench.py's gpu_launches).
+struct Runtime {
+  cudaStream_t stream = nullptr;
+  int device = -1;
+  int sm_count = 0;
+  i64 launches = 0;
+  bool ready = false;
+};
+Runtime& rt();
+void ensure_device();  // throws CF_ERR_CUDA when no device is usable (no CPU fallback)
+inline cudaStream_t stream() { return rt().stream; }
+inline void count_launch(i64 n = 1) { rt().launches += n; }
+#define CF_LAUNCHED() ::cfb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__), ::cfb::count_launch()
+
+// Stream-ordered device allocation (cudaMallocAsync on the library stream; the pool keeps
+// freed blocks cached, so per-Newton-iteration reallocations are cheap).
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  i64 n = 0;
+  DevBuf() = default;
+  explicit DevBuf(i64 count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(i64 count) {
+    release();
+    n = count;
+    if (count > 0) CF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), size_t(count) * sizeof(T), stream()));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, stream());
+    p = nullptr;
+    n = 0;
+  }
+  void zero() {
+    if (n) CF_CUDA(cudaMemsetAsync(p, 0, size_t(n) * sizeof(T), stream()));
+  }
+  T* get() const { return p; }
+  i64 size() const { return n; }
+};
+
+// Host-or-device argument staging for the ABI: device pointers pass through, host arrays are
+// copied in (and, for outputs, back out at the end of the call).
+bool is_device_ptr(const void* p);
+
+template <class T>
+struct InArg {
+  const T* dev = nullptr;
+  DevBuf<T> staged;
+  InArg(const T* p, i64 n) {
+    if (n == 0 || p == nullptr) { dev = p; return; }
+    if (is_device_ptr(p)) { dev = p; return; }
+    staged.alloc(n);
+    CF_CUDA(cudaMemcpyAsync(staged.p, p, size_t(n) * sizeof(T), cudaMemcpyHostToDevice, stream()));
+    dev = staged.p;
+  }
+};
+
+template <class T>
+struct OutArg {
+  T* host = nullptr;
+  T* dev = nullptr;
+  i64 n = 0;
+  DevBuf<T> staged;
+  OutArg(T* p, i64 count, bool copy_in = false) : n(count) {
+    if (count == 0 || p == nullptr) { dev = p; return; }
+    if (is_device_ptr(p)) { dev = p; return; }
+    host = p;
+    staged.alloc(count);
+    dev = staged.p;
+    if (copy_in) CF_CUDA(cudaMemcpyAsync(dev, p, size_t(count) * sizeof(T), cudaMemcpyHostToDevice, stream()));
+  }
+  // copy back (synchronous) when the caller passed host memory
+  void finish() {
+    if (host) {
+      CF_CUDA(cudaMemcpyAsync(host, dev, size_t(n) * sizeof(T), cudaMemcpyDeviceToHost, stream()));
+      CF_CUDA(cudaStreamSynchronize(stream()));
+    }
+  }
+};
+
+inline unsigned grid_for(i64 n, int block) { return unsigned((n + block - 1) / block); }
+
+}  // namespace cfb

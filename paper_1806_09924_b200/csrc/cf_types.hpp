@@ -1,0 +1,83 @@
+// Device-resident data structures of the hot path: the uniform grid + DofMap descriptor
+// (mesh.hpp / fem.hpp), the constraint set, CSR matrices and the block system.
+#pragma once
+
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "cf_common.hpp"
+
+namespace cfb {
+
+// Uniform grid of (n0 << r)^d cells on (-K, K)^d.  Vertex v = x + nn*(y + nn*z) (fem.cpp:98-116
+// numbers vertices by the packed key x | y<<21 | z<<42, i.e. lexicographically with x fastest).
+struct GridDesc {
+  int d, r, n0;
+  i64 nc, nn, V, ncells;
+  double K, unit, h, detJ;
+  __host__ __device__ i64 n_u() const { return d * V; }
+  __host__ __device__ i64 n_total() const { return (d + 1) * V; }
+};
+
+// Quadrature / Q1 tables of one problem (fem.cpp:53-96; model.cpp:111-123), computed on the
+// host with the reference's expressions (compiled without FMA contraction) so device
+// assembly reproduces the reference's element arithmetic bit for bit.
+struct Tables {
+  double w[8];                 // quad weight * detJ
+  double s[8][8];              // shape[q][k]
+  double G[8][8][3];           // reference gradients[q][k][a]
+  double gp[8][8][3];          // G / h  (gphys, model.cpp:245-247)
+  double gg[8][8][8];          // sum_b gphys(k,b) gphys(l,b)
+  double val[8][8][8][3][3];   // mu((a==b)gg + gp(l,a)gp(k,b)) + lam gp(l,b)gp(k,a)  (model.cpp:274-275)
+};
+
+struct Problem {
+  GridDesc g{};
+  Tables host_tab{};
+  DevBuf<Tables> tab;
+  double mu = 0.0, lam = 0.0;  // cached for the material the tables were built with
+  bool val_ready = false;
+};
+
+struct Constraints {
+  const Problem* prob = nullptr;
+  DevBuf<std::uint8_t> flag;  // per dof
+  DevBuf<double> inhom;       // per dof (phi_old on the active set, 0 elsewhere)
+  i64 count = 0;
+};
+
+struct Csr {
+  i64 rows = 0, cols = 0, nnz = 0;
+  DevBuf<i64> ptr;
+  DevBuf<int> col;
+  DevBuf<double> val;
+};
+
+struct BlockSystem {
+  i64 nu = 0, np = 0;
+  Csr uu, pu, pp;
+  int d = 2;
+};
+
+// ---- host helpers implemented in the .cu files
+Problem* make_problem(int d, double K, int n0, int r);
+void build_tables(Problem& P, double mu, double lam);
+std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64 n_active,
+                                               const i64* dofs_dev, const double* vals_dev);
+void distribute(const Constraints& c, double* v_dev, bool homogeneous);
+void assemble_residual(Problem& P, const Constraints& c, const cf_material& m, const cf_regularization& reg,
+                       const double* x, const double* pt, double* R);
+std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& c, const cf_material& m,
+                                               const cf_regularization& reg, const double* x, const double* pt);
+void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add);  // y = A x (+ add)
+void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
+void block_apply(const BlockSystem& J, const double* x, double* y);
+
+inline double mat_mu(const cf_material& m) { return m.E / (2.0 * (1.0 + m.nu)); }              // model.hpp:26
+inline double mat_lambda(const cf_material& m) {                                                  // model.hpp:27
+  return m.E * m.nu / ((1.0 + m.nu) * (1.0 - 2.0 * m.nu));
+}
+void validate_material(const cf_material& m);  // model.cpp:8-17
+
+}  // namespace cfb

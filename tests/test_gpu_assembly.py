@@ -1,0 +1,199 @@
+"""GPU parity of K1/K2/K4 (residual, Jacobian, block apply) against the CPU oracle.
+
+Assembly is bit-exact: same pattern (int64 row pointers, int32 columns) and the same IEEE
+doubles, because the kernels reproduce the reference's expression order and cell order
+(model.cpp:127-322).  SpMV/apply is compared within 1e-13 relative (different summation order).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cf():
+    import paper_1806_09924_b200 as cf
+    return cf
+
+
+def _pair(cf, orc, d, K, n0, r):
+    return cf.Problem(d, K, n0, r), orc.Problem(d, K, n0, r)
+
+
+def _state(P, rng, uscale=1e-2):
+    x = np.zeros(P.n_total)
+    x[:P.n_u] = uscale * rng.uniform(-1, 1, P.n_u)
+    x[P.n_u:] = rng.uniform(0, 1, P.n_vertices)
+    return x, rng.uniform(0, 1, P.n_vertices)
+
+
+def _assert_blocks_equal(J, Jo):
+    for w in range(3):
+        a, b = J.csr(w), Jo.csr(w)
+        assert np.array_equal(a.ptr, b.ptr), f"row pointers differ in block {w}"
+        assert np.array_equal(a.col, b.col), f"columns differ in block {w}"
+        bad = np.nonzero(a.val != b.val)[0]
+        assert bad.size == 0, f"block {w}: {bad.size} values differ, max {np.abs(a.val - b.val).max()}"
+
+
+CASES = [
+    (2, 1.0, 4, 2, True, 0.0, 0),   # 16x16, clamp
+    (2, 1.0, 3, 1, False, 0.0, 0),  # unconstrained
+    (2, 1.0, 4, 2, True, 0.2, 1),   # with an active set, current pressure coupling
+    (3, 1.0, 2, 1, True, 0.0, 0),   # 4^3
+    (3, 1.0, 3, 1, True, 0.15, 0),  # 6^3 + active set
+    (3, 2.0, 2, 2, False, 0.1, 1),  # 8^3 unconstrained + active
+]
+
+
+@pytest.mark.parametrize("d,K,n0,r,clamp,frac_active,coupling", CASES)
+def test_assembly_bit_exact(cf, orc, d, K, n0, r, clamp, frac_active, coupling):
+    P, O = _pair(cf, orc, d, K, n0, r)
+    rng = np.random.default_rng(100 + d * 10 + n0 + r)
+    x, pt = _state(P, rng)
+    nact = int(frac_active * P.n_vertices)
+    verts = rng.choice(P.n_vertices, nact, replace=False) if nact else np.zeros(0, dtype=np.int64)
+    act = {int(P.n_u + v): float(rng.uniform(0, 1)) for v in verts}
+    cs = cf.build_constraints(P, clamp, act)
+    ocs = O.constraints(clamp, list(act.keys()), list(act.values()))
+    mat = cf.Material(pressure=2e-3, pressure_coupling=coupling)
+    omat = orc.material(pressure=2e-3, pressure_coupling=coupling)
+    reg, oreg = cf.Regularization(0.3, 1e-6), orc.Regularization(0.3, 1e-6)
+    R = cf.assemble_residual(P, cs, mat, reg, x, pt)
+    Ro = O.residual(ocs, omat, oreg, x, pt)
+    assert np.array_equal(R, Ro), np.abs(R - Ro).max()
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    Jo = O.jacobian(ocs, omat, oreg, x, pt)
+    _assert_blocks_equal(J, Jo)
+    z = rng.standard_normal(P.n_total)
+    y, yo = J.apply(z), Jo.apply(z)
+    assert np.linalg.norm(y - yo) <= 1e-13 * np.linalg.norm(yo)
+    for w, (rows, cols) in enumerate(((P.n_u, P.n_u), (P.n_phi, P.n_u), (P.n_phi, P.n_phi))):
+        xin = rng.standard_normal(cols)
+        ref = Jo.csr(w).to_scipy() @ xin
+        got = J.spmv(w, xin)
+        assert np.linalg.norm(got - ref) <= 1e-13 * max(np.linalg.norm(ref), 1e-300)
+
+
+def _sneddon(cf, orc, d, n0, r, K=10.0):
+    P, O = _pair(cf, orc, d, K, n0, r)
+    h = P.h
+    kw = dict(eps_mode=1, eps_fixed=2 * h, kappa_factor=1e-12 / h)
+    omat = orc.material(**kw)
+    phi, _ = O.initial_crack(omat)
+    oreg = O.resolve_regularization(omat, O.slit_band_edge(omat))
+    return P, O, cf.Material(**kw), omat, cf.Regularization(oreg.eps, oreg.kappa), oreg, phi
+
+
+def test_config0_sneddon_bit_exact(cf, orc):
+    """BASELINE config 0 (2d 256^2, eps=2h, kappa=1e-12): initial and perturbed states."""
+    P, O, mat, omat, reg, oreg, phi = _sneddon(cf, orc, 2, 8, 5)
+    assert P.n_total == 198147
+    rng = np.random.default_rng(0)
+    x = np.zeros(P.n_total)
+    x[P.n_u:] = phi
+    for trial in range(2):
+        cs, ocs = cf.build_constraints(P), O.constraints()
+        R, Ro = cf.assemble_residual(P, cs, mat, reg, x, phi), O.residual(ocs, omat, oreg, x, phi)
+        assert np.array_equal(R, Ro)
+        J, Jo = cf.assemble_jacobian(P, cs, mat, reg, x, phi), O.jacobian(ocs, omat, oreg, x, phi)
+        _assert_blocks_equal(J, Jo)
+        x[:P.n_u] += 1e-3 * rng.standard_normal(P.n_u)
+        ocs.distribute(x, homogeneous=True)
+        x = ocs.distribute(x, homogeneous=True)
+
+
+def test_3d_penny_bit_exact(cf, orc):
+    """3d penny crack on 32^3 (config 3 family)."""
+    P, O, mat, omat, reg, oreg, phi = _sneddon(cf, orc, 3, 8, 2)
+    rng = np.random.default_rng(1)
+    x = np.zeros(P.n_total)
+    x[:P.n_u] = 1e-3 * rng.standard_normal(P.n_u)
+    x[P.n_u:] = phi
+    act = {int(P.n_u + v): 0.0 for v in np.nonzero(phi == 0)[0]}
+    cs, ocs = cf.build_constraints(P, True, act), O.constraints(True, list(act.keys()), list(act.values()))
+    x = ocs.distribute(x)
+    R, Ro = cf.assemble_residual(P, cs, mat, reg, x, phi), O.residual(ocs, omat, oreg, x, phi)
+    assert np.array_equal(R, Ro)
+    _assert_blocks_equal(cf.assemble_jacobian(P, cs, mat, reg, x, phi), O.jacobian(ocs, omat, oreg, x, phi))
+
+
+def test_jacobian_fd_on_device(cf):
+    """model_test.cpp:211-240 on the device path: J delta vs central differences <= 1e-5."""
+    rng = np.random.default_rng(13)
+    for d, n0 in ((2, 4), (3, 2)):
+        P = cf.Problem(d, 1.0, n0, 1)
+        cs = cf.build_constraints(P)
+        mat, reg = cf.Material(pressure=1e-3), cf.Regularization(0.25, 1e-10)
+        x, pt = _state(P, rng)
+        cs.distribute_homogeneous(x)
+        J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+        for _ in range(3):
+            dl = rng.uniform(-1, 1, P.n_total)
+            cs.distribute_homogeneous(dl)
+            t = 1e-6 * max(1.0, np.abs(x).max())
+            fd = (cf.assemble_residual(P, cs, mat, reg, x + t * dl, pt)
+                  - cf.assemble_residual(P, cs, mat, reg, x - t * dl, pt)) / (2 * t)
+            jd = J.apply(dl)
+            assert np.linalg.norm(fd - jd) / np.linalg.norm(jd) <= 1e-5
+
+
+def test_device_pointer_path_matches_host(cf):
+    import torch
+    P = cf.Problem(3, 1.0, 2, 2)
+    rng = np.random.default_rng(3)
+    x, pt = _state(P, rng)
+    cs = cf.build_constraints(P)
+    mat, reg = cf.Material(), cf.Regularization(0.25, 1e-10)
+    Rh = cf.assemble_residual(P, cs, mat, reg, x, pt)
+    xd, ptd = torch.from_numpy(x).cuda(), torch.from_numpy(pt).cuda()
+    Rd = cf.assemble_residual(P, cs, mat, reg, xd, ptd)
+    torch.cuda.synchronize()
+    assert np.array_equal(Rd.cpu().numpy(), Rh)
+    J = cf.assemble_jacobian(P, cs, mat, reg, xd, ptd)
+    yd = J.apply(xd)
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), J.apply(x))
+
+
+def test_constraints_distribute(cf, orc):  # fem_test.cpp:213-225
+    P = cf.Problem(2, 1.0, 2, 0)
+    cs = cf.build_constraints(P, True, {P.phi_dof(0): 0.25, P.phi_dof(3): 1.0})
+    v = np.zeros(P.n_total)
+    cs.distribute(v)
+    assert v[P.phi_dof(0)] == 0.25 and v[P.phi_dof(3)] == 1.0
+    inc = np.ones(P.n_total)
+    cs.distribute_homogeneous(inc)
+    assert inc[P.phi_dof(0)] == 0.0
+    O = orc.Problem(2, 1.0, 2, 0)
+    ocs = O.constraints(True, [P.phi_dof(0), P.phi_dof(3)], [0.25, 1.0])
+    w = np.ones(P.n_total)
+    assert np.array_equal(cs.distribute(w.copy()), ocs.distribute(w))
+    with pytest.raises(ValueError):
+        cf.build_constraints(P, True, {10 ** 9: 0.0})
+
+
+@pytest.mark.slow
+def test_config1_operator_properties(cf):
+    """Config 1 at full size (3d 192^3, 21.5M u dofs): the exact nnz of SURVEY §8(a) and
+    size-independent properties of y = M_uu u (symmetry, rigid-translation kernel)."""
+    import torch
+    from bench import config1_inputs
+    P, cs, mat, reg, x, pt = config1_inputs(cf, device="cuda")
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    assert J.nnz[0] == 1_676_188_257
+    u = x[:P.n_u].contiguous()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    w = torch.randn(P.n_u, dtype=torch.float64, device="cuda", generator=g)
+    Mu, Mw = J.spmv(0, u), J.spmv(0, w)
+    a, b = torch.dot(w, Mu).item(), torch.dot(u, Mw).item()
+    assert abs(a - b) <= 1e-10 * (abs(a) + abs(b))
+    t = torch.zeros(P.n_u, dtype=torch.float64, device="cuda")
+    t[0::3] = 1.0
+    Mt = J.spmv(0, t)
+    n = P.nodes_per_side
+    idx = torch.arange(P.n_vertices, device="cuda")
+    xi, yi, zi = idx % n, (idx // n) % n, idx // (n * n)
+    interior = (xi > 1) & (xi < n - 2) & (yi > 1) & (yi < n - 2) & (zi > 1) & (zi < n - 2)
+    rows = Mt.view(-1, 3)[interior]
+    assert rows.abs().max().item() <= 1e-12 * Mu.abs().max().item() + 1e-14
