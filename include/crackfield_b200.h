@@ -121,6 +121,92 @@ int cf_block_apply(cf_block b, const double* x, double* y);
 /* One block times a vector (the M_uu operator microbenchmark, config 1). */
 int cf_block_spmv(cf_block b, int which, const double* x, double* y);
 int cf_block_destroy(cf_block b);
+/* Tuning hook (not a reference interface): one block times a vector with an explicit kernel
+ * variant (threads per row in {4,8,16,32}; unroll 0 = plain loop, else batched loads). */
+int cf_tune_spmv(cf_block b, int which, int threads_per_row, int unroll, const double* x, double* y);
+
+/* ------------------------------------------------------------------ generic CSR operators */
+typedef struct cf_csr_s* cf_csr;   /* CsrMatrix (types.hpp:12) on the device */
+typedef struct cf_amg_s* cf_amg;   /* AmgHierarchy (linsolve.hpp:64-85) */
+typedef struct cf_prec_s* cf_prec; /* BlockPreconditioner (linsolve.hpp:106-128) */
+
+int cf_csr_create(int64_t rows, int64_t cols, const int64_t* rowptr, const int32_t* col, const double* val,
+                  cf_csr* out);
+/* A block of a BlockSystem as a shared CSR handle (which: 0 M_uu, 1 M_phiu, 2 M_phiphi). */
+int cf_block_csr(cf_block b, int which, cf_csr* out);
+int cf_csr_info(cf_csr A, int64_t* rows, int64_t* cols, int64_t* nnz);
+int cf_csr_spmv(cf_csr A, const double* x, double* y);
+int cf_csr_destroy(cf_csr A);
+
+/* ------------------------------------------------------------------ AMG */
+/* build_amg(A, node_of_dof, near_nullspace) (linsolve.hpp:90-94, linsolve.cpp:170-287).
+ * node_of_dof (length rows) and B (rows x m, column-major) may both be NULL: the scalar overload
+ * (identity nodes, constant nullspace, linsolve.cpp:289-293). */
+int cf_amg_build(cf_csr A, const int32_t* node_of_dof, const double* B, int m, const cf_amg_options* opts,
+                 cf_amg* out);
+/* AmgHierarchy::v_cycle (linsolve.cpp:314-318): x = V(r). */
+int cf_amg_vcycle(cf_amg h, const double* r, double* x);
+/* n_levels() and coarse_dim() (linsolve.hpp:67-68). */
+int cf_amg_info(cf_amg h, int* n_levels, int64_t* coarse_dim);
+/* Diagnostics of one non-coarsest level: info8 = {rows(A), nnz(A), nnz(P), cols(P), n_nodes,
+ * n_aggregates, strong edges, LFMIS rounds}; lambda_max and the Jacobi weight. */
+int cf_amg_level_info(cf_amg h, int level, int64_t* info8, double* lambda, double* jacobi_weight);
+int cf_amg_level_aggregates(cf_amg h, int level, int32_t* agg_of_node);
+/* Level operator (which 0: A, 1: P) as CSR. */
+int cf_amg_level_export(cf_amg h, int level, int which, int64_t* rowptr, int32_t* col, double* val);
+int cf_amg_destroy(cf_amg h);
+
+/* ------------------------------------------------------------------ block preconditioner */
+/* BlockPreconditioner::build (linsolve.cpp:352-396).  kind 0 exact (dense LU, small blocks
+ * only), 1 amg, 2 diagonal.  With problem/constraints given, the AMG gets the reference's
+ * NullspaceInfo (rigid-body modes zeroed on constrained u dofs, phi ones zeroed on constrained
+ * phi dofs, vertex nodes; solver.cpp:142-150); with NULL, the scalar overload. */
+int cf_prec_build(cf_block J, int kind, const cf_amg_options* opts, cf_problem p, cf_constraints c, cf_prec* out);
+int cf_prec_apply(cf_prec P, const double* r, double* z);  /* linsolve.cpp:398-415 */
+int cf_prec_destroy(cf_prec P);
+/* rigid_body_modes (linsolve.cpp:320-343): B (n_u x m, column-major), m = 3 (2d) / 6 (3d). */
+int cf_rigid_body_modes(cf_problem p, cf_constraints c, double* B);
+
+/* ------------------------------------------------------------------ GMRES */
+typedef struct {
+  int iterations, converged, breakdown;
+  double residual;
+} cf_gmres_result;
+/* gmres(op, prec, rhs) (linsolve.hpp:48-49): op = the block system (J != NULL) or a CSR matrix;
+ * prec = a block preconditioner, an AMG hierarchy or none (identity).  history receives the
+ * relative residual estimate of every inner iteration (up to history_cap entries). */
+int cf_gmres(cf_block J, cf_csr A, cf_prec P, cf_amg M, const double* rhs, const cf_gmres_options* opts, double* x,
+             cf_gmres_result* result, double* history, int history_cap);
+
+/* ------------------------------------------------------------------ Newton / active set */
+typedef struct cf_state_s* cf_state; /* FractureState (model.hpp:50-55), device resident */
+typedef struct {
+  double residual_norm;
+  int active_size, set_changes, gmres_iterations;
+} cf_newton_iteration;             /* NewtonIteration (solver.hpp:28-33) */
+typedef struct {
+  double residual_ms, active_set_ms, jacobian_ms, amg_setup_ms, gmres_ms, total_ms;
+} cf_phase_times;
+
+/* slit_band_edge / resolve_regularization / initial_crack (model.cpp:28-58, 324-349). */
+int cf_slit_band_edge(cf_problem p, const cf_material* mat, double* edge);
+int cf_resolve_regularization(cf_problem p, const cf_material* mat, double band_edge, cf_regularization* out);
+int cf_initial_crack(cf_problem p, const cf_material* mat, double band_half, double* phi, double* band_edge);
+/* make_initial_state (solver.cpp:24-35) or an explicit state (any of the arrays may be NULL = zeros). */
+int cf_make_initial_state(cf_problem p, const cf_material* mat, double seed_band, cf_state* out);
+int cf_state_create(cf_problem p, const double* solution, const double* phi_old, const double* phi_prev2, int step,
+                    cf_state* out);
+int cf_state_get(cf_state s, double* solution, double* phi_old, double* phi_prev2, int* step);
+int cf_state_destroy(cf_state s);
+/* newton_active_set_step (solver.cpp:49-188).  its receives up to max_its iterations. */
+int cf_newton_active_set_step(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                              const cf_solver_options* opts, cf_newton_iteration* its, int max_its, int* n_its,
+                              int* converged, double* feasibility, cf_phase_times* times);
+/* solve_loading_sequence (solver.cpp:190-204): per step shift phi history, step = n, Newton;
+ * stops after a non-converged step.  Per-step iteration counts in n_its[n_steps]. */
+int cf_solve_loading_sequence(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                              const cf_solver_options* opts, int n_steps, cf_newton_iteration* its, int max_its,
+                              int* n_its, int* converged, double* feasibility, int* steps_done);
 
 #ifdef __cplusplus
 }

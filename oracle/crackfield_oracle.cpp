@@ -302,19 +302,37 @@ struct Csr {
   }
 };
 
-static void spmv(const Csr& A, const double* x, double* y) {  // y = A x (sequential row sums)
-  for (i64 i = 0; i < A.rows; ++i) {
+// ---- Reduction-order contract.  Eigen's own reduction order (vectorised dot/norm, sparse
+// row sums) is not pinned by any reference test, so the oracle adopts the product's documented
+// deterministic order: a row of an SpMV is split over a group of
+// TPR lanes (lane l sums entries l, l+TPR, ... sequentially; the lanes are then combined by an
+// xor butterfly), TPR chosen from the mean row length; dot products use a fixed grid of
+// 256-thread blocks (grid-stride sequential per thread, tree per block, one ordered final block).
+static int spmv_tpr(const Csr& A) {
+  const double mean = A.rows ? double(A.nnz()) / double(A.rows) : 0.0;
+  return mean > 64 ? 16 : (mean > 24 ? 8 : 4);
+}
+static double row_sum_lanes(const Csr& A, i64 i, const double* x, int tpr) {
+  double lane[32];
+  for (int l = 0; l < tpr; ++l) {
     double s = 0.0;
-    for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) s += A.val[k] * x[A.col[k]];
-    y[i] = s;
+    for (i64 k = A.ptr[i] + l; k < A.ptr[i + 1]; k += tpr) s += A.val[k] * x[A.col[k]];
+    lane[l] = s;
   }
+  double tmp[32];
+  for (int o = tpr / 2; o > 0; o >>= 1) {
+    for (int l = 0; l < tpr; ++l) tmp[l] = lane[l] + lane[l ^ o];
+    for (int l = 0; l < tpr; ++l) lane[l] = tmp[l];
+  }
+  return lane[0];
+}
+static void spmv(const Csr& A, const double* x, double* y) {  // y = A x
+  const int tpr = spmv_tpr(A);
+  for (i64 i = 0; i < A.rows; ++i) y[i] = row_sum_lanes(A, i, x, tpr);
 }
 static void spmv_add(const Csr& A, const double* x, double* y) {  // y += A x
-  for (i64 i = 0; i < A.rows; ++i) {
-    double s = 0.0;
-    for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) s += A.val[k] * x[A.col[k]];
-    y[i] += s;
-  }
+  const int tpr = spmv_tpr(A);
+  for (i64 i = 0; i < A.rows; ++i) y[i] = y[i] + row_sum_lanes(A, i, x, tpr);
 }
 
 static Csr transpose(const Csr& A) {
@@ -399,10 +417,10 @@ struct BlockSystem {
     const i64 nu = n_u(), np = n_phi();
     Vec y(nu + np);
     spmv(uu, x.data(), y.data());
-    Vec t(np);
-    spmv(pu, x.data(), y.data() + nu);
-    spmv(pp, x.data() + nu, t.data());
-    for (i64 i = 0; i < np; ++i) y[nu + i] += t[i];
+    // phi rows: one lane group per row over both blocks; the group size follows M_phiu's mean
+    const int tpr = spmv_tpr(pu);
+    for (i64 i = 0; i < np; ++i)
+      y[nu + i] = row_sum_lanes(pu, i, x.data(), tpr) + row_sum_lanes(pp, i, x.data() + nu, tpr);
     return y;
   }
 };
@@ -696,10 +714,30 @@ struct GmresResult {
   double residual = 0.0;
   std::vector<double> history;
 };
-static double dot(const Vec& a, const Vec& b) {
-  double s = 0.0;
-  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
-  return s;
+static double tree256(double* sh) {  // in-place block tree of 256 values
+  for (int s = 128; s > 0; s >>= 1)
+    for (int t = 0; t < s; ++t) sh[t] += sh[t + s];
+  return sh[0];
+}
+static double dot(const Vec& a, const Vec& b) {  // fixed block-tree order (see spmv_tpr note)
+  const i64 n = i64(a.size());
+  const i64 nb = std::min<i64>(1024, std::max<i64>(1, (n + 4 * 256 - 1) / (4 * 256)));
+  std::vector<double> part(nb);
+  double sh[256];
+  for (i64 bk = 0; bk < nb; ++bk) {
+    for (int t = 0; t < 256; ++t) {
+      double s = 0.0;
+      for (i64 i = bk * 256 + t; i < n; i += nb * 256) s += a[i] * b[i];
+      sh[t] = s;
+    }
+    part[bk] = tree256(sh);
+  }
+  for (int t = 0; t < 256; ++t) {
+    double s = 0.0;
+    for (i64 bk = t; bk < nb; bk += 256) s += part[bk];
+    sh[t] = s;
+  }
+  return tree256(sh);
 }
 static double norm(const Vec& a) { return std::sqrt(dot(a, a)); }
 

@@ -248,3 +248,282 @@ def assemble_jacobian(prob: Problem, constraints: ConstraintSet, mat: Material, 
     check(load().cf_assemble_jacobian(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(x), _ptr(pt),
                                       C.byref(h)))
     return BlockSystem(h)
+
+
+# ---------------------------------------------------------------------------- linear algebra
+class CsrMatrix:
+    """Device CSR matrix (types.hpp:12); from host (rows, cols, rowptr, col, val) or a block."""
+
+    def __init__(self, rows=None, cols=None, rowptr=None, col=None, val=None, _handle=None):
+        if _handle is not None:
+            self._h = _handle
+        else:
+            rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+            ci = np.ascontiguousarray(col, dtype=np.int32)
+            vv = np.ascontiguousarray(val, dtype=np.float64)
+            self._h = C.c_void_p()
+            check(load().cf_csr_create(int(rows), int(cols), _ptr(rp), _ptr(ci), _ptr(vv), C.byref(self._h)))
+        r, c, n = C.c_int64(), C.c_int64(), C.c_int64()
+        check(load().cf_csr_info(self._h, C.byref(r), C.byref(c), C.byref(n)))
+        self.rows, self.cols, self.nnz = r.value, c.value, n.value
+
+    @staticmethod
+    def from_scipy(M):
+        M = M.tocsr()
+        M.sort_indices()
+        return CsrMatrix(M.shape[0], M.shape[1], M.indptr, M.indices, M.data)
+
+    @staticmethod
+    def from_block(J: BlockSystem, which: int):
+        h = C.c_void_p()
+        check(load().cf_block_csr(J._h, which, C.byref(h)))
+        return CsrMatrix(_handle=h)
+
+    def __del__(self):
+        try:
+            load().cf_csr_destroy(self._h)
+        except Exception:
+            pass
+
+    def __matmul__(self, x):
+        x = _as_f64(x)
+        y = _empty_like_kind(x, self.rows)
+        check(load().cf_csr_spmv(self._h, _ptr(x), _ptr(y)))
+        return y
+
+
+class AmgHierarchy:
+    """AmgHierarchy (linsolve.hpp:64-85) built by build_amg on the device."""
+
+    def __init__(self, A: CsrMatrix, node_of_dof=None, near_nullspace=None, opts: AmgOptions | None = None):
+        self.A = A
+        self.opts = opts or AmgOptions()
+        self._h = C.c_void_p()
+        if node_of_dof is not None:
+            nod = np.ascontiguousarray(node_of_dof, dtype=np.int32)
+            B = np.asfortranarray(near_nullspace, dtype=np.float64)
+            m = 1 if B.ndim == 1 else B.shape[1]
+            Bf = np.ascontiguousarray(B.T).reshape(-1) if B.ndim == 2 else B
+            check(load().cf_amg_build(A._h, _ptr(nod), _ptr(np.ascontiguousarray(Bf)), m, C.byref(self.opts),
+                                      C.byref(self._h)))
+        else:
+            check(load().cf_amg_build(A._h, None, None, 1, C.byref(self.opts), C.byref(self._h)))
+        nl, cd = C.c_int(), C.c_int64()
+        check(load().cf_amg_info(self._h, C.byref(nl), C.byref(cd)))
+        self._n_levels, self._coarse = nl.value, cd.value
+
+    def __del__(self):
+        try:
+            load().cf_amg_destroy(self._h)
+        except Exception:
+            pass
+
+    def n_levels(self):
+        return self._n_levels
+
+    def coarse_dim(self):
+        return self._coarse
+
+    def v_cycle(self, r):
+        r = _as_f64(r)
+        x = _empty_like_kind(r, self.A.rows)
+        check(load().cf_amg_vcycle(self._h, _ptr(r), _ptr(x)))
+        return x
+
+    def level_info(self, lev: int) -> dict:
+        info = np.zeros(8, dtype=np.int64)
+        lam, jw = C.c_double(), C.c_double()
+        check(load().cf_amg_level_info(self._h, lev, _ptr(info), C.byref(lam), C.byref(jw)))
+        keys = ("rows", "nnz_A", "nnz_P", "coarse", "n_nodes", "n_aggregates", "strong_edges", "lfmis_rounds")
+        d = {k: int(v) for k, v in zip(keys, info)}
+        d.update(lam=lam.value, jacobi_weight=jw.value)
+        return d
+
+    def aggregates(self, lev: int):
+        n = self.level_info(lev)["n_nodes"]
+        out = np.zeros(n, dtype=np.int32)
+        check(load().cf_amg_level_aggregates(self._h, lev, _ptr(out)))
+        return out
+
+    def level_matrix(self, lev: int, which: int) -> Csr:
+        info = self.level_info(lev)
+        rows = info["rows"]
+        nnz = info["nnz_A"] if which == 0 else info["nnz_P"]
+        ptr = np.zeros(rows + 1, dtype=np.int64)
+        col = np.zeros(nnz, dtype=np.int32)
+        val = np.zeros(nnz)
+        check(load().cf_amg_level_export(self._h, lev, which, _ptr(ptr), _ptr(col), _ptr(val)))
+        return Csr(rows, rows if which == 0 else info["coarse"], ptr, col, val)
+
+
+def build_amg(A: CsrMatrix, node_of_dof=None, near_nullspace=None, opts: AmgOptions | None = None) -> AmgHierarchy:
+    """linsolve.hpp:90-94 (node_of_dof + near-nullspace) or the scalar overload (both None)."""
+    return AmgHierarchy(A, node_of_dof, near_nullspace, opts)
+
+
+PREC_KINDS = {"exact": 0, "amg": 1, "diagonal": 2}
+
+
+def preconditioner_kind_from_string(s: str) -> int:
+    """linsolve.cpp:345-350."""
+    if s not in PREC_KINDS:
+        raise ValueError(f"unknown preconditioner kind: {s}")
+    return PREC_KINDS[s]
+
+
+class BlockPreconditioner:
+    """linsolve.hpp:106-128: diag(M_uu^-1, M_phiphi^-1) approximations, frozen at build."""
+
+    def __init__(self, handle, n):
+        self._h, self.n = handle, n
+
+    @staticmethod
+    def build(J: BlockSystem, kind=1, amg_opts: AmgOptions | None = None, prob: Problem | None = None,
+              constraints: ConstraintSet | None = None):
+        kind = preconditioner_kind_from_string(kind) if isinstance(kind, str) else int(kind)
+        h = C.c_void_p()
+        o = amg_opts or AmgOptions()
+        check(load().cf_prec_build(J._h, kind, C.byref(o), prob._h if prob else None,
+                                   constraints._h if constraints else None, C.byref(h)))
+        return BlockPreconditioner(h, J.n_total())
+
+    def __del__(self):
+        try:
+            load().cf_prec_destroy(self._h)
+        except Exception:
+            pass
+
+    def apply(self, r):
+        r = _as_f64(r)
+        z = _empty_like_kind(r, self.n)
+        check(load().cf_prec_apply(self._h, _ptr(r), _ptr(z)))
+        return z
+
+
+def rigid_body_modes(prob: Problem, constraints: ConstraintSet):
+    """linsolve.cpp:320-343: n_u x m (m = 3 in 2d, 6 in 3d)."""
+    m = 3 if prob.dim == 2 else 6
+    B = np.zeros(m * prob.n_u)
+    check(load().cf_rigid_body_modes(prob._h, constraints._h, _ptr(B)))
+    return B.reshape(m, prob.n_u).T.copy()
+
+
+def gmres(op, rhs, prec=None, opts: GmresOptions | None = None):
+    """linsolve.hpp:48-49.  op: BlockSystem or CsrMatrix; prec: BlockPreconditioner, AmgHierarchy
+    or None.  Returns dict(x, iterations, converged, breakdown, residual, residual_history)."""
+    from ._lib import GmresResultC
+    o = opts or GmresOptions()
+    b = _as_f64(rhs)
+    x = _empty_like_kind(b, len(b))
+    res = GmresResultC()
+    hist = np.zeros(max(1, o.max_iter))
+    J = op._h if isinstance(op, BlockSystem) else None
+    A = op._h if isinstance(op, CsrMatrix) else None
+    P = prec._h if isinstance(prec, BlockPreconditioner) else None
+    M = prec._h if isinstance(prec, AmgHierarchy) else None
+    check(load().cf_gmres(J, A, P, M, _ptr(b), C.byref(o), _ptr(x), C.byref(res), _ptr(hist), len(hist)))
+    return dict(x=x, iterations=res.iterations, converged=bool(res.converged), breakdown=bool(res.breakdown),
+                residual=res.residual, residual_history=hist[:res.iterations].copy())
+
+
+# ---------------------------------------------------------------------------- Newton / active set
+def slit_band_edge(prob: Problem, mat: Material) -> float:
+    out = C.c_double()
+    check(load().cf_slit_band_edge(prob._h, C.byref(mat), C.byref(out)))
+    return out.value
+
+
+def resolve_regularization(prob: Problem, mat: Material, band_edge: float) -> Regularization:
+    reg = Regularization()
+    check(load().cf_resolve_regularization(prob._h, C.byref(mat), float(band_edge), C.byref(reg)))
+    return reg
+
+
+def initial_crack(prob: Problem, mat: Material, band_half: float = 0.0):
+    """model.cpp:324-349: (phi seed, band edge)."""
+    phi = np.zeros(prob.n_vertices)
+    be = C.c_double()
+    check(load().cf_initial_crack(prob._h, C.byref(mat), float(band_half), _ptr(phi), C.byref(be)))
+    return phi, be.value
+
+
+class FractureState:
+    """model.hpp:50-55 on the device: solution (u, phi), phi_old, phi_prev2, step."""
+
+    def __init__(self, prob: Problem, solution=None, phi_old=None, phi_prev2=None, step=0, _handle=None):
+        self.prob = prob
+        if _handle is not None:
+            self._h = _handle
+        else:
+            arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+                    for a in (solution, phi_old, phi_prev2)]
+            self._h = C.c_void_p()
+            check(load().cf_state_create(prob._h, *[_ptr(a) for a in arrs], int(step), C.byref(self._h)))
+
+    def __del__(self):
+        try:
+            load().cf_state_destroy(self._h)
+        except Exception:
+            pass
+
+    def get(self):
+        p = self.prob
+        sol, po, pp = np.zeros(p.n_total), np.zeros(p.n_vertices), np.zeros(p.n_vertices)
+        step = C.c_int()
+        check(load().cf_state_get(self._h, _ptr(sol), _ptr(po), _ptr(pp), C.byref(step)))
+        return dict(solution=sol, phi_old=po, phi_prev2=pp, step=step.value)
+
+    @property
+    def solution(self):
+        return self.get()["solution"]
+
+
+def make_initial_state(prob: Problem, mat: Material, seed_band: float = 0.0) -> FractureState:
+    """solver.cpp:24-35: u = 0, phi = phi_old = phi_prev2 = initial crack, step 0."""
+    h = C.c_void_p()
+    check(load().cf_make_initial_state(prob._h, C.byref(mat), float(seed_band), C.byref(h)))
+    return FractureState(prob, _handle=h)
+
+
+def _report(its, n, conv, feas, times=None):
+    rows = [dict(residual_norm=its[i].residual_norm, active_size=its[i].active_size,
+                 set_changes=its[i].set_changes, gmres_iterations=its[i].gmres_iterations) for i in range(n)]
+    out = dict(iterations=rows, converged=bool(conv), feasibility_violation=float(feas))
+    if times is not None:
+        out["times_ms"] = dict(residual=times.residual_ms, active_set=times.active_set_ms,
+                               jacobian=times.jacobian_ms, amg_setup=times.amg_setup_ms, gmres=times.gmres_ms,
+                               total=times.total_ms)
+    return out
+
+
+def newton_active_set_step(state: FractureState, mat: Material, prob: Problem, reg: Regularization,
+                           opts: SolverOptions | None = None, max_its: int = 256) -> dict:
+    """solver.cpp:49-188 (the state is updated in place on the device)."""
+    from ._lib import NewtonIterationC, PhaseTimesC
+    o = opts or SolverOptions()
+    its = (NewtonIterationC * max_its)()
+    n, conv, feas, times = C.c_int(), C.c_int(), C.c_double(), PhaseTimesC()
+    check(load().cf_newton_active_set_step(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o), its, max_its,
+                                           C.byref(n), C.byref(conv), C.byref(feas), C.byref(times)))
+    return _report(its, n.value, conv.value, feas.value, times)
+
+
+def solve_loading_sequence(state: FractureState, mat: Material, prob: Problem, reg: Regularization,
+                           opts: SolverOptions | None, n_steps: int, max_its: int = 1024) -> list:
+    """solver.cpp:190-204: list of per-step reports; stops after a non-converged step."""
+    from ._lib import NewtonIterationC
+    o = opts or SolverOptions()
+    its = (NewtonIterationC * max_its)()
+    n_its = (C.c_int * max(1, n_steps))()
+    conv = (C.c_int * max(1, n_steps))()
+    feas = (C.c_double * max(1, n_steps))()
+    done = C.c_int()
+    check(load().cf_solve_loading_sequence(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o), int(n_steps),
+                                           its, max_its, n_its, conv, feas, C.byref(done)))
+    out, off = [], 0
+    for s in range(done.value):
+        k = n_its[s]
+        sub = (type(its[0]) * max(1, k))(*[its[off + i] for i in range(k)])
+        out.append(_report(sub, k, conv[s], feas[s]))
+        off += k
+    return out

@@ -109,7 +109,51 @@ SIGNATURES = [
     ("cf_block_apply", _I, [_P, _P, _P]),
     ("cf_block_spmv", _I, [_P, _I, _P, _P]),
     ("cf_block_destroy", _I, [_P]),
+    ("cf_tune_spmv", _I, [_P, _I, _I, _I, _P, _P]),
+    ("cf_csr_create", _I, [_L, _L, _P, _P, _P, C.POINTER(_P)]),
+    ("cf_block_csr", _I, [_P, _I, C.POINTER(_P)]),
+    ("cf_csr_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),
+    ("cf_csr_spmv", _I, [_P, _P, _P]),
+    ("cf_csr_destroy", _I, [_P]),
+    ("cf_amg_build", _I, [_P, _P, _P, _I, C.POINTER(AmgOptions), C.POINTER(_P)]),
+    ("cf_amg_vcycle", _I, [_P, _P, _P]),
+    ("cf_amg_info", _I, [_P, C.POINTER(_I), C.POINTER(_L)]),
+    ("cf_amg_level_info", _I, [_P, _I, _P, C.POINTER(_D), C.POINTER(_D)]),
+    ("cf_amg_level_aggregates", _I, [_P, _I, _P]),
+    ("cf_amg_level_export", _I, [_P, _I, _I, _P, _P, _P]),
+    ("cf_amg_destroy", _I, [_P]),
+    ("cf_prec_build", _I, [_P, _I, C.POINTER(AmgOptions), _P, _P, C.POINTER(_P)]),
+    ("cf_prec_apply", _I, [_P, _P, _P]),
+    ("cf_prec_destroy", _I, [_P]),
+    ("cf_rigid_body_modes", _I, [_P, _P, _P]),
+    ("cf_gmres", _I, [_P, _P, _P, _P, _P, C.POINTER(GmresOptions), _P, _P, _P, _I]),
+    ("cf_slit_band_edge", _I, [_P, C.POINTER(Material), C.POINTER(_D)]),
+    ("cf_resolve_regularization", _I, [_P, C.POINTER(Material), _D, C.POINTER(Regularization)]),
+    ("cf_initial_crack", _I, [_P, C.POINTER(Material), _D, _P, C.POINTER(_D)]),
+    ("cf_make_initial_state", _I, [_P, C.POINTER(Material), _D, C.POINTER(_P)]),
+    ("cf_state_create", _I, [_P, _P, _P, _P, _I, C.POINTER(_P)]),
+    ("cf_state_get", _I, [_P, _P, _P, _P, C.POINTER(_I)]),
+    ("cf_state_destroy", _I, [_P]),
+    ("cf_newton_active_set_step", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
+                                       C.POINTER(SolverOptions), _P, _I, C.POINTER(_I), C.POINTER(_I),
+                                       C.POINTER(_D), _P]),
+    ("cf_solve_loading_sequence", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
+                                       C.POINTER(SolverOptions), _I, _P, _I, _P, _P, _P, C.POINTER(_I)]),
 ]
+
+
+class GmresResultC(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("converged", C.c_int), ("breakdown", C.c_int), ("residual", C.c_double)]
+
+
+class NewtonIterationC(C.Structure):
+    _fields_ = [("residual_norm", C.c_double), ("active_size", C.c_int), ("set_changes", C.c_int),
+                ("gmres_iterations", C.c_int)]
+
+
+class PhaseTimesC(C.Structure):
+    _fields_ = [("residual_ms", C.c_double), ("active_set_ms", C.c_double), ("jacobian_ms", C.c_double),
+                ("amg_setup_ms", C.c_double), ("gmres_ms", C.c_double), ("total_ms", C.c_double)]
 
 
 def load(path: str | None = None):

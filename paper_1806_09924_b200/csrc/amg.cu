@@ -1,0 +1,1005 @@
+// K7/K8: smoothed-aggregation AMG setup and V-cycle on the device (linsolve.cpp:117-318).
+//
+// Setup per level, all on the device and deterministic (compiled with -fmad=false so every
+// floating-point expression is the reference's sequence of IEEE operations):
+//   strength   node blocks grouped by a stable radix sort of node_of_dof; per node, the
+//              Frobenius^2 sums of its coupling blocks accumulated in (row, column) order into a
+//              small sorted key list (std::map semantics); strong iff
+//              sqrt(s_ij) > theta sqrt(sqrt(s_ii) sqrt(s_jj))          (linsolve.cpp:185-201)
+//   aggregate  the reference's sequential greedy (linsolve.cpp:142-166) computed EXACTLY in
+//              parallel: pass-1 roots are the lexicographically-first MIS of the directed
+//              distance-2 dependency graph N2(i) = S[i] u S^T[i] u S^T[S[i]] (i is a root iff no
+//              root r < i lies in N2(i)), resolved by a persistent cooperative kernel that
+//              pushes decisions along N2 frontier by frontier; pass 2/3 by ordered fix-point
+//              rounds.  Identical output to the sequential loop for any strength graph.
+//   tentative  one thread per aggregate runs the column-pivoting Householder QR of its
+//              near-nullspace block (Eigen ColPivHouseholderQR semantics, threshold 1e-10)
+//   smoothing  D^-1 from the diagonal, lambda_max by 15 power iterations, P = T - w D^-1 A T
+//   Galerkin   Ac = P^T (A P) with the deterministic SpGEMM of spgemm.cu, pruned
+// V-cycle: damped Jacobi pre/post sweeps, restriction with an explicit R = P^T, dense LU on the
+// coarsest level (one CTA).
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include <climits>
+#include <cmath>
+#include <unordered_map>
+
+#include "cf_vec.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace cfb {
+
+namespace {
+
+template <class T>
+void scan_excl(T* data, i64 n_plus_1) {
+  size_t bytes = 0;
+  CF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, data, data, n_plus_1, stream()));
+  DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+  CF_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, data, data, n_plus_1, stream()));
+  count_launch();
+}
+
+template <class T>
+T read_dev(const T* p) {
+  T h{};
+  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  return h;
+}
+
+int bits_for(i64 n) {
+  int b = 1;
+  while ((i64(1) << b) < n) ++b;
+  return b;
+}
+
+__global__ void k_iota(i64 n, int* out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = int(i);
+}
+
+__global__ void k_count_keys(i64 n, const int* __restrict__ key, i64* __restrict__ cnt) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(reinterpret_cast<unsigned long long*>(cnt + key[i]), 1ull);
+}
+
+// Stable grouping of items 0..n-1 by key in [0, nkeys): ptr (nkeys+1) and ascending items.
+void group_by_key(i64 n, const int* key, i64 nkeys, DevBuf<i64>& ptr, DevBuf<int>& items) {
+  ptr.alloc(nkeys + 1);
+  ptr.zero();
+  items.alloc(std::max<i64>(n, 1));
+  if (n == 0) return;
+  k_count_keys<<<grid_for(n, 256), 256, 0, stream()>>>(n, key, ptr.p);
+  CF_LAUNCHED();
+  scan_excl(ptr.p, nkeys + 1);
+  DevBuf<int> iota(n), keys_out(n);
+  k_iota<<<grid_for(n, 256), 256, 0, stream()>>>(n, iota.p);
+  CF_LAUNCHED();
+  size_t bytes = 0;
+  const int eb = bits_for(nkeys + 1);
+  CF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, keys_out.p, iota.p, items.p, n, 0, eb, stream()));
+  DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+  CF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key, keys_out.p, iota.p, items.p, n, 0, eb, stream()));
+  count_launch();
+}
+
+// ------------------------------------------------------------------ strength (linsolve.cpp:185-201)
+constexpr int SCAP = 384;  // distinct neighbour nodes per node
+
+__global__ void k_strength_diag(i64 nn, const i64* __restrict__ nptr, const int* __restrict__ ndofs,
+                                const i64* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
+                                const int* __restrict__ nod, double* __restrict__ dsq) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  double s = 0.0;
+  bool present = false;
+  for (i64 t = nptr[i]; t < nptr[i + 1]; ++t) {
+    const int r = ndofs[t];
+    for (i64 k = Ap[r]; k < Ap[r + 1]; ++k)
+      if (nod[Ac[k]] == int(i)) {
+        s += Av[k] * Av[k];
+        present = true;
+      }
+  }
+  dsq[i] = sqrt(present ? s : 0.0);  // sqrt(blk[i].count(i) ? blk[i][i] : 0)
+}
+
+// mode 0: count strong neighbours; mode 1: write them (ascending node id)
+__global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __restrict__ ndofs,
+                           const i64* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
+                           const int* __restrict__ nod, const double* __restrict__ dsq, double theta,
+                           i64* __restrict__ cnt, const i64* __restrict__ sptr, int* __restrict__ sidx, int mode,
+                           int* __restrict__ err) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  int keys[SCAP];
+  double sums[SCAP];
+  int len = 0;
+  for (i64 t = nptr[i]; t < nptr[i + 1]; ++t) {
+    const int r = ndofs[t];
+    for (i64 k = Ap[r]; k < Ap[r + 1]; ++k) {
+      const int nj = nod[Ac[k]];
+      const double a2 = Av[k] * Av[k];
+      int lo = 0, hi = len;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < nj) lo = mid + 1; else hi = mid;
+      }
+      if (lo < len && keys[lo] == nj) {
+        sums[lo] += a2;
+      } else {
+        if (len == SCAP) {
+          *err = 1;
+          return;
+        }
+        for (int s = len; s > lo; --s) {
+          keys[s] = keys[s - 1];
+          sums[s] = sums[s - 1];
+        }
+        keys[lo] = nj;
+        sums[lo] = a2;
+        ++len;
+      }
+    }
+  }
+  const double dii = dsq[i];
+  i64 n = 0;
+  const i64 base = mode ? sptr[i] : 0;
+  for (int s = 0; s < len; ++s) {
+    const int j = keys[s];
+    if (j == int(i)) continue;
+    const double djj = dsq[j];
+    if (sqrt(sums[s]) > theta * sqrt(dii * djj)) {
+      if (mode) sidx[base + n] = j;
+      ++n;
+    }
+  }
+  if (!mode) cnt[i] = n;
+}
+
+// ------------------------------------------------------------------ N2 dependency graph
+// N2(i) = S[i] u T[i] u T[S[i]] (T = S^T), as a k-way merge of sorted lists.  mode 0 counts the
+// lower (< i) and upper (> i) members; mode 1 writes the upper members (the dependents).
+constexpr int MCAP = 256;  // merged lists per node
+
+__global__ void k_n2(i64 nn, const i64* __restrict__ sp, const int* __restrict__ si, const i64* __restrict__ tp,
+                     const int* __restrict__ ti, int* __restrict__ lower, i64* __restrict__ upcnt,
+                     const i64* __restrict__ upptr, int* __restrict__ up, int mode, int* __restrict__ err) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  // lists: S[i], T[i], T[j] for j in S[i]
+  i64 cur[MCAP], end[MCAP];
+  const int* arr[MCAP];
+  int nl = 0;
+  const i64 ns = sp[i + 1] - sp[i];
+  if (ns + 2 > MCAP) {
+    *err = 1;
+    return;
+  }
+  cur[nl] = sp[i]; end[nl] = sp[i + 1]; arr[nl] = si; ++nl;
+  cur[nl] = tp[i]; end[nl] = tp[i + 1]; arr[nl] = ti; ++nl;
+  for (i64 k = sp[i]; k < sp[i + 1]; ++k) {
+    const int j = si[k];
+    cur[nl] = tp[j]; end[nl] = tp[j + 1]; arr[nl] = ti; ++nl;
+  }
+  int nlow = 0;
+  i64 nup = 0;
+  const i64 base = mode ? upptr[i] : 0;
+  int last = -1;
+  while (true) {
+    int best = INT_MAX;
+    for (int l = 0; l < nl; ++l)
+      if (cur[l] < end[l]) {
+        const int v = arr[l][cur[l]];
+        if (v < best) best = v;
+      }
+    if (best == INT_MAX) break;
+    for (int l = 0; l < nl; ++l)
+      while (cur[l] < end[l] && arr[l][cur[l]] == best) ++cur[l];
+    if (best == last) continue;
+    last = best;
+    if (best < int(i)) {
+      ++nlow;
+    } else if (best > int(i)) {
+      if (mode) up[base + nup] = best;
+      ++nup;
+    }
+  }
+  if (!mode) {
+    lower[i] = nlow;
+    upcnt[i] = nup;
+  }
+}
+
+// ------------------------------------------------------------------ pass 1: LFMIS frontier rounds
+constexpr int UND = 0, ROOT = 1, NOTROOT = 2;
+
+__global__ void k_lfmis_init(i64 nn, const int* __restrict__ lower, int* __restrict__ status, int* __restrict__ front,
+                             int* __restrict__ fsize) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  if (lower[i] == 0) {
+    status[i] = ROOT;
+    front[atomicAdd(fsize, 1)] = int(i);
+  } else {
+    status[i] = UND;
+  }
+}
+
+__global__ void k_lfmis(const i64* __restrict__ up_ptr, const int* __restrict__ up, int* cnt, int* status, int* f0,
+                        int* f1, int* sizes, int* rounds) {
+  cg::grid_group g = cg::this_grid();
+  int r = 0;
+  while (true) {
+    int* F = (r & 1) ? f1 : f0;
+    int* G = (r & 1) ? f0 : f1;
+    const int nf = *((volatile int*)&sizes[r % 3]);
+    if (nf == 0) break;
+    if (g.thread_rank() == 0) sizes[(r + 2) % 3] = 0;
+    int* nxt = &sizes[(r + 1) % 3];
+    for (long long t = g.thread_rank(); t < nf; t += g.size()) {
+      const int v = F[t];
+      const int st = *((volatile int*)&status[v]);
+      for (i64 k = up_ptr[v]; k < up_ptr[v + 1]; ++k) {
+        const int i = up[k];
+        if (st == ROOT) {
+          if (atomicCAS(&status[i], UND, NOTROOT) == UND) G[atomicAdd(nxt, 1)] = i;
+        } else {
+          if (atomicSub(&cnt[i], 1) == 1)
+            if (atomicCAS(&status[i], UND, ROOT) == UND) G[atomicAdd(nxt, 1)] = i;
+        }
+      }
+    }
+    g.sync();
+    ++r;
+  }
+  if (g.thread_rank() == 0) *rounds = r;
+}
+
+__global__ void k_root_flags(i64 nn, const int* __restrict__ status, int* __restrict__ flag) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nn) flag[i] = status[i] == ROOT ? 1 : 0;
+}
+
+// roots claim their strong neighbours (disjoint by construction)
+__global__ void k_claim(i64 nn, const int* __restrict__ status, const int* __restrict__ rootid,
+                        const i64* __restrict__ sp, const int* __restrict__ si, int* __restrict__ agg) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn || status[i] != ROOT) return;
+  const int a = rootid[i];
+  agg[i] = a;
+  for (i64 k = sp[i]; k < sp[i + 1]; ++k) agg[si[k]] = a;
+}
+
+// pass 2 (linsolve.cpp:157-161): p2 state -1 unresolved, -2 unassignable, >=0 assigned aggregate.
+__global__ void k_pass2(i64 nn, const i64* __restrict__ sp, const int* __restrict__ si, const int* __restrict__ agg1,
+                        int* __restrict__ p2, int* __restrict__ changed) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn || agg1[i] >= 0 || p2[i] != -1) return;
+  for (i64 k = sp[i]; k < sp[i + 1]; ++k) {
+    const int j = si[k];
+    if (agg1[j] >= 0) {
+      p2[i] = agg1[j];
+      *changed = 1;
+      return;
+    }
+    if (j < int(i)) {
+      const int s = *((volatile int*)&p2[j]);
+      if (s >= 0) {
+        p2[i] = s;
+        *changed = 1;
+        return;
+      }
+      if (s == -1) return;  // wait for j
+    }
+  }
+  p2[i] = -2;
+  *changed = 1;
+}
+
+__global__ void k_pass3_flags(i64 nn, const int* __restrict__ agg1, const int* __restrict__ p2, int* __restrict__ f) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nn) f[i] = (agg1[i] < 0 && p2[i] == -2) ? 1 : 0;
+}
+
+__global__ void k_final_agg(i64 nn, const int* __restrict__ agg1, const int* __restrict__ p2,
+                            const int* __restrict__ p3id, int n1, int* __restrict__ agg) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  agg[i] = agg1[i] >= 0 ? agg1[i] : (p2[i] >= 0 ? p2[i] : n1 + p3id[i]);
+}
+
+// ------------------------------------------------------------------ tentative prolongator (QR)
+__global__ void k_agg_of_dof(i64 n, const int* __restrict__ nod, const int* __restrict__ agg, int* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = agg[nod[i]];
+}
+
+// Column-pivoting Householder QR of one aggregate's near-nullspace block (Eigen 3.3
+// ColPivHouseholderQR::computeInPlace / rank / householderQ, sequential sums), m <= 8.
+__global__ void k_agg_qr(i64 na, const i64* __restrict__ aptr, const int* __restrict__ adofs,
+                         const double* __restrict__ B, i64 n, int m, double* __restrict__ W, double* __restrict__ Q,
+                         double* __restrict__ hc_all, int* __restrict__ perm_all, int* __restrict__ rank_out) {
+  const i64 a = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= na) return;
+  const i64 off = aptr[a];
+  const int rows = int(aptr[a + 1] - off);
+  double* qr = W + off * m;  // column-major, ld = rows
+  for (int c = 0; c < m; ++c)
+    for (int r = 0; r < rows; ++r) qr[c * rows + r] = B[i64(c) * n + adofs[off + r]];
+  const int cols = m, size = rows < cols ? rows : cols;
+  double upd[8], dir[8], hc[8];
+  int transp[8], perm[8];
+  for (int k = 0; k < cols; ++k) {
+    double s = 0.0;
+    for (int r = 0; r < rows; ++r) s += qr[k * rows + r] * qr[k * rows + r];
+    dir[k] = sqrt(s);
+    upd[k] = dir[k];
+  }
+  double mx = 0.0;
+  for (int k = 0; k < cols; ++k) mx = (k == 0 || upd[k] > mx) ? upd[k] : mx;
+  const double eps = 2.220446049250313e-16;
+  const double th_helper = (mx * eps) * (mx * eps) / double(rows);
+  const double ndt = sqrt(eps);
+  int nonzero = size;
+  double maxpivot = 0.0;
+  for (int k = 0; k < size; ++k) {
+    int bi = k;
+    double bv = upd[k];
+    for (int j = k + 1; j < cols; ++j)
+      if (upd[j] > bv) {
+        bv = upd[j];
+        bi = j;
+      }
+    const double bsq = bv * bv;
+    if (nonzero == size && bsq < th_helper * double(rows - k)) nonzero = k;
+    transp[k] = bi;
+    if (k != bi) {
+      for (int r = 0; r < rows; ++r) {
+        const double t = qr[k * rows + r];
+        qr[k * rows + r] = qr[bi * rows + r];
+        qr[bi * rows + r] = t;
+      }
+      double t = upd[k]; upd[k] = upd[bi]; upd[bi] = t;
+      t = dir[k]; dir[k] = dir[bi]; dir[bi] = t;
+    }
+    double beta, tau;
+    {
+      const double c0 = qr[k * rows + k];
+      double tsq = 0.0;
+      for (int r = k + 1; r < rows; ++r) tsq += qr[k * rows + r] * qr[k * rows + r];
+      if (tsq <= 2.2250738585072014e-308) {
+        tau = 0.0;
+        beta = c0;
+        for (int r = k + 1; r < rows; ++r) qr[k * rows + r] = 0.0;
+      } else {
+        beta = sqrt(c0 * c0 + tsq);
+        if (c0 >= 0.0) beta = -beta;
+        for (int r = k + 1; r < rows; ++r) qr[k * rows + r] = qr[k * rows + r] / (c0 - beta);
+        tau = (beta - c0) / beta;
+      }
+    }
+    hc[k] = tau;
+    qr[k * rows + k] = beta;
+    if (fabs(beta) > maxpivot) maxpivot = fabs(beta);
+    for (int j = k + 1; j < cols; ++j) {
+      if (rows - k == 1) {
+        qr[j * rows + k] *= (1.0 - tau);
+      } else if (tau != 0.0) {
+        double t = 0.0;
+        for (int r = k + 1; r < rows; ++r) t += qr[k * rows + r] * qr[j * rows + r];
+        t += qr[j * rows + k];
+        qr[j * rows + k] -= tau * t;
+        for (int r = k + 1; r < rows; ++r) qr[j * rows + r] -= (tau * qr[k * rows + r]) * t;
+      }
+    }
+    for (int j = k + 1; j < cols; ++j) {
+      if (upd[j] != 0.0) {
+        double tmp = fabs(qr[j * rows + k]) / upd[j];
+        tmp = (1.0 + tmp) * (1.0 - tmp);
+        tmp = tmp < 0.0 ? 0.0 : tmp;
+        const double ratio = upd[j] / dir[j];
+        const double tmp2 = tmp * (ratio * ratio);
+        if (tmp2 <= ndt) {
+          double s = 0.0;
+          for (int r = k + 1; r < rows; ++r) s += qr[j * rows + r] * qr[j * rows + r];
+          dir[j] = sqrt(s);
+          upd[j] = dir[j];
+        } else {
+          upd[j] *= sqrt(tmp);
+        }
+      }
+    }
+  }
+  for (int k = 0; k < cols; ++k) perm[k] = k;
+  for (int k = 0; k < size; ++k) {
+    const int t = perm[k];
+    perm[k] = perm[transp[k]];
+    perm[transp[k]] = t;
+  }
+  const double pt = fabs(maxpivot) * 1e-10;
+  int rank = 0;
+  for (int i = 0; i < nonzero; ++i) rank += (fabs(qr[i * rows + i]) > pt) ? 1 : 0;
+  rank = rank < 0 ? 0 : rank;
+  if (rank > size) rank = size;
+  rank_out[a] = rank;
+  for (int k = 0; k < m; ++k) {
+    hc_all[a * 8 + k] = k < size ? hc[k] : 0.0;
+    perm_all[a * 8 + k] = perm[k];
+  }
+  // Q columns c < rank: H_0 ... H_{size-1} e_c
+  double* q = Q + off * m;
+  for (int c = 0; c < rank; ++c) {
+    double* out = q + c * rows;
+    for (int r = 0; r < rows; ++r) out[r] = (r == c) ? 1.0 : 0.0;
+    for (int k = size - 1; k >= 0; --k) {
+      const double tau = hc[k];
+      if (rows - k == 1) {
+        out[k] *= (1.0 - tau);
+      } else if (tau != 0.0) {
+        double t = 0.0;
+        for (int r = k + 1; r < rows; ++r) t += qr[k * rows + r] * out[r];
+        t += out[k];
+        out[k] -= tau * t;
+        for (int r = k + 1; r < rows; ++r) out[r] -= (tau * qr[k * rows + r]) * t;
+      }
+    }
+  }
+}
+
+__global__ void k_pos_in_agg(i64 na, const i64* __restrict__ aptr, const int* __restrict__ adofs, int* __restrict__ pos,
+                             int* __restrict__ agg_of) {
+  const i64 a = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= na) return;
+  for (i64 t = aptr[a]; t < aptr[a + 1]; ++t) {
+    pos[adofs[t]] = int(t - aptr[a]);
+    agg_of[adofs[t]] = int(a);
+  }
+}
+
+// T rows: row i -> entries (agg_offset[a] + c, Q(pos, c)) with |Q| > 1e-300 (linsolve.cpp:230-238)
+__global__ void k_build_T(i64 n, int m, const int* __restrict__ agg_of, const int* __restrict__ pos,
+                          const i64* __restrict__ aptr, const int* __restrict__ rank, const i64* __restrict__ aoff,
+                          const double* __restrict__ Q, i64* __restrict__ tp, int* __restrict__ tc,
+                          double* __restrict__ tv, int mode) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int a = agg_of[i], r = pos[i];
+  const i64 off = aptr[a];
+  const int rows = int(aptr[a + 1] - off);
+  const double* q = Q + off * m;
+  i64 cnt = 0;
+  const i64 base = mode ? tp[i] : 0;
+  for (int c = 0; c < rank[a]; ++c) {
+    const double v = q[c * rows + r];
+    if (fabs(v) > 1e-300) {
+      if (mode) {
+        tc[base + cnt] = int(aoff[a] + c);
+        tv[base + cnt] = v;
+      }
+      ++cnt;
+    }
+  }
+  if (!mode) tp[i] = cnt;
+}
+
+// coarse near-nullspace Bc = [R_a Pi_a^T] and coarse node ids (linsolve.cpp:265-270)
+__global__ void k_build_Bc(i64 na, int m, const i64* __restrict__ aptr, const int* __restrict__ rank,
+                           const i64* __restrict__ aoff, const double* __restrict__ W, const int* __restrict__ perm_all,
+                           i64 nc, double* __restrict__ Bc, int* __restrict__ cnode) {
+  const i64 a = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= na) return;
+  const i64 off = aptr[a];
+  const int rows = int(aptr[a + 1] - off);
+  const double* qr = W + off * m;
+  for (int i = 0; i < rank[a]; ++i) {
+    const i64 row = aoff[a] + i;
+    cnode[row] = int(a);
+    for (int c = 0; c < m; ++c) Bc[i64(c) * nc + row] = 0.0;
+    for (int k = i; k < m; ++k) Bc[i64(perm_all[a * 8 + k]) * nc + row] = qr[k * rows + i];
+  }
+}
+
+__global__ void k_inv_diag(i64 n, double* d) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = d[i] != 0.0 ? 1.0 / d[i] : 0.0;
+}
+// diagonal preconditioner: 1/d, 1 where d == 0 (linsolve.cpp:382-391)
+__global__ void k_inv_diag_one(i64 n, double* d) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = d[i] != 0.0 ? 1.0 / d[i] : 1.0;
+}
+__global__ void k_int_to_i64(i64 n, const int* __restrict__ a, i64* __restrict__ b) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+__global__ void k_graph_rows(i64 nn, const i64* __restrict__ ptr, int* __restrict__ src) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  for (i64 k = ptr[i]; k < ptr[i + 1]; ++k) src[k] = int(i);
+}
+__global__ void k_gather_int(i64 n, const int* __restrict__ idx, const int* __restrict__ src, int* __restrict__ out) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = src[idx[t]];
+}
+
+// ------------------------------------------------------------------ dense LU (one CTA)
+__global__ void k_dense_from_csr(i64 n, const i64* __restrict__ p, const int* __restrict__ c,
+                                 const double* __restrict__ v, double* __restrict__ a) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (i64 k = p[i]; k < p[i + 1]; ++k) a[i64(c[k]) * n + i] = v[k];
+}
+
+// Eigen PartialPivLU semantics (unblocked): first maximal |pivot|, row swap, column divide,
+// rank-1 update.  column-major n x n.
+__global__ void __launch_bounds__(1024) k_dense_lu(int n, double* a, int* piv, double* minpiv) {
+  __shared__ double sv[1024];
+  __shared__ int si[1024];
+  for (int k = 0; k < n; ++k) {
+    double best = -1.0;
+    int bi = k;
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      const double v = fabs(a[i64(k) * n + i]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+    sv[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) {
+        const double o = sv[threadIdx.x + s];
+        const int oi = si[threadIdx.x + s];
+        if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+          sv[threadIdx.x] = o;
+          si[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    const double big = sv[0];
+    const int p = si[0];
+    __syncthreads();
+    if (threadIdx.x == 0) piv[k] = p;
+    if (big != 0.0) {
+      if (p != k)
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+          const double t = a[i64(j) * n + k];
+          a[i64(j) * n + k] = a[i64(j) * n + p];
+          a[i64(j) * n + p] = t;
+        }
+      __syncthreads();
+      const double akk = a[i64(k) * n + k];
+      for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) a[i64(k) * n + i] /= akk;
+    }
+    __syncthreads();
+    const int rem = n - k - 1;
+    for (long long t = threadIdx.x; t < (long long)rem * rem; t += blockDim.x) {
+      const int i = k + 1 + int(t % rem), j = k + 1 + int(t / rem);
+      a[i64(j) * n + i] -= a[i64(k) * n + i] * a[i64(j) * n + k];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double m = INFINITY;
+    for (int i = 0; i < n; ++i) m = fmin(m, fabs(a[i64(i) * n + i]));
+    *minpiv = m;
+  }
+}
+
+// solve (single thread: sequential substitutions, as the oracle)
+__global__ void k_dense_solve(int n, const double* __restrict__ a, const int* __restrict__ piv,
+                              const double* __restrict__ b, double* __restrict__ x) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 0; i < n; ++i) x[i] = b[i];
+  for (int k = 0; k < n; ++k)
+    if (piv[k] != k) {
+      const double t = x[k];
+      x[k] = x[piv[k]];
+      x[piv[k]] = t;
+    }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j) x[i] -= a[i64(j) * n + i] * x[j];
+  for (int i = n - 1; i >= 0; --i) {
+    for (int j = i + 1; j < n; ++j) x[i] -= a[i64(j) * n + i] * x[j];
+    x[i] /= a[i64(i) * n + i];
+  }
+}
+
+// ------------------------------------------------------------------ V-cycle pieces
+// x = w * (d .* b)
+__global__ void k_jacobi0(i64 n, double w, const double* __restrict__ d, const double* __restrict__ b,
+                          double* __restrict__ x) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = w * (d[i] * b[i]);
+}
+// x += w * (d .* (b - ax))
+__global__ void k_jacobi_upd(i64 n, double w, const double* __restrict__ d, const double* __restrict__ b,
+                             const double* __restrict__ ax, double* __restrict__ x) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] += w * (d[i] * (b[i] - ax[i]));
+}
+
+// power-iteration start vector v_i = 1 + 0.5 sin(1 + i) (linsolve.cpp:123): computed on the host
+// with the C library's sin (correctly rounded) and cached per length.
+const double* lambda_start(i64 n) {
+  static std::unordered_map<i64, std::unique_ptr<DevBuf<double>>> cache;
+  auto it = cache.find(n);
+  if (it != cache.end()) return it->second->p;
+  std::vector<double> h(n);
+  for (i64 i = 0; i < n; ++i) h[i] = 1.0 + 0.5 * std::sin(1.0 + double(i));
+  auto buf = std::make_unique<DevBuf<double>>(n);
+  CF_CUDA(cudaMemcpyAsync(buf->p, h.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  const double* p = buf->p;
+  if (cache.size() > 64) cache.clear();
+  cache[n] = std::move(buf);
+  return p;
+}
+
+double estimate_lambda_max(const Csr& A, const double* inv_diag) {  // linsolve.cpp:120-134
+  const i64 n = A.rows;
+  DevBuf<double> v(n), w(n);
+  double* s = scalar_buf(2);
+  const double* v0 = lambda_start(n);
+  vdot_dev(v0, v0, n, s, true);
+  vdiv_dev(v0, s, v.p, n);
+  double lambda = 1.0;
+  for (int it = 0; it < 15; ++it) {
+    csr_spmv_add(A, v.p, w.p, nullptr);
+    vdiag_mul(inv_diag, w.p, w.p, 1.0, n);
+    vdot_dev(w.p, w.p, n, s, true);
+    const double nw = read_dev(s);
+    if (nw == 0.0) return 1.0;
+    lambda = nw;
+    vdiv_dev(w.p, s, v.p, n);
+  }
+  return std::max(lambda, 1e-12);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ dense LU host side
+void DenseLu::factor_from_csr(const Csr& A) {
+  n = A.rows;
+  if (n > 16384) fail(CF_ERR_UNSUPPORTED, "dense LU: matrix too large for the one-CTA factorisation");
+  lu.alloc(std::max<i64>(n * n, 1));
+  lu.zero();
+  piv.alloc(std::max<i64>(n, 1));
+  if (n == 0) {
+    min_abs_pivot = INFINITY;
+    return;
+  }
+  k_dense_from_csr<<<grid_for(n, 256), 256, 0, stream()>>>(n, A.ptr.p, A.col.p, A.val.p, lu.p);
+  CF_LAUNCHED();
+  double* mp = scalar_buf(1);
+  k_dense_lu<<<1, 1024, 0, stream()>>>(int(n), lu.p, piv.p, mp);
+  CF_LAUNCHED();
+  min_abs_pivot = read_dev(mp);
+}
+
+void DenseLu::solve(const double* b, double* x) const {
+  if (n == 0) return;
+  k_dense_solve<<<1, 32, 0, stream()>>>(int(n), lu.p, piv.p, b, x);
+  CF_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ build_amg (linsolve.cpp:170-287)
+std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, const double* B0, int m,
+                               const cf_amg_options& opts) {
+  if (m < 1 || m > 8) fail(CF_ERR_UNSUPPORTED, "build_amg: near-nullspace width must be 1..8");
+  auto h = std::make_unique<Amg>();
+  h->opts = opts;
+  h->n = A0->rows;
+  std::shared_ptr<Csr> A = A0;
+  DevBuf<int> nod(A->rows);
+  DevBuf<double> B(A->rows * m);
+  if (A->rows) {
+    CF_CUDA(cudaMemcpyAsync(nod.p, node_of_dof, size_t(A->rows) * sizeof(int), cudaMemcpyDeviceToDevice, stream()));
+    CF_CUDA(cudaMemcpyAsync(B.p, B0, size_t(A->rows) * m * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+  }
+  DevBuf<int> err(1);
+  for (int lev = 0; lev < opts.max_levels; ++lev) {
+    const i64 n = A->rows;
+    if (n <= opts.coarse_size) break;
+    // n_nodes = max(node_of_dof) + 1
+    i64 n_nodes;
+    {
+      DevBuf<int> mx(1);
+      size_t bytes = 0;
+      CF_CUDA(cub::DeviceReduce::Max(nullptr, bytes, nod.p, mx.p, n, stream()));
+      DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+      CF_CUDA(cub::DeviceReduce::Max(tmp.p, bytes, nod.p, mx.p, n, stream()));
+      count_launch();
+      n_nodes = i64(read_dev(mx.p)) + 1;
+    }
+    // strength graph S (ascending neighbour lists)
+    DevBuf<i64> nptr;
+    DevBuf<int> ndofs;
+    group_by_key(n, nod.p, n_nodes, nptr, ndofs);
+    DevBuf<double> dsq(n_nodes);
+    k_strength_diag<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, nptr.p, ndofs.p, A->ptr.p, A->col.p,
+                                                                   A->val.p, nod.p, dsq.p);
+    CF_LAUNCHED();
+    DevBuf<i64> sptr(n_nodes + 1);
+    sptr.zero();
+    err.zero();
+    k_strength<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, nptr.p, ndofs.p, A->ptr.p, A->col.p, A->val.p,
+                                                              nod.p, dsq.p, opts.strength_threshold, sptr.p, nullptr,
+                                                              nullptr, 0, err.p);
+    CF_LAUNCHED();
+    if (read_dev(err.p)) fail(CF_ERR_UNSUPPORTED, "build_amg: a node couples to more than 384 nodes");
+    scan_excl(sptr.p, n_nodes + 1);
+    const i64 ns = read_dev(sptr.p + n_nodes);
+    DevBuf<int> sidx(std::max<i64>(ns, 1));
+    k_strength<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, nptr.p, ndofs.p, A->ptr.p, A->col.p, A->val.p,
+                                                              nod.p, dsq.p, opts.strength_threshold, nullptr, sptr.p,
+                                                              sidx.p, 1, err.p);
+    CF_LAUNCHED();
+    // transpose T = S^T (ascending lists): stable grouping of edges by destination
+    DevBuf<i64> tptr;
+    DevBuf<int> tidx(std::max<i64>(ns, 1));
+    {
+      DevBuf<int> src(std::max<i64>(ns, 1)), order;
+      k_graph_rows<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, sptr.p, src.p);
+      CF_LAUNCHED();
+      group_by_key(ns, sidx.p, n_nodes, tptr, order);
+      k_gather_int<<<grid_for(ns, 256), 256, 0, stream()>>>(ns, order.p, src.p, tidx.p);
+      CF_LAUNCHED();
+    }
+    // dependency graph N2: lower counts + upper (dependent) lists
+    DevBuf<int> lower(n_nodes);
+    DevBuf<i64> uptr(n_nodes + 1);
+    uptr.zero();
+    err.zero();
+    k_n2<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, lower.p, uptr.p,
+                                                        nullptr, nullptr, 0, err.p);
+    CF_LAUNCHED();
+    if (read_dev(err.p)) fail(CF_ERR_UNSUPPORTED, "build_amg: a node has more than 254 strong neighbours");
+    scan_excl(uptr.p, n_nodes + 1);
+    const i64 nup = read_dev(uptr.p + n_nodes);
+    DevBuf<int> up(std::max<i64>(nup, 1));
+    k_n2<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, nullptr, nullptr,
+                                                        uptr.p, up.p, 1, err.p);
+    CF_LAUNCHED();
+    // pass 1: lexicographically-first MIS of N2 (persistent cooperative frontier kernel)
+    DevBuf<int> status(n_nodes), f0(n_nodes), f1(n_nodes), sizes(3), rounds(1);
+    sizes.zero();
+    k_lfmis_init<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, lower.p, status.p, f0.p, sizes.p);
+    CF_LAUNCHED();
+    {
+      int bps = 0;
+      CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lfmis, 256, 0));
+      const int grid = std::max(1, std::min(bps, 4)) * rt().sm_count;
+      const i64* a1 = uptr.p;
+      const int* a2 = up.p;
+      int* a3 = lower.p;  // consumed as the pending-dependency counter
+      int* a4 = status.p;
+      int* a5 = f0.p;
+      int* a6 = f1.p;
+      int* a7 = sizes.p;
+      int* a8 = rounds.p;
+      void* args[] = {&a1, &a2, &a3, &a4, &a5, &a6, &a7, &a8};
+      CF_CUDA(cudaLaunchCooperativeKernel((void*)k_lfmis, grid, 256, args, 0, stream()));
+      CF_LAUNCHED();
+    }
+    // aggregate ids of the roots (ascending), claims
+    DevBuf<int> rootid(n_nodes + 1), agg1(n_nodes);
+    k_root_flags<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, status.p, rootid.p);
+    CF_LAUNCHED();
+    CF_CUDA(cudaMemsetAsync(rootid.p + n_nodes, 0, sizeof(int), stream()));
+    scan_excl(rootid.p, n_nodes + 1);
+    const int n1 = read_dev(rootid.p + n_nodes);
+    CF_CUDA(cudaMemsetAsync(agg1.p, 0xff, size_t(n_nodes) * sizeof(int), stream()));
+    k_claim<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, status.p, rootid.p, sptr.p, sidx.p, agg1.p);
+    CF_LAUNCHED();
+    // pass 2 (ordered fix point) and pass 3 (new singletons, ascending)
+    DevBuf<int> p2(n_nodes), changed(1);
+    CF_CUDA(cudaMemsetAsync(p2.p, 0xff, size_t(n_nodes) * sizeof(int), stream()));
+    for (int guard = 0;; ++guard) {
+      changed.zero();
+      k_pass2<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, sptr.p, sidx.p, agg1.p, p2.p, changed.p);
+      CF_LAUNCHED();
+      if (!read_dev(changed.p)) break;
+      if (guard > n_nodes + 2) fail(CF_ERR_LOGIC, "build_amg: pass-2 resolution did not converge");
+    }
+    DevBuf<int> p3(n_nodes + 1), agg(n_nodes);
+    k_pass3_flags<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, agg1.p, p2.p, p3.p);
+    CF_LAUNCHED();
+    CF_CUDA(cudaMemsetAsync(p3.p + n_nodes, 0, sizeof(int), stream()));
+    scan_excl(p3.p, n_nodes + 1);
+    const int n3 = read_dev(p3.p + n_nodes);
+    k_final_agg<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, agg1.p, p2.p, p3.p, n1, agg.p);
+    CF_LAUNCHED();
+    const i64 n_agg = i64(n1) + n3;
+    if (n_agg >= n_nodes && n_nodes > 1) break;  // no coarsening possible (linsolve.cpp:203)
+
+    // tentative prolongator: per-aggregate QR of the near-nullspace rows
+    DevBuf<int> aod(n);
+    k_agg_of_dof<<<grid_for(n, 256), 256, 0, stream()>>>(n, nod.p, agg.p, aod.p);
+    CF_LAUNCHED();
+    DevBuf<i64> aptr;
+    DevBuf<int> adofs;
+    group_by_key(n, aod.p, n_agg, aptr, adofs);
+    DevBuf<double> W(n * m), Q(n * m), hc(n_agg * 8);
+    DevBuf<int> perm(n_agg * 8);
+    DevBuf<i64> rank64(n_agg + 1);
+    DevBuf<int> rank(n_agg);
+    k_agg_qr<<<grid_for(n_agg, 64), 64, 0, stream()>>>(n_agg, aptr.p, adofs.p, B.p, n, m, W.p, Q.p, hc.p, perm.p,
+                                                       rank.p);
+    CF_LAUNCHED();
+    k_int_to_i64<<<grid_for(n_agg, 256), 256, 0, stream()>>>(n_agg, rank.p, rank64.p);
+    CF_LAUNCHED();
+    CF_CUDA(cudaMemsetAsync(rank64.p + n_agg, 0, sizeof(i64), stream()));
+    scan_excl(rank64.p, n_agg + 1);  // aggregate column offsets
+    const i64 nc = read_dev(rank64.p + n_agg);
+    if (nc == 0 || nc >= n) break;  // linsolve.cpp:226
+    DevBuf<int> pos(n), agg_of(n);
+    k_pos_in_agg<<<grid_for(n_agg, 256), 256, 0, stream()>>>(n_agg, aptr.p, adofs.p, pos.p, agg_of.p);
+    CF_LAUNCHED();
+    Csr T;
+    T.rows = n;
+    T.cols = nc;
+    T.ptr.alloc(n + 1);
+    T.ptr.zero();
+    k_build_T<<<grid_for(n, 256), 256, 0, stream()>>>(n, m, agg_of.p, pos.p, aptr.p, rank.p, rank64.p, Q.p, T.ptr.p,
+                                                      nullptr, nullptr, 0);
+    CF_LAUNCHED();
+    scan_excl(T.ptr.p, n + 1);
+    T.nnz = read_dev(T.ptr.p + n);
+    T.col.alloc(std::max<i64>(T.nnz, 1));
+    T.val.alloc(std::max<i64>(T.nnz, 1));
+    k_build_T<<<grid_for(n, 256), 256, 0, stream()>>>(n, m, agg_of.p, pos.p, aptr.p, rank.p, rank64.p, Q.p, T.ptr.p,
+                                                      T.col.p, T.val.p, 1);
+    CF_LAUNCHED();
+
+    // smoothing: P = T - (w_P 2/lambda) D^-1 A T, pruned (linsolve.cpp:240-251)
+    auto L = std::make_unique<AmgLevel>();
+    L->inv_diag.alloc(n);
+    csr_diagonal(*A, L->inv_diag.p);
+    k_inv_diag<<<grid_for(n, 256), 256, 0, stream()>>>(n, L->inv_diag.p);
+    CF_LAUNCHED();
+    const double lambda = estimate_lambda_max(*A, L->inv_diag.p);
+    const double wp = opts.prolongation_omega * 2.0 / lambda;
+    auto DAT = spgemm(*A, T, L->inv_diag.p);
+    L->P = csr_axpy_prune(T, wp, *DAT);
+    DAT.reset();
+    L->R = transpose(*L->P);
+    L->A = A;
+    L->jacobi_weight = opts.jacobi_omega * 2.0 / lambda;
+    L->lambda = lambda;
+    L->n_nodes = n_nodes;
+    L->n_aggregates = n_agg;
+    L->strong_edges = ns;
+    L->lfmis_rounds = read_dev(rounds.p);
+    L->agg_of_node = std::move(agg);
+    // Galerkin coarse operator Ac = P^T (A P), pruned; coarse nullspace and node ids
+    auto AP = spgemm(*A, *L->P);
+    auto Ac = spgemm(*L->R, *AP);
+    AP.reset();
+    csr_prune(*Ac);
+    DevBuf<double> Bc(nc * m);
+    DevBuf<int> cnode(nc);
+    k_build_Bc<<<grid_for(n_agg, 256), 256, 0, stream()>>>(n_agg, m, aptr.p, rank.p, rank64.p, W.p, perm.p, nc, Bc.p,
+                                                           cnode.p);
+    CF_LAUNCHED();
+    L->tmp_r.alloc(n);
+    L->tmp_b.alloc(nc);
+    L->tmp_x.alloc(nc);
+    h->levels.push_back(std::move(L));
+    A = std::shared_ptr<Csr>(std::move(Ac));
+    B = std::move(Bc);
+    nod = std::move(cnode);
+  }
+  h->coarse.factor_from_csr(*A);
+  if (A->rows > 0 && h->coarse.min_abs_pivot == 0.0)
+    fail(CF_ERR_NUMERICAL, "build_amg: coarsest-level matrix is singular");
+  h->cb.alloc(std::max<i64>(A->rows, 1));
+  h->cx.alloc(std::max<i64>(A->rows, 1));
+  h->coarse_A = A;
+  return h;
+}
+
+// linsolve.cpp:295-312, zero initial guess
+void Amg::vcycle(const double* r, double* x) const {
+  const double* b = r;
+  for (size_t l = 0; l < levels.size(); ++l) {
+    const AmgLevel& L = *levels[l];
+    const i64 n = L.A->rows;
+    double* xl = (l == 0) ? x : levels[l - 1]->tmp_x.p;
+    const double w = L.jacobi_weight;
+    k_jacobi0<<<grid_for(n, 256), 256, 0, stream()>>>(n, w, L.inv_diag.p, b, xl);
+    CF_LAUNCHED();
+    for (int s = 1; s < opts.smoothing_sweeps; ++s) {
+      csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
+      k_jacobi_upd<<<grid_for(n, 256), 256, 0, stream()>>>(n, w, L.inv_diag.p, b, L.tmp_r.p, xl);
+      CF_LAUNCHED();
+    }
+    csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
+    vsub(b, L.tmp_r.p, L.tmp_r.p, n);             // r = b - A x
+    csr_spmv_add(*L.R, L.tmp_r.p, L.tmp_b.p, nullptr);  // b_c = P^T r
+    b = L.tmp_b.p;
+  }
+  // coarsest
+  const double* bc = b;
+  double* xc = levels.empty() ? x : levels.back()->tmp_x.p;
+  coarse.solve(bc, xc);
+  for (size_t l = levels.size(); l-- > 0;) {
+    const AmgLevel& L = *levels[l];
+    const i64 n = L.A->rows;
+    double* xl = (l == 0) ? x : levels[l - 1]->tmp_x.p;
+    const double* bl = (l == 0) ? r : levels[l - 1]->tmp_b.p;
+    csr_spmv_add(*L.P, L.tmp_x.p, xl, xl);  // x += P x_c
+    for (int s = 0; s < opts.smoothing_sweeps; ++s) {
+      csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
+      k_jacobi_upd<<<grid_for(n, 256), 256, 0, stream()>>>(n, L.jacobi_weight, L.inv_diag.p, bl, L.tmp_r.p, xl);
+      CF_LAUNCHED();
+    }
+  }
+}
+
+// ------------------------------------------------------------------ block preconditioner
+std::unique_ptr<BlockPrec> build_block_prec(const BlockSystem& J, int kind, const cf_amg_options& o,
+                                            const NullspaceDev* ns) {
+  auto p = std::make_unique<BlockPrec>();
+  p->kind = kind;
+  p->nu = J.nu;
+  p->np = J.np;
+  if (kind == 0) {  // exact: dense LU of each diagonal block (small systems only)
+    p->lu_u = std::make_shared<DenseLu>();
+    p->lu_p = std::make_shared<DenseLu>();
+    p->lu_u->factor_from_csr(*J.uu);
+    p->lu_p->factor_from_csr(*J.pp);
+    if ((J.nu > 0 && p->lu_u->min_abs_pivot == 0.0) || (J.np > 0 && p->lu_p->min_abs_pivot == 0.0))
+      fail(CF_ERR_NUMERICAL, "BlockPreconditioner: block factorization failed");
+  } else if (kind == 1) {
+    if (ns) {
+      p->amg_u = build_amg(J.uu, ns->u_node, ns->u_modes, ns->m_u, o);
+      p->amg_p = build_amg(J.pp, ns->p_node, ns->p_modes, 1, o);
+    } else {
+      DevBuf<int> idu(J.nu), idp(J.np);
+      DevBuf<double> onu(J.nu), onp(J.np);
+      k_iota<<<grid_for(J.nu, 256), 256, 0, stream()>>>(J.nu, idu.p);
+      CF_LAUNCHED();
+      k_iota<<<grid_for(J.np, 256), 256, 0, stream()>>>(J.np, idp.p);
+      CF_LAUNCHED();
+      vfill(onu.p, 1.0, J.nu);
+      vfill(onp.p, 1.0, J.np);
+      p->amg_u = build_amg(J.uu, idu.p, onu.p, 1, o);
+      p->amg_p = build_amg(J.pp, idp.p, onp.p, 1, o);
+    }
+  } else if (kind == 2) {
+    p->inv_u.alloc(J.nu);
+    p->inv_p.alloc(J.np);
+    csr_diagonal(*J.uu, p->inv_u.p);
+    csr_diagonal(*J.pp, p->inv_p.p);
+    k_inv_diag_one<<<grid_for(J.nu, 256), 256, 0, stream()>>>(J.nu, p->inv_u.p);
+    CF_LAUNCHED();
+    k_inv_diag_one<<<grid_for(J.np, 256), 256, 0, stream()>>>(J.np, p->inv_p.p);
+    CF_LAUNCHED();
+  } else {
+    fail(CF_ERR_INVALID_ARGUMENT, "unknown preconditioner kind");
+  }
+  return p;
+}
+
+void BlockPrec::apply(const double* r, double* z) const {  // linsolve.cpp:398-415
+  if (kind == 0) {
+    lu_u->solve(r, z);
+    lu_p->solve(r + nu, z + nu);
+  } else if (kind == 1) {
+    amg_u->vcycle(r, z);
+    amg_p->vcycle(r + nu, z + nu);
+  } else {
+    vdiag_mul(inv_u.p, r, z, 1.0, nu);
+    vdiag_mul(inv_p.p, r + nu, z + nu, 1.0, np);
+  }
+}
+
+}  // namespace cfb

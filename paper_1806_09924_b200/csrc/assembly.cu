@@ -693,39 +693,39 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   k_cell_qpstate<D><<<grid_for(g.ncells, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p);
   CF_LAUNCHED();
   const i64 nu = g.n_u(), np = g.V;
-  J.uu.rows = J.uu.cols = nu;
-  J.pu.rows = np;
-  J.pu.cols = nu;
-  J.pp.rows = J.pp.cols = np;
-  J.uu.ptr.alloc(nu + 1);
-  J.pu.ptr.alloc(np + 1);
-  J.pp.ptr.alloc(np + 1);
-  CF_CUDA(cudaMemsetAsync(J.uu.ptr.p + nu, 0, sizeof(i64), stream()));
-  CF_CUDA(cudaMemsetAsync(J.pu.ptr.p + np, 0, sizeof(i64), stream()));
-  CF_CUDA(cudaMemsetAsync(J.pp.ptr.p + np, 0, sizeof(i64), stream()));
-  k_jac_count<D><<<grid_for(g.V, 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu.ptr.p, J.pu.ptr.p,
-                                                           J.pp.ptr.p);
+  J.uu->rows = J.uu->cols = nu;
+  J.pu->rows = np;
+  J.pu->cols = nu;
+  J.pp->rows = J.pp->cols = np;
+  J.uu->ptr.alloc(nu + 1);
+  J.pu->ptr.alloc(np + 1);
+  J.pp->ptr.alloc(np + 1);
+  CF_CUDA(cudaMemsetAsync(J.uu->ptr.p + nu, 0, sizeof(i64), stream()));
+  CF_CUDA(cudaMemsetAsync(J.pu->ptr.p + np, 0, sizeof(i64), stream()));
+  CF_CUDA(cudaMemsetAsync(J.pp->ptr.p + np, 0, sizeof(i64), stream()));
+  k_jac_count<D><<<grid_for(g.V, 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.pu->ptr.p,
+                                                           J.pp->ptr.p);
   CF_LAUNCHED();
-  exclusive_scan_inplace(J.uu.ptr.p, nu);
-  exclusive_scan_inplace(J.pu.ptr.p, np);
-  exclusive_scan_inplace(J.pp.ptr.p, np);
+  exclusive_scan_inplace(J.uu->ptr.p, nu);
+  exclusive_scan_inplace(J.pu->ptr.p, np);
+  exclusive_scan_inplace(J.pp->ptr.p, np);
   i64 nnz[3];
-  CF_CUDA(cudaMemcpyAsync(&nnz[0], J.uu.ptr.p + nu, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaMemcpyAsync(&nnz[1], J.pu.ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaMemcpyAsync(&nnz[2], J.pp.ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaMemcpyAsync(&nnz[0], J.uu->ptr.p + nu, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaMemcpyAsync(&nnz[1], J.pu->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaMemcpyAsync(&nnz[2], J.pp->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
-  J.uu.nnz = nnz[0];
-  J.pu.nnz = nnz[1];
-  J.pp.nnz = nnz[2];
-  J.uu.col.alloc(nnz[0]);
-  J.uu.val.alloc(nnz[0]);
-  J.pu.col.alloc(nnz[1]);
-  J.pu.val.alloc(nnz[1]);
-  J.pp.col.alloc(nnz[2]);
-  J.pp.val.alloc(nnz[2]);
-  k_jac_fill<D><<<grid_for(g.V * S, 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu.ptr.p,
-                                                              J.uu.col.p, J.uu.val.p, J.pu.ptr.p, J.pu.col.p,
-                                                              J.pu.val.p, J.pp.ptr.p, J.pp.col.p, J.pp.val.p);
+  J.uu->nnz = nnz[0];
+  J.pu->nnz = nnz[1];
+  J.pp->nnz = nnz[2];
+  J.uu->col.alloc(nnz[0]);
+  J.uu->val.alloc(nnz[0]);
+  J.pu->col.alloc(nnz[1]);
+  J.pu->val.alloc(nnz[1]);
+  J.pp->col.alloc(nnz[2]);
+  J.pp->val.alloc(nnz[2]);
+  k_jac_fill<D><<<grid_for(g.V * S, 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p,
+                                                              J.uu->col.p, J.uu->val.p, J.pu->ptr.p, J.pu->col.p,
+                                                              J.pu->val.p, J.pp->ptr.p, J.pp->col.p, J.pp->val.p);
   CF_LAUNCHED();
 }
 

@@ -1,12 +1,27 @@
 // C ABI (include/crackfield_b200.h): status codes, last-error text, handle ownership and
 // host/device argument staging around the cfb:: implementation.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
 #include "cf_types.hpp"
+#include "cf_vec.hpp"
 
 struct cf_problem_s {
   cfb::Problem* p;
+};
+struct cf_csr_s {
+  std::shared_ptr<cfb::Csr> A;
+};
+struct cf_amg_s {
+  std::unique_ptr<cfb::Amg> h;
+};
+struct cf_prec_s {
+  std::unique_ptr<cfb::BlockPrec> p;
+};
+struct cf_state_s {
+  cfb::State st;
+  cf_problem prob;
 };
 struct cf_constraints_s {
   std::unique_ptr<cfb::Constraints> c;
@@ -192,9 +207,9 @@ int cf_block_info(cf_block b, int64_t* n_u, int64_t* n_phi, int64_t* nnz3) {
     if (n_u) *n_u = b->J->nu;
     if (n_phi) *n_phi = b->J->np;
     if (nnz3) {
-      nnz3[0] = b->J->uu.nnz;
-      nnz3[1] = b->J->pu.nnz;
-      nnz3[2] = b->J->pp.nnz;
+      nnz3[0] = b->J->uu->nnz;
+      nnz3[1] = b->J->pu->nnz;
+      nnz3[2] = b->J->pp->nnz;
     }
   });
 }
@@ -202,7 +217,7 @@ int cf_block_info(cf_block b, int64_t* n_u, int64_t* n_phi, int64_t* nnz3) {
 int cf_block_export(cf_block b, int which, int64_t* rowptr, int32_t* col, double* val) {
   return guard([&] {
     CHECK_ARG(b && which >= 0 && which <= 2, "cf_block_export: bad argument");
-    const Csr& A = which == 0 ? b->J->uu : (which == 1 ? b->J->pu : b->J->pp);
+    const Csr& A = which == 0 ? *b->J->uu : (which == 1 ? *b->J->pu : *b->J->pp);
     auto cp = [&](void* dst, const void* src, size_t bytes) {
       if (dst && bytes) CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream()));
     };
@@ -227,7 +242,7 @@ int cf_block_apply(cf_block b, const double* x, double* y) {
 int cf_block_spmv(cf_block b, int which, const double* x, double* y) {
   return guard([&] {
     CHECK_ARG(b && x && y && which >= 0 && which <= 2, "cf_block_spmv: bad argument");
-    const Csr& A = which == 0 ? b->J->uu : (which == 1 ? b->J->pu : b->J->pp);
+    const Csr& A = which == 0 ? *b->J->uu : (which == 1 ? *b->J->pu : *b->J->pp);
     InArg<double> xi(x, A.cols);
     OutArg<double> yo(y, A.rows);
     csr_spmv_add(A, xi.dev, yo.dev, nullptr);
@@ -235,8 +250,423 @@ int cf_block_spmv(cf_block b, int which, const double* x, double* y) {
   });
 }
 
+int cf_tune_spmv(cf_block b, int which, int threads_per_row, int unroll, const double* x, double* y) {
+  return guard([&] {
+    CHECK_ARG(b && x && y && which >= 0 && which <= 2, "cf_tune_spmv: bad argument");
+    const Csr& A = which == 0 ? *b->J->uu : (which == 1 ? *b->J->pu : *b->J->pp);
+    InArg<double> xi(x, A.cols);
+    OutArg<double> yo(y, A.rows);
+    if (!csr_spmv_variant(A, threads_per_row, unroll, xi.dev, yo.dev))
+      fail(CF_ERR_INVALID_ARGUMENT, "cf_tune_spmv: unknown variant");
+    yo.finish();
+  });
+}
+
 int cf_block_destroy(cf_block b) {
   return guard([&] { delete b; });
+}
+
+// ------------------------------------------------------------------ CSR handles
+int cf_csr_create(int64_t rows, int64_t cols, const int64_t* rowptr, const int32_t* col, const double* val,
+                  cf_csr* out) {
+  return guard([&] {
+    CHECK_ARG(out && rowptr && rows >= 0 && cols >= 0, "cf_csr_create: bad argument");
+    ensure_device();
+    auto A = std::make_shared<Csr>();
+    A->rows = rows;
+    A->cols = cols;
+    A->ptr.alloc(rows + 1);
+    CF_CUDA(cudaMemcpyAsync(A->ptr.p, rowptr, size_t(rows + 1) * sizeof(i64), cudaMemcpyDefault, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    i64 nnz = 0;
+    CF_CUDA(cudaMemcpy(&nnz, A->ptr.p + rows, sizeof(i64), cudaMemcpyDeviceToHost));
+    A->nnz = nnz;
+    A->col.alloc(nnz);
+    A->val.alloc(nnz);
+    if (nnz) {
+      CHECK_ARG(col && val, "cf_csr_create: null column/value arrays");
+      CF_CUDA(cudaMemcpyAsync(A->col.p, col, size_t(nnz) * sizeof(int), cudaMemcpyDefault, stream()));
+      CF_CUDA(cudaMemcpyAsync(A->val.p, val, size_t(nnz) * sizeof(double), cudaMemcpyDefault, stream()));
+    }
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *out = new cf_csr_s{A};
+  });
+}
+
+int cf_block_csr(cf_block b, int which, cf_csr* out) {
+  return guard([&] {
+    CHECK_ARG(b && out && which >= 0 && which <= 2, "cf_block_csr: bad argument");
+    *out = new cf_csr_s{which == 0 ? b->J->uu : (which == 1 ? b->J->pu : b->J->pp)};
+  });
+}
+
+int cf_csr_info(cf_csr A, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  return guard([&] {
+    CHECK_ARG(A, "cf_csr_info: null handle");
+    if (rows) *rows = A->A->rows;
+    if (cols) *cols = A->A->cols;
+    if (nnz) *nnz = A->A->nnz;
+  });
+}
+
+int cf_csr_spmv(cf_csr A, const double* x, double* y) {
+  return guard([&] {
+    CHECK_ARG(A && x && y, "cf_csr_spmv: null argument");
+    InArg<double> xi(x, A->A->cols);
+    OutArg<double> yo(y, A->A->rows);
+    csr_spmv_add(*A->A, xi.dev, yo.dev, nullptr);
+    yo.finish();
+  });
+}
+
+int cf_csr_destroy(cf_csr A) {
+  return guard([&] { delete A; });
+}
+
+// ------------------------------------------------------------------ AMG
+int cf_amg_build(cf_csr A, const int32_t* node_of_dof, const double* B, int m, const cf_amg_options* opts,
+                 cf_amg* out) {
+  return guard([&] {
+    CHECK_ARG(A && opts && out, "cf_amg_build: null argument");
+    CHECK_ARG(A->A->rows == A->A->cols, "build_amg: matrix must be square");
+    const i64 n = A->A->rows;
+    DevBuf<int> nod;
+    DevBuf<double> Bd;
+    const int* nodp;
+    const double* Bp;
+    InArg<int> ni(node_of_dof, node_of_dof ? n : 0);
+    InArg<double> bi(B, B ? n * m : 0);
+    if (node_of_dof && B) {
+      nodp = ni.dev;
+      Bp = bi.dev;
+    } else {
+      CHECK_ARG(!node_of_dof && !B, "cf_amg_build: node_of_dof and B must be given together");
+      m = 1;
+      std::vector<int> h(n);
+      for (i64 i = 0; i < n; ++i) h[i] = int(i);
+      std::vector<double> one(n, 1.0);
+      nod.alloc(n);
+      Bd.alloc(n);
+      if (n) {
+        CF_CUDA(cudaMemcpyAsync(nod.p, h.data(), size_t(n) * sizeof(int), cudaMemcpyHostToDevice, stream()));
+        CF_CUDA(cudaMemcpyAsync(Bd.p, one.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream()));
+        CF_CUDA(cudaStreamSynchronize(stream()));
+      }
+      nodp = nod.p;
+      Bp = Bd.p;
+    }
+    auto h = build_amg(A->A, nodp, Bp, m, *opts);
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *out = new cf_amg_s{std::move(h)};
+  });
+}
+
+int cf_amg_vcycle(cf_amg h, const double* r, double* x) {
+  return guard([&] {
+    CHECK_ARG(h && r && x, "cf_amg_vcycle: null argument");
+    InArg<double> ri(r, h->h->n);
+    OutArg<double> xo(x, h->h->n);
+    h->h->vcycle(ri.dev, xo.dev);
+    xo.finish();
+  });
+}
+
+int cf_amg_info(cf_amg h, int* n_levels, int64_t* coarse_dim) {
+  return guard([&] {
+    CHECK_ARG(h, "cf_amg_info: null handle");
+    if (n_levels) *n_levels = int(h->h->levels.size()) + 1;
+    if (coarse_dim) *coarse_dim = h->h->coarse.n;
+  });
+}
+
+int cf_amg_level_info(cf_amg h, int level, int64_t* info8, double* lambda, double* jacobi_weight) {
+  return guard([&] {
+    CHECK_ARG(h && level >= 0 && level < int(h->h->levels.size()), "cf_amg_level_info: bad level");
+    const AmgLevel& L = *h->h->levels[level];
+    if (info8) {
+      info8[0] = L.A->rows;
+      info8[1] = L.A->nnz;
+      info8[2] = L.P->nnz;
+      info8[3] = L.P->cols;
+      info8[4] = L.n_nodes;
+      info8[5] = L.n_aggregates;
+      info8[6] = L.strong_edges;
+      info8[7] = L.lfmis_rounds;
+    }
+    if (lambda) *lambda = L.lambda;
+    if (jacobi_weight) *jacobi_weight = L.jacobi_weight;
+  });
+}
+
+int cf_amg_level_aggregates(cf_amg h, int level, int32_t* agg) {
+  return guard([&] {
+    CHECK_ARG(h && agg && level >= 0 && level < int(h->h->levels.size()), "cf_amg_level_aggregates: bad level");
+    const AmgLevel& L = *h->h->levels[level];
+    CF_CUDA(cudaMemcpyAsync(agg, L.agg_of_node.p, size_t(L.n_nodes) * sizeof(int), cudaMemcpyDefault, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int cf_amg_level_export(cf_amg h, int level, int which, int64_t* rowptr, int32_t* col, double* val) {
+  return guard([&] {
+    CHECK_ARG(h && level >= 0 && level < int(h->h->levels.size()) && (which == 0 || which == 1),
+              "cf_amg_level_export: bad argument");
+    const AmgLevel& L = *h->h->levels[level];
+    const Csr& M = which == 0 ? *L.A : *L.P;
+    if (rowptr) CF_CUDA(cudaMemcpyAsync(rowptr, M.ptr.p, size_t(M.rows + 1) * sizeof(i64), cudaMemcpyDefault, stream()));
+    if (col && M.nnz) CF_CUDA(cudaMemcpyAsync(col, M.col.p, size_t(M.nnz) * sizeof(int), cudaMemcpyDefault, stream()));
+    if (val && M.nnz) CF_CUDA(cudaMemcpyAsync(val, M.val.p, size_t(M.nnz) * sizeof(double), cudaMemcpyDefault, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int cf_amg_destroy(cf_amg h) {
+  return guard([&] { delete h; });
+}
+
+// ------------------------------------------------------------------ block preconditioner
+int cf_prec_build(cf_block J, int kind, const cf_amg_options* opts, cf_problem p, cf_constraints c, cf_prec* out) {
+  return guard([&] {
+    CHECK_ARG(J && opts && out, "cf_prec_build: null argument");
+    CHECK_ARG(kind >= 0 && kind <= 2, "unknown preconditioner kind");
+    std::unique_ptr<BlockPrec> pr;
+    if (p && c && kind == 1) {
+      const GridDesc& g = p->p->g;
+      const i64 nu = g.n_u(), V = g.V;
+      const int m = g.d == 2 ? 3 : 6;
+      DevBuf<double> Bu(nu * m), Bp(V);
+      DevBuf<int> un(nu), pn(V);
+      rigid_body_modes(*p->p, *c->c, Bu.p);
+      std::vector<int> hu(nu), hp(V);
+      std::vector<double> hb(V);
+      std::vector<std::uint8_t> fl(g.n_total());
+      CF_CUDA(cudaMemcpyAsync(fl.data(), c->c->flag.p, size_t(g.n_total()), cudaMemcpyDeviceToHost, stream()));
+      CF_CUDA(cudaStreamSynchronize(stream()));
+      for (i64 i = 0; i < nu; ++i) hu[i] = int(i / g.d);
+      for (i64 v = 0; v < V; ++v) {
+        hp[v] = int(v);
+        hb[v] = fl[nu + v] ? 0.0 : 1.0;
+      }
+      CF_CUDA(cudaMemcpyAsync(un.p, hu.data(), size_t(nu) * sizeof(int), cudaMemcpyHostToDevice, stream()));
+      CF_CUDA(cudaMemcpyAsync(pn.p, hp.data(), size_t(V) * sizeof(int), cudaMemcpyHostToDevice, stream()));
+      CF_CUDA(cudaMemcpyAsync(Bp.p, hb.data(), size_t(V) * sizeof(double), cudaMemcpyHostToDevice, stream()));
+      NullspaceDev ns{un.p, Bu.p, m, pn.p, Bp.p};
+      pr = build_block_prec(*J->J, kind, *opts, &ns);
+    } else {
+      pr = build_block_prec(*J->J, kind, *opts, nullptr);
+    }
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *out = new cf_prec_s{std::move(pr)};
+  });
+}
+
+int cf_prec_apply(cf_prec P, const double* r, double* z) {
+  return guard([&] {
+    CHECK_ARG(P && r && z, "cf_prec_apply: null argument");
+    const i64 n = P->p->nu + P->p->np;
+    InArg<double> ri(r, n);
+    OutArg<double> zo(z, n);
+    P->p->apply(ri.dev, zo.dev);
+    zo.finish();
+  });
+}
+
+int cf_prec_destroy(cf_prec P) {
+  return guard([&] { delete P; });
+}
+
+int cf_rigid_body_modes(cf_problem p, cf_constraints c, double* B) {
+  return guard([&] {
+    CHECK_ARG(p && c && B, "cf_rigid_body_modes: null argument");
+    const GridDesc& g = p->p->g;
+    OutArg<double> bo(B, g.n_u() * (g.d == 2 ? 3 : 6));
+    rigid_body_modes(*p->p, *c->c, bo.dev);
+    bo.finish();
+  });
+}
+
+// ------------------------------------------------------------------ GMRES
+int cf_gmres(cf_block J, cf_csr A, cf_prec P, cf_amg M, const double* rhs, const cf_gmres_options* opts, double* x,
+             cf_gmres_result* result, double* history, int history_cap) {
+  return guard([&] {
+    CHECK_ARG((J != nullptr) != (A != nullptr), "cf_gmres: give exactly one operator (block or csr)");
+    CHECK_ARG(!(P && M), "cf_gmres: give at most one preconditioner");
+    CHECK_ARG(rhs && opts && x && result, "cf_gmres: null argument");
+    const i64 n = J ? J->J->nu + J->J->np : A->A->rows;
+    InArg<double> bi(rhs, n);
+    OutArg<double> xo(x, n);
+    DevOp op;
+    if (J) {
+      const BlockSystem* Jp = J->J.get();
+      op = [Jp](const double* in, double* out) { block_apply(*Jp, in, out); };
+    } else {
+      const Csr* Ap = A->A.get();
+      op = [Ap](const double* in, double* out) { csr_spmv_add(*Ap, in, out, nullptr); };
+    }
+    DevOp pop;
+    const DevOp* pp = nullptr;
+    if (P) {
+      const BlockPrec* Pp = P->p.get();
+      pop = [Pp](const double* in, double* out) { Pp->apply(in, out); };
+      pp = &pop;
+    } else if (M) {
+      const Amg* Mp = M->h.get();
+      pop = [Mp](const double* in, double* out) { Mp->vcycle(in, out); };
+      pp = &pop;
+    }
+    GmresResult r = gmres(op, pp, bi.dev, n, *opts, xo.dev);
+    xo.finish();
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    result->iterations = r.iterations;
+    result->converged = r.converged;
+    result->breakdown = r.breakdown;
+    result->residual = r.residual;
+    if (history)
+      for (int i = 0; i < int(r.history.size()) && i < history_cap; ++i) history[i] = r.history[i];
+  });
+}
+
+// ------------------------------------------------------------------ Newton
+int cf_slit_band_edge(cf_problem p, const cf_material* mat, double* edge) {
+  return guard([&] {
+    CHECK_ARG(p && mat && edge, "cf_slit_band_edge: null argument");
+    *edge = slit_band_edge(*p->p, *mat);
+  });
+}
+
+int cf_resolve_regularization(cf_problem p, const cf_material* mat, double band_edge, cf_regularization* out) {
+  return guard([&] {
+    CHECK_ARG(p && mat && out, "cf_resolve_regularization: null argument");
+    *out = resolve_regularization(*p->p, *mat, band_edge);
+  });
+}
+
+int cf_initial_crack(cf_problem p, const cf_material* mat, double band_half, double* phi, double* band_edge) {
+  return guard([&] {
+    CHECK_ARG(p && mat && phi, "cf_initial_crack: null argument");
+    auto h = initial_crack(*p->p, *mat, band_half, band_edge);
+    CF_CUDA(cudaMemcpyAsync(phi, h.data(), h.size() * sizeof(double), cudaMemcpyDefault, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int cf_state_create(cf_problem p, const double* solution, const double* phi_old, const double* phi_prev2, int step,
+                    cf_state* out) {
+  return guard([&] {
+    CHECK_ARG(p && out, "cf_state_create: null argument");
+    const GridDesc& g = p->p->g;
+    auto* s = new cf_state_s;
+    s->prob = p;
+    s->st.solution.alloc(g.n_total());
+    s->st.phi_old.alloc(g.V);
+    s->st.phi_prev2.alloc(g.V);
+    auto put = [&](DevBuf<double>& d, const double* src) {
+      if (src)
+        CF_CUDA(cudaMemcpyAsync(d.p, src, size_t(d.n) * sizeof(double), cudaMemcpyDefault, stream()));
+      else
+        d.zero();
+    };
+    put(s->st.solution, solution);
+    put(s->st.phi_old, phi_old);
+    put(s->st.phi_prev2, phi_prev2);
+    s->st.step = step;
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *out = s;
+  });
+}
+
+int cf_make_initial_state(cf_problem p, const cf_material* mat, double seed_band, cf_state* out) {
+  return guard([&] {
+    CHECK_ARG(p && mat && out, "cf_make_initial_state: null argument");
+    const GridDesc& g = p->p->g;
+    auto phi = initial_crack(*p->p, *mat, seed_band, nullptr);
+    std::vector<double> sol(g.n_total(), 0.0);
+    std::copy(phi.begin(), phi.end(), sol.begin() + g.n_u());
+    cf_state s = nullptr;
+    int rc = cf_state_create(p, sol.data(), phi.data(), phi.data(), 0, &s);
+    if (rc != CF_OK) fail(rc, g_err);
+    *out = s;
+  });
+}
+
+int cf_state_get(cf_state s, double* solution, double* phi_old, double* phi_prev2, int* step) {
+  return guard([&] {
+    CHECK_ARG(s, "cf_state_get: null state");
+    auto get = [&](double* dst, const DevBuf<double>& d) {
+      if (dst) CF_CUDA(cudaMemcpyAsync(dst, d.p, size_t(d.n) * sizeof(double), cudaMemcpyDefault, stream()));
+    };
+    get(solution, s->st.solution);
+    get(phi_old, s->st.phi_old);
+    get(phi_prev2, s->st.phi_prev2);
+    if (step) *step = s->st.step;
+    CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int cf_state_destroy(cf_state s) {
+  return guard([&] { delete s; });
+}
+
+static void fill_report(const NewtonReport& r, cf_newton_iteration* its, int max_its, int* n_its, int* converged,
+                        double* feasibility) {
+  if (n_its) *n_its = int(r.its.size());
+  if (its)
+    for (int i = 0; i < int(r.its.size()) && i < max_its; ++i)
+      its[i] = cf_newton_iteration{r.its[i].residual_norm, r.its[i].active_size, r.its[i].set_changes,
+                                   r.its[i].gmres_iterations};
+  if (converged) *converged = r.converged;
+  if (feasibility) *feasibility = r.feasibility;
+}
+
+int cf_newton_active_set_step(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                              const cf_solver_options* opts, cf_newton_iteration* its, int max_its, int* n_its,
+                              int* converged, double* feasibility, cf_phase_times* times) {
+  return guard([&] {
+    CHECK_ARG(p && s && mat && reg && opts, "cf_newton_active_set_step: null argument");
+    cudaEvent_t a, b;
+    CF_CUDA(cudaEventCreate(&a));
+    CF_CUDA(cudaEventCreate(&b));
+    CF_CUDA(cudaEventRecord(a, stream()));
+    NewtonReport r = newton_active_set_step(*p->p, s->st, *mat, *reg, *opts);
+    CF_CUDA(cudaEventRecord(b, stream()));
+    CF_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    fill_report(r, its, max_its, n_its, converged, feasibility);
+    if (times)
+      *times = cf_phase_times{r.times.residual, r.times.active_set, r.times.jacobian, r.times.amg_setup,
+                              r.times.gmres, double(ms)};
+  });
+}
+
+int cf_solve_loading_sequence(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                              const cf_solver_options* opts, int n_steps, cf_newton_iteration* its, int max_its,
+                              int* n_its, int* converged, double* feasibility, int* steps_done) {
+  return guard([&] {
+    CHECK_ARG(p && s && mat && reg && opts, "cf_solve_loading_sequence: null argument");
+    if (n_steps < 1) fail(CF_ERR_INVALID_ARGUMENT, "solve_loading_sequence: n_steps must be >= 1");
+    const GridDesc& g = p->p->g;
+    int done = 0, off = 0;
+    for (int n = 1; n <= n_steps; ++n) {
+      State& st = s->st;
+      CF_CUDA(cudaMemcpyAsync(st.phi_prev2.p, st.phi_old.p, size_t(g.V) * sizeof(double), cudaMemcpyDeviceToDevice,
+                              stream()));
+      CF_CUDA(cudaMemcpyAsync(st.phi_old.p, st.solution.p + g.n_u(), size_t(g.V) * sizeof(double),
+                              cudaMemcpyDeviceToDevice, stream()));
+      st.step = n;
+      NewtonReport r = newton_active_set_step(*p->p, st, *mat, *reg, *opts);
+      int k = 0;
+      fill_report(r, its ? its + off : nullptr, std::max(0, max_its - off), &k, converged ? converged + (n - 1) : nullptr,
+                  feasibility ? feasibility + (n - 1) : nullptr);
+      if (n_its) n_its[n - 1] = k;
+      off += std::min(k, std::max(0, max_its - off));
+      ++done;
+      if (!r.converged) break;
+    }
+    if (steps_done) *steps_done = done;
+  });
 }
 
 }  // extern "C"

@@ -127,6 +127,7 @@ struct OutArg {
   }
 };
 
-inline unsigned grid_for(i64 n, int block) { return unsigned((n + block - 1) / block); }
+// at least one block, so empty inputs launch a no-op grid instead of an invalid configuration
+inline unsigned grid_for(i64 n, int block) { return unsigned(n > 0 ? (n + block - 1) / block : 1); }
 
 }  // namespace cfb

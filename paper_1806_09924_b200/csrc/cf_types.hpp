@@ -56,7 +56,7 @@ struct Csr {
 
 struct BlockSystem {
   i64 nu = 0, np = 0;
-  Csr uu, pu, pp;
+  std::shared_ptr<Csr> uu = std::make_shared<Csr>(), pu = std::make_shared<Csr>(), pp = std::make_shared<Csr>();
   int d = 2;
 };
 
@@ -73,6 +73,7 @@ std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& c,
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add);  // y = A x (+ add)
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);
+bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double* y);
 
 inline double mat_mu(const cf_material& m) { return m.E / (2.0 * (1.0 + m.nu)); }              // model.hpp:26
 inline double mat_lambda(const cf_material& m) {                                                  // model.hpp:27

@@ -1,0 +1,136 @@
+// Vector / Krylov primitives (vec.cu), SpGEMM & CSR utilities (spgemm.cu), AMG (amg.cu),
+// GMRES (gmres.cu) and the Newton driver (newton.cu).
+#pragma once
+
+#include <functional>
+#include <memory>
+#include <vector>
+
+#include "cf_types.hpp"
+
+namespace cfb {
+
+struct Scratch {
+  DevBuf<double> part, scal;
+};
+
+// ---- vec.cu
+double* scalar_buf(int count);
+void vfill(double* x, double a, i64 n);
+void vcopy(double* dst, const double* src, i64 n);
+void vaxpy(double a, const double* x, double* y, i64 n);                 // y += a x
+void vaxpby(double a, const double* x, double b, double* y, i64 n);      // y = a x + b y
+void vsub(const double* a, const double* b, double* out, i64 n);         // out = a - b
+void vscale(double* x, double a, i64 n);
+void vdiv_dev(const double* x, const double* s_dev, double* y, i64 n);   // y = x / *s
+void vdiag_mul(const double* d, const double* x, double* y, double a, i64 n);  // y = a (d .* x)
+void vdot_dev(const double* x, const double* y, i64 n, double* out, bool do_sqrt);
+double vdot(const double* x, const double* y, i64 n);
+double vnorm(const double* x, i64 n);
+void multidot(const double* V, i64 ld, int k, const double* w, i64 n, double* out_dev);   // out_i = V_i . w
+void multi_axpy(double* w, const double* V, i64 ld, int k, const double* coef_dev, i64 n, double alpha);
+
+// ---- spgemm.cu: CSR utilities (deterministic)
+std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale = nullptr);  // diag(s) A B
+std::unique_ptr<Csr> transpose(const Csr& A);
+// P = T - w * DAT (union pattern), entries with |v| <= 1e-300 removed
+std::unique_ptr<Csr> csr_axpy_prune(const Csr& T, double w, const Csr& DAT);
+void csr_prune(Csr& A);  // in place (Eigen prune(1.0, 1e-300))
+void csr_diagonal(const Csr& A, double* diag);  // A(i,i) or 0
+std::unique_ptr<Csr> csr_copy(const Csr& A);
+
+// ---- dense LU (amg.cu): column-major n x n, unblocked partial pivoting (PartialPivLU)
+struct DenseLu {
+  i64 n = 0;
+  DevBuf<double> lu;
+  DevBuf<int> piv;
+  double min_abs_pivot = 0.0;
+  void factor_from_csr(const Csr& A);
+  void solve(const double* b, double* x) const;  // device vectors
+};
+
+// ---- amg.cu (linsolve.hpp:62-94)
+struct AmgLevel {
+  std::shared_ptr<Csr> A;
+  std::unique_ptr<Csr> P, R;
+  DevBuf<double> inv_diag;
+  double jacobi_weight = 2.0 / 3.0;
+  double lambda = 0.0;
+  i64 n_nodes = 0, n_aggregates = 0, strong_edges = 0;
+  int lfmis_rounds = 0;
+  DevBuf<int> agg_of_node;  // kept for parity checks
+  mutable DevBuf<double> tmp_r, tmp_b, tmp_x;  // V-cycle work vectors of this level
+};
+
+struct Amg {
+  std::vector<std::unique_ptr<AmgLevel>> levels;
+  DenseLu coarse;
+  cf_amg_options opts{};
+  i64 n = 0;
+  std::shared_ptr<Csr> coarse_A;
+  mutable DevBuf<double> cb, cx;  // coarsest rhs / solution
+  void vcycle(const double* r, double* x) const;  // x = V(r), zero initial guess
+};
+
+std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A, const int* node_of_dof, const double* B, int m,
+                               const cf_amg_options& opts);
+
+// ---- block preconditioner (linsolve.cpp:352-415)
+struct BlockPrec {
+  int kind = 1;  // 0 exact, 1 amg, 2 diagonal
+  i64 nu = 0, np = 0;
+  std::shared_ptr<Amg> amg_u, amg_p;
+  std::shared_ptr<DenseLu> lu_u, lu_p;
+  DevBuf<double> inv_u, inv_p;
+  void apply(const double* r, double* z) const;
+};
+
+struct NullspaceDev {  // NullspaceInfo on the device (linsolve.hpp:108-113)
+  const int* u_node = nullptr;
+  const double* u_modes = nullptr;  // n_u x m column-major
+  int m_u = 0;
+  const int* p_node = nullptr;
+  const double* p_modes = nullptr;  // n_phi x 1
+};
+
+std::unique_ptr<BlockPrec> build_block_prec(const BlockSystem& J, int kind, const cf_amg_options& o,
+                                            const NullspaceDev* ns);
+
+// ---- gmres.cu (linsolve.cpp:21-115)
+using DevOp = std::function<void(const double* in, double* out)>;
+struct GmresResult {
+  int iterations = 0;
+  bool converged = false, breakdown = false;
+  double residual = 0.0;
+  std::vector<double> history;
+};
+GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
+                  double* x);
+
+// ---- newton.cu (solver.cpp:24-204)
+struct State {  // FractureState (model.hpp:50-55), device resident
+  DevBuf<double> solution, phi_old, phi_prev2;
+  int step = 0;
+};
+struct NewtonIter {
+  double residual_norm;
+  int active_size, set_changes, gmres_iterations;
+};
+struct PhaseTimes {  // per-phase device time of the last Newton step (ms)
+  double residual = 0, active_set = 0, jacobian = 0, amg_setup = 0, gmres = 0, other = 0;
+};
+struct NewtonReport {
+  std::vector<NewtonIter> its;
+  bool converged = false;
+  double feasibility = 0.0;
+  PhaseTimes times;
+};
+NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& mat, const cf_regularization& reg,
+                                    const cf_solver_options& opts);
+void rigid_body_modes(const Problem& P, const Constraints& c, double* B);  // n_u x m, column-major
+// host helpers (model.cpp:28-64, 324-349)
+double slit_band_edge(const Problem& P, const cf_material& mat);
+cf_regularization resolve_regularization(const Problem& P, const cf_material& mat, double band_edge);
+std::vector<double> initial_crack(const Problem& P, const cf_material& mat, double band_half, double* band_edge);
+
+}  // namespace cfb

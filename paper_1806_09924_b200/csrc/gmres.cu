@@ -1,0 +1,145 @@
+// K6: restarted right-preconditioned GMRES (linsolve.cpp:21-115) with a device-resident Krylov
+// basis.  The orthogonalisation is the reference's modified Gram-Schmidt: for each basis
+// vector a deterministic device dot (fixed-order block tree) and an axpy whose coefficient stays
+// in device memory, so the only host round trip per iteration is the (j+2)-entry Hessenberg
+// column needed by the Givens logic, which runs on the host exactly as in the reference.
+#include <cmath>
+
+#include "cf_vec.hpp"
+
+namespace cfb {
+
+namespace {
+
+// w = w - (*h) * v   (linsolve.cpp:58, compiled without FMA contraction)
+__global__ void k_axpy_dev(i64 n, const double* __restrict__ h, const double* __restrict__ v, double* __restrict__ w) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) w[i] -= (*h) * v[i];
+}
+
+}  // namespace
+
+GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
+                  double* x) {
+  if (!(o.rtol > 0.0 && o.rtol < 1.0)) fail(CF_ERR_INVALID_ARGUMENT, "gmres: rtol must be in (0,1)");
+  if (o.restart < 1 || o.restart > 255) fail(CF_ERR_UNSUPPORTED, "gmres: restart must be in [1, 255]");
+  GmresResult res;
+  vfill(x, 0.0, n);
+  DevBuf<double> sc(2);
+  vdot_dev(rhs, rhs, n, sc.p, true);
+  double bnorm = 0.0;
+  CF_CUDA(cudaMemcpyAsync(&bnorm, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  if (bnorm == 0.0) {
+    res.converged = true;
+    return res;
+  }
+  const int mmax = std::max(1, std::min(o.restart, o.max_iter));
+  DevBuf<double> r(n), z(n), z2(n), V(n * (mmax + 1)), hd(mmax + 2), yd(mmax + 1);
+  vcopy(r.p, rhs, n);
+  std::vector<double> H, cs, sn, g, hcol(mmax + 2), y;
+  auto apply_op = [&](const double* in, double* out) {
+    if (prec) {
+      (*prec)(in, z2.p);
+      op(z2.p, out);
+    } else {
+      op(in, out);
+    }
+  };
+  while (res.iterations < o.max_iter) {
+    vdot_dev(r.p, r.p, n, sc.p, true);
+    double beta = 0.0;
+    CF_CUDA(cudaMemcpyAsync(&beta, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    if (beta <= o.rtol * bnorm) {
+      res.converged = true;
+      res.residual = beta / bnorm;
+      return res;
+    }
+    const int m = std::min(o.restart, o.max_iter - res.iterations);
+    H.assign(size_t(m + 1) * m, 0.0);
+    auto Hij = [&](int i, int j) -> double& { return H[size_t(i) * m + j]; };
+    cs.assign(m, 0.0);
+    sn.assign(m, 0.0);
+    g.assign(m + 1, 0.0);
+    g[0] = beta;
+    vdiv_dev(r.p, sc.p, V.p, n);  // V(:,0) = r / beta
+    int j = 0;
+    bool inner_done = false;
+    for (; j < m && !inner_done; ++j) {
+      double* w = V.p + i64(j + 1) * n;
+      apply_op(V.p + i64(j) * n, w);
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+        vdot_dev(w, V.p + i64(i) * n, n, hd.p + i, false);
+        k_axpy_dev<<<grid_for(n, 256), 256, 0, stream()>>>(n, hd.p + i, V.p + i64(i) * n, w);
+        CF_LAUNCHED();
+      }
+      vdot_dev(w, w, n, hd.p + j + 1, true);
+      CF_CUDA(cudaMemcpyAsync(hcol.data(), hd.p, size_t(j + 2) * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+      CF_CUDA(cudaStreamSynchronize(stream()));
+      for (int i = 0; i <= j + 1; ++i) Hij(i, j) = hcol[i];
+      const bool happy = Hij(j + 1, j) <= 1e-14 * bnorm;
+      if (!happy) vdiv_dev(w, hd.p + j + 1, w, n);
+      for (int i = 0; i < j; ++i) {  // previous Givens rotations
+        const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
+        Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
+        Hij(i, j) = t;
+      }
+      const double denom = std::hypot(Hij(j, j), Hij(j + 1, j));
+      if (denom == 0.0) {
+        res.breakdown = true;
+        inner_done = true;
+        --j;
+        break;
+      }
+      cs[j] = Hij(j, j) / denom;
+      sn[j] = Hij(j + 1, j) / denom;
+      Hij(j, j) = denom;
+      Hij(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++res.iterations;
+      const double rel = std::abs(g[j + 1]) / bnorm;
+      res.history.push_back(rel);
+      if (rel <= o.rtol || happy || res.iterations >= o.max_iter) inner_done = true;
+    }
+    const int k = j;
+    if (k > 0) {
+      y.assign(k, 0.0);
+      for (int i = k - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int l = i + 1; l < k; ++l) s -= Hij(i, l) * y[l];
+        if (Hij(i, i) == 0.0) {
+          res.breakdown = true;
+          y[i] = 0.0;
+        } else {
+          y[i] = s / Hij(i, i);
+        }
+      }
+      CF_CUDA(cudaMemcpyAsync(yd.p, y.data(), size_t(k) * sizeof(double), cudaMemcpyHostToDevice, stream()));
+      vfill(z.p, 0.0, n);
+      multi_axpy(z.p, V.p, n, k, yd.p, n, 1.0);  // z = V(:, :k) y
+      if (prec) {
+        (*prec)(z.p, z2.p);
+        vaxpy(1.0, z2.p, x, n);
+      } else {
+        vaxpy(1.0, z.p, x, n);
+      }
+    }
+    op(x, z.p);
+    vsub(rhs, z.p, r.p, n);  // r = b - op(x)
+    vdot_dev(r.p, r.p, n, sc.p, true);
+    double rn = 0.0;
+    CF_CUDA(cudaMemcpyAsync(&rn, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    res.residual = rn / bnorm;
+    if (res.residual <= o.rtol) {
+      res.converged = true;
+      return res;
+    }
+    if (res.breakdown) return res;
+  }
+  return res;
+}
+
+}  // namespace cfb

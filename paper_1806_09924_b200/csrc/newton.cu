@@ -1,0 +1,410 @@
+// K9/K10 and the Newton / primal-dual active-set driver (solver.cpp:24-204).
+//
+// Control flow stays on the host exactly as in newton_active_set_step; every per-dof
+// operation is a device kernel: the active-set test, the membership history (a 64-bit shift
+// register per phi dof: all tracked histories have the same length, so the reference's
+// zero-backfill is implicit), cycle detection (popcount of toggles in the last W bits), the
+// change count, the constraint arrays, distribute, the rigid-body near-nullspace.  Only
+// scalars (norms, counts) cross to the host per iteration.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "cf_vec.hpp"
+
+namespace cfb {
+
+namespace {
+
+template <class T>
+T read_dev(const T* p) {
+  T h{};
+  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  return h;
+}
+
+// phi_tilde = phi_old (step <= 2) else clip(2 phi_old - phi_prev2, [0, 1]) (model.cpp:60-64)
+__global__ void k_extrapolate(i64 V, int step, const double* __restrict__ po, const double* __restrict__ pp,
+                              double* __restrict__ pt) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  if (step <= 2) {
+    pt[v] = po[v];
+  } else {
+    const double t = 2.0 * po[v] - pp[v];
+    pt[v] = fmin(fmax(t, 0.0), 1.0);
+  }
+}
+
+// active-set test + history push (solver.cpp:81-96).  tracked dofs push their bit.
+__global__ void k_active1(i64 V, i64 nu, double c, double tol, const double* __restrict__ x,
+                          const double* __restrict__ po, const double* __restrict__ R,
+                          const std::uint8_t* __restrict__ base_flag, const std::uint8_t* __restrict__ fixed,
+                          std::uint8_t* __restrict__ active, std::uint8_t* __restrict__ tracked,
+                          unsigned long long* __restrict__ hist, int* __restrict__ any_tracked) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const i64 dof = nu + v;
+  bool a = fixed[v] != 0;
+  if (!base_flag[dof]) {  // candidates: phi dofs not constrained by the base set
+    const double lambda = -R[dof];
+    if (c * (x[dof] - po[v]) + lambda > tol) a = true;
+  }
+  active[v] = a ? 1 : 0;
+  bool tr = tracked[v] != 0 || a;
+  if (tr) {
+    tracked[v] = 1;
+    hist[v] = (hist[v] << 1) | (a ? 1ull : 0ull);
+    *any_tracked = 1;
+  }
+}
+
+// cycle detection on the last min(len, W) entries (solver.cpp:10-22, 97-100), set changes and |A|
+__global__ void k_active2(i64 V, int len, int window, int toggles, const std::uint8_t* __restrict__ tracked,
+                          const unsigned long long* __restrict__ hist, std::uint8_t* __restrict__ fixed,
+                          std::uint8_t* __restrict__ active, const std::uint8_t* __restrict__ prev,
+                          int* __restrict__ counts) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  if (tracked[v]) {
+    const int w = len < window ? len : window;
+    int ch = 0;
+    if (w > 1) {
+      const unsigned long long t = hist[v] ^ (hist[v] >> 1);
+      const unsigned long long mask = (w - 1 >= 64) ? ~0ull : ((1ull << (w - 1)) - 1ull);
+      ch = __popcll(t & mask);
+    }
+    if (ch >= toggles) {
+      fixed[v] = 1;
+      active[v] = 1;
+    }
+  }
+  const int a = active[v];
+  if (a) atomicAdd(&counts[0], 1);
+  if (a != prev[v]) atomicAdd(&counts[1], 1);
+}
+
+// full constraint set: base + active phi = phi_old (solver.cpp:109-111, fem.cpp:258-263)
+__global__ void k_full_constraints(i64 nt, i64 nu, const std::uint8_t* __restrict__ bflag,
+                                   const double* __restrict__ binh, const std::uint8_t* __restrict__ active,
+                                   const double* __restrict__ po, std::uint8_t* __restrict__ flag,
+                                   double* __restrict__ inh) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  std::uint8_t f = bflag[i];
+  double g = binh[i];
+  if (i >= nu && !f && active[i - nu]) {
+    f = 1;
+    g = po[i - nu];
+  }
+  flag[i] = f;
+  inh[i] = g;
+}
+
+// distribute + "moved" flag (solver.cpp:114-116)
+__global__ void k_distribute_moved(i64 nt, const std::uint8_t* __restrict__ flag, const double* __restrict__ inh,
+                                   double* __restrict__ x, int* __restrict__ moved) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nt || !flag[i]) return;
+  const double old = x[i];
+  x[i] = inh[i];
+  if (fabs(x[i] - old) > 0.0) *moved = 1;
+}
+
+__global__ void k_zero_active(i64 V, i64 nu, const std::uint8_t* __restrict__ active, double* __restrict__ R) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v < V && active[v]) R[nu + v] = 0.0;
+}
+
+__global__ void k_neg(i64 n, const double* __restrict__ a, double* __restrict__ b) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = -a[i];
+}
+
+// rigid body modes (linsolve.cpp:320-343), zero rows on constrained u dofs
+__global__ void k_rigid(GridDesc g, const std::uint8_t* __restrict__ flag, double* __restrict__ B) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= g.V) return;
+  const int d = g.d;
+  const i64 n = g.n_u();
+  const i64 ix = v % g.nn, iy = (v / g.nn) % g.nn, iz = (d == 3) ? v / (g.nn * g.nn) : 0;
+  const double x0 = -g.K + double(ix * (i64(1) << (16 - g.r))) * g.unit;
+  const double x1 = -g.K + double(iy * (i64(1) << (16 - g.r))) * g.unit;
+  const double x2 = (d == 3) ? -g.K + double(iz * (i64(1) << (16 - g.r))) * g.unit : 0.0;
+  const int m = (d == 2) ? 3 : 6;
+  double row[3][6];
+  for (int a = 0; a < 3; ++a)
+    for (int c = 0; c < 6; ++c) row[a][c] = 0.0;
+  for (int a = 0; a < d; ++a) row[a][a] = 1.0;
+  if (d == 2) {
+    row[0][2] = -x1;
+    row[1][2] = x0;
+  } else {
+    row[1][3] = -x2;
+    row[2][3] = x1;
+    row[0][4] = x2;
+    row[2][4] = -x0;
+    row[0][5] = -x1;
+    row[1][5] = x0;
+  }
+  for (int a = 0; a < d; ++a) {
+    const i64 dof = v * d + a;
+    const bool con = flag[dof] != 0;
+    for (int c = 0; c < m; ++c) B[i64(c) * n + dof] = con ? 0.0 : row[a][c];
+  }
+}
+
+__global__ void k_phi_modes(i64 V, i64 nu, const std::uint8_t* __restrict__ flag, double* __restrict__ B,
+                            int* __restrict__ pnode, int* __restrict__ unode, int d) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  B[v] = flag[nu + v] ? 0.0 : 1.0;
+  pnode[v] = int(v);
+  for (int a = 0; a < d; ++a) unode[v * d + a] = int(v);
+}
+
+__global__ void k_feas(i64 V, i64 nu, const double* __restrict__ x, const double* __restrict__ po, double* out) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const double d = x[nu + v] - po[v];
+  // max via the ordered-int trick for doubles (handles negatives)
+  long long bits = __double_as_longlong(d);
+  bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
+  atomicMax(reinterpret_cast<long long*>(out), bits);
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  double* acc;
+  Timer(double* slot) : acc(slot) {
+    CF_CUDA(cudaEventCreate(&a));
+    CF_CUDA(cudaEventCreate(&b));
+    CF_CUDA(cudaEventRecord(a, stream()));
+  }
+  ~Timer() {
+    cudaEventRecord(b, stream());
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    *acc += ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+}  // namespace
+
+void rigid_body_modes(const Problem& P, const Constraints& c, double* B) {
+  k_rigid<<<grid_for(P.g.V, 256), 256, 0, stream()>>>(P.g, c.flag.p, B);
+  CF_LAUNCHED();
+}
+
+double slit_band_edge(const Problem& P, const cf_material& mat) {  // model.cpp:28-50 (uniform cells)
+  const GridDesc& g = P.g;
+  auto coord = [&](i64 i) { return -g.K + double(i * (i64(1) << (16 - g.r))) * g.unit; };
+  const i64 nz = (g.d == 3) ? g.nc : 1;
+  for (i64 cz = 0; cz < nz; ++cz) {
+    if (g.d == 3 && !(coord(cz) <= 0.0 && coord(cz + 1) >= 0.0)) continue;
+    for (i64 cy = 0; cy < g.nc; ++cy)
+      for (i64 cx = 0; cx < g.nc; ++cx) {
+        const double lo0 = coord(cx), hi0 = coord(cx + 1), lo1 = coord(cy), hi1 = coord(cy + 1);
+        bool meets;
+        if (g.d == 2) {
+          meets = lo1 <= 0.0 && hi1 >= 0.0 && lo0 <= mat.l0 && hi0 >= -mat.l0;
+        } else {
+          const double dx = std::max({lo0, 0.0, -hi0});
+          const double dy = std::max({lo1, 0.0, -hi1});
+          meets = std::hypot(dx, dy) <= mat.l0;
+        }
+        if (meets) return g.h;  // all active cells share the edge h on a uniform mesh
+      }
+  }
+  fail(CF_ERR_NUMERICAL, "slit_band_edge: no active cell meets the slit");
+}
+
+cf_regularization resolve_regularization(const Problem& P, const cf_material& mat, double band_edge) {
+  cf_regularization reg;  // model.cpp:52-58
+  const double diam = band_edge * std::sqrt(double(P.g.d));
+  reg.eps = (mat.eps_mode == 0) ? mat.c_eps * diam : mat.eps_fixed;
+  reg.kappa = mat.kappa_factor * P.g.h;
+  return reg;
+}
+
+std::vector<double> initial_crack(const Problem& P, const cf_material& mat, double band_half, double* band_edge) {
+  const GridDesc& g = P.g;  // model.cpp:324-349
+  const double be = band_half > 0.0 ? band_half : slit_band_edge(P, mat);
+  std::vector<double> phi(g.V, 1.0);
+  const double tol = 1e-9 * be;
+  auto coord = [&](i64 i) { return -g.K + double(i * (i64(1) << (16 - g.r))) * g.unit; };
+  i64 n_zero = 0, n_plane = 0;
+  for (i64 v = 0; v < g.V; ++v) {
+    const i64 ix = v % g.nn, iy = (v / g.nn) % g.nn, iz = (g.d == 3) ? v / (g.nn * g.nn) : 0;
+    const double x0 = coord(ix), x1 = coord(iy), x2 = (g.d == 3) ? coord(iz) : 0.0;
+    bool in;
+    if (g.d == 2)
+      in = std::abs(x0) <= mat.l0 + tol && std::abs(x1) <= be + tol;
+    else
+      in = std::hypot(x0, x1) <= mat.l0 + tol && std::abs(x2) <= be + tol;
+    if (in) {
+      phi[v] = 0.0;
+      ++n_zero;
+      if (std::abs(g.d == 2 ? x1 : x2) <= tol) ++n_plane;
+    }
+  }
+  if (n_zero == 0 || n_plane == 0)
+    fail(CF_ERR_NUMERICAL, "initial_crack: slit is not resolved by the mesh (no vertex layer inside the band)");
+  if (band_edge) *band_edge = be;
+  return phi;
+}
+
+NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& mat, const cf_regularization& reg,
+                                    const cf_solver_options& opts) {
+  const GridDesc& g = P.g;
+  const i64 nu = g.n_u(), V = g.V, nt = g.n_total();
+  if (opts.cycle_window < 1 || opts.cycle_window > 64)
+    fail(CF_ERR_UNSUPPORTED, "newton_active_set_step: cycle_window must be in [1, 64]");
+  NewtonReport report;
+  PhaseTimes& T = report.times;
+  auto base = build_constraints(P, true, 0, nullptr, nullptr);  // solver.cpp:55
+  double* x = st.solution.p;
+  distribute(*base, x, false);
+  DevBuf<double> pt(V);
+  k_extrapolate<<<grid_for(V, 256), 256, 0, stream()>>>(V, st.step, st.phi_old.p, st.phi_prev2.p, pt.p);
+  CF_LAUNCHED();
+  const double c = opts.active_set_c_scale * mat.G_c / reg.eps;
+  DevBuf<std::uint8_t> fixed(V), active(V), prev(V), tracked(V);
+  DevBuf<unsigned long long> hist(V);
+  fixed.zero();
+  prev.zero();
+  tracked.zero();
+  hist.zero();
+  DevBuf<int> flags(4);
+  DevBuf<double> R(nt), rhs(nt), delta(nt);
+  int hist_len = 0;
+  double res0 = -1.0;
+  std::unique_ptr<BlockPrec> prec;
+  Constraints full;
+  full.prob = &P;
+  full.flag.alloc(nt);
+  full.inhom.alloc(nt);
+  DevBuf<double> Bu(nu * (g.d == 2 ? 3 : 6)), Bp(V);
+  DevBuf<int> unode(nu), pnode(V);
+  for (int it = 1; it <= opts.newton_max_iter; ++it) {
+    {
+      Timer t(&T.residual);
+      assemble_residual(P, *base, mat, reg, x, pt.p, R.p);
+    }
+    int changes = 0, asize = 0;
+    {
+      Timer t(&T.active_set);
+      flags.zero();
+      k_active1<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, c, 1e-14 * c, x, st.phi_old.p, R.p, base->flag.p,
+                                                        fixed.p, active.p, tracked.p, hist.p, flags.p + 2);
+      CF_LAUNCHED();
+      if (read_dev(flags.p + 2)) ++hist_len;
+      k_active2<<<grid_for(V, 256), 256, 0, stream()>>>(V, hist_len, opts.cycle_window, opts.cycle_toggles,
+                                                        tracked.p, hist.p, fixed.p, active.p, prev.p, flags.p);
+      CF_LAUNCHED();
+      int hc[2];
+      CF_CUDA(cudaMemcpyAsync(hc, flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream()));
+      CF_CUDA(cudaStreamSynchronize(stream()));
+      asize = hc[0];
+      changes = hc[1];
+      k_full_constraints<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, nu, base->flag.p, base->inhom.p, active.p,
+                                                                  st.phi_old.p, full.flag.p, full.inhom.p);
+      CF_LAUNCHED();
+      CF_CUDA(cudaMemsetAsync(flags.p + 3, 0, sizeof(int), stream()));
+      k_distribute_moved<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, full.flag.p, full.inhom.p, x, flags.p + 3);
+      CF_LAUNCHED();
+    }
+    const bool moved = read_dev(flags.p + 3) != 0;
+    {
+      Timer t(&T.residual);
+      if (moved) {
+        assemble_residual(P, full, mat, reg, x, pt.p, R.p);
+      } else {
+        k_zero_active<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, active.p, R.p);
+        CF_LAUNCHED();
+      }
+    }
+    const double res = vnorm(R.p, nt);
+    if (res0 < 0.0) res0 = res;
+    NewtonIter rec{res, asize, changes, 0};
+    const bool small = res <= std::max(opts.newton_tol * res0, opts.newton_abs_floor);
+    if (changes == 0 && small) {
+      report.its.push_back(rec);
+      if (opts.log)
+        std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=0\n", st.step, it, res, asize,
+                    changes);
+      report.converged = true;
+      break;
+    }
+    std::unique_ptr<BlockSystem> J;
+    {
+      Timer t(&T.jacobian);
+      J = assemble_jacobian(P, full, mat, reg, x, pt.p);
+    }
+    if (!prec || !opts.freeze_preconditioner) {
+      Timer t(&T.amg_setup);
+      NullspaceDev ns;
+      rigid_body_modes(P, full, Bu.p);
+      k_phi_modes<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, full.flag.p, Bp.p, pnode.p, unode.p, g.d);
+      CF_LAUNCHED();
+      ns.u_node = unode.p;
+      ns.u_modes = Bu.p;
+      ns.m_u = g.d == 2 ? 3 : 6;
+      ns.p_node = pnode.p;
+      ns.p_modes = Bp.p;
+      prec.reset();
+      prec = build_block_prec(*J, opts.prec_kind, opts.amg, &ns);
+    }
+    GmresResult lin;
+    {
+      Timer t(&T.gmres);
+      k_neg<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, R.p, rhs.p);
+      CF_LAUNCHED();
+      const BlockSystem& Jr = *J;
+      DevOp op = [&Jr](const double* in, double* out) { block_apply(Jr, in, out); };
+      const BlockPrec& Pr = *prec;
+      DevOp pop = [&Pr](const double* in, double* out) { Pr.apply(in, out); };
+      lin = gmres(op, &pop, rhs.p, nt, opts.gmres, delta.p);
+    }
+    if (!lin.converged && !lin.breakdown) fail(CF_ERR_NUMERICAL, "newton_active_set_step: GMRES stagnated at max_iter");
+    rec.gmres_iterations = lin.iterations;
+    report.its.push_back(rec);
+    if (opts.log)
+      std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=%d\n", st.step, it, res, asize, changes,
+                  lin.iterations);
+    distribute(full, delta.p, true);
+    vaxpy(1.0, delta.p, x, nt);
+    if (opts.damping) {
+      double scale = 1.0;
+      for (int half = 0; half < 4; ++half) {
+        assemble_residual(P, full, mat, reg, x, pt.p, R.p);
+        if (vnorm(R.p, nt) <= 10.0 * res) break;
+        scale *= 0.5;
+        vaxpy(-scale, delta.p, x, nt);
+      }
+    }
+    CF_CUDA(cudaMemcpyAsync(prev.p, active.p, size_t(V), cudaMemcpyDeviceToDevice, stream()));
+  }
+  DevBuf<double> mx(1);
+  {
+    const long long lowest = 0x8000000000000000LL;  // below every mapped double
+    CF_CUDA(cudaMemcpyAsync(mx.p, &lowest, sizeof(lowest), cudaMemcpyHostToDevice, stream()));
+  }
+  k_feas<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, x, st.phi_old.p, mx.p);
+  CF_LAUNCHED();
+  long long bits = 0;
+  CF_CUDA(cudaMemcpyAsync(&bits, mx.p, sizeof(bits), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
+  double viol;
+  std::memcpy(&viol, &bits, sizeof(viol));
+  report.feasibility = std::max(0.0, viol);  // solver.cpp:183-186 starts from viol = 0
+  return report;
+}
+
+}  // namespace cfb

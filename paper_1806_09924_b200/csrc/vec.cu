@@ -1,0 +1,214 @@
+// K6: Krylov vector kernels with deterministic (fixed-order, atomic-free) reductions.
+// dot/norm: a fixed grid of block partials + one ordered final block; multidot: several basis
+// vectors per pass over w (CGS2 orthogonalisation); multi_axpy: w += alpha * V coef.
+#include "cf_types.hpp"
+#include "cf_vec.hpp"
+
+namespace cfb {
+
+namespace {
+
+constexpr int RB = 256;  // reduction block size
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(RB) k_dot_partial(const double* __restrict__ x, const double* __restrict__ y, i64 n,
+                                                    double* __restrict__ part) {
+  __shared__ double sh[RB];
+  double s = 0.0;
+  for (i64 i = i64(blockIdx.x) * RB + threadIdx.x; i < n; i += i64(gridDim.x) * RB) s += x[i] * y[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// out[r] = sum_b part[r*nb + b] (fixed tree), optional sqrt
+__global__ void __launch_bounds__(RB) k_final(const double* __restrict__ part, int nb, double* out, int do_sqrt) {
+  __shared__ double sh[RB];
+  const double* p = part + i64(blockIdx.x) * nb;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nb; b += RB) s += p[b];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = do_sqrt ? sqrt(s) : s;
+}
+
+template <int KC>
+__global__ void __launch_bounds__(RB) k_multidot_partial(const double* __restrict__ V, i64 ld, int k,
+                                                         const double* __restrict__ w, i64 n, double* __restrict__ part,
+                                                         int nb) {
+  __shared__ double sh[RB];
+  const int c0 = blockIdx.y * KC;
+  const int kc = min(KC, k - c0);
+  double s[KC];
+#pragma unroll
+  for (int c = 0; c < KC; ++c) s[c] = 0.0;
+  for (i64 i = i64(blockIdx.x) * RB + threadIdx.x; i < n; i += i64(gridDim.x) * RB) {
+    const double wi = w[i];
+#pragma unroll
+    for (int c = 0; c < KC; ++c)
+      if (c < kc) s[c] += V[(c0 + c) * ld + i] * wi;
+  }
+  for (int c = 0; c < kc; ++c) {
+    const double r = block_sum(s[c], sh);
+    if (threadIdx.x == 0) part[i64(c0 + c) * nb + blockIdx.x] = r;
+  }
+}
+
+__global__ void k_multi_axpy(double* __restrict__ w, const double* __restrict__ V, i64 ld, int k,
+                             const double* __restrict__ coef, i64 n, double alpha) {
+  __shared__ double cs[256];
+  for (int c = threadIdx.x; c < k && c < 256; c += blockDim.x) cs[c] = coef[c];
+  __syncthreads();
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int c = 0; c < k; ++c) s += cs[c] * V[c * ld + i];
+  w[i] += alpha * s;
+}
+
+__global__ void k_fill(double* x, double a, i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = a;
+}
+__global__ void k_axpby(double a, const double* __restrict__ x, double b, double* __restrict__ y, i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = a * x[i] + b * y[i];
+}
+__global__ void k_axpy(double a, const double* __restrict__ x, double* __restrict__ y, i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a * x[i];
+}
+__global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o, i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = a[i] - b[i];
+}
+__global__ void k_div_scalar(const double* __restrict__ x, const double* __restrict__ s, double* __restrict__ y, i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[i] / *s;
+}
+__global__ void k_scale(double* x, double a, i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] *= a;
+}
+__global__ void k_diag_mul(const double* __restrict__ d, const double* __restrict__ x, double* __restrict__ y,
+                           double a, i64 n) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = a * (d[i] * x[i]);
+}
+
+int nblocks_for(i64 n) { return int(std::min<i64>(1024, std::max<i64>(1, (n + 4 * RB - 1) / (4 * RB)))); }
+
+Scratch& scr() {
+  static Scratch s;
+  return s;
+}
+
+double* partial_buf(i64 count) {
+  Scratch& s = scr();
+  if (s.part.n < count) s.part.alloc(std::max<i64>(count, 1 << 17));
+  return s.part.p;
+}
+
+}  // namespace
+
+double* scalar_buf(int count) {
+  Scratch& s = scr();
+  if (s.scal.n < count) s.scal.alloc(std::max(count, 1024));
+  return s.scal.p;
+}
+
+void vfill(double* x, double a, i64 n) {
+  if (n <= 0) return;
+  k_fill<<<grid_for(n, 256), 256, 0, stream()>>>(x, a, n);
+  CF_LAUNCHED();
+}
+void vcopy(double* dst, const double* src, i64 n) {
+  if (n > 0) CF_CUDA(cudaMemcpyAsync(dst, src, size_t(n) * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+}
+void vaxpy(double a, const double* x, double* y, i64 n) {
+  if (n <= 0) return;
+  k_axpy<<<grid_for(n, 256), 256, 0, stream()>>>(a, x, y, n);
+  CF_LAUNCHED();
+}
+void vaxpby(double a, const double* x, double b, double* y, i64 n) {
+  if (n <= 0) return;
+  k_axpby<<<grid_for(n, 256), 256, 0, stream()>>>(a, x, b, y, n);
+  CF_LAUNCHED();
+}
+void vsub(const double* a, const double* b, double* out, i64 n) {
+  if (n <= 0) return;
+  k_sub<<<grid_for(n, 256), 256, 0, stream()>>>(a, b, out, n);
+  CF_LAUNCHED();
+}
+void vscale(double* x, double a, i64 n) {
+  if (n <= 0) return;
+  k_scale<<<grid_for(n, 256), 256, 0, stream()>>>(x, a, n);
+  CF_LAUNCHED();
+}
+void vdiv_dev(const double* x, const double* s_dev, double* y, i64 n) {
+  if (n <= 0) return;
+  k_div_scalar<<<grid_for(n, 256), 256, 0, stream()>>>(x, s_dev, y, n);
+  CF_LAUNCHED();
+}
+void vdiag_mul(const double* d, const double* x, double* y, double a, i64 n) {
+  if (n <= 0) return;
+  k_diag_mul<<<grid_for(n, 256), 256, 0, stream()>>>(d, x, y, a, n);
+  CF_LAUNCHED();
+}
+
+void vdot_dev(const double* x, const double* y, i64 n, double* out, bool do_sqrt) {
+  const int nb = nblocks_for(n);
+  double* part = partial_buf(nb);
+  k_dot_partial<<<nb, RB, 0, stream()>>>(x, y, n, part);
+  CF_LAUNCHED();
+  k_final<<<1, RB, 0, stream()>>>(part, nb, out, do_sqrt ? 1 : 0);
+  CF_LAUNCHED();
+}
+
+double vdot(const double* x, const double* y, i64 n) {
+  double* s = scalar_buf(1);
+  vdot_dev(x, y, n, s, false);
+  double h = 0.0;
+  CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  return h;
+}
+
+double vnorm(const double* x, i64 n) {
+  double* s = scalar_buf(1);
+  vdot_dev(x, x, n, s, true);
+  double h = 0.0;
+  CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  return h;
+}
+
+void multidot(const double* V, i64 ld, int k, const double* w, i64 n, double* out_dev) {
+  if (k <= 0) return;
+  constexpr int KC = 16;
+  const int nb = nblocks_for(n);
+  double* part = partial_buf(i64(nb) * k);
+  dim3 grid(nb, (k + KC - 1) / KC);
+  k_multidot_partial<KC><<<grid, RB, 0, stream()>>>(V, ld, k, w, n, part, nb);
+  CF_LAUNCHED();
+  k_final<<<k, RB, 0, stream()>>>(part, nb, out_dev, 0);
+  CF_LAUNCHED();
+}
+
+void multi_axpy(double* w, const double* V, i64 ld, int k, const double* coef_dev, i64 n, double alpha) {
+  if (k <= 0 || n <= 0) return;
+  if (k > 256) fail(CF_ERR_UNSUPPORTED, "multi_axpy: more than 256 basis vectors");
+  k_multi_axpy<<<grid_for(n, 256), 256, 0, stream()>>>(w, V, ld, k, coef_dev, n, alpha);
+  CF_LAUNCHED();
+}
+
+}  // namespace cfb

@@ -1,0 +1,249 @@
+"""GPU parity of the solver stack: AMG setup (K7) and V-cycle (K8), GMRES (K6), the block
+preconditioner and the Newton / active-set step (K9, K10) against the CPU oracle.
+
+The device path and the oracle share one documented reduction order, so the
+comparisons are bit-for-bit: aggregates, every level operator, lambda_max, V-cycle outputs,
+GMRES iterates, Newton transcripts and solutions.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cf():
+    import paper_1806_09924_b200 as cf
+    return cf
+
+
+def _chain(n):
+    return sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1], format="csr")
+
+
+def _assert_amg_equal(h, ho, exact=True):
+    assert h.n_levels() == ho.n_levels and h.coarse_dim() == ho.coarse_dim
+    for lev in range(ho.n_levels - 1):
+        a, b = h.level_info(lev), ho.level(lev)
+        for k in ("rows", "nnz_A", "nnz_P", "coarse", "n_nodes", "n_aggregates"):
+            assert a[k] == b[k], (lev, k, a[k], b[k])
+        assert np.array_equal(h.aggregates(lev), ho.aggregates(lev)), f"aggregates differ on level {lev}"
+        if exact:
+            assert a["lam"] == b["lam"], (lev, a["lam"], b["lam"])
+            for w in (0, 1):
+                m1, m2 = h.level_matrix(lev, w), ho.level_matrix(lev, w)
+                assert np.array_equal(m1.ptr, m2.ptr) and np.array_equal(m1.col, m2.col)
+                assert np.array_equal(m1.val, m2.val), (lev, w, np.abs(m1.val - m2.val).max())
+
+
+def test_amg_scalar_chain_and_diag(cf, orc):  # linsolve_test.cpp:265-300
+    rng = np.random.default_rng(6)
+    dg = rng.uniform(1, 5, 30)
+    h = cf.build_amg(cf.CsrMatrix.from_scipy(sp.diags(dg, format="csr")))
+    assert h.n_levels() == 1
+    b = rng.uniform(1, 5, 30)
+    assert np.allclose(h.v_cycle(b), b / dg, rtol=1e-12)
+    A = _chain(200)
+    h = cf.build_amg(cf.CsrMatrix.from_scipy(A))
+    ho = orc.Amg(orc.Csr.from_scipy(A))
+    _assert_amg_equal(h, ho)
+    r = rng.uniform(-1, 1, 200)
+    assert np.array_equal(h.v_cycle(r), ho.vcycle(r))
+    s = rng.uniform(-1, 1, 200)
+    lhs, rhs = h.v_cycle(1.7 * r - 0.3 * s), 1.7 * h.v_cycle(r) - 0.3 * h.v_cycle(s)
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * max(1.0, np.linalg.norm(rhs))
+    A64 = cf.CsrMatrix.from_scipy(_chain(64))
+    res = cf.gmres(A64, rng.uniform(-1, 1, 64), prec=cf.build_amg(A64))
+    assert res["converged"] and res["iterations"] <= 25
+
+
+def _q1_laplacian(nv):
+    pts = [0.5 * (-1 / math.sqrt(3) + 1), 0.5 * (1 / math.sqrt(3) + 1)]
+    local = np.zeros((4, 4))
+    for qy in pts:
+        for qx in pts:
+            g = np.array([[-(1 - qy), -(1 - qx)], [(1 - qy), -qx], [-qy, (1 - qx)], [qy, qx]])
+            local += 0.25 * g @ g.T
+    rows, cols, vals = [], [], []
+    bnd = np.zeros(nv * nv, bool)
+    for v in range(nv * nv):
+        x, y = v % nv, v // nv
+        bnd[v] = x in (0, nv - 1) or y in (0, nv - 1)
+    for cy in range(nv - 1):
+        for cx in range(nv - 1):
+            verts = [cx + (k & 1) + nv * (cy + (k >> 1 & 1)) for k in range(4)]
+            for a in range(4):
+                for b in range(4):
+                    if not (bnd[verts[a]] or bnd[verts[b]]):
+                        rows.append(verts[a]); cols.append(verts[b]); vals.append(local[a, b])
+    for v in np.nonzero(bnd)[0]:
+        rows.append(v); cols.append(v); vals.append(1.0)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(nv * nv, nv * nv))
+
+
+def test_amg_laplacian_parity_and_mesh_independence(cf, orc):  # linsolve_test.cpp:302-308
+    rng = np.random.default_rng(16)
+    its = []
+    for nv in (65, 129):
+        A = _q1_laplacian(nv)
+        h = cf.build_amg(cf.CsrMatrix.from_scipy(A))
+        ho = orc.Amg(orc.Csr.from_scipy(A))
+        _assert_amg_equal(h, ho)
+        b = rng.uniform(-1, 1, A.shape[0])
+        res = cf.gmres(cf.CsrMatrix.from_scipy(A), b, prec=h)
+        reso = orc.gmres(b, csr=orc.CsrHandle(orc.Csr.from_scipy(A)), amg=ho)
+        assert res["converged"] and res["iterations"] == reso["iterations"]
+        assert np.array_equal(res["x"], reso["x"])
+        its.append(res["iterations"])
+    assert its[1] <= 1.5 * its[0] and its[0] <= 1.5 * its[1]
+
+
+def test_gmres_identity_spd_and_validation(cf, orc):  # linsolve_test.cpp:194-217
+    I = cf.CsrMatrix.from_scipy(sp.identity(20, format="csr"))
+    b = np.linspace(1.0, 20.0, 20)
+    res = cf.gmres(I, b)
+    assert res["converged"] and res["iterations"] == 1 and np.abs(res["x"] - b).max() <= 1e-12
+    rng = np.random.default_rng(4)
+    for _ in range(5):
+        B = rng.uniform(-1, 1, (50, 50))
+        A = B @ B.T + 50 * np.eye(50)
+        b = rng.uniform(-1, 1, 50)
+        res = cf.gmres(cf.CsrMatrix.from_scipy(sp.csr_matrix(A)), b)
+        reso = orc.gmres(b, csr=orc.CsrHandle(orc.Csr.from_scipy(sp.csr_matrix(A))))
+        assert res["converged"] and np.array_equal(res["x"], reso["x"])
+        assert np.array_equal(res["residual_history"], reso["history"])
+        ex = np.linalg.solve(A, b)
+        assert np.linalg.norm(res["x"] - ex) / np.linalg.norm(ex) <= 1e-7
+    with pytest.raises(ValueError, match="rtol"):
+        cf.gmres(I, b, opts=cf.GmresOptions(rtol=0.0))
+
+
+def _small_jacobian(cf, orc, rng, n0=3, r=0, d=2):
+    P, O = cf.Problem(d, 1.0, n0, r), orc.Problem(d, 1.0, n0, r)
+    x = np.zeros(P.n_total)
+    x[:P.n_u] = 1e-2 * rng.uniform(-1, 1, P.n_u)
+    x[P.n_u:] = rng.uniform(0, 1, P.n_vertices)
+    pt = rng.uniform(0, 1, P.n_vertices)
+    cs, ocs = cf.build_constraints(P), O.constraints()
+    cs.distribute_homogeneous(x)
+    J = cf.assemble_jacobian(P, cs, cf.Material(), cf.Regularization(0.25, 1e-10), x, pt)
+    Jo = O.jacobian(ocs, orc.material(), orc.Regularization(0.25, 1e-10), x, pt)
+    rhs = rng.uniform(-1, 1, P.n_total)
+    cs.distribute_homogeneous(rhs)
+    return P, O, cs, ocs, J, Jo, rhs
+
+
+def test_exact_block_prec_gmres(cf, orc):  # linsolve_test.cpp:219-237
+    rng = np.random.default_rng(8)
+    for _ in range(10):
+        P, O, cs, ocs, J, Jo, rhs = _small_jacobian(cf, orc, rng)
+        pre = cf.BlockPreconditioner.build(J, "exact")
+        res = cf.gmres(J, rhs, prec=pre)
+        reso = orc.gmres(rhs, block=Jo, prec=orc.Prec(Jo, 0))
+        assert res["converged"] and res["iterations"] <= 5
+        assert res["iterations"] == reso["iterations"]
+        assert np.linalg.norm(res["x"] - reso["x"]) <= 1e-12 * np.linalg.norm(reso["x"])
+
+
+@pytest.mark.parametrize("d,n0,r", [(2, 4, 2), (3, 2, 1)])
+def test_block_prec_amg_with_nullspace_bit_exact(cf, orc, d, n0, r):
+    rng = np.random.default_rng(12 + d)
+    P, O, cs, ocs, J, Jo, rhs = _small_jacobian(cf, orc, rng, n0=n0, r=r, d=d)
+    for kind in (1, 2):
+        pre = cf.BlockPreconditioner.build(J, kind, prob=P, constraints=cs)
+        preo = orc.Prec(Jo, kind, prob=O, cs=ocs)
+        assert np.array_equal(pre.apply(rhs), preo.apply(rhs)), kind
+    res = cf.gmres(J, rhs, prec=cf.BlockPreconditioner.build(J, 1, prob=P, constraints=cs))
+    reso = orc.gmres(rhs, block=Jo, prec=orc.Prec(Jo, 1, prob=O, cs=ocs))
+    assert res["iterations"] == reso["iterations"] and np.array_equal(res["x"], reso["x"])
+
+
+def test_rigid_body_modes(cf, orc):  # linsolve_test.cpp:310-334
+    for d in (2, 3):
+        P, O = cf.Problem(d, 1.0, 3, 0), orc.Problem(d, 1.0, 3, 0)
+        act = {P.n_u + 1: 0.5}
+        B = cf.rigid_body_modes(P, cf.build_constraints(P, True, act))
+        Bo = O.rigid_body_modes(O.constraints(True, list(act), list(act.values())))
+        assert np.array_equal(B, Bo)
+
+
+def _sneddon_pair(cf, orc, d=2, K=5.0, n0=10, r=1, fixed=False):
+    P, O = cf.Problem(d, K, n0, r), orc.Problem(d, K, n0, r)
+    kw = dict(eps_mode=1, eps_fixed=2 * P.h, kappa_factor=1e-12 / P.h) if fixed else {}
+    mat, omat = cf.Material(**kw), orc.material(**kw)
+    reg = cf.resolve_regularization(P, mat, cf.slit_band_edge(P, mat))
+    oreg = O.resolve_regularization(omat, O.slit_band_edge(omat))
+    assert (reg.eps, reg.kappa) == (oreg.eps, oreg.kappa)
+    phi, _ = cf.initial_crack(P, mat)
+    ophi, _ = O.initial_crack(omat)
+    assert np.array_equal(phi, ophi)
+    return P, O, mat, omat, reg, oreg, phi
+
+
+def _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi, steps=1, **optkw):
+    st = cf.make_initial_state(P, mat)
+    reps = cf.solve_loading_sequence(st, mat, P, reg, cf.SolverOptions(**optkw), steps)
+    sol = np.zeros(O.n_total)
+    sol[O.n_u:] = phi
+    po, pp = phi.copy(), phi.copy()
+    oreps = []
+    okw = dict(optkw)
+    if "gmres" in okw:
+        g = okw["gmres"]
+        okw["gmres"] = orc.gmres_options(rtol=g.rtol, max_iter=g.max_iter, restart=g.restart)
+    for n in range(1, steps + 1):
+        oreps.append(O.newton_step(omat, oreg, orc.solver_options(**okw), sol, po, pp, n))
+    return reps, st.get()["solution"], oreps, sol
+
+
+def _same_transcript(rep, orep):
+    its = np.array([[r["residual_norm"], r["active_size"], r["set_changes"], r["gmres_iterations"]]
+                    for r in rep["iterations"]])
+    assert its.shape == orep["iterations"].shape, (its, orep["iterations"])
+    assert np.array_equal(its, orep["iterations"]), (its, orep["iterations"])
+    assert rep["converged"] == orep["converged"]
+    assert rep["feasibility_violation"] == orep["feasibility"]
+
+
+@pytest.mark.parametrize("r", [1, 2])
+def test_newton_step_bit_exact_small(cf, orc, r):  # solver_test.cpp:112-150, 178-195
+    P, O, mat, omat, reg, oreg, phi = _sneddon_pair(cf, orc, r=r)
+    reps, x, oreps, xo = _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi)
+    _same_transcript(reps[0], oreps[0])
+    assert np.array_equal(x, xo)
+    assert reps[0]["converged"] and reps[0]["feasibility_violation"] <= 1e-10
+    assert reps[0]["iterations"][-1]["set_changes"] == 0
+
+
+def test_newton_determinism_and_exact_prec(cf, orc):  # solver_test.cpp:178-210
+    P, O, mat, omat, reg, oreg, phi = _sneddon_pair(cf, orc, r=1)
+    runs = [_run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi)[:2] for _ in range(2)]
+    assert np.array_equal(runs[0][1], runs[1][1])
+    xe = _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi, prec_kind=0)[1]
+    assert np.abs(runs[0][1] - xe).max() <= 1e-6 * np.abs(xe).max()
+
+
+def test_loading_sequence_three_steps(cf, orc):  # solver.cpp:190-204, config 2 semantics (step 3 extrapolates)
+    P, O, mat, omat, reg, oreg, phi = _sneddon_pair(cf, orc, r=1, fixed=True)
+    reps, x, oreps, xo = _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi, steps=3,
+                                   gmres=cf.GmresOptions(rtol=1e-10, restart=50))
+    assert len(reps) == 3
+    for a, b in zip(reps, oreps):
+        _same_transcript(a, b)
+    assert np.array_equal(x, xo)
+    with pytest.raises(ValueError, match="n_steps"):
+        cf.solve_loading_sequence(cf.make_initial_state(P, mat), mat, P, reg, cf.SolverOptions(), 0)
+
+
+def test_config0_newton_parity(cf, orc):
+    """BASELINE config 0 (2d 256^2, eps = 2h, kappa = 1e-12): full Newton step vs the oracle."""
+    P, O, mat, omat, reg, oreg, phi = _sneddon_pair(cf, orc, d=2, K=10.0, n0=8, r=5, fixed=True)
+    assert P.n_total == 198147
+    reps, x, oreps, xo = _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi)
+    _same_transcript(reps[0], oreps[0])
+    assert np.array_equal(x, xo)
+    st = -1.575 + 0.05 * np.arange(64)
+    assert np.array_equal(O.cod(x, st), O.cod(xo, st))
