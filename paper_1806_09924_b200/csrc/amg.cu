@@ -23,6 +23,8 @@
 
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <unordered_map>
 
 #include "cf_vec.hpp"
@@ -56,9 +58,63 @@ int bits_for(i64 n) {
   return b;
 }
 
+// CF_TIMING=1: per-phase device times of build_amg on stderr (profiling aid, off by default)
+struct PhaseClock {
+  bool on;
+  cudaEvent_t last;
+  int lev = 0;
+  PhaseClock() : on(std::getenv("CF_TIMING") != nullptr) {
+    if (on) {
+      cudaEventCreate(&last);
+      cudaEventRecord(last, stream());
+    }
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, stream());
+    cudaEventSynchronize(e);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, last, e);
+    std::fprintf(stderr, "[amg L%d] %-12s %8.3f ms\n", lev, what, ms);
+    cudaEventDestroy(last);
+    last = e;
+  }
+  ~PhaseClock() {
+    if (on) cudaEventDestroy(last);
+  }
+};
+
+i64 pow2_at_least(i64 n) {
+  i64 c = 16;
+  while (c < n) c <<= 1;
+  return c;
+}
+
 __global__ void k_iota(i64 n, int* out) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] = int(i);
+}
+
+__global__ void k_flag_list(i64 n, const int* __restrict__ flag, int* __restrict__ list, int* __restrict__ count);
+__global__ void k_sort_list(int n, int* list);
+
+struct OvfList {
+  DevBuf<int> list;
+  int n = 0;
+};
+
+// ascending list of flagged nodes
+OvfList make_ovf_list(i64 n, const int* flag) {
+  OvfList o;
+  DevBuf<int> c(1);
+  c.zero();
+  o.list.alloc(std::max<i64>(n, 1));
+  k_flag_list<<<grid_for(n, 256), 256, 0, stream()>>>(n, flag, o.list.p, c.p);
+  CF_LAUNCHED();
+  o.n = read_dev(c.p);  // list order is irrelevant: every listed node is processed independently
+  return o;
 }
 
 __global__ void k_count_keys(i64 n, const int* __restrict__ key, i64* __restrict__ cnt) {
@@ -87,7 +143,117 @@ void group_by_key(i64 n, const int* key, i64 nkeys, DevBuf<i64>& ptr, DevBuf<int
 }
 
 // ------------------------------------------------------------------ strength (linsolve.cpp:185-201)
-constexpr int SCAP = 384;  // distinct neighbour nodes per node
+constexpr int SCAP = 96;  // distinct neighbour nodes per node in the register/local tier
+
+// Overflow tier: nodes with more distinct neighbour nodes than SCAP get a private open-addressing
+// table in global memory (capacity = next pow2 >= 2 x their entry count); one thread per node
+// keeps the (row, column) accumulation order, then compacts and heap-sorts its keys.
+__device__ __forceinline__ unsigned hash_u(int k) { return unsigned(k) * 2654435761u; }
+
+__device__ void heap_sort_pairs(int* key, double* val, int n) {
+  auto sift = [&](int start, int end) {
+    int root = start;
+    while (2 * root + 1 <= end) {
+      int child = 2 * root + 1, sw = root;
+      if (key[sw] < key[child]) sw = child;
+      if (child + 1 <= end && key[sw] < key[child + 1]) sw = child + 1;
+      if (sw == root) return;
+      const int tk = key[root]; key[root] = key[sw]; key[sw] = tk;
+      if (val) { const double tv = val[root]; val[root] = val[sw]; val[sw] = tv; }
+      root = sw;
+    }
+  };
+  for (int s = (n - 2) / 2; s >= 0; --s) sift(s, n - 1);
+  for (int e = n - 1; e > 0; --e) {
+    const int tk = key[0]; key[0] = key[e]; key[e] = tk;
+    if (val) { const double tv = val[0]; val[0] = val[e]; val[e] = tv; }
+    sift(0, e - 1);
+  }
+}
+
+__global__ void k_node_entries(i64 nov, const int* __restrict__ list, const i64* __restrict__ nptr,
+                               const int* __restrict__ ndofs, const i64* __restrict__ Ap, i64 cap_max,
+                               i64* __restrict__ cap) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nov) return;
+  const int i = list[t];
+  i64 e = 0;
+  for (i64 k = nptr[i]; k < nptr[i + 1]; ++k) e += Ap[ndofs[k] + 1] - Ap[ndofs[k]];
+  i64 c = 16;
+  while (c < 2 * e && c < cap_max) c <<= 1;
+  cap[t] = c;
+}
+
+__global__ void k_strength_big(i64 nov, const int* __restrict__ list, const i64* __restrict__ off,
+                               const i64* __restrict__ nptr, const int* __restrict__ ndofs, const i64* __restrict__ Ap,
+                               const int* __restrict__ Ac, const double* __restrict__ Av, const int* __restrict__ nod,
+                               int* __restrict__ keys, double* __restrict__ sums, int* __restrict__ len_out) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nov) return;
+  const int i = list[t];
+  int* K = keys + off[t];
+  double* S = sums + off[t];
+  const unsigned mask = unsigned(off[t + 1] - off[t]) - 1u;
+  int len = 0;
+  for (i64 q = nptr[i]; q < nptr[i + 1]; ++q) {
+    const int r = ndofs[q];
+    for (i64 k = Ap[r]; k < Ap[r + 1]; ++k) {
+      const int nj = nod[Ac[k]];
+      const double a2 = Av[k] * Av[k];
+      unsigned s = hash_u(nj) & mask;
+      while (K[s] != -1 && K[s] != nj) s = (s + 1) & mask;
+      if (K[s] == nj) {
+        S[s] += a2;
+      } else {
+        K[s] = nj;
+        S[s] = a2;
+        ++len;
+      }
+    }
+  }
+  int p = 0;
+  for (unsigned s = 0; s <= mask; ++s)
+    if (K[s] != -1) {
+      K[p] = K[s];
+      S[p] = S[s];
+      ++p;
+    }
+  heap_sort_pairs(K, S, len);
+  len_out[t] = len;
+}
+
+// strong test on the sorted overflow lists; mode 0 counts, mode 1 writes
+__global__ void k_strength_big_emit(i64 nov, const int* __restrict__ list, const i64* __restrict__ off,
+                                    const int* __restrict__ keys, const double* __restrict__ sums,
+                                    const int* __restrict__ len, const double* __restrict__ dsq, double theta,
+                                    i64* __restrict__ cnt, const i64* __restrict__ sptr, int* __restrict__ sidx,
+                                    int mode) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nov) return;
+  const int i = list[t];
+  const int* K = keys + off[t];
+  const double* S = sums + off[t];
+  const double dii = dsq[i];
+  i64 n = 0;
+  const i64 base = mode ? sptr[i] : 0;
+  for (int s = 0; s < len[t]; ++s) {
+    const int j = K[s];
+    if (j == i) continue;
+    if (sqrt(S[s]) > theta * sqrt(dii * dsq[j])) {
+      if (mode) sidx[base + n] = j;
+      ++n;
+    }
+  }
+  if (!mode) cnt[i] = n;
+}
+
+__global__ void k_flag_list(i64 n, const int* __restrict__ flag, int* __restrict__ list, int* __restrict__ count) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && flag[i]) list[atomicAdd(count, 1)] = int(i);
+}
+__global__ void k_sort_list(int n, int* list) {  // small lists: deterministic order of overflow nodes
+  if (threadIdx.x == 0 && blockIdx.x == 0) heap_sort_pairs(list, nullptr, n);
+}
 
 __global__ void k_strength_diag(i64 nn, const i64* __restrict__ nptr, const int* __restrict__ ndofs,
                                 const i64* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
@@ -112,9 +278,10 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
                            const i64* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
                            const int* __restrict__ nod, const double* __restrict__ dsq, double theta,
                            i64* __restrict__ cnt, const i64* __restrict__ sptr, int* __restrict__ sidx, int mode,
-                           int* __restrict__ err) {
+                           int* __restrict__ ovf) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nn) return;
+  if (mode && ovf[i]) return;  // handled by the overflow tier
   int keys[SCAP];
   double sums[SCAP];
   int len = 0;
@@ -132,7 +299,7 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
         sums[lo] += a2;
       } else {
         if (len == SCAP) {
-          *err = 1;
+          ovf[i] = 1;
           return;
         }
         for (int s = len; s > lo; --s) {
@@ -163,11 +330,144 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
 // ------------------------------------------------------------------ N2 dependency graph
 // N2(i) = S[i] u T[i] u T[S[i]] (T = S^T), as a k-way merge of sorted lists.  mode 0 counts the
 // lower (< i) and upper (> i) members; mode 1 writes the upper members (the dependents).
-constexpr int MCAP = 256;  // merged lists per node
+constexpr int MCAP = 64;  // merged lists per node in the local tier (|S[i]| <= 62)
+
+// overflow tier of N2: a private hash set per node in global memory
+__global__ void k_n2_cap(i64 nov, const int* __restrict__ list, const i64* __restrict__ sp, const int* __restrict__ si,
+                         const i64* __restrict__ tp, i64 cap_max, i64* __restrict__ cap) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nov) return;
+  const int i = list[t];
+  i64 e = (sp[i + 1] - sp[i]) + (tp[i + 1] - tp[i]);
+  for (i64 k = sp[i]; k < sp[i + 1]; ++k) e += tp[si[k] + 1] - tp[si[k]];
+  i64 c = 16;
+  while (c < 2 * e && c < cap_max) c <<= 1;
+  cap[t] = c;
+}
+
+__device__ __forceinline__ void set_insert(int* K, unsigned mask, int v) {
+  unsigned s = hash_u(v) & mask;
+  while (K[s] != -1 && K[s] != v) s = (s + 1) & mask;
+  K[s] = v;
+}
+
+__global__ void k_n2_big(i64 nov, const int* __restrict__ list, const i64* __restrict__ off, const i64* __restrict__ sp,
+                         const int* __restrict__ si, const i64* __restrict__ tp, const int* __restrict__ ti,
+                         int* __restrict__ keys, int* __restrict__ lower, i64* __restrict__ upcnt,
+                         const i64* __restrict__ upptr, int* __restrict__ up, int mode) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= nov) return;
+  const int i = list[t];
+  int* K = keys + off[t];
+  const unsigned mask = unsigned(off[t + 1] - off[t]) - 1u;
+  if (mode == 0) {
+    for (i64 k = sp[i]; k < sp[i + 1]; ++k) set_insert(K, mask, si[k]);
+    for (i64 k = tp[i]; k < tp[i + 1]; ++k) set_insert(K, mask, ti[k]);
+    for (i64 k = sp[i]; k < sp[i + 1]; ++k) {
+      const int j = si[k];
+      for (i64 q = tp[j]; q < tp[j + 1]; ++q) set_insert(K, mask, ti[q]);
+    }
+    int nlow = 0;
+    i64 nup = 0;
+    for (unsigned s = 0; s <= mask; ++s) {
+      if (K[s] < 0) continue;
+      if (K[s] < i) ++nlow;
+      else if (K[s] > i) ++nup;
+    }
+    lower[i] = nlow;
+    upcnt[i] = nup;
+  } else {
+    i64 n = 0;
+    const i64 base = upptr[i];
+    for (unsigned s = 0; s <= mask; ++s)
+      if (K[s] > i) up[base + n++] = K[s];
+  }
+}
+
+// warp per node, shared-memory hash set of N2(i) (set semantics: the insertion order is
+// irrelevant); more than 3/4 x N2CAP members -> overflow tier
+constexpr int N2CAP = 1024, N2WPB = 4;
+__global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restrict__ sp, const int* __restrict__ si,
+                                                    const i64* __restrict__ tp, const int* __restrict__ ti,
+                                                    int* __restrict__ lower, i64* __restrict__ upcnt,
+                                                    const i64* __restrict__ upptr, int* __restrict__ up, int mode,
+                                                    int* __restrict__ ovf) {
+  __shared__ int tab[N2WPB][N2CAP];
+  __shared__ int cnt[N2WPB];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 node = i64(blockIdx.x) * N2WPB + w;
+  if (node >= nn) return;
+  const int i = int(node);
+  if (mode == 1 && ovf[i]) return;
+  int* T = tab[w];
+  for (int s = lane; s < N2CAP; s += 32) T[s] = -1;
+  if (lane == 0) cnt[w] = 0;
+  __syncwarp();
+  const unsigned mask = N2CAP - 1;
+  bool full = false;
+  auto ins = [&](int v) {
+    unsigned s = hash_u(v) & mask;
+    for (int p = 0; p < N2CAP; ++p) {
+      const int cur = T[s];
+      if (cur == v) return;
+      if (cur == -1) {
+        const int old = atomicCAS(&T[s], -1, v);
+        if (old == -1) {
+          atomicAdd(&cnt[w], 1);
+          return;
+        }
+        if (old == v) return;
+      }
+      s = (s + 1) & mask;
+    }
+    full = true;
+  };
+  for (i64 k = sp[i] + lane; k < sp[i + 1]; k += 32) ins(si[k]);
+  for (i64 k = tp[i] + lane; k < tp[i + 1]; k += 32) ins(ti[k]);
+  for (i64 k = sp[i]; k < sp[i + 1]; ++k) {
+    const int j = si[k];
+    for (i64 q = tp[j] + lane; q < tp[j + 1]; q += 32) ins(ti[q]);
+    if (__any_sync(0xffffffffu, full) || cnt[w] > (N2CAP * 3) / 4) {
+      full = true;
+      break;
+    }
+  }
+  __syncwarp();
+  if (__any_sync(0xffffffffu, full) || cnt[w] > (N2CAP * 3) / 4) {
+    if (mode == 0 && lane == 0) ovf[i] = 1;
+    return;
+  }
+  if (mode == 0) {
+    int nl = 0, nu = 0;
+    for (int s = lane; s < N2CAP; s += 32) {
+      const int v = T[s];
+      if (v < 0) continue;
+      nl += v < i;
+      nu += v > i;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      nl += __shfl_xor_sync(0xffffffffu, nl, o);
+      nu += __shfl_xor_sync(0xffffffffu, nu, o);
+    }
+    if (lane == 0) {
+      lower[i] = nl;
+      upcnt[i] = nu;
+    }
+  } else {
+    __syncwarp();
+    if (lane == 0) cnt[w] = 0;
+    __syncwarp();
+    const i64 base = upptr[i];
+    for (int s = lane; s < N2CAP; s += 32) {
+      const int v = T[s];
+      if (v > i) up[base + atomicAdd(&cnt[w], 1)] = v;
+    }
+  }
+}
 
 __global__ void k_n2(i64 nn, const i64* __restrict__ sp, const int* __restrict__ si, const i64* __restrict__ tp,
                      const int* __restrict__ ti, int* __restrict__ lower, i64* __restrict__ upcnt,
-                     const i64* __restrict__ upptr, int* __restrict__ up, int mode, int* __restrict__ err) {
+                     const i64* __restrict__ upptr, int* __restrict__ up, int mode, int* __restrict__ ovf) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   // lists: S[i], T[i], T[j] for j in S[i]
@@ -176,7 +476,7 @@ __global__ void k_n2(i64 nn, const i64* __restrict__ sp, const int* __restrict__
   int nl = 0;
   const i64 ns = sp[i + 1] - sp[i];
   if (ns + 2 > MCAP) {
-    *err = 1;
+    if (mode == 0) ovf[i] = 1;
     return;
   }
   cur[nl] = sp[i]; end[nl] = sp[i + 1]; arr[nl] = si; ++nl;
@@ -705,7 +1005,9 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     CF_CUDA(cudaMemcpyAsync(B.p, B0, size_t(A->rows) * m * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
   }
   DevBuf<int> err(1);
+  PhaseClock clk;
   for (int lev = 0; lev < opts.max_levels; ++lev) {
+    clk.lev = lev;
     const i64 n = A->rows;
     if (n <= opts.coarse_size) break;
     // n_nodes = max(node_of_dof) + 1
@@ -729,19 +1031,53 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     CF_LAUNCHED();
     DevBuf<i64> sptr(n_nodes + 1);
     sptr.zero();
-    err.zero();
+    DevBuf<int> ovf(n_nodes);
+    ovf.zero();
     k_strength<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, nptr.p, ndofs.p, A->ptr.p, A->col.p, A->val.p,
                                                               nod.p, dsq.p, opts.strength_threshold, sptr.p, nullptr,
-                                                              nullptr, 0, err.p);
+                                                              nullptr, 0, ovf.p);
     CF_LAUNCHED();
-    if (read_dev(err.p)) fail(CF_ERR_UNSUPPORTED, "build_amg: a node couples to more than 384 nodes");
+    // overflow tier for high-degree nodes
+    OvfList big = make_ovf_list(n_nodes, ovf.p);
+    DevBuf<i64> boff;
+    DevBuf<int> bkeys, blen;
+    DevBuf<double> bsums;
+    if (big.n) {
+      boff.alloc(big.n + 1);
+      k_node_entries<<<grid_for(big.n, 128), 128, 0, stream()>>>(big.n, big.list.p, nptr.p, ndofs.p, A->ptr.p,
+                                                                 pow2_at_least(2 * n_nodes), boff.p);
+      CF_LAUNCHED();
+      CF_CUDA(cudaMemsetAsync(boff.p + big.n, 0, sizeof(i64), stream()));
+      scan_excl(boff.p, big.n + 1);
+      const i64 tot = read_dev(boff.p + big.n);
+      bkeys.alloc(tot);
+      bsums.alloc(tot);
+      blen.alloc(big.n);
+      CF_CUDA(cudaMemsetAsync(bkeys.p, 0xff, size_t(tot) * sizeof(int), stream()));
+      k_strength_big<<<grid_for(big.n, 64), 64, 0, stream()>>>(big.n, big.list.p, boff.p, nptr.p, ndofs.p, A->ptr.p,
+                                                               A->col.p, A->val.p, nod.p, bkeys.p, bsums.p, blen.p);
+      CF_LAUNCHED();
+      k_strength_big_emit<<<grid_for(big.n, 128), 128, 0, stream()>>>(big.n, big.list.p, boff.p, bkeys.p, bsums.p,
+                                                                      blen.p, dsq.p, opts.strength_threshold, sptr.p,
+                                                                      nullptr, nullptr, 0);
+      CF_LAUNCHED();
+    }
     scan_excl(sptr.p, n_nodes + 1);
     const i64 ns = read_dev(sptr.p + n_nodes);
     DevBuf<int> sidx(std::max<i64>(ns, 1));
     k_strength<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, nptr.p, ndofs.p, A->ptr.p, A->col.p, A->val.p,
                                                               nod.p, dsq.p, opts.strength_threshold, nullptr, sptr.p,
-                                                              sidx.p, 1, err.p);
+                                                              sidx.p, 1, ovf.p);
     CF_LAUNCHED();
+    if (big.n) {
+      k_strength_big_emit<<<grid_for(big.n, 128), 128, 0, stream()>>>(big.n, big.list.p, boff.p, bkeys.p, bsums.p,
+                                                                      blen.p, dsq.p, opts.strength_threshold, nullptr,
+                                                                      sptr.p, sidx.p, 1);
+      CF_LAUNCHED();
+    }
+    bkeys.release();
+    bsums.release();
+    clk.mark("strength");
     // transpose T = S^T (ascending lists): stable grouping of edges by destination
     DevBuf<i64> tptr;
     DevBuf<int> tidx(std::max<i64>(ns, 1));
@@ -757,17 +1093,40 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     DevBuf<int> lower(n_nodes);
     DevBuf<i64> uptr(n_nodes + 1);
     uptr.zero();
-    err.zero();
-    k_n2<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, lower.p, uptr.p,
-                                                        nullptr, nullptr, 0, err.p);
+    ovf.zero();
+    k_n2w<<<grid_for(n_nodes, N2WPB), N2WPB * 32, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, lower.p,
+                                                                 uptr.p, nullptr, nullptr, 0, ovf.p);
     CF_LAUNCHED();
-    if (read_dev(err.p)) fail(CF_ERR_UNSUPPORTED, "build_amg: a node has more than 254 strong neighbours");
+    OvfList big2 = make_ovf_list(n_nodes, ovf.p);
+    DevBuf<i64> noff;
+    DevBuf<int> nkeys;
+    if (big2.n) {
+      noff.alloc(big2.n + 1);
+      k_n2_cap<<<grid_for(big2.n, 128), 128, 0, stream()>>>(big2.n, big2.list.p, sptr.p, sidx.p, tptr.p,
+                                                            pow2_at_least(2 * n_nodes), noff.p);
+      CF_LAUNCHED();
+      CF_CUDA(cudaMemsetAsync(noff.p + big2.n, 0, sizeof(i64), stream()));
+      scan_excl(noff.p, big2.n + 1);
+      const i64 tot = read_dev(noff.p + big2.n);
+      nkeys.alloc(tot);
+      CF_CUDA(cudaMemsetAsync(nkeys.p, 0xff, size_t(tot) * sizeof(int), stream()));
+      k_n2_big<<<grid_for(big2.n, 64), 64, 0, stream()>>>(big2.n, big2.list.p, noff.p, sptr.p, sidx.p, tptr.p, tidx.p,
+                                                          nkeys.p, lower.p, uptr.p, nullptr, nullptr, 0);
+      CF_LAUNCHED();
+    }
     scan_excl(uptr.p, n_nodes + 1);
     const i64 nup = read_dev(uptr.p + n_nodes);
     DevBuf<int> up(std::max<i64>(nup, 1));
-    k_n2<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, nullptr, nullptr,
-                                                        uptr.p, up.p, 1, err.p);
+    k_n2w<<<grid_for(n_nodes, N2WPB), N2WPB * 32, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, nullptr,
+                                                                 nullptr, uptr.p, up.p, 1, ovf.p);
     CF_LAUNCHED();
+    if (big2.n) {
+      k_n2_big<<<grid_for(big2.n, 64), 64, 0, stream()>>>(big2.n, big2.list.p, noff.p, sptr.p, sidx.p, tptr.p, tidx.p,
+                                                          nkeys.p, nullptr, nullptr, uptr.p, up.p, 1);
+      CF_LAUNCHED();
+    }
+    nkeys.release();
+    clk.mark("S^T + N2");
     // pass 1: lexicographically-first MIS of N2 (persistent cooperative frontier kernel)
     DevBuf<int> status(n_nodes), f0(n_nodes), f1(n_nodes), sizes(3), rounds(1);
     sizes.zero();
@@ -789,6 +1148,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
       CF_CUDA(cudaLaunchCooperativeKernel((void*)k_lfmis, grid, 256, args, 0, stream()));
       CF_LAUNCHED();
     }
+    clk.mark("lfmis");
     // aggregate ids of the roots (ascending), claims
     DevBuf<int> rootid(n_nodes + 1), agg1(n_nodes);
     k_root_flags<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, status.p, rootid.p);
@@ -820,6 +1180,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     const i64 n_agg = i64(n1) + n3;
     if (n_agg >= n_nodes && n_nodes > 1) break;  // no coarsening possible (linsolve.cpp:203)
 
+    clk.mark("pass 2/3");
     // tentative prolongator: per-aggregate QR of the near-nullspace rows
     DevBuf<int> aod(n);
     k_agg_of_dof<<<grid_for(n, 256), 256, 0, stream()>>>(n, nod.p, agg.p, aod.p);
@@ -865,12 +1226,16 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     csr_diagonal(*A, L->inv_diag.p);
     k_inv_diag<<<grid_for(n, 256), 256, 0, stream()>>>(n, L->inv_diag.p);
     CF_LAUNCHED();
+    clk.mark("qr+T");
     const double lambda = estimate_lambda_max(*A, L->inv_diag.p);
+    clk.mark("lambda");
     const double wp = opts.prolongation_omega * 2.0 / lambda;
     auto DAT = spgemm(*A, T, L->inv_diag.p);
+    clk.mark("spgemm DAT");
     L->P = csr_axpy_prune(T, wp, *DAT);
     DAT.reset();
     L->R = transpose(*L->P);
+    clk.mark("P+R");
     L->A = A;
     L->jacobi_weight = opts.jacobi_omega * 2.0 / lambda;
     L->lambda = lambda;
@@ -881,7 +1246,9 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     L->agg_of_node = std::move(agg);
     // Galerkin coarse operator Ac = P^T (A P), pruned; coarse nullspace and node ids
     auto AP = spgemm(*A, *L->P);
+    clk.mark("spgemm AP");
     auto Ac = spgemm(*L->R, *AP);
+    clk.mark("spgemm RAP");
     AP.reset();
     csr_prune(*Ac);
     DevBuf<double> Bc(nc * m);

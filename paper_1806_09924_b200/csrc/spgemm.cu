@@ -2,14 +2,16 @@
 // transpose, union-axpy with pruning, prune, diagonal extraction.
 //
 // SpGEMM C = diag(s) A B (linsolve.cpp:248-263: D^-1 A T, A P, P^T (A P)) in three passes:
-//   1. symbolic count — per row, a shared-memory hash set of the output columns (warp per row
-//      with 512 / 2048 slots; rows that overflow are redone by a CTA with 16384 slots);
-//   2. symbolic fill  — the same hash, then a bitonic sort of the unique columns (sorted CSR);
-//   3. numeric        — per row, A's entries are visited in ascending column order and each
-//      B row is spread over the lanes; the accumulator slot comes from a binary search in the
-//      row's sorted column list.  Every C(i,j) is therefore the k-ascending sequential sum
-//      sum_k (s_i A_ik) B_kj — the same IEEE sequence as Eigen's conservative sparse product
-//      and the oracle, independent of the launch configuration (no floating-point atomics).
+//   1. symbolic count — per row a shared-memory hash set of the output columns (warp per row,
+//      512 slots; rows that overflow retry with 2048 slots, then a CTA with 16384 slots);
+//   2. symbolic fill  — the same hash sized to the known row length, then a bitonic sort of the
+//      unique columns (sorted CSR);
+//   3. numeric        — the row's columns are loaded into a shared-memory hash whose slots carry
+//      the accumulators.  A warp processes G = 32/L consecutive A entries at once (L lanes per
+//      B row); lanes compute (slot, value) pairs in parallel, then the G groups add in ascending
+//      k order, so every C(i,j) is the k-ascending sequential sum sum_k (s_i A_ik) B_kj — the same
+//      IEEE sequence as Eigen's conservative sparse product and the oracle, with no
+//      floating-point atomics and independent of the launch configuration.
 #include <cub/cub.cuh>
 
 #include <climits>
@@ -41,6 +43,18 @@ __device__ __forceinline__ int hinsert(int* tab, unsigned mask, int key) {
   return -1;
 }
 
+// slot of a present key (read-only probe)
+__device__ __forceinline__ int hfind(const int* tab, unsigned mask, int key) {
+  unsigned s = hslot(key, mask);
+  for (unsigned p = 0; p <= mask; ++p) {
+    const int cur = tab[s];
+    if (cur == key) return int(s);
+    if (cur == EMPTY) return -1;
+    s = (s + 1) & mask;
+  }
+  return -1;
+}
+
 __global__ void k_row_bound(i64 rows, const i64* __restrict__ ap, const int* __restrict__ ac,
                             const i64* __restrict__ bp, i64* __restrict__ ub) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -53,68 +67,13 @@ __global__ void k_row_bound(i64 rows, const i64* __restrict__ ap, const int* __r
   ub[i] = s;
 }
 
-// --- symbolic, warp per row ---------------------------------------------------------------
-// mode 0: count (cnt[row] = unique, or -1 on overflow); mode 1: fill sorted columns into ccol
-template <int CAP, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_sym_warp(const int* __restrict__ rowlist, i64 nrows,
-                                                       const i64* __restrict__ ap, const int* __restrict__ ac,
-                                                       const i64* __restrict__ bp, const int* __restrict__ bc,
-                                                       i64* __restrict__ cnt, const i64* __restrict__ cptr,
-                                                       int* __restrict__ ccol, int mode) {
-  __shared__ int tab[WPB][CAP];
-  __shared__ int nuniq[WPB];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const i64 r = i64(blockIdx.x) * WPB + w;
-  if (r >= nrows) return;
-  const i64 i = rowlist ? rowlist[r] : r;
-  int* T = tab[w];
-  for (int s = lane; s < CAP; s += 32) T[s] = EMPTY;
-  if (lane == 0) nuniq[w] = 0;
-  __syncwarp();
-  const unsigned mask = CAP - 1;
-  int mine = 0;
-  bool full = false;
-  for (i64 ka = ap[i]; ka < ap[i + 1] && !full; ++ka) {
-    const int k = ac[ka];
-    for (i64 kb = bp[k] + lane; kb < bp[k + 1]; kb += 32) {
-      const int r2 = hinsert(T, mask, bc[kb]);
-      if (r2 < 0) full = true; else mine += r2;
-    }
-    // warp-uniform early exit once the table is 3/4 full (overflow -> CTA tier)
-    int tot = mine;
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    full = __any_sync(0xffffffffu, full) || tot > (CAP * 3) / 4;
-  }
-  // warp total
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  __syncwarp();
-  if (full || mine > (CAP * 3) / 4) {
-    if (lane == 0 && mode == 0) cnt[i] = -1;
-    return;  // mode 1 is only launched for rows known to fit
-  }
-  if (mode == 0) {
-    if (lane == 0) cnt[i] = mine;
-    return;
-  }
-  // compact + bitonic sort (size = next pow2 of the unique count)
-  int n2 = 1;
-  while (n2 < mine) n2 <<= 1;
-  // compact keys to the front of a second region: reuse T by first collecting in registers is
-  // impractical, so compact in place through a prefix over slots.
-  __shared__ int buf[WPB][CAP];
-  int* Bf = buf[w];
-  if (lane == 0) nuniq[w] = 0;
-  __syncwarp();
-  for (int s = lane; s < CAP; s += 32) {
-    const int key = T[s];
-    if (key != EMPTY) {
-      const int p = atomicAdd(&nuniq[w], 1);
-      Bf[p] = key;
-    }
-  }
-  __syncwarp();
-  for (int s = mine + lane; s < n2; s += 32) Bf[s] = INT_MAX;
-  __syncwarp();
+__global__ void k_max_row(i64 rows, const i64* __restrict__ p, unsigned long long* __restrict__ mx) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < rows) atomicMax(mx, (unsigned long long)(p[i + 1] - p[i]));
+}
+
+template <int WPB>
+__device__ __forceinline__ void bitonic_warp(int* Bf, int n2, int lane) {
   for (int k2 = 2; k2 <= n2; k2 <<= 1)
     for (int j = k2 >> 1; j > 0; j >>= 1) {
       for (int t = lane; t < n2; t += 32) {
@@ -130,11 +89,73 @@ __global__ void __launch_bounds__(WPB * 32) k_sym_warp(const int* __restrict__ r
       }
       __syncwarp();
     }
+}
+
+// --- symbolic, warp per row: G = 32/L consecutive A entries per step (set semantics, any order)
+// mode 0: cnt[row] = unique count or -1 (overflow); mode 1: sorted columns -> ccol
+template <int CAP, int L, int WPB, int MODE>
+__global__ void __launch_bounds__(WPB * 32) k_sym(const int* __restrict__ rowlist, i64 nrows,
+                                                  const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                  const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                  i64* __restrict__ cnt, const i64* __restrict__ cptr,
+                                                  int* __restrict__ ccol) {
+  constexpr int G = 32 / L;
+  __shared__ int tab[WPB][CAP];
+  __shared__ int buf[MODE ? WPB : 1][MODE ? CAP : 1];
+  __shared__ int nuniq[WPB];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 r = i64(blockIdx.x) * WPB + w;
+  if (r >= nrows) return;
+  const i64 i = rowlist ? rowlist[r] : r;
+  int* T = tab[w];
+  for (int s = lane; s < CAP; s += 32) T[s] = EMPTY;
+  __syncwarp();
+  const unsigned mask = CAP - 1;
+  const int g = lane / L, lig = lane % L;
+  int mine = 0;
+  bool full = false;
+  const i64 a0 = ap[i], a1 = ap[i + 1];
+  for (i64 kb0 = a0; kb0 < a1 && !full; kb0 += G) {
+    const i64 ka = kb0 + g;
+    if (ka < a1) {
+      const int k = ac[ka];
+      for (i64 q = bp[k] + lig; q < bp[k + 1]; q += L) {
+        const int r2 = hinsert(T, mask, bc[q]);
+        if (r2 < 0) full = true; else mine += r2;
+      }
+    }
+    int tot = mine;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    full = __any_sync(0xffffffffu, full) || tot > (CAP * 3) / 4;
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  __syncwarp();
+  if (full || mine > (CAP * 3) / 4) {
+    if (MODE == 0 && lane == 0) cnt[i] = -1;
+    return;
+  }
+  if (MODE == 0) {
+    if (lane == 0) cnt[i] = mine;
+    return;
+  }
+  int* Bf = buf[w];
+  if (lane == 0) nuniq[w] = 0;
+  __syncwarp();
+  for (int s = lane; s < CAP; s += 32) {
+    const int key = T[s];
+    if (key != EMPTY) Bf[atomicAdd(&nuniq[w], 1)] = key;
+  }
+  __syncwarp();
+  int n2 = 1;
+  while (n2 < mine) n2 <<= 1;
+  for (int s = mine + lane; s < n2; s += 32) Bf[s] = INT_MAX;
+  __syncwarp();
+  bitonic_warp<WPB>(Bf, n2, lane);
   const i64 base = cptr[i];
   for (int t = lane; t < mine; t += 32) ccol[base + t] = Bf[t];
 }
 
-// --- symbolic, CTA per row (overflow rows) ---------------------------------------------------
+// --- symbolic, CTA per row (rows beyond the warp tiers) -----------------------------------
 template <int CAP>
 __global__ void __launch_bounds__(256) k_sym_cta(const int* __restrict__ rowlist, i64 nrows,
                                                  const i64* __restrict__ ap, const int* __restrict__ ac,
@@ -142,19 +163,20 @@ __global__ void __launch_bounds__(256) k_sym_cta(const int* __restrict__ rowlist
                                                  i64* __restrict__ cnt, const i64* __restrict__ cptr,
                                                  int* __restrict__ ccol, int mode, int* __restrict__ overflow) {
   extern __shared__ int sm[];
-  int* T = sm;            // CAP
-  int* Bf = sm + CAP;     // CAP (mode 1)
+  int* T = sm;         // CAP
+  int* Bf = sm + CAP;  // CAP (mode 1)
   __shared__ int nuniq;
+  __shared__ int sfull;
   const i64 r = blockIdx.x;
   if (r >= nrows) return;
   const i64 i = rowlist ? rowlist[r] : r;
   for (int s = threadIdx.x; s < CAP; s += blockDim.x) T[s] = EMPTY;
-  if (threadIdx.x == 0) nuniq = 0;
+  if (threadIdx.x == 0) {
+    nuniq = 0;
+    sfull = 0;
+  }
   __syncthreads();
   const unsigned mask = CAP - 1;
-  __shared__ int sfull;
-  if (threadIdx.x == 0) sfull = 0;
-  __syncthreads();
   for (i64 ka = ap[i]; ka < ap[i + 1]; ++ka) {
     const int k = ac[ka];
     for (i64 kb = bp[k] + threadIdx.x; kb < bp[k + 1]; kb += blockDim.x) {
@@ -205,6 +227,141 @@ __global__ void __launch_bounds__(256) k_sym_cta(const int* __restrict__ rowlist
   for (int t = threadIdx.x; t < mine; t += blockDim.x) ccol[base + t] = Bf[t];
 }
 
+// --- numeric, warp per row: hash slots carry the accumulators; ordered group adds ------------
+template <int CAP, int L, int WPB, int CMAX>
+__global__ void __launch_bounds__(WPB * 32) k_num(const int* __restrict__ rowlist, i64 nrows,
+                                                  const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                  const double* __restrict__ av, const double* __restrict__ rs,
+                                                  const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                  const double* __restrict__ bv, const i64* __restrict__ cp,
+                                                  const int* __restrict__ cc, double* __restrict__ cv) {
+  constexpr int G = 32 / L;
+  __shared__ int tab[WPB][CAP];
+  __shared__ double acc[WPB][CAP];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 r = i64(blockIdx.x) * WPB + w;
+  if (r >= nrows) return;
+  const i64 i = rowlist ? rowlist[r] : r;
+  int* T = tab[w];
+  double* Acc = acc[w];
+  for (int s = lane; s < CAP; s += 32) {
+    T[s] = EMPTY;
+    Acc[s] = 0.0;
+  }
+  __syncwarp();
+  const unsigned mask = CAP - 1;
+  const i64 c0 = cp[i];
+  const int nc = int(cp[i + 1] - c0);
+  for (int t = lane; t < nc; t += 32) hinsert(T, mask, cc[c0 + t]);
+  __syncwarp();
+  const double si = rs ? rs[i] : 1.0;
+  const int g = lane / L, lig = lane % L;
+  const i64 a0 = ap[i], a1 = ap[i + 1];
+  for (i64 kb0 = a0; kb0 < a1; kb0 += G) {
+    const i64 ka = kb0 + g;
+    int slot[CMAX];
+    double val[CMAX];
+    int np = 0;
+    if (ka < a1) {
+      const int k = ac[ka];
+      const double a = rs ? si * av[ka] : av[ka];
+      for (i64 q = bp[k] + lig; q < bp[k + 1] && np < CMAX; q += L) {
+        slot[np] = hfind(T, mask, bc[q]);
+        val[np] = a * bv[q];
+        ++np;
+      }
+    }
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {  // ascending k: group gg holds A entry kb0 + gg
+      if (g == gg)
+        for (int t = 0; t < np; ++t) Acc[slot[t]] += val[t];
+      __syncwarp();
+    }
+  }
+  for (int t = lane; t < nc; t += 32) cv[c0 + t] = Acc[hfind(T, mask, cc[c0 + t])];
+}
+
+// --- flat numeric, warp per row ---------------------------------------------------------------
+// The row's products are enumerated in (A column, B column) order as p = 0..U-1 and spread over
+// the lanes 32 at a time, so every lane's loads are independent (no per-k dependency chain).
+// Lanes of one chunk that hit the same output slot are resolved with __match_any_sync and add in
+// lane order, i.e. in ascending k: each C(i,j) is still the k-ascending sequential sum.
+template <int CAP, int WPB, int PCAP>
+__global__ void __launch_bounds__(WPB * 32) k_num_flat(const int* __restrict__ rowlist, i64 nrows,
+                                                       const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                       const double* __restrict__ av, const double* __restrict__ rs,
+                                                       const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                       const double* __restrict__ bv, const i64* __restrict__ cp,
+                                                       const int* __restrict__ cc, double* __restrict__ cv) {
+  __shared__ int tab[WPB][CAP];
+  __shared__ double acc[WPB][CAP];
+  __shared__ int pre[WPB][PCAP + 1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 r = i64(blockIdx.x) * WPB + w;
+  if (r >= nrows) return;
+  const i64 i = rowlist ? rowlist[r] : r;
+  int* T = tab[w];
+  double* Acc = acc[w];
+  int* Pre = pre[w];
+  for (int s = lane; s < CAP; s += 32) {
+    T[s] = EMPTY;
+    Acc[s] = 0.0;
+  }
+  __syncwarp();
+  const unsigned mask = CAP - 1;
+  const i64 c0 = cp[i];
+  const int nc = int(cp[i + 1] - c0);
+  for (int t = lane; t < nc; t += 32) hinsert(T, mask, cc[c0 + t]);
+  // prefix of the B row lengths over the A row
+  const i64 a0 = ap[i];
+  const int na = int(ap[i + 1] - a0);
+  int carry = 0;
+  if (lane == 0) Pre[0] = 0;
+  for (int t0 = 0; t0 < na; t0 += 32) {
+    const int t = t0 + lane;
+    int len = 0;
+    if (t < na) {
+      const int k = ac[a0 + t];
+      len = int(bp[k + 1] - bp[k]);
+    }
+    int incl = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (t < na) Pre[t + 1] = carry + incl;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncwarp();
+  const int U = carry;
+  const double si = rs ? rs[i] : 1.0;
+  int lo = 0;  // this lane's A-row cursor: largest ka with Pre[ka] <= p (p only grows)
+  for (int p0 = 0; p0 < U; p0 += 32) {
+    const int p = p0 + lane;
+    const bool valid = p < U;
+    int slot = 0;
+    double v = 0.0;
+    if (valid) {
+      while (lo + 1 < na && Pre[lo + 1] <= p) ++lo;
+      const int k = ac[a0 + lo];
+      const double a = rs ? si * av[a0 + lo] : av[a0 + lo];
+      const i64 q = bp[k] + (p - Pre[lo]);
+      slot = hfind(T, mask, bc[q]);
+      v = a * bv[q];
+    }
+    // lanes sharing an A entry hit distinct columns; different A entries add in ascending order
+    const int kfirst = __shfl_sync(0xffffffffu, lo, 0);
+    const int last_lane = min(31, U - 1 - p0);
+    const int klast = __shfl_sync(0xffffffffu, lo, last_lane);
+    for (int kk = kfirst; kk <= klast; ++kk) {
+      if (valid && lo == kk) Acc[slot] += v;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  for (int t = lane; t < nc; t += 32) cv[c0 + t] = Acc[hfind(T, mask, cc[c0 + t])];
+}
+
 __device__ __forceinline__ int lower_bound_sm(const int* a, int n, int key) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -214,41 +371,7 @@ __device__ __forceinline__ int lower_bound_sm(const int* a, int n, int key) {
   return lo;
 }
 
-// --- numeric, warp per row with smem columns/accumulators -----------------------------------
-template <int CAP, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_num_warp(const int* __restrict__ rowlist, i64 nrows,
-                                                       const i64* __restrict__ ap, const int* __restrict__ ac,
-                                                       const double* __restrict__ av,
-                                                       const double* __restrict__ rs, const i64* __restrict__ bp,
-                                                       const int* __restrict__ bc, const double* __restrict__ bv,
-                                                       const i64* __restrict__ cp, const int* __restrict__ cc,
-                                                       double* __restrict__ cv) {
-  __shared__ int cols[WPB][CAP];
-  __shared__ double acc[WPB][CAP];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const i64 r = i64(blockIdx.x) * WPB + w;
-  if (r >= nrows) return;
-  const i64 i = rowlist ? rowlist[r] : r;
-  const i64 c0 = cp[i];
-  const int nc = int(cp[i + 1] - c0);
-  for (int t = lane; t < nc; t += 32) {
-    cols[w][t] = cc[c0 + t];
-    acc[w][t] = 0.0;
-  }
-  __syncwarp();
-  const double si = rs ? rs[i] : 1.0;
-  for (i64 ka = ap[i]; ka < ap[i + 1]; ++ka) {
-    const int k = ac[ka];
-    const double a = rs ? si * av[ka] : av[ka];
-    for (i64 kb = bp[k] + lane; kb < bp[k + 1]; kb += 32) {
-      const int pos = lower_bound_sm(cols[w], nc, bc[kb]);
-      acc[w][pos] += a * bv[kb];
-    }
-    __syncwarp();
-  }
-  for (int t = lane; t < nc; t += 32) cv[c0 + t] = acc[w][t];
-}
-
+// numeric, CTA per row (long rows): sorted columns in smem, binary-search slots, k sequential
 __global__ void __launch_bounds__(256) k_num_cta(const int* __restrict__ rowlist, i64 nrows,
                                                  const i64* __restrict__ ap, const int* __restrict__ ac,
                                                  const double* __restrict__ av, const double* __restrict__ rs,
@@ -281,7 +404,8 @@ __global__ void __launch_bounds__(256) k_num_cta(const int* __restrict__ rowlist
   for (int t = threadIdx.x; t < nc; t += blockDim.x) cv[c0 + t] = acc[t];
 }
 
-// partition rows by a predicate on a per-row value: out lists in ascending row order
+// partition rows by a predicate on a per-row value (order within a bin is irrelevant: every
+// listed row is processed independently)
 __global__ void k_bin_rows(i64 rows, const i64* __restrict__ v, i64 lo, i64 hi, int* __restrict__ list,
                            int* __restrict__ count) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -289,13 +413,22 @@ __global__ void k_bin_rows(i64 rows, const i64* __restrict__ v, i64 lo, i64 hi, 
   const i64 x = v[i];
   if (x > lo && x <= hi) list[atomicAdd(count, 1)] = int(i);
 }
+// numeric tier by (row length nc, A row length na): 0 (nc <= 128, na <= 512), 1 (nc <= 512,
+// na <= 1024), 2 (nc <= 1024, na <= 1024), 3 otherwise
+__global__ void k_num_tier(i64 m, const i64* __restrict__ ap, const i64* __restrict__ cp, i64* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const i64 nc = cp[i + 1] - cp[i], na = ap[i + 1] - ap[i];
+  out[i] = (nc <= 128 && na <= 512) ? 0 : (na <= 1024 && nc <= 512) ? 1 : (na <= 1024 && nc <= 1024) ? 2 : 3;
+}
 __global__ void k_row_len(i64 m, const i64* __restrict__ p, i64* __restrict__ out) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < m) out[i] = p[i + 1] - p[i];
 }
-__global__ void k_bin_overflow(i64 rows, const i64* __restrict__ cnt, int* __restrict__ list, int* __restrict__ count) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < rows && cnt[i] < 0) list[atomicAdd(count, 1)] = int(i);
+__global__ void k_bin_overflow(i64 rows, const int* __restrict__ list, int n, const i64* __restrict__ cnt,
+                               int* __restrict__ out, int* __restrict__ count) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n && cnt[list[t]] < 0) out[atomicAdd(count, 1)] = list[t];
 }
 
 template <class T>
@@ -336,7 +469,65 @@ RowBin make_bin(i64 rows, const i64* v, i64 lo, i64 hi) {
   return b;
 }
 
+RowBin overflow_of(const RowBin& in, const i64* cnt) {
+  RowBin o;
+  o.list.alloc(std::max(in.n, 1));
+  if (!in.n) return o;
+  DevBuf<int> c(1);
+  c.zero();
+  k_bin_overflow<<<grid_for(in.n, 256), 256, 0, stream()>>>(0, in.list.p, in.n, cnt, o.list.p, c.p);
+  CF_LAUNCHED();
+  o.n = read_int(c.p);
+  return o;
+}
+
 constexpr int SYM_BIG = 16384;
+
+// lanes per A entry in the warp kernels, from the longest B row
+// 8 lanes (4 A entries in flight per step, <= 16 independent B loads per lane) unless B rows are
+// long; this is what hides the per-A-entry dependency chain (ac -> bp -> bc -> hash)
+int lanes_for(i64 maxb) { return maxb <= 128 ? 8 : 32; }
+
+template <int L>
+void sym_launch(int mode, const RowBin& b, int cap, const Csr& A, const Csr& B, i64* cnt, const Csr* C) {
+  if (!b.n) return;
+  if (cap == 512) {
+    if (mode == 0)
+      k_sym<512, L, 8, 0><<<grid_for(b.n, 8), 256, 0, stream()>>>(b.list.p, b.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p,
+                                                                  cnt, nullptr, nullptr);
+    else
+      k_sym<512, L, 8, 1><<<grid_for(b.n, 8), 256, 0, stream()>>>(b.list.p, b.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p,
+                                                                  nullptr, C->ptr.p, C->col.p);
+  } else {
+    if (mode == 0)
+      k_sym<2048, L, 4, 0><<<grid_for(b.n, 4), 128, 0, stream()>>>(b.list.p, b.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p,
+                                                                   cnt, nullptr, nullptr);
+    else
+      k_sym<2048, L, 2, 1><<<grid_for(b.n, 2), 64, 0, stream()>>>(b.list.p, b.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p,
+                                                                  nullptr, C->ptr.p, C->col.p);
+  }
+  CF_LAUNCHED();
+}
+
+void sym_dispatch(int L, int mode, const RowBin& b, int cap, const Csr& A, const Csr& B, i64* cnt, const Csr* C) {
+  if (L == 8) sym_launch<8>(mode, b, cap, A, B, cnt, C);
+  else if (L == 16) sym_launch<16>(mode, b, cap, A, B, cnt, C);
+  else sym_launch<32>(mode, b, cap, A, B, cnt, C);
+}
+
+template <int L, int CMAX>
+void num_launch(const RowBin& b, int cap, const Csr& A, const Csr& B, const double* rs, Csr& C) {
+  if (!b.n) return;
+  if (cap == 512)
+    k_num<512, L, 8, CMAX><<<grid_for(b.n, 8), 256, 0, stream()>>>(b.list.p, b.n, A.ptr.p, A.col.p, A.val.p, rs,
+                                                                   B.ptr.p, B.col.p, B.val.p, C.ptr.p, C.col.p,
+                                                                   C.val.p);
+  else
+    k_num<2048, L, 2, CMAX><<<grid_for(b.n, 2), 64, 0, stream()>>>(b.list.p, b.n, A.ptr.p, A.col.p, A.val.p, rs,
+                                                                   B.ptr.p, B.col.p, B.val.p, C.ptr.p, C.col.p,
+                                                                   C.val.p);
+  CF_LAUNCHED();
+}
 
 }  // namespace
 
@@ -349,97 +540,82 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   C->ptr.zero();
   const i64 m = A.rows;
   if (m == 0) return C;
+  i64 maxb;
+  {
+    DevBuf<unsigned long long> mx(1);
+    mx.zero();
+    k_max_row<<<grid_for(B.rows, 256), 256, 0, stream()>>>(B.rows, B.ptr.p, mx.p);
+    CF_LAUNCHED();
+    unsigned long long h = 0;
+    CF_CUDA(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    maxb = i64(h);
+  }
+  const int L = lanes_for(maxb);
   i64* cnt = C->ptr.p;  // row counts in place, scanned into offsets afterwards
-  // 1. symbolic count, binned by the product-count bound U_i (unique columns <= U_i)
+  // 1. symbolic count: all rows with products try the 512-slot tier, overflow -> 2048 -> CTA
   {
     DevBuf<i64> ub(m);
     k_row_bound<<<grid_for(m, 256), 256, 0, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, ub.p);
     CF_LAUNCHED();
-    RowBin small = make_bin(m, ub.p, 0, 256);
-    RowBin large = make_bin(m, ub.p, 256, LLONG_MAX);
-    if (small.n) {
-      k_sym_warp<512, 8><<<grid_for(small.n, 8), 256, 0, stream()>>>(small.list.p, small.n, A.ptr.p, A.col.p,
-                                                                      B.ptr.p, B.col.p, cnt, nullptr, nullptr, 0);
+    RowBin all = make_bin(m, ub.p, 0, LLONG_MAX);
+    sym_dispatch(L, 0, all, 512, A, B, cnt, nullptr);
+    RowBin o1 = overflow_of(all, cnt);
+    sym_dispatch(L, 0, o1, 2048, A, B, cnt, nullptr);
+    RowBin o2 = overflow_of(o1, cnt);
+    if (o2.n) {
+      DevBuf<int> flag(1);
+      flag.zero();
+      const size_t sm = size_t(2) * SYM_BIG * sizeof(int);
+      CF_CUDA(cudaFuncSetAttribute(k_sym_cta<SYM_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      k_sym_cta<SYM_BIG><<<o2.n, 256, sm, stream()>>>(o2.list.p, o2.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p, cnt,
+                                                      nullptr, nullptr, 0, flag.p);
       CF_LAUNCHED();
-    }
-    if (large.n) {
-      k_sym_warp<2048, 2><<<grid_for(large.n, 2), 64, 0, stream()>>>(large.list.p, large.n, A.ptr.p, A.col.p,
-                                                                       B.ptr.p, B.col.p, cnt, nullptr, nullptr, 0);
-      CF_LAUNCHED();
-      RowBin ovf;
-      ovf.list.alloc(large.n);
-      DevBuf<int> c(1);
-      c.zero();
-      k_bin_overflow<<<grid_for(m, 256), 256, 0, stream()>>>(m, cnt, ovf.list.p, c.p);
-      CF_LAUNCHED();
-      ovf.n = read_int(c.p);
-      if (ovf.n) {
-        DevBuf<int> flag(1);
-        flag.zero();
-        const size_t sm = size_t(2) * SYM_BIG * sizeof(int);
-        CF_CUDA(cudaFuncSetAttribute(k_sym_cta<SYM_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        k_sym_cta<SYM_BIG><<<ovf.n, 256, sm, stream()>>>(ovf.list.p, ovf.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p, cnt,
-                                                         nullptr, nullptr, 0, flag.p);
-        CF_LAUNCHED();
-        if (read_int(flag.p)) fail(CF_ERR_UNSUPPORTED, "spgemm: an output row exceeds 12288 columns");
-      }
+      if (read_int(flag.p)) fail(CF_ERR_UNSUPPORTED, "spgemm: an output row exceeds 12288 columns");
     }
   }
   scan_excl(C->ptr.p, m + 1);
   C->nnz = read_i64(C->ptr.p + m);
   C->col.alloc(C->nnz);
   C->val.alloc(C->nnz);
-  // 2. symbolic fill (sorted columns) and 3. numeric, binned by the exact row length
+  // 2. symbolic fill and 3. numeric, binned by the exact row length
   DevBuf<i64> len(m);
   k_row_len<<<grid_for(m, 256), 256, 0, stream()>>>(m, C->ptr.p, len.p);
   CF_LAUNCHED();
-  {
-    RowBin f1 = make_bin(m, len.p, 0, 384);
-    RowBin f2 = make_bin(m, len.p, 384, 1536);
-    RowBin f3 = make_bin(m, len.p, 1536, LLONG_MAX);
-    if (f1.n) {
-      k_sym_warp<512, 8><<<grid_for(f1.n, 8), 256, 0, stream()>>>(f1.list.p, f1.n, A.ptr.p, A.col.p, B.ptr.p,
-                                                                   B.col.p, nullptr, C->ptr.p, C->col.p, 1);
-      CF_LAUNCHED();
-    }
-    if (f2.n) {
-      k_sym_warp<2048, 2><<<grid_for(f2.n, 2), 64, 0, stream()>>>(f2.list.p, f2.n, A.ptr.p, A.col.p, B.ptr.p,
-                                                                    B.col.p, nullptr, C->ptr.p, C->col.p, 1);
-      CF_LAUNCHED();
-    }
-    if (f3.n) {
-      DevBuf<int> flag(1);
-      flag.zero();
-      const size_t sm = size_t(2) * SYM_BIG * sizeof(int);
-      CF_CUDA(cudaFuncSetAttribute(k_sym_cta<SYM_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      k_sym_cta<SYM_BIG><<<f3.n, 256, sm, stream()>>>(f3.list.p, f3.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p, nullptr,
-                                                      C->ptr.p, C->col.p, 1, flag.p);
-      CF_LAUNCHED();
-    }
+  RowBin f1 = make_bin(m, len.p, 0, 256);
+  RowBin f2 = make_bin(m, len.p, 256, 1024);
+  RowBin f3 = make_bin(m, len.p, 1024, LLONG_MAX);
+  sym_dispatch(L, 1, f1, 512, A, B, nullptr, C.get());
+  sym_dispatch(L, 1, f2, 2048, A, B, nullptr, C.get());
+  if (f3.n) {
+    DevBuf<int> flag(1);
+    flag.zero();
+    const size_t sm = size_t(2) * SYM_BIG * sizeof(int);
+    CF_CUDA(cudaFuncSetAttribute(k_sym_cta<SYM_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    k_sym_cta<SYM_BIG><<<f3.n, 256, sm, stream()>>>(f3.list.p, f3.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p, nullptr,
+                                                    C->ptr.p, C->col.p, 1, flag.p);
+    CF_LAUNCHED();
   }
-  {
-    RowBin n1 = make_bin(m, len.p, 0, 256);
-    RowBin n2 = make_bin(m, len.p, 256, 1536);
-    RowBin n3 = make_bin(m, len.p, 1536, LLONG_MAX);
-    if (n1.n) {
-      k_num_warp<256, 8><<<grid_for(n1.n, 8), 256, 0, stream()>>>(n1.list.p, n1.n, A.ptr.p, A.col.p, A.val.p,
-                                                                   row_scale, B.ptr.p, B.col.p, B.val.p, C->ptr.p,
-                                                                   C->col.p, C->val.p);
-      CF_LAUNCHED();
-    }
-    if (n2.n) {
-      k_num_warp<1536, 2><<<grid_for(n2.n, 2), 64, 0, stream()>>>(n2.list.p, n2.n, A.ptr.p, A.col.p, A.val.p,
-                                                                    row_scale, B.ptr.p, B.col.p, B.val.p, C->ptr.p,
-                                                                    C->col.p, C->val.p);
-      CF_LAUNCHED();
-    }
-    if (n3.n) {
-      const size_t sm = size_t(SYM_BIG) * (sizeof(double) + sizeof(int));
-      CF_CUDA(cudaFuncSetAttribute(k_num_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      k_num_cta<<<n3.n, 256, sm, stream()>>>(n3.list.p, n3.n, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p,
-                                             B.col.p, B.val.p, C->ptr.p, C->col.p, C->val.p);
-      CF_LAUNCHED();
-    }
+  // numeric: k-grouped warp kernels (G = 32/L A entries per step) by row length; CTA otherwise
+  const i64 cmax_need = (maxb + L - 1) / L;
+  bool warp_ok = true;
+  if (cmax_need <= 8) {
+    if (L == 8) { num_launch<8, 8>(f1, 512, A, B, row_scale, *C); num_launch<8, 8>(f2, 2048, A, B, row_scale, *C); }
+    else if (L == 16) { num_launch<16, 8>(f1, 512, A, B, row_scale, *C); num_launch<16, 8>(f2, 2048, A, B, row_scale, *C); }
+    else { num_launch<32, 8>(f1, 512, A, B, row_scale, *C); num_launch<32, 8>(f2, 2048, A, B, row_scale, *C); }
+  } else if (cmax_need <= 16) {
+    if (L == 8) { num_launch<8, 16>(f1, 512, A, B, row_scale, *C); num_launch<8, 16>(f2, 2048, A, B, row_scale, *C); }
+    else { num_launch<32, 16>(f1, 512, A, B, row_scale, *C); num_launch<32, 16>(f2, 2048, A, B, row_scale, *C); }
+  } else {
+    warp_ok = false;
+  }
+  RowBin n3 = warp_ok ? std::move(f3) : make_bin(m, len.p, 0, LLONG_MAX);
+  if (n3.n) {
+    const size_t sm = size_t(SYM_BIG) * (sizeof(double) + sizeof(int));
+    CF_CUDA(cudaFuncSetAttribute(k_num_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    k_num_cta<<<n3.n, 256, sm, stream()>>>(n3.list.p, n3.n, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p, B.col.p,
+                                           B.val.p, C->ptr.p, C->col.p, C->val.p);
+    CF_LAUNCHED();
   }
   return C;
 }
