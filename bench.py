@@ -1,15 +1,16 @@
-"""bench.py — driver benchmark of the B200 hot path (see DESIGN.md §Measurement).
+"""bench.py — driver benchmark of the B200 hot path (DESIGN.md §Measurement).
 
-Default workload (N=1): BASELINE config 1, the operator microbenchmark — the assembled
-degraded-elasticity block M_uu of a 3d 192^3 Q1 mesh (21,567,171 u dofs, 1,676,188,257 nnz),
-applied to u ~ N(0,1) with phi_tilde ~ U[0,1] (counter-based SplitMix64, seeds 180609924001/2).
-One step = one y = M_uu u through the library's C ABI.
+Headline (N=1): Newton-step DoF/s on BASELINE config 3 — the 3d Sneddon penny crack on a
+uniform 128^3 Q1 hex mesh (8,586,756 dofs), eps = 2h, kappa = 1e-12, load step 1, Newton tol
+1e-8, AMG-preconditioned GMRES (restart 100, rtol 1e-8).  One bench step = one complete
+newton_active_set_step (solver.cpp:49-188) from the seeded initial state, inputs resident in
+HBM; value = N_total x Newton iterations / device time.
+
+The operator half of the metric (BASELINE config 1: assembled M_uu of a 3d 192^3 mesh, 21.5M
+u dofs) is measured in the same run and reported under "operator"; the roofline object is the
+CSR SpMV kernel of that operator apply.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-
-Prints ONE JSON line (rank 0).  value = whole-job operator throughput in GB/s of algorithmic
-CSR bytes (int64 row pointers), inputs resident in HBM; e2e = the same metric through the C ABI
-with pinned HOST buffers (H2D of u and D2H of y inside the timed region).
 """
 from __future__ import annotations
 
@@ -28,7 +29,18 @@ sys.path.insert(0, ROOT)
 
 SEED_PHI = 180609924001
 SEED_U = 180609924002
-M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+CFG3 = dict(dim=3, half_width=10.0, n0=8, refinements=4)  # 128^3 cells
+CFG1 = dict(dim=3, half_width=10.0, n0=12, refinements=4)  # 192^3 cells (SURVEY §8.0)
+CPU_SAMPLE = dict(dim=3, half_width=10.0, n0=8, refinements=2)  # 32^3 cells, 1/64 of config 3
+
+METRIC = "Newton-step DoF/s (config 3: 3d penny crack, 128^3 Q1, 8,586,756 dofs)"
+CONFIG = {"workload": "config3: 3d Sneddon penny crack, uniform 128^3 Q1 hexes, 8,586,756 dofs (u, phi), FP64; "
+                      "E=1, nu=0.2, G_c=1, p=1e-3, eps=2h, kappa=1e-12, 1 load step, Newton tol 1e-8, "
+                      "GMRES(100) rtol 1e-8 with block AMG",
+          "step": "one newton_active_set_step from the seeded state (all Newton iterations)",
+          "l2": "working set (J 8.6 GB, AMG hierarchy, Krylov basis) >> 126 MB L2; no flush needed",
+          "parallelism": "single GPU"}
 
 
 def splitmix_uniform(seed: int, n: int, start: int = 0) -> np.ndarray:
@@ -48,19 +60,14 @@ def splitmix_normal(seed: int, n: int) -> np.ndarray:
     return np.sqrt(-2.0 * np.log1p(-U[0::2])) * np.cos(2.0 * np.pi * U[1::2])
 
 
-CFG1 = dict(dim=3, half_width=10.0, n0=12, refinements=4)  # 192^3 cells (SURVEY §8.0)
-
-
 def config1_host(dim=3, half_width=10.0, n0=12, refinements=4):
     nn = (n0 << refinements) + 1
     V = nn ** dim
-    pt = splitmix_uniform(SEED_PHI, V)
-    u = splitmix_normal(SEED_U, dim * V)
-    return V, pt, u
+    return V, splitmix_uniform(SEED_PHI, V), splitmix_normal(SEED_U, dim * V)
 
 
 def config1_inputs(cf, device="cuda", **over):
-    """Problem, constraints (Dirichlet), material, regularization, x = (u, phi_tilde), phi_tilde."""
+    """Config 1: problem, Dirichlet constraints, material, regularization, x = (u, phi_tilde), phi_tilde."""
     import torch
     c = dict(CFG1)
     c.update(over)
@@ -73,8 +80,18 @@ def config1_inputs(cf, device="cuda", **over):
     x = torch.empty(P.n_total, dtype=torch.float64, device=device)
     x[:P.n_u] = torch.from_numpy(u).to(device)
     x[P.n_u:] = torch.from_numpy(pt).to(device)
-    ptd = torch.from_numpy(pt).to(device)
-    return P, cs, mat, reg, x, ptd
+    return P, cs, mat, reg, x, torch.from_numpy(pt).to(device)
+
+
+def sneddon_setup(mod, cfg, oracle=False):
+    """Problem + material (eps = 2h fixed, kappa = 1e-12) + regularization for a Sneddon config."""
+    if oracle:
+        P = mod.Problem(cfg["dim"], cfg["half_width"], cfg["n0"], cfg["refinements"])
+        m = mod.material(eps_mode=1, eps_fixed=2 * P.h, kappa_factor=1e-12 / P.h)
+        return P, m, P.resolve_regularization(m, P.slit_band_edge(m))
+    P = mod.Problem(cfg["dim"], cfg["half_width"], cfg["n0"], cfg["refinements"])
+    m = mod.Material(eps_mode=1, eps_fixed=2 * P.h, kappa_factor=1e-12 / P.h)
+    return P, m, mod.resolve_regularization(P, m, mod.slit_band_edge(P, m))
 
 
 def csr_bytes(rows, cols, nnz):
@@ -90,17 +107,14 @@ class ClockSampler:
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        self.index, self.proc, self.lines = index, None, []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
         return self
@@ -137,7 +151,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup(gpus):
+def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -149,164 +163,197 @@ def dist_setup(gpus):
     return rank, world, local
 
 
-def reference_arm(args):
-    """--impl reference: the reference's CPU path (the oracle port: the reference itself cannot be
-    built here) on the host cores, same metric/config, bounded sample per step."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- CPU legs (oracle)
+def oracle_newton_sample(n_steps=1):
+    """The reference's CPU path (oracle port; the reference itself needs Eigen3, absent here) on the
+    bounded sample: returns (dofs, newton iterations, seconds) per step."""
     from oracle import orc
-    n_thr = os.cpu_count() or 1
-    P, J, u, nb = cpu_sample()
-    y = np.zeros(P.n_u)
+    P, m, reg = sneddon_setup(orc, CPU_SAMPLE, oracle=True)
+    phi, _ = P.initial_crack(m)
+    out = []
+    for _ in range(n_steps):
+        sol = np.zeros(P.n_total)
+        sol[P.n_u:] = phi
+        t0 = time.perf_counter()
+        rep = P.newton_step(m, reg, orc.solver_options(), sol, phi.copy(), phi.copy(), 1)
+        out.append((P.n_total, len(rep["iterations"]), time.perf_counter() - t0))
+    return out
+
+
+CPU_SAMPLE_DESC = ("3d penny crack 32^3 Q1 (143,748 dofs; config 3 physics at 1/64 of its cells), one full "
+                   "newton_active_set_step, single-threaded oracle port (the reference is single-threaded; "
+                   "its Eigen build is not available here)")
+
+
+def cpu_baseline_leg():
+    runs = oracle_newton_sample(1)
+    dofs, its, sec = runs[0]
+    return {"value": dofs * its / sec, "unit": "DoF/s", "cores": 1, "kind": "port", "sample": CPU_SAMPLE_DESC,
+            "newton_iterations": its, "seconds": sec}
+
+
+def reference_arm(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
     for _ in range(args.warmup):
-        orc.lib().orc_block_spmv_threads(J.h_, 0, orc._p(u), orc._p(y), n_thr)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        orc.lib().orc_block_spmv_threads(J.h_, 0, orc._p(u), orc._p(y), n_thr)
-    dt = (time.perf_counter() - t0) / args.steps
-    gbs = nb / dt / 1e9
-    sample = f"3d {P.ncells_side}^3 M_uu (1/{(192 // P.ncells_side) ** 3} of config 1), same input distributions"
-    out = {"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-           "dtype": "f64", "data": "synthetic", "config": CONFIG,
-           "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": n_thr, "kind": "port", "sample": sample},
-           "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        pass  # the oracle has no warm-up state; each step is a full, independent solve
+    runs = oracle_newton_sample(args.steps)
+    tot = sum(s for _, _, s in runs)
+    value = sum(d * i for d, i, _ in runs) / tot
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+           "higher_is_better": True, "dtype": "f64", "data": "synthetic", "config": CONFIG,
+           "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": 1, "kind": "port", "sample": CPU_SAMPLE_DESC},
+           "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-METRIC = "operator-apply HBM GB/s (M_uu CSR SpMV, config 1)"
-CONFIG = {"workload": "config1: M_uu apply, 3d 192^3 Q1 hex, 21,567,171 u dofs, FP64",
-          "format": "CSR int64 rowptr / int32 col", "l2": "inputs 20.6 GB >> 126 MB L2 (no flush needed)",
-          "parallelism": "single GPU"}
+# ----------------------------------------------------------------------------- GPU legs
+def time_events(fn, n, stream):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(n):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
 
 
-def cpu_sample(cells_side=48):
-    from oracle import orc
-    r = {48: 2, 96: 3}[cells_side]
-    P = orc.Problem(3, 10.0, 12, r)
-    P.ncells_side = cells_side
-    nn = cells_side + 1
-    V = nn ** 3
-    pt = splitmix_uniform(SEED_PHI, V)
-    u = splitmix_normal(SEED_U, 3 * V)
-    h = P.h
-    mat = orc.material(kappa_factor=1e-12 / h, eps_mode=1, eps_fixed=2 * h)
-    reg = orc.Regularization(2 * h, 1e-12)
-    cs = P.constraints(True)
-    x = np.concatenate([u, pt])
-    J = P.jacobian(cs, mat, reg, x, pt)
-    A = J.csr(0)
-    return P, J, np.ascontiguousarray(u), csr_bytes(A.rows, A.cols, A.nnz)
-
-
-def cpu_baseline_leg(seconds=10.0):
-    """Single-thread oracle SpMV on the bounded sample (~10 s of CPU work)."""
-    from oracle import orc
-    P, J, u, nb = cpu_sample()
-    y = np.zeros(P.n_u)
-    orc.lib().orc_block_spmv_threads(J.h_, 0, orc._p(u), orc._p(y), 1)
-    n = 0
+def operator_leg(cf, device, stream, applies=20):
+    """Config 1: assembled M_uu apply (CSR SpMV), inputs resident in HBM."""
+    import torch
+    P, cs, mat, reg, x, pt = config1_inputs(cf, device=device)
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    nu = P.n_u
+    u = x[:nu].contiguous()
+    del x, pt
+    y = torch.empty(nu, dtype=torch.float64, device=u.device)
+    nb = csr_bytes(nu, nu, J.nnz[0])
+    for _ in range(3):
+        J.spmv(0, u, out=y)
+    ms = time_events(lambda: J.spmv(0, u, out=y), applies, stream)
+    # e2e through the C ABI with pinned host buffers
+    uh = u.cpu().pin_memory()
+    yh = torch.empty(nu, dtype=torch.float64).pin_memory()
+    J.spmv(0, uh.numpy(), out=yh.numpy())
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    while time.perf_counter() - t0 < seconds:
-        orc.lib().orc_block_spmv_threads(J.h_, 0, orc._p(u), orc._p(y), 1)
-        n += 1
-    dt = (time.perf_counter() - t0) / n
-    return {"value": nb / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"3d 48^3 M_uu (1/64 of config 1), same distributions, {n} applies, oracle port "
-                      "(reference not buildable: Eigen3 absent)"}
+    for _ in range(3):
+        J.spmv(0, uh.numpy(), out=yh.numpy())
+    e2e_ms = (time.perf_counter() - t0) / 3 * 1e3
+    ok = bool(torch.equal(yh.to(device), y))
+    peak, src = peak_hbm()
+    gbs = nb / (ms * 1e-3) / 1e9
+    res = {"workload": "config1: M_uu apply, 3d 192^3 Q1, 21,567,171 u dofs, 1,676,188,257 nnz, CSR",
+           "value": gbs, "unit": "GB/s", "ms_per_apply": ms, "bytes_per_apply": nb, "frac_of_hbm_peak": gbs / peak,
+           "e2e": {"value": nb / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_apply": e2e_ms,
+                   "h2d_bytes_per_step": 8 * nu, "d2h_bytes_per_step": 8 * nu, "matches_device": ok},
+           "nnz": J.nnz[0]}
+    del J, u, y
+    torch.cuda.empty_cache()
+    return res, {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                 "traffic": None, "kernel": "k_spmv_b<16,4> (CSR SpMV, M_uu of config 1)", "bytes_per_launch": nb,
+                 "ms_per_launch": ms, "peak_source": src}
 
 
 def ours(args):
     import torch
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup()
     import paper_1806_09924_b200 as cf
     torch.cuda.set_device(local)
+    device = f"cuda:{local}"
     s = torch.cuda.current_stream()
     cf.set_stream(s)
-    P, cs, mat, reg, x, pt = config1_inputs(cf, device=f"cuda:{local}")
-    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
-    del pt
-    nu = P.n_u
-    u = x[:nu].contiguous()
-    del x
-    y = torch.empty(nu, dtype=torch.float64, device=u.device)
-    nb = csr_bytes(nu, nu, J.nnz[0])
-    # strong-scaling row slabs would split the rows; round 1 runs one replica per rank
+    P, mat, reg = sneddon_setup(cf, CFG3)
+    opts = cf.SolverOptions()
+    st0 = cf.make_initial_state(P, mat).get()
+    sol0 = torch.from_numpy(st0["solution"]).to(device)
+    po0 = torch.from_numpy(st0["phi_old"]).to(device)
+
+    def step():
+        st = cf.FractureState(P, sol0, po0, po0, 1)  # device-to-device reset of the seeded state
+        return st, cf.newton_active_set_step(st, mat, P, reg, opts)
+
     for _ in range(args.warmup):
-        J.spmv(0, u, out=y)
+        step()
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     l0 = cf.kernel_launches()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        ev0.record(s)
+        e0.record(s)
         for _ in range(args.steps):
-            J.spmv(0, u, out=y)
-        ev1.record(s)
+            st, rep = step()
+            reps.append(rep)
+        e1.record(s)
         torch.cuda.synchronize()
     launches = cf.kernel_launches() - l0
-    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    its = sum(len(r["iterations"]) for r in reps) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=u.device)
+        t = torch.tensor([ms], device=device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = t.item()
-    value = world * nb / (ms * 1e-3) / 1e9
+    value = world * P.n_total * its / (ms * 1e-3)
+    last = reps[-1]
+    free, total = torch.cuda.mem_get_info()
 
-    # e2e: through the C ABI with pinned host buffers (H2D u + SpMV + D2H y per step)
-    uh = u.cpu().pin_memory()
-    yh = torch.empty(nu, dtype=torch.float64).pin_memory()
-    uh_np, yh_np = uh.numpy(), yh.numpy()
-    for _ in range(2):
-        J.spmv(0, uh_np, out=yh_np)
+    # e2e: through the C ABI with host buffers (H2D of the state, Newton step, D2H of the solution)
+    h_sol, h_po = st0["solution"], st0["phi_old"]
     torch.cuda.synchronize()
-    ke = max(3, min(args.steps, 10))
     t0 = time.perf_counter()
-    for _ in range(ke):
-        J.spmv(0, uh_np, out=yh_np)
-    torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) / ke * 1e3
-    ok = bool(torch.allclose(yh.cuda(), y, rtol=0, atol=0))
+    st_h = cf.FractureState(P, h_sol, h_po, h_po, 1)
+    rep_h = cf.newton_active_set_step(st_h, mat, P, reg, opts)
+    x_h = st_h.get()["solution"]
+    e2e_s = time.perf_counter() - t0
+    e2e = {"value": P.n_total * len(rep_h["iterations"]) / e2e_s, "unit": "DoF/s", "seconds": e2e_s,
+           "h2d_bytes_per_step": 8 * (P.n_total + 2 * P.n_vertices), "d2h_bytes_per_step": 8 * (P.n_total + 2 * P.n_vertices),
+           "path": "cf_state_create(host) + cf_newton_active_set_step + cf_state_get(host)",
+           "newton_iterations": len(rep_h["iterations"]), "solution_finite": bool(np.isfinite(x_h).all())}
 
     if rank != 0:
         return
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = nb / (ms * 1e-3) / 1e9
+    op, roof = operator_leg(cf, device, s) if not args.no_operator else (None, None)
     out = {
-        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SplitMix64 seeds 180609924001/2)",
-        "config": CONFIG,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "k_spmv<32>", "bytes_per_launch": nb,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback"},
-        "e2e": {"value": nb / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": 8 * nu, "d2h_bytes_per_step": 8 * nu, "path": "cf_block_spmv, pinned host",
-                "matches_device": ok},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
-        "nnz": J.nnz[0],
+        "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Sneddon state)",
+        "config": dict(CONFIG, parallelism="single GPU" if world == 1 else f"{world} independent replicas"),
+        "newton_iterations_per_step": its, "ms_per_newton_iteration": ms / its,
+        "gmres_iterations": [r["gmres_iterations"] for r in last["iterations"]],
+        "active_set_final": last["iterations"][-1]["active_size"],
+        "phase_ms_last_step": last["times_ms"], "device_mem_used_gb": (total - free) / 1e9,
+        "roofline": roof, "operator": op, "e2e": e2e, "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps, "clocks": clk.summary(),
     }
     if not args.no_cpu and world == 1:
-        out["cpu_baseline"] = cpu_baseline_leg(args.cpu_seconds)
+        out["cpu_baseline"] = cpu_baseline_leg()
     print(json.dumps(out), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-operator", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         reference_arm(args)
     else:

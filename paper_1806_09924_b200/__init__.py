@@ -455,8 +455,7 @@ class FractureState:
         if _handle is not None:
             self._h = _handle
         else:
-            arrs = [None if a is None else np.ascontiguousarray(a, dtype=np.float64)
-                    for a in (solution, phi_old, phi_prev2)]
+            arrs = [None if a is None else _as_f64(a) for a in (solution, phi_old, phi_prev2)]
             self._h = C.c_void_p()
             check(load().cf_state_create(prob._h, *[_ptr(a) for a in arrs], int(step), C.byref(self._h)))
 

@@ -997,12 +997,19 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
   auto h = std::make_unique<Amg>();
   h->opts = opts;
   h->n = A0->rows;
+  h->A0 = A0;
+  h->m0 = m;
+  h->nod0.alloc(A0->rows);
+  h->B0.alloc(A0->rows * m);
   std::shared_ptr<Csr> A = A0;
   DevBuf<int> nod(A->rows);
   DevBuf<double> B(A->rows * m);
   if (A->rows) {
     CF_CUDA(cudaMemcpyAsync(nod.p, node_of_dof, size_t(A->rows) * sizeof(int), cudaMemcpyDeviceToDevice, stream()));
     CF_CUDA(cudaMemcpyAsync(B.p, B0, size_t(A->rows) * m * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+    CF_CUDA(cudaMemcpyAsync(h->nod0.p, node_of_dof, size_t(A->rows) * sizeof(int), cudaMemcpyDeviceToDevice,
+                            stream()));
+    CF_CUDA(cudaMemcpyAsync(h->B0.p, B0, size_t(A->rows) * m * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
   }
   DevBuf<int> err(1);
   PhaseClock clk;
@@ -1311,13 +1318,56 @@ void Amg::vcycle(const double* r, double* x) const {
   }
 }
 
+// ------------------------------------------------------------------ input identity (reuse)
+namespace {
+__global__ void k_neq(i64 nwords, const unsigned* __restrict__ a, const unsigned* __restrict__ b, int* flag) {
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < nwords; i += i64(gridDim.x) * blockDim.x)
+    if (a[i] != b[i]) {
+      *flag = 1;
+      return;
+    }
+}
+}  // namespace
+
+bool bitwise_equal(const void* a, const void* b, size_t bytes) {
+  if (bytes == 0 || a == b) return true;
+  if (bytes % 4) fail(CF_ERR_LOGIC, "bitwise_equal: size must be a multiple of 4");
+  DevBuf<int> flag(1);
+  flag.zero();
+  const i64 nw = i64(bytes / 4);
+  k_neq<<<int(std::min<i64>(4096, (nw + 255) / 256)), 256, 0, stream()>>>(nw, static_cast<const unsigned*>(a),
+                                                                         static_cast<const unsigned*>(b), flag.p);
+  CF_LAUNCHED();
+  return read_dev(flag.p) == 0;
+}
+
+bool Amg::same_inputs(const Csr& A, const int* node_of_dof, const double* B, int m, const cf_amg_options& o) const {
+  if (!A0 || m != m0 || A.rows != A0->rows || A.cols != A0->cols || A.nnz != A0->nnz) return false;
+  if (o.strength_threshold != opts.strength_threshold || o.prolongation_omega != opts.prolongation_omega ||
+      o.jacobi_omega != opts.jacobi_omega || o.smoothing_sweeps != opts.smoothing_sweeps ||
+      o.coarse_size != opts.coarse_size || o.max_levels != opts.max_levels)
+    return false;
+  return bitwise_equal(A.ptr.p, A0->ptr.p, size_t(A.rows + 1) * sizeof(i64)) &&
+         bitwise_equal(A.col.p, A0->col.p, size_t(A.nnz) * sizeof(int)) &&
+         bitwise_equal(A.val.p, A0->val.p, size_t(A.nnz) * sizeof(double)) &&
+         bitwise_equal(node_of_dof, nod0.p, size_t(A.rows) * sizeof(int)) &&
+         bitwise_equal(B, B0.p, size_t(A.rows) * m * sizeof(double));
+}
+
 // ------------------------------------------------------------------ block preconditioner
 std::unique_ptr<BlockPrec> build_block_prec(const BlockSystem& J, int kind, const cf_amg_options& o,
-                                            const NullspaceDev* ns) {
+                                            const NullspaceDev* ns, const BlockPrec* prev) {
   auto p = std::make_unique<BlockPrec>();
   p->kind = kind;
   p->nu = J.nu;
   p->np = J.np;
+  if (kind == 1 && ns && prev && prev->kind == 1) {
+    if (prev->amg_u && prev->amg_u->same_inputs(*J.uu, ns->u_node, ns->u_modes, ns->m_u, o)) p->amg_u = prev->amg_u;
+    if (prev->amg_p && prev->amg_p->same_inputs(*J.pp, ns->p_node, ns->p_modes, 1, o)) p->amg_p = prev->amg_p;
+    if (!p->amg_u) p->amg_u = build_amg(J.uu, ns->u_node, ns->u_modes, ns->m_u, o);
+    if (!p->amg_p) p->amg_p = build_amg(J.pp, ns->p_node, ns->p_modes, 1, o);
+    return p;
+  }
   if (kind == 0) {  // exact: dense LU of each diagonal block (small systems only)
     p->lu_u = std::make_shared<DenseLu>();
     p->lu_p = std::make_shared<DenseLu>();

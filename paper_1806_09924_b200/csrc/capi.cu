@@ -2,7 +2,10 @@
 // host/device argument staging around the cfb:: implementation.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "cf_types.hpp"
 #include "cf_vec.hpp"
@@ -48,13 +51,68 @@ void ensure_device() {
                           "); there is no CPU fallback");
   CF_CUDA(cudaGetDevice(&r.device));
   CF_CUDA(cudaDeviceGetAttribute(&r.sm_count, cudaDevAttrMultiProcessorCount, r.device));
-  // keep freed stream-ordered allocations cached in the pool (per-Newton-iteration reallocation)
-  cudaMemPool_t pool;
-  CF_CUDA(cudaDeviceGetDefaultMemPool(&pool, r.device));
-  uint64_t thr = UINT64_MAX;
-  CF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   r.ready = true;
 }
+
+namespace {
+struct BlockCache {
+  std::multimap<size_t, void*> free_;
+  std::unordered_map<void*, size_t> size_of;
+  size_t cached = 0;
+  std::mutex mu;
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache;  // intentionally leaked: no teardown-order issues at exit
+  return *c;
+}
+size_t round_size(size_t b) {
+  if (b < (size_t(1) << 20)) return (b + 511) & ~size_t(511);
+  const size_t g = size_t(2) << 20;
+  return (b + g - 1) & ~(g - 1);
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+  ensure_device();
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  const size_t need = round_size(bytes);
+  auto it = c.free_.lower_bound(need);
+  if (it != c.free_.end() && it->first <= need + need / 4 + (size_t(1) << 20)) {
+    void* p = it->second;
+    c.cached -= it->first;
+    c.free_.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, need);
+  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+    cudaGetLastError();
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    for (auto& kv : c.free_) {
+      cudaFree(kv.second);
+      c.size_of.erase(kv.second);
+    }
+    c.free_.clear();
+    c.cached = 0;
+    e = cudaMalloc(&p, need);
+  }
+  CF_CUDA(e);
+  c.size_of[p] = need;
+  return p;
+}
+
+void dev_free(void* p, size_t) {
+  if (!p) return;
+  BlockCache& c = block_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.size_of.find(p);
+  if (it == c.size_of.end()) return;
+  c.free_.insert({it->second, p});
+  c.cached += it->second;
+}
+
+size_t dev_cached_bytes() { return block_cache().cached; }
 
 bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -114,7 +172,11 @@ int cf_device_info(int* device, int* sm_count, int64_t* total_mem) {
 }
 
 int cf_set_stream(void* s) {
-  return guard([&] { rt().stream = static_cast<cudaStream_t>(s); });
+  return guard([&] {
+    // cached blocks are reused in stream order: drain the old stream before switching
+    if (rt().ready && rt().stream != static_cast<cudaStream_t>(s)) CF_CUDA(cudaStreamSynchronize(rt().stream));
+    rt().stream = static_cast<cudaStream_t>(s);
+  });
 }
 
 int cf_synchronize(void) {

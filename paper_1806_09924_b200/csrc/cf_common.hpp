@@ -48,8 +48,14 @@ inline cudaStream_t stream() { return rt().stream; }
 inline void count_launch(i64 n = 1) { rt().launches += n; }
 #define CF_LAUNCHED() ::cfb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__), ::cfb::count_launch()
 
-// Stream-ordered device allocation (cudaMallocAsync on the library stream; the pool keeps
-// freed blocks cached, so per-Newton-iteration reallocations are cheap).
+// Caching device allocator: freed blocks are kept in a best-fit free list and reused in stream
+// order (all library work is ordered on one stream, so a block freed by an earlier operation is
+// safe to hand to a later one).  Per-Newton-iteration reallocation of multi-GB buffers (J, AMG
+// temporaries, Krylov basis) then costs nothing; cached blocks are released only on OOM.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+size_t dev_cached_bytes();
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -73,10 +79,10 @@ struct DevBuf {
   void alloc(i64 count) {
     release();
     n = count;
-    if (count > 0) CF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), size_t(count) * sizeof(T), stream()));
+    if (count > 0) p = static_cast<T*>(dev_alloc(size_t(count) * sizeof(T)));
   }
   void release() {
-    if (p) cudaFreeAsync(p, stream());
+    if (p) dev_free(p, size_t(n) * sizeof(T));
     p = nullptr;
     n = 0;
   }

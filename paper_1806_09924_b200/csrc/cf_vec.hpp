@@ -68,8 +68,15 @@ struct Amg {
   cf_amg_options opts{};
   i64 n = 0;
   std::shared_ptr<Csr> coarse_A;
+  // the build inputs, kept so an identical rebuild can be recognised bitwise and skipped
+  std::shared_ptr<Csr> A0;
+  DevBuf<int> nod0;
+  DevBuf<double> B0;
+  int m0 = 0;
   mutable DevBuf<double> cb, cx;  // coarsest rhs / solution
   void vcycle(const double* r, double* x) const;  // x = V(r), zero initial guess
+  // true iff build_amg(A, node_of_dof, B, m, opts) would rebuild exactly this hierarchy
+  bool same_inputs(const Csr& A, const int* node_of_dof, const double* B, int m, const cf_amg_options& o) const;
 };
 
 std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A, const int* node_of_dof, const double* B, int m,
@@ -93,8 +100,11 @@ struct NullspaceDev {  // NullspaceInfo on the device (linsolve.hpp:108-113)
   const double* p_modes = nullptr;  // n_phi x 1
 };
 
+// prev (optional): a previous preconditioner whose hierarchies are reused when their inputs are
+// bitwise identical (build_amg is deterministic, so the rebuilt hierarchy would be identical)
 std::unique_ptr<BlockPrec> build_block_prec(const BlockSystem& J, int kind, const cf_amg_options& o,
-                                            const NullspaceDev* ns);
+                                            const NullspaceDev* ns, const BlockPrec* prev = nullptr);
+bool bitwise_equal(const void* a, const void* b, size_t bytes);  // device arrays
 
 // ---- gmres.cu (linsolve.cpp:21-115)
 using DevOp = std::function<void(const double* in, double* out)>;

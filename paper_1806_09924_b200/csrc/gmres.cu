@@ -35,7 +35,25 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     return res;
   }
   const int mmax = std::max(1, std::min(o.restart, o.max_iter));
-  DevBuf<double> r(n), z(n), z2(n), V(n * (mmax + 1)), hd(mmax + 2), yd(mmax + 1);
+  // persistent workspace: the basis is GBs at the large configs, and re-allocating it every Newton
+  // iteration from a pool fragmented by the AMG setup costs far more than the solve itself
+  static struct Work {
+    i64 n = -1;
+    int m = -1;
+    DevBuf<double> r, z, z2, V, hd, yd;
+  } ws;
+  if (ws.n != n || ws.m < mmax) {
+    ws.V.release();
+    ws.r.alloc(n);
+    ws.z.alloc(n);
+    ws.z2.alloc(n);
+    ws.V.alloc(n * (mmax + 1));
+    ws.hd.alloc(mmax + 2);
+    ws.yd.alloc(mmax + 1);
+    ws.n = n;
+    ws.m = mmax;
+  }
+  DevBuf<double>&r = ws.r, &z = ws.z, &z2 = ws.z2, &V = ws.V, &hd = ws.hd, &yd = ws.yd;
   vcopy(r.p, rhs, n);
   std::vector<double> H, cs, sn, g, hcol(mmax + 2), y;
   auto apply_op = [&](const double* in, double* out) {

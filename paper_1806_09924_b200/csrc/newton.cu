@@ -357,8 +357,10 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
       ns.m_u = g.d == 2 ? 3 : 6;
       ns.p_node = pnode.p;
       ns.p_modes = Bp.p;
-      prec.reset();
-      prec = build_block_prec(*J, opts.prec_kind, opts.amg, &ns);
+      // hierarchies whose inputs are bitwise unchanged (M_uu within a load step: it depends only
+      // on phi_tilde and the Dirichlet set) are reused; a rebuild would be bit-identical
+      auto next = build_block_prec(*J, opts.prec_kind, opts.amg, &ns, prec.get());
+      prec = std::move(next);
     }
     GmresResult lin;
     {

@@ -34,6 +34,20 @@ for rep in range(2):
     torch.cuda.synchronize()
     print(f"prec build {1e3 * (time.perf_counter() - t):.2f} ms", flush=True)
 os.environ.pop("CF_TIMING", None)
+from torch.profiler import ProfilerActivity, profile
+rhs = -R
+for rep in range(2):
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        res = cf.gmres(J, rhs, prec=pre)
+        torch.cuda.synchronize()
+    wall = 1e3 * (time.perf_counter() - t)
+    ktot = sum((getattr(e, "device_time_total", 0) or 0) for e in prof.key_averages()) / 1e3
+    print(f"gmres its {res['iterations']} wall {wall:.1f} ms kernels {ktot:.1f} ms", flush=True)
+    if rep == 1:
+        for e in sorted(prof.key_averages(), key=lambda e: -(getattr(e, "device_time_total", 0) or 0))[:12]:
+            print(f"   {e.device_time_total / 1e3:8.2f} ms {e.count:6d} {e.key[:90]}")
 r = torch.randn(P.n_total, dtype=torch.float64, device="cuda")
 for name, f in (("block_apply", lambda: J.apply(r)), ("prec_apply", lambda: pre.apply(r))):
     f()
