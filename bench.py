@@ -254,6 +254,10 @@ def operator_leg(cf, device, stream, applies=20):
     ok = bool(torch.equal(yh.to(device), y))
     peak, src = peak_hbm()
     gbs = nb / (ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01_spmv_cfg1_ncu.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("traffic_bytes")
     res = {"workload": "config1: M_uu apply, 3d 192^3 Q1, 21,567,171 u dofs, 1,676,188,257 nnz, CSR",
            "value": gbs, "unit": "GB/s", "ms_per_apply": ms, "bytes_per_apply": nb, "frac_of_hbm_peak": gbs / peak,
            "e2e": {"value": nb / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_apply": e2e_ms,
@@ -262,7 +266,8 @@ def operator_leg(cf, device, stream, applies=20):
     del J, u, y
     torch.cuda.empty_cache()
     return res, {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
-                 "traffic": None, "kernel": "k_spmv_b<16,4> (CSR SpMV, M_uu of config 1)", "bytes_per_launch": nb,
+                 "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
+                 "kernel": "k_spmv_b<16,4> (CSR SpMV, M_uu of config 1)", "bytes_per_launch": nb,
                  "ms_per_launch": ms, "peak_source": src}
 
 
