@@ -178,6 +178,13 @@ typedef struct {
 int cf_gmres(cf_block J, cf_csr A, cf_prec P, cf_amg M, const double* rhs, const cf_gmres_options* opts, double* x,
              cf_gmres_result* result, double* history, int history_cap);
 
+/* ------------------------------------------------------------------ functionals */
+/* compute_tcv (postproc.cpp:12-28): signed TCV of a solution (length n_total). */
+int cf_compute_tcv(cf_problem p, const double* solution, double* tcv);
+/* compute_cod, CodMethod::line_integral (postproc.cpp:38-99): openings at strictly increasing
+ * stations (host arrays). */
+int cf_compute_cod(cf_problem p, const double* solution, const double* stations, int n_stations, double* openings);
+
 /* ------------------------------------------------------------------ Newton / active set */
 typedef struct cf_state_s* cf_state; /* FractureState (model.hpp:50-55), device resident */
 typedef struct {

@@ -426,6 +426,29 @@ def gmres(op, rhs, prec=None, opts: GmresOptions | None = None):
                 residual=res.residual, residual_history=hist[:res.iterations].copy())
 
 
+# ---------------------------------------------------------------------------- functionals
+def compute_tcv(prob: Problem, solution) -> float:
+    """postproc.cpp:12-28: signed total crack volume."""
+    x = _as_f64(solution)
+    out = C.c_double()
+    check(load().cf_compute_tcv(prob._h, _ptr(x), C.byref(out)))
+    return out.value
+
+
+def default_cod_stations():
+    """postproc.cpp:30-34: -1.5 .. 1.5 step 0.05 (61 stations)."""
+    return [0.05 * i for i in range(-30, 31)]
+
+
+def compute_cod(prob: Problem, solution, stations) -> np.ndarray:
+    """postproc.cpp:70-99 (line-integral method): crack opening at each station."""
+    x = _as_f64(solution)
+    st = np.ascontiguousarray(stations, dtype=np.float64)
+    out = np.zeros(len(st))
+    check(load().cf_compute_cod(prob._h, _ptr(x), _ptr(st), len(st), _ptr(out)))
+    return out
+
+
 # ---------------------------------------------------------------------------- Newton / active set
 def slit_band_edge(prob: Problem, mat: Material) -> float:
     out = C.c_double()

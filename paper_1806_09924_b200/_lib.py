@@ -127,6 +127,8 @@ SIGNATURES = [
     ("cf_prec_destroy", _I, [_P]),
     ("cf_rigid_body_modes", _I, [_P, _P, _P]),
     ("cf_gmres", _I, [_P, _P, _P, _P, _P, C.POINTER(GmresOptions), _P, _P, _P, _I]),
+    ("cf_compute_tcv", _I, [_P, _P, C.POINTER(_D)]),
+    ("cf_compute_cod", _I, [_P, _P, _P, _I, _P]),
     ("cf_slit_band_edge", _I, [_P, C.POINTER(Material), C.POINTER(_D)]),
     ("cf_resolve_regularization", _I, [_P, C.POINTER(Material), _D, C.POINTER(Regularization)]),
     ("cf_initial_crack", _I, [_P, C.POINTER(Material), _D, _P, C.POINTER(_D)]),

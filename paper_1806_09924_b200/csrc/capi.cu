@@ -588,6 +588,24 @@ int cf_gmres(cf_block J, cf_csr A, cf_prec P, cf_amg M, const double* rhs, const
   });
 }
 
+// ------------------------------------------------------------------ functionals
+int cf_compute_tcv(cf_problem p, const double* solution, double* tcv) {
+  return guard([&] {
+    CHECK_ARG(p && solution && tcv, "cf_compute_tcv: null argument");
+    InArg<double> x(solution, p->p->g.n_total());
+    *tcv = compute_tcv(*p->p, x.dev);
+  });
+}
+
+int cf_compute_cod(cf_problem p, const double* solution, const double* stations, int n_stations, double* openings) {
+  return guard([&] {
+    CHECK_ARG(p && solution && (n_stations == 0 || (stations && openings)) && n_stations >= 0,
+              "cf_compute_cod: bad argument");
+    InArg<double> x(solution, p->p->g.n_total());
+    compute_cod(*p->p, x.dev, stations, n_stations, openings);
+  });
+}
+
 // ------------------------------------------------------------------ Newton
 int cf_slit_band_edge(cf_problem p, const cf_material* mat, double* edge) {
   return guard([&] {

@@ -117,6 +117,10 @@ struct GmresResult {
 GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
                   double* x);
 
+// ---- postproc.cu (postproc.cpp:12-99)
+double compute_tcv(const Problem& P, const double* sol);
+void compute_cod(const Problem& P, const double* sol, const double* stations_host, int ns, double* out_host);
+
 // ---- newton.cu (solver.cpp:24-204)
 struct State {  // FractureState (model.hpp:50-55), device resident
   DevBuf<double> solution, phi_old, phi_prev2;

@@ -239,11 +239,44 @@ def test_loading_sequence_three_steps(cf, orc):  # solver.cpp:190-204, config 2 
 
 
 def test_config0_newton_parity(cf, orc):
-    """BASELINE config 0 (2d 256^2, eps = 2h, kappa = 1e-12): full Newton step vs the oracle."""
+    """BASELINE config 0 (2d 256^2, eps = 2h, kappa = 1e-12): full Newton step vs the oracle,
+    then TCV and COD on the 64 stations x = -1.575 + 0.05 i computed on the device."""
     P, O, mat, omat, reg, oreg, phi = _sneddon_pair(cf, orc, d=2, K=10.0, n0=8, r=5, fixed=True)
     assert P.n_total == 198147
     reps, x, oreps, xo = _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi)
     _same_transcript(reps[0], oreps[0])
     assert np.array_equal(x, xo)
     st = -1.575 + 0.05 * np.arange(64)
-    assert np.array_equal(O.cod(x, st), O.cod(xo, st))
+    cod, codo = cf.compute_cod(P, x, st), O.cod(xo, st)
+    assert np.allclose(cod, codo, rtol=1e-12, atol=1e-18)
+    tcv, tcvo = cf.compute_tcv(P, x), O.tcv(xo)
+    assert abs(tcv - tcvo) <= 1e-12 * abs(tcvo)
+    exact = 2 * math.pi * 1e-3 * (1 - 0.2 ** 2)  # PAPER.md:321, 6.0319e-3
+    assert 0.8 * exact < abs(tcv) < 1.2 * exact
+    assert 1.6e-3 < cod[np.argmin(np.abs(st))] < 2.1e-3  # COD(0) ~ 1.92e-3 (SPEC.md:510)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_functionals_random_fields(cf, orc, d):  # postproc_test.cpp:35-105
+    rng = np.random.default_rng(31 + d)
+    P, O = cf.Problem(d, 2.0, 4, 1), orc.Problem(d, 2.0, 4, 1)
+    x = rng.uniform(-1, 1, P.n_total)
+    assert abs(cf.compute_tcv(P, x) - O.tcv(x)) <= 1e-12 * max(1.0, abs(O.tcv(x)))
+    st = np.array([-2.0, -1.3, -0.25, 0.0, 0.6, 1.9, 2.0])
+    assert np.allclose(cf.compute_cod(P, x, st), O.cod(x, st), rtol=1e-12, atol=1e-14)
+    flat = x.copy()
+    flat[P.n_u:] = 0.7  # constant phi: zero TCV and zero profile
+    assert abs(cf.compute_tcv(P, flat)) <= 1e-13 and np.abs(cf.compute_cod(P, flat, st)).max() <= 1e-13
+    with pytest.raises(ValueError, match="strictly increasing"):
+        cf.compute_cod(P, x, [0.0, 0.0])
+    with pytest.raises(ValueError, match="outside"):
+        cf.compute_cod(P, x, [-3.0, 0.0])
+
+
+def test_3d_penny_newton_bit_exact(cf, orc):
+    """3d penny crack (config 3 physics) on 16^3: full Newton step vs the oracle."""
+    P, O, mat, omat, reg, oreg, phi = _sneddon_pair(cf, orc, d=3, K=10.0, n0=8, r=1, fixed=True)
+    reps, x, oreps, xo = _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi)
+    _same_transcript(reps[0], oreps[0])
+    assert np.array_equal(x, xo)
+    assert reps[0]["converged"] and reps[0]["feasibility_violation"] <= 1e-10

@@ -449,7 +449,7 @@ def _sneddon(orc, d=2, K=5.0, n0=10, r=2, fixed=False):
 
 
 def test_sneddon_feasibility_and_opening(orc):  # solver_test.cpp:112-150 (uniform mesh)
-    P, m, reg, sol, po, pp = _sneddon(orc)
+    P, m, reg, sol, po, pp = _sneddon(orc, r=1)
     rep = P.newton_step(m, reg, orc.solver_options(prec_kind=0), sol, po, pp, 1)
     assert rep["converged"] and rep["feasibility"] <= 1e-10
     assert rep["iterations"][-1, 2] == 0
@@ -466,7 +466,7 @@ def test_sneddon_feasibility_and_opening(orc):  # solver_test.cpp:112-150 (unifo
 def test_newton_determinism_and_amg_vs_exact(orc):  # solver_test.cpp:178-210
     runs = []
     for kind in (1, 1, 0):
-        P, m, reg, sol, po, pp = _sneddon(orc)
+        P, m, reg, sol, po, pp = _sneddon(orc, r=1)
         rep = P.newton_step(m, reg, orc.solver_options(prec_kind=kind), sol, po, pp, 1)
         assert rep["converged"]
         runs.append((rep, sol))
