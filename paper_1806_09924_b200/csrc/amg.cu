@@ -399,6 +399,13 @@ __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restric
   if (node >= nn) return;
   const int i = int(node);
   if (mode == 1 && ovf[i]) return;
+  if (sp[i + 1] == sp[i] && tp[i + 1] == tp[i]) {  // isolated node: N2(i) is empty
+    if (mode == 0 && lane == 0) {
+      lower[i] = 0;
+      upcnt[i] = 0;
+    }
+    return;
+  }
   int* T = tab[w];
   for (int s = lane; s < N2CAP; s += 32) T[s] = -1;
   if (lane == 0) cnt[w] = 0;
@@ -545,6 +552,9 @@ __global__ void k_lfmis(const i64* __restrict__ up_ptr, const int* __restrict__ 
       const int st = *((volatile int*)&status[v]);
       for (i64 k = up_ptr[v]; k < up_ptr[v + 1]; ++k) {
         const int i = up[k];
+        // a decided dependent needs no message: its status is final (a pending count is only
+        // consulted while the node is undecided), so skip the atomic after a plain read
+        if (*((volatile int*)&status[i]) != UND) continue;
         if (st == ROOT) {
           if (atomicCAS(&status[i], UND, NOTROOT) == UND) G[atomicAdd(nxt, 1)] = i;
         } else {
@@ -1156,6 +1166,8 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
       CF_LAUNCHED();
     }
     clk.mark("lfmis");
+    if (clk.on) std::fprintf(stderr, "[amg L%d] nodes %lld strong edges %lld lfmis rounds %d\n", lev,
+                             (long long)n_nodes, (long long)ns, read_dev(rounds.p));
     // aggregate ids of the roots (ascending), claims
     DevBuf<int> rootid(n_nodes + 1), agg1(n_nodes);
     k_root_flags<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, status.p, rootid.p);

@@ -68,8 +68,17 @@ __global__ void k_row_bound(i64 rows, const i64* __restrict__ ap, const int* __r
 }
 
 __global__ void k_max_row(i64 rows, const i64* __restrict__ p, unsigned long long* __restrict__ mx) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < rows) atomicMax(mx, (unsigned long long)(p[i + 1] - p[i]));
+  __shared__ unsigned long long sm[256];
+  unsigned long long m = 0;
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += i64(gridDim.x) * blockDim.x)
+    m = max(m, (unsigned long long)(p[i + 1] - p[i]));
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] = max(sm[threadIdx.x], sm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(mx, sm[0]);  // one atomic per block
 }
 
 template <int WPB>
@@ -544,7 +553,7 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   {
     DevBuf<unsigned long long> mx(1);
     mx.zero();
-    k_max_row<<<grid_for(B.rows, 256), 256, 0, stream()>>>(B.rows, B.ptr.p, mx.p);
+    k_max_row<<<int(std::min<i64>(1024, grid_for(B.rows, 256))), 256, 0, stream()>>>(B.rows, B.ptr.p, mx.p);
     CF_LAUNCHED();
     unsigned long long h = 0;
     CF_CUDA(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, stream()));
