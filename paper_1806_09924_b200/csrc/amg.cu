@@ -547,10 +547,14 @@ __global__ void k_lfmis(const i64* __restrict__ up_ptr, const int* __restrict__ 
     if (nf == 0) break;
     if (g.thread_rank() == 0) sizes[(r + 2) % 3] = 0;
     int* nxt = &sizes[(r + 1) % 3];
-    for (long long t = g.thread_rank(); t < nf; t += g.size()) {
+    // one warp per frontier node, lanes over its dependents: a node's ~100 dependents would
+    // otherwise be a serial chain of returning atomics on one thread (the round's critical path)
+    const long long nwarps = g.size() / 32;
+    const int lane = threadIdx.x & 31;
+    for (long long t = g.thread_rank() / 32; t < nf; t += nwarps) {
       const int v = F[t];
       const int st = *((volatile int*)&status[v]);
-      for (i64 k = up_ptr[v]; k < up_ptr[v + 1]; ++k) {
+      for (i64 k = up_ptr[v] + lane; k < up_ptr[v + 1]; k += 32) {
         const int i = up[k];
         // a decided dependent needs no message: its status is final (a pending count is only
         // consulted while the node is undecided), so skip the atomic after a plain read
