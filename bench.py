@@ -271,6 +271,30 @@ def operator_leg(cf, device, stream, applies=20):
                  "ms_per_launch": ms, "peak_source": src}
 
 
+def rebuild_probe():
+    """One warm config-3 step with CF_NO_AMG_REUSE=1 (every hierarchy rebuilt every iteration)."""
+    import torch
+    import paper_1806_09924_b200 as cf
+    s = torch.cuda.current_stream()
+    cf.set_stream(s)
+    P, mat, reg = sneddon_setup(cf, CFG3)
+    st0 = cf.make_initial_state(P, mat).get()
+    sol0 = torch.from_numpy(st0["solution"]).cuda()
+    po0 = torch.from_numpy(st0["phi_old"]).cuda()
+    cf.newton_active_set_step(cf.FractureState(P, sol0, po0, po0, 1), mat, P, reg, cf.SolverOptions())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    rep = cf.newton_active_set_step(cf.FractureState(P, sol0, po0, po0, 1), mat, P, reg, cf.SolverOptions())
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    its = len(rep["iterations"])
+    print(json.dumps({"value": P.n_total * its / (ms * 1e-3), "unit": "DoF/s", "ms_per_step": ms,
+                      "newton_iterations": its, "note": "CF_NO_AMG_REUSE=1: u- and phi-hierarchies rebuilt "
+                      "every Newton iteration, as the reference does; identical iterates"}))
+
+
 def ours(args):
     import torch
     rank, world, local = dist_setup()
@@ -329,6 +353,18 @@ def ours(args):
            "path": "cf_state_create(host) + cf_newton_active_set_step + cf_state_get(host)",
            "newton_iterations": len(rep_h["iterations"]), "solution_finite": bool(np.isfinite(x_h).all())}
 
+    # the same step with every AMG hierarchy rebuilt (no bitwise-verified reuse), in a subprocess
+    # because the switch is read once per process
+    full = None
+    if rank == 0 and world == 1 and not args.no_rebuild_check:
+        try:
+            env = dict(os.environ, CF_NO_AMG_REUSE="1")
+            r = subprocess.run([sys.executable, __file__, "--rebuild-probe"], env=env, capture_output=True,
+                               text=True, timeout=600)
+            full = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as ex:  # reported, never fatal
+            full = {"error": str(ex)[:200]}
+
     if rank != 0:
         return
     op, roof = operator_leg(cf, device, s) if not args.no_operator else (None, None)
@@ -342,6 +378,7 @@ def ours(args):
         "active_set_final": last["iterations"][-1]["active_size"],
         "phase_ms_last_step": last["times_ms"], "device_mem_used_gb": (total - free) / 1e9,
         "roofline": roof, "operator": op, "e2e": e2e, "gpu_launches": int(launches),
+        "full_rebuild": full,
         "gpu_launches_per_step": launches / args.steps, "clocks": clk.summary(),
     }
     if not args.no_cpu and world == 1:
@@ -357,8 +394,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-operator", action="store_true")
+    ap.add_argument("--no-rebuild-check", action="store_true")
+    ap.add_argument("--rebuild-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.rebuild_probe:
+        rebuild_probe()
+        return
     if args.impl == "reference":
         reference_arm(args)
     else:

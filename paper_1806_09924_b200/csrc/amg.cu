@@ -1377,7 +1377,8 @@ std::unique_ptr<BlockPrec> build_block_prec(const BlockSystem& J, int kind, cons
   p->kind = kind;
   p->nu = J.nu;
   p->np = J.np;
-  if (kind == 1 && ns && prev && prev->kind == 1) {
+  static const bool no_reuse = std::getenv("CF_NO_AMG_REUSE") != nullptr;  // rebuild every hierarchy
+  if (kind == 1 && ns && prev && prev->kind == 1 && !no_reuse) {
     if (prev->amg_u && prev->amg_u->same_inputs(*J.uu, ns->u_node, ns->u_modes, ns->m_u, o)) p->amg_u = prev->amg_u;
     if (prev->amg_p && prev->amg_p->same_inputs(*J.pp, ns->p_node, ns->p_modes, 1, o)) p->amg_p = prev->amg_p;
     if (!p->amg_u) p->amg_u = build_amg(J.uu, ns->u_node, ns->u_modes, ns->m_u, o);

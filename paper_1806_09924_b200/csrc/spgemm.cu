@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(WPB * 32) k_sym(const int* __restrict__ rowlis
                                                   int* __restrict__ ccol) {
   constexpr int G = 32 / L;
   __shared__ int tab[WPB][CAP];
-  __shared__ int buf[MODE ? WPB : 1][MODE ? CAP : 1];
+  __shared__ int buf[MODE == 1 ? WPB : 1][MODE == 1 ? CAP : 1];
   __shared__ int nuniq[WPB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const i64 r = i64(blockIdx.x) * WPB + w;
@@ -140,10 +140,21 @@ __global__ void __launch_bounds__(WPB * 32) k_sym(const int* __restrict__ rowlis
   for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
   __syncwarp();
   if (full || mine > (CAP * 3) / 4) {
-    if (MODE == 0 && lane == 0) cnt[i] = -1;
+    if (MODE != 1 && lane == 0) cnt[i] = -1;  // overflow: retried by the next tier
     return;
   }
   if (MODE == 0) {
+    if (lane == 0) cnt[i] = mine;
+    return;
+  }
+  if (MODE == 2) {  // count + spill the unsorted unique columns to scratch (ccol at cptr[i])
+    if (lane == 0) nuniq[w] = 0;
+    __syncwarp();
+    const i64 base = cptr[i];
+    for (int s = lane; s < CAP; s += 32) {
+      const int key = T[s];
+      if (key != EMPTY) ccol[base + atomicAdd(&nuniq[w], 1)] = key;
+    }
     if (lane == 0) cnt[i] = mine;
     return;
   }
@@ -162,6 +173,37 @@ __global__ void __launch_bounds__(WPB * 32) k_sym(const int* __restrict__ rowlis
   bitonic_warp<WPB>(Bf, n2, lane);
   const i64 base = cptr[i];
   for (int t = lane; t < mine; t += 32) ccol[base + t] = Bf[t];
+}
+
+// sort each row's spilled columns (scratch at soff[i], length cnt) into the CSR (warp per row)
+template <int CAP, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_sort_rows(const int* __restrict__ rowlist, i64 nrows,
+                                                        const i64* __restrict__ soff, const int* __restrict__ scratch,
+                                                        const i64* __restrict__ cptr, int* __restrict__ ccol) {
+  __shared__ int Bf[WPB][CAP];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 r = i64(blockIdx.x) * WPB + w;
+  if (r >= nrows) return;
+  const i64 i = rowlist ? rowlist[r] : r;
+  const i64 c0 = cptr[i];
+  const int n = int(cptr[i + 1] - c0);
+  const int* src = scratch + soff[i];
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  for (int t = lane; t < n2; t += 32) Bf[w][t] = t < n ? src[t] : INT_MAX;
+  __syncwarp();
+  bitonic_warp<WPB>(Bf[w], n2, lane);
+  for (int t = lane; t < n; t += 32) ccol[c0 + t] = Bf[w][t];
+}
+
+__global__ void k_scatter_len(const int* __restrict__ list, int n, const i64* __restrict__ len, i64* __restrict__ out) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) out[list[t]] = len[list[t]];
+}
+
+__global__ void k_spill_cap(i64 m, const i64* __restrict__ ub, i64 cap, i64* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = ub[i] < cap ? ub[i] : cap;
 }
 
 // --- symbolic, CTA per row (rows beyond the warp tiers) -----------------------------------
@@ -562,14 +604,36 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   }
   const int L = lanes_for(maxb);
   i64* cnt = C->ptr.p;  // row counts in place, scanned into offsets afterwards
-  // 1. symbolic count: all rows with products try the 512-slot tier, overflow -> 2048 -> CTA
+  // 1. symbolic count: all rows with products try the 512-slot tier, which also spills its
+  //    unsorted unique columns (<= 384 per row) to scratch; overflow -> 2048 -> CTA tiers
+  DevBuf<i64> soff(m + 1);
+  DevBuf<int> spill;
+  RowBin spilled;
+  RowBin o1;
   {
     DevBuf<i64> ub(m);
     k_row_bound<<<grid_for(m, 256), 256, 0, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, ub.p);
     CF_LAUNCHED();
+    k_spill_cap<<<grid_for(m, 256), 256, 0, stream()>>>(m, ub.p, 384, soff.p);
+    CF_LAUNCHED();
+    CF_CUDA(cudaMemsetAsync(soff.p + m, 0, sizeof(i64), stream()));
+    scan_excl(soff.p, m + 1);
+    spill.alloc(std::max<i64>(1, read_i64(soff.p + m)));
     RowBin all = make_bin(m, ub.p, 0, LLONG_MAX);
-    sym_dispatch(L, 0, all, 512, A, B, cnt, nullptr);
-    RowBin o1 = overflow_of(all, cnt);
+    if (all.n) {
+      if (L == 8)
+        k_sym<512, 8, 8, 2><<<grid_for(all.n, 8), 256, 0, stream()>>>(all.list.p, all.n, A.ptr.p, A.col.p, B.ptr.p,
+                                                                      B.col.p, cnt, soff.p, spill.p);
+      else if (L == 16)
+        k_sym<512, 16, 8, 2><<<grid_for(all.n, 8), 256, 0, stream()>>>(all.list.p, all.n, A.ptr.p, A.col.p,
+                                                                       B.ptr.p, B.col.p, cnt, soff.p, spill.p);
+      else
+        k_sym<512, 32, 8, 2><<<grid_for(all.n, 8), 256, 0, stream()>>>(all.list.p, all.n, A.ptr.p, A.col.p,
+                                                                       B.ptr.p, B.col.p, cnt, soff.p, spill.p);
+      CF_LAUNCHED();
+    }
+    o1 = overflow_of(all, cnt);
+    spilled = make_bin(m, cnt, 0, LLONG_MAX);  // rows fully handled by the spill tier (cnt >= 1)
     sym_dispatch(L, 0, o1, 2048, A, B, cnt, nullptr);
     RowBin o2 = overflow_of(o1, cnt);
     if (o2.n) {
@@ -594,9 +658,26 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   RowBin f1 = make_bin(m, len.p, 0, 256);
   RowBin f2 = make_bin(m, len.p, 256, 1024);
   RowBin f3 = make_bin(m, len.p, 1024, LLONG_MAX);
-  sym_dispatch(L, 1, f1, 512, A, B, nullptr, C.get());
-  sym_dispatch(L, 1, f2, 2048, A, B, nullptr, C.get());
-  if (f3.n) {
+  // spilled rows: sort their scratch columns; overflow rows: hash again in the 2048/CTA tiers
+  if (spilled.n) {
+    k_sort_rows<512, 8><<<grid_for(spilled.n, 8), 256, 0, stream()>>>(spilled.list.p, spilled.n, soff.p, spill.p,
+                                                                       C->ptr.p, C->col.p);
+    CF_LAUNCHED();
+  }
+  spill.release();
+  RowBin g2, g3;
+  {
+    // overflow rows split by exact length (they are > 384 columns)
+    DevBuf<i64> olen(m);
+    CF_CUDA(cudaMemsetAsync(olen.p, 0, size_t(m) * sizeof(i64), stream()));
+    k_scatter_len<<<grid_for(o1.n, 256), 256, 0, stream()>>>(o1.list.p, o1.n, len.p, olen.p);
+    CF_LAUNCHED();
+    g2 = make_bin(m, olen.p, 0, 1024);
+    g3 = make_bin(m, olen.p, 1024, LLONG_MAX);
+  }
+  sym_dispatch(L, 1, g2, 2048, A, B, nullptr, C.get());
+  if (g3.n) {
+    RowBin& f3 = g3;
     DevBuf<int> flag(1);
     flag.zero();
     const size_t sm = size_t(2) * SYM_BIG * sizeof(int);

@@ -60,6 +60,31 @@ def test_amg_scalar_chain_and_diag(cf, orc):  # linsolve_test.cpp:265-300
     assert res["converged"] and res["iterations"] <= 25
 
 
+def _random_graph_spd(n, deg, seed):
+    rng = np.random.default_rng(seed)
+    rows = np.repeat(np.arange(n), deg)
+    cols = rng.integers(0, n, n * deg)
+    vals = -rng.uniform(0.5, 1.0, n * deg)
+    S = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    S = S + S.T
+    S.setdiag(0.0)
+    S.eliminate_zeros()
+    d = np.asarray(abs(S).sum(axis=1)).ravel() + 1.0
+    return (S + sp.diags(d)).tocsr()
+
+
+def test_amg_high_degree_tiers_bit_exact(cf, orc):
+    """Random graph (~80 neighbours per row, a fully dense 2752^2 coarse level): strength/N2 overflow
+    tiers and SpGEMM rows beyond the 384- and 1024-column tiers must still reproduce the oracle's
+    hierarchy bit for bit."""
+    A = _random_graph_spd(4000, 40, 5)
+    h = cf.build_amg(cf.CsrMatrix.from_scipy(A))
+    ho = orc.Amg(orc.Csr.from_scipy(A))
+    _assert_amg_equal(h, ho)
+    r = np.random.default_rng(2).uniform(-1, 1, A.shape[0])
+    assert np.array_equal(h.v_cycle(r), ho.vcycle(r))
+
+
 def _q1_laplacian(nv):
     pts = [0.5 * (-1 / math.sqrt(3) + 1), 0.5 * (1 / math.sqrt(3) + 1)]
     local = np.zeros((4, 4))
