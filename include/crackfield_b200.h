@@ -34,6 +34,7 @@ extern "C" {
 #define CF_ERR_CUDA 4             /* CUDA runtime / no device */
 #define CF_ERR_OUT_OF_MEMORY 5
 #define CF_ERR_UNSUPPORTED 6
+#define CF_ERR_COMM 7             /* NCCL (multi-GPU communicator) */
 
 /* Material (model.hpp:14-30). eps_mode: 0 tied, 1 fixed; pressure_coupling: 0 extrapolated, 1 current. */
 typedef struct {
@@ -111,7 +112,26 @@ int cf_assemble_residual(cf_problem p, cf_constraints c, const cf_material* mat,
 int cf_assemble_jacobian(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
                          const double* solution, const double* phi_tilde, cf_block* out);
 
+/* Slab decomposition (no reference counterpart: the reference is single-threaded).
+ * A slab owns vertex planes [p_lo, p_hi) along the slowest axis (z in 3d, y in 2d) = a
+ * contiguous vertex range.  Its residual rows come back in the local layout
+ * [u_own (d*nv) | phi_own (nv)]; its Jacobian rows are the owned rows with columns numbered
+ * over the owned + one ghost plane each side ("ext" layout [u_ext (d*ne) | phi_ext (ne)]).
+ * x / phi_tilde are global-length and must be valid on the ext planes.  The full slab
+ * [0, n_planes) reproduces cf_assemble_residual / cf_assemble_jacobian exactly. */
+int cf_assemble_residual_planes(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                                const double* solution, const double* phi_tilde, int64_t p_lo, int64_t p_hi,
+                                double* R);
+int cf_assemble_jacobian_planes(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                                const double* solution, const double* phi_tilde, int64_t p_lo, int64_t p_hi,
+                                cf_block* out);
+/* The slab of rank `rank` of `size` (planes split evenly): {v_lo, v_hi, ve_lo, ve_hi, c_lo, c_hi,
+ * vertices per plane}. */
+int cf_slab_info(cf_problem p, int rank, int size, int64_t info[7]);
+
 /* ------------------------------------------------------------------ block system */
+/* {n_u rows, n_phi rows, n_u input columns, n_phi input columns} (inputs > rows for a slab). */
+int cf_block_shape(cf_block b, int64_t shape[4]);
 /* Sizes: n_u, n_phi and nnz of M_uu, M_phiu, M_phiphi (linsolve.hpp:17-28). */
 int cf_block_info(cf_block b, int64_t* n_u, int64_t* n_phi, int64_t* nnz3);
 /* Copy one block out as CSR (which: 0 M_uu, 1 M_phiu, 2 M_phiphi). */
@@ -214,6 +234,28 @@ int cf_newton_active_set_step(cf_problem p, cf_state s, const cf_material* mat, 
 int cf_solve_loading_sequence(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
                               const cf_solver_options* opts, int n_steps, cf_newton_iteration* its, int max_its,
                               int* n_its, int* converged, double* feasibility, int* steps_done);
+
+/* ------------------------------------------------------------------ multi-GPU
+ * One process per GPU.  Rank 0 makes an id, the launcher broadcasts it (e.g. over
+ * torch.distributed), every rank creates its communicator on its current CUDA device.  The _comm
+ * variants run the slab-decomposed step: rank r owns the planes of cf_slab_info(r, size); halo
+ * planes move by NCCL send/recv, every dot / norm is a rank-ordered sum (bitwise identical on
+ * all ranks), the preconditioner is block-Jacobi over the slabs (each rank's AMG on its diagonal
+ * block).  The state is global-length on every rank and holds the full solution on return.
+ * size == 1 is the single-GPU step exactly. */
+typedef struct cf_comm_s* cf_comm;
+int cf_comm_unique_id(uint8_t id[128]);
+int cf_comm_create(const uint8_t id[128], int rank, int size, cf_comm* out);
+int cf_comm_info(cf_comm c, int* rank, int* size);
+int cf_comm_destroy(cf_comm c);
+int cf_newton_active_set_step_comm(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, cf_comm comm, cf_newton_iteration* its,
+                                   int max_its, int* n_its, int* converged, double* feasibility,
+                                   cf_phase_times* times);
+int cf_solve_loading_sequence_comm(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, cf_comm comm, int n_steps,
+                                   cf_newton_iteration* its, int max_its, int* n_its, int* converged,
+                                   double* feasibility, int* steps_done);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,9 @@ class Problem:
         self.n_u, self.n_phi = dim * self.n_vertices, self.n_vertices
         self.n_total = self.n_u + self.n_phi
         self.nodes_per_side = (n0 << refinements) + 1
+        # vertex planes along the slowest axis (z in 3d, y in 2d): the slab decomposition unit
+        self.n_planes = self.nodes_per_side
+        self.plane = self.nodes_per_side ** (dim - 1)
 
     def __del__(self):
         try:
@@ -177,6 +180,9 @@ class BlockSystem:
         check(load().cf_block_info(self._h, C.byref(nu), C.byref(np_), nnz))
         self._n_u, self._n_phi = nu.value, np_.value
         self.nnz = tuple(int(v) for v in nnz)
+        shape = (C.c_int64 * 4)()
+        check(load().cf_block_shape(self._h, shape))
+        self._in_u, self._in_phi = int(shape[2]), int(shape[3])  # > rows for a slab (ghost planes)
 
     def __del__(self):
         try:
@@ -192,6 +198,10 @@ class BlockSystem:
 
     def n_total(self):
         return self._n_u + self._n_phi
+
+    def n_in(self):
+        """Input length of apply: n_total, or the ext layout [u_ext | phi_ext] of a slab."""
+        return self._in_u + self._in_phi
 
     def apply(self, x, out=None):
         """BlockSystem::apply (linsolve.cpp:13-19)."""
@@ -209,7 +219,7 @@ class BlockSystem:
 
     def csr(self, which: int) -> Csr:
         rows = self._n_u if which == 0 else self._n_phi
-        cols = self._n_phi if which == 2 else self._n_u
+        cols = self._in_phi if which == 2 else self._in_u
         nnz = self.nnz[which]
         ptr = np.empty(rows + 1, dtype=np.int64)
         col = np.empty(nnz, dtype=np.int32)
@@ -231,23 +241,81 @@ class BlockSystem:
 
 
 def assemble_residual(prob: Problem, constraints: ConstraintSet, mat: Material, reg: Regularization, solution,
-                      phi_tilde, out=None):
-    """model.hpp:62-64: residual (F_u, F_phi), condensed (constrained entries 0)."""
+                      phi_tilde, out=None, planes=None):
+    """model.hpp:62-64: residual (F_u, F_phi), condensed (constrained entries 0).
+
+    planes=(p_lo, p_hi): only the rows of the vertex planes [p_lo, p_hi) along the slowest axis
+    (a slab), in the local layout [u_own | phi_own]."""
     x, pt = _as_f64(solution), _as_f64(phi_tilde)
-    R = out if out is not None else _empty_like_kind(x, prob.n_total)
-    check(load().cf_assemble_residual(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(x), _ptr(pt),
-                                      _ptr(R)))
+    if planes is None:
+        R = out if out is not None else _empty_like_kind(x, prob.n_total)
+        check(load().cf_assemble_residual(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(x), _ptr(pt),
+                                          _ptr(R)))
+        return R
+    nv = (planes[1] - planes[0]) * prob.plane
+    R = out if out is not None else _empty_like_kind(x, (prob.dim + 1) * nv)
+    check(load().cf_assemble_residual_planes(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(x),
+                                             _ptr(pt), int(planes[0]), int(planes[1]), _ptr(R)))
     return R
 
 
 def assemble_jacobian(prob: Problem, constraints: ConstraintSet, mat: Material, reg: Regularization, solution,
-                      phi_tilde) -> BlockSystem:
-    """model.hpp:68-70: exact Gateaux derivative with phi_tilde frozen (M_uphi = 0)."""
+                      phi_tilde, planes=None) -> BlockSystem:
+    """model.hpp:68-70: exact Gateaux derivative with phi_tilde frozen (M_uphi = 0).
+
+    planes=(p_lo, p_hi): the slab's rows, columns over its planes plus one ghost plane each side."""
     x, pt = _as_f64(solution), _as_f64(phi_tilde)
     h = C.c_void_p()
-    check(load().cf_assemble_jacobian(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(x), _ptr(pt),
-                                      C.byref(h)))
+    if planes is None:
+        check(load().cf_assemble_jacobian(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(x), _ptr(pt),
+                                          C.byref(h)))
+    else:
+        check(load().cf_assemble_jacobian_planes(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(x),
+                                                 _ptr(pt), int(planes[0]), int(planes[1]), C.byref(h)))
     return BlockSystem(h)
+
+
+def slab_info(prob: Problem, rank: int, size: int) -> dict:
+    """The slab of rank `rank` of `size` (cf_slab_info): owned / ext vertex ranges, cell range."""
+    info = (C.c_int64 * 7)()
+    check(load().cf_slab_info(prob._h, int(rank), int(size), info))
+    keys = ("v_lo", "v_hi", "ve_lo", "ve_hi", "c_lo", "c_hi", "plane")
+    return {k: int(v) for k, v in zip(keys, info)}
+
+
+class Communicator:
+    """NCCL communicator of the slab-decomposed Newton step (one process per GPU).
+
+    from_torch_distributed(): rank 0 makes the NCCL id, torch.distributed broadcasts it, every
+    rank creates its communicator on its current CUDA device (set it first)."""
+
+    def __init__(self, rank: int, size: int, uid: bytes | None = None):
+        self._h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid is not None else None
+        check(load().cf_comm_create(buf, int(rank), int(size), C.byref(self._h)))
+        self.rank, self.size = int(rank), int(size)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(load().cf_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_torch_distributed(cls, group=None) -> "Communicator":
+        import torch.distributed as dist
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+        if size == 1:
+            return cls(0, 1)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(rank, size, obj[0])
+
+    def __del__(self):
+        try:
+            load().cf_comm_destroy(self._h)
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------------------- linear algebra
@@ -519,19 +587,28 @@ def _report(its, n, conv, feas, times=None):
 
 
 def newton_active_set_step(state: FractureState, mat: Material, prob: Problem, reg: Regularization,
-                           opts: SolverOptions | None = None, max_its: int = 256) -> dict:
-    """solver.cpp:49-188 (the state is updated in place on the device)."""
+                           opts: SolverOptions | None = None, max_its: int = 256,
+                           comm: Communicator | None = None) -> dict:
+    """solver.cpp:49-188 (the state is updated in place on the device).
+
+    comm: run this rank's slab of the decomposed step (every rank calls it with the same state)."""
     from ._lib import NewtonIterationC, PhaseTimesC
     o = opts or SolverOptions()
     its = (NewtonIterationC * max_its)()
     n, conv, feas, times = C.c_int(), C.c_int(), C.c_double(), PhaseTimesC()
-    check(load().cf_newton_active_set_step(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o), its, max_its,
-                                           C.byref(n), C.byref(conv), C.byref(feas), C.byref(times)))
+    if comm is None:
+        check(load().cf_newton_active_set_step(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o), its,
+                                               max_its, C.byref(n), C.byref(conv), C.byref(feas), C.byref(times)))
+    else:
+        check(load().cf_newton_active_set_step_comm(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o),
+                                                    comm._h, its, max_its, C.byref(n), C.byref(conv), C.byref(feas),
+                                                    C.byref(times)))
     return _report(its, n.value, conv.value, feas.value, times)
 
 
 def solve_loading_sequence(state: FractureState, mat: Material, prob: Problem, reg: Regularization,
-                           opts: SolverOptions | None, n_steps: int, max_its: int = 1024) -> list:
+                           opts: SolverOptions | None, n_steps: int, max_its: int = 1024,
+                           comm: Communicator | None = None) -> list:
     """solver.cpp:190-204: list of per-step reports; stops after a non-converged step."""
     from ._lib import NewtonIterationC
     o = opts or SolverOptions()
@@ -540,8 +617,13 @@ def solve_loading_sequence(state: FractureState, mat: Material, prob: Problem, r
     conv = (C.c_int * max(1, n_steps))()
     feas = (C.c_double * max(1, n_steps))()
     done = C.c_int()
-    check(load().cf_solve_loading_sequence(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o), int(n_steps),
-                                           its, max_its, n_its, conv, feas, C.byref(done)))
+    if comm is None:
+        check(load().cf_solve_loading_sequence(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o),
+                                               int(n_steps), its, max_its, n_its, conv, feas, C.byref(done)))
+    else:
+        check(load().cf_solve_loading_sequence_comm(prob._h, state._h, C.byref(mat), C.byref(reg), C.byref(o),
+                                                    comm._h, int(n_steps), its, max_its, n_its, conv, feas,
+                                                    C.byref(done)))
     out, off = [], 0
     for s in range(done.value):
         k = n_its[s]

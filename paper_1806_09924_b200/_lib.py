@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcrackfield_b200.so")
 
 CF_OK = 0
-ERRORS = {1: ValueError, 2: RuntimeError, 3: RuntimeError, 4: RuntimeError, 5: MemoryError, 6: NotImplementedError}
+ERRORS = {1: ValueError, 2: RuntimeError, 3: RuntimeError, 4: RuntimeError, 5: MemoryError, 6: NotImplementedError,
+          7: RuntimeError}
 
 
 class CfError(RuntimeError):
@@ -104,6 +105,12 @@ SIGNATURES = [
     ("cf_constraints_distribute", _I, [_P, _P, _I]),
     ("cf_assemble_residual", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, _P]),
     ("cf_assemble_jacobian", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, C.POINTER(_P)]),
+    ("cf_assemble_residual_planes", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, _L, _L,
+                                         _P]),
+    ("cf_assemble_jacobian_planes", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, _L, _L,
+                                         C.POINTER(_P)]),
+    ("cf_slab_info", _I, [_P, _I, _I, _P]),
+    ("cf_block_shape", _I, [_P, _P]),
     ("cf_block_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),
     ("cf_block_export", _I, [_P, _I, _P, _P, _P]),
     ("cf_block_apply", _I, [_P, _P, _P]),
@@ -141,6 +148,15 @@ SIGNATURES = [
                                        C.POINTER(_D), _P]),
     ("cf_solve_loading_sequence", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
                                        C.POINTER(SolverOptions), _I, _P, _I, _P, _P, _P, C.POINTER(_I)]),
+    ("cf_comm_unique_id", _I, [_P]),
+    ("cf_comm_create", _I, [_P, _I, _I, C.POINTER(_P)]),
+    ("cf_comm_info", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
+    ("cf_comm_destroy", _I, [_P]),
+    ("cf_newton_active_set_step_comm", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
+                                            C.POINTER(SolverOptions), _P, _P, _I, C.POINTER(_I), C.POINTER(_I),
+                                            C.POINTER(_D), _P]),
+    ("cf_solve_loading_sequence_comm", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
+                                            C.POINTER(SolverOptions), _P, _I, _P, _I, _P, _P, _P, C.POINTER(_I)]),
 ]
 
 

@@ -100,97 +100,6 @@ struct Coef {
 };
 
 // ------------------------------------------------------------------ K1a: element residuals
-// model.cpp:145-194, one thread per cell; writes ru/rphi of all 2^d local nodes.
-template <int D>
-__global__ void __launch_bounds__(128) k_cell_residual(GridDesc g, const Tables* __restrict__ T, Coef cf,
-                                                       const double* __restrict__ sol,
-                                                       const double* __restrict__ ptil,
-                                                       double* __restrict__ out) {
-  constexpr int NV = 1 << D, NQ = 1 << D;
-  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= g.ncells) return;
-  const i64 cx = c % g.nc, cy = (c / g.nc) % g.nc, cz = (D == 3) ? c / (g.nc * g.nc) : 0;
-  const i64 nu = g.n_u();
-  double uloc[NV][D], philoc[NV], ptloc[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const i64 v = (cx + (k & 1)) + g.nn * ((cy + ((k >> 1) & 1)) + g.nn * (cz + ((k >> 2) & 1)));
-#pragma unroll
-    for (int a = 0; a < D; ++a) uloc[k][a] = sol[v * D + a];
-    philoc[k] = sol[nu + v];
-    ptloc[k] = ptil[v];
-  }
-  const double h = g.h;
-  double ru[NV * D], rphi[NV];
-#pragma unroll
-  for (int i = 0; i < NV * D; ++i) ru[i] = 0.0;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) rphi[i] = 0.0;
-  for (int q = 0; q < NQ; ++q) {
-    double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    double gphi[3] = {0, 0, 0};
-    double phi = 0.0, pt = 0.0;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const double sk = T->s[q][k];
-      phi += sk * philoc[k];
-      pt += sk * ptloc[k];
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        const double Gkb = T->G[q][k][b];
-        gphi[b] += philoc[k] * Gkb / h;
-#pragma unroll
-        for (int a = 0; a < D; ++a) gu[a][b] += uloc[k][a] * Gkb / h;
-      }
-    }
-    double e[3][3], sig[3][3];
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
-    double tre = 0.0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) tre += e[a][a];
-    const double two_mu = 2.0 * cf.mu;
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) sig[a][b] = two_mu * e[a][b];
-#pragma unroll
-    for (int a = 0; a < D; ++a) sig[a][a] += cf.lam * tre;
-    double sig_ee = 0.0;
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) sig_ee += sig[a][b] * e[a][b];
-    const double gcoef = (1.0 - cf.kap) * pt * pt + cf.kap;
-    const double pphi = (cf.coupling == 0) ? pt * pt : phi * phi;
-    const double w = T->w[q];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        double val = 0.0;
-#pragma unroll
-        for (int b = 0; b < D; ++b) val += gcoef * sig[a][b] * T->G[q][k][b] / h;
-        val += pphi * cf.p * T->G[q][k][a] / h;
-        ru[k * D + a] += w * val;
-      }
-      double vphi = ((1.0 - cf.kap) * phi * sig_ee + 2.0 * phi * cf.p * tre - cf.Gc / cf.eps * (1.0 - phi)) * T->s[q][k];
-#pragma unroll
-      for (int b = 0; b < D; ++b) vphi += cf.Gc * cf.eps * gphi[b] * T->G[q][k][b] / h;
-      rphi[k] += w * vphi;
-    }
-  }
-  double* o = out + c * (NV * (D + 1));
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-#pragma unroll
-    for (int a = 0; a < D; ++a) o[k * (D + 1) + a] = ru[k * D + a];
-    o[k * (D + 1) + D] = rphi[k];
-  }
-}
-
 // K1a (fast form): one thread per (cell, quadrature point), the 2^d lanes of a cell adjacent in
 // the warp.  Lane q loads corner q's values and the cell's corner data is exchanged with
 // shuffles; each lane evaluates its point's state and its contribution to every (k, a); the
@@ -200,7 +109,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Tables* __restrict__ T, Coef cf,
                                                          const double* __restrict__ sol,
                                                          const double* __restrict__ ptil,
-                                                         double* __restrict__ out) {
+                                                         double* __restrict__ out, i64 c_lo, i64 c_hi) {
   constexpr int NV = 1 << D, NQ = 1 << D;
   __shared__ double sG[NQ][NV][D], sS[NQ][NV], sW[NQ];
   for (int i = threadIdx.x; i < NQ * NV; i += blockDim.x) {
@@ -211,10 +120,10 @@ __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Table
   if (threadIdx.x < NQ) sW[threadIdx.x] = T->w[threadIdx.x];
   __syncthreads();
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  const i64 c = t / NQ;
+  const i64 c = c_lo + t / NQ;
   const int q = int(t % NQ);
-  const bool valid = c < g.ncells;
-  const i64 cc = valid ? c : 0;
+  const bool valid = c < c_hi;
+  const i64 cc = valid ? c : c_lo;
   const i64 cx = cc % g.nc, cy = (cc / g.nc) % g.nc, cz = (D == 3) ? cc / (g.nc * g.nc) : 0;
   const i64 nu = g.n_u();
   double my_u[D], my_phi, my_pt;
@@ -296,7 +205,7 @@ __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Table
     }
   }
   if (valid) {
-    double* o = out + c * (NV * (D + 1)) + q * (D + 1);
+    double* o = out + (c - c_lo) * (NV * (D + 1)) + q * (D + 1);
 #pragma unroll
     for (int a = 0; a <= D; ++a) o[a] = keep[a];
   }
@@ -305,10 +214,11 @@ __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Table
 // K1b: vertex gather with condensation (Scatter::vector_add, model.cpp:74-80; entry-free lines drop).
 template <int D>
 __global__ void k_vertex_residual(GridDesc g, const double* __restrict__ cellres,
-                                  const std::uint8_t* __restrict__ flag, double* __restrict__ R) {
+                                  const std::uint8_t* __restrict__ flag, double* __restrict__ R, Slab sl) {
   constexpr int NV = 1 << D;
-  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= g.V) return;
+  const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lv >= sl.nv()) return;
+  const i64 v = sl.v_lo + lv;
   i64 x, y, z;
   vxyz<D>(g, v, x, y, z);
   CellList<D> L;
@@ -317,14 +227,14 @@ __global__ void k_vertex_residual(GridDesc g, const double* __restrict__ cellres
 #pragma unroll
   for (int a = 0; a <= D; ++a) acc[a] = 0.0;
   for (int i = 0; i < L.n; ++i) {
-    const double* o = cellres + L.cell[i] * (NV * (D + 1)) + L.kv[i] * (D + 1);
+    const double* o = cellres + (L.cell[i] - sl.c_lo) * (NV * (D + 1)) + L.kv[i] * (D + 1);
 #pragma unroll
     for (int a = 0; a <= D; ++a) acc[a] += o[a];
   }
-  const i64 nu = g.n_u();
+  const i64 nu = g.n_u(), nul = D * sl.nv();
 #pragma unroll
-  for (int a = 0; a < D; ++a) R[v * D + a] = flag[v * D + a] ? 0.0 : acc[a];
-  R[nu + v] = flag[nu + v] ? 0.0 : acc[D];
+  for (int a = 0; a < D; ++a) R[lv * D + a] = flag[v * D + a] ? 0.0 : acc[a];
+  R[nul + lv] = flag[nu + v] ? 0.0 : acc[D];
 }
 
 // ------------------------------------------------------------------ K2a: quadrature-point state
@@ -338,10 +248,10 @@ template <int D>
 __global__ void __launch_bounds__(128) k_cell_qpstate(GridDesc g, const Tables* __restrict__ T, Coef cf,
                                                       const double* __restrict__ sol,
                                                       const double* __restrict__ ptil,
-                                                      double* __restrict__ out) {
+                                                      double* __restrict__ out, i64 c_lo, i64 c_hi) {
   constexpr int NV = 1 << D, NQ = 1 << D, NS = QS<D>::NS;
-  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c >= g.ncells) return;
+  const i64 c = c_lo + i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= c_hi) return;
   const i64 cx = c % g.nc, cy = (c / g.nc) % g.nc, cz = (D == 3) ? c / (g.nc * g.nc) : 0;
   const i64 nu = g.n_u();
   double uloc[NV][D], philoc[NV], ptloc[NV];
@@ -389,7 +299,7 @@ __global__ void __launch_bounds__(128) k_cell_qpstate(GridDesc g, const Tables* 
     const double gcoef = (1.0 - cf.kap) * pt * pt + cf.kap;
     const double w = T->w[q];
     // AoS layout: the NQ x NS states of a cell are contiguous (one coalesced 832-byte read per cell)
-    auto put = [&](int f, double val) { out[c * (NQ * NS) + q * NS + f] = val; };
+    auto put = [&](int f, double val) { out[(c - c_lo) * (NQ * NS) + q * NS + f] = val; };
     put(0, w * gcoef);
     put(1, phi);
     put(2, tre);
@@ -473,18 +383,13 @@ __device__ inline void pair_blocks(const Tables* __restrict__ T, const Coef& cf,
 // K2 count pass: row lengths of the three blocks; constrained rows keep a diagonal iff its
 // summed value is non-zero (model.cpp:295,300,308-311).
 template <int D>
-struct SmTables;
-template <int D>
-__device__ inline void pair_blocks_soa(const SmTables<D>& T, const Coef& cf, const double* __restrict__ qs,
-                                       i64 ncells, const CellList<D>& L, bool need_u, bool need_p,
-                                       PairBlocks<D>& out);
-
-template <int D>
 __global__ void k_jac_count(GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
                             const std::uint8_t* __restrict__ flag, i64* __restrict__ cnt_uu,
-                            i64* __restrict__ cnt_pu, i64* __restrict__ cnt_pp) {
-  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= g.V) return;
+                            i64* __restrict__ cnt_pu, i64* __restrict__ cnt_pp, Slab sl) {
+  const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lv >= sl.nv()) return;
+  const i64 v = sl.v_lo + lv;
+  qs -= sl.c_lo * ((1 << D) * QS<D>::NS);  // cell states are stored from the slab's first cell
   i64 x, y, z;
   vxyz<D>(g, v, x, y, z);
   const i64 nu = g.n_u();
@@ -510,105 +415,10 @@ __global__ void k_jac_count(GridDesc g, const Tables* __restrict__ T, Coef cf, c
     pair_blocks<D>(T, cf, qs, L, true, true, pb);
   }
 #pragma unroll
-  for (int a = 0; a < D; ++a) cnt_uu[v * D + a] = flag[v * D + a] ? (pb.uu[a][a] != 0.0 ? 1 : 0) : nfu;
+  for (int a = 0; a < D; ++a) cnt_uu[lv * D + a] = flag[v * D + a] ? (pb.uu[a][a] != 0.0 ? 1 : 0) : nfu;
   const bool pf = flag[nu + v] == 0;
-  cnt_pu[v] = pf ? nfu : 0;
-  cnt_pp[v] = pf ? nfp : (pb.pp != 0.0 ? 1 : 0);
-}
-
-// K2 fill pass: one thread per (row vertex v, stencil slot s) writes the columns and values
-// of the v-w coupling in all three blocks.
-template <int D>
-__global__ void __launch_bounds__(128) k_jac_fill(GridDesc g, const Tables* __restrict__ T, Coef cf,
-                                                  const double* __restrict__ qs,
-                                                  const std::uint8_t* __restrict__ flag,
-                                                  const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
-                                                  double* __restrict__ val_uu, const i64* __restrict__ ptr_pu,
-                                                  int* __restrict__ col_pu, double* __restrict__ val_pu,
-                                                  const i64* __restrict__ ptr_pp, int* __restrict__ col_pp,
-                                                  double* __restrict__ val_pp) {
-  constexpr int S = (D == 3) ? 27 : 9;
-  __shared__ SmTables<D> sT;
-  sT.load(T);
-  __syncthreads();
-  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= g.V * S) return;
-  const i64 v = t / S;
-  const int s = int(t % S);
-  const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
-  i64 x, y, z;
-  vxyz<D>(g, v, x, y, z);
-  const i64 X = x + dx, Y = y + dy, Z = z + dz;
-  if (X < 0 || Y < 0 || Z < 0 || X >= g.nn || Y >= g.nn || Z >= ((D == 3) ? g.nn : 1)) return;
-  const i64 w = X + g.nn * (Y + g.nn * Z);
-  const i64 nu = g.n_u();
-  bool rowfree_u[D], colfree_u[D];
-  bool any_row_u = false, any_col_u = false;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    rowfree_u[a] = flag[v * D + a] == 0;
-    colfree_u[a] = flag[w * D + a] == 0;
-    any_row_u |= rowfree_u[a];
-    any_col_u |= colfree_u[a];
-  }
-  const bool rowfree_p = flag[nu + v] == 0, colfree_p = flag[nu + w] == 0;
-  const bool center = (w == v);
-  bool any_con_row = !rowfree_p;
-#pragma unroll
-  for (int a = 0; a < D; ++a) any_con_row |= !rowfree_u[a];
-  const bool need_u = (any_row_u && any_col_u) || (center && any_con_row);
-  const bool need_p = (rowfree_p && (any_col_u || colfree_p)) || (center && !rowfree_p);
-  if (!need_u && !need_p) return;
-  // offsets of w's columns inside v's rows: free components of lower stencil slots
-  i64 off_u = 0, off_p = 0;
-  for (int s2 = 0; s2 < s; ++s2) {
-    const int ex = s2 % 3 - 1, ey = (s2 / 3) % 3 - 1, ez = (D == 3) ? s2 / 9 - 1 : 0;
-    const i64 X2 = x + ex, Y2 = y + ey, Z2 = z + ez;
-    if (X2 < 0 || Y2 < 0 || Z2 < 0 || X2 >= g.nn || Y2 >= g.nn || Z2 >= ((D == 3) ? g.nn : 1)) continue;
-    const i64 w2 = X2 + g.nn * (Y2 + g.nn * Z2);
-#pragma unroll
-    for (int b = 0; b < D; ++b) off_u += flag[w2 * D + b] ? 0 : 1;
-    off_p += flag[nu + w2] ? 0 : 1;
-  }
-  CellList<D> L;
-  common_cells<D>(g, x, y, z, dx, dy, dz, L);
-  PairBlocks<D> pb;
-  pair_blocks_soa<D>(sT, cf, qs, g.ncells, L, need_u, need_p, pb);
-  // M_uu rows (v, a)
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    const i64 row = v * D + a;
-    if (rowfree_u[a]) {
-      i64 pos = ptr_uu[row] + off_u;
-#pragma unroll
-      for (int b = 0; b < D; ++b)
-        if (colfree_u[b]) {
-          col_uu[pos] = int(w * D + b);
-          val_uu[pos] = pb.uu[a][b];
-          ++pos;
-        }
-    } else if (center && ptr_uu[row + 1] > ptr_uu[row]) {
-      col_uu[ptr_uu[row]] = int(row);
-      val_uu[ptr_uu[row]] = pb.uu[a][a];
-    }
-  }
-  if (rowfree_p) {
-    i64 pos = ptr_pu[v] + off_u;
-#pragma unroll
-    for (int b = 0; b < D; ++b)
-      if (colfree_u[b]) {
-        col_pu[pos] = int(w * D + b);
-        val_pu[pos] = pb.pu[b];
-        ++pos;
-      }
-    if (colfree_p) {
-      col_pp[ptr_pp[v] + off_p] = int(w);
-      val_pp[ptr_pp[v] + off_p] = pb.pp;
-    }
-  } else if (center && ptr_pp[v + 1] > ptr_pp[v]) {
-    col_pp[ptr_pp[v]] = int(v);
-    val_pp[ptr_pp[v]] = pb.pp;
-  }
+  cnt_pu[lv] = pf ? nfu : 0;
+  cnt_pp[lv] = pf ? nfp : (pb.pp != 0.0 ? 1 : 0);
 }
 
 // Shared-memory copy of the per-problem quadrature tables (the 36 KB integrand table is not
@@ -636,244 +446,12 @@ struct SmTables {
   }
 };
 
-template <int D>
-__device__ inline void pair_blocks_sm(const SmTables<D>& T, const Coef& cf, const double* __restrict__ qs,
-                                      const CellList<D>& L, bool need_u, bool need_p, PairBlocks<D>& out) {
-  constexpr int NQ = 1 << D, NS = QS<D>::NS;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-#pragma unroll
-    for (int b = 0; b < D; ++b) out.uu[a][b] = 0.0;
-    out.pu[a] = 0.0;
-  }
-  out.pp = 0.0;
-  const double c2k = 2.0 * (1.0 - cf.kap);
-  const double c2p = 2.0 * cf.p;
-  const double omk = 1.0 - cf.kap;
-  const double gce = cf.Gc / cf.eps;
-  const double gcx = cf.Gc * cf.eps;
-  for (int i = 0; i < L.n; ++i) {
-    const int k = L.kv[i], l = L.kw[i];
-    const double* cs = qs + L.cell[i] * (NQ * NS);
-    double bu[D][D], bp[D], bpp = 0.0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-#pragma unroll
-      for (int b = 0; b < D; ++b) bu[a][b] = 0.0;
-      bp[a] = 0.0;
-    }
-    for (int q = 0; q < NQ; ++q) {
-      const double* st = cs + q * NS;
-      double gk[D], gl[D];
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        gk[b] = T.gp[q][k][b];
-        gl[b] = T.gp[q][l][b];
-      }
-      const double gg = T.gg[q][k][l];
-      if (need_u) {
-        const double wg = st[0];
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int b = 0; b < D; ++b) {
-            const double val = cf.mu * ((a == b ? gg : 0.0) + gl[a] * gk[b]) + cf.lam * gl[b] * gk[a];
-            bu[a][b] += wg * val;
-          }
-      }
-      if (need_p) {
-        const double w = T.w[q];
-        const double phi = st[1], tre = st[2], see = st[3];
-        const double sk = T.s[q][k], sl = T.s[q][l];
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          double sgl = 0.0;
-#pragma unroll
-          for (int c = 0; c < D; ++c) sgl += st[4 + b * D + c] * gl[c];
-          bp[b] += w * (c2k * phi * sgl + c2p * phi * gl[b]) * sk;
-        }
-        bpp += w * ((omk * see + c2p * tre + gce) * sl * sk + gcx * gg);
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-#pragma unroll
-      for (int b = 0; b < D; ++b) out.uu[a][b] += bu[a][b];
-      out.pu[a] += bp[a];
-    }
-    out.pp += bpp;
-  }
-}
-
-// Structure-of-arrays qp states: field f of point q of cell c at qs[(q*NS + f)*ncells + c], so a warp
-// of x-consecutive vertices reads x-consecutive cells coalesced.
-template <int D>
-__device__ inline void pair_blocks_soa(const SmTables<D>& T, const Coef& cf, const double* __restrict__ qs,
-                                       i64 ncells, const CellList<D>& L, bool need_u, bool need_p,
-                                       PairBlocks<D>& out) {
-  constexpr int NQ = 1 << D, NS = QS<D>::NS;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-#pragma unroll
-    for (int b = 0; b < D; ++b) out.uu[a][b] = 0.0;
-    out.pu[a] = 0.0;
-  }
-  out.pp = 0.0;
-  const double c2k = 2.0 * (1.0 - cf.kap);
-  const double c2p = 2.0 * cf.p;
-  const double omk = 1.0 - cf.kap;
-  const double gce = cf.Gc / cf.eps;
-  const double gcx = cf.Gc * cf.eps;
-  for (int i = 0; i < L.n; ++i) {
-    const int k = L.kv[i], l = L.kw[i];
-    const double* cs = qs + L.cell[i];
-    double bu[D][D], bp[D], bpp = 0.0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-#pragma unroll
-      for (int b = 0; b < D; ++b) bu[a][b] = 0.0;
-      bp[a] = 0.0;
-    }
-#pragma unroll 2
-    for (int q = 0; q < NQ; ++q) {
-      auto st = [&](int f) { return __ldg(cs + (i64(q) * NS + f) * ncells); };
-      double gk[D], gl[D];
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        gk[b] = T.gp[q][k][b];
-        gl[b] = T.gp[q][l][b];
-      }
-      const double gg = T.gg[q][k][l];
-      if (need_u) {
-        const double wg = st(0);
-        const double* vl = T.val[q][k][l];
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int b = 0; b < D; ++b) bu[a][b] += wg * vl[a * D + b];
-      }
-      if (need_p) {
-        const double w = T.w[q];
-        const double phi = st(1), tre = st(2), see = st(3);
-        const double sk = T.s[q][k], sl = T.s[q][l];
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          double sgl = 0.0;
-#pragma unroll
-          for (int c = 0; c < D; ++c) sgl += st(4 + b * D + c) * gl[c];
-          bp[b] += w * (c2k * phi * sgl + c2p * phi * gl[b]) * sk;
-        }
-        bpp += w * ((omk * see + c2p * tre + gce) * sl * sk + gcx * gg);
-      }
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-#pragma unroll
-      for (int b = 0; b < D; ++b) out.uu[a][b] += bu[a][b];
-      out.pu[a] += bp[a];
-    }
-    out.pp += bpp;
-  }
-}
-
-// Slot-major fill pass: each warp is 32 x-consecutive row vertices with the SAME stencil slot, so
-// every lane visits the same number of common cells in the same canonical roles (no divergence
-// on the 8-cell centre slot) and reads the SoA states coalesced.  blockIdx.x: x tile,
-// blockIdx.y: (slot group of 8, y), blockIdx.z: z.  Values identical to k_jac_fill.
-template <int D>
-__global__ void __launch_bounds__(256) k_jac_fill_slot(
-    GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
-    const std::uint8_t* __restrict__ flag, const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
-    double* __restrict__ val_uu, const i64* __restrict__ ptr_pu, int* __restrict__ col_pu,
-    double* __restrict__ val_pu, const i64* __restrict__ ptr_pp, int* __restrict__ col_pp,
-    double* __restrict__ val_pp) {
-  constexpr int S = (D == 3) ? 27 : 9, SG = (S + 7) / 8;
-  __shared__ SmTables<D> sT;
-  sT.load(T);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
-  const int s = int(blockIdx.y % SG) * 8 + wv;
-  const i64 y = blockIdx.y / SG, z = (D == 3) ? blockIdx.z : 0;
-  const i64 x = i64(blockIdx.x) * 32 + lane;
-  if (s >= S || x >= g.nn) return;
-  const i64 v = x + g.nn * (y + g.nn * z);
-  const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
-  const i64 X = x + dx, Y = y + dy, Z = z + dz;
-  if (X < 0 || Y < 0 || Z < 0 || X >= g.nn || Y >= g.nn || Z >= ((D == 3) ? g.nn : 1)) return;
-  const i64 w = X + g.nn * (Y + g.nn * Z);
-  const i64 nu = g.n_u();
-  bool rowfree_u[D], colfree_u[D];
-  bool any_row_u = false, any_col_u = false;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    rowfree_u[a] = flag[v * D + a] == 0;
-    colfree_u[a] = flag[w * D + a] == 0;
-    any_row_u |= rowfree_u[a];
-    any_col_u |= colfree_u[a];
-  }
-  const bool rowfree_p = flag[nu + v] == 0, colfree_p = flag[nu + w] == 0;
-  const bool center = (w == v);
-  bool any_con_row = !rowfree_p;
-#pragma unroll
-  for (int a = 0; a < D; ++a) any_con_row |= !rowfree_u[a];
-  const bool need_u = (any_row_u && any_col_u) || (center && any_con_row);
-  const bool need_p = (rowfree_p && (any_col_u || colfree_p)) || (center && !rowfree_p);
-  if (!need_u && !need_p) return;
-  i64 off_u = 0, off_p = 0;
-  for (int s2 = 0; s2 < s; ++s2) {
-    const int ex = s2 % 3 - 1, ey = (s2 / 3) % 3 - 1, ez = (D == 3) ? s2 / 9 - 1 : 0;
-    const i64 X2 = x + ex, Y2 = y + ey, Z2 = z + ez;
-    if (X2 < 0 || Y2 < 0 || Z2 < 0 || X2 >= g.nn || Y2 >= g.nn || Z2 >= ((D == 3) ? g.nn : 1)) continue;
-    const i64 w2 = X2 + g.nn * (Y2 + g.nn * Z2);
-#pragma unroll
-    for (int b = 0; b < D; ++b) off_u += flag[w2 * D + b] ? 0 : 1;
-    off_p += flag[nu + w2] ? 0 : 1;
-  }
-  CellList<D> L;
-  common_cells<D>(g, x, y, z, dx, dy, dz, L);
-  PairBlocks<D> pb;
-  pair_blocks_soa<D>(sT, cf, qs, g.ncells, L, need_u, need_p, pb);
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    const i64 row = v * D + a;
-    if (rowfree_u[a]) {
-      i64 pos = ptr_uu[row] + off_u;
-#pragma unroll
-      for (int b = 0; b < D; ++b)
-        if (colfree_u[b]) {
-          col_uu[pos] = int(w * D + b);
-          val_uu[pos] = pb.uu[a][b];
-          ++pos;
-        }
-    } else if (center && ptr_uu[row + 1] > ptr_uu[row]) {
-      col_uu[ptr_uu[row]] = int(row);
-      val_uu[ptr_uu[row]] = pb.uu[a][a];
-    }
-  }
-  if (rowfree_p) {
-    i64 pos = ptr_pu[v] + off_u;
-#pragma unroll
-    for (int b = 0; b < D; ++b)
-      if (colfree_u[b]) {
-        col_pu[pos] = int(w * D + b);
-        val_pu[pos] = pb.pu[b];
-        ++pos;
-      }
-    if (colfree_p) {
-      col_pp[ptr_pp[v] + off_p] = int(w);
-      val_pp[ptr_pp[v] + off_p] = pb.pp;
-    }
-  } else if (center && ptr_pp[v + 1] > ptr_pp[v]) {
-    col_pp[ptr_pp[v]] = int(v);
-    val_pp[ptr_pp[v]] = pb.pp;
-  }
-}
-
 // Warp-per-vertex fill pass (persistent grid).  Lane s owns stencil slot s of the row vertex v.
 // The warp walks v's adjacent cells in the reference order (the same for every lane), stages the
 // cell's AoS qp states once in shared memory, and every lane whose column vertex is a corner of
 // that cell adds the cell's element-matrix block for (k = v's corner, l = w's corner): per lane the
-// cells are still summed in reference order, so every value equals k_jac_fill's.
+// cells are still summed in reference order, so every value is the reference's element sum.
+// Rows are the slab's owned vertices (local numbering), columns are ext-numbered.
 template <int D>
 constexpr int fill_wpb() { return D == 3 ? 4 : 8; }  // 3d: 42 KB of tables + 4 x 832 B staging
 
@@ -883,7 +461,7 @@ __global__ void __launch_bounds__(fill_wpb<D>() * 32) k_jac_fill_warp(
     const std::uint8_t* __restrict__ flag, const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
     double* __restrict__ val_uu, const i64* __restrict__ ptr_pu, int* __restrict__ col_pu,
     double* __restrict__ val_pu, const i64* __restrict__ ptr_pp, int* __restrict__ col_pp,
-    double* __restrict__ val_pp) {
+    double* __restrict__ val_pp, Slab sl) {
   constexpr int S = (D == 3) ? 27 : 9, NQ = 1 << D, NS = QS<D>::NS, CS = NQ * NS, WPB = fill_wpb<D>();
   __shared__ SmTables<D> sT;
   __shared__ double sst[WPB][CS];
@@ -893,7 +471,10 @@ __global__ void __launch_bounds__(fill_wpb<D>() * 32) k_jac_fill_warp(
   const double c2k = 2.0 * (1.0 - cf.kap), c2p = 2.0 * cf.p, omk = 1.0 - cf.kap;
   const double gce = cf.Gc / cf.eps, gcx = cf.Gc * cf.eps;
   const i64 nu = g.n_u();
-  for (i64 v = i64(blockIdx.x) * WPB + wv; v < g.V; v += i64(gridDim.x) * WPB) {
+  const i64 ushift = D * sl.ve_lo, pshift = sl.ve_lo;  // global column -> ext column
+  qs -= sl.c_lo * CS;
+  for (i64 lv = i64(blockIdx.x) * WPB + wv; lv < sl.nv(); lv += i64(gridDim.x) * WPB) {
+    const i64 v = sl.v_lo + lv;
     i64 x, y, z;
     vxyz<D>(g, v, x, y, z);
     const int s = lane;
@@ -1002,145 +583,38 @@ __global__ void __launch_bounds__(fill_wpb<D>() * 32) k_jac_fill_warp(
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const i64 row = v * D + a;
+      const i64 row = lv * D + a;
       if (rowfree_u[a]) {
         i64 pos = ptr_uu[row] + off_u;
 #pragma unroll
         for (int b = 0; b < D; ++b)
           if (colfree_u[b]) {
-            col_uu[pos] = int(w * D + b);
+            col_uu[pos] = int(w * D + b - ushift);
             val_uu[pos] = pb.uu[a][b];
             ++pos;
           }
       } else if (center && ptr_uu[row + 1] > ptr_uu[row]) {
-        col_uu[ptr_uu[row]] = int(row);
+        col_uu[ptr_uu[row]] = int(v * D + a - ushift);
         val_uu[ptr_uu[row]] = pb.uu[a][a];
       }
     }
     if (rowfree_p) {
-      i64 pos = ptr_pu[v] + off_u;
+      i64 pos = ptr_pu[lv] + off_u;
 #pragma unroll
       for (int b = 0; b < D; ++b)
         if (colfree_u[b]) {
-          col_pu[pos] = int(w * D + b);
+          col_pu[pos] = int(w * D + b - ushift);
           val_pu[pos] = pb.pu[b];
           ++pos;
         }
       if (colfree_p) {
-        col_pp[ptr_pp[v] + off_p] = int(w);
-        val_pp[ptr_pp[v] + off_p] = pb.pp;
+        col_pp[ptr_pp[lv] + off_p] = int(w - pshift);
+        val_pp[ptr_pp[lv] + off_p] = pb.pp;
       }
-    } else if (center && ptr_pp[v + 1] > ptr_pp[v]) {
-      col_pp[ptr_pp[v]] = int(v);
-      val_pp[ptr_pp[v]] = pb.pp;
+    } else if (center && ptr_pp[lv + 1] > ptr_pp[lv]) {
+      col_pp[ptr_pp[lv]] = int(v - pshift);
+      val_pp[ptr_pp[lv]] = pb.pp;
     }
-  }
-}
-
-// Tiled form of the fill pass: one CTA per run of TX vertices along x at fixed (y, z).  The
-// quadrature-point states of the (TX+1) x 2 (x 2) cells the run touches are staged once in shared
-// memory (each cell's state is otherwise re-read by up to 8 x 27 threads from L1/L2); threads are
-// (vertex, stencil slot) pairs exactly as in k_jac_fill, so every value is computed identically.
-template <int D, int TX>
-__global__ void __launch_bounds__(TX*((D == 3) ? 27 : 9)) k_jac_fill_tiled(
-    GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
-    const std::uint8_t* __restrict__ flag, const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
-    double* __restrict__ val_uu, const i64* __restrict__ ptr_pu, int* __restrict__ col_pu,
-    double* __restrict__ val_pu, const i64* __restrict__ ptr_pp, int* __restrict__ col_pp,
-    double* __restrict__ val_pp) {
-  constexpr int S = (D == 3) ? 27 : 9, NQ = 1 << D, CS = NQ * QS<D>::NS;
-  constexpr int NCX = TX + 1, NY = 2, NZ = (D == 3) ? 2 : 1;
-  __shared__ double st[NCX * NY * NZ * CS];
-  __shared__ SmTables<D> sT;
-  sT.load(T);
-  const i64 x0 = i64(blockIdx.x) * TX, y = blockIdx.y, z = (D == 3) ? blockIdx.z : 0;
-  for (int idx = threadIdx.x; idx < NCX * NY * NZ * CS; idx += blockDim.x) {
-    const int cl = idx / CS, e = idx % CS;
-    const int lx = cl % NCX, ly = (cl / NCX) % NY, lz = cl / (NCX * NY);
-    const i64 cx = x0 - 1 + lx, cy = y - 1 + ly, cz = (D == 3) ? z - 1 + lz : 0;
-    const bool in = cx >= 0 && cx < g.nc && cy >= 0 && cy < g.nc && cz >= 0 && (D == 2 || cz < g.nc);
-    st[idx] = in ? qs[(cx + g.nc * (cy + g.nc * cz)) * CS + e] : 0.0;
-  }
-  __syncthreads();
-  const int vl = threadIdx.x / S, s = threadIdx.x % S;
-  const i64 x = x0 + vl;
-  if (x >= g.nn) return;
-  const i64 v = x + g.nn * (y + g.nn * z);
-  const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
-  const i64 X = x + dx, Y = y + dy, Z = z + dz;
-  if (X < 0 || Y < 0 || Z < 0 || X >= g.nn || Y >= g.nn || Z >= ((D == 3) ? g.nn : 1)) return;
-  const i64 w = X + g.nn * (Y + g.nn * Z);
-  const i64 nu = g.n_u();
-  bool rowfree_u[D], colfree_u[D];
-  bool any_row_u = false, any_col_u = false;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    rowfree_u[a] = flag[v * D + a] == 0;
-    colfree_u[a] = flag[w * D + a] == 0;
-    any_row_u |= rowfree_u[a];
-    any_col_u |= colfree_u[a];
-  }
-  const bool rowfree_p = flag[nu + v] == 0, colfree_p = flag[nu + w] == 0;
-  const bool center = (w == v);
-  bool any_con_row = !rowfree_p;
-#pragma unroll
-  for (int a = 0; a < D; ++a) any_con_row |= !rowfree_u[a];
-  const bool need_u = (any_row_u && any_col_u) || (center && any_con_row);
-  const bool need_p = (rowfree_p && (any_col_u || colfree_p)) || (center && !rowfree_p);
-  if (!need_u && !need_p) return;
-  i64 off_u = 0, off_p = 0;
-  for (int s2 = 0; s2 < s; ++s2) {
-    const int ex = s2 % 3 - 1, ey = (s2 / 3) % 3 - 1, ez = (D == 3) ? s2 / 9 - 1 : 0;
-    const i64 X2 = x + ex, Y2 = y + ey, Z2 = z + ez;
-    if (X2 < 0 || Y2 < 0 || Z2 < 0 || X2 >= g.nn || Y2 >= g.nn || Z2 >= ((D == 3) ? g.nn : 1)) continue;
-    const i64 w2 = X2 + g.nn * (Y2 + g.nn * Z2);
-#pragma unroll
-    for (int b = 0; b < D; ++b) off_u += flag[w2 * D + b] ? 0 : 1;
-    off_p += flag[nu + w2] ? 0 : 1;
-  }
-  CellList<D> L;
-  common_cells<D>(g, x, y, z, dx, dy, dz, L);
-  for (int i = 0; i < L.n; ++i) {  // global cell id -> shared-memory slot
-    const i64 c = L.cell[i];
-    const i64 cx = c % g.nc, cy = (c / g.nc) % g.nc, cz = (D == 3) ? c / (g.nc * g.nc) : 0;
-    const i64 lz = (D == 3) ? cz - (z - 1) : 0;
-    L.cell[i] = (lz * NY + (cy - (y - 1))) * NCX + (cx - (x0 - 1));
-  }
-  PairBlocks<D> pb;
-  pair_blocks_sm<D>(sT, cf, st, L, need_u, need_p, pb);
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    const i64 row = v * D + a;
-    if (rowfree_u[a]) {
-      i64 pos = ptr_uu[row] + off_u;
-#pragma unroll
-      for (int b = 0; b < D; ++b)
-        if (colfree_u[b]) {
-          col_uu[pos] = int(w * D + b);
-          val_uu[pos] = pb.uu[a][b];
-          ++pos;
-        }
-    } else if (center && ptr_uu[row + 1] > ptr_uu[row]) {
-      col_uu[ptr_uu[row]] = int(row);
-      val_uu[ptr_uu[row]] = pb.uu[a][a];
-    }
-  }
-  if (rowfree_p) {
-    i64 pos = ptr_pu[v] + off_u;
-#pragma unroll
-    for (int b = 0; b < D; ++b)
-      if (colfree_u[b]) {
-        col_pu[pos] = int(w * D + b);
-        val_pu[pos] = pb.pu[b];
-        ++pos;
-      }
-    if (colfree_p) {
-      col_pp[ptr_pp[v] + off_p] = int(w);
-      val_pp[ptr_pp[v] + off_p] = pb.pp;
-    }
-  } else if (center && ptr_pp[v + 1] > ptr_pp[v]) {
-    col_pp[ptr_pp[v]] = int(v);
-    val_pp[ptr_pp[v]] = pb.pp;
   }
 }
 
@@ -1318,47 +792,68 @@ void distribute(const Constraints& c, double* v, bool homogeneous) {
   CF_LAUNCHED();
 }
 
+Slab make_slab(const GridDesc& g, i64 p_lo, i64 p_hi) {
+  if (p_lo < 0 || p_hi > g.nn || p_lo >= p_hi) fail(CF_ERR_INVALID_ARGUMENT, "make_slab: empty or out-of-range planes");
+  Slab s;
+  s.plane = (g.d == 3) ? g.nn * g.nn : g.nn;
+  const i64 cplane = (g.d == 3) ? g.nc * g.nc : g.nc;
+  s.v_lo = p_lo * s.plane;
+  s.v_hi = p_hi * s.plane;
+  s.ve_lo = std::max<i64>(p_lo - 1, 0) * s.plane;
+  s.ve_hi = std::min<i64>(p_hi + 1, g.nn) * s.plane;
+  s.c_lo = std::max<i64>(p_lo - 1, 0) * cplane;  // cells of planes [p_lo - 1, p_hi) touch owned vertices
+  s.c_hi = std::min<i64>(p_hi, g.nc) * cplane;
+  return s;
+}
+
 void assemble_residual(Problem& P, const Constraints& cs, const cf_material& m, const cf_regularization& reg,
-                       const double* x, const double* pt, double* R) {
+                       const double* x, const double* pt, double* R, const Slab* slab) {
   build_tables(P, mat_mu(m), mat_lambda(m));
   const Coef cf = make_coef(P, m, reg);
   const GridDesc& g = P.g;
+  const Slab sl = slab ? *slab : full_slab(g);
   const int nv = 1 << g.d;
-  DevBuf<double> cellres(g.ncells * nv * (g.d + 1));
+  const i64 nc = sl.c_hi - sl.c_lo;
+  DevBuf<double> cellres(nc * nv * (g.d + 1));
   if (g.d == 2) {
-    k_cell_residual_q<2><<<grid_for(g.ncells * 4, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p);
+    k_cell_residual_q<2><<<grid_for(nc * 4, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p, sl.c_lo,
+                                                                      sl.c_hi);
     CF_LAUNCHED();
-    k_vertex_residual<2><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R);
+    k_vertex_residual<2><<<grid_for(sl.nv(), 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R, sl);
     CF_LAUNCHED();
   } else {
-    k_cell_residual_q<3><<<grid_for(g.ncells * 8, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p);
+    k_cell_residual_q<3><<<grid_for(nc * 8, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p, sl.c_lo,
+                                                                      sl.c_hi);
     CF_LAUNCHED();
-    k_vertex_residual<3><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R);
+    k_vertex_residual<3><<<grid_for(sl.nv(), 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R, sl);
     CF_LAUNCHED();
   }
 }
 
 template <int D>
 static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, const double* x, const double* pt,
-                          BlockSystem& J) {
+                          const Slab& sl, BlockSystem& J) {
   const GridDesc& g = P.g;
-  constexpr int NQ = 1 << D, NS = QS<D>::NS, S = (D == 3) ? 27 : 9;
-  DevBuf<double> qs(g.ncells * NQ * NS);
-  k_cell_qpstate<D><<<grid_for(g.ncells, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p);
+  constexpr int NQ = 1 << D, NS = QS<D>::NS;
+  const i64 ncl = sl.c_hi - sl.c_lo;
+  DevBuf<double> qs(ncl * NQ * NS);
+  k_cell_qpstate<D><<<grid_for(ncl, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p, sl.c_lo, sl.c_hi);
   CF_LAUNCHED();
-  const i64 nu = g.n_u(), np = g.V;
-  J.uu->rows = J.uu->cols = nu;
+  const i64 nu = D * sl.nv(), np = sl.nv();
+  J.uu->rows = nu;
+  J.uu->cols = D * sl.ne();
   J.pu->rows = np;
-  J.pu->cols = nu;
-  J.pp->rows = J.pp->cols = np;
+  J.pu->cols = D * sl.ne();
+  J.pp->rows = np;
+  J.pp->cols = sl.ne();
   J.uu->ptr.alloc(nu + 1);
   J.pu->ptr.alloc(np + 1);
   J.pp->ptr.alloc(np + 1);
   CF_CUDA(cudaMemsetAsync(J.uu->ptr.p + nu, 0, sizeof(i64), stream()));
   CF_CUDA(cudaMemsetAsync(J.pu->ptr.p + np, 0, sizeof(i64), stream()));
   CF_CUDA(cudaMemsetAsync(J.pp->ptr.p + np, 0, sizeof(i64), stream()));
-  k_jac_count<D><<<grid_for(g.V, 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.pu->ptr.p,
-                                                           J.pp->ptr.p);
+  k_jac_count<D><<<grid_for(sl.nv(), 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p,
+                                                               J.pu->ptr.p, J.pp->ptr.p, sl);
   CF_LAUNCHED();
   exclusive_scan_inplace(J.uu->ptr.p, nu);
   exclusive_scan_inplace(J.pu->ptr.p, np);
@@ -1377,29 +872,34 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   J.pu->val.alloc(nnz[1]);
   J.pp->col.alloc(nnz[2]);
   J.pp->val.alloc(nnz[2]);
-  (void)S;
   int bps = 0;
   constexpr int FT = fill_wpb<D>() * 32;
   CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_jac_fill_warp<D>, FT, 0));
   const int grid = std::max(1, bps) * rt().sm_count;
   k_jac_fill_warp<D><<<grid, FT, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.uu->col.p,
                                                  J.uu->val.p, J.pu->ptr.p, J.pu->col.p, J.pu->val.p, J.pp->ptr.p,
-                                                 J.pp->col.p, J.pp->val.p);
+                                                 J.pp->col.p, J.pp->val.p, sl);
   CF_LAUNCHED();
 }
 
 std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& cs, const cf_material& m,
-                                               const cf_regularization& reg, const double* x, const double* pt) {
+                                               const cf_regularization& reg, const double* x, const double* pt,
+                                               const Slab* slab) {
   build_tables(P, mat_mu(m), mat_lambda(m));
   const Coef cf = make_coef(P, m, reg);
+  const Slab sl = slab ? *slab : full_slab(P.g);
   auto J = std::make_unique<BlockSystem>();
   J->d = P.g.d;
-  J->nu = P.g.n_u();
-  J->np = P.g.V;
+  J->nu = P.g.d * sl.nv();
+  J->np = sl.nv();
+  if (!sl.full(P.g)) {
+    J->nu_in = P.g.d * sl.ne();
+    J->np_in = sl.ne();
+  }
   if (P.g.d == 2)
-    jacobian_impl<2>(P, cs, cf, x, pt, *J);
+    jacobian_impl<2>(P, cs, cf, x, pt, sl, *J);
   else
-    jacobian_impl<3>(P, cs, cf, x, pt, *J);
+    jacobian_impl<3>(P, cs, cf, x, pt, sl, *J);
   return J;
 }
 

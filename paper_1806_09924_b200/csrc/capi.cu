@@ -7,6 +7,7 @@
 #include <string>
 #include <unordered_map>
 
+#include "cf_comm.hpp"
 #include "cf_types.hpp"
 #include "cf_vec.hpp"
 
@@ -32,6 +33,9 @@ struct cf_constraints_s {
 };
 struct cf_block_s {
   std::unique_ptr<cfb::BlockSystem> J;
+};
+struct cf_comm_s {
+  std::unique_ptr<cfb::Comm> c;
 };
 
 namespace cfb {
@@ -263,6 +267,61 @@ int cf_assemble_jacobian(cf_problem p, cf_constraints c, const cf_material* mat,
   });
 }
 
+static Slab planes_slab(const GridDesc& g, int64_t p_lo, int64_t p_hi) {
+  CHECK_ARG(p_lo >= 0 && p_hi <= g.nn && p_lo < p_hi, "slab planes out of range");
+  return make_slab(g, p_lo, p_hi);
+}
+
+int cf_slab_info(cf_problem p, int rank, int size, int64_t info[7]) {
+  return guard([&] {
+    CHECK_ARG(p && info, "cf_slab_info: null argument");
+    const Slab s = rank_slab(p->p->g, rank, size);
+    const int64_t v[7] = {s.v_lo, s.v_hi, s.ve_lo, s.ve_hi, s.c_lo, s.c_hi, s.plane};
+    std::memcpy(info, v, sizeof(v));
+  });
+}
+
+int cf_assemble_residual_planes(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                                const double* solution, const double* phi_tilde, int64_t p_lo, int64_t p_hi,
+                                double* R) {
+  return guard([&] {
+    CHECK_ARG(p && c && mat && reg && solution && phi_tilde && R, "cf_assemble_residual_planes: null argument");
+    const GridDesc& g = p->p->g;
+    const Slab sl = planes_slab(g, p_lo, p_hi);
+    InArg<double> x(solution, g.n_total());
+    InArg<double> pt(phi_tilde, g.V);
+    OutArg<double> out(R, (g.d + 1) * sl.nv());
+    assemble_residual(*p->p, *c->c, *mat, *reg, x.dev, pt.dev, out.dev, &sl);
+    out.finish();
+  });
+}
+
+int cf_assemble_jacobian_planes(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                                const double* solution, const double* phi_tilde, int64_t p_lo, int64_t p_hi,
+                                cf_block* outb) {
+  return guard([&] {
+    CHECK_ARG(p && c && mat && reg && solution && phi_tilde && outb, "cf_assemble_jacobian_planes: null argument");
+    const GridDesc& g = p->p->g;
+    const Slab sl = planes_slab(g, p_lo, p_hi);
+    InArg<double> x(solution, g.n_total());
+    InArg<double> pt(phi_tilde, g.V);
+    auto J = assemble_jacobian(*p->p, *c->c, *mat, *reg, x.dev, pt.dev, &sl);
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *outb = new cf_block_s{std::move(J)};
+  });
+}
+
+int cf_block_shape(cf_block b, int64_t shape[4]) {
+  return guard([&] {
+    CHECK_ARG(b && shape, "cf_block_shape: null argument");
+    const BlockSystem& J = *b->J;
+    shape[0] = J.nu;
+    shape[1] = J.np;
+    shape[2] = J.in_u();
+    shape[3] = J.np_in >= 0 ? J.np_in : J.np;
+  });
+}
+
 int cf_block_info(cf_block b, int64_t* n_u, int64_t* n_phi, int64_t* nnz3) {
   return guard([&] {
     CHECK_ARG(b, "cf_block_info: null block");
@@ -293,8 +352,9 @@ int cf_block_export(cf_block b, int which, int64_t* rowptr, int32_t* col, double
 int cf_block_apply(cf_block b, const double* x, double* y) {
   return guard([&] {
     CHECK_ARG(b && x && y, "cf_block_apply: null argument");
-    const i64 n = b->J->nu + b->J->np;
-    InArg<double> xi(x, n);
+    const BlockSystem& J = *b->J;
+    const i64 n = J.nu + J.np, n_in = J.in_u() + (J.np_in >= 0 ? J.np_in : J.np);
+    InArg<double> xi(x, n_in);
     OutArg<double> yo(y, n);
     block_apply(*b->J, xi.dev, yo.dev);
     yo.finish();
@@ -698,27 +758,96 @@ static void fill_report(const NewtonReport& r, cf_newton_iteration* its, int max
   if (feasibility) *feasibility = r.feasibility;
 }
 
+// ------------------------------------------------------------------ communicator
+int cf_comm_unique_id(uint8_t id[128]) {
+  return guard([&] {
+    CHECK_ARG(id, "cf_comm_unique_id: null argument");
+    comm_unique_id(id);
+  });
+}
+
+int cf_comm_create(const uint8_t id[128], int rank, int size, cf_comm* out) {
+  return guard([&] {
+    CHECK_ARG(out && (size == 1 || id), "cf_comm_create: null argument");
+    unsigned char zero[128] = {0};
+    *out = new cf_comm_s{comm_create(id ? id : zero, rank, size)};
+  });
+}
+
+int cf_comm_info(cf_comm c, int* rank, int* size) {
+  return guard([&] {
+    CHECK_ARG(c, "cf_comm_info: null communicator");
+    if (rank) *rank = c->c->rank;
+    if (size) *size = c->c->size;
+  });
+}
+
+int cf_comm_destroy(cf_comm c) {
+  return guard([&] { delete c; });
+}
+
+static void newton_timed(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                         const cf_solver_options* opts, const Comm* comm, cf_newton_iteration* its, int max_its,
+                         int* n_its, int* converged, double* feasibility, cf_phase_times* times) {
+  cudaEvent_t a, b;
+  CF_CUDA(cudaEventCreate(&a));
+  CF_CUDA(cudaEventCreate(&b));
+  CF_CUDA(cudaEventRecord(a, stream()));
+  NewtonReport r = newton_active_set_step(*p->p, s->st, *mat, *reg, *opts, comm);
+  CF_CUDA(cudaEventRecord(b, stream()));
+  CF_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  fill_report(r, its, max_its, n_its, converged, feasibility);
+  if (times)
+    *times = cf_phase_times{r.times.residual, r.times.active_set, r.times.jacobian, r.times.amg_setup, r.times.gmres,
+                            double(ms)};
+}
+
 int cf_newton_active_set_step(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
                               const cf_solver_options* opts, cf_newton_iteration* its, int max_its, int* n_its,
                               int* converged, double* feasibility, cf_phase_times* times) {
   return guard([&] {
     CHECK_ARG(p && s && mat && reg && opts, "cf_newton_active_set_step: null argument");
-    cudaEvent_t a, b;
-    CF_CUDA(cudaEventCreate(&a));
-    CF_CUDA(cudaEventCreate(&b));
-    CF_CUDA(cudaEventRecord(a, stream()));
-    NewtonReport r = newton_active_set_step(*p->p, s->st, *mat, *reg, *opts);
-    CF_CUDA(cudaEventRecord(b, stream()));
-    CF_CUDA(cudaEventSynchronize(b));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, a, b);
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    fill_report(r, its, max_its, n_its, converged, feasibility);
-    if (times)
-      *times = cf_phase_times{r.times.residual, r.times.active_set, r.times.jacobian, r.times.amg_setup,
-                              r.times.gmres, double(ms)};
+    newton_timed(p, s, mat, reg, opts, nullptr, its, max_its, n_its, converged, feasibility, times);
   });
+}
+
+int cf_newton_active_set_step_comm(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, cf_comm comm, cf_newton_iteration* its,
+                                   int max_its, int* n_its, int* converged, double* feasibility,
+                                   cf_phase_times* times) {
+  return guard([&] {
+    CHECK_ARG(p && s && mat && reg && opts && comm, "cf_newton_active_set_step_comm: null argument");
+    newton_timed(p, s, mat, reg, opts, comm->c.get(), its, max_its, n_its, converged, feasibility, times);
+  });
+}
+
+static void loading_sequence(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                             const cf_solver_options* opts, const Comm* comm, int n_steps, cf_newton_iteration* its,
+                             int max_its, int* n_its, int* converged, double* feasibility, int* steps_done) {
+  if (n_steps < 1) fail(CF_ERR_INVALID_ARGUMENT, "solve_loading_sequence: n_steps must be >= 1");
+  const GridDesc& g = p->p->g;
+  int done = 0, off = 0;
+  for (int n = 1; n <= n_steps; ++n) {
+    State& st = s->st;
+    CF_CUDA(cudaMemcpyAsync(st.phi_prev2.p, st.phi_old.p, size_t(g.V) * sizeof(double), cudaMemcpyDeviceToDevice,
+                            stream()));
+    CF_CUDA(cudaMemcpyAsync(st.phi_old.p, st.solution.p + g.n_u(), size_t(g.V) * sizeof(double),
+                            cudaMemcpyDeviceToDevice, stream()));
+    st.step = n;
+    NewtonReport r = newton_active_set_step(*p->p, st, *mat, *reg, *opts, comm);
+    int k = 0;
+    fill_report(r, its ? its + off : nullptr, std::max(0, max_its - off), &k, converged ? converged + (n - 1) : nullptr,
+                feasibility ? feasibility + (n - 1) : nullptr);
+    if (n_its) n_its[n - 1] = k;
+    off += std::min(k, std::max(0, max_its - off));
+    ++done;
+    if (!r.converged) break;
+  }
+  if (steps_done) *steps_done = done;
 }
 
 int cf_solve_loading_sequence(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
@@ -726,26 +855,18 @@ int cf_solve_loading_sequence(cf_problem p, cf_state s, const cf_material* mat, 
                               int* n_its, int* converged, double* feasibility, int* steps_done) {
   return guard([&] {
     CHECK_ARG(p && s && mat && reg && opts, "cf_solve_loading_sequence: null argument");
-    if (n_steps < 1) fail(CF_ERR_INVALID_ARGUMENT, "solve_loading_sequence: n_steps must be >= 1");
-    const GridDesc& g = p->p->g;
-    int done = 0, off = 0;
-    for (int n = 1; n <= n_steps; ++n) {
-      State& st = s->st;
-      CF_CUDA(cudaMemcpyAsync(st.phi_prev2.p, st.phi_old.p, size_t(g.V) * sizeof(double), cudaMemcpyDeviceToDevice,
-                              stream()));
-      CF_CUDA(cudaMemcpyAsync(st.phi_old.p, st.solution.p + g.n_u(), size_t(g.V) * sizeof(double),
-                              cudaMemcpyDeviceToDevice, stream()));
-      st.step = n;
-      NewtonReport r = newton_active_set_step(*p->p, st, *mat, *reg, *opts);
-      int k = 0;
-      fill_report(r, its ? its + off : nullptr, std::max(0, max_its - off), &k, converged ? converged + (n - 1) : nullptr,
-                  feasibility ? feasibility + (n - 1) : nullptr);
-      if (n_its) n_its[n - 1] = k;
-      off += std::min(k, std::max(0, max_its - off));
-      ++done;
-      if (!r.converged) break;
-    }
-    if (steps_done) *steps_done = done;
+    loading_sequence(p, s, mat, reg, opts, nullptr, n_steps, its, max_its, n_its, converged, feasibility, steps_done);
+  });
+}
+
+int cf_solve_loading_sequence_comm(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, cf_comm comm, int n_steps,
+                                   cf_newton_iteration* its, int max_its, int* n_its, int* converged,
+                                   double* feasibility, int* steps_done) {
+  return guard([&] {
+    CHECK_ARG(p && s && mat && reg && opts && comm, "cf_solve_loading_sequence_comm: null argument");
+    loading_sequence(p, s, mat, reg, opts, comm->c.get(), n_steps, its, max_its, n_its, converged, feasibility,
+                     steps_done);
   });
 }
 

@@ -32,6 +32,25 @@ struct Tables {
   double val[8][8][8][3][3];   // mu((a==b)gg + gp(l,a)gp(k,b)) + lam gp(l,b)gp(k,a)  (model.cpp:274-275)
 };
 
+// Slab decomposition: a rank owns a contiguous run of vertex planes along the slowest
+// axis (z in 3d, y in 2d), i.e. a contiguous vertex range in the reference's lexicographic
+// numbering.  Its rows need x on one ghost plane each side ("ext" range) and the cells touching
+// its planes (a contiguous range of lexicographic cell indices).  Local vectors are laid out
+// [u_own (d*nv) | phi_own (nv)], ext vectors [u_ext (d*ne) | phi_ext (ne)]; the full slab of a
+// single GPU makes both layouts the global [u | phi].
+struct Slab {
+  i64 v_lo = 0, v_hi = 0;    // owned vertices
+  i64 ve_lo = 0, ve_hi = 0;  // owned + ghost planes (clipped to the grid)
+  i64 c_lo = 0, c_hi = 0;    // cells adjacent to owned vertices
+  i64 plane = 0;             // vertices per plane
+  __host__ __device__ i64 nv() const { return v_hi - v_lo; }
+  __host__ __device__ i64 ne() const { return ve_hi - ve_lo; }
+  bool full(const GridDesc& g) const { return v_lo == 0 && v_hi == g.V; }
+};
+// planes [p_lo, p_hi) of the nn vertex planes
+Slab make_slab(const GridDesc& g, i64 p_lo, i64 p_hi);
+inline Slab full_slab(const GridDesc& g) { return make_slab(g, 0, g.nn); }
+
 struct Problem {
   GridDesc g{};
   Tables host_tab{};
@@ -52,12 +71,19 @@ struct Csr {
   DevBuf<i64> ptr;
   DevBuf<int> col;
   DevBuf<double> val;
+  // mean row length that picks the SpMV lane split (< 0: nnz / rows).  A slab of a distributed
+  // matrix carries the global mean so its rows reduce exactly as the undivided matrix's.
+  double mean_hint = -1.0;
 };
 
 struct BlockSystem {
   i64 nu = 0, np = 0;
+  // input layout of block_apply: [u (nu_in) | phi (np_in)]; < 0 means square (nu, np).  A slab's
+  // blocks read ext vectors (owned rows, columns over owned + ghost planes).
+  i64 nu_in = -1, np_in = -1;
   std::shared_ptr<Csr> uu = std::make_shared<Csr>(), pu = std::make_shared<Csr>(), pp = std::make_shared<Csr>();
   int d = 2;
+  i64 in_u() const { return nu_in >= 0 ? nu_in : nu; }
 };
 
 // ---- host helpers implemented in the .cu files
@@ -66,10 +92,13 @@ void build_tables(Problem& P, double mu, double lam);
 std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64 n_active,
                                                const i64* dofs_dev, const double* vals_dev);
 void distribute(const Constraints& c, double* v_dev, bool homogeneous);
+// x, pt: global-length vectors (valid on the slab's ext range).  R: local layout of the slab.
 void assemble_residual(Problem& P, const Constraints& c, const cf_material& m, const cf_regularization& reg,
-                       const double* x, const double* pt, double* R);
+                       const double* x, const double* pt, double* R, const Slab* slab = nullptr);
+// rows of the slab's owned vertices; columns in the slab's ext numbering
 std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& c, const cf_material& m,
-                                               const cf_regularization& reg, const double* x, const double* pt);
+                                               const cf_regularization& reg, const double* x, const double* pt,
+                                               const Slab* slab = nullptr);
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add);  // y = A x (+ add)
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);

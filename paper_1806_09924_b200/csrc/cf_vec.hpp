@@ -38,6 +38,8 @@ std::unique_ptr<Csr> csr_axpy_prune(const Csr& T, double w, const Csr& DAT);
 void csr_prune(Csr& A);  // in place (Eigen prune(1.0, 1e-300))
 void csr_diagonal(const Csr& A, double* diag);  // A(i,i) or 0
 std::unique_ptr<Csr> csr_copy(const Csr& A);
+// the entries with column in [lo, hi), columns renumbered from lo (a slab's diagonal block)
+std::unique_ptr<Csr> csr_extract_cols(const Csr& A, i64 lo, i64 hi);
 
 // ---- dense LU (amg.cu): column-major n x n, unblocked partial pivoting (PartialPivLU)
 struct DenseLu {
@@ -114,8 +116,10 @@ struct GmresResult {
   double residual = 0.0;
   std::vector<double> history;
 };
+struct Comm;
+// comm (optional, distributed): rhs / x are this rank's rows; every dot is summed over the ranks
 GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
-                  double* x);
+                  double* x, const Comm* comm = nullptr);
 
 // ---- postproc.cu (postproc.cpp:12-99)
 double compute_tcv(const Problem& P, const double* sol);
@@ -139,9 +143,14 @@ struct NewtonReport {
   double feasibility = 0.0;
   PhaseTimes times;
 };
+// comm / slab (optional): the slab-decomposed step of one rank.  The state's vectors
+// are global-length on every rank; on return they hold the full solution on every rank.
 NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& mat, const cf_regularization& reg,
-                                    const cf_solver_options& opts);
-void rigid_body_modes(const Problem& P, const Constraints& c, double* B);  // n_u x m, column-major
+                                    const cf_solver_options& opts, const Comm* comm = nullptr,
+                                    const Slab* slab = nullptr);
+Slab rank_slab(const GridDesc& g, int rank, int size);  // planes split evenly over the ranks
+// n_u x m column-major rigid-body modes (rows of the slab's owned u dofs when slab is given)
+void rigid_body_modes(const Problem& P, const Constraints& c, double* B, const Slab* slab = nullptr);
 // host helpers (model.cpp:28-64, 324-349)
 double slit_band_edge(const Problem& P, const cf_material& mat);
 cf_regularization resolve_regularization(const Problem& P, const cf_material& mat, double band_edge);

@@ -1,0 +1,170 @@
+// NCCL communicator of the slab-decomposed Newton step (cf_comm.hpp).  NCCL is resolved at run
+// time from the process (torch.distributed has normally loaded libnccl.so.2 already, so both use
+// the same library instance); a single-GPU run never touches it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "cf_comm.hpp"
+
+namespace cfb {
+
+namespace {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("NCCL not loadable: ") + dlerror();
+      return;
+    }
+    auto sym = [&](const char* name) {
+      void* p = dlsym(h, name);
+      if (!p && err.empty()) err = std::string("NCCL symbol missing: ") + name;
+      return p;
+    };
+#define CFB_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(sym("nccl" #f))
+    CFB_SYM(GetUniqueId);
+    CFB_SYM(CommInitRank);
+    CFB_SYM(CommDestroy);
+    CFB_SYM(AllGather);
+    CFB_SYM(AllReduce);
+    CFB_SYM(Broadcast);
+    CFB_SYM(Send);
+    CFB_SYM(Recv);
+    CFB_SYM(GroupStart);
+    CFB_SYM(GroupEnd);
+    CFB_SYM(GetErrorString);
+#undef CFB_SYM
+  });
+  if (!err.empty()) fail(CF_ERR_COMM, err);
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(CF_ERR_COMM, std::string(what) + ": " + nccl().GetErrorString(r));
+}
+#define CF_NCCL(x) nccl_check((x), #x)
+
+ncclComm_t H(void* p) { return static_cast<ncclComm_t>(p); }
+
+// out[i] = ((g[0][i] + g[1][i]) + ...) + g[P-1][i]: the same left-to-right sum on every rank
+__global__ void k_rank_sum(const double* __restrict__ g, int P, int k, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  double s = g[i];
+  for (int r = 1; r < P; ++r) s += g[size_t(r) * k + i];
+  out[i] = s;
+}
+
+}  // namespace
+
+void comm_unique_id(unsigned char out[128]) {
+  ncclUniqueId id;
+  CF_NCCL(nccl().GetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+}
+
+std::unique_ptr<Comm> comm_create(const unsigned char id_bytes[128], int rank, int size) {
+  if (size < 1 || rank < 0 || rank >= size) fail(CF_ERR_INVALID_ARGUMENT, "comm_create: bad rank / size");
+  auto c = std::make_unique<Comm>();
+  c->rank = rank;
+  c->size = size;
+  if (size > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, 128);
+    ncclComm_t h = nullptr;
+    CF_NCCL(nccl().CommInitRank(&h, size, id, rank));
+    c->nccl = h;
+  }
+  return c;
+}
+
+Comm::~Comm() {
+  if (nccl) {
+    cudaStreamSynchronize(stream());
+    ::cfb::nccl().CommDestroy(H(nccl));
+  }
+}
+
+void Comm::sum_ordered(double* dev, int k) const {
+  if (size == 1 || k <= 0) return;
+  if (gather.n < i64(size) * k) gather.alloc(i64(size) * k);
+  CF_NCCL(::cfb::nccl().AllGather(dev, gather.p, size_t(k), ncclFloat64, H(nccl), stream()));
+  k_rank_sum<<<(k + 127) / 128, 128, 0, stream()>>>(gather.p, size, k, dev);
+  CF_LAUNCHED();
+}
+
+void Comm::sum_i64(long long* host, int k) const {
+  if (size == 1 || k <= 0) return;
+  if (ibuf.n < k) ibuf.alloc(k);
+  CF_CUDA(cudaMemcpyAsync(ibuf.p, host, size_t(k) * sizeof(long long), cudaMemcpyHostToDevice, stream()));
+  CF_NCCL(::cfb::nccl().AllReduce(ibuf.p, ibuf.p, size_t(k), ncclInt64, ncclSum, H(nccl), stream()));
+  CF_CUDA(cudaMemcpyAsync(host, ibuf.p, size_t(k) * sizeof(long long), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+}
+
+void Comm::max_i64(long long* host, int k) const {
+  if (size == 1 || k <= 0) return;
+  if (ibuf.n < k) ibuf.alloc(k);
+  CF_CUDA(cudaMemcpyAsync(ibuf.p, host, size_t(k) * sizeof(long long), cudaMemcpyHostToDevice, stream()));
+  CF_NCCL(::cfb::nccl().AllReduce(ibuf.p, ibuf.p, size_t(k), ncclInt64, ncclMax, H(nccl), stream()));
+  CF_CUDA(cudaMemcpyAsync(host, ibuf.p, size_t(k) * sizeof(long long), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+}
+
+void Comm::sendrecv(const std::vector<HaloOp>& ops) const {
+  if (size == 1 || ops.empty()) return;
+  const NcclApi& api = ::cfb::nccl();
+  CF_NCCL(api.GroupStart());
+  for (const HaloOp& o : ops) {
+    if (o.bytes == 0) continue;
+    if (o.send) CF_NCCL(api.Send(o.send, o.bytes, ncclUint8, o.peer, H(nccl), stream()));
+    if (o.recv) CF_NCCL(api.Recv(o.recv, o.bytes, ncclUint8, o.peer, H(nccl), stream()));
+  }
+  CF_NCCL(api.GroupEnd());
+}
+
+void Comm::bcast(void* buf, size_t bytes, int root) const {
+  if (size == 1 || bytes == 0) return;
+  CF_NCCL(::cfb::nccl().Broadcast(buf, buf, bytes, ncclUint8, root, H(nccl), stream()));
+}
+
+void Comm::bcast_many(const std::vector<HaloOp>& ops) const {
+  if (size == 1 || ops.empty()) return;
+  const NcclApi& api = ::cfb::nccl();
+  CF_NCCL(api.GroupStart());
+  for (const HaloOp& o : ops)
+    if (o.bytes) CF_NCCL(api.Broadcast(o.recv, o.recv, o.bytes, ncclUint8, o.peer, H(nccl), stream()));
+  CF_NCCL(api.GroupEnd());
+}
+
+void Comm::barrier() const {
+  if (size == 1) return;
+  long long one = 1;
+  sum_i64(&one, 1);
+}
+
+}  // namespace cfb

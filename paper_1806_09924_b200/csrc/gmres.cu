@@ -5,6 +5,7 @@
 // column needed by the Givens logic, which runs on the host exactly as in the reference.
 #include <cmath>
 
+#include "cf_comm.hpp"
 #include "cf_vec.hpp"
 
 namespace cfb {
@@ -17,16 +18,32 @@ __global__ void k_axpy_dev(i64 n, const double* __restrict__ h, const double* __
   if (i < n) w[i] -= (*h) * v[i];
 }
 
+__global__ void k_sqrt1(double* s) { s[0] = sqrt(s[0]); }
+
+// dot over all ranks' rows: the local fixed-order dot, then the rank-ordered sum
+void gdot(const double* x, const double* y, i64 n, double* out, bool do_sqrt, const Comm* comm) {
+  if (!comm || !comm->distributed()) {
+    vdot_dev(x, y, n, out, do_sqrt);
+    return;
+  }
+  vdot_dev(x, y, n, out, false);
+  comm->sum_ordered(out, 1);
+  if (do_sqrt) {
+    k_sqrt1<<<1, 1, 0, stream()>>>(out);
+    CF_LAUNCHED();
+  }
+}
+
 }  // namespace
 
 GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
-                  double* x) {
+                  double* x, const Comm* comm) {
   if (!(o.rtol > 0.0 && o.rtol < 1.0)) fail(CF_ERR_INVALID_ARGUMENT, "gmres: rtol must be in (0,1)");
   if (o.restart < 1 || o.restart > 255) fail(CF_ERR_UNSUPPORTED, "gmres: restart must be in [1, 255]");
   GmresResult res;
   vfill(x, 0.0, n);
   DevBuf<double> sc(2);
-  vdot_dev(rhs, rhs, n, sc.p, true);
+  gdot(rhs, rhs, n, sc.p, true, comm);
   double bnorm = 0.0;
   CF_CUDA(cudaMemcpyAsync(&bnorm, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
@@ -65,7 +82,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     }
   };
   while (res.iterations < o.max_iter) {
-    vdot_dev(r.p, r.p, n, sc.p, true);
+    gdot(r.p, r.p, n, sc.p, true, comm);
     double beta = 0.0;
     CF_CUDA(cudaMemcpyAsync(&beta, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
@@ -88,11 +105,11 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
       double* w = V.p + i64(j + 1) * n;
       apply_op(V.p + i64(j) * n, w);
       for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
-        vdot_dev(w, V.p + i64(i) * n, n, hd.p + i, false);
+        gdot(w, V.p + i64(i) * n, n, hd.p + i, false, comm);
         k_axpy_dev<<<grid_for(n, 256), 256, 0, stream()>>>(n, hd.p + i, V.p + i64(i) * n, w);
         CF_LAUNCHED();
       }
-      vdot_dev(w, w, n, hd.p + j + 1, true);
+      gdot(w, w, n, hd.p + j + 1, true, comm);
       CF_CUDA(cudaMemcpyAsync(hcol.data(), hd.p, size_t(j + 2) * sizeof(double), cudaMemcpyDeviceToHost, stream()));
       CF_CUDA(cudaStreamSynchronize(stream()));
       for (int i = 0; i <= j + 1; ++i) Hij(i, j) = hcol[i];
@@ -146,7 +163,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     }
     op(x, z.p);
     vsub(rhs, z.p, r.p, n);  // r = b - op(x)
-    vdot_dev(r.p, r.p, n, sc.p, true);
+    gdot(r.p, r.p, n, sc.p, true, comm);
     double rn = 0.0;
     CF_CUDA(cudaMemcpyAsync(&rn, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 
+#include "cf_comm.hpp"
 #include "cf_vec.hpp"
 
 namespace cfb {
@@ -38,25 +39,30 @@ __global__ void k_extrapolate(i64 V, int step, const double* __restrict__ po, co
   }
 }
 
+// Kernels below run over the slab's owned vertices lv in [0, nv) (v = v_lo + lv; the full slab of
+// one GPU is v = lv).  Global-layout arrays (x, phi_old, constraint flags) are indexed by v,
+// local-layout ones (R, delta, active-set state) by lv.
+
 // active-set test + history push (solver.cpp:81-96).  tracked dofs push their bit.
-__global__ void k_active1(i64 V, i64 nu, double c, double tol, const double* __restrict__ x,
+__global__ void k_active1(Slab sl, i64 nu, double c, double tol, const double* __restrict__ x,
                           const double* __restrict__ po, const double* __restrict__ R,
                           const std::uint8_t* __restrict__ base_flag, const std::uint8_t* __restrict__ fixed,
                           std::uint8_t* __restrict__ active, std::uint8_t* __restrict__ tracked,
-                          unsigned long long* __restrict__ hist, int* __restrict__ any_tracked) {
-  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= V) return;
+                          unsigned long long* __restrict__ hist, int* __restrict__ any_tracked, int d) {
+  const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lv >= sl.nv()) return;
+  const i64 v = sl.v_lo + lv;
   const i64 dof = nu + v;
-  bool a = fixed[v] != 0;
+  bool a = fixed[lv] != 0;
   if (!base_flag[dof]) {  // candidates: phi dofs not constrained by the base set
-    const double lambda = -R[dof];
+    const double lambda = -R[d * sl.nv() + lv];
     if (c * (x[dof] - po[v]) + lambda > tol) a = true;
   }
-  active[v] = a ? 1 : 0;
-  bool tr = tracked[v] != 0 || a;
+  active[lv] = a ? 1 : 0;
+  bool tr = tracked[lv] != 0 || a;
   if (tr) {
-    tracked[v] = 1;
-    hist[v] = (hist[v] << 1) | (a ? 1ull : 0ull);
+    tracked[lv] = 1;
+    hist[lv] = (hist[lv] << 1) | (a ? 1ull : 0ull);
     *any_tracked = 1;
   }
 }
@@ -86,31 +92,58 @@ __global__ void k_active2(i64 V, int len, int window, int toggles, const std::ui
   if (a != prev[v]) atomicAdd(&counts[1], 1);
 }
 
-// full constraint set: base + active phi = phi_old (solver.cpp:109-111, fem.cpp:258-263)
-__global__ void k_full_constraints(i64 nt, i64 nu, const std::uint8_t* __restrict__ bflag,
+// full constraint set on the owned phi dofs: base + active phi = phi_old (solver.cpp:109-111,
+// fem.cpp:258-263); the u dofs keep the base (Dirichlet) lines
+__global__ void k_full_constraints(Slab sl, i64 nu, const std::uint8_t* __restrict__ bflag,
                                    const double* __restrict__ binh, const std::uint8_t* __restrict__ active,
                                    const double* __restrict__ po, std::uint8_t* __restrict__ flag,
                                    double* __restrict__ inh) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
+  const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lv >= sl.nv()) return;
+  const i64 v = sl.v_lo + lv, i = nu + v;
   std::uint8_t f = bflag[i];
   double g = binh[i];
-  if (i >= nu && !f && active[i - nu]) {
+  if (!f && active[lv]) {
     f = 1;
-    g = po[i - nu];
+    g = po[v];
   }
   flag[i] = f;
   inh[i] = g;
 }
 
-// distribute + "moved" flag (solver.cpp:114-116)
-__global__ void k_distribute_moved(i64 nt, const std::uint8_t* __restrict__ flag, const double* __restrict__ inh,
-                                   double* __restrict__ x, int* __restrict__ moved) {
+// local dof i of the slab -> global dof
+__device__ __forceinline__ i64 global_dof(const Slab& sl, int d, i64 nu, i64 i) {
+  const i64 nul = d * sl.nv();
+  return i < nul ? d * sl.v_lo + i : nu + sl.v_lo + (i - nul);
+}
+
+// distribute on the owned dofs of the global-layout x + "moved" flag (solver.cpp:114-116)
+__global__ void k_distribute_moved(Slab sl, int d, i64 nu, const std::uint8_t* __restrict__ flag,
+                                   const double* __restrict__ inh, double* __restrict__ x, int* __restrict__ moved) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= nt || !flag[i]) return;
-  const double old = x[i];
-  x[i] = inh[i];
-  if (fabs(x[i] - old) > 0.0) *moved = 1;
+  if (i >= (d + 1) * sl.nv()) return;
+  const i64 gi = global_dof(sl, d, nu, i);
+  if (!flag[gi]) return;
+  const double old = x[gi];
+  x[gi] = inh[gi];
+  if (fabs(x[gi] - old) > 0.0) *moved = 1;
+}
+
+// distribute on a local-layout vector (fem.cpp:229-247 on uniform meshes)
+__global__ void k_distribute_local(Slab sl, int d, i64 nu, const std::uint8_t* __restrict__ flag,
+                                   const double* __restrict__ inh, double* __restrict__ v, int homogeneous) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= (d + 1) * sl.nv()) return;
+  const i64 gi = global_dof(sl, d, nu, i);
+  if (flag[gi]) v[i] = homogeneous ? 0.0 : inh[gi];
+}
+
+// x(owned, global layout) += a * delta(local layout)
+__global__ void k_axpy_owned(Slab sl, int d, i64 nu, double a, const double* __restrict__ delta,
+                             double* __restrict__ x) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= (d + 1) * sl.nv()) return;
+  x[global_dof(sl, d, nu, i)] += a * delta[i];
 }
 
 __global__ void k_zero_active(i64 V, i64 nu, const std::uint8_t* __restrict__ active, double* __restrict__ R) {
@@ -123,12 +156,13 @@ __global__ void k_neg(i64 n, const double* __restrict__ a, double* __restrict__ 
   if (i < n) b[i] = -a[i];
 }
 
-// rigid body modes (linsolve.cpp:320-343), zero rows on constrained u dofs
-__global__ void k_rigid(GridDesc g, const std::uint8_t* __restrict__ flag, double* __restrict__ B) {
-  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= g.V) return;
+// rigid body modes (linsolve.cpp:320-343) of the owned vertices, zero rows on constrained u dofs
+__global__ void k_rigid(GridDesc g, Slab sl, const std::uint8_t* __restrict__ flag, double* __restrict__ B) {
+  const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lv >= sl.nv()) return;
+  const i64 v = sl.v_lo + lv;
   const int d = g.d;
-  const i64 n = g.n_u();
+  const i64 n = d * sl.nv();
   const i64 ix = v % g.nn, iy = (v / g.nn) % g.nn, iz = (d == 3) ? v / (g.nn * g.nn) : 0;
   const double x0 = -g.K + double(ix * (i64(1) << (16 - g.r))) * g.unit;
   const double x1 = -g.K + double(iy * (i64(1) << (16 - g.r))) * g.unit;
@@ -150,24 +184,24 @@ __global__ void k_rigid(GridDesc g, const std::uint8_t* __restrict__ flag, doubl
     row[1][5] = x0;
   }
   for (int a = 0; a < d; ++a) {
-    const i64 dof = v * d + a;
-    const bool con = flag[dof] != 0;
-    for (int c = 0; c < m; ++c) B[i64(c) * n + dof] = con ? 0.0 : row[a][c];
+    const bool con = flag[v * d + a] != 0;
+    for (int c = 0; c < m; ++c) B[i64(c) * n + lv * d + a] = con ? 0.0 : row[a][c];
   }
 }
 
-__global__ void k_phi_modes(i64 V, i64 nu, const std::uint8_t* __restrict__ flag, double* __restrict__ B,
+__global__ void k_phi_modes(Slab sl, i64 nu, const std::uint8_t* __restrict__ flag, double* __restrict__ B,
                             int* __restrict__ pnode, int* __restrict__ unode, int d) {
-  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  B[v] = flag[nu + v] ? 0.0 : 1.0;
-  pnode[v] = int(v);
-  for (int a = 0; a < d; ++a) unode[v * d + a] = int(v);
+  const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lv >= sl.nv()) return;
+  B[lv] = flag[nu + sl.v_lo + lv] ? 0.0 : 1.0;
+  pnode[lv] = int(lv);
+  for (int a = 0; a < d; ++a) unode[lv * d + a] = int(lv);
 }
 
-__global__ void k_feas(i64 V, i64 nu, const double* __restrict__ x, const double* __restrict__ po, double* out) {
-  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= V) return;
+__global__ void k_feas(Slab sl, i64 nu, const double* __restrict__ x, const double* __restrict__ po, double* out) {
+  const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (lv >= sl.nv()) return;
+  const i64 v = sl.v_lo + lv;
   const double d = x[nu + v] - po[v];
   // max via the ordered-int trick for doubles (handles negatives)
   long long bits = __double_as_longlong(d);
@@ -196,10 +230,84 @@ struct Timer {
 
 }  // namespace
 
-void rigid_body_modes(const Problem& P, const Constraints& c, double* B) {
-  k_rigid<<<grid_for(P.g.V, 256), 256, 0, stream()>>>(P.g, c.flag.p, B);
+void rigid_body_modes(const Problem& P, const Constraints& c, double* B, const Slab* slab) {
+  const Slab sl = slab ? *slab : full_slab(P.g);
+  k_rigid<<<grid_for(sl.nv(), 256), 256, 0, stream()>>>(P.g, sl, c.flag.p, B);
   CF_LAUNCHED();
 }
+
+Slab rank_slab(const GridDesc& g, int rank, int size) {
+  if (size < 1 || rank < 0 || rank >= size) fail(CF_ERR_INVALID_ARGUMENT, "rank_slab: bad rank / size");
+  if (g.nn < size) fail(CF_ERR_UNSUPPORTED, "rank_slab: fewer vertex planes than ranks");
+  return make_slab(g, g.nn * rank / size, g.nn * (rank + 1) / size);
+}
+
+namespace {
+
+// Ghost-plane exchange of a global-layout vector [u (d V) | phi (V)] of element size es: the
+// owned boundary planes go to the neighbours, their planes land in this rank's ghost planes.
+void halo_global(const Comm& cm, const GridDesc& g, const Slab& sl, void* vec, size_t es, bool u_part, bool p_part) {
+  if (!cm.distributed()) return;
+  auto* b = static_cast<unsigned char*>(vec);
+  const i64 d = g.d, pl = sl.plane;
+  std::vector<HaloOp> ops;
+  auto add = [&](i64 send_off, i64 recv_off, i64 count, int peer) {
+    ops.push_back({b + size_t(send_off) * es, b + size_t(recv_off) * es, size_t(count) * es, peer});
+  };
+  if (cm.rank > 0) {
+    if (u_part) add(d * sl.v_lo, d * (sl.v_lo - pl), d * pl, cm.rank - 1);
+    if (p_part) add(g.n_u() + sl.v_lo, g.n_u() + sl.v_lo - pl, pl, cm.rank - 1);
+  }
+  if (cm.rank + 1 < cm.size) {
+    if (u_part) add(d * (sl.v_hi - pl), d * sl.v_hi, d * pl, cm.rank + 1);
+    if (p_part) add(g.n_u() + sl.v_hi - pl, g.n_u() + sl.v_hi, pl, cm.rank + 1);
+  }
+  cm.sendrecv(ops);
+}
+
+// local-layout z [u_own | phi_own] -> ext-layout e [u_ext | phi_ext] (interior copy + ghost planes)
+void to_ext(const Comm& cm, const GridDesc& g, const Slab& sl, const double* z, double* e) {
+  const i64 d = g.d, nv = sl.nv(), ne = sl.ne(), pl = sl.plane, lo = sl.v_lo - sl.ve_lo;
+  const i64 nul = d * nv, nue = d * ne;
+  CF_CUDA(cudaMemcpyAsync(e + d * lo, z, size_t(nul) * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+  CF_CUDA(cudaMemcpyAsync(e + nue + lo, z + nul, size_t(nv) * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+  std::vector<HaloOp> ops;
+  const size_t ub = size_t(d * pl) * sizeof(double), pb = size_t(pl) * sizeof(double);
+  if (cm.rank > 0) {
+    ops.push_back({z, e, ub, cm.rank - 1});
+    ops.push_back({z + nul, e + nue, pb, cm.rank - 1});
+  }
+  if (cm.rank + 1 < cm.size) {
+    ops.push_back({z + nul - d * pl, e + d * (ne - pl), ub, cm.rank + 1});
+    ops.push_back({z + nul + nv - pl, e + nue + ne - pl, pb, cm.rank + 1});
+  }
+  cm.sendrecv(ops);
+}
+
+// every rank's owned part of a global-layout vector to every rank
+void allgather_owned(const Comm& cm, const GridDesc& g, double* x) {
+  if (!cm.distributed()) return;
+  std::vector<HaloOp> ops;
+  for (int r = 0; r < cm.size; ++r) {
+    const Slab s = rank_slab(g, r, cm.size);
+    ops.push_back({nullptr, x + g.d * s.v_lo, size_t(g.d * s.nv()) * sizeof(double), r});
+    ops.push_back({nullptr, x + g.n_u() + s.v_lo, size_t(s.nv()) * sizeof(double), r});
+  }
+  cm.bcast_many(ops);
+}
+
+double gnorm(const Comm* cm, const double* v, i64 n) {
+  if (!cm || !cm->distributed()) return vnorm(v, n);
+  double* s = scalar_buf(1);
+  vdot_dev(v, v, n, s, false);
+  cm->sum_ordered(s, 1);
+  double h = 0.0;
+  CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  return std::sqrt(h);
+}
+
+}  // namespace
 
 double slit_band_edge(const Problem& P, const cf_material& mat) {  // model.cpp:28-50 (uniform cells)
   const GridDesc& g = P.g;
@@ -260,9 +368,16 @@ std::vector<double> initial_crack(const Problem& P, const cf_material& mat, doub
 }
 
 NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& mat, const cf_regularization& reg,
-                                    const cf_solver_options& opts) {
+                                    const cf_solver_options& opts, const Comm* comm, const Slab* slab) {
   const GridDesc& g = P.g;
+  const Comm solo;
+  const Comm& cm = comm ? *comm : solo;
+  const bool dist = cm.distributed();
+  const Slab sl = slab ? *slab : (dist ? rank_slab(g, cm.rank, cm.size) : full_slab(g));
+  if (!dist && !sl.full(g)) fail(CF_ERR_INVALID_ARGUMENT, "newton_active_set_step: a partial slab needs a communicator");
+  const int d = g.d;
   const i64 nu = g.n_u(), V = g.V, nt = g.n_total();
+  const i64 nv = sl.nv(), nul = d * nv, ntl = (d + 1) * nv;  // this rank's rows
   if (opts.cycle_window < 1 || opts.cycle_window > 64)
     fail(CF_ERR_UNSUPPORTED, "newton_active_set_step: cycle_window must be in [1, 64]");
   NewtonReport report;
@@ -274,14 +389,15 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   k_extrapolate<<<grid_for(V, 256), 256, 0, stream()>>>(V, st.step, st.phi_old.p, st.phi_prev2.p, pt.p);
   CF_LAUNCHED();
   const double c = opts.active_set_c_scale * mat.G_c / reg.eps;
-  DevBuf<std::uint8_t> fixed(V), active(V), prev(V), tracked(V);
-  DevBuf<unsigned long long> hist(V);
+  DevBuf<std::uint8_t> fixed(nv), active(nv), prev(nv), tracked(nv);
+  DevBuf<unsigned long long> hist(nv);
   fixed.zero();
   prev.zero();
   tracked.zero();
   hist.zero();
   DevBuf<int> flags(4);
-  DevBuf<double> R(nt), rhs(nt), delta(nt);
+  DevBuf<double> R(ntl), rhs(ntl), delta(ntl);
+  DevBuf<double> ext(dist ? (d + 1) * sl.ne() : 0);  // GMRES operator input with ghost planes
   int hist_len = 0;
   double res0 = -1.0;
   std::unique_ptr<BlockPrec> prec;
@@ -289,53 +405,64 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   full.prob = &P;
   full.flag.alloc(nt);
   full.inhom.alloc(nt);
-  DevBuf<double> Bu(nu * (g.d == 2 ? 3 : 6)), Bp(V);
-  DevBuf<int> unode(nu), pnode(V);
+  CF_CUDA(cudaMemcpyAsync(full.flag.p, base->flag.p, size_t(nt), cudaMemcpyDeviceToDevice, stream()));
+  CF_CUDA(cudaMemcpyAsync(full.inhom.p, base->inhom.p, size_t(nt) * sizeof(double), cudaMemcpyDeviceToDevice,
+                          stream()));
+  DevBuf<double> Bu(nul * (d == 2 ? 3 : 6)), Bp(nv);
+  DevBuf<int> unode(nul), pnode(nv);
+  const unsigned gv = grid_for(nv, 256), gl = grid_for(ntl, 256);
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
     {
       Timer t(&T.residual);
-      assemble_residual(P, *base, mat, reg, x, pt.p, R.p);
+      assemble_residual(P, *base, mat, reg, x, pt.p, R.p, &sl);
     }
     int changes = 0, asize = 0;
     {
       Timer t(&T.active_set);
       flags.zero();
-      k_active1<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, c, 1e-14 * c, x, st.phi_old.p, R.p, base->flag.p,
-                                                        fixed.p, active.p, tracked.p, hist.p, flags.p + 2);
+      k_active1<<<gv, 256, 0, stream()>>>(sl, nu, c, 1e-14 * c, x, st.phi_old.p, R.p, base->flag.p, fixed.p,
+                                          active.p, tracked.p, hist.p, flags.p + 2, d);
       CF_LAUNCHED();
-      if (read_dev(flags.p + 2)) ++hist_len;
-      k_active2<<<grid_for(V, 256), 256, 0, stream()>>>(V, hist_len, opts.cycle_window, opts.cycle_toggles,
-                                                        tracked.p, hist.p, fixed.p, active.p, prev.p, flags.p);
+      long long any = read_dev(flags.p + 2);
+      cm.max_i64(&any, 1);
+      if (any) ++hist_len;
+      k_active2<<<gv, 256, 0, stream()>>>(nv, hist_len, opts.cycle_window, opts.cycle_toggles, tracked.p, hist.p,
+                                          fixed.p, active.p, prev.p, flags.p);
       CF_LAUNCHED();
       int hc[2];
       CF_CUDA(cudaMemcpyAsync(hc, flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream()));
       CF_CUDA(cudaStreamSynchronize(stream()));
-      asize = hc[0];
-      changes = hc[1];
-      k_full_constraints<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, nu, base->flag.p, base->inhom.p, active.p,
-                                                                  st.phi_old.p, full.flag.p, full.inhom.p);
+      long long counts[2] = {hc[0], hc[1]};
+      cm.sum_i64(counts, 2);
+      asize = int(counts[0]);
+      changes = int(counts[1]);
+      k_full_constraints<<<gv, 256, 0, stream()>>>(sl, nu, base->flag.p, base->inhom.p, active.p, st.phi_old.p,
+                                                   full.flag.p, full.inhom.p);
       CF_LAUNCHED();
+      halo_global(cm, g, sl, full.flag.p, 1, false, true);  // neighbours' active phi columns
       CF_CUDA(cudaMemsetAsync(flags.p + 3, 0, sizeof(int), stream()));
-      k_distribute_moved<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, full.flag.p, full.inhom.p, x, flags.p + 3);
+      k_distribute_moved<<<gl, 256, 0, stream()>>>(sl, d, nu, full.flag.p, full.inhom.p, x, flags.p + 3);
       CF_LAUNCHED();
+      halo_global(cm, g, sl, x, sizeof(double), false, true);
     }
-    const bool moved = read_dev(flags.p + 3) != 0;
+    long long moved = read_dev(flags.p + 3);
+    cm.max_i64(&moved, 1);
     {
       Timer t(&T.residual);
       if (moved) {
-        assemble_residual(P, full, mat, reg, x, pt.p, R.p);
+        assemble_residual(P, full, mat, reg, x, pt.p, R.p, &sl);
       } else {
-        k_zero_active<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, active.p, R.p);
+        k_zero_active<<<gv, 256, 0, stream()>>>(nv, nul, active.p, R.p);
         CF_LAUNCHED();
       }
     }
-    const double res = vnorm(R.p, nt);
+    const double res = gnorm(comm, R.p, ntl);
     if (res0 < 0.0) res0 = res;
     NewtonIter rec{res, asize, changes, 0};
     const bool small = res <= std::max(opts.newton_tol * res0, opts.newton_abs_floor);
     if (changes == 0 && small) {
       report.its.push_back(rec);
-      if (opts.log)
+      if (opts.log && cm.rank == 0)
         std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=0\n", st.step, it, res, asize,
                     changes);
       report.converged = true;
@@ -344,68 +471,111 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
     std::unique_ptr<BlockSystem> J;
     {
       Timer t(&T.jacobian);
-      J = assemble_jacobian(P, full, mat, reg, x, pt.p);
+      J = assemble_jacobian(P, full, mat, reg, x, pt.p, &sl);
+      if (dist) {  // lane split of the undivided matrix, so every row reduces as on one GPU
+        long long tot[4] = {J->uu->nnz, J->uu->rows, J->pu->nnz, J->pu->rows};
+        cm.sum_i64(tot, 4);
+        J->uu->mean_hint = tot[1] ? double(tot[0]) / double(tot[1]) : 0.0;
+        J->pu->mean_hint = tot[3] ? double(tot[2]) / double(tot[3]) : 0.0;
+      }
     }
     if (!prec || !opts.freeze_preconditioner) {
       Timer t(&T.amg_setup);
       NullspaceDev ns;
-      rigid_body_modes(P, full, Bu.p);
-      k_phi_modes<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, full.flag.p, Bp.p, pnode.p, unode.p, g.d);
+      rigid_body_modes(P, full, Bu.p, &sl);
+      k_phi_modes<<<gv, 256, 0, stream()>>>(sl, nu, full.flag.p, Bp.p, pnode.p, unode.p, d);
       CF_LAUNCHED();
       ns.u_node = unode.p;
       ns.u_modes = Bu.p;
-      ns.m_u = g.d == 2 ? 3 : 6;
+      ns.m_u = d == 2 ? 3 : 6;
       ns.p_node = pnode.p;
       ns.p_modes = Bp.p;
       // hierarchies whose inputs are bitwise unchanged (M_uu within a load step: it depends only
       // on phi_tilde and the Dirichlet set) are reused; a rebuild would be bit-identical
-      auto next = build_block_prec(*J, opts.prec_kind, opts.amg, &ns, prec.get());
-      prec = std::move(next);
+      if (dist) {
+        // block-Jacobi over the slabs: the preconditioner of each rank is built on the diagonal
+        // block of its rows (owned columns only); one GPU is the undivided block
+        BlockSystem Jl;
+        Jl.d = d;
+        Jl.nu = nul;
+        Jl.np = nv;
+        const i64 lo = sl.v_lo - sl.ve_lo;
+        Jl.uu = csr_extract_cols(*J->uu, d * lo, d * (lo + nv));
+        Jl.pp = csr_extract_cols(*J->pp, lo, lo + nv);
+        prec = build_block_prec(Jl, opts.prec_kind, opts.amg, &ns, prec.get());
+      } else {
+        prec = build_block_prec(*J, opts.prec_kind, opts.amg, &ns, prec.get());
+      }
     }
     GmresResult lin;
     {
       Timer t(&T.gmres);
-      k_neg<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, R.p, rhs.p);
+      k_neg<<<gl, 256, 0, stream()>>>(ntl, R.p, rhs.p);
       CF_LAUNCHED();
       const BlockSystem& Jr = *J;
-      DevOp op = [&Jr](const double* in, double* out) { block_apply(Jr, in, out); };
+      DevOp op;
+      if (dist) {
+        double* e = ext.p;
+        op = [&Jr, &cm, &g, &sl, e](const double* in, double* out) {
+          to_ext(cm, g, sl, in, e);
+          block_apply(Jr, e, out);
+        };
+      } else {
+        op = [&Jr](const double* in, double* out) { block_apply(Jr, in, out); };
+      }
       const BlockPrec& Pr = *prec;
       DevOp pop = [&Pr](const double* in, double* out) { Pr.apply(in, out); };
-      lin = gmres(op, &pop, rhs.p, nt, opts.gmres, delta.p);
+      lin = gmres(op, &pop, rhs.p, ntl, opts.gmres, delta.p, comm);
     }
     if (!lin.converged && !lin.breakdown) fail(CF_ERR_NUMERICAL, "newton_active_set_step: GMRES stagnated at max_iter");
     rec.gmres_iterations = lin.iterations;
     report.its.push_back(rec);
-    if (opts.log)
+    if (opts.log && cm.rank == 0)
       std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=%d\n", st.step, it, res, asize, changes,
                   lin.iterations);
-    distribute(full, delta.p, true);
-    vaxpy(1.0, delta.p, x, nt);
+    auto update_x = [&](double a) {
+      if (sl.full(g)) {
+        vaxpy(a, delta.p, x, nt);
+      } else {
+        k_axpy_owned<<<gl, 256, 0, stream()>>>(sl, d, nu, a, delta.p, x);
+        CF_LAUNCHED();
+        halo_global(cm, g, sl, x, sizeof(double), true, true);
+      }
+    };
+    if (sl.full(g)) {
+      distribute(full, delta.p, true);
+    } else {
+      k_distribute_local<<<gl, 256, 0, stream()>>>(sl, d, nu, full.flag.p, full.inhom.p, delta.p, 1);
+      CF_LAUNCHED();
+    }
+    update_x(1.0);
     if (opts.damping) {
       double scale = 1.0;
       for (int half = 0; half < 4; ++half) {
-        assemble_residual(P, full, mat, reg, x, pt.p, R.p);
-        if (vnorm(R.p, nt) <= 10.0 * res) break;
+        assemble_residual(P, full, mat, reg, x, pt.p, R.p, &sl);
+        if (gnorm(comm, R.p, ntl) <= 10.0 * res) break;
         scale *= 0.5;
-        vaxpy(-scale, delta.p, x, nt);
+        update_x(-scale);
       }
     }
-    CF_CUDA(cudaMemcpyAsync(prev.p, active.p, size_t(V), cudaMemcpyDeviceToDevice, stream()));
+    CF_CUDA(cudaMemcpyAsync(prev.p, active.p, size_t(nv), cudaMemcpyDeviceToDevice, stream()));
   }
   DevBuf<double> mx(1);
   {
     const long long lowest = 0x8000000000000000LL;  // below every mapped double
     CF_CUDA(cudaMemcpyAsync(mx.p, &lowest, sizeof(lowest), cudaMemcpyHostToDevice, stream()));
   }
-  k_feas<<<grid_for(V, 256), 256, 0, stream()>>>(V, nu, x, st.phi_old.p, mx.p);
+  k_feas<<<gv, 256, 0, stream()>>>(sl, nu, x, st.phi_old.p, mx.p);
   CF_LAUNCHED();
   long long bits = 0;
   CF_CUDA(cudaMemcpyAsync(&bits, mx.p, sizeof(bits), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  cm.max_i64(&bits, 1);
   bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
   double viol;
   std::memcpy(&viol, &bits, sizeof(viol));
   report.feasibility = std::max(0.0, viol);  // solver.cpp:183-186 starts from viol = 0
+  allgather_owned(cm, g, x);  // every rank leaves with the full solution
   return report;
 }
 

@@ -888,6 +888,67 @@ void csr_diagonal(const Csr& A, double* d) {
   CF_LAUNCHED();
 }
 
+namespace {
+// columns are sorted, so a row's entries in [lo, hi) are one contiguous run
+__device__ inline void col_run(const i64* p, const int* c, i64 i, int lo, int hi, i64& b, i64& e) {
+  i64 a = p[i], z = p[i + 1];
+  while (a < z) {  // first entry >= lo
+    const i64 m = (a + z) >> 1;
+    if (c[m] < lo) a = m + 1; else z = m;
+  }
+  b = a;
+  z = p[i + 1];
+  while (a < z) {  // first entry >= hi
+    const i64 m = (a + z) >> 1;
+    if (c[m] < hi) a = m + 1; else z = m;
+  }
+  e = a;
+}
+
+__global__ void k_extract_count(i64 rows, const i64* __restrict__ p, const int* __restrict__ c, int lo, int hi,
+                                i64* __restrict__ cnt) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  i64 b, e;
+  col_run(p, c, i, lo, hi, b, e);
+  cnt[i] = e - b;
+}
+
+// warp per row: coalesced copy of the row's run, columns shifted by -lo
+__global__ void k_extract_fill(i64 rows, const i64* __restrict__ p, const int* __restrict__ c,
+                               const double* __restrict__ v, int lo, int hi, const i64* __restrict__ np,
+                               int* __restrict__ nc, double* __restrict__ nv) {
+  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= rows) return;
+  i64 b, e;
+  col_run(p, c, i, lo, hi, b, e);
+  const i64 o = np[i];
+  for (i64 k = b + lane; k < e; k += 32) {
+    nc[o + (k - b)] = c[k] - lo;
+    nv[o + (k - b)] = v[k];
+  }
+}
+}  // namespace
+
+std::unique_ptr<Csr> csr_extract_cols(const Csr& A, i64 lo, i64 hi) {
+  auto C = std::make_unique<Csr>();
+  C->rows = A.rows;
+  C->cols = hi - lo;
+  C->ptr.alloc(A.rows + 1);
+  C->ptr.zero();
+  k_extract_count<<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, int(lo), int(hi), C->ptr.p);
+  CF_LAUNCHED();
+  scan_excl(C->ptr.p, A.rows + 1);
+  C->nnz = read_i64(C->ptr.p + A.rows);
+  C->col.alloc(C->nnz);
+  C->val.alloc(C->nnz);
+  k_extract_fill<<<grid_for(A.rows * 32, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, int(lo),
+                                                                   int(hi), C->ptr.p, C->col.p, C->val.p);
+  CF_LAUNCHED();
+  return C;
+}
+
 std::unique_ptr<Csr> csr_copy(const Csr& A) {
   auto C = std::make_unique<Csr>();
   C->rows = A.rows;

@@ -140,8 +140,8 @@ void launch_phi(const BlockSystem& J, const double* x, double* y) {
   const int block = 256;
   const i64 threads = J.np * TPR;
   k_spmv_phi<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(J.np, J.pu->ptr.p, J.pu->col.p, J.pu->val.p, x,
-                                                                    J.pp->ptr.p, J.pp->col.p, J.pp->val.p, x + J.nu,
-                                                                    y + J.nu);
+                                                                    J.pp->ptr.p, J.pp->col.p, J.pp->val.p,
+                                                                    x + J.in_u(), y + J.nu);
   CF_LAUNCHED();
 }
 
@@ -178,7 +178,7 @@ bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double
 // one batch of TPR*U slots should cover a typical row.
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add) {
   if (A.rows == 0) return;
-  const double mean = double(A.nnz) / double(A.rows);
+  const double mean = A.mean_hint >= 0.0 ? A.mean_hint : double(A.nnz) / double(A.rows);
   if (mean > 64) launch_b<16, 4>(A, x, y, add);
   else if (mean > 24) launch_b<8, 4>(A, x, y, add);
   else if (mean > 12) launch_b<4, 5>(A, x, y, add);
@@ -190,7 +190,7 @@ void csr_spmv(const Csr& A, const double* x, double* y, double) { csr_spmv_add(A
 void block_apply(const BlockSystem& J, const double* x, double* y) {
   csr_spmv_add(*J.uu, x, y, nullptr);
   if (J.np == 0) return;
-  const double mean = double(J.pu->nnz) / double(J.np);
+  const double mean = J.pu->mean_hint >= 0.0 ? J.pu->mean_hint : double(J.pu->nnz) / double(J.np);
   if (mean > 64) launch_phi<16, 4>(J, x, y);
   else if (mean > 24) launch_phi<8, 4>(J, x, y);
   else launch_phi<4, 5>(J, x, y);
