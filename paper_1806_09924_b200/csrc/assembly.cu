@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "cf_types.hpp"
@@ -618,6 +619,244 @@ __global__ void __launch_bounds__(fill_wpb<D>() * 32) k_jac_fill_warp(
   }
 }
 
+// Pair-parallel fill pass (persistent grid, one warp per row vertex v).  The work of a row
+// vertex is 2^d cells x 2^d corners: unit (i, l) = the element block of v's i-th adjacent cell (in
+// reference order) for v's corner k and column corner l, summed over q exactly as the reference
+// does.  The 32 lanes take 32 units per round (3d: cells 0-3, then 4-7), so every lane does useful
+// FP64 work (a slot-per-lane form leaves ~3/4 of the lanes idle on a cell that does not hold
+// their column vertex).  After each round lane s adds, for stencil slot s, the round's units of
+// the cells holding w in reference order, so every value is the reference's sum.  The cell list
+// lives in registers (lane t < 2^d owns candidate cell t, ranks by shuffles) and the integrand
+// table in shared memory.
+template <int D>
+constexpr int pair_wpb() { return 4; }
+
+template <int D>
+struct PairSmem {
+  static constexpr int NQ = 1 << D, NV = 1 << D, NR = D * D + D + 1;
+  double val[NQ][NV][NV][D * D];
+  double s[NQ][NV], gp[NQ][NV][D], gg[NQ][NV][NV], w[NQ];
+  double res[pair_wpb<D>()][32][NR];
+};
+
+template <int D>
+__global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
+    GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
+    const std::uint8_t* __restrict__ flag, const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
+    double* __restrict__ val_uu, const i64* __restrict__ ptr_pu, int* __restrict__ col_pu,
+    double* __restrict__ val_pu, const i64* __restrict__ ptr_pp, int* __restrict__ col_pp,
+    double* __restrict__ val_pp, Slab sl) {
+  constexpr int S = (D == 3) ? 27 : 9, NQ = 1 << D, NV = 1 << D, NC = 1 << D, NS = QS<D>::NS, CS = NQ * NS;
+  constexpr int NR = D * D + D + 1, CPR = 32 / NV, ROUNDS = (NC + CPR - 1) / CPR;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  PairSmem<D>& sm = *reinterpret_cast<PairSmem<D>*>(smraw);
+  for (int i = threadIdx.x; i < NQ * NV * NV * D * D; i += blockDim.x) {
+    const int ab = i % (D * D), l = (i / (D * D)) % NV, k = (i / (D * D * NV)) % NV, q = i / (D * D * NV * NV);
+    sm.val[q][k][l][ab] = T->val[q][k][l][ab / D][ab % D];
+  }
+  for (int i = threadIdx.x; i < NQ * NV; i += blockDim.x) {
+    const int q = i / NV, k = i % NV;
+    sm.s[q][k] = T->s[q][k];
+    for (int b = 0; b < D; ++b) sm.gp[q][k][b] = T->gp[q][k][b];
+    for (int l = 0; l < NV; ++l) sm.gg[q][k][l] = T->gg[q][k][l];
+  }
+  if (threadIdx.x < NQ) sm.w[threadIdx.x] = T->w[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const double c2k = 2.0 * (1.0 - cf.kap), c2p = 2.0 * cf.p, omk = 1.0 - cf.kap;
+  const double gce = cf.Gc / cf.eps, gcx = cf.Gc * cf.eps;
+  const i64 nu = g.n_u();
+  const i64 ushift = D * sl.ve_lo, pshift = sl.ve_lo;
+  qs -= sl.c_lo * CS;
+  double(*res)[NR] = sm.res[wv];
+  for (i64 lv = i64(blockIdx.x) * pair_wpb<D>() + wv; lv < sl.nv(); lv += i64(gridDim.x) * pair_wpb<D>()) {
+    const i64 v = sl.v_lo + lv;
+    i64 x, y, z;
+    vxyz<D>(g, v, x, y, z);
+    // ---- candidate cell t = lane (t < 2^d): v is its corner t; rank = reference order position
+    bool cvalid = false;
+    i64 ccell = 0, ckey = 0;
+    if (lane < NC) {
+      const i64 vc[3] = {x, y, z};
+      i64 anc[3] = {0, 0, 0};
+      cvalid = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        anc[a] = vc[a] - ((lane >> a) & 1);
+        cvalid = cvalid && anc[a] >= 0 && anc[a] < g.nc;
+      }
+      if (cvalid) {
+        ccell = anc[0] + g.nc * (anc[1] + g.nc * anc[2]);
+        ckey = cell_key(g, anc[0], anc[1], anc[2]);
+      }
+    }
+    int crank = 0;
+#pragma unroll
+    for (int t = 0; t < NC; ++t) {
+      const i64 kt = __shfl_sync(FULL, ckey, t);
+      const bool vt = __shfl_sync(FULL, cvalid, t);
+      crank += (vt && kt < ckey) ? 1 : 0;
+    }
+    const unsigned vmask = __ballot_sync(FULL, cvalid) & ((1u << NC) - 1u);
+    const int ncell = __popc(vmask);
+    auto src_of = [&](int i) {  // lane holding the i-th cell in reference order (uniform i)
+      return __ffs(__ballot_sync(FULL, cvalid && crank == i)) - 1;
+    };
+    // ---- slot lane setup
+    const int s = lane;
+    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
+    const i64 X = x + dx, Y = y + dy, Z = z + dz;
+    const bool slot_ok = s < S && X >= 0 && Y >= 0 && Z >= 0 && X < g.nn && Y < g.nn &&
+                         Z < ((D == 3) ? g.nn : 1);
+    const int del[3] = {dx, dy, dz};
+    PairBlocks<D> pb;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int b = 0; b < D; ++b) pb.uu[a][b] = 0.0;
+      pb.pu[a] = 0.0;
+    }
+    pb.pp = 0.0;
+#pragma unroll
+    for (int rd = 0; rd < ROUNDS; ++rd) {
+      // my unit: cell rank i = rd * CPR + lane / NV, column corner l = lane % NV
+      const int i = rd * CPR + lane / NV, l = lane % NV;
+      int src = -1;
+#pragma unroll
+      for (int t = 0; t < NC; ++t) {
+        const int rt = __shfl_sync(FULL, crank, t);
+        const bool vt = __shfl_sync(FULL, cvalid, t);
+        if (vt && rt == i) src = t;
+      }
+      const i64 mycell = __shfl_sync(FULL, ccell, src < 0 ? 0 : src);
+      if (lane < CPR * NV && src >= 0) {
+        const int k = src;  // v is corner t of candidate cell t
+        const double* cst = qs + mycell * CS;
+        double bu[D][D], bp[D], bpp = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+#pragma unroll
+          for (int b = 0; b < D; ++b) bu[a][b] = 0.0;
+          bp[a] = 0.0;
+        }
+#pragma unroll 2
+        for (int q = 0; q < NQ; ++q) {
+          const double* st = cst + q * NS;
+          double gl[D];
+#pragma unroll
+          for (int b = 0; b < D; ++b) gl[b] = sm.gp[q][l][b];
+          const double wg = __ldg(st);
+          const double* vl = sm.val[q][k][l];
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) bu[a][b] += wg * vl[a * D + b];
+          const double wq = sm.w[q];
+          const double phi = __ldg(st + 1), tre = __ldg(st + 2), see = __ldg(st + 3);
+          const double sk = sm.s[q][k], slv = sm.s[q][l];
+#pragma unroll
+          for (int b = 0; b < D; ++b) {
+            double sgl = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) sgl += __ldg(st + 4 + b * D + c) * gl[c];
+            bp[b] += wq * (c2k * phi * sgl + c2p * phi * gl[b]) * sk;
+          }
+          bpp += wq * ((omk * see + c2p * tre + gce) * slv * sk + gcx * sm.gg[q][k][l]);
+        }
+        double* o = res[lane];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+#pragma unroll
+          for (int b = 0; b < D; ++b) o[a * D + b] = bu[a][b];
+          o[D * D + a] = bp[a];
+        }
+        o[D * D + D] = bpp;
+      }
+      __syncwarp();
+      // slot lanes add this round's cells in reference order
+      const int i_end = min(ncell, (rd + 1) * CPR);
+      for (int ii = rd * CPR; ii < i_end; ++ii) {
+        const int k = src_of(ii);
+        if (!slot_ok) continue;
+        int lw = 0;
+        bool in = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const int la = ((k >> a) & 1) + del[a];
+          in = in && la >= 0 && la <= 1;
+          lw |= (la & 1) << a;
+        }
+        if (!in) continue;
+        const double* o = res[(ii - rd * CPR) * NV + lw];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+#pragma unroll
+          for (int b = 0; b < D; ++b) pb.uu[a][b] += o[a * D + b];
+          pb.pu[a] += o[D * D + a];
+        }
+        pb.pp += o[D * D + D];
+      }
+      __syncwarp();
+    }
+    (void)vmask;
+    if (!slot_ok) continue;
+    const i64 w = X + g.nn * (Y + g.nn * Z);
+    bool rowfree_u[D], colfree_u[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      rowfree_u[a] = flag[v * D + a] == 0;
+      colfree_u[a] = flag[w * D + a] == 0;
+    }
+    const bool rowfree_p = flag[nu + v] == 0, colfree_p = flag[nu + w] == 0;
+    const bool center = w == v;
+    i64 off_u = 0, off_p = 0;
+    for (int s2 = 0; s2 < s; ++s2) {
+      const int ex = s2 % 3 - 1, ey = (s2 / 3) % 3 - 1, ez = (D == 3) ? s2 / 9 - 1 : 0;
+      const i64 X2 = x + ex, Y2 = y + ey, Z2 = z + ez;
+      if (X2 < 0 || Y2 < 0 || Z2 < 0 || X2 >= g.nn || Y2 >= g.nn || Z2 >= ((D == 3) ? g.nn : 1)) continue;
+      const i64 w2 = X2 + g.nn * (Y2 + g.nn * Z2);
+#pragma unroll
+      for (int b = 0; b < D; ++b) off_u += flag[w2 * D + b] ? 0 : 1;
+      off_p += flag[nu + w2] ? 0 : 1;
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const i64 row = lv * D + a;
+      if (rowfree_u[a]) {
+        i64 pos = ptr_uu[row] + off_u;
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+          if (colfree_u[b]) {
+            col_uu[pos] = int(w * D + b - ushift);
+            val_uu[pos] = pb.uu[a][b];
+            ++pos;
+          }
+      } else if (center && ptr_uu[row + 1] > ptr_uu[row]) {
+        col_uu[ptr_uu[row]] = int(v * D + a - ushift);
+        val_uu[ptr_uu[row]] = pb.uu[a][a];
+      }
+    }
+    if (rowfree_p) {
+      i64 pos = ptr_pu[lv] + off_u;
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        if (colfree_u[b]) {
+          col_pu[pos] = int(w * D + b - ushift);
+          val_pu[pos] = pb.pu[b];
+          ++pos;
+        }
+      if (colfree_p) {
+        col_pp[ptr_pp[lv] + off_p] = int(w - pshift);
+        val_pp[ptr_pp[lv] + off_p] = pb.pp;
+      }
+    } else if (center && ptr_pp[lv + 1] > ptr_pp[lv]) {
+      col_pp[ptr_pp[lv]] = int(v - pshift);
+      val_pp[ptr_pp[lv]] = pb.pp;
+    }
+  }
+}
+
 __global__ void k_build_flags(GridDesc g, int clamp, std::uint8_t* flag) {
   const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= g.V) return;
@@ -873,12 +1112,23 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   J.pp->col.alloc(nnz[2]);
   J.pp->val.alloc(nnz[2]);
   int bps = 0;
-  constexpr int FT = fill_wpb<D>() * 32;
-  CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_jac_fill_warp<D>, FT, 0));
-  const int grid = std::max(1, bps) * rt().sm_count;
-  k_jac_fill_warp<D><<<grid, FT, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.uu->col.p,
-                                                 J.uu->val.p, J.pu->ptr.p, J.pu->col.p, J.pu->val.p, J.pp->ptr.p,
-                                                 J.pp->col.p, J.pp->val.p, sl);
+  if (std::getenv("CF_JAC_WARP")) {  // the slot-per-lane form, kept for A/B measurement
+    constexpr int FT = fill_wpb<D>() * 32;
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_jac_fill_warp<D>, FT, 0));
+    const int grid = std::max(1, bps) * rt().sm_count;
+    k_jac_fill_warp<D><<<grid, FT, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.uu->col.p,
+                                                   J.uu->val.p, J.pu->ptr.p, J.pu->col.p, J.pu->val.p,
+                                                   J.pp->ptr.p, J.pp->col.p, J.pp->val.p, sl);
+  } else {
+    constexpr int FT = pair_wpb<D>() * 32;
+    const int smem = int(sizeof(PairSmem<D>));
+    CF_CUDA(cudaFuncSetAttribute(k_jac_fill_pair<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_jac_fill_pair<D>, FT, smem));
+    const int grid = std::max(1, bps) * rt().sm_count;
+    k_jac_fill_pair<D><<<grid, FT, smem, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.uu->col.p,
+                                                   J.uu->val.p, J.pu->ptr.p, J.pu->col.p, J.pu->val.p,
+                                                   J.pp->ptr.p, J.pp->col.p, J.pp->val.p, sl);
+  }
   CF_LAUNCHED();
 }
 
