@@ -1130,6 +1130,9 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
                                                    J.pp->ptr.p, J.pp->col.p, J.pp->val.p, sl);
   }
   CF_LAUNCHED();
+  // value-only SpMV streams for the blocks whose pattern is the clamped stencil
+  csr_enable_stencil(*J.uu, StencilCols{1, D, g.nn, sl.v_lo, D * sl.ve_lo, 1.0 / double(g.nn)});
+  csr_enable_stencil(*J.pu, StencilCols{2, D, g.nn, sl.v_lo, D * sl.ve_lo, 1.0 / double(g.nn)});
 }
 
 std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& cs, const cf_material& m,

@@ -66,8 +66,21 @@ struct Constraints {
   i64 count = 0;
 };
 
+// Stencil-implicit columns of the uniform-grid blocks M_uu / M_phiu when the Dirichlet clamp is the
+// only u constraint: the columns of a row follow from its vertex (the 3^d neighbours whose u dofs
+// are free, ascending), so an SpMV can stream the values alone (8 instead of 12 bytes per entry).
+// Set by assemble_jacobian only after a device check that every stored column equals the computed
+// one; the stored columns stay (AMG setup reads them).
+struct StencilCols {
+  int kind = 0;  // 0 off, 1 rows are u dofs (row = lv * d + a), 2 rows are phi dofs (row = lv)
+  int d = 0;
+  i64 nn = 0, v_lo = 0, shift = 0;  // nodes per side, first row vertex, global -> stored column shift
+  double inv_nn = 0.0;
+};
+
 struct Csr {
   i64 rows = 0, cols = 0, nnz = 0;
+  StencilCols st;
   DevBuf<i64> ptr;
   DevBuf<int> col;
   DevBuf<double> val;
@@ -103,6 +116,7 @@ void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add); 
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);
 bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double* y);
+bool csr_enable_stencil(Csr& A, const StencilCols& sc);  // CF_NO_STENCIL_COLS=1 disables
 
 inline double mat_mu(const cf_material& m) { return m.E / (2.0 * (1.0 + m.nu)); }              // model.hpp:26
 inline double mat_lambda(const cf_material& m) {                                                  // model.hpp:27

@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <climits>
+#include <cstdlib>
 
 #include "cf_vec.hpp"
 

@@ -2,6 +2,8 @@
 // proj/src/linsolve.cpp:13-19).  HBM-bound: the matrix is streamed once with L1-bypassing
 // non-coherent loads, x is read through the read-only cache, a group of TPR lanes owns one
 // row (TPR picked from the mean row length) and reduces with warp shuffles.
+#include <cstdlib>
+
 #include "cf_types.hpp"
 
 namespace cfb {
@@ -127,6 +129,311 @@ __global__ void __launch_bounds__(256) k_spmv_phi(i64 rows, const i64* __restric
   if (row < rows && lane == 0) y[row] = s1 + s2;
 }
 
+// ---- stencil-implicit columns (cf_types.hpp StencilCols): the column of entry e of a row
+template <int D>
+struct StGeo {
+  int colbase, diag_col;  // column of the first valid neighbour (component 0); diagonal of a clamp row
+  int nnD, nn2D;          // column strides of y and z neighbours
+  int cx, cy, cz;         // valid neighbour offsets per axis (contiguous ranges)
+  bool diag_only;         // clamped (Dirichlet) u row: at most its diagonal
+  bool interior;          // all 3^d neighbours free: column = colbase + the block's offset table
+};
+
+// offsets of entry e of an interior row from its colbase (3^d neighbours x d components)
+template <int D>
+struct StOff {
+  static constexpr int N = (D == 3 ? 27 : 9) * D;
+  __device__ static void fill(int* off, int nn) {
+    for (int e = threadIdx.x; e < N; e += blockDim.x) {
+      const int n = e / D, b = e - n * D;
+      off[e] = D * ((n % 3) + nn * ((n / 3) % 3 + nn * (n / 9))) + b;
+    }
+  }
+};
+
+// 32-bit arithmetic throughout: columns are int32 by construction (make_problem checks)
+template <int D>
+__device__ __forceinline__ void st_geo(const StencilCols& sc, i64 row, StGeo<D>& G) {
+  const unsigned r32 = unsigned(row);
+  unsigned lv = r32, a = 0;
+  if (sc.kind == 1) {
+    lv = r32 / D;
+    a = r32 - lv * D;
+  }
+  const int nn = int(sc.nn);
+  const unsigned v = unsigned(sc.v_lo) + lv;
+  // v / nn and (v / nn) / nn through the double reciprocal (exact after the +-1 correction)
+  auto divn = [&](unsigned t) {
+    unsigned q = unsigned(double(t) * sc.inv_nn);
+    if (q * unsigned(nn) > t) --q;
+    else if ((q + 1) * unsigned(nn) <= t) ++q;
+    return q;
+  };
+  const unsigned vy = divn(v);
+  const int x = int(v - vy * unsigned(nn));
+  int y = int(vy), z = 0;
+  if (D == 3) {
+    const unsigned vz = divn(vy);
+    y = int(vy - vz * unsigned(nn));
+    z = int(vz);
+  }
+  bool bnd = x == 0 || x == nn - 1 || y == 0 || y == nn - 1;
+  if (D == 3) bnd = bnd || z == 0 || z == nn - 1;
+  G.diag_only = sc.kind == 1 && bnd;
+  G.diag_col = int(v * D + a) - int(sc.shift);
+  // neighbour offsets c + delta in [1, nn - 2] (free u dofs): delta in [max(-1, 1 - c), min(1, nn - 2 - c)]
+  auto lo = [](int c) { return c >= 2 ? -1 : 1 - c; };
+  auto cnt = [&](int c) { return min(1, nn - 2 - c) - lo(c) + 1; };
+  G.cx = cnt(x);
+  G.cy = cnt(y);
+  G.cz = (D == 3) ? cnt(z) : 1;
+  const int z0 = (D == 3) ? z + lo(z) : 0;
+  G.colbase = D * ((x + lo(x)) + nn * ((y + lo(y)) + nn * z0)) - int(sc.shift);
+  G.nnD = D * nn;
+  G.nn2D = D * nn * nn;
+  G.interior = !G.diag_only && G.cx == 3 && G.cy == 3 && G.cz == 3;
+}
+
+template <int D>
+__device__ __forceinline__ int st_col(const StGeo<D>& G, int e) {
+  if (G.diag_only) return G.diag_col;
+  const int n = e / D, b = e - n * D;
+  int ix, iy, iz;
+  if (G.cx == 3 && G.cy == 3) {  // interior rows: constant divisors
+    const int t = n / 3;
+    ix = n - 3 * t;
+    iz = t / 3;
+    iy = t - 3 * iz;
+  } else {
+    const int t = n / G.cx;
+    ix = n - G.cx * t;
+    iz = t / G.cy;
+    iy = t - G.cy * iz;
+  }
+  return G.colbase + ix * D + iy * G.nnD + iz * G.nn2D + b;
+}
+
+template <int TPR, int U, int D>
+__device__ __forceinline__ double row_dot_st(const i64* __restrict__ ptr, const double* __restrict__ val,
+                                             const double* __restrict__ x, i64 row, int lane, const StencilCols& sc,
+                                             const int* __restrict__ off) {
+  StGeo<D> G;
+  st_geo<D>(sc, row, G);
+  double s = 0.0;
+  const i64 b0 = ptr[row], e = ptr[row + 1];
+  for (i64 k0 = b0 + lane; k0 < e; k0 += i64(TPR) * U) {
+    double v[U], xv[U];
+    int c[U];
+    const int e0 = int(k0 - b0);
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const i64 k = k0 + i64(j) * TPR;
+      const bool in = k < e;
+      v[j] = in ? ld_stream(val + k) : 0.0;
+      c[j] = !in ? -1 : (G.interior ? G.colbase + off[e0 + j * TPR] : st_col<D>(G, e0 + j * TPR));
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < U; ++j) s += v[j] * xv[j];
+  }
+  return s;
+}
+
+// The TPR-lane reduction of a row emulated by PH < TPR threads: thread t owns the logical lanes
+// t, t + PH, ..., keeps one accumulator per logical lane (entries L, L + TPR, ... in order, as
+// logical lane L would), folds the butterfly steps with offsets >= PH inside the thread and the
+// rest with shuffles.  Bitwise the TPR-lane result (padding adds +0.0, which never changes a sum
+// that starts at +0.0), with PH-wide row groups: more rows per warp, more loads in flight.
+template <int TPR, int PH, int U, int D>
+__device__ __forceinline__ double row_dot_st_emu(const i64* __restrict__ ptr, const double* __restrict__ val,
+                                                 const double* __restrict__ x, i64 row, int t, const StencilCols& sc,
+                                                 const int* __restrict__ off) {
+  constexpr int R = TPR / PH;
+  StGeo<D> G;
+  st_geo<D>(sc, row, G);
+  double s[R];
+#pragma unroll
+  for (int m = 0; m < R; ++m) s[m] = 0.0;
+  const i64 b0 = ptr[row], e = ptr[row + 1];
+  for (i64 base = b0; base < e; base += i64(TPR) * U) {
+    double v[U][R], xv[U][R];
+    int c[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const i64 k = base + u * TPR + t + PH * m;
+        const bool in = k < e;
+        const int ei = int(k - b0);
+        v[u][m] = in ? ld_stream(val + k) : 0.0;
+        c[u][m] = !in ? -1 : (G.interior ? G.colbase + off[ei] : st_col<D>(G, ei));
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int m = 0; m < R; ++m) xv[u][m] = c[u][m] >= 0 ? __ldg(x + c[u][m]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int m = 0; m < R; ++m) s[m] += v[u][m] * xv[u][m];
+  }
+  // butterfly offsets TPR/2 .. PH inside the thread (logical lane t + PH m <-> t + PH (m ^ (o / PH)))
+#pragma unroll
+  for (int o = TPR / 2; o >= PH; o >>= 1) {
+    double n[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) n[m] = s[m] + s[m ^ (o / PH)];
+#pragma unroll
+    for (int m = 0; m < R; ++m) s[m] = n[m];
+  }
+  return s[0];  // logical lane t; offsets < PH follow as shuffles over the PH threads
+}
+
+// the same emulation for a stored-column row
+template <int TPR, int PH, int U>
+__device__ __forceinline__ double row_dot_b_emu(const i64* __restrict__ ptr, const int* __restrict__ col,
+                                                const double* __restrict__ val, const double* __restrict__ x, i64 row,
+                                                int t) {
+  constexpr int R = TPR / PH;
+  double s[R];
+#pragma unroll
+  for (int m = 0; m < R; ++m) s[m] = 0.0;
+  const i64 e = ptr[row + 1];
+  for (i64 base = ptr[row]; base < e; base += i64(TPR) * U) {
+    double v[U][R], xv[U][R];
+    int c[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const i64 k = base + u * TPR + t + PH * m;
+        const bool in = k < e;
+        v[u][m] = in ? ld_stream(val + k) : 0.0;
+        c[u][m] = in ? ld_stream(col + k) : -1;
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int m = 0; m < R; ++m) xv[u][m] = c[u][m] >= 0 ? __ldg(x + c[u][m]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int m = 0; m < R; ++m) s[m] += v[u][m] * xv[u][m];
+  }
+#pragma unroll
+  for (int o = TPR / 2; o >= PH; o >>= 1) {
+    double n[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) n[m] = s[m] + s[m ^ (o / PH)];
+#pragma unroll
+    for (int m = 0; m < R; ++m) s[m] = n[m];
+  }
+  return s[0];
+}
+
+template <int TPR, int PH, int U, int D>
+__global__ void __launch_bounds__(256) k_spmv_st_emu(i64 rows, const i64* __restrict__ ptr,
+                                                     const double* __restrict__ val, const double* __restrict__ x,
+                                                     double* y, const double* add, StencilCols sc) {
+  __shared__ int off[StOff<D>::N];
+  StOff<D>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 row = g / PH;
+  const int t = int(g % PH);
+  double s = 0.0;
+  if (row < rows) s = row_dot_st_emu<TPR, PH, U, D>(ptr, val, x, row, t, sc, off);
+  s = group_sum<PH>(s);
+  if (row < rows && t == 0) y[row] = add ? add[row] + s : s;
+}
+
+template <int TPR, int PH, int U, int D>
+__global__ void __launch_bounds__(256) k_spmv_phi_st_emu(i64 rows, const i64* __restrict__ p1,
+                                                         const double* __restrict__ v1, const double* __restrict__ x1,
+                                                         StencilCols sc, const i64* __restrict__ p2,
+                                                         const int* __restrict__ c2, const double* __restrict__ v2,
+                                                         const double* __restrict__ x2, double* __restrict__ y) {
+  __shared__ int off[StOff<D>::N];
+  StOff<D>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 row = g / PH;
+  const int t = int(g % PH);
+  double s1 = 0.0, s2 = 0.0;
+  if (row < rows) {
+    s1 = row_dot_st_emu<TPR, PH, U, D>(p1, v1, x1, row, t, sc, off);
+    s2 = row_dot_b_emu<TPR, PH, 2>(p2, c2, v2, x2, row, t);
+  }
+  s1 = group_sum<PH>(s1);
+  s2 = group_sum<PH>(s2);
+  if (row < rows && t == 0) y[row] = s1 + s2;
+}
+
+// k_spmv_b with the columns computed from the row's vertex: the same entries in the same lane
+// order, so the result is bitwise k_spmv_b's
+template <int TPR, int U, int D>
+__global__ void __launch_bounds__(256) k_spmv_st(i64 rows, const i64* __restrict__ ptr, const double* __restrict__ val,
+                                                 const double* __restrict__ x, double* y, const double* add,
+                                                 StencilCols sc) {
+  __shared__ int off[StOff<D>::N];
+  StOff<D>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 row = t / TPR;
+  const int lane = int(t % TPR);
+  double s = 0.0;
+  if (row < rows) s = row_dot_st<TPR, U, D>(ptr, val, x, row, lane, sc, off);
+  s = group_sum<TPR>(s);
+  if (row < rows && lane == 0) y[row] = add ? add[row] + s : s;
+}
+
+template <int TPR, int U, int D>
+__global__ void __launch_bounds__(256) k_spmv_phi_st(i64 rows, const i64* __restrict__ p1,
+                                                     const double* __restrict__ v1, const double* __restrict__ x1,
+                                                     StencilCols sc, const i64* __restrict__ p2,
+                                                     const int* __restrict__ c2, const double* __restrict__ v2,
+                                                     const double* __restrict__ x2, double* __restrict__ y) {
+  __shared__ int off[StOff<D>::N];
+  StOff<D>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 row = t / TPR;
+  const int lane = int(t % TPR);
+  double s1 = 0.0, s2 = 0.0;
+  if (row < rows) {
+    s1 = row_dot_st<TPR, U, D>(p1, v1, x1, row, lane, sc, off);
+    s2 = row_dot_b<TPR, U>(p2, c2, v2, x2, row, lane);
+  }
+  s1 = group_sum<TPR>(s1);
+  s2 = group_sum<TPR>(s2);
+  if (row < rows && lane == 0) y[row] = s1 + s2;
+}
+
+// one thread per row: every stored column equals the computed one and the row has the
+// stencil's length (0 or 1 on clamp rows, 0 allowed on constrained phi rows)
+template <int D>
+__global__ void k_st_check(i64 rows, const i64* __restrict__ ptr, const int* __restrict__ col, StencilCols sc,
+                           int* __restrict__ bad) {
+  const i64 row = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  StGeo<D> G;
+  st_geo<D>(sc, row, G);
+  const i64 b0 = ptr[row];
+  const i64 len = ptr[row + 1] - b0;
+  bool ok;
+  if (G.diag_only) ok = len <= 1;
+  else ok = (len == i64(G.cx) * G.cy * G.cz * D) || (sc.kind == 2 && len == 0);
+  if (G.cx <= 0 || G.cy <= 0 || G.cz <= 0) ok = ok && (len == 0 || G.diag_only);
+  for (i64 e = 0; ok && e < len; ++e) ok = col[b0 + e] == st_col<D>(G, int(e));
+  if (ok && G.interior)  // the offset-table form used by the SpMV
+    for (i64 e = 0; ok && e < len; ++e) {
+      const int n = int(e) / D, b = int(e) - n * D;
+      ok = col[b0 + e] == G.colbase + D * ((n % 3) + int(sc.nn) * ((n / 3) % 3 + int(sc.nn) * (n / 9))) + b;
+    }
+  if (!ok) atomicOr(bad, 1);
+}
+
 template <int TPR>
 void launch_spmv(const Csr& A, const double* x, double* y, const double* add) {
   const int block = 256;
@@ -139,6 +446,20 @@ template <int TPR, int U>
 void launch_phi(const BlockSystem& J, const double* x, double* y) {
   const int block = 256;
   const i64 threads = J.np * TPR;
+  if (J.pu->st.kind != 0) {
+    const Csr &A = *J.pu, &B = *J.pp;
+    if (TPR == 16 && A.st.d == 3)
+      k_spmv_phi_st_emu<16, 8, 2, 3><<<grid_for(J.np * 8, block), block, 0, stream()>>>(
+          J.np, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p, x + J.in_u(), y + J.nu);
+    else if (A.st.d == 3)
+      k_spmv_phi_st<TPR, U, 3><<<grid_for(threads, block), block, 0, stream()>>>(
+          J.np, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p, x + J.in_u(), y + J.nu);
+    else
+      k_spmv_phi_st<TPR, U, 2><<<grid_for(threads, block), block, 0, stream()>>>(
+          J.np, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p, x + J.in_u(), y + J.nu);
+    CF_LAUNCHED();
+    return;
+  }
   k_spmv_phi<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(J.np, J.pu->ptr.p, J.pu->col.p, J.pu->val.p, x,
                                                                     J.pp->ptr.p, J.pp->col.p, J.pp->val.p,
                                                                     x + J.in_u(), y + J.nu);
@@ -149,14 +470,53 @@ template <int TPR, int U>
 void launch_b(const Csr& A, const double* x, double* y, const double* add) {
   const int block = 256;
   const i64 threads = A.rows * TPR;
-  k_spmv_b<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, add);
+  if (A.st.kind == 0)
+    k_spmv_b<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, add);
+  else if (TPR == 16 && A.st.d == 3)  // 8 threads per row emulating the 16-lane reduction (sweep)
+    k_spmv_st_emu<16, 8, 2, 3><<<grid_for(A.rows * 8, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y,
+                                                                                   add, A.st);
+  else if (A.st.d == 3)
+    k_spmv_st<TPR, U, 3><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, add, A.st);
+  else
+    k_spmv_st<TPR, U, 2><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, add, A.st);
   CF_LAUNCHED();
 }
 
 }  // namespace
 
+// Enable stencil-implicit columns on A if every stored column matches (one check pass).
+bool csr_enable_stencil(Csr& A, const StencilCols& sc) {
+  A.st = StencilCols{};
+  if (A.rows == 0 || std::getenv("CF_NO_STENCIL_COLS")) return false;
+  DevBuf<int> bad(1);
+  bad.zero();
+  if (sc.d == 3)
+    k_st_check<3><<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, sc, bad.p);
+  else
+    k_st_check<2><<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, sc, bad.p);
+  CF_LAUNCHED();
+  int h = 1;
+  CF_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  if (h == 0) A.st = sc;
+  return h == 0;
+}
+
 // Tuning hook: explicit (threads-per-row, unroll) variant.  Returns false for an unknown pair.
 bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double* y) {
+  if (A.st.kind != 0 && A.st.d == 3 && tpr == 16 && unroll >= 100) {  // emulated: unroll = 100 + 10 PH + U
+    const int ph = (unroll - 100) / 10, u = unroll % 10;
+#define CFB_E(P, U)                                                                                          \
+  if (ph == P && u == U) {                                                                                   \
+    k_spmv_st_emu<16, P, U, 3><<<grid_for(A.rows * P, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, \
+                                                                               nullptr, A.st);               \
+    CF_LAUNCHED();                                                                                           \
+    return true;                                                                                             \
+  }
+    CFB_E(4, 1) CFB_E(4, 2) CFB_E(8, 1) CFB_E(8, 2) CFB_E(2, 1) CFB_E(1, 1)
+#undef CFB_E
+    return false;
+  }
 #define CFB_V(T, U) if (tpr == T && unroll == U) { launch_b<T, U>(A, x, y, nullptr); return true; }
   CFB_V(32, 1) CFB_V(32, 2) CFB_V(32, 3) CFB_V(32, 4)
   CFB_V(16, 2) CFB_V(16, 4) CFB_V(16, 6)
