@@ -132,6 +132,10 @@ int cf_slab_info(cf_problem p, int rank, int size, int64_t info[7]);
 /* ------------------------------------------------------------------ block system */
 /* {n_u rows, n_phi rows, n_u input columns, n_phi input columns} (inputs > rows for a slab). */
 int cf_block_shape(cf_block b, int64_t shape[4]);
+/* Storage format the SpMV of one block streams (which: 0 M_uu, 1 M_phiu, 2 M_phiphi): 0 CSR
+ * (8 B value + 4 B column per entry), 1 stencil-implicit columns (values only; the columns of a
+ * row follow from its vertex, verified against the stored CSR columns at assembly). */
+int cf_block_format(cf_block b, int which, int* format);
 /* Sizes: n_u, n_phi and nnz of M_uu, M_phiu, M_phiphi (linsolve.hpp:17-28). */
 int cf_block_info(cf_block b, int64_t* n_u, int64_t* n_phi, int64_t* nnz3);
 /* Copy one block out as CSR (which: 0 M_uu, 1 M_phiu, 2 M_phiphi). */

@@ -210,6 +210,12 @@ class BlockSystem:
         check(load().cf_block_apply(self._h, _ptr(x), _ptr(y)))
         return y
 
+    def format(self, which: int) -> str:
+        """Storage the SpMV of a block streams: "csr" or "stencil" (values only, implicit columns)."""
+        f = C.c_int()
+        check(load().cf_block_format(self._h, which, C.byref(f)))
+        return "stencil" if f.value == 1 else "csr"
+
     def spmv(self, which: int, x, out=None):
         """One block times a vector (which: 0 M_uu, 1 M_phiu, 2 M_phiphi)."""
         rows = self._n_u if which == 0 else self._n_phi

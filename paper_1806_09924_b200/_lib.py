@@ -111,6 +111,7 @@ SIGNATURES = [
                                          C.POINTER(_P)]),
     ("cf_slab_info", _I, [_P, _I, _I, _P]),
     ("cf_block_shape", _I, [_P, _P]),
+    ("cf_block_format", _I, [_P, _I, C.POINTER(_I)]),
     ("cf_block_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),
     ("cf_block_export", _I, [_P, _I, _P, _P, _P]),
     ("cf_block_apply", _I, [_P, _P, _P]),

@@ -311,6 +311,14 @@ int cf_assemble_jacobian_planes(cf_problem p, cf_constraints c, const cf_materia
   });
 }
 
+int cf_block_format(cf_block b, int which, int* format) {
+  return guard([&] {
+    CHECK_ARG(b && format && which >= 0 && which <= 2, "cf_block_format: bad argument");
+    const Csr& A = which == 0 ? *b->J->uu : (which == 1 ? *b->J->pu : *b->J->pp);
+    *format = A.st.kind != 0 ? 1 : 0;
+  });
+}
+
 int cf_block_shape(cf_block b, int64_t shape[4]) {
   return guard([&] {
     CHECK_ARG(b && shape, "cf_block_shape: null argument");
