@@ -239,6 +239,15 @@ int cf_solve_loading_sequence(cf_problem p, cf_state s, const cf_material* mat, 
                               const cf_solver_options* opts, int n_steps, cf_newton_iteration* its, int max_its,
                               int* n_its, int* converged, double* feasibility, int* steps_done);
 
+/* ------------------------------------------------------------------ I/O
+ * write_matrix_market (linsolve.cpp:478-490): one block (which: 0 M_uu, 1 M_phiu, 2 M_phiphi)
+ * or a CSR handle, byte-identical text.  write_vtk (postproc.cpp:111-167): the solution (and
+ * phi_old, may be NULL) on the problem's mesh; binary = 0 is the reference's ASCII file, 1 the
+ * same dataset in legacy big-endian BINARY encoding.  Arrays may be host or device. */
+int cf_block_write_matrix_market(cf_block b, int which, const char* path);
+int cf_csr_write_matrix_market(cf_csr A, const char* path);
+int cf_write_vtk(cf_problem p, const double* solution, const double* phi_old, const char* path, int binary);
+
 /* ------------------------------------------------------------------ multi-GPU
  * One process per GPU.  Rank 0 makes an id, the launcher broadcasts it (e.g. over
  * torch.distributed), every rank creates its communicator on its current CUDA device.  The _comm

@@ -233,6 +233,10 @@ class BlockSystem:
         check(load().cf_block_export(self._h, which, _ptr(ptr), _ptr(col), _ptr(val)))
         return Csr(rows, cols, ptr, col, val)
 
+    def write_matrix_market(self, which: int, path: str) -> None:
+        """write_matrix_market (linsolve.cpp:478-490) of one block, byte-identical text."""
+        check(load().cf_block_write_matrix_market(self._h, int(which), str(path).encode()))
+
     @property
     def M_uu(self):
         return self.csr(0)
@@ -524,6 +528,19 @@ def compute_cod(prob: Problem, solution, stations) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------- Newton / active set
+def write_matrix_market(path: str, A) -> None:
+    """linsolve.cpp:478-490 for a CsrMatrix (use BlockSystem.write_matrix_market for a block)."""
+    check(load().cf_csr_write_matrix_market(A._h, str(path).encode()))
+
+
+def write_vtk(path: str, prob: Problem, solution, phi_old=None, binary: bool = False) -> None:
+    """postproc.cpp:111-167: legacy VTK of the solution (ASCII = the reference's text; binary = the
+    same dataset in big-endian BINARY encoding)."""
+    x = _as_f64(solution)
+    po = _as_f64(phi_old) if phi_old is not None else None
+    check(load().cf_write_vtk(prob._h, _ptr(x), _ptr(po), str(path).encode(), int(bool(binary))))
+
+
 def slit_band_edge(prob: Problem, mat: Material) -> float:
     out = C.c_double()
     check(load().cf_slit_band_edge(prob._h, C.byref(mat), C.byref(out)))

@@ -149,6 +149,9 @@ SIGNATURES = [
                                        C.POINTER(_D), _P]),
     ("cf_solve_loading_sequence", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
                                        C.POINTER(SolverOptions), _I, _P, _I, _P, _P, _P, C.POINTER(_I)]),
+    ("cf_block_write_matrix_market", _I, [_P, _I, C.c_char_p]),
+    ("cf_csr_write_matrix_market", _I, [_P, C.c_char_p]),
+    ("cf_write_vtk", _I, [_P, _P, _P, C.c_char_p, _I]),
     ("cf_comm_unique_id", _I, [_P]),
     ("cf_comm_create", _I, [_P, _I, _I, C.POINTER(_P)]),
     ("cf_comm_info", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),

@@ -766,6 +766,30 @@ static void fill_report(const NewtonReport& r, cf_newton_iteration* its, int max
   if (feasibility) *feasibility = r.feasibility;
 }
 
+// ------------------------------------------------------------------ I/O
+int cf_block_write_matrix_market(cf_block b, int which, const char* path) {
+  return guard([&] {
+    CHECK_ARG(b && path && which >= 0 && which <= 2, "cf_block_write_matrix_market: bad argument");
+    write_matrix_market(which == 0 ? *b->J->uu : (which == 1 ? *b->J->pu : *b->J->pp), path);
+  });
+}
+
+int cf_csr_write_matrix_market(cf_csr A, const char* path) {
+  return guard([&] {
+    CHECK_ARG(A && path, "cf_csr_write_matrix_market: null argument");
+    write_matrix_market(*A->A, path);
+  });
+}
+
+int cf_write_vtk(cf_problem p, const double* solution, const double* phi_old, const char* path, int binary) {
+  return guard([&] {
+    CHECK_ARG(p && solution && path, "cf_write_vtk: null argument");
+    InArg<double> x(solution, p->p->g.n_total());
+    InArg<double> po(phi_old, phi_old ? p->p->g.V : 0);
+    write_vtk(*p->p, x.dev, phi_old ? po.dev : nullptr, path, binary != 0);
+  });
+}
+
 // ------------------------------------------------------------------ communicator
 int cf_comm_unique_id(uint8_t id[128]) {
   return guard([&] {

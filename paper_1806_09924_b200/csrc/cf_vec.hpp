@@ -4,6 +4,7 @@
 
 #include <functional>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "cf_types.hpp"
@@ -124,6 +125,11 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
 // ---- postproc.cu (postproc.cpp:12-99)
 double compute_tcv(const Problem& P, const double* sol);
 void compute_cod(const Problem& P, const double* sol, const double* stations_host, int ns, double* out_host);
+
+// ---- io.cu (linsolve.cpp:478-490, postproc.cpp:111-167)
+void write_matrix_market(const Csr& A, const std::string& path);
+void write_vtk(const Problem& P, const double* sol_dev, const double* phi_old_dev, const std::string& path,
+               bool binary);
 
 // ---- newton.cu (solver.cpp:24-204)
 struct State {  // FractureState (model.hpp:50-55), device resident
