@@ -538,7 +538,9 @@ constexpr int SYM_BIG = 16384;
 // lanes per A entry in the warp kernels, from the longest B row
 // 8 lanes (4 A entries in flight per step, <= 16 independent B loads per lane) unless B rows are
 // long; this is what hides the per-A-entry dependency chain (ac -> bp -> bc -> hash)
-int lanes_for(i64 maxb) { return maxb <= 128 ? 8 : 32; }
+// lanes per B row in the symbolic and numeric kernels (measured on config 3: 16 lanes beat 8 lanes
+// with 16 buffered products per lane for B rows of 65-128 entries, 32 lanes beat 16 beyond 128)
+int lanes_for(i64 maxb) { return maxb <= 64 ? 8 : (maxb <= 128 ? 16 : 32); }
 
 template <int L>
 void sym_launch(int mode, const RowBin& b, int cap, const Csr& A, const Csr& B, i64* cnt, const Csr* C) {
@@ -696,6 +698,7 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
     else { num_launch<32, 8>(f1, 512, A, B, row_scale, *C); num_launch<32, 8>(f2, 2048, A, B, row_scale, *C); }
   } else if (cmax_need <= 16) {
     if (L == 8) { num_launch<8, 16>(f1, 512, A, B, row_scale, *C); num_launch<8, 16>(f2, 2048, A, B, row_scale, *C); }
+    else if (L == 16) { num_launch<16, 16>(f1, 512, A, B, row_scale, *C); num_launch<16, 16>(f2, 2048, A, B, row_scale, *C); }
     else { num_launch<32, 16>(f1, 512, A, B, row_scale, *C); num_launch<32, 16>(f2, 2048, A, B, row_scale, *C); }
   } else {
     warp_ok = false;

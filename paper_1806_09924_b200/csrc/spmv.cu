@@ -410,28 +410,32 @@ __global__ void __launch_bounds__(256) k_spmv_phi_st(i64 rows, const i64* __rest
   if (row < rows && lane == 0) y[row] = s1 + s2;
 }
 
-// one thread per row: every stored column equals the computed one and the row has the
-// stencil's length (0 or 1 on clamp rows, 0 allowed on constrained phi rows)
+// every stored column equals the computed one and the row has the stencil's length (0 or 1 on
+// clamp rows, 0 allowed on constrained phi rows); 8 threads per row read the columns coalesced
 template <int D>
-__global__ void k_st_check(i64 rows, const i64* __restrict__ ptr, const int* __restrict__ col, StencilCols sc,
-                           int* __restrict__ bad) {
-  const i64 row = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (row >= rows) return;
-  StGeo<D> G;
-  st_geo<D>(sc, row, G);
-  const i64 b0 = ptr[row];
-  const i64 len = ptr[row + 1] - b0;
-  bool ok;
-  if (G.diag_only) ok = len <= 1;
-  else ok = (len == i64(G.cx) * G.cy * G.cz * D) || (sc.kind == 2 && len == 0);
-  if (G.cx <= 0 || G.cy <= 0 || G.cz <= 0) ok = ok && (len == 0 || G.diag_only);
-  for (i64 e = 0; ok && e < len; ++e) ok = col[b0 + e] == st_col<D>(G, int(e));
-  if (ok && G.interior)  // the offset-table form used by the SpMV
-    for (i64 e = 0; ok && e < len; ++e) {
-      const int n = int(e) / D, b = int(e) - n * D;
-      ok = col[b0 + e] == G.colbase + D * ((n % 3) + int(sc.nn) * ((n / 3) % 3 + int(sc.nn) * (n / 9))) + b;
+__global__ void __launch_bounds__(256) k_st_check(i64 rows, const i64* __restrict__ ptr, const int* __restrict__ col,
+                                                  StencilCols sc, int* __restrict__ bad) {
+  __shared__ int off[StOff<D>::N];
+  StOff<D>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 row = g >> 3;
+  const int t = int(g & 7);
+  bool ok = true;
+  if (row < rows) {
+    StGeo<D> G;
+    st_geo<D>(sc, row, G);
+    const i64 b0 = ptr[row];
+    const i64 len = ptr[row + 1] - b0;
+    if (G.diag_only) ok = len <= 1;
+    else ok = (len == i64(G.cx) * G.cy * G.cz * D) || (sc.kind == 2 && len == 0);
+    if (G.cx <= 0 || G.cy <= 0 || G.cz <= 0) ok = ok && (len == 0 || G.diag_only);
+    for (i64 e = t; ok && e < len; e += 8) {
+      const int c = ld_stream(col + b0 + e);
+      ok = c == st_col<D>(G, int(e)) && (!G.interior || c == G.colbase + off[e]);
     }
-  if (!ok) atomicOr(bad, 1);
+  }
+  if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
 template <int TPR>
@@ -491,9 +495,9 @@ bool csr_enable_stencil(Csr& A, const StencilCols& sc) {
   DevBuf<int> bad(1);
   bad.zero();
   if (sc.d == 3)
-    k_st_check<3><<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, sc, bad.p);
+    k_st_check<3><<<grid_for(A.rows * 8, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, sc, bad.p);
   else
-    k_st_check<2><<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, sc, bad.p);
+    k_st_check<2><<<grid_for(A.rows * 8, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, sc, bad.p);
   CF_LAUNCHED();
   int h = 1;
   CF_CUDA(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
