@@ -517,7 +517,7 @@ bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double
     CF_LAUNCHED();                                                                                           \
     return true;                                                                                             \
   }
-    CFB_E(4, 1) CFB_E(4, 2) CFB_E(8, 1) CFB_E(8, 2) CFB_E(2, 1) CFB_E(1, 1)
+    CFB_E(4, 1) CFB_E(4, 2) CFB_E(4, 3) CFB_E(4, 4) CFB_E(8, 1) CFB_E(8, 2) CFB_E(8, 3) CFB_E(8, 4) CFB_E(2, 1)
 #undef CFB_E
     return false;
   }

@@ -17,7 +17,7 @@ J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
 u = x[:P.n_u].contiguous()
 y = torch.empty_like(u)
 ref = J.spmv(0, u)
-V = [(16, 141), (16, 142), (16, 181), (16, 182), (16, 121)]
+V = [(16, 141), (16, 142), (16, 143), (16, 144), (16, 181), (16, 182), (16, 183), (16, 184)]
 res = {v: [] for v in V}
 for rep in range(4):
     for tpr, un in V:
