@@ -98,7 +98,6 @@ __global__ void k_iota(i64 n, int* out) {
 }
 
 __global__ void k_flag_list(i64 n, const int* __restrict__ flag, int* __restrict__ list, int* __restrict__ count);
-__global__ void k_sort_list(int n, int* list);
 
 struct OvfList {
   DevBuf<int> list;
@@ -251,9 +250,6 @@ __global__ void k_flag_list(i64 n, const int* __restrict__ flag, int* __restrict
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n && flag[i]) list[atomicAdd(count, 1)] = int(i);
 }
-__global__ void k_sort_list(int n, int* list) {  // small lists: deterministic order of overflow nodes
-  if (threadIdx.x == 0 && blockIdx.x == 0) heap_sort_pairs(list, nullptr, n);
-}
 
 __global__ void k_strength_diag(i64 nn, const i64* __restrict__ nptr, const int* __restrict__ ndofs,
                                 const i64* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
@@ -328,9 +324,9 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
 }
 
 // ------------------------------------------------------------------ N2 dependency graph
-// N2(i) = S[i] u T[i] u T[S[i]] (T = S^T), as a k-way merge of sorted lists.  mode 0 counts the
-// lower (< i) and upper (> i) members; mode 1 writes the upper members (the dependents).
-constexpr int MCAP = 64;  // merged lists per node in the local tier (|S[i]| <= 62)
+// N2(i) = S[i] u T[i] u T[S[i]] (T = S^T): per node a hash set (k_n2w: warp, shared memory;
+// k_n2_big: global memory for high-degree nodes).  mode 0 counts the lower (< i) and upper (> i)
+// members; mode 1 writes the upper members (the dependents).
 
 // overflow tier of N2: a private hash set per node in global memory
 __global__ void k_n2_cap(i64 nov, const int* __restrict__ list, const i64* __restrict__ sp, const int* __restrict__ si,
@@ -472,54 +468,6 @@ __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restric
   }
 }
 
-__global__ void k_n2(i64 nn, const i64* __restrict__ sp, const int* __restrict__ si, const i64* __restrict__ tp,
-                     const int* __restrict__ ti, int* __restrict__ lower, i64* __restrict__ upcnt,
-                     const i64* __restrict__ upptr, int* __restrict__ up, int mode, int* __restrict__ ovf) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= nn) return;
-  // lists: S[i], T[i], T[j] for j in S[i]
-  i64 cur[MCAP], end[MCAP];
-  const int* arr[MCAP];
-  int nl = 0;
-  const i64 ns = sp[i + 1] - sp[i];
-  if (ns + 2 > MCAP) {
-    if (mode == 0) ovf[i] = 1;
-    return;
-  }
-  cur[nl] = sp[i]; end[nl] = sp[i + 1]; arr[nl] = si; ++nl;
-  cur[nl] = tp[i]; end[nl] = tp[i + 1]; arr[nl] = ti; ++nl;
-  for (i64 k = sp[i]; k < sp[i + 1]; ++k) {
-    const int j = si[k];
-    cur[nl] = tp[j]; end[nl] = tp[j + 1]; arr[nl] = ti; ++nl;
-  }
-  int nlow = 0;
-  i64 nup = 0;
-  const i64 base = mode ? upptr[i] : 0;
-  int last = -1;
-  while (true) {
-    int best = INT_MAX;
-    for (int l = 0; l < nl; ++l)
-      if (cur[l] < end[l]) {
-        const int v = arr[l][cur[l]];
-        if (v < best) best = v;
-      }
-    if (best == INT_MAX) break;
-    for (int l = 0; l < nl; ++l)
-      while (cur[l] < end[l] && arr[l][cur[l]] == best) ++cur[l];
-    if (best == last) continue;
-    last = best;
-    if (best < int(i)) {
-      ++nlow;
-    } else if (best > int(i)) {
-      if (mode) up[base + nup] = best;
-      ++nup;
-    }
-  }
-  if (!mode) {
-    lower[i] = nlow;
-    upcnt[i] = nup;
-  }
-}
 
 // ------------------------------------------------------------------ pass 1: LFMIS frontier rounds
 constexpr int UND = 0, ROOT = 1, NOTROOT = 2;

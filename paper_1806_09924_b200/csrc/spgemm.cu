@@ -333,87 +333,6 @@ __global__ void __launch_bounds__(WPB * 32) k_num(const int* __restrict__ rowlis
   for (int t = lane; t < nc; t += 32) cv[c0 + t] = Acc[hfind(T, mask, cc[c0 + t])];
 }
 
-// --- flat numeric, warp per row ---------------------------------------------------------------
-// The row's products are enumerated in (A column, B column) order as p = 0..U-1 and spread over
-// the lanes 32 at a time, so every lane's loads are independent (no per-k dependency chain).
-// Lanes of one chunk that hit the same output slot are resolved with __match_any_sync and add in
-// lane order, i.e. in ascending k: each C(i,j) is still the k-ascending sequential sum.
-template <int CAP, int WPB, int PCAP>
-__global__ void __launch_bounds__(WPB * 32) k_num_flat(const int* __restrict__ rowlist, i64 nrows,
-                                                       const i64* __restrict__ ap, const int* __restrict__ ac,
-                                                       const double* __restrict__ av, const double* __restrict__ rs,
-                                                       const i64* __restrict__ bp, const int* __restrict__ bc,
-                                                       const double* __restrict__ bv, const i64* __restrict__ cp,
-                                                       const int* __restrict__ cc, double* __restrict__ cv) {
-  __shared__ int tab[WPB][CAP];
-  __shared__ double acc[WPB][CAP];
-  __shared__ int pre[WPB][PCAP + 1];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const i64 r = i64(blockIdx.x) * WPB + w;
-  if (r >= nrows) return;
-  const i64 i = rowlist ? rowlist[r] : r;
-  int* T = tab[w];
-  double* Acc = acc[w];
-  int* Pre = pre[w];
-  for (int s = lane; s < CAP; s += 32) {
-    T[s] = EMPTY;
-    Acc[s] = 0.0;
-  }
-  __syncwarp();
-  const unsigned mask = CAP - 1;
-  const i64 c0 = cp[i];
-  const int nc = int(cp[i + 1] - c0);
-  for (int t = lane; t < nc; t += 32) hinsert(T, mask, cc[c0 + t]);
-  // prefix of the B row lengths over the A row
-  const i64 a0 = ap[i];
-  const int na = int(ap[i + 1] - a0);
-  int carry = 0;
-  if (lane == 0) Pre[0] = 0;
-  for (int t0 = 0; t0 < na; t0 += 32) {
-    const int t = t0 + lane;
-    int len = 0;
-    if (t < na) {
-      const int k = ac[a0 + t];
-      len = int(bp[k + 1] - bp[k]);
-    }
-    int incl = len;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (t < na) Pre[t + 1] = carry + incl;
-    carry += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  __syncwarp();
-  const int U = carry;
-  const double si = rs ? rs[i] : 1.0;
-  int lo = 0;  // this lane's A-row cursor: largest ka with Pre[ka] <= p (p only grows)
-  for (int p0 = 0; p0 < U; p0 += 32) {
-    const int p = p0 + lane;
-    const bool valid = p < U;
-    int slot = 0;
-    double v = 0.0;
-    if (valid) {
-      while (lo + 1 < na && Pre[lo + 1] <= p) ++lo;
-      const int k = ac[a0 + lo];
-      const double a = rs ? si * av[a0 + lo] : av[a0 + lo];
-      const i64 q = bp[k] + (p - Pre[lo]);
-      slot = hfind(T, mask, bc[q]);
-      v = a * bv[q];
-    }
-    // lanes sharing an A entry hit distinct columns; different A entries add in ascending order
-    const int kfirst = __shfl_sync(0xffffffffu, lo, 0);
-    const int last_lane = min(31, U - 1 - p0);
-    const int klast = __shfl_sync(0xffffffffu, lo, last_lane);
-    for (int kk = kfirst; kk <= klast; ++kk) {
-      if (valid && lo == kk) Acc[slot] += v;
-      __syncwarp();
-    }
-  }
-  __syncwarp();
-  for (int t = lane; t < nc; t += 32) cv[c0 + t] = Acc[hfind(T, mask, cc[c0 + t])];
-}
-
 __device__ __forceinline__ int lower_bound_sm(const int* a, int n, int key) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -464,14 +383,6 @@ __global__ void k_bin_rows(i64 rows, const i64* __restrict__ v, i64 lo, i64 hi, 
   if (i >= rows) return;
   const i64 x = v[i];
   if (x > lo && x <= hi) list[atomicAdd(count, 1)] = int(i);
-}
-// numeric tier by (row length nc, A row length na): 0 (nc <= 128, na <= 512), 1 (nc <= 512,
-// na <= 1024), 2 (nc <= 1024, na <= 1024), 3 otherwise
-__global__ void k_num_tier(i64 m, const i64* __restrict__ ap, const i64* __restrict__ cp, i64* __restrict__ out) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const i64 nc = cp[i + 1] - cp[i], na = ap[i + 1] - ap[i];
-  out[i] = (nc <= 128 && na <= 512) ? 0 : (na <= 1024 && nc <= 512) ? 1 : (na <= 1024 && nc <= 1024) ? 2 : 3;
 }
 __global__ void k_row_len(i64 m, const i64* __restrict__ p, i64* __restrict__ out) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
