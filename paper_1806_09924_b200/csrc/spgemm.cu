@@ -449,9 +449,10 @@ constexpr int SYM_BIG = 16384;
 // lanes per A entry in the warp kernels, from the longest B row
 // 8 lanes (4 A entries in flight per step, <= 16 independent B loads per lane) unless B rows are
 // long; this is what hides the per-A-entry dependency chain (ac -> bp -> bc -> hash)
-// lanes per B row in the symbolic and numeric kernels (measured on config 3: 16 lanes beat 8 lanes
-// with 16 buffered products per lane for B rows of 65-128 entries, 32 lanes beat 16 beyond 128)
-int lanes_for(i64 maxb) { return maxb <= 64 ? 8 : (maxb <= 128 ? 16 : 32); }
+// lanes per B row in the symbolic and numeric kernels (measured on config 3: 4 lanes for the <= 6
+// entry rows of the tentative prolongator, 16 lanes beat 8 lanes with 16 buffered products per
+// lane for B rows of 65-128 entries, 32 lanes beat 16 beyond 128)
+int lanes_for(i64 maxb) { return maxb <= 8 ? 4 : (maxb <= 64 ? 8 : (maxb <= 128 ? 16 : 32)); }
 
 template <int L>
 void sym_launch(int mode, const RowBin& b, int cap, const Csr& A, const Csr& B, i64* cnt, const Csr* C) {
@@ -475,7 +476,8 @@ void sym_launch(int mode, const RowBin& b, int cap, const Csr& A, const Csr& B, 
 }
 
 void sym_dispatch(int L, int mode, const RowBin& b, int cap, const Csr& A, const Csr& B, i64* cnt, const Csr* C) {
-  if (L == 8) sym_launch<8>(mode, b, cap, A, B, cnt, C);
+  if (L == 4) sym_launch<4>(mode, b, cap, A, B, cnt, C);
+  else if (L == 8) sym_launch<8>(mode, b, cap, A, B, cnt, C);
   else if (L == 16) sym_launch<16>(mode, b, cap, A, B, cnt, C);
   else sym_launch<32>(mode, b, cap, A, B, cnt, C);
 }
@@ -535,7 +537,10 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
     spill.alloc(std::max<i64>(1, read_i64(soff.p + m)));
     RowBin all = make_bin(m, ub.p, 0, LLONG_MAX);
     if (all.n) {
-      if (L == 8)
+      if (L == 4)
+        k_sym<512, 4, 8, 2><<<grid_for(all.n, 8), 256, 0, stream()>>>(all.list.p, all.n, A.ptr.p, A.col.p, B.ptr.p,
+                                                                      B.col.p, cnt, soff.p, spill.p);
+      else if (L == 8)
         k_sym<512, 8, 8, 2><<<grid_for(all.n, 8), 256, 0, stream()>>>(all.list.p, all.n, A.ptr.p, A.col.p, B.ptr.p,
                                                                       B.col.p, cnt, soff.p, spill.p);
       else if (L == 16)
@@ -604,7 +609,8 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   const i64 cmax_need = (maxb + L - 1) / L;
   bool warp_ok = true;
   if (cmax_need <= 8) {
-    if (L == 8) { num_launch<8, 8>(f1, 512, A, B, row_scale, *C); num_launch<8, 8>(f2, 2048, A, B, row_scale, *C); }
+    if (L == 4) { num_launch<4, 2>(f1, 512, A, B, row_scale, *C); num_launch<4, 2>(f2, 2048, A, B, row_scale, *C); }
+    else if (L == 8) { num_launch<8, 8>(f1, 512, A, B, row_scale, *C); num_launch<8, 8>(f2, 2048, A, B, row_scale, *C); }
     else if (L == 16) { num_launch<16, 8>(f1, 512, A, B, row_scale, *C); num_launch<16, 8>(f2, 2048, A, B, row_scale, *C); }
     else { num_launch<32, 8>(f1, 512, A, B, row_scale, *C); num_launch<32, 8>(f2, 2048, A, B, row_scale, *C); }
   } else if (cmax_need <= 16) {
