@@ -257,6 +257,18 @@ int cf_write_vtk(cf_problem p, const double* solution, const double* phi_old, co
  * block).  The state is global-length on every rank and holds the full solution on return.
  * size == 1 is the single-GPU step exactly. */
 typedef struct cf_comm_s* cf_comm;
+/* Host-staged transport (TEST ONLY: lets several ranks share one GPU to exercise the decomposed
+ * step's control flow without NCCL; device data is staged through host memory, so it is never
+ * used for a measurement).  Callbacks return 0 on success; rank-ordered semantics as NCCL's. */
+typedef struct {
+  void* ctx;
+  int (*allgather_f64)(void* ctx, const double* send, double* recv, int count);  /* recv: size*count */
+  int (*allreduce_i64)(void* ctx, long long* vals, int count, int op);           /* in place; op 0 sum, 1 max */
+  int (*sendrecv)(void* ctx, int n, const void* const* send, void* const* recv, const size_t* bytes,
+                  const int* peer);                                              /* send/recv may be NULL */
+  int (*bcast)(void* ctx, void* buf, size_t bytes, int root);
+} cf_host_transport;
+int cf_comm_create_host(int rank, int size, const cf_host_transport* transport, cf_comm* out);
 int cf_comm_unique_id(uint8_t id[128]);
 int cf_comm_create(const uint8_t id[128], int rank, int size, cf_comm* out);
 int cf_comm_info(cf_comm c, int* rank, int* size);

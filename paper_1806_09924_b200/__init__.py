@@ -321,6 +321,78 @@ class Communicator:
         dist.broadcast_object_list(obj, src=0, group=group)
         return cls(rank, size, obj[0])
 
+    @classmethod
+    def from_gloo(cls, group=None) -> "Communicator":
+        """TEST ONLY: a communicator whose transport is torch.distributed on host memory (e.g. gloo),
+        so several ranks can share one GPU to exercise the decomposed step's control flow.  Device
+        data is staged through the host; never used for a measurement."""
+        import torch
+        import torch.distributed as dist
+        from ._lib import AllgatherF64, AllreduceI64, Bcast, HostTransport, SendRecv
+        rank, size = dist.get_rank(group), dist.get_world_size(group)
+
+        def buf(ptr, n, ctype):
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(n,)) if n else np.zeros(0)
+
+        def allgather(_ctx, send, recv, k):
+            try:
+                t = torch.from_numpy(buf(send, k, C.c_double).copy())
+                parts = [torch.empty_like(t) for _ in range(size)]
+                dist.all_gather(parts, t, group=group)
+                buf(recv, size * k, C.c_double)[:] = torch.cat(parts).numpy()
+                return 0
+            except Exception:
+                return 1
+
+        def allreduce(_ctx, vals, k, op):
+            try:
+                a = buf(vals, k, C.c_longlong)
+                t = torch.from_numpy(a.astype(np.int64))
+                dist.all_reduce(t, op=dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX, group=group)
+                a[:] = t.numpy()
+                return 0
+            except Exception:
+                return 1
+
+        def sendrecv(_ctx, n, send, recv, nbytes, peer):
+            try:
+                ops, outs = [], []
+                for j in range(n):
+                    b = int(nbytes[j])
+                    if send[j]:
+                        t = torch.from_numpy(buf(send[j], b, C.c_uint8).copy())
+                        ops.append(dist.P2POp(dist.isend, t, int(peer[j]), group=group))
+                    if recv[j]:
+                        t = torch.empty(b, dtype=torch.uint8)
+                        ops.append(dist.P2POp(dist.irecv, t, int(peer[j]), group=group))
+                        outs.append((recv[j], b, t))
+                if ops:
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+                for p, b, t in outs:
+                    buf(p, b, C.c_uint8)[:] = t.numpy()
+                return 0
+            except Exception:
+                return 1
+
+        def bcast(_ctx, p, nbytes, root):
+            try:
+                a = buf(p, int(nbytes), C.c_uint8)
+                t = torch.from_numpy(a.copy())
+                dist.broadcast(t, src=root, group=group)
+                a[:] = t.numpy()
+                return 0
+            except Exception:
+                return 1
+
+        obj = cls.__new__(cls)
+        obj._callbacks = (AllgatherF64(allgather), AllreduceI64(allreduce), SendRecv(sendrecv), Bcast(bcast))
+        obj._transport = HostTransport(None, *obj._callbacks)
+        obj._h = C.c_void_p()
+        check(load().cf_comm_create_host(rank, size, C.byref(obj._transport), C.byref(obj._h)))
+        obj.rank, obj.size = rank, size
+        return obj
+
     def __del__(self):
         try:
             load().cf_comm_destroy(self._h)

@@ -154,6 +154,7 @@ SIGNATURES = [
     ("cf_write_vtk", _I, [_P, _P, _P, C.c_char_p, _I]),
     ("cf_comm_unique_id", _I, [_P]),
     ("cf_comm_create", _I, [_P, _I, _I, C.POINTER(_P)]),
+    ("cf_comm_create_host", _I, [_I, _I, _P, C.POINTER(_P)]),
     ("cf_comm_info", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
     ("cf_comm_destroy", _I, [_P]),
     ("cf_newton_active_set_step_comm", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
@@ -162,6 +163,18 @@ SIGNATURES = [
     ("cf_solve_loading_sequence_comm", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
                                             C.POINTER(SolverOptions), _P, _I, _P, _I, _P, _P, _P, C.POINTER(_I)]),
 ]
+
+
+AllgatherF64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int)
+AllreduceI64 = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_longlong), C.c_int, C.c_int)
+SendRecv = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                       C.POINTER(C.c_size_t), C.POINTER(C.c_int))
+Bcast = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int)
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather_f64", AllgatherF64), ("allreduce_i64", AllreduceI64),
+                ("sendrecv", SendRecv), ("bcast", Bcast)]
 
 
 class GmresResultC(C.Structure):

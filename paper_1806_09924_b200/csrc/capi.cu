@@ -798,6 +798,13 @@ int cf_comm_unique_id(uint8_t id[128]) {
   });
 }
 
+int cf_comm_create_host(int rank, int size, const cf_host_transport* transport, cf_comm* out) {
+  return guard([&] {
+    CHECK_ARG(out && transport, "cf_comm_create_host: null argument");
+    *out = new cf_comm_s{comm_create_host(rank, size, *transport)};
+  });
+}
+
 int cf_comm_create(const uint8_t id[128], int rank, int size, cf_comm* out) {
   return guard([&] {
     CHECK_ARG(out && (size == 1 || id), "cf_comm_create: null argument");

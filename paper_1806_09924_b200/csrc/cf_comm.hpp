@@ -21,6 +21,8 @@ struct HaloOp {
 struct Comm {
   int rank = 0, size = 1;
   void* nccl = nullptr;  // ncclComm_t
+  bool host = false;     // host-staged test transport (cf_host_transport) instead of NCCL
+  cf_host_transport ht{};
   mutable DevBuf<double> gather;
   mutable DevBuf<long long> ibuf;
   ~Comm();
@@ -40,5 +42,6 @@ struct Comm {
 
 void comm_unique_id(unsigned char out[128]);
 std::unique_ptr<Comm> comm_create(const unsigned char id[128], int rank, int size);
+std::unique_ptr<Comm> comm_create_host(int rank, int size, const cf_host_transport& t);
 
 }  // namespace cfb

@@ -6,6 +6,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "cf_comm.hpp"
 
@@ -102,6 +103,31 @@ std::unique_ptr<Comm> comm_create(const unsigned char id_bytes[128], int rank, i
   return c;
 }
 
+std::unique_ptr<Comm> comm_create_host(int rank, int size, const cf_host_transport& t) {
+  if (size < 1 || rank < 0 || rank >= size) fail(CF_ERR_INVALID_ARGUMENT, "comm_create_host: bad rank / size");
+  if (!t.allgather_f64 || !t.allreduce_i64 || !t.sendrecv || !t.bcast)
+    fail(CF_ERR_INVALID_ARGUMENT, "comm_create_host: missing callback");
+  auto c = std::make_unique<Comm>();
+  c->rank = rank;
+  c->size = size;
+  c->host = true;
+  c->ht = t;
+  return c;
+}
+
+namespace {
+void host_check(int rc, const char* what) {
+  if (rc != 0) fail(CF_ERR_COMM, std::string("host transport: ") + what + " failed");
+}
+void d2h(void* h, const void* d, size_t bytes) {
+  if (bytes) CF_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, stream()));
+}
+void h2d(void* d, const void* h, size_t bytes) {
+  if (bytes) CF_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream()));
+}
+void sync() { CF_CUDA(cudaStreamSynchronize(stream())); }
+}  // namespace
+
 Comm::~Comm() {
   if (nccl) {
     cudaStreamSynchronize(stream());
@@ -112,13 +138,26 @@ Comm::~Comm() {
 void Comm::sum_ordered(double* dev, int k) const {
   if (size == 1 || k <= 0) return;
   if (gather.n < i64(size) * k) gather.alloc(i64(size) * k);
-  CF_NCCL(::cfb::nccl().AllGather(dev, gather.p, size_t(k), ncclFloat64, H(nccl), stream()));
+  if (host) {
+    std::vector<double> mine(static_cast<size_t>(k)), all(static_cast<size_t>(size) * k);
+    d2h(mine.data(), dev, size_t(k) * sizeof(double));
+    sync();
+    host_check(ht.allgather_f64(ht.ctx, mine.data(), all.data(), k), "allgather");
+    h2d(gather.p, all.data(), all.size() * sizeof(double));
+  } else {
+    CF_NCCL(::cfb::nccl().AllGather(dev, gather.p, size_t(k), ncclFloat64, H(nccl), stream()));
+  }
   k_rank_sum<<<(k + 127) / 128, 128, 0, stream()>>>(gather.p, size, k, dev);
   CF_LAUNCHED();
 }
 
 void Comm::sum_i64(long long* host, int k) const {
   if (size == 1 || k <= 0) return;
+  if (this->host) {
+    sync();
+    host_check(ht.allreduce_i64(ht.ctx, host, k, 0), "allreduce");
+    return;
+  }
   if (ibuf.n < k) ibuf.alloc(k);
   CF_CUDA(cudaMemcpyAsync(ibuf.p, host, size_t(k) * sizeof(long long), cudaMemcpyHostToDevice, stream()));
   CF_NCCL(::cfb::nccl().AllReduce(ibuf.p, ibuf.p, size_t(k), ncclInt64, ncclSum, H(nccl), stream()));
@@ -128,6 +167,11 @@ void Comm::sum_i64(long long* host, int k) const {
 
 void Comm::max_i64(long long* host, int k) const {
   if (size == 1 || k <= 0) return;
+  if (this->host) {
+    sync();
+    host_check(ht.allreduce_i64(ht.ctx, host, k, 1), "allreduce");
+    return;
+  }
   if (ibuf.n < k) ibuf.alloc(k);
   CF_CUDA(cudaMemcpyAsync(ibuf.p, host, size_t(k) * sizeof(long long), cudaMemcpyHostToDevice, stream()));
   CF_NCCL(::cfb::nccl().AllReduce(ibuf.p, ibuf.p, size_t(k), ncclInt64, ncclMax, H(nccl), stream()));
@@ -137,6 +181,32 @@ void Comm::max_i64(long long* host, int k) const {
 
 void Comm::sendrecv(const std::vector<HaloOp>& ops) const {
   if (size == 1 || ops.empty()) return;
+  if (host) {
+    std::vector<std::vector<unsigned char>> sb(ops.size()), rb(ops.size());
+    std::vector<const void*> sp(ops.size(), nullptr);
+    std::vector<void*> rp(ops.size(), nullptr);
+    std::vector<size_t> by(ops.size());
+    std::vector<int> pe(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) {
+      by[i] = ops[i].bytes;
+      pe[i] = ops[i].peer;
+      if (ops[i].send) {
+        sb[i].resize(ops[i].bytes);
+        d2h(sb[i].data(), ops[i].send, ops[i].bytes);
+        sp[i] = sb[i].data();
+      }
+      if (ops[i].recv) {
+        rb[i].resize(ops[i].bytes);
+        rp[i] = rb[i].data();
+      }
+    }
+    sync();
+    host_check(ht.sendrecv(ht.ctx, int(ops.size()), sp.data(), rp.data(), by.data(), pe.data()), "sendrecv");
+    for (size_t i = 0; i < ops.size(); ++i)
+      if (ops[i].recv) h2d(ops[i].recv, rb[i].data(), ops[i].bytes);
+    sync();
+    return;
+  }
   const NcclApi& api = ::cfb::nccl();
   CF_NCCL(api.GroupStart());
   for (const HaloOp& o : ops) {
@@ -149,11 +219,24 @@ void Comm::sendrecv(const std::vector<HaloOp>& ops) const {
 
 void Comm::bcast(void* buf, size_t bytes, int root) const {
   if (size == 1 || bytes == 0) return;
+  if (host) {
+    std::vector<unsigned char> hb(bytes);
+    if (rank == root) d2h(hb.data(), buf, bytes);
+    sync();
+    host_check(ht.bcast(ht.ctx, hb.data(), bytes, root), "bcast");
+    if (rank != root) h2d(buf, hb.data(), bytes);
+    sync();
+    return;
+  }
   CF_NCCL(::cfb::nccl().Broadcast(buf, buf, bytes, ncclUint8, root, H(nccl), stream()));
 }
 
 void Comm::bcast_many(const std::vector<HaloOp>& ops) const {
   if (size == 1 || ops.empty()) return;
+  if (host) {
+    for (const HaloOp& o : ops) bcast(o.recv, o.bytes, o.peer);
+    return;
+  }
   const NcclApi& api = ::cfb::nccl();
   CF_NCCL(api.GroupStart());
   for (const HaloOp& o : ops)
