@@ -290,6 +290,74 @@ __device__ __forceinline__ double row_dot_st_emu(const i64* __restrict__ ptr, co
   return s[0];  // logical lane t; offsets < PH follow as shuffles over the PH threads
 }
 
+// ---- 3d stencil rows, 16 logical lanes on 8 threads, fast path for interior rows -------------
+// An interior row (all 27 neighbours free) has exactly 81 entries with the columns
+// colbase + off(e); thread t owns logical lanes t and t + 8, i.e. entries t + 16 j and t + 8 + 16 j
+// (j < 5) plus entry 80 for t = 0, whose offsets are fixed per thread and kept in registers.  The
+// two accumulators fold with the butterfly step 8 inside the thread; steps 4, 2, 1 are shuffles.
+__device__ __forceinline__ int st_off3(int e, int nn) {
+  const int n = e / 3, b = e - 3 * n;
+  return 3 * ((n % 3) + nn * ((n / 3) % 3 + nn * (n / 9))) + b;
+}
+
+struct St16Regs {
+  int a[6], b[5];
+  __device__ void init(int t, int nn) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      a[j] = st_off3(t + 16 * j, nn);
+      b[j] = st_off3(t + 8 + 16 * j, nn);
+    }
+    a[5] = st_off3(80, nn);
+  }
+};
+
+// logical-lane-t value after the in-thread butterfly step (s_t + s_{t+8}) of an interior row
+__device__ __forceinline__ double row16_interior(const double* __restrict__ vrow, const double* __restrict__ xb,
+                                                 int t, const St16Regs& o) {
+  double va[6], vb[5], xa[6], xv[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    va[j] = ld_stream(vrow + t + 16 * j);
+    vb[j] = ld_stream(vrow + t + 8 + 16 * j);
+  }
+  va[5] = (t == 0) ? ld_stream(vrow + 80) : 0.0;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    xa[j] = __ldg(xb + o.a[j]);
+    xv[j] = __ldg(xb + o.b[j]);
+  }
+  xa[5] = (t == 0) ? __ldg(xb + o.a[5]) : 0.0;
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    sa += va[j] * xa[j];
+    sb += vb[j] * xv[j];
+  }
+  sa += va[5] * xa[5];  // +0.0 for t != 0: never changes a sum that starts at +0.0
+  return sa + sb;
+}
+
+// interior test and column base of a row (3d); false for rows that need the general path
+__device__ __forceinline__ bool st16_interior(const StencilCols& sc, i64 row, i64 len, const double* __restrict__ x,
+                                              const double*& xb) {
+  if (len != 81) return false;
+  const unsigned lv = sc.kind == 1 ? unsigned(row) / 3u : unsigned(row);
+  const unsigned v = unsigned(sc.v_lo) + lv, nn = unsigned(sc.nn);
+  auto divn = [&](unsigned t) {
+    unsigned q = unsigned(double(t) * sc.inv_nn);
+    if (q * nn > t) --q;
+    else if ((q + 1) * nn <= t) ++q;
+    return q;
+  };
+  const unsigned vy = divn(v), vz = divn(vy);
+  const unsigned xx = v - vy * nn, yy = vy - vz * nn, zz = vz;
+  const unsigned lo = 2u, hi = nn - 3u;
+  if (xx < lo || xx > hi || yy < lo || yy > hi || zz < lo || zz > hi) return false;
+  xb = x + (i64(3) * (v - 1u - nn - nn * nn) - sc.shift);
+  return true;
+}
+
 // the same emulation for a stored-column row
 template <int TPR, int PH, int U>
 __device__ __forceinline__ double row_dot_b_emu(const i64* __restrict__ ptr, const int* __restrict__ col,
@@ -346,6 +414,78 @@ __global__ void __launch_bounds__(256) k_spmv_st_emu(i64 rows, const i64* __rest
   if (row < rows) s = row_dot_st_emu<TPR, PH, U, D>(ptr, val, x, row, t, sc, off);
   s = group_sum<PH>(s);
   if (row < rows && t == 0) y[row] = add ? add[row] + s : s;
+}
+
+// persistent form: each 8-thread group walks rows g, g + G, ... and fetches the next row's
+// pointers before the current row's loads, so the row-pointer latency overlaps the value stream
+__global__ void __launch_bounds__(256) k_spmv_st16p(i64 rows, const i64* __restrict__ ptr,
+                                                    const double* __restrict__ val, const double* __restrict__ x,
+                                                    double* y, const double* add, StencilCols sc) {
+  __shared__ int off[StOff<3>::N];
+  StOff<3>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 G = (i64(gridDim.x) * blockDim.x) >> 3;
+  const i64 g0 = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
+  const int t = int(threadIdx.x & 7);
+  St16Regs o;
+  o.init(t, int(sc.nn));
+  i64 b0 = 0, b1 = 0;
+  if (g0 < rows) {
+    b0 = ptr[g0];
+    b1 = ptr[g0 + 1];
+  }
+  for (i64 row = g0; row < rows; row += G) {
+    i64 n0 = 0, n1 = 0;
+    if (row + G < rows) {
+      n0 = ptr[row + G];
+      n1 = ptr[row + G + 1];
+    }
+    const double* xb = nullptr;
+    double s;
+    if (st16_interior(sc, row, b1 - b0, x, xb)) s = row16_interior(val + b0, xb, t, o);
+    else s = row_dot_st_emu<16, 8, 1, 3>(ptr, val, x, row, t, sc, off);
+    s = group_sum<8>(s);
+    if (t == 0) y[row] = add ? add[row] + s : s;
+    b0 = n0;
+    b1 = n1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_spmv_phi_st16p(i64 rows, const i64* __restrict__ p1,
+                                                        const double* __restrict__ v1, const double* __restrict__ x1,
+                                                        StencilCols sc, const i64* __restrict__ p2,
+                                                        const int* __restrict__ c2, const double* __restrict__ v2,
+                                                        const double* __restrict__ x2, double* __restrict__ y) {
+  __shared__ int off[StOff<3>::N];
+  StOff<3>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 G = (i64(gridDim.x) * blockDim.x) >> 3;
+  const i64 g0 = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
+  const int t = int(threadIdx.x & 7);
+  St16Regs o;
+  o.init(t, int(sc.nn));
+  i64 b0 = 0, b1 = 0;
+  if (g0 < rows) {
+    b0 = p1[g0];
+    b1 = p1[g0 + 1];
+  }
+  for (i64 row = g0; row < rows; row += G) {
+    i64 n0 = 0, n1 = 0;
+    if (row + G < rows) {
+      n0 = p1[row + G];
+      n1 = p1[row + G + 1];
+    }
+    const double* xb = nullptr;
+    double s1;
+    if (st16_interior(sc, row, b1 - b0, x1, xb)) s1 = row16_interior(v1 + b0, xb, t, o);
+    else s1 = row_dot_st_emu<16, 8, 1, 3>(p1, v1, x1, row, t, sc, off);
+    double s2 = row_dot_b_emu<16, 8, 2>(p2, c2, v2, x2, row, t);
+    s1 = group_sum<8>(s1);
+    s2 = group_sum<8>(s2);
+    if (t == 0) y[row] = s1 + s2;
+    b0 = n0;
+    b1 = n1;
+  }
 }
 
 template <int TPR, int PH, int U, int D>
@@ -438,6 +578,11 @@ __global__ void __launch_bounds__(256) k_st_check(i64 rows, const i64* __restric
   if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
+bool st_emu_only() {  // A/B switch: CF_ST_EMU=1 keeps the generic emulated kernel
+  static const bool v = std::getenv("CF_ST_EMU") != nullptr;
+  return v;
+}
+
 template <int TPR>
 void launch_spmv(const Csr& A, const double* x, double* y, const double* add) {
   const int block = 256;
@@ -452,7 +597,15 @@ void launch_phi(const BlockSystem& J, const double* x, double* y) {
   const i64 threads = J.np * TPR;
   if (J.pu->st.kind != 0) {
     const Csr &A = *J.pu, &B = *J.pp;
-    if (TPR == 16 && A.st.d == 3)
+    if (TPR == 16 && A.st.d == 3 && !st_emu_only()) {
+      static int bps = 0;
+      if (!bps) CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_phi_st16p, block, 0));
+      const i64 want = grid_for(J.np * 8, block);
+      const int grid = int(std::min<i64>(want, i64(std::max(1, bps)) * rt().sm_count));
+      k_spmv_phi_st16p<<<grid, block, 0, stream()>>>(J.np, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p,
+                                                     x + J.in_u(), y + J.nu);
+    }
+    else if (TPR == 16 && A.st.d == 3)
       k_spmv_phi_st_emu<16, 8, 2, 3><<<grid_for(J.np * 8, block), block, 0, stream()>>>(
           J.np, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p, x + J.in_u(), y + J.nu);
     else if (A.st.d == 3)
@@ -476,6 +629,13 @@ void launch_b(const Csr& A, const double* x, double* y, const double* add) {
   const i64 threads = A.rows * TPR;
   if (A.st.kind == 0)
     k_spmv_b<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, add);
+  else if (TPR == 16 && A.st.d == 3 && !st_emu_only()) {  // persistent, pointer prefetch
+    static int bps = 0;
+    if (!bps) CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_st16p, block, 0));
+    const i64 want = grid_for(A.rows * 8, block);
+    const int grid = int(std::min<i64>(want, i64(std::max(1, bps)) * rt().sm_count));
+    k_spmv_st16p<<<grid, block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, add, A.st);
+  }
   else if (TPR == 16 && A.st.d == 3)  // 8 threads per row emulating the 16-lane reduction (sweep)
     k_spmv_st_emu<16, 8, 2, 3><<<grid_for(A.rows * 8, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y,
                                                                                    add, A.st);
