@@ -279,7 +279,7 @@ def operator_leg(cf, device, stream, applies=20):
     torch.cuda.empty_cache()
     return res, {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                  "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
-                 "kernel": ("k_spmv_st_emu<16,8,2,3> (stencil-implicit columns, M_uu of config 1)" if fmt == "stencil"
+                 "kernel": ("k_spmv_st16p (stencil-implicit columns, M_uu of config 1)" if fmt == "stencil"
                             else "k_spmv_b<16,4> (CSR SpMV, M_uu of config 1)"), "bytes_per_launch": nb,
                  "ms_per_launch": ms, "peak_source": src}
 
