@@ -284,6 +284,29 @@ def operator_leg(cf, device, stream, applies=20):
                  "ms_per_launch": ms, "peak_source": src}
 
 
+def vcycle_leg(cf, P, mat, reg, x_final, phi_old, stream):
+    """AMG V-cycle time per application, u- and phi-hierarchies separately, built from the
+    Jacobian at the converged state of the measured step (active set = phi dofs at phi_old)."""
+    import torch
+    xs = x_final.cpu().numpy()
+    po = phi_old.cpu().numpy()
+    act = np.nonzero(xs[P.n_u:] == po)[0]
+    cs = cf.build_constraints(P, True, {int(P.n_u + v): float(po[v]) for v in act})
+    J = cf.assemble_jacobian(P, cs, mat, reg, x_final, phi_old)
+    node_u = np.repeat(np.arange(P.n_vertices, dtype=np.int32), P.dim)
+    hu = cf.build_amg(cf.CsrMatrix.from_block(J, 0), node_u, cf.rigid_body_modes(P, cs))
+    free = 1.0 - np.isin(np.arange(P.n_vertices), act)
+    hp = cf.build_amg(cf.CsrMatrix.from_block(J, 2), np.arange(P.n_vertices, dtype=np.int32), free.reshape(-1, 1))
+    out = {}
+    for name, h, n in (("u", hu, P.n_u), ("phi", hp, P.n_phi)):
+        r = torch.randn(n, dtype=torch.float64, device=x_final.device)
+        h.v_cycle(r)
+        out[name + "_ms"] = time_events(lambda: h.v_cycle(r), 10, stream)
+        out[name + "_levels"] = h.n_levels()
+    out["note"] = "one V-cycle application (zero initial guess, 1+1 damped Jacobi sweeps per level, dense LU on the coarsest)"
+    return out
+
+
 def rebuild_probe():
     """One warm config-3 step with CF_NO_AMG_REUSE=1 (every hierarchy rebuilt every iteration)."""
     import torch
@@ -381,6 +404,12 @@ def ours(args):
         except Exception as ex:  # reported, never fatal
             full = {"error": str(ex)[:200]}
 
+    vcyc = None
+    if rank == 0 and world == 1:
+        try:
+            vcyc = vcycle_leg(cf, P, mat, reg, torch.from_numpy(st.get()["solution"]).to(device), po0, s)
+        except Exception as ex:  # reported, never fatal
+            vcyc = {"error": str(ex)[:200]}
     if rank != 0:
         return
     op, roof = operator_leg(cf, device, s) if not args.no_operator else (None, None)
@@ -395,7 +424,7 @@ def ours(args):
         "active_set_final": last["iterations"][-1]["active_size"],
         "phase_ms_last_step": last["times_ms"], "device_mem_used_gb": (total - free) / 1e9,
         "roofline": roof, "operator": op, "e2e": e2e, "gpu_launches": int(launches),
-        "full_rebuild": full,
+        "full_rebuild": full, "vcycle": vcyc,
         "gpu_launches_per_step": launches / args.steps, "clocks": clk.summary(),
     }
     if not args.no_cpu and world == 1:
