@@ -34,6 +34,9 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
 #include <unordered_map>
 #include <vector>
 
@@ -326,13 +329,92 @@ static double row_sum_lanes(const Csr& A, i64 i, const double* x, int tpr) {
   }
   return lane[0];
 }
+// Row-parallel SpMV on a persistent host thread pool (orc_set_threads; 1 = the single-threaded
+// reference).  The reference's only multi-threaded kernel is Eigen's sparse x dense product under
+// Eigen::setNbThreads (crackfield.cpp:39); every row is still summed exactly as above, so results do
+// not depend on the thread count.
+class RowPool {
+ public:
+  void resize(int n) {
+    stop_all();
+    n_ = std::max(1, n);
+    for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { loop(t); });
+  }
+  int size() const { return n_; }
+  template <class F>
+  void run(i64 rows, F&& f) {  // f(lo, hi) over n_ chunks, chunk 0 on the caller
+    if (n_ == 1 || rows < 4096) {
+      f(i64(0), rows);
+      return;
+    }
+    std::function<void(int)> job = [&](int t) {
+      const i64 chunk = (rows + n_ - 1) / n_;
+      f(std::min(rows, t * chunk), std::min(rows, (t + 1) * chunk));
+    };
+    {
+      std::unique_lock<std::mutex> lk(m_);
+      job_ = &job;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    job(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+  ~RowPool() { stop_all(); }
+
+ private:
+  void loop(int t) {
+    int seen = 0;
+    for (;;) {
+      std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        job = job_;
+      }
+      (*job)(t);
+      std::lock_guard<std::mutex> lk(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  void stop_all() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& x : th_) x.join();
+    th_.clear();
+    stop_ = false;
+  }
+  int n_ = 1, gen_ = 0, pending_ = 0;
+  bool stop_ = false;
+  std::function<void(int)>* job_ = nullptr;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+};
+static RowPool& row_pool() {
+  static RowPool p;
+  return p;
+}
+
 static void spmv(const Csr& A, const double* x, double* y) {  // y = A x
   const int tpr = spmv_tpr(A);
-  for (i64 i = 0; i < A.rows; ++i) y[i] = row_sum_lanes(A, i, x, tpr);
+  row_pool().run(A.rows, [&](i64 lo, i64 hi) {
+    for (i64 i = lo; i < hi; ++i) y[i] = row_sum_lanes(A, i, x, tpr);
+  });
 }
 static void spmv_add(const Csr& A, const double* x, double* y) {  // y += A x
   const int tpr = spmv_tpr(A);
-  for (i64 i = 0; i < A.rows; ++i) y[i] = y[i] + row_sum_lanes(A, i, x, tpr);
+  row_pool().run(A.rows, [&](i64 lo, i64 hi) {
+    for (i64 i = lo; i < hi; ++i) y[i] = y[i] + row_sum_lanes(A, i, x, tpr);
+  });
 }
 
 static Csr transpose(const Csr& A) {
@@ -419,8 +501,10 @@ struct BlockSystem {
     spmv(uu, x.data(), y.data());
     // phi rows: one lane group per row over both blocks; the group size follows M_phiu's mean
     const int tpr = spmv_tpr(pu);
-    for (i64 i = 0; i < np; ++i)
-      y[nu + i] = row_sum_lanes(pu, i, x.data(), tpr) + row_sum_lanes(pp, i, x.data() + nu, tpr);
+    row_pool().run(np, [&](i64 lo, i64 hi) {
+      for (i64 i = lo; i < hi; ++i)
+        y[nu + i] = row_sum_lanes(pu, i, x.data(), tpr) + row_sum_lanes(pp, i, x.data() + nu, tpr);
+    });
     return y;
   }
 };
@@ -1847,6 +1931,13 @@ int orc_block_apply(orc_block* b, const double* x, double* y) {
   std::copy(yv.begin(), yv.end(), y);
   return 0;
 }
+// host threads of the row-parallel SpMV (1 = the single-threaded reference)
+int orc_set_threads(int threads) {
+  row_pool().resize(threads);
+  return 0;
+}
+int orc_get_threads(void) { return row_pool().size(); }
+
 // SpMV of one block with `threads` OpenMP threads (row-parallel; each row summed sequentially,
 // so the result is independent of the thread count).  Used for the bounded CPU baseline.
 int orc_block_spmv_threads(orc_block* b, int which, const double* x, double* y, int threads) {

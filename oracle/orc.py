@@ -93,6 +93,16 @@ def lib():
     return _lib
 
 
+def set_threads(n: int) -> None:
+    """Host threads of the oracle's row-parallel SpMV (1 = the single-threaded reference; results
+    are bitwise independent of the count)."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
+
+
 def _p(a, ct=C.c_double):
     return a.ctypes.data_as(C.POINTER(ct)) if a is not None else None
 

@@ -514,3 +514,22 @@ def test_tcv_closed_form_convergence(orc):  # reference_test.cpp:21-40, PAPER.md
     assert rep["converged"]
     tcv = abs(P.tcv(sol))
     assert 0.5 * exact < tcv < 1.5 * exact
+
+
+def test_oracle_threads_bitwise(orc):
+    """The row-parallel SpMV of the oracle (orc_set_threads) leaves every Newton result bitwise
+    unchanged: a 2d Sneddon step (80x80, SpMVs above the pool's 4096-row threshold) with 1 and
+    with 4 host threads."""
+    O = orc.Problem(2, 5.0, 10, 3)
+    m = orc.material()
+    reg = O.resolve_regularization(m, O.slit_band_edge(m))
+    phi, _ = O.initial_crack(m)
+    out = []
+    for t in (1, 4):
+        orc.set_threads(t)
+        sol = np.zeros(O.n_total)
+        sol[O.n_u:] = phi
+        rep = O.newton_step(m, reg, orc.solver_options(), sol, phi.copy(), phi.copy(), 0, shift=False)
+        out.append((rep["iterations"], sol))
+    orc.set_threads(1)
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
