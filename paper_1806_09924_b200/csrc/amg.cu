@@ -1311,10 +1311,11 @@ bool Amg::same_inputs(const Csr& A, const int* node_of_dof, const double* B, int
       o.jacobi_omega != opts.jacobi_omega || o.smoothing_sweeps != opts.smoothing_sweeps ||
       o.coarse_size != opts.coarse_size || o.max_levels != opts.max_levels)
     return false;
-  return bitwise_equal(A.ptr.p, A0->ptr.p, size_t(A.rows + 1) * sizeof(i64)) &&
-         bitwise_equal(A.col.p, A0->col.p, size_t(A.nnz) * sizeof(int)) &&
-         bitwise_equal(A.val.p, A0->val.p, size_t(A.nnz) * sizeof(double)) &&
-         bitwise_equal(node_of_dof, nod0.p, size_t(A.rows) * sizeof(int)) &&
+  const bool same_matrix = &A == A0.get() ||  // the very matrix the hierarchy was built from
+                           (bitwise_equal(A.ptr.p, A0->ptr.p, size_t(A.rows + 1) * sizeof(i64)) &&
+                            bitwise_equal(A.col.p, A0->col.p, size_t(A.nnz) * sizeof(int)) &&
+                            bitwise_equal(A.val.p, A0->val.p, size_t(A.nnz) * sizeof(double)));
+  return same_matrix && bitwise_equal(node_of_dof, nod0.p, size_t(A.rows) * sizeof(int)) &&
          bitwise_equal(B, B0.p, size_t(A.rows) * m * sizeof(double));
 }
 

@@ -383,7 +383,7 @@ __device__ inline void pair_blocks(const Tables* __restrict__ T, const Coef& cf,
 
 // K2 count pass: row lengths of the three blocks; constrained rows keep a diagonal iff its
 // summed value is non-zero (model.cpp:295,300,308-311).
-template <int D>
+template <int D, bool UU>
 __global__ void k_jac_count(GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
                             const std::uint8_t* __restrict__ flag, i64* __restrict__ cnt_uu,
                             i64* __restrict__ cnt_pu, i64* __restrict__ cnt_pp, Slab sl) {
@@ -415,208 +415,13 @@ __global__ void k_jac_count(GridDesc g, const Tables* __restrict__ T, Coef cf, c
     common_cells<D>(g, x, y, z, 0, 0, 0, L);
     pair_blocks<D>(T, cf, qs, L, true, true, pb);
   }
+  if (UU) {
 #pragma unroll
-  for (int a = 0; a < D; ++a) cnt_uu[lv * D + a] = flag[v * D + a] ? (pb.uu[a][a] != 0.0 ? 1 : 0) : nfu;
+    for (int a = 0; a < D; ++a) cnt_uu[lv * D + a] = flag[v * D + a] ? (pb.uu[a][a] != 0.0 ? 1 : 0) : nfu;
+  }
   const bool pf = flag[nu + v] == 0;
   cnt_pu[lv] = pf ? nfu : 0;
   cnt_pp[lv] = pf ? nfp : (pb.pp != 0.0 ? 1 : 0);
-}
-
-// Shared-memory copy of the per-problem quadrature tables (the 36 KB integrand table is not
-// staged: its entries are recomputed from gp with the reference's expression, bit-identically).
-template <int D>
-struct SmTables {
-  static constexpr int NQ = 1 << D, NV = 1 << D;
-  double s[NQ][NV];
-  double gp[NQ][NV][D];
-  double gg[NQ][NV][NV];
-  double w[NQ];
-  double val[NQ][NV][NV][D * D];  // integrand table (host-computed, model.cpp:274-275)
-  __device__ void load(const Tables* __restrict__ T) {
-    for (int i = threadIdx.x; i < NQ * NV; i += blockDim.x) {
-      const int q = i / NV, k = i % NV;
-      s[q][k] = T->s[q][k];
-      for (int b = 0; b < D; ++b) gp[q][k][b] = T->gp[q][k][b];
-      for (int l = 0; l < NV; ++l) gg[q][k][l] = T->gg[q][k][l];
-    }
-    for (int i = threadIdx.x; i < NQ * NV * NV * D * D; i += blockDim.x) {
-      const int ab = i % (D * D), l = (i / (D * D)) % NV, k = (i / (D * D * NV)) % NV, q = i / (D * D * NV * NV);
-      val[q][k][l][ab] = T->val[q][k][l][ab / D][ab % D];
-    }
-    for (int q = threadIdx.x; q < NQ; q += blockDim.x) w[q] = T->w[q];
-  }
-};
-
-// Warp-per-vertex fill pass (persistent grid).  Lane s owns stencil slot s of the row vertex v.
-// The warp walks v's adjacent cells in the reference order (the same for every lane), stages the
-// cell's AoS qp states once in shared memory, and every lane whose column vertex is a corner of
-// that cell adds the cell's element-matrix block for (k = v's corner, l = w's corner): per lane the
-// cells are still summed in reference order, so every value is the reference's element sum.
-// Rows are the slab's owned vertices (local numbering), columns are ext-numbered.
-template <int D>
-constexpr int fill_wpb() { return D == 3 ? 4 : 8; }  // 3d: 42 KB of tables + 4 x 832 B staging
-
-template <int D>
-__global__ void __launch_bounds__(fill_wpb<D>() * 32) k_jac_fill_warp(
-    GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
-    const std::uint8_t* __restrict__ flag, const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
-    double* __restrict__ val_uu, const i64* __restrict__ ptr_pu, int* __restrict__ col_pu,
-    double* __restrict__ val_pu, const i64* __restrict__ ptr_pp, int* __restrict__ col_pp,
-    double* __restrict__ val_pp, Slab sl) {
-  constexpr int S = (D == 3) ? 27 : 9, NQ = 1 << D, NS = QS<D>::NS, CS = NQ * NS, WPB = fill_wpb<D>();
-  __shared__ SmTables<D> sT;
-  __shared__ double sst[WPB][CS];
-  sT.load(T);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
-  const double c2k = 2.0 * (1.0 - cf.kap), c2p = 2.0 * cf.p, omk = 1.0 - cf.kap;
-  const double gce = cf.Gc / cf.eps, gcx = cf.Gc * cf.eps;
-  const i64 nu = g.n_u();
-  const i64 ushift = D * sl.ve_lo, pshift = sl.ve_lo;  // global column -> ext column
-  qs -= sl.c_lo * CS;
-  for (i64 lv = i64(blockIdx.x) * WPB + wv; lv < sl.nv(); lv += i64(gridDim.x) * WPB) {
-    const i64 v = sl.v_lo + lv;
-    i64 x, y, z;
-    vxyz<D>(g, v, x, y, z);
-    const int s = lane;
-    const int dx = s % 3 - 1, dy = (s / 3) % 3 - 1, dz = (D == 3) ? s / 9 - 1 : 0;
-    const i64 X = x + dx, Y = y + dy, Z = z + dz;
-    const bool slot_ok = s < S && X >= 0 && Y >= 0 && Z >= 0 && X < g.nn && Y < g.nn &&
-                         Z < ((D == 3) ? g.nn : 1);
-    const i64 w = slot_ok ? X + g.nn * (Y + g.nn * Z) : v;
-    bool rowfree_u[D], colfree_u[D];
-    bool any_row_u = false, any_col_u = false;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      rowfree_u[a] = flag[v * D + a] == 0;
-      colfree_u[a] = flag[w * D + a] == 0;
-      any_row_u |= rowfree_u[a];
-      any_col_u |= colfree_u[a];
-    }
-    const bool rowfree_p = flag[nu + v] == 0, colfree_p = flag[nu + w] == 0;
-    const bool center = slot_ok && (w == v);
-    bool any_con_row = !rowfree_p;
-#pragma unroll
-    for (int a = 0; a < D; ++a) any_con_row |= !rowfree_u[a];
-    const bool need_u = slot_ok && ((any_row_u && any_col_u) || (center && any_con_row));
-    const bool need_p = slot_ok && ((rowfree_p && (any_col_u || colfree_p)) || (center && !rowfree_p));
-    // v's adjacent cells in reference order (identical for every lane)
-    CellList<D> L;
-    common_cells<D>(g, x, y, z, 0, 0, 0, L);
-    PairBlocks<D> pb;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-#pragma unroll
-      for (int b = 0; b < D; ++b) pb.uu[a][b] = 0.0;
-      pb.pu[a] = 0.0;
-    }
-    pb.pp = 0.0;
-    for (int i = 0; i < L.n; ++i) {
-      const double* src = qs + L.cell[i] * CS;
-      for (int e = lane; e < CS; e += 32) sst[wv][e] = src[e];
-      __syncwarp();
-      // is w a corner of this cell?  t_a = bit a of k (v is the high corner along a)
-      const int k = L.kv[i];
-      int l = 0;
-      bool in = need_u || need_p;
-      const int del[3] = {dx, dy, dz};
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        const int la = ((k >> a) & 1) + del[a];
-        in = in && la >= 0 && la <= 1;
-        l |= (la & 1) << a;
-      }
-      if (in) {
-        double bu[D][D], bp[D], bpp = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-#pragma unroll
-          for (int b = 0; b < D; ++b) bu[a][b] = 0.0;
-          bp[a] = 0.0;
-        }
-        for (int q = 0; q < NQ; ++q) {
-          const double* st = &sst[wv][q * NS];
-          double gl[D];
-#pragma unroll
-          for (int b = 0; b < D; ++b) gl[b] = sT.gp[q][l][b];
-          if (need_u) {
-            const double wg = st[0];
-            const double* vl = sT.val[q][k][l];
-#pragma unroll
-            for (int a = 0; a < D; ++a)
-#pragma unroll
-              for (int b = 0; b < D; ++b) bu[a][b] += wg * vl[a * D + b];
-          }
-          if (need_p) {
-            const double wq = sT.w[q];
-            const double phi = st[1], tre = st[2], see = st[3];
-            const double sk = sT.s[q][k], sl = sT.s[q][l];
-#pragma unroll
-            for (int b = 0; b < D; ++b) {
-              double sgl = 0.0;
-#pragma unroll
-              for (int c = 0; c < D; ++c) sgl += st[4 + b * D + c] * gl[c];
-              bp[b] += wq * (c2k * phi * sgl + c2p * phi * gl[b]) * sk;
-            }
-            bpp += wq * ((omk * see + c2p * tre + gce) * sl * sk + gcx * sT.gg[q][k][l]);
-          }
-        }
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-#pragma unroll
-          for (int b = 0; b < D; ++b) pb.uu[a][b] += bu[a][b];
-          pb.pu[a] += bp[a];
-        }
-        pb.pp += bpp;
-      }
-      __syncwarp();
-    }
-    if (!(need_u || need_p)) continue;
-    i64 off_u = 0, off_p = 0;
-    for (int s2 = 0; s2 < s; ++s2) {
-      const int ex = s2 % 3 - 1, ey = (s2 / 3) % 3 - 1, ez = (D == 3) ? s2 / 9 - 1 : 0;
-      const i64 X2 = x + ex, Y2 = y + ey, Z2 = z + ez;
-      if (X2 < 0 || Y2 < 0 || Z2 < 0 || X2 >= g.nn || Y2 >= g.nn || Z2 >= ((D == 3) ? g.nn : 1)) continue;
-      const i64 w2 = X2 + g.nn * (Y2 + g.nn * Z2);
-#pragma unroll
-      for (int b = 0; b < D; ++b) off_u += flag[w2 * D + b] ? 0 : 1;
-      off_p += flag[nu + w2] ? 0 : 1;
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const i64 row = lv * D + a;
-      if (rowfree_u[a]) {
-        i64 pos = ptr_uu[row] + off_u;
-#pragma unroll
-        for (int b = 0; b < D; ++b)
-          if (colfree_u[b]) {
-            col_uu[pos] = int(w * D + b - ushift);
-            val_uu[pos] = pb.uu[a][b];
-            ++pos;
-          }
-      } else if (center && ptr_uu[row + 1] > ptr_uu[row]) {
-        col_uu[ptr_uu[row]] = int(v * D + a - ushift);
-        val_uu[ptr_uu[row]] = pb.uu[a][a];
-      }
-    }
-    if (rowfree_p) {
-      i64 pos = ptr_pu[lv] + off_u;
-#pragma unroll
-      for (int b = 0; b < D; ++b)
-        if (colfree_u[b]) {
-          col_pu[pos] = int(w * D + b - ushift);
-          val_pu[pos] = pb.pu[b];
-          ++pos;
-        }
-      if (colfree_p) {
-        col_pp[ptr_pp[lv] + off_p] = int(w - pshift);
-        val_pp[ptr_pp[lv] + off_p] = pb.pp;
-      }
-    } else if (center && ptr_pp[lv + 1] > ptr_pp[lv]) {
-      col_pp[ptr_pp[lv]] = int(v - pshift);
-      val_pp[ptr_pp[lv]] = pb.pp;
-    }
-  }
 }
 
 // Pair-parallel fill pass (persistent grid, one warp per row vertex v).  The work of a row
@@ -639,7 +444,7 @@ struct PairSmem {
   double res[pair_wpb<D>()][32][NR];
 };
 
-template <int D>
+template <int D, bool UU>
 __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
     GridDesc g, const Tables* __restrict__ T, Coef cf, const double* __restrict__ qs,
     const std::uint8_t* __restrict__ flag, const i64* __restrict__ ptr_uu, int* __restrict__ col_uu,
@@ -746,12 +551,14 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
           double gl[D];
 #pragma unroll
           for (int b = 0; b < D; ++b) gl[b] = sm.gp[q][l][b];
-          const double wg = __ldg(st);
-          const double* vl = sm.val[q][k][l];
+          if (UU) {
+            const double wg = __ldg(st);
+            const double* vl = sm.val[q][k][l];
 #pragma unroll
-          for (int a = 0; a < D; ++a)
+            for (int a = 0; a < D; ++a)
 #pragma unroll
-            for (int b = 0; b < D; ++b) bu[a][b] += wg * vl[a * D + b];
+              for (int b = 0; b < D; ++b) bu[a][b] += wg * vl[a * D + b];
+          }
           const double wq = sm.w[q];
           const double phi = __ldg(st + 1), tre = __ldg(st + 2), see = __ldg(st + 3);
           const double sk = sm.s[q][k], slv = sm.s[q][l];
@@ -821,7 +628,7 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
       off_p += flag[nu + w2] ? 0 : 1;
     }
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
+    for (int a = 0; a < D && UU; ++a) {
       const i64 row = lv * D + a;
       if (rowfree_u[a]) {
         i64 pos = ptr_uu[row] + off_u;
@@ -1071,7 +878,7 @@ void assemble_residual(Problem& P, const Constraints& cs, const cf_material& m, 
 
 template <int D>
 static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, const double* x, const double* pt,
-                          const Slab& sl, BlockSystem& J) {
+                          const Slab& sl, BlockSystem& J, bool with_uu) {
   const GridDesc& g = P.g;
   constexpr int NQ = 1 << D, NS = QS<D>::NS;
   const i64 ncl = sl.c_hi - sl.c_lo;
@@ -1079,65 +886,67 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   k_cell_qpstate<D><<<grid_for(ncl, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p, sl.c_lo, sl.c_hi);
   CF_LAUNCHED();
   const i64 nu = D * sl.nv(), np = sl.nv();
-  J.uu->rows = nu;
-  J.uu->cols = D * sl.ne();
   J.pu->rows = np;
   J.pu->cols = D * sl.ne();
   J.pp->rows = np;
   J.pp->cols = sl.ne();
-  J.uu->ptr.alloc(nu + 1);
+  if (with_uu) {
+    J.uu->rows = nu;
+    J.uu->cols = D * sl.ne();
+    J.uu->ptr.alloc(nu + 1);
+    CF_CUDA(cudaMemsetAsync(J.uu->ptr.p + nu, 0, sizeof(i64), stream()));
+  }
   J.pu->ptr.alloc(np + 1);
   J.pp->ptr.alloc(np + 1);
-  CF_CUDA(cudaMemsetAsync(J.uu->ptr.p + nu, 0, sizeof(i64), stream()));
   CF_CUDA(cudaMemsetAsync(J.pu->ptr.p + np, 0, sizeof(i64), stream()));
   CF_CUDA(cudaMemsetAsync(J.pp->ptr.p + np, 0, sizeof(i64), stream()));
-  k_jac_count<D><<<grid_for(sl.nv(), 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p,
-                                                               J.pu->ptr.p, J.pp->ptr.p, sl);
+  if (with_uu)
+    k_jac_count<D, true><<<grid_for(sl.nv(), 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p,
+                                                                       J.pu->ptr.p, J.pp->ptr.p, sl);
+  else
+    k_jac_count<D, false><<<grid_for(sl.nv(), 128), 128, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, nullptr,
+                                                                        J.pu->ptr.p, J.pp->ptr.p, sl);
   CF_LAUNCHED();
-  exclusive_scan_inplace(J.uu->ptr.p, nu);
+  if (with_uu) exclusive_scan_inplace(J.uu->ptr.p, nu);
   exclusive_scan_inplace(J.pu->ptr.p, np);
   exclusive_scan_inplace(J.pp->ptr.p, np);
-  i64 nnz[3];
-  CF_CUDA(cudaMemcpyAsync(&nnz[0], J.uu->ptr.p + nu, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  i64 nnz[3] = {0, 0, 0};
+  if (with_uu) CF_CUDA(cudaMemcpyAsync(&nnz[0], J.uu->ptr.p + nu, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaMemcpyAsync(&nnz[1], J.pu->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaMemcpyAsync(&nnz[2], J.pp->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
-  J.uu->nnz = nnz[0];
+  if (with_uu) {
+    J.uu->nnz = nnz[0];
+    J.uu->col.alloc(nnz[0]);
+    J.uu->val.alloc(nnz[0]);
+  }
   J.pu->nnz = nnz[1];
   J.pp->nnz = nnz[2];
-  J.uu->col.alloc(nnz[0]);
-  J.uu->val.alloc(nnz[0]);
   J.pu->col.alloc(nnz[1]);
   J.pu->val.alloc(nnz[1]);
   J.pp->col.alloc(nnz[2]);
   J.pp->val.alloc(nnz[2]);
   int bps = 0;
-  if (std::getenv("CF_JAC_WARP")) {  // the slot-per-lane form, kept for A/B measurement
-    constexpr int FT = fill_wpb<D>() * 32;
-    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_jac_fill_warp<D>, FT, 0));
-    const int grid = std::max(1, bps) * rt().sm_count;
-    k_jac_fill_warp<D><<<grid, FT, 0, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.uu->col.p,
-                                                   J.uu->val.p, J.pu->ptr.p, J.pu->col.p, J.pu->val.p,
-                                                   J.pp->ptr.p, J.pp->col.p, J.pp->val.p, sl);
-  } else {
-    constexpr int FT = pair_wpb<D>() * 32;
-    const int smem = int(sizeof(PairSmem<D>));
-    CF_CUDA(cudaFuncSetAttribute(k_jac_fill_pair<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_jac_fill_pair<D>, FT, smem));
-    const int grid = std::max(1, bps) * rt().sm_count;
-    k_jac_fill_pair<D><<<grid, FT, smem, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, J.uu->ptr.p, J.uu->col.p,
-                                                   J.uu->val.p, J.pu->ptr.p, J.pu->col.p, J.pu->val.p,
-                                                   J.pp->ptr.p, J.pp->col.p, J.pp->val.p, sl);
-  }
+  constexpr int FT = pair_wpb<D>() * 32;
+  const int smem = int(sizeof(PairSmem<D>));
+  auto kern = with_uu ? k_jac_fill_pair<D, true> : k_jac_fill_pair<D, false>;
+  CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, FT, smem));
+  const int grid = std::max(1, bps) * rt().sm_count;
+  i64* uptr = with_uu ? J.uu->ptr.p : nullptr;
+  int* ucol = with_uu ? J.uu->col.p : nullptr;
+  double* uval = with_uu ? J.uu->val.p : nullptr;
+  kern<<<grid, FT, smem, stream()>>>(g, P.tab.p, cf, qs.p, cs.flag.p, uptr, ucol, uval, J.pu->ptr.p, J.pu->col.p,
+                                     J.pu->val.p, J.pp->ptr.p, J.pp->col.p, J.pp->val.p, sl);
   CF_LAUNCHED();
   // value-only SpMV streams for the blocks whose pattern is the clamped stencil
-  csr_enable_stencil(*J.uu, StencilCols{1, D, g.nn, sl.v_lo, D * sl.ve_lo, 1.0 / double(g.nn)});
+  if (with_uu) csr_enable_stencil(*J.uu, StencilCols{1, D, g.nn, sl.v_lo, D * sl.ve_lo, 1.0 / double(g.nn)});
   csr_enable_stencil(*J.pu, StencilCols{2, D, g.nn, sl.v_lo, D * sl.ve_lo, 1.0 / double(g.nn)});
 }
 
 std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& cs, const cf_material& m,
                                                const cf_regularization& reg, const double* x, const double* pt,
-                                               const Slab* slab) {
+                                               const Slab* slab, std::shared_ptr<Csr> reuse_uu) {
   build_tables(P, mat_mu(m), mat_lambda(m));
   const Coef cf = make_coef(P, m, reg);
   const Slab sl = slab ? *slab : full_slab(P.g);
@@ -1149,10 +958,11 @@ std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& cs
     J->nu_in = P.g.d * sl.ne();
     J->np_in = sl.ne();
   }
+  if (reuse_uu) J->uu = std::move(reuse_uu);  // M_uu depends only on phi_tilde and the Dirichlet set
   if (P.g.d == 2)
-    jacobian_impl<2>(P, cs, cf, x, pt, sl, *J);
+    jacobian_impl<2>(P, cs, cf, x, pt, sl, *J, !J->uu->ptr.p);
   else
-    jacobian_impl<3>(P, cs, cf, x, pt, sl, *J);
+    jacobian_impl<3>(P, cs, cf, x, pt, sl, *J, !J->uu->ptr.p);
   return J;
 }
 

@@ -108,10 +108,13 @@ void distribute(const Constraints& c, double* v_dev, bool homogeneous);
 // x, pt: global-length vectors (valid on the slab's ext range).  R: local layout of the slab.
 void assemble_residual(Problem& P, const Constraints& c, const cf_material& m, const cf_regularization& reg,
                        const double* x, const double* pt, double* R, const Slab* slab = nullptr);
-// rows of the slab's owned vertices; columns in the slab's ext numbering
+// rows of the slab's owned vertices; columns in the slab's ext numbering.  reuse_uu: an M_uu of
+// the same phi_tilde, slab and Dirichlet set (M_uu depends on nothing else, model.cpp:268-276),
+// taken as is instead of being recomputed.
+struct Csr;
 std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& c, const cf_material& m,
                                                const cf_regularization& reg, const double* x, const double* pt,
-                                               const Slab* slab = nullptr);
+                                               const Slab* slab = nullptr, std::shared_ptr<Csr> reuse_uu = nullptr);
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add);  // y = A x (+ add)
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "cf_comm.hpp"
@@ -409,6 +410,9 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   CF_CUDA(cudaMemcpyAsync(full.inhom.p, base->inhom.p, size_t(nt) * sizeof(double), cudaMemcpyDeviceToDevice,
                           stream()));
   DevBuf<double> Bu(nul * (d == 2 ? 3 : 6)), Bp(nv);
+  std::shared_ptr<Csr> uu_step;  // this load step's M_uu
+  std::shared_ptr<Csr> uu_loc;   // its diagonal slab block (distributed preconditioner)
+  const Csr* uu_loc_src = nullptr;
   DevBuf<int> unode(nul), pnode(nv);
   const unsigned gv = grid_for(nv, 256), gl = grid_for(ntl, 256);
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
@@ -471,7 +475,21 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
     std::unique_ptr<BlockSystem> J;
     {
       Timer t(&T.jacobian);
-      J = assemble_jacobian(P, full, mat, reg, x, pt.p, &sl);
+      // M_uu depends only on phi_tilde (fixed for the load step) and the Dirichlet set
+      // (model.cpp:268-276): it is assembled once per step and shared by the later iterations.
+      // CF_VERIFY_UU_REUSE=1 re-assembles it every iteration and checks it bitwise.
+      static const bool verify = std::getenv("CF_VERIFY_UU_REUSE") != nullptr;
+      static const bool no_reuse = std::getenv("CF_NO_UU_REUSE") != nullptr;
+      J = assemble_jacobian(P, full, mat, reg, x, pt.p, &sl, (verify || no_reuse) ? nullptr : uu_step);
+      if (verify && uu_step) {
+        const Csr &a = *J->uu, &b = *uu_step;
+        if (a.nnz != b.nnz || !bitwise_equal(a.ptr.p, b.ptr.p, size_t(a.rows + 1) * sizeof(i64)) ||
+            !bitwise_equal(a.col.p, b.col.p, size_t(a.nnz) * sizeof(int)) ||
+            !bitwise_equal(a.val.p, b.val.p, size_t(a.nnz) * sizeof(double)))
+          fail(CF_ERR_LOGIC, "newton_active_set_step: M_uu changed within a load step");
+        J->uu = uu_step;
+      }
+      if (!uu_step) uu_step = J->uu;
       if (dist) {  // lane split of the undivided matrix, so every row reduces as on one GPU
         long long tot[4] = {J->uu->nnz, J->uu->rows, J->pu->nnz, J->pu->rows};
         cm.sum_i64(tot, 4);
@@ -500,7 +518,11 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         Jl.nu = nul;
         Jl.np = nv;
         const i64 lo = sl.v_lo - sl.ve_lo;
-        Jl.uu = csr_extract_cols(*J->uu, d * lo, d * (lo + nv));
+        if (uu_loc_src != J->uu.get()) {  // the diagonal block of a reused M_uu is reused too
+          uu_loc = csr_extract_cols(*J->uu, d * lo, d * (lo + nv));
+          uu_loc_src = J->uu.get();
+        }
+        Jl.uu = uu_loc;
         Jl.pp = csr_extract_cols(*J->pp, lo, lo + nv);
         prec = build_block_prec(Jl, opts.prec_kind, opts.amg, &ns, prec.get());
       } else {
