@@ -321,7 +321,8 @@ def vcycle_leg(cf, P, mat, reg, x_final, phi_old, stream):
 
 
 def rebuild_probe():
-    """One warm config-3 step with CF_NO_AMG_REUSE=1 (every hierarchy rebuilt every iteration)."""
+    """One warm config-3 step with CF_NO_AMG_REUSE=1 CF_NO_UU_REUSE=1 (M_uu re-assembled and every
+    hierarchy rebuilt every iteration, as the reference does)."""
     import torch
     import paper_1806_09924_b200 as cf
     s = torch.cuda.current_stream()
@@ -340,8 +341,8 @@ def rebuild_probe():
     ms = e0.elapsed_time(e1)
     its = len(rep["iterations"])
     print(json.dumps({"value": P.n_total * its / (ms * 1e-3), "unit": "DoF/s", "ms_per_step": ms,
-                      "newton_iterations": its, "note": "CF_NO_AMG_REUSE=1: u- and phi-hierarchies rebuilt "
-                      "every Newton iteration, as the reference does; identical iterates"}))
+                      "newton_iterations": its, "note": "CF_NO_AMG_REUSE=1 CF_NO_UU_REUSE=1: M_uu re-assembled and u- and "
+                      "phi-hierarchies rebuilt every Newton iteration, as the reference does; identical iterates"}))
 
 
 def ours(args):
@@ -410,7 +411,7 @@ def ours(args):
     full = None
     if rank == 0 and world == 1 and not args.no_rebuild_check:
         try:
-            env = dict(os.environ, CF_NO_AMG_REUSE="1")
+            env = dict(os.environ, CF_NO_AMG_REUSE="1", CF_NO_UU_REUSE="1")
             r = subprocess.run([sys.executable, __file__, "--rebuild-probe"], env=env, capture_output=True,
                                text=True, timeout=600)
             full = json.loads(r.stdout.strip().splitlines()[-1])
