@@ -26,6 +26,9 @@ void vscale(double* x, double a, i64 n);
 void vdiv_dev(const double* x, const double* s_dev, double* y, i64 n);   // y = x / *s
 void vdiag_mul(const double* d, const double* x, double* y, double a, i64 n);  // y = a (d .* x)
 void vdot_dev(const double* x, const double* y, i64 n, double* out, bool do_sqrt);
+// w -= (*h_dev) v; *out = w . y (y = nullptr: w . w), bitwise the separate axpy + vdot_dev
+void vaxpy_dot_dev(const double* h_dev, const double* v, double* w, const double* y, i64 n, double* out,
+                   bool do_sqrt);
 double vdot(const double* x, const double* y, i64 n);
 double vnorm(const double* x, i64 n);
 void multidot(const double* V, i64 ld, int k, const double* w, i64 n, double* out_dev);   // out_i = V_i . w

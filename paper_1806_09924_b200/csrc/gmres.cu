@@ -12,12 +12,6 @@ namespace cfb {
 
 namespace {
 
-// w = w - (*h) * v   (linsolve.cpp:58, compiled without FMA contraction)
-__global__ void k_axpy_dev(i64 n, const double* __restrict__ h, const double* __restrict__ v, double* __restrict__ w) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) w[i] -= (*h) * v[i];
-}
-
 __global__ void k_sqrt1(double* s) { s[0] = sqrt(s[0]); }
 
 // dot over all ranks' rows: the local fixed-order dot, then the rank-ordered sum
@@ -104,12 +98,23 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     for (; j < m && !inner_done; ++j) {
       double* w = V.p + i64(j + 1) * n;
       apply_op(V.p + i64(j) * n, w);
-      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
-        gdot(w, V.p + i64(i) * n, n, hd.p + i, false, comm);
-        k_axpy_dev<<<grid_for(n, 256), 256, 0, stream()>>>(n, hd.p + i, V.p + i64(i) * n, w);
-        CF_LAUNCHED();
+      // modified Gram-Schmidt: h_i = w . v_i, w -= h_i v_i (i = 0..j), then |w|; each axpy is fused
+      // with the following dot (same operations, same reduction order)
+      gdot(w, V.p, n, hd.p, false, comm);
+      for (int i = 0; i <= j; ++i) {
+        const double* next = i < j ? V.p + i64(i + 1) * n : nullptr;
+        const bool last = i == j;
+        if (!comm || !comm->distributed()) {
+          vaxpy_dot_dev(hd.p + i, V.p + i64(i) * n, w, next, n, hd.p + i + 1, last);
+        } else {
+          vaxpy_dot_dev(hd.p + i, V.p + i64(i) * n, w, next, n, hd.p + i + 1, false);
+          comm->sum_ordered(hd.p + i + 1, 1);
+          if (last) {
+            k_sqrt1<<<1, 1, 0, stream()>>>(hd.p + i + 1);
+            CF_LAUNCHED();
+          }
+        }
       }
-      gdot(w, w, n, hd.p + j + 1, true, comm);
       CF_CUDA(cudaMemcpyAsync(hcol.data(), hd.p, size_t(j + 2) * sizeof(double), cudaMemcpyDeviceToHost, stream()));
       CF_CUDA(cudaStreamSynchronize(stream()));
       for (int i = 0; i <= j + 1; ++i) Hij(i, j) = hcol[i];

@@ -31,6 +31,24 @@ __global__ void __launch_bounds__(RB) k_dot_partial(const double* __restrict__ x
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// MGS step fused with the next dot: w -= (*h) v, then the partials of w . y (y = nullptr: w . w) in
+// exactly k_dot_partial's order (same grid, same grid-stride, same block tree)
+__global__ void __launch_bounds__(RB) k_axpy_dot_partial(const double* __restrict__ h, const double* __restrict__ v,
+                                                         double* __restrict__ w, const double* __restrict__ y, i64 n,
+                                                         double* __restrict__ part) {
+  __shared__ double sh[RB];
+  const double hv = *h;
+  double s = 0.0;
+  for (i64 i = i64(blockIdx.x) * RB + threadIdx.x; i < n; i += i64(gridDim.x) * RB) {
+    double wi = w[i];
+    wi -= hv * v[i];
+    w[i] = wi;
+    s += wi * (y ? y[i] : wi);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 // out[r] = sum_b part[r*nb + b] (fixed tree), optional sqrt
 __global__ void __launch_bounds__(RB) k_final(const double* __restrict__ part, int nb, double* out, int do_sqrt) {
   __shared__ double sh[RB];
@@ -169,6 +187,16 @@ void vdot_dev(const double* x, const double* y, i64 n, double* out, bool do_sqrt
   const int nb = nblocks_for(n);
   double* part = partial_buf(nb);
   k_dot_partial<<<nb, RB, 0, stream()>>>(x, y, n, part);
+  CF_LAUNCHED();
+  k_final<<<1, RB, 0, stream()>>>(part, nb, out, do_sqrt ? 1 : 0);
+  CF_LAUNCHED();
+}
+
+void vaxpy_dot_dev(const double* h_dev, const double* v, double* w, const double* y, i64 n, double* out,
+                   bool do_sqrt) {
+  const int nb = nblocks_for(n);
+  double* part = partial_buf(nb);
+  k_axpy_dot_partial<<<nb, RB, 0, stream()>>>(h_dev, v, w, y, n, part);
   CF_LAUNCHED();
   k_final<<<1, RB, 0, stream()>>>(part, nb, out, do_sqrt ? 1 : 0);
   CF_LAUNCHED();
