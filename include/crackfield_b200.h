@@ -112,6 +112,11 @@ int cf_assemble_residual(cf_problem p, cf_constraints c, const cf_material* mat,
 int cf_assemble_jacobian(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
                          const double* solution, const double* phi_tilde, cf_block* out);
 
+/* assemble_pattern (linsolve.hpp:138, linsolve.cpp:417-476): the BlockSparsity after condensation as
+ * a block handle whose values are 0 (constrained dofs keep their diagonal, unlike the Jacobian,
+ * which drops a constrained diagonal that sums to 0). */
+int cf_assemble_pattern(cf_problem p, cf_constraints c, cf_block* out);
+
 /* Slab decomposition (no reference counterpart: the reference is single-threaded).
  * A slab owns vertex planes [p_lo, p_hi) along the slowest axis (z in 3d, y in 2d) = a
  * contiguous vertex range.  Its residual rows come back in the local layout

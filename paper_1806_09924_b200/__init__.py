@@ -285,6 +285,13 @@ def assemble_jacobian(prob: Problem, constraints: ConstraintSet, mat: Material, 
     return BlockSystem(h)
 
 
+def assemble_pattern(prob: Problem, constraints: ConstraintSet) -> BlockSystem:
+    """linsolve.hpp:138 / linsolve.cpp:417-476: the block sparsity after condensation (values 0)."""
+    h = C.c_void_p()
+    check(load().cf_assemble_pattern(prob._h, constraints._h, C.byref(h)))
+    return BlockSystem(h)
+
+
 def slab_info(prob: Problem, rank: int, size: int) -> dict:
     """The slab of rank `rank` of `size` (cf_slab_info): owned / ext vertex ranges, cell range."""
     info = (C.c_int64 * 7)()

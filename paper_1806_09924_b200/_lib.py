@@ -110,6 +110,7 @@ SIGNATURES = [
     ("cf_assemble_jacobian_planes", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, _L, _L,
                                          C.POINTER(_P)]),
     ("cf_slab_info", _I, [_P, _I, _I, _P]),
+    ("cf_assemble_pattern", _I, [_P, _P, C.POINTER(_P)]),
     ("cf_block_shape", _I, [_P, _P]),
     ("cf_block_format", _I, [_P, _I, C.POINTER(_I)]),
     ("cf_block_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),

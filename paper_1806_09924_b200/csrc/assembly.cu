@@ -664,6 +664,70 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
   }
 }
 
+// assemble_pattern (linsolve.cpp:417-476): the sparsity after condensation on a uniform grid.
+// Rows and columns of constrained dofs are dropped (Dirichlet / active lines have no masters),
+// every constrained dof keeps its diagonal; free dofs couple with the free dofs of the 3^d
+// vertices sharing a cell.  fill = false counts, fill = true writes ascending columns.
+template <int D>
+__global__ void k_pattern(GridDesc g, const std::uint8_t* __restrict__ flag, i64* __restrict__ ptr_uu,
+                          int* __restrict__ col_uu, i64* __restrict__ ptr_pu, int* __restrict__ col_pu,
+                          i64* __restrict__ ptr_pp, int* __restrict__ col_pp, bool fill) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= g.V) return;
+  i64 x, y, z;
+  vxyz<D>(g, v, x, y, z);
+  const i64 nu = g.n_u();
+  const bool pfree = flag[nu + v] == 0;
+  i64 pos_u[D], pos_pu = fill ? ptr_pu[v] : 0, pos_pp = fill ? ptr_pp[v] : 0;
+  bool ufree[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    ufree[a] = flag[v * D + a] == 0;
+    pos_u[a] = fill ? ptr_uu[v * D + a] : 0;
+  }
+  const int zl = (D == 3) ? -1 : 0, zh = (D == 3) ? 1 : 0;
+  for (int dz = zl; dz <= zh; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const i64 X = x + dx, Y = y + dy, Z = z + dz;
+        if (X < 0 || Y < 0 || Z < 0 || X >= g.nn || Y >= g.nn || Z >= ((D == 3) ? g.nn : 1)) continue;
+        const i64 w = X + g.nn * (Y + g.nn * Z);
+        for (int b = 0; b < D; ++b) {
+          if (flag[w * D + b]) continue;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+            if (ufree[a]) {
+              if (fill) col_uu[pos_u[a]] = int(w * D + b);
+              ++pos_u[a];
+            }
+          if (pfree) {
+            if (fill) col_pu[pos_pu] = int(w * D + b);
+            ++pos_pu;
+          }
+        }
+        if (pfree && !flag[nu + w]) {
+          if (fill) col_pp[pos_pp] = int(w);
+          ++pos_pp;
+        }
+      }
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    if (!ufree[a]) {  // constrained: its diagonal only
+      if (fill) col_uu[pos_u[a]] = int(v * D + a);
+      ++pos_u[a];
+    }
+  if (!pfree) {
+    if (fill) col_pp[pos_pp] = int(v);
+    ++pos_pp;
+  }
+  if (!fill) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) ptr_uu[v * D + a] = pos_u[a];
+    ptr_pu[v] = pos_pu;
+    ptr_pp[v] = pos_pp;
+  }
+}
+
 __global__ void k_build_flags(GridDesc g, int clamp, std::uint8_t* flag) {
   const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (v >= g.V) return;
@@ -963,6 +1027,48 @@ std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& cs
     jacobian_impl<2>(P, cs, cf, x, pt, sl, *J, !J->uu->ptr.p);
   else
     jacobian_impl<3>(P, cs, cf, x, pt, sl, *J, !J->uu->ptr.p);
+  return J;
+}
+
+template <int D>
+static void pattern_impl(const Problem& P, const Constraints& cs, BlockSystem& J) {
+  const GridDesc& g = P.g;
+  const i64 nu = g.n_u(), np = g.V;
+  Csr* B[3] = {J.uu.get(), J.pu.get(), J.pp.get()};
+  const i64 rows[3] = {nu, np, np}, cols[3] = {nu, nu, np};
+  for (int b = 0; b < 3; ++b) {
+    B[b]->rows = rows[b];
+    B[b]->cols = cols[b];
+    B[b]->ptr.alloc(rows[b] + 1);
+    CF_CUDA(cudaMemsetAsync(B[b]->ptr.p + rows[b], 0, sizeof(i64), stream()));
+  }
+  k_pattern<D><<<grid_for(g.V, 128), 128, 0, stream()>>>(g, cs.flag.p, J.uu->ptr.p, nullptr, J.pu->ptr.p, nullptr,
+                                                          J.pp->ptr.p, nullptr, false);
+  CF_LAUNCHED();
+  for (int b = 0; b < 3; ++b) {
+    exclusive_scan_inplace(B[b]->ptr.p, rows[b]);
+    CF_CUDA(cudaMemcpyAsync(&B[b]->nnz, B[b]->ptr.p + rows[b], sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  }
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  for (int b = 0; b < 3; ++b) {
+    B[b]->col.alloc(B[b]->nnz);
+    B[b]->val.alloc(B[b]->nnz);
+    B[b]->val.zero();  // a pattern: explicit zeros
+  }
+  k_pattern<D><<<grid_for(g.V, 128), 128, 0, stream()>>>(g, cs.flag.p, J.uu->ptr.p, J.uu->col.p, J.pu->ptr.p,
+                                                          J.pu->col.p, J.pp->ptr.p, J.pp->col.p, true);
+  CF_LAUNCHED();
+}
+
+std::unique_ptr<BlockSystem> assemble_pattern(const Problem& P, const Constraints& cs) {
+  auto J = std::make_unique<BlockSystem>();
+  J->d = P.g.d;
+  J->nu = P.g.n_u();
+  J->np = P.g.V;
+  if (P.g.d == 2)
+    pattern_impl<2>(P, cs, *J);
+  else
+    pattern_impl<3>(P, cs, *J);
   return J;
 }
 

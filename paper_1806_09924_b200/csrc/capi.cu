@@ -311,6 +311,15 @@ int cf_assemble_jacobian_planes(cf_problem p, cf_constraints c, const cf_materia
   });
 }
 
+int cf_assemble_pattern(cf_problem p, cf_constraints c, cf_block* outb) {
+  return guard([&] {
+    CHECK_ARG(p && c && outb, "cf_assemble_pattern: null argument");
+    auto J = assemble_pattern(*p->p, *c->c);
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *outb = new cf_block_s{std::move(J)};
+  });
+}
+
 int cf_block_format(cf_block b, int which, int* format) {
   return guard([&] {
     CHECK_ARG(b && format && which >= 0 && which <= 2, "cf_block_format: bad argument");

@@ -115,6 +115,8 @@ struct Csr;
 std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& c, const cf_material& m,
                                                const cf_regularization& reg, const double* x, const double* pt,
                                                const Slab* slab = nullptr, std::shared_ptr<Csr> reuse_uu = nullptr);
+// assemble_pattern (linsolve.cpp:417-476): BlockSparsity as CSR blocks with zero values
+std::unique_ptr<BlockSystem> assemble_pattern(const Problem& P, const Constraints& c);
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add);  // y = A x (+ add)
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);

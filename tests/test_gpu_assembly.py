@@ -197,3 +197,63 @@ def test_config1_operator_properties(cf):
     interior = (xi > 1) & (xi < n - 2) & (yi > 1) & (yi < n - 2) & (zi > 1) & (zi < n - 2)
     rows = Mt.view(-1, 3)[interior]
     assert rows.abs().max().item() <= 1e-12 * Mu.abs().max().item() + 1e-14
+
+
+@pytest.mark.parametrize("d,n0,r,frac", [(2, 2, 1, 0.0), (2, 3, 1, 0.2), (3, 2, 1, 0.15)])
+def test_assemble_pattern_covers_support_overlaps(cf, d, n0, r, frac):
+    """linsolve_test.cpp:147-190: dofs couple when their vertices share a cell, routed through the
+    constraint masters (Dirichlet / active lines have none); constrained dofs keep their diagonal."""
+    P = cf.Problem(d, 1.0, n0, r)
+    rng = np.random.default_rng(5 + d)
+    nact = int(frac * P.n_vertices)
+    act = {int(P.n_u + v): 0.5 for v in rng.choice(P.n_vertices, nact, replace=False)}
+    cs = cf.build_constraints(P, True, act)
+    pat = cf.assemble_pattern(P, cs)
+    nn = P.nodes_per_side
+    nc = nn - 1
+    xyz = lambda v: (v % nn, (v // nn) % nn, v // (nn * nn) if d == 3 else 0)
+    bnd = lambda v: any(c in (0, nc) for c in xyz(v)[:d])
+    cons = set(act)
+    for v in range(P.n_vertices):
+        if bnd(v):
+            cons.update(v * d + a for a in range(d))
+    uu, pu, pp = set(), set(), set()
+    for cz in range(nc if d == 3 else 1):
+        for cy in range(nc):
+            for cx in range(nc):
+                verts = [(cx + (k & 1)) + nn * ((cy + ((k >> 1) & 1)) + nn * (cz + ((k >> 2) & 1)))
+                         for k in range(1 << d)]
+                for a in verts:
+                    for b in verts:
+                        for ca in range(d):
+                            for cb in range(d):
+                                i, j = a * d + ca, b * d + cb
+                                if i not in cons and j not in cons:
+                                    uu.add((i, j))
+                        for cb in range(d):
+                            i, j = P.n_u + a, b * d + cb
+                            if i not in cons and j not in cons:
+                                pu.add((a, j))
+                        if P.n_u + a not in cons and P.n_u + b not in cons:
+                            pp.add((a, b))
+    for dof in cons:
+        if dof < P.n_u:
+            uu.add((dof, dof))
+        else:
+            pp.add((dof - P.n_u, dof - P.n_u))
+    for w, ref in enumerate((uu, pu, pp)):
+        A = pat.csr(w)
+        got = {(i, int(A.col[k])) for i in range(A.rows) for k in range(A.ptr[i], A.ptr[i + 1])}
+        assert got == ref, f"block {w}"
+        for i in range(A.rows):  # ascending columns
+            assert np.all(np.diff(A.col[A.ptr[i]:A.ptr[i + 1]]) > 0)
+        assert not A.val.any()
+    # the Jacobian's pattern is the same except constrained diagonals that sum to exactly zero
+    x = np.zeros(P.n_total)
+    x[P.n_u:] = rng.uniform(0, 1, P.n_vertices)
+    J = cf.assemble_jacobian(P, cs, cf.Material(), cf.Regularization(0.3, 1e-6), x, rng.uniform(0, 1, P.n_vertices))
+    for w in range(3):
+        A, B = J.csr(w), pat.csr(w)
+        ja = {(i, int(A.col[k])) for i in range(A.rows) for k in range(A.ptr[i], A.ptr[i + 1])}
+        jb = {(i, int(B.col[k])) for i in range(B.rows) for k in range(B.ptr[i], B.ptr[i + 1])}
+        assert ja <= jb and all(i == j for i, j in jb - ja)
