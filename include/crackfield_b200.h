@@ -112,6 +112,15 @@ int cf_assemble_residual(cf_problem p, cf_constraints c, const cf_material* mat,
 int cf_assemble_jacobian(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
                          const double* solution, const double* phi_tilde, cf_block* out);
 
+/* Host helpers of the model (no device needed): sigma (model.cpp:19-26; grad_u and out row-major
+ * 3x3), q1_shape (fem.cpp:76-96; values[2^d], grads[2^d x d] row-major), detect_cycles
+ * (solver.cpp:10-22; the histories of n dofs as one byte array with offsets[n+1]; out receives the
+ * cycling dofs ascending, *n_out their count). */
+int cf_sigma(const double grad_u[9], const cf_material* mat, int d, double out[9]);
+int cf_q1_shape(int d, const double xi[3], double* values, double* grads);
+int cf_detect_cycles(int n, const int32_t* dofs, const int64_t* offsets, const uint8_t* bits, int window,
+                     int toggles, int32_t* out, int* n_out);
+
 /* assemble_pattern (linsolve.hpp:138, linsolve.cpp:417-476): the BlockSparsity after condensation as
  * a block handle whose values are 0 (constrained dofs keep their diagonal, unlike the Jacobian,
  * which drops a constrained diagonal that sums to 0). */
@@ -234,6 +243,9 @@ int cf_state_create(cf_problem p, const double* solution, const double* phi_old,
                     cf_state* out);
 int cf_state_get(cf_state s, double* solution, double* phi_old, double* phi_prev2, int* step);
 int cf_state_destroy(cf_state s);
+/* extrapolate_phi (model.cpp:60-64): phi_tilde of the state (phi_old for step <= 2, else
+ * clip(2 phi_old - phi_prev2, [0, 1])); phi_tilde host or device, n_phi entries. */
+int cf_extrapolate_phi(cf_state s, double* phi_tilde);
 /* newton_active_set_step (solver.cpp:49-188).  its receives up to max_its iterations. */
 int cf_newton_active_set_step(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
                               const cf_solver_options* opts, cf_newton_iteration* its, int max_its, int* n_its,

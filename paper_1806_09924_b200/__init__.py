@@ -285,6 +285,45 @@ def assemble_jacobian(prob: Problem, constraints: ConstraintSet, mat: Material, 
     return BlockSystem(h)
 
 
+def sigma(grad_u, mat: Material, d: int) -> np.ndarray:
+    """model.cpp:19-26: sigma = 2 mu e + lambda tr(e) I, e = sym(grad u) (3x3, first d x d used)."""
+    g = np.ascontiguousarray(np.asarray(grad_u, dtype=np.float64).reshape(3, 3))
+    out = np.zeros((3, 3))
+    check(load().cf_sigma(_ptr(g), C.byref(mat), int(d), _ptr(out)))
+    return out
+
+
+def q1_shape(d: int, xi):
+    """fem.cpp:76-96: Q1 values (2^d) and gradients (2^d x d) at reference point xi."""
+    x = np.zeros(3)
+    x[:len(xi)] = xi
+    vals, grads = np.zeros(1 << d), np.zeros((1 << d, d))
+    check(load().cf_q1_shape(int(d), _ptr(x), _ptr(vals), _ptr(grads)))
+    return vals, grads
+
+
+def detect_cycles(history: dict, window: int = 8, toggles: int = 3) -> set:
+    """solver.cpp:10-22: dofs whose membership history toggles >= `toggles` times within the last
+    `window` entries."""
+    dofs = np.fromiter(history.keys(), dtype=np.int32, count=len(history))
+    lens = np.array([len(history[int(k)]) for k in dofs], dtype=np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    bits = np.concatenate([np.asarray(history[int(k)], dtype=np.uint8) for k in dofs]) if len(dofs) else \
+        np.zeros(1, dtype=np.uint8)
+    out = np.zeros(max(1, len(dofs)), dtype=np.int32)
+    n = C.c_int()
+    check(load().cf_detect_cycles(len(dofs), _ptr(dofs), _ptr(offs), _ptr(bits), int(window), int(toggles),
+                                  _ptr(out), C.byref(n)))
+    return set(int(v) for v in out[:n.value])
+
+
+def extrapolate_phi(state) -> np.ndarray:
+    """model.cpp:60-64: phi_tilde of a FractureState (host copy)."""
+    out = np.zeros(state.prob.n_phi)
+    check(load().cf_extrapolate_phi(state._h, _ptr(out)))
+    return out
+
+
 def assemble_pattern(prob: Problem, constraints: ConstraintSet) -> BlockSystem:
     """linsolve.hpp:138 / linsolve.cpp:417-476: the block sparsity after condensation (values 0)."""
     h = C.c_void_p()

@@ -111,6 +111,10 @@ SIGNATURES = [
                                          C.POINTER(_P)]),
     ("cf_slab_info", _I, [_P, _I, _I, _P]),
     ("cf_assemble_pattern", _I, [_P, _P, C.POINTER(_P)]),
+    ("cf_sigma", _I, [_P, C.POINTER(Material), _I, _P]),
+    ("cf_q1_shape", _I, [_I, _P, _P, _P]),
+    ("cf_detect_cycles", _I, [_I, _P, _P, _P, _I, _I, _P, C.POINTER(_I)]),
+    ("cf_extrapolate_phi", _I, [_P, _P]),
     ("cf_block_shape", _I, [_P, _P]),
     ("cf_block_format", _I, [_P, _I, C.POINTER(_I)]),
     ("cf_block_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),

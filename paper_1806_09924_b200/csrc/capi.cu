@@ -311,6 +311,61 @@ int cf_assemble_jacobian_planes(cf_problem p, cf_constraints c, const cf_materia
   });
 }
 
+int cf_sigma(const double grad_u[9], const cf_material* mat, int d, double out[9]) {
+  return guard([&] {
+    CHECK_ARG(grad_u && mat && out && (d == 2 || d == 3), "cf_sigma: bad argument");
+    double e[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) e[a][b] = 0.5 * (grad_u[3 * a + b] + grad_u[3 * b + a]);
+    double tr = 0.0;
+    for (int a = 0; a < d; ++a) tr += e[a][a];
+    const double two_mu = 2.0 * mat_mu(*mat);
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) out[3 * a + b] = two_mu * e[a][b];
+    for (int a = 0; a < d; ++a) out[3 * a + a] += mat_lambda(*mat) * tr;
+  });
+}
+
+int cf_q1_shape(int d, const double xi[3], double* values, double* grads) {
+  return guard([&] {
+    CHECK_ARG(xi && values && grads && (d == 2 || d == 3), "cf_q1_shape: bad argument");
+    const int n = 1 << d;
+    for (int k = 0; k < n; ++k) {
+      double v = 1.0;
+      for (int a = 0; a < d; ++a) v *= (k & (1 << a)) ? xi[a] : 1.0 - xi[a];
+      values[k] = v;
+      for (int a = 0; a < d; ++a) {
+        double g = (k & (1 << a)) ? 1.0 : -1.0;
+        for (int b = 0; b < d; ++b) {
+          if (b == a) continue;
+          g *= (k & (1 << b)) ? xi[b] : 1.0 - xi[b];
+        }
+        grads[k * d + a] = g;
+      }
+    }
+  });
+}
+
+int cf_detect_cycles(int n, const int32_t* dofs, const int64_t* offsets, const uint8_t* bits, int window,
+                     int toggles, int32_t* out, int* n_out) {
+  return guard([&] {
+    CHECK_ARG(n >= 0 && n_out && (n == 0 || (dofs && offsets && bits && out)), "cf_detect_cycles: bad argument");
+    std::vector<int32_t> found;
+    for (int t = 0; t < n; ++t) {
+      const i64 lo = offsets[t], len = offsets[t + 1] - offsets[t];
+      const i64 start = std::max<i64>(0, len - window);
+      int changes = 0;
+      for (i64 i = start + 1; i < len; ++i)
+        if (bits[lo + i] != bits[lo + i - 1]) ++changes;
+      if (changes >= toggles) found.push_back(dofs[t]);
+    }
+    std::sort(found.begin(), found.end());
+    found.erase(std::unique(found.begin(), found.end()), found.end());
+    std::copy(found.begin(), found.end(), out);
+    *n_out = int(found.size());
+  });
+}
+
 int cf_assemble_pattern(cf_problem p, cf_constraints c, cf_block* outb) {
   return guard([&] {
     CHECK_ARG(p && c && outb, "cf_assemble_pattern: null argument");
@@ -757,6 +812,16 @@ int cf_state_get(cf_state s, double* solution, double* phi_old, double* phi_prev
     get(phi_prev2, s->st.phi_prev2);
     if (step) *step = s->st.step;
     CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int cf_extrapolate_phi(cf_state s, double* phi_tilde) {
+  return guard([&] {
+    CHECK_ARG(s && phi_tilde, "cf_extrapolate_phi: null argument");
+    const i64 V = s->prob->p->g.V;
+    OutArg<double> out(phi_tilde, V);
+    extrapolate_phi(s->st, out.dev, V);
+    out.finish();
   });
 }
 

@@ -158,6 +158,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
                                     const cf_solver_options& opts, const Comm* comm = nullptr,
                                     const Slab* slab = nullptr);
 Slab rank_slab(const GridDesc& g, int rank, int size);  // planes split evenly over the ranks
+void extrapolate_phi(const State& st, double* pt, i64 V);  // model.cpp:60-64
 // n_u x m column-major rigid-body modes (rows of the slab's owned u dofs when slab is given)
 void rigid_body_modes(const Problem& P, const Constraints& c, double* B, const Slab* slab = nullptr);
 // host helpers (model.cpp:28-64, 324-349)

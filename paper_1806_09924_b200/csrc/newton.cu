@@ -237,6 +237,11 @@ void rigid_body_modes(const Problem& P, const Constraints& c, double* B, const S
   CF_LAUNCHED();
 }
 
+void extrapolate_phi(const State& st, double* pt, i64 V) {
+  k_extrapolate<<<grid_for(V, 256), 256, 0, stream()>>>(V, st.step, st.phi_old.p, st.phi_prev2.p, pt);
+  CF_LAUNCHED();
+}
+
 Slab rank_slab(const GridDesc& g, int rank, int size) {
   if (size < 1 || rank < 0 || rank >= size) fail(CF_ERR_INVALID_ARGUMENT, "rank_slab: bad rank / size");
   if (g.nn < size) fail(CF_ERR_UNSUPPORTED, "rank_slab: fewer vertex planes than ranks");
@@ -387,8 +392,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   double* x = st.solution.p;
   distribute(*base, x, false);
   DevBuf<double> pt(V);
-  k_extrapolate<<<grid_for(V, 256), 256, 0, stream()>>>(V, st.step, st.phi_old.p, st.phi_prev2.p, pt.p);
-  CF_LAUNCHED();
+  extrapolate_phi(st, pt.p, V);
   const double c = opts.active_set_c_scale * mat.G_c / reg.eps;
   DevBuf<std::uint8_t> fixed(nv), active(nv), prev(nv), tracked(nv);
   DevBuf<unsigned long long> hist(nv);

@@ -257,3 +257,15 @@ def test_assemble_pattern_covers_support_overlaps(cf, d, n0, r, frac):
         ja = {(i, int(A.col[k])) for i in range(A.rows) for k in range(A.ptr[i], A.ptr[i + 1])}
         jb = {(i, int(B.col[k])) for i in range(B.rows) for k in range(B.ptr[i], B.ptr[i + 1])}
         assert ja <= jb and all(i == j for i, j in jb - ja)
+
+
+def test_extrapolate_phi(cf):
+    """model.cpp:60-64: phi_old for step <= 2, else clip(2 phi_old - phi_prev2, [0, 1])."""
+    P = cf.Problem(2, 1.0, 4, 1)
+    rng = np.random.default_rng(8)
+    po, pp = rng.uniform(-0.2, 1.2, P.n_vertices), rng.uniform(-0.2, 1.2, P.n_vertices)
+    for step in (0, 2, 3, 7):
+        st = cf.FractureState(P, np.zeros(P.n_total), po, pp, step)
+        got = cf.extrapolate_phi(st)
+        ref = po if step <= 2 else np.minimum(np.maximum(2.0 * po - pp, 0.0), 1.0)
+        assert np.array_equal(got, ref)
