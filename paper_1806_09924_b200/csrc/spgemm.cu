@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(WPB * 32) k_num(const int* __restrict__ rowlis
   const double si = rs ? rs[i] : 1.0;
   const int g = lane / L, lig = lane % L;
   const i64 a0 = ap[i], a1 = ap[i + 1];
+  static_assert(CMAX <= 16, "k_num: product buffer");
   for (i64 kb0 = a0; kb0 < a1; kb0 += G) {
     const i64 ka = kb0 + g;
     int slot[CMAX];
@@ -317,10 +318,31 @@ __global__ void __launch_bounds__(WPB * 32) k_num(const int* __restrict__ rowlis
     if (ka < a1) {
       const int k = ac[ka];
       const double a = rs ? si * av[ka] : av[ka];
-      for (i64 q = bp[k] + lig; q < bp[k + 1] && np < CMAX; q += L) {
-        slot[np] = hfind(T, mask, bc[q]);
-        val[np] = a * bv[q];
-        ++np;
+      if constexpr (L >= 16) {  // measured: a loss for the 4- and 8-lane groups
+        // issue all of the lane's B loads first (in flight together), then the hash lookups
+        const i64 q0 = bp[k] + lig, q1 = bp[k + 1];
+        const i64 nq = q1 > q0 ? (q1 - q0 + L - 1) / L : 0;
+        np = int(nq < CMAX ? nq : CMAX);
+        int cb[CMAX];
+        double vb[CMAX];
+#pragma unroll
+        for (int t = 0; t < CMAX; ++t)
+          if (t < np) {
+            cb[t] = bc[q0 + i64(t) * L];
+            vb[t] = bv[q0 + i64(t) * L];
+          }
+#pragma unroll
+        for (int t = 0; t < CMAX; ++t)
+          if (t < np) {
+            slot[t] = hfind(T, mask, cb[t]);
+            val[t] = a * vb[t];
+          }
+      } else {
+        for (i64 q = bp[k] + lig; q < bp[k + 1] && np < CMAX; q += L) {
+          slot[np] = hfind(T, mask, bc[q]);
+          val[np] = a * bv[q];
+          ++np;
+        }
       }
     }
 #pragma unroll

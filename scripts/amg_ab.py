@@ -45,5 +45,5 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     torch.cuda.synchronize()
 rows = sorted(((getattr(e, "device_time_total", 0) or 0) / 1e3, e.count, e.key) for e in prof.key_averages())[::-1]
 print(f"  kernel total {sum(r[0] for r in rows):.1f} ms")
-for t, c, k in rows[:14]:
+for t, c, k in rows[:22]:
     print(f"  {t:8.2f} ms {c:5d} {k[:90]}")
