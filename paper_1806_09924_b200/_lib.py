@@ -201,7 +201,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("CF_LIB_PATH") or LIB_PATH  # CF_LIB_PATH: A/B builds of the same ABI
     if not os.path.exists(path):
         raise ImportError(f"crackfield_b200: {path} is missing; run __graft_entry__.build() "
                           "(there is no CPU fallback)")

@@ -47,3 +47,5 @@ rows = sorted(((getattr(e, "device_time_total", 0) or 0) / 1e3, e.count, e.key) 
 print(f"  kernel total {sum(r[0] for r in rows):.1f} ms")
 for t, c, k in rows[:22]:
     print(f"  {t:8.2f} ms {c:5d} {k[:90]}")
+for lev in range(h.n_levels() - 1):
+    print("level", lev, h.level_info(lev))
