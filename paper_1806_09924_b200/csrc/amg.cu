@@ -1377,8 +1377,35 @@ void BlockPrec::apply(const double* r, double* z) const {  // linsolve.cpp:398-4
     lu_u->solve(r, z);
     lu_p->solve(r + nu, z + nu);
   } else if (kind == 1) {
+    // the two V-cycles are independent (separate hierarchies, work vectors and output ranges): the
+    // phi cycle runs on the auxiliary stream while the u cycle runs on the library stream, so
+    // the small coarse-level kernels of one overlap the other
+    static const bool serial = std::getenv("CF_SERIAL_VCYCLES") != nullptr;
+    Runtime& R = rt();
+    if (serial || np == 0) {
+      amg_u->vcycle(r, z);
+      amg_p->vcycle(r + nu, z + nu);
+      return;
+    }
+    if (!R.aux) {
+      CF_CUDA(cudaStreamCreateWithFlags(&R.aux, cudaStreamNonBlocking));
+      CF_CUDA(cudaEventCreateWithFlags(&R.ev_fork, cudaEventDisableTiming));
+      CF_CUDA(cudaEventCreateWithFlags(&R.ev_join, cudaEventDisableTiming));
+    }
+    const cudaStream_t main = R.stream;
+    CF_CUDA(cudaEventRecord(R.ev_fork, main));
+    CF_CUDA(cudaStreamWaitEvent(R.aux, R.ev_fork, 0));
+    R.stream = R.aux;
+    try {
+      amg_p->vcycle(r + nu, z + nu);
+    } catch (...) {
+      R.stream = main;
+      throw;
+    }
+    R.stream = main;
+    CF_CUDA(cudaEventRecord(R.ev_join, R.aux));
     amg_u->vcycle(r, z);
-    amg_p->vcycle(r + nu, z + nu);
+    CF_CUDA(cudaStreamWaitEvent(main, R.ev_join, 0));
   } else {
     vdiag_mul(inv_u.p, r, z, 1.0, nu);
     vdiag_mul(inv_p.p, r + nu, z + nu, 1.0, np);

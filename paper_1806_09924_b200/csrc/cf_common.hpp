@@ -41,6 +41,9 @@ struct Runtime {
   int sm_count = 0;
   i64 launches = 0;
   bool ready = false;
+  // a second stream for independent work forked from and joined back into `stream` by events
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 Runtime& rt();
 void ensure_device();  // throws CF_ERR_CUDA when no device is usable (no CPU fallback)

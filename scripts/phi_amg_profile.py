@@ -12,7 +12,8 @@ from torch.profiler import ProfilerActivity, profile
 import bench
 import paper_1806_09924_b200 as cf
 
-P, mat, reg = bench.sneddon_setup(cf, bench.CFG3)
+CFG = {"cfg3": bench.CFG3, "cfg2": dict(dim=2, half_width=10.0, n0=8, refinements=8)}[sys.argv[1] if len(sys.argv) > 1 else "cfg3"]
+P, mat, reg = bench.sneddon_setup(cf, CFG)
 st = cf.make_initial_state(P, mat)
 s0 = st.get()
 cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions())
@@ -37,7 +38,7 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     torch.cuda.synchronize()
 rows = sorted(((getattr(e, "device_time_total", 0) or 0) / 1e3, e.count, e.key) for e in prof.key_averages())[::-1]
 print(f"kernel total {sum(r[0] for r in rows):.1f} ms over {sum(r[1] for r in rows)} launches")
-for t, c, k in sorted(rows, key=lambda r: -r[1])[:30]:
+for t, c, k in rows[:25]:
     print(f"  {t:8.2f} ms {c:5d} {k[:90]}")
 for lev in range(h.n_levels() - 1):
     print(lev, h.level_info(lev))
