@@ -2,6 +2,12 @@
 // proj/src/linsolve.cpp:13-19).  HBM-bound: the matrix is streamed once with L1-bypassing
 // non-coherent loads, x is read through the read-only cache, a group of TPR lanes owns one
 // row (TPR picked from the mean row length) and reduces with warp shuffles.
+//
+// Kernels: k_spmv_b (CSR: AMG levels, P, R, M_phiphi); k_spmv_st* (stencil-implicit columns of
+// M_uu / M_phiu, values only); k_spmv_st16p / k_spmv_phi_st16p (the 3d production path of those:
+// persistent 8-thread row groups carrying the 16 logical lanes, interior fast path);
+// k_spmv_st_emu (general emulated form: tuning sweeps, CF_ST_EMU=1).  Every variant produces
+// bitwise the TPR-lane reduction of the contract.
 #include <cstdlib>
 
 #include "cf_types.hpp"
