@@ -31,16 +31,20 @@ SEED_PHI = 180609924001
 SEED_U = 180609924002
 
 CFG3 = dict(dim=3, half_width=10.0, n0=8, refinements=4)  # 128^3 cells
+CFG4 = dict(dim=3, half_width=10.0, n0=8, refinements=5)  # 256^3 cells, 67,898,372 dofs (needs >= 4 GPUs)
 CFG1 = dict(dim=3, half_width=10.0, n0=12, refinements=4)  # 192^3 cells
 CPU_SAMPLE = dict(dim=3, half_width=10.0, n0=8, refinements=2)  # 32^3 cells, 1/64 of config 3
 
 METRIC = "Newton-step DoF/s (config 3: 3d penny crack, 128^3 Q1, 8,586,756 dofs)"
+METRIC4 = "Newton-step DoF/s (config 4: 3d penny crack, 256^3 Q1, 67,898,372 dofs)"
 CONFIG = {"workload": "config3: 3d Sneddon penny crack, uniform 128^3 Q1 hexes, 8,586,756 dofs (u, phi), FP64; "
                       "E=1, nu=0.2, G_c=1, p=1e-3, eps=2h, kappa=1e-12, 1 load step, Newton tol 1e-8, "
                       "GMRES(100) rtol 1e-8 with block AMG",
           "step": "one newton_active_set_step from the seeded state (all Newton iterations)",
           "l2": "working set (J 8.6 GB, AMG hierarchy, Krylov basis) >> 126 MB L2; no flush needed",
           "parallelism": "single GPU"}
+CONFIG4 = dict(CONFIG, workload="config4: 3d Sneddon penny crack, uniform 256^3 Q1 hexes, 67,898,372 dofs (u, phi), "
+                                "FP64; otherwise as config 3 (strong-scaling configuration, >= 4 GPUs)")
 
 
 def splitmix_uniform(seed: int, n: int, start: int = 0) -> np.ndarray:
@@ -353,7 +357,7 @@ def ours(args):
     device = f"cuda:{local}"
     s = torch.cuda.current_stream()
     cf.set_stream(s)
-    P, mat, reg = sneddon_setup(cf, CFG3)
+    P, mat, reg = sneddon_setup(cf, CFG4 if args.workload == "cfg4" else CFG3)
     opts = cf.SolverOptions()
     st0 = cf.make_initial_state(P, mat).get()
     sol0 = torch.from_numpy(st0["solution"]).to(device)
@@ -428,10 +432,11 @@ def ours(args):
         return
     op, roof = operator_leg(cf, device, s) if not args.no_operator else (None, None)
     out = {
-        "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC if args.workload == "cfg3" else METRIC4, "value": value, "unit": "DoF/s", "n_gpus": world,
+        "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Sneddon state)",
-        "config": dict(CONFIG, parallelism="single GPU" if world == 1 else
+        "config": dict(CONFIG if args.workload == "cfg3" else CONFIG4, parallelism="single GPU" if world == 1 else
                        f"{world} GPUs: z-slab decomposition, NCCL halo planes, block-Jacobi AMG over slabs"),
         "newton_iterations_per_step": its, "ms_per_newton_iteration": ms / its,
         "gmres_iterations": [r["gmres_iterations"] for r in last["iterations"]],
@@ -452,6 +457,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg3", "cfg4"],
+                    help="cfg4 (256^3, the strong-scaling config) needs >= 4 GPUs of memory")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-operator", action="store_true")
     ap.add_argument("--no-rebuild-check", action="store_true")
