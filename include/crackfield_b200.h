@@ -112,6 +112,14 @@ int cf_assemble_residual(cf_problem p, cf_constraints c, const cf_material* mat,
 int cf_assemble_jacobian(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
                          const double* solution, const double* phi_tilde, cf_block* out);
 
+/* Matrix-free M_uu apply (BASELINE config 1's "matrix-free equivalent"): y_u = M_uu x_u computed
+ * cell by cell from phi_tilde, without the assembled matrix (the assembled block's Dirichlet
+ * condensation included).  Equal to cf_block_spmv(M_uu) to rounding (not bitwise).  x, y: n_u. */
+int cf_mf_apply_uu(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                   const double* phi_tilde, const double* x, double* y);
+/* FP64 FMA throughput of the device (TFLOP/s, a DFMA loop), the roofline of the matrix-free apply. */
+int cf_fp64_peak(double* tflops);
+
 /* Host helpers of the model (no device needed): sigma (model.cpp:19-26; grad_u and out row-major
  * 3x3), q1_shape (fem.cpp:76-96; values[2^d], grads[2^d x d] row-major), detect_cycles
  * (solver.cpp:10-22; the histories of n dofs as one byte array with offsets[n+1]; out receives the

@@ -285,6 +285,23 @@ def assemble_jacobian(prob: Problem, constraints: ConstraintSet, mat: Material, 
     return BlockSystem(h)
 
 
+def mf_apply_uu(prob: Problem, constraints: ConstraintSet, mat: Material, reg: Regularization, phi_tilde, x,
+                out=None):
+    """Matrix-free y_u = M_uu x_u (BASELINE config 1's matrix-free operator; equal to the assembled
+    apply to rounding)."""
+    xx, pt = _as_f64(x), _as_f64(phi_tilde)
+    y = out if out is not None else _empty_like_kind(xx, prob.n_u)
+    check(load().cf_mf_apply_uu(prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(pt), _ptr(xx), _ptr(y)))
+    return y
+
+
+def fp64_peak_tflops() -> float:
+    """FP64 FMA throughput of the device (DFMA loop), TFLOP/s."""
+    v = C.c_double()
+    check(load().cf_fp64_peak(C.byref(v)))
+    return v.value
+
+
 def sigma(grad_u, mat: Material, d: int) -> np.ndarray:
     """model.cpp:19-26: sigma = 2 mu e + lambda tr(e) I, e = sym(grad u) (3x3, first d x d used)."""
     g = np.ascontiguousarray(np.asarray(grad_u, dtype=np.float64).reshape(3, 3))

@@ -111,6 +111,8 @@ SIGNATURES = [
                                          C.POINTER(_P)]),
     ("cf_slab_info", _I, [_P, _I, _I, _P]),
     ("cf_assemble_pattern", _I, [_P, _P, C.POINTER(_P)]),
+    ("cf_mf_apply_uu", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, _P]),
+    ("cf_fp64_peak", _I, [C.POINTER(_D)]),
     ("cf_sigma", _I, [_P, C.POINTER(Material), _I, _P]),
     ("cf_q1_shape", _I, [_I, _P, _P, _P]),
     ("cf_detect_cycles", _I, [_I, _P, _P, _P, _I, _I, _P, C.POINTER(_I)]),

@@ -311,6 +311,27 @@ int cf_assemble_jacobian_planes(cf_problem p, cf_constraints c, const cf_materia
   });
 }
 
+int cf_mf_apply_uu(cf_problem p, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                   const double* phi_tilde, const double* x, double* y) {
+  return guard([&] {
+    CHECK_ARG(p && c && mat && reg && phi_tilde && x && y, "cf_mf_apply_uu: null argument");
+    const GridDesc& g = p->p->g;
+    InArg<double> pt(phi_tilde, g.V);
+    InArg<double> xi(x, g.n_u());
+    OutArg<double> yo(y, g.n_u());
+    mf_apply_uu(*p->p, *c->c, *mat, *reg, pt.dev, xi.dev, yo.dev);
+    yo.finish();
+  });
+}
+
+int cf_fp64_peak(double* tflops) {
+  return guard([&] {
+    CHECK_ARG(tflops, "cf_fp64_peak: null argument");
+    ensure_device();
+    *tflops = fp64_peak_tflops();
+  });
+}
+
 int cf_sigma(const double grad_u[9], const cf_material* mat, int d, double out[9]) {
   return guard([&] {
     CHECK_ARG(grad_u && mat && out && (d == 2 || d == 3), "cf_sigma: bad argument");

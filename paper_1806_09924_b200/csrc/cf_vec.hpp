@@ -129,6 +129,11 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
 double compute_tcv(const Problem& P, const double* sol);
 void compute_cod(const Problem& P, const double* sol, const double* stations_host, int ns, double* out_host);
 
+// ---- mf.cu: matrix-free M_uu apply (x, y: n_u), FP64 FMA probe
+void mf_apply_uu(Problem& P, const Constraints& cs, const cf_material& m, const cf_regularization& reg,
+                 const double* pt, const double* x, double* y);
+double fp64_peak_tflops();
+
 // ---- io.cu (linsolve.cpp:478-490, postproc.cpp:111-167)
 void write_matrix_market(const Csr& A, const std::string& path);
 void write_vtk(const Problem& P, const double* sol_dev, const double* phi_old_dev, const std::string& path,

@@ -269,3 +269,21 @@ def test_extrapolate_phi(cf):
         got = cf.extrapolate_phi(st)
         ref = po if step <= 2 else np.minimum(np.maximum(2.0 * po - pp, 0.0), 1.0)
         assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("d,n0,r,clamp", [(2, 4, 2, True), (2, 3, 2, False), (3, 3, 1, True), (3, 2, 2, True)])
+def test_matrix_free_apply_equals_assembled(cf, d, n0, r, clamp):
+    """BASELINE config 1's matrix-free operator: y = M_uu x from phi_tilde cell by cell, equal to the
+    assembled block's apply (Dirichlet condensation included) to 1e-12 relative."""
+    P = cf.Problem(d, 1.0, n0, r)
+    rng = np.random.default_rng(21 + d + n0)
+    cs = cf.build_constraints(P, clamp)
+    pt = rng.uniform(0, 1, P.n_vertices)
+    x = np.zeros(P.n_total)
+    x[P.n_u:] = pt
+    mat, reg = cf.Material(pressure=1e-3), cf.Regularization(0.3, 1e-12)
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    u = rng.standard_normal(P.n_u)
+    ref = J.spmv(0, u)
+    got = cf.mf_apply_uu(P, cs, mat, reg, pt, u)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
