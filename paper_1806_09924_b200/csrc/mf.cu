@@ -135,43 +135,66 @@ __global__ void k_mf_gather(GridDesc g, const double* __restrict__ out, const st
     if (!flag[v * D + a]) y[v * D + a] = acc[a];
 }
 
-// constrained rows keep the summed element diagonal: y = d x (the assembled block's condensation)
+// constrained rows keep the summed element diagonal: y = d x (the assembled block's condensation).
+// 2^d threads per vertex, one per adjacent cell, combined with shuffles; interior vertices exit.
+template <int D>
+__global__ void k_mf_constrained(i64 V, int d, const std::uint8_t* __restrict__ flag, int* __restrict__ list,
+                                 int* __restrict__ count) {
+  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  bool any = false;
+  for (int a = 0; a < d; ++a) any |= flag[v * d + a] != 0;
+  if (any) list[atomicAdd(count, 1)] = int(v);  // rows are independent: the order is irrelevant
+}
+
 template <int D>
 __global__ void k_mf_diag(GridDesc g, const Tables* __restrict__ T, double mu, double lam, double kap,
                           const double* __restrict__ x, const double* __restrict__ pt,
-                          const std::uint8_t* __restrict__ flag, double* __restrict__ y) {
+                          const std::uint8_t* __restrict__ flag, const int* __restrict__ list, int n,
+                          double* __restrict__ y) {
   constexpr int NV = 1 << D, NQ = 1 << D;
-  const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (v >= g.V) return;
-  bool any = false;
-#pragma unroll
-  for (int a = 0; a < D; ++a) any |= flag[v * D + a] != 0;
-  if (!any) return;
-  const i64 vx = v % g.nn, vy = (v / g.nn) % g.nn, vz = (D == 3) ? v / (g.nn * g.nn) : 0;
+  const i64 gt = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 li = gt / NV;
+  const int t = int(gt % NV);  // v is corner t of the cell
+  if (li >= n) return;  // whole vertex groups leave together
+  const i64 v = list[li];
+  const unsigned uv = unsigned(v), nn = unsigned(g.nn);
+  const i64 vx = uv % nn, vy = (uv / nn) % nn, vz = (D == 3) ? uv / (nn * nn) : 0;
   double d[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) d[a] = 0.0;
-  for (int t = 0; t < NV; ++t) {
-    const i64 cx = vx - (t & 1), cy = vy - ((t >> 1) & 1), cz = vz - ((t >> 2) & 1);
-    if (cx < 0 || cy < 0 || cz < 0 || cx >= g.nc || cy >= g.nc || (D == 3 && cz >= g.nc)) continue;
+  const i64 cx = vx - (t & 1), cy = vy - ((t >> 1) & 1), cz = vz - ((t >> 2) & 1);
+  if (!(cx < 0 || cy < 0 || cz < 0 || cx >= g.nc || cy >= g.nc || (D == 3 && cz >= g.nc))) {
     double ptc[NV];
+#pragma unroll
     for (int k = 0; k < NV; ++k)
       ptc[k] = pt[(cx + (k & 1)) + g.nn * ((cy + ((k >> 1) & 1)) + g.nn * (cz + ((k >> 2) & 1)))];
+#pragma unroll
     for (int q = 0; q < NQ; ++q) {
       double p = 0.0;
+#pragma unroll
       for (int k = 0; k < NV; ++k) p += T->s[q][k] * ptc[k];
       const double wg = T->w[q] * ((1.0 - kap) * p * p + kap);
       double gg = 0.0;
+#pragma unroll
       for (int b = 0; b < D; ++b) gg += T->gp[q][t][b] * T->gp[q][t][b];
+#pragma unroll
       for (int a = 0; a < D; ++a) {
         const double da = T->gp[q][t][a];
         d[a] += wg * (mu * (gg + da * da) + lam * da * da);
       }
     }
   }
+  const unsigned grp = __activemask();  // the NV lanes of this vertex are all active here
 #pragma unroll
   for (int a = 0; a < D; ++a)
-    if (flag[v * D + a]) y[v * D + a] = d[a] * x[v * D + a];
+#pragma unroll
+    for (int o = NV / 2; o > 0; o >>= 1) d[a] += __shfl_xor_sync(grp, d[a], o, NV);
+  if (t == 0) {
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+      if (flag[v * D + a]) y[v * D + a] = d[a] * x[v * D + a];
+  }
 }
 
 // FP64 FMA throughput probe ("measure FP64 with a DFMA loop")
@@ -201,8 +224,17 @@ void mf_apply_uu(Problem& P, const Constraints& cs, const cf_material& m, const 
   const GridDesc& g = P.g;
   const int nv = 1 << g.d;
   static DevBuf<double> out;  // per-cell corner sums (scratch reused across applies)
+  static DevBuf<int> list, cnt;
   const i64 need = g.ncells * nv * g.d;
   if (out.n < need) out.alloc(need);
+  if (list.n < g.V) list.alloc(g.V);
+  if (!cnt.n) cnt.alloc(1);
+  cnt.zero();
+  k_mf_constrained<1><<<grid_for(g.V, 256), 256, 0, stream()>>>(g.V, g.d, cs.flag.p, list.p, cnt.p);
+  CF_LAUNCHED();
+  int n_con = 0;
+  CF_CUDA(cudaMemcpyAsync(&n_con, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
   const double mu = mat_mu(m), lam = mat_lambda(m);
   if (g.d == 2) {
     k_mf_cell<2><<<grid_for(g.ncells * 4, MF_BLOCK), MF_BLOCK, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, x, pt,
@@ -210,14 +242,16 @@ void mf_apply_uu(Problem& P, const Constraints& cs, const cf_material& m, const 
     CF_LAUNCHED();
     k_mf_gather<2><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, out.p, cs.flag.p, y);
     CF_LAUNCHED();
-    k_mf_diag<2><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, x, pt, cs.flag.p, y);
+    k_mf_diag<2><<<grid_for(i64(n_con) * 4, 256), 256, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, x, pt,
+                                                                       cs.flag.p, list.p, n_con, y);
   } else {
     k_mf_cell<3><<<grid_for(g.ncells * 8, MF_BLOCK), MF_BLOCK, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, x, pt,
                                                                               cs.flag.p, out.p);
     CF_LAUNCHED();
     k_mf_gather<3><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, out.p, cs.flag.p, y);
     CF_LAUNCHED();
-    k_mf_diag<3><<<grid_for(g.V, 256), 256, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, x, pt, cs.flag.p, y);
+    k_mf_diag<3><<<grid_for(i64(n_con) * 8, 256), 256, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, x, pt,
+                                                                       cs.flag.p, list.p, n_con, y);
   }
   CF_LAUNCHED();
 }
