@@ -422,6 +422,13 @@ def ours(args):
            "h2d_bytes_per_step": 8 * (P.n_total + 2 * P.n_vertices), "d2h_bytes_per_step": 8 * (P.n_total + 2 * P.n_vertices),
            "path": "cf_state_create(host) + cf_newton_active_set_step + cf_state_get(host)",
            "newton_iterations": len(rep_h["iterations"]), "solution_finite": bool(np.isfinite(x_h).all())}
+    if comm is not None:  # release the NCCL communicator while every rank is alive (not at exit)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        del comm
+        import gc
+        gc.collect()
+        torch.distributed.barrier()
 
     # the same step with every AMG hierarchy rebuilt (no bitwise-verified reuse), in a subprocess
     # because the switch is read once per process
@@ -441,6 +448,9 @@ def ours(args):
             vcyc = vcycle_leg(cf, P, mat, reg, torch.from_numpy(st.get()["solution"]).to(device), po0, s)
         except Exception as ex:  # reported, never fatal
             vcyc = {"error": str(ex)[:200]}
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
     if rank != 0:
         return
     op, roof = operator_leg(cf, device, s) if not args.no_operator else (None, None)
