@@ -24,6 +24,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <unordered_map>
 
@@ -855,6 +856,30 @@ __global__ void __launch_bounds__(1024) k_dense_lu(int n, double* a, int* piv, d
   }
 }
 
+// is the CSR diagonal (no off-diagonal entries)?  diag[i] = a_ii (0 when absent)
+__global__ void k_check_diag(i64 n, const i64* __restrict__ p, const int* __restrict__ c,
+                             const double* __restrict__ v, double* __restrict__ diag, int* __restrict__ offdiag) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double d = 0.0;
+  for (i64 k = p[i]; k < p[i + 1]; ++k) {
+    if (c[k] == int(i)) d = v[k];
+    else atomicOr(offdiag, 1);
+  }
+  diag[i] = d;
+}
+
+__global__ void k_diag_solve(i64 n, const double* __restrict__ d, const double* __restrict__ b,
+                             double* __restrict__ x) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = b[i] / d[i];
+}
+
+__global__ void k_min_abs(i64 n, const double* __restrict__ d, unsigned long long* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) atomicMin(out, __double_as_longlong(fabs(d[i])));  // non-negative doubles order as integers
+}
+
 // solve (single thread: sequential substitutions, as the oracle)
 __global__ void k_dense_solve(int n, const double* __restrict__ a, const int* __restrict__ piv,
                               const double* __restrict__ b, double* __restrict__ x) {
@@ -930,7 +955,28 @@ double estimate_lambda_max(const Csr& A, const double* inv_diag) {  // linsolve.
 // ------------------------------------------------------------------ dense LU host side
 void DenseLu::factor_from_csr(const Csr& A) {
   n = A.rows;
-  if (n > 16384) fail(CF_ERR_UNSUPPORTED, "dense LU: matrix too large for the one-CTA factorisation");
+  diagonal = false;
+  if (n > 16384) {
+    lu.alloc(n);
+    DevBuf<int> off(1);
+    off.zero();
+    k_check_diag<<<grid_for(n, 256), 256, 0, stream()>>>(n, A.ptr.p, A.col.p, A.val.p, lu.p, off.p);
+    CF_LAUNCHED();
+    DevBuf<unsigned long long> mn(1);
+    const unsigned long long inf_bits = 0x7ff0000000000000ull;
+    CF_CUDA(cudaMemcpyAsync(mn.p, &inf_bits, sizeof(inf_bits), cudaMemcpyHostToDevice, stream()));
+    k_min_abs<<<grid_for(n, 256), 256, 0, stream()>>>(n, lu.p, mn.p);
+    CF_LAUNCHED();
+    int h_off = 0;
+    unsigned long long h_mn = 0;
+    CF_CUDA(cudaMemcpyAsync(&h_off, off.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaMemcpyAsync(&h_mn, mn.p, sizeof(h_mn), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    if (h_off) fail(CF_ERR_UNSUPPORTED, "dense LU: matrix too large for the one-CTA factorisation");
+    std::memcpy(&min_abs_pivot, &h_mn, sizeof(double));
+    diagonal = true;
+    return;
+  }
   lu.alloc(std::max<i64>(n * n, 1));
   lu.zero();
   piv.alloc(std::max<i64>(n, 1));
@@ -948,6 +994,11 @@ void DenseLu::factor_from_csr(const Csr& A) {
 
 void DenseLu::solve(const double* b, double* x) const {
   if (n == 0) return;
+  if (diagonal) {
+    k_diag_solve<<<grid_for(n, 256), 256, 0, stream()>>>(n, lu.p, b, x);
+    CF_LAUNCHED();
+    return;
+  }
   k_dense_solve<<<1, 32, 0, stream()>>>(int(n), lu.p, piv.p, b, x);
   CF_LAUNCHED();
 }
@@ -1235,7 +1286,10 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     B = std::move(Bc);
     nod = std::move(cnode);
   }
+  if (clk.on) std::fprintf(stderr, "[amg] coarsest dense LU n=%lld after %zu levels\n", (long long)A->rows,
+                           h->levels.size());
   h->coarse.factor_from_csr(*A);
+  clk.mark("coarse LU");
   if (A->rows > 0 && h->coarse.min_abs_pivot == 0.0)
     fail(CF_ERR_NUMERICAL, "build_amg: coarsest-level matrix is singular");
   h->cb.alloc(std::max<i64>(A->rows, 1));

@@ -51,6 +51,10 @@ struct DenseLu {
   DevBuf<double> lu;
   DevBuf<int> piv;
   double min_abs_pivot = 0.0;
+  // a diagonal coarsest matrix beyond the dense size (e.g. the all-active phi block of a slab far
+  // from the crack, where aggregation stops at once): LU without pivoting is the diagonal itself,
+  // so the solve is x_i = b_i / a_ii
+  bool diagonal = false;
   void factor_from_csr(const Csr& A);
   void solve(const double* b, double* x) const;  // device vectors
 };

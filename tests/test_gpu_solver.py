@@ -305,3 +305,15 @@ def test_3d_penny_newton_bit_exact(cf, orc):
     _same_transcript(reps[0], oreps[0])
     assert np.array_equal(x, xo)
     assert reps[0]["converged"] and reps[0]["feasibility_violation"] <= 1e-10
+
+
+def test_amg_large_diagonal_coarsest(cf):
+    """A diagonal matrix beyond the dense-LU size (the all-active phi block of a slab far from the
+    crack): aggregation stops at once and the coarsest 'LU' is the diagonal itself."""
+    import scipy.sparse as sp
+    n = 20000
+    d = np.random.default_rng(2).uniform(1.0, 3.0, n)
+    h = cf.build_amg(cf.CsrMatrix.from_scipy(sp.diags(d).tocsr()))
+    assert h.n_levels() == 1
+    r = np.random.default_rng(3).standard_normal(n)
+    assert np.array_equal(h.v_cycle(r), r / d)
