@@ -376,7 +376,7 @@ def ours(args):
     sol0 = torch.from_numpy(st0["solution"]).to(device)
     po0 = torch.from_numpy(st0["phi_old"]).to(device)
     # N > 1: one config-3 step split over the ranks (z-slabs, NCCL halo planes, rank-ordered dots,
-    # block-Jacobi AMG over the slabs): strong scaling of the same workload
+    # restricted additive Schwarz with per-slab block AMG): strong scaling of the same workload
     comm = cf.Communicator.from_torch_distributed() if world > 1 else None
 
     def step():
@@ -460,7 +460,7 @@ def ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Sneddon state)",
         "config": dict(CONFIG if args.workload == "cfg3" else CONFIG4, parallelism="single GPU" if world == 1 else
-                       f"{world} GPUs: z-slab decomposition, NCCL halo planes, block-Jacobi AMG over slabs"),
+                       f"{world} GPUs: z-slab decomposition, NCCL halo planes, restricted additive Schwarz (per-slab block AMG)"),
         "newton_iterations_per_step": its, "ms_per_newton_iteration": ms / its,
         "gmres_iterations": [r["gmres_iterations"] for r in last["iterations"]],
         "active_set_final": last["iterations"][-1]["active_size"],

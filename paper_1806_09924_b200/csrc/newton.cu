@@ -417,6 +417,15 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   std::shared_ptr<Csr> uu_step;  // this load step's M_uu
   std::shared_ptr<Csr> uu_loc;   // its diagonal slab block (distributed preconditioner)
   const Csr* uu_loc_src = nullptr;
+  // distributed preconditioner: restricted additive Schwarz with one plane of overlap (default), or
+  // block-Jacobi over the slabs (CF_BLOCK_JACOBI=1)
+  static const bool ras_env = std::getenv("CF_BLOCK_JACOBI") == nullptr;
+  const bool ras = dist && ras_env;
+  const Slab sx = ras ? make_slab(g, sl.ve_lo / sl.plane, sl.ve_hi / sl.plane) : sl;
+  std::shared_ptr<Csr> uu_x_step;
+  DevBuf<double> Bux(ras ? d * sx.nv() * (d == 2 ? 3 : 6) : 0), Bpx(ras ? sx.nv() : 0);
+  DevBuf<int> unodex(ras ? d * sx.nv() : 0), pnodex(ras ? sx.nv() : 0);
+  DevBuf<double> pin(ras ? (d + 1) * sx.nv() : 0), pout(ras ? (d + 1) * sx.nv() : 0);
   DevBuf<int> unode(nul), pnode(nv);
   const unsigned gv = grid_for(nv, 256), gl = grid_for(ntl, 256);
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
@@ -519,16 +528,38 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         // block of its rows (owned columns only); one GPU is the undivided block
         BlockSystem Jl;
         Jl.d = d;
-        Jl.nu = nul;
-        Jl.np = nv;
-        const i64 lo = sl.v_lo - sl.ve_lo;
-        if (uu_loc_src != J->uu.get()) {  // the diagonal block of a reused M_uu is reused too
-          uu_loc = csr_extract_cols(*J->uu, d * lo, d * (lo + nv));
-          uu_loc_src = J->uu.get();
+        if (ras) {
+          // restricted additive Schwarz: the block of the owned planes plus one plane of overlap
+          // on each side (rows assembled for the extended slab, columns cut to it)
+          auto Jx = assemble_jacobian(P, full, mat, reg, x, pt.p, &sx, uu_x_step);
+          if (!uu_x_step) uu_x_step = Jx->uu;
+          const i64 lo = sx.v_lo - sx.ve_lo, nx = sx.nv();
+          if (uu_loc_src != Jx->uu.get()) {
+            uu_loc = csr_extract_cols(*Jx->uu, d * lo, d * (lo + nx));
+            uu_loc_src = Jx->uu.get();
+          }
+          Jl.nu = d * nx;
+          Jl.np = nx;
+          Jl.uu = uu_loc;
+          Jl.pp = csr_extract_cols(*Jx->pp, lo, lo + nx);
+          rigid_body_modes(P, full, Bux.p, &sx);
+          k_phi_modes<<<grid_for(nx, 256), 256, 0, stream()>>>(sx, nu, full.flag.p, Bpx.p, pnodex.p, unodex.p, d);
+          CF_LAUNCHED();
+          NullspaceDev nsx{unodex.p, Bux.p, d == 2 ? 3 : 6, pnodex.p, Bpx.p};
+          prec = build_block_prec(Jl, opts.prec_kind, opts.amg, &nsx, prec.get());
+        } else {
+          // block-Jacobi over the slabs: each rank's preconditioner on its diagonal block
+          Jl.nu = nul;
+          Jl.np = nv;
+          const i64 lo = sl.v_lo - sl.ve_lo;
+          if (uu_loc_src != J->uu.get()) {  // the diagonal block of a reused M_uu is reused too
+            uu_loc = csr_extract_cols(*J->uu, d * lo, d * (lo + nv));
+            uu_loc_src = J->uu.get();
+          }
+          Jl.uu = uu_loc;
+          Jl.pp = csr_extract_cols(*J->pp, lo, lo + nv);
+          prec = build_block_prec(Jl, opts.prec_kind, opts.amg, &ns, prec.get());
         }
-        Jl.uu = uu_loc;
-        Jl.pp = csr_extract_cols(*J->pp, lo, lo + nv);
-        prec = build_block_prec(Jl, opts.prec_kind, opts.amg, &ns, prec.get());
       } else {
         prec = build_block_prec(*J, opts.prec_kind, opts.amg, &ns, prec.get());
       }
@@ -551,6 +582,17 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
       }
       const BlockPrec& Pr = *prec;
       DevOp pop = [&Pr](const double* in, double* out) { Pr.apply(in, out); };
+      if (ras) {  // residual on the extended slab (halo planes), local solve, keep the owned rows
+        double *pi = pin.p, *po = pout.p;
+        pop = [&Pr, &cm, &g, &sl, &sx, pi, po, d, nv, nul](const double* in, double* out) {
+          to_ext(cm, g, sl, in, pi);
+          Pr.apply(pi, po);
+          const i64 lo = sl.v_lo - sl.ve_lo, nx = sx.nv();
+          CF_CUDA(cudaMemcpyAsync(out, po + d * lo, size_t(nul) * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+          CF_CUDA(cudaMemcpyAsync(out + nul, po + d * nx + lo, size_t(nv) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  stream()));
+        };
+      }
       lin = gmres(op, &pop, rhs.p, ntl, opts.gmres, delta.p, comm);
     }
     if (!lin.converged && !lin.breakdown) fail(CF_ERR_NUMERICAL, "newton_active_set_step: GMRES stagnated at max_iter");
