@@ -279,8 +279,9 @@ int cf_write_vtk(cf_problem p, const double* solution, const double* phi_old, co
  * variants run the slab-decomposed step: rank r owns the planes of cf_slab_info(r, size); halo
  * planes move by NCCL send/recv, every dot / norm is a rank-ordered sum (bitwise identical on
  * all ranks), the preconditioner is restricted additive Schwarz over the slabs (each rank's block
- * AMG on its planes plus one overlap plane each side; CF_BLOCK_JACOBI=1: block-Jacobi).  The state is global-length on every rank and holds the full solution on return.
- * size == 1 is the single-GPU step exactly. */
+ * AMG on its planes plus one overlap plane each side; CF_BLOCK_JACOBI=1: block-Jacobi).  The
+ * state is global-length on every rank and holds the full solution on return.  size == 1 is the
+ * single-GPU step exactly. */
 typedef struct cf_comm_s* cf_comm;
 /* Host-staged transport (TEST ONLY: lets several ranks share one GPU to exercise the decomposed
  * step's control flow without NCCL; device data is staged through host memory, so it is never
