@@ -1,5 +1,6 @@
 """Algorithmic scaling of the slab decomposition: GMRES / Newton iteration counts of one config-3
-Newton step with N ranks (block-Jacobi AMG over N z-slabs), run with N processes sharing one GPU
+Newton step with N ranks (restricted additive Schwarz over N z-slabs, or block-Jacobi with
+CF_BLOCK_JACOBI=1), run with N processes sharing one GPU
 through the host-staged test transport (Communicator.from_gloo).  Only the iteration counts and the
 agreement of the solutions are meaningful here — the transport is not a timing.
 

@@ -9,8 +9,9 @@ transport:
     [u_ext | phi_ext] is complete, and the halo exchange fills exactly those planes;
   * a slab's rows times the ext vector are bitwise the rows of the undivided product;
   * rank-ordered sums are bitwise identical on every rank;
-  * GMRES with rank-ordered dots and the block-Jacobi preconditioner converges to the undivided
-    solution.
+  * GMRES with rank-ordered dots and the preconditioners of the product — restricted additive
+    Schwarz with one overlap plane (default) and block-Jacobi (CF_BLOCK_JACOBI=1) — converges to
+    the undivided solution.
 """
 import os
 import socket
@@ -68,7 +69,7 @@ def sum_ordered(vals, size):  # comm.cu Comm::sum_ordered: all-gather, then left
     return s.numpy()
 
 
-def _worker(rank, size, port, out_dir):
+def _worker(rank, size, port, out_dir, ras):
     sys.path.insert(0, ROOT)
     import scipy.sparse as sp
     import scipy.sparse.linalg as spla
@@ -119,12 +120,22 @@ def _worker(rank, size, port, out_dir):
     # rank-ordered sum (compared across ranks by the parent)
     tot = sum_ordered([own(z) @ own(z)], size)
 
-    # block-Jacobi (exact inverse of the diagonal block of each slab) + MGS GMRES, rank-ordered dots
-    Luu = spla.splu(sp.csc_matrix(Suu[:, d * (lo - elo):d * (hi - elo)]))
-    Lpp = spla.splu(sp.csc_matrix(Spp[:, lo - elo:hi - elo]))
+    # preconditioner (exact local solves in place of the per-slab AMG) + MGS GMRES, rank-ordered dots
+    if ras:  # restricted additive Schwarz: the block of the planes plus one overlap plane each side
+        Xuu = sp.csc_matrix(Muu[d * elo:d * ehi, d * elo:d * ehi])
+        Xpp = sp.csc_matrix(Mpp[elo:ehi, elo:ehi])
+        Luu, Lpp = spla.splu(Xuu), spla.splu(Xpp)
 
-    def prec(rl):
-        return np.concatenate([Luu.solve(rl[:d * nv]), Lpp.solve(rl[d * nv:])])
+        def prec(rl):
+            e = to_ext(rl, s, d, rank, size)
+            zu, zp = Luu.solve(e[:d * ne]), Lpp.solve(e[d * ne:])
+            return np.concatenate([zu[d * (lo - elo):d * (hi - elo)], zp[lo - elo:hi - elo]])
+    else:  # block-Jacobi: the diagonal block of the slab
+        Luu = spla.splu(sp.csc_matrix(Suu[:, d * (lo - elo):d * (hi - elo)]))
+        Lpp = spla.splu(sp.csc_matrix(Spp[:, lo - elo:hi - elo]))
+
+        def prec(rl):
+            return np.concatenate([Luu.solve(rl[:d * nv]), Lpp.solve(rl[d * nv:])])
 
     def gdot(a, b):
         return float(sum_ordered([a @ b], size)[0])
@@ -167,10 +178,10 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-@pytest.mark.parametrize("size", [2])
-def test_slab_protocol_gloo(orc, tmp_path, size):
+@pytest.mark.parametrize("size,ras", [(2, True), (2, False)])
+def test_slab_protocol_gloo(orc, tmp_path, size, ras):
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(size, _free_port(), str(tmp_path)), nprocs=size, join=True)
+    mp.spawn(_worker, args=(size, _free_port(), str(tmp_path), ras), nprocs=size, join=True)
     outs = [np.load(tmp_path / f"rank{r}.npy") for r in range(size)]
     assert all(o[0] <= 1e-9 for o in outs), [o[0] for o in outs]
     assert len({o[1] for o in outs}) == 1, "ranks disagree on the iteration count"
