@@ -143,7 +143,8 @@ void group_by_key(i64 n, const int* key, i64 nkeys, DevBuf<i64>& ptr, DevBuf<int
 }
 
 // ------------------------------------------------------------------ strength (linsolve.cpp:185-201)
-constexpr int SCAP = 96;  // distinct neighbour nodes per node in the register/local tier
+constexpr int SCAP = 96;        // distinct neighbour nodes per node in the register/local tier
+constexpr int SWARP_MIN = 320;  // nodes with more entries than this use the warp tier
 
 // Overflow tier: nodes with more distinct neighbour nodes than SCAP get a private open-addressing
 // table in global memory (capacity = next pow2 >= 2 x their entry count); one thread per node
@@ -222,6 +223,95 @@ __global__ void k_strength_big(i64 nov, const int* __restrict__ list, const i64*
   len_out[t] = len;
 }
 
+// Warp-per-node variant of k_strength_big (the same table, sums and ascending output): the 32 lanes
+// take consecutive entries of one dof row; lanes that hit the same neighbour node are applied by the
+// lowest of them in lane (= column) order, and rows follow one another, so every sum is accumulated
+// in exactly the serial (row, column) order.  Tables come in with keys = -1 and sums = 0.
+constexpr int SBW_WPB = 4;
+__global__ void __launch_bounds__(SBW_WPB * 32)
+    k_strength_bigw(i64 nov, const int* __restrict__ list, const i64* __restrict__ off, const i64* __restrict__ nptr,
+                    const int* __restrict__ ndofs, const i64* __restrict__ Ap, const int* __restrict__ Ac,
+                    const double* __restrict__ Av, const int* __restrict__ nod, int* __restrict__ keys,
+                    double* __restrict__ sums, int* __restrict__ len_out) {
+  __shared__ double sbuf[SBW_WPB][32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 t = i64(blockIdx.x) * SBW_WPB + w;
+  if (t >= nov) return;
+  const int i = list[t];
+  int* K = keys + off[t];
+  double* S = sums + off[t];
+  const unsigned cap = unsigned(off[t + 1] - off[t]), mask = cap - 1u;
+  for (i64 q = nptr[i]; q < nptr[i + 1]; ++q) {
+    const int r = ndofs[q];
+    const i64 e0 = Ap[r], e1 = Ap[r + 1];
+    for (i64 b = e0; b < e1; b += 32) {
+      const i64 k = b + lane;
+      const bool v = k < e1;
+      int slot = -1;
+      if (v) {
+        const int nj = nod[Ac[k]];
+        const double x = Av[k];
+        sbuf[w][lane] = x * x;
+        unsigned s = hash_u(nj) & mask;
+        for (unsigned p = 0; p < cap; ++p) {
+          int cur = K[s];
+          if (cur == -1) cur = atomicCAS(&K[s], -1, nj);
+          if (cur == -1 || cur == nj) break;
+          s = (s + 1) & mask;
+        }
+        slot = int(s);
+      }
+      __syncwarp();
+      const unsigned act = __ballot_sync(0xffffffffu, v);
+      const unsigned peers = __match_any_sync(0xffffffffu, slot);
+      if (v && (peers & act & ((1u << lane) - 1u)) == 0) {  // lowest lane of its group
+        double acc = S[slot];
+        for (unsigned m = peers & act; m; m &= m - 1) acc += sbuf[w][__ffs(m) - 1];
+        S[slot] = acc;
+      }
+      __syncwarp();
+    }
+  }
+  // compact the occupied slots (ascending slot order) to the front, pad, bitonic-sort by key
+  int len = 0;
+  for (unsigned b = 0; b < cap; b += 32) {
+    const unsigned s = b + lane;
+    const int key = s < cap ? K[s] : -1;
+    const double sm = s < cap ? S[s] : 0.0;
+    const unsigned occ = __ballot_sync(0xffffffffu, key != -1);
+    __syncwarp();
+    if (key != -1) {
+      const int dst = len + __popc(occ & ((1u << lane) - 1u));
+      K[dst] = key;
+      S[dst] = sm;
+    }
+    len += __popc(occ);
+    __syncwarp();
+  }
+  unsigned n2 = 1;
+  while (n2 < unsigned(len)) n2 <<= 1;
+  for (unsigned s = len + lane; s < n2; s += 32) K[s] = INT_MAX;
+  __syncwarp();
+  for (unsigned k2 = 2; k2 <= n2; k2 <<= 1)
+    for (unsigned j = k2 >> 1; j > 0; j >>= 1) {
+      for (unsigned s = lane; s < n2; s += 32) {
+        const unsigned o = s ^ j;
+        if (o > s) {
+          const int a = K[s], c = K[o];
+          if ((a > c) == ((s & k2) == 0)) {
+            K[s] = c;
+            K[o] = a;
+            const double ta = S[s];
+            S[s] = S[o];
+            S[o] = ta;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  if (lane == 0) len_out[t] = len;
+}
+
 // strong test on the sorted overflow lists; mode 0 counts, mode 1 writes
 __global__ void k_strength_big_emit(i64 nov, const int* __restrict__ list, const i64* __restrict__ off,
                                     const int* __restrict__ keys, const double* __restrict__ sums,
@@ -279,6 +369,14 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   if (mode && ovf[i]) return;  // handled by the overflow tier
+  if (!mode) {  // long nodes go straight to the warp tier (one thread would walk them serially)
+    i64 e = 0;
+    for (i64 t = nptr[i]; t < nptr[i + 1]; ++t) e += Ap[ndofs[t] + 1] - Ap[ndofs[t]];
+    if (e > SWARP_MIN) {
+      ovf[i] = 1;
+      return;
+    }
+  }
   int keys[SCAP];
   double sums[SCAP];
   int len = 0;
@@ -1074,8 +1172,15 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
       bsums.alloc(tot);
       blen.alloc(big.n);
       CF_CUDA(cudaMemsetAsync(bkeys.p, 0xff, size_t(tot) * sizeof(int), stream()));
-      k_strength_big<<<grid_for(big.n, 64), 64, 0, stream()>>>(big.n, big.list.p, boff.p, nptr.p, ndofs.p, A->ptr.p,
-                                                               A->col.p, A->val.p, nod.p, bkeys.p, bsums.p, blen.p);
+      if (std::getenv("CF_STRENGTH_SERIAL")) {  // A/B switch: the one-thread-per-node tier
+        k_strength_big<<<grid_for(big.n, 64), 64, 0, stream()>>>(big.n, big.list.p, boff.p, nptr.p, ndofs.p,
+                                                                 A->ptr.p, A->col.p, A->val.p, nod.p, bkeys.p, bsums.p,
+                                                                 blen.p);
+      } else {
+        CF_CUDA(cudaMemsetAsync(bsums.p, 0, size_t(tot) * sizeof(double), stream()));
+        k_strength_bigw<<<grid_for(big.n, SBW_WPB), SBW_WPB * 32, 0, stream()>>>(
+            big.n, big.list.p, boff.p, nptr.p, ndofs.p, A->ptr.p, A->col.p, A->val.p, nod.p, bkeys.p, bsums.p, blen.p);
+      }
       CF_LAUNCHED();
       k_strength_big_emit<<<grid_for(big.n, 128), 128, 0, stream()>>>(big.n, big.list.p, boff.p, bkeys.p, bsums.p,
                                                                       blen.p, dsq.p, opts.strength_threshold, sptr.p,

@@ -42,3 +42,13 @@ for t, c, k in rows[:25]:
     print(f"  {t:8.2f} ms {c:5d} {k[:90]}")
 for lev in range(h.n_levels() - 1):
     print(lev, h.level_info(lev))
+
+if os.environ.get("PHI_TRACE"):
+    # chronological kernel list of one build (name, duration, gap before)
+    evs = sorted((e for e in prof.events() if e.device_type.name == "CUDA"), key=lambda e: e.time_range.start)
+    t0 = evs[0].time_range.start
+    prev = t0
+    with open(os.environ["PHI_TRACE"], "w") as f:
+        for e in evs:
+            f.write(f"{(e.time_range.start - t0) / 1e3:9.3f} ms  dur {e.time_range.elapsed_us():8.1f} us  gap {(e.time_range.start - prev):8.1f} us  {e.name[:80]}\n")
+            prev = e.time_range.end
