@@ -13,6 +13,7 @@
 //      IEEE sequence as Eigen's conservative sparse product and the oracle, with no
 //      floating-point atomics and independent of the launch configuration.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <climits>
 #include <cstdlib>
@@ -518,10 +519,195 @@ void num_launch(const RowBin& b, int cap, const Csr& A, const Csr& B, const doub
   CF_LAUNCHED();
 }
 
+// --- row groups: runs of consecutive A rows with one column pattern ------------------------
+// Rows of one mesh node (or of one aggregate on the coarse levels) share their pattern, and so do
+// their product rows: the symbolic phase runs once per group and the numeric kernel below applies
+// each B row once for all rows of the group.  Per row, every C(i,j) is still the k-ascending
+// sequential sum, so C is bitwise that of the row-wise kernels.
+__global__ void k_same_prev(i64 rows, const i64* __restrict__ p, const int* __restrict__ c, int* __restrict__ head) {
+  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= rows) return;
+  bool same = i > 0;
+  i64 n = 0, b0 = 0, b1 = 0;
+  if (same) {
+    b0 = p[i - 1];
+    b1 = p[i];
+    n = p[i + 1] - b1;
+    same = n > 0 && n == b1 - b0;
+  }
+  for (i64 t = lane; same && t < n; t += 32)
+    if (c[b0 + t] != c[b1 + t]) same = false;
+  same = __all_sync(0xffffffffu, same);
+  if (lane == 0) head[i] = same ? 0 : 1;
+}
+
+// run start of each row: max over j <= i of (head[j] ? j : 0) via a max-scan of these keys
+__global__ void k_head_key(i64 rows, const int* __restrict__ head, int* __restrict__ key) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < rows) key[i] = head[i] ? int(i) : 0;
+}
+__global__ void k_chunk_heads(i64 rows, const int* __restrict__ runstart, int gm, int* __restrict__ head) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < rows) head[i] = ((int(i) - runstart[i]) % gm) == 0 ? 1 : 0;
+}
+__global__ void k_group_len(int ng, const int* __restrict__ heads, i64 rows, int* __restrict__ glen) {
+  const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < ng) glen[g] = (g + 1 < ng ? heads[g + 1] : int(rows)) - heads[g];
+}
+
+// gathered head rows (pattern only)
+__global__ void k_head_len(int ng, const int* __restrict__ heads, const i64* __restrict__ p, i64* __restrict__ out) {
+  const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < ng) out[g] = p[heads[g] + 1] - p[heads[g]];
+}
+__global__ void k_gather_rows(int ng, const int* __restrict__ heads, const i64* __restrict__ p,
+                              const int* __restrict__ c, const i64* __restrict__ gp, int* __restrict__ gc) {
+  const i64 g = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= ng) return;
+  const i64 b = p[heads[g]], n = gp[g + 1] - gp[g];
+  for (i64 t = lane; t < n; t += 32) gc[gp[g] + t] = c[b + t];
+}
+// expand the group pattern to the rows: lengths, then columns
+__global__ void k_expand_len(int ng, const int* __restrict__ heads, const int* __restrict__ glen,
+                             const i64* __restrict__ gp, i64* __restrict__ cnt) {
+  const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const i64 n = gp[g + 1] - gp[g];
+  for (int r = 0; r < glen[g]; ++r) cnt[heads[g] + r] = n;
+}
+__global__ void k_expand_cols(int ng, const int* __restrict__ heads, const int* __restrict__ glen,
+                              const i64* __restrict__ gp, const int* __restrict__ gc, const i64* __restrict__ cp,
+                              int* __restrict__ cc) {
+  const i64 g = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (g >= ng) return;
+  const i64 b = gp[g], n = gp[g + 1] - b;
+  for (int r = 0; r < glen[g]; ++r) {
+    const i64 o = cp[heads[g] + r];
+    for (i64 t = lane; t < n; t += 32) cc[o + t] = gc[b + t];
+  }
+}
+// per-row selection of the rows of the listed groups (their C row length), for the row-wise tiers
+__global__ void k_select_group_rows(int n, const int* __restrict__ list, const int* __restrict__ heads,
+                                    const int* __restrict__ glen, const i64* __restrict__ cp, i64* __restrict__ sel) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int g = list[t];
+  for (int r = 0; r < glen[g]; ++r) {
+    const i64 i = heads[g] + r;
+    sel[i] = cp[i + 1] - cp[i];
+  }
+}
+
+constexpr int GRP_MAX = 6;  // rows per group (longer runs are chunked)
+
+// numeric, warp per group: the group's (shared) columns in a hash of cap slots, one accumulator row
+// per group row.  The A positions k are taken in ascending order, one at a time; the lanes cover
+// the entries of B row k (CB per lane), find each slot once and apply it to every row of the group.
+// Within one k the slots are distinct, so no two lanes touch one accumulator; __syncwarp orders
+// successive k.  The next k's B row and A values are loaded while the current one is applied.
+template <int CB>
+__global__ void __launch_bounds__(256) k_num_grp(const int* __restrict__ glist, int ng, const int* __restrict__ heads,
+                                                 const int* __restrict__ glen, int cap, int wpb,
+                                                 const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                 const double* __restrict__ av, const double* __restrict__ rs,
+                                                 const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                 const double* __restrict__ bv, const i64* __restrict__ cp,
+                                                 const int* __restrict__ cc, double* __restrict__ cv) {
+  extern __shared__ double grp_sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 gi = i64(blockIdx.x) * wpb + w;
+  if (gi >= ng) return;
+  const int grp = glist[gi];
+  const int row0 = heads[grp], nr = glen[grp];
+  double* Acc = grp_sm + size_t(w) * cap * GRP_MAX;  // [GRP_MAX][cap]
+  int* T = reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * GRP_MAX) + size_t(w) * cap;
+  for (int s = lane; s < cap; s += 32) T[s] = EMPTY;
+  for (int s = lane; s < cap * nr; s += 32) Acc[s] = 0.0;
+  __syncwarp();
+  const unsigned mask = unsigned(cap) - 1u;
+  const i64 c0 = cp[row0];
+  const int nc = int(cp[row0 + 1] - c0);
+  for (int t = lane; t < nc; t += 32) hinsert(T, mask, cc[c0 + t]);
+  __syncwarp();
+  double si[GRP_MAX];
+#pragma unroll
+  for (int r = 0; r < GRP_MAX; ++r) si[r] = (r < nr && rs) ? rs[row0 + r] : 1.0;
+  const i64 a0 = ap[row0];
+  const int alen = int(ap[row0 + 1] - a0);
+  int ck[CB], nk[CB];
+  double cb[CB], nb[CB], ca[GRP_MAX], na[GRP_MAX];
+  int cn = 0, nn = 0;
+  auto load = [&](int pos, int* kc, double* kv, double* ka, int& n) {
+    const int k = ac[a0 + pos];
+    const i64 q0 = bp[k];
+    n = int(bp[k + 1] - q0);
+#pragma unroll
+    for (int t = 0; t < CB; ++t) {
+      const int e = t * 32 + lane;
+      if (e < n) {
+        kc[t] = bc[q0 + e];
+        kv[t] = bv[q0 + e];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < GRP_MAX; ++r)
+      if (r < nr) ka[r] = rs ? si[r] * av[a0 + i64(r) * alen + pos] : av[a0 + i64(r) * alen + pos];
+  };
+  if (alen > 0) load(0, ck, cb, ca, cn);
+  for (int pos = 0; pos < alen; ++pos) {
+    if (pos + 1 < alen) load(pos + 1, nk, nb, na, nn);
+#pragma unroll
+    for (int t = 0; t < CB; ++t) {
+      const int e = t * 32 + lane;
+      if (e < cn) {
+        const int sl = hfind(T, mask, ck[t]);
+#pragma unroll
+        for (int r = 0; r < GRP_MAX; ++r)
+          if (r < nr) Acc[size_t(r) * cap + sl] += ca[r] * cb[t];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < CB; ++t) {
+      ck[t] = nk[t];
+      cb[t] = nb[t];
+    }
+#pragma unroll
+    for (int r = 0; r < GRP_MAX; ++r) ca[r] = na[r];
+    cn = nn;
+  }
+  for (int t = lane; t < nc; t += 32) {
+    const int sl = hfind(T, mask, cc[c0 + t]);
+    for (int r = 0; r < nr; ++r) cv[c0 + i64(r) * nc + t] = Acc[size_t(r) * cap + sl];
+  }
+}
+
+template <int CB>
+void num_grp_launch(const RowBin& b, int cap, const int* heads, const int* glen, const Csr& A, const Csr& B,
+                    const double* rs, Csr& C) {
+  if (!b.n) return;
+  const size_t per_warp = size_t(cap) * (sizeof(int) + sizeof(double) * GRP_MAX);
+  const int wpb = int(std::min<size_t>(8, std::max<size_t>(1, (100u << 10) / per_warp)));
+  const size_t sm = per_warp * wpb;
+  CF_CUDA(cudaFuncSetAttribute(k_num_grp<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+  k_num_grp<CB><<<grid_for(b.n, wpb), wpb * 32, sm, stream()>>>(b.list.p, b.n, heads, glen, cap, wpb, A.ptr.p,
+                                                               A.col.p, A.val.p, rs, B.ptr.p, B.col.p, B.val.p,
+                                                               C.ptr.p, C.col.p, C.val.p);
+  CF_LAUNCHED();
+}
+
+__global__ void k_group_clen(int ng, const int* __restrict__ heads, const i64* __restrict__ cp, i64* __restrict__ out) {
+  const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < ng) out[g] = cp[heads[g] + 1] - cp[heads[g]];
+}
+
 }  // namespace
 
-std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale) {
-  if (A.cols != B.rows) fail(CF_ERR_LOGIC, "spgemm: inner dimensions differ");
+// pattern of C = A B (sorted columns; values allocated, not computed); L lanes per B row
+static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L) {
   auto C = std::make_unique<Csr>();
   C->rows = A.rows;
   C->cols = B.cols;
@@ -529,18 +715,6 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   C->ptr.zero();
   const i64 m = A.rows;
   if (m == 0) return C;
-  i64 maxb;
-  {
-    DevBuf<unsigned long long> mx(1);
-    mx.zero();
-    k_max_row<<<int(std::min<i64>(1024, grid_for(B.rows, 256))), 256, 0, stream()>>>(B.rows, B.ptr.p, mx.p);
-    CF_LAUNCHED();
-    unsigned long long h = 0;
-    CF_CUDA(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    maxb = i64(h);
-  }
-  const int L = lanes_for(maxb);
   i64* cnt = C->ptr.p;  // row counts in place, scanned into offsets afterwards
   // 1. symbolic count: all rows with products try the 512-slot tier, which also spills its
   //    unsorted unique columns (<= 384 per row) to scratch; overflow -> 2048 -> CTA tiers
@@ -592,13 +766,10 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   C->nnz = read_i64(C->ptr.p + m);
   C->col.alloc(C->nnz);
   C->val.alloc(C->nnz);
-  // 2. symbolic fill and 3. numeric, binned by the exact row length
+  // 2. symbolic fill
   DevBuf<i64> len(m);
   k_row_len<<<grid_for(m, 256), 256, 0, stream()>>>(m, C->ptr.p, len.p);
   CF_LAUNCHED();
-  RowBin f1 = make_bin(m, len.p, 0, 256);
-  RowBin f2 = make_bin(m, len.p, 256, 1024);
-  RowBin f3 = make_bin(m, len.p, 1024, LLONG_MAX);
   // spilled rows: sort their scratch columns; overflow rows: hash again in the 2048/CTA tiers
   if (spilled.n) {
     k_sort_rows<512, 8><<<grid_for(spilled.n, 8), 256, 0, stream()>>>(spilled.list.p, spilled.n, soff.p, spill.p,
@@ -627,28 +798,158 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
                                                     C->ptr.p, C->col.p, 1, flag.p);
     CF_LAUNCHED();
   }
-  // numeric: k-grouped warp kernels (G = 32/L A entries per step) by row length; CTA otherwise
+  return C;
+}
+
+// values of C = diag(rs) A B on the rows whose entry of lensel (the C row length, 0 = skip) is
+// positive, binned by that length: k-grouped warp kernels (G = 32/L A entries per step), CTA beyond
+static void spgemm_numeric(const Csr& A, const Csr& B, const double* row_scale, Csr& C, i64 maxb, int L,
+                           const i64* lensel) {
+  const i64 m = A.rows;
+  RowBin f1 = make_bin(m, lensel, 0, 256);
+  RowBin f2 = make_bin(m, lensel, 256, 1024);
+  RowBin f3 = make_bin(m, lensel, 1024, LLONG_MAX);
   const i64 cmax_need = (maxb + L - 1) / L;
   bool warp_ok = true;
   if (cmax_need <= 8) {
-    if (L == 4) { num_launch<4, 2>(f1, 512, A, B, row_scale, *C); num_launch<4, 2>(f2, 2048, A, B, row_scale, *C); }
-    else if (L == 8) { num_launch<8, 8>(f1, 512, A, B, row_scale, *C); num_launch<8, 8>(f2, 2048, A, B, row_scale, *C); }
-    else if (L == 16) { num_launch<16, 8>(f1, 512, A, B, row_scale, *C); num_launch<16, 8>(f2, 2048, A, B, row_scale, *C); }
-    else { num_launch<32, 8>(f1, 512, A, B, row_scale, *C); num_launch<32, 8>(f2, 2048, A, B, row_scale, *C); }
+    if (L == 4) { num_launch<4, 2>(f1, 512, A, B, row_scale, C); num_launch<4, 2>(f2, 2048, A, B, row_scale, C); }
+    else if (L == 8) { num_launch<8, 8>(f1, 512, A, B, row_scale, C); num_launch<8, 8>(f2, 2048, A, B, row_scale, C); }
+    else if (L == 16) { num_launch<16, 8>(f1, 512, A, B, row_scale, C); num_launch<16, 8>(f2, 2048, A, B, row_scale, C); }
+    else { num_launch<32, 8>(f1, 512, A, B, row_scale, C); num_launch<32, 8>(f2, 2048, A, B, row_scale, C); }
   } else if (cmax_need <= 16) {
-    if (L == 8) { num_launch<8, 16>(f1, 512, A, B, row_scale, *C); num_launch<8, 16>(f2, 2048, A, B, row_scale, *C); }
-    else if (L == 16) { num_launch<16, 16>(f1, 512, A, B, row_scale, *C); num_launch<16, 16>(f2, 2048, A, B, row_scale, *C); }
-    else { num_launch<32, 16>(f1, 512, A, B, row_scale, *C); num_launch<32, 16>(f2, 2048, A, B, row_scale, *C); }
+    if (L == 8) { num_launch<8, 16>(f1, 512, A, B, row_scale, C); num_launch<8, 16>(f2, 2048, A, B, row_scale, C); }
+    else if (L == 16) { num_launch<16, 16>(f1, 512, A, B, row_scale, C); num_launch<16, 16>(f2, 2048, A, B, row_scale, C); }
+    else { num_launch<32, 16>(f1, 512, A, B, row_scale, C); num_launch<32, 16>(f2, 2048, A, B, row_scale, C); }
   } else {
     warp_ok = false;
   }
-  RowBin n3 = warp_ok ? std::move(f3) : make_bin(m, len.p, 0, LLONG_MAX);
+  RowBin n3 = warp_ok ? std::move(f3) : make_bin(m, lensel, 0, LLONG_MAX);
   if (n3.n) {
     const size_t sm = size_t(SYM_BIG) * (sizeof(double) + sizeof(int));
     CF_CUDA(cudaFuncSetAttribute(k_num_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     k_num_cta<<<n3.n, 256, sm, stream()>>>(n3.list.p, n3.n, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p, B.col.p,
-                                           B.val.p, C->ptr.p, C->col.p, C->val.p);
+                                           B.val.p, C.ptr.p, C.col.p, C.val.p);
     CF_LAUNCHED();
+  }
+}
+
+
+std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale) {
+  if (A.cols != B.rows) fail(CF_ERR_LOGIC, "spgemm: inner dimensions differ");
+  const i64 m = A.rows;
+  i64 maxb = 0;
+  if (m > 0) {
+    DevBuf<unsigned long long> mx(1);
+    mx.zero();
+    k_max_row<<<int(std::min<i64>(1024, grid_for(B.rows, 256))), 256, 0, stream()>>>(B.rows, B.ptr.p, mx.p);
+    CF_LAUNCHED();
+    unsigned long long h = 0;
+    CF_CUDA(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    maxb = i64(h);
+  }
+  const int L = lanes_for(maxb);
+  // A/B and test switches: CF_SPGEMM_NOGROUP=1 row-wise only; CF_SPGEMM_GROUP_ALL=1 groups every
+  // product the grouped kernel can take (small matrices, short B rows, few shared patterns)
+  static const bool no_group = std::getenv("CF_SPGEMM_NOGROUP") != nullptr;
+  static const bool group_all = std::getenv("CF_SPGEMM_GROUP_ALL") != nullptr;
+  const bool try_group = group_all ? (m >= 1 && maxb >= 1) : (m >= 1024 && maxb > 16);
+  if (!no_group && try_group && maxb <= 256 && m < INT_MAX) {
+    // row groups, chunked to GRP_MAX rows
+    DevBuf<int> head(m), key(m), runstart(m);
+    k_same_prev<<<grid_for(m * 32, 256), 256, 0, stream()>>>(m, A.ptr.p, A.col.p, head.p);
+    CF_LAUNCHED();
+    k_head_key<<<grid_for(m, 256), 256, 0, stream()>>>(m, head.p, key.p);
+    CF_LAUNCHED();
+    {
+      size_t bytes = 0;
+      CF_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, key.p, runstart.p, cub::Max(), m, stream()));
+      DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+      CF_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, bytes, key.p, runstart.p, cub::Max(), m, stream()));
+      count_launch();
+    }
+    k_chunk_heads<<<grid_for(m, 256), 256, 0, stream()>>>(m, runstart.p, GRP_MAX, head.p);
+    CF_LAUNCHED();
+    DevBuf<int> heads(m), nsel(1);
+    {
+      size_t bytes = 0;
+      thrust::counting_iterator<int> it(0);
+      CF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, head.p, heads.p, nsel.p, m, stream()));
+      DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+      CF_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, head.p, heads.p, nsel.p, m, stream()));
+      count_launch();
+    }
+    const int ng = read_int(nsel.p);
+    if (group_all || double(ng) <= 0.6 * double(m)) {
+      key.release();
+      runstart.release();
+      head.release();
+      DevBuf<int> glen(ng);
+      k_group_len<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, heads.p, m, glen.p);
+      CF_LAUNCHED();
+      // symbolic on the head rows
+      Csr Ag;
+      Ag.rows = ng;
+      Ag.cols = A.cols;
+      Ag.ptr.alloc(ng + 1);
+      CF_CUDA(cudaMemsetAsync(Ag.ptr.p + ng, 0, sizeof(i64), stream()));
+      k_head_len<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, heads.p, A.ptr.p, Ag.ptr.p);
+      CF_LAUNCHED();
+      scan_excl(Ag.ptr.p, ng + 1);
+      Ag.nnz = read_i64(Ag.ptr.p + ng);
+      Ag.col.alloc(std::max<i64>(Ag.nnz, 1));
+      k_gather_rows<<<grid_for(i64(ng) * 32, 256), 256, 0, stream()>>>(ng, heads.p, A.ptr.p, A.col.p, Ag.ptr.p,
+                                                                      Ag.col.p);
+      CF_LAUNCHED();
+      auto Cg = spgemm_symbolic(Ag, B, L);
+      Ag.col.release();
+      // expand to the rows
+      auto C = std::make_unique<Csr>();
+      C->rows = m;
+      C->cols = B.cols;
+      C->ptr.alloc(m + 1);
+      CF_CUDA(cudaMemsetAsync(C->ptr.p + m, 0, sizeof(i64), stream()));
+      k_expand_len<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, heads.p, glen.p, Cg->ptr.p, C->ptr.p);
+      CF_LAUNCHED();
+      scan_excl(C->ptr.p, m + 1);
+      C->nnz = read_i64(C->ptr.p + m);
+      C->col.alloc(std::max<i64>(C->nnz, 1));
+      C->val.alloc(std::max<i64>(C->nnz, 1));
+      k_expand_cols<<<grid_for(i64(ng) * 32, 256), 256, 0, stream()>>>(ng, heads.p, glen.p, Cg->ptr.p, Cg->col.p,
+                                                                      C->ptr.p, C->col.p);
+      CF_LAUNCHED();
+      Cg.reset();
+      // numeric: groups binned by their row length (hash tiers); beyond 384 columns row-wise
+      DevBuf<i64> gl(ng);
+      k_group_clen<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, heads.p, C->ptr.p, gl.p);
+      CF_LAUNCHED();
+      const int caps[3] = {128, 256, 512};
+      const i64 lims[4] = {0, 96, 192, 384};
+      for (int t = 0; t < 3; ++t) {
+        RowBin b = make_bin(ng, gl.p, lims[t], lims[t + 1]);
+        if (maxb <= 32) num_grp_launch<1>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
+        else if (maxb <= 64) num_grp_launch<2>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
+        else if (maxb <= 128) num_grp_launch<4>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
+        else num_grp_launch<8>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
+      }
+      RowBin big = make_bin(ng, gl.p, 384, LLONG_MAX);
+      if (big.n) {
+        DevBuf<i64> sel(m);
+        CF_CUDA(cudaMemsetAsync(sel.p, 0, size_t(m) * sizeof(i64), stream()));
+        k_select_group_rows<<<grid_for(big.n, 256), 256, 0, stream()>>>(big.n, big.list.p, heads.p, glen.p, C->ptr.p,
+                                                                        sel.p);
+        CF_LAUNCHED();
+        spgemm_numeric(A, B, row_scale, *C, maxb, L, sel.p);
+      }
+      return C;
+    }
+  }
+  auto C = spgemm_symbolic(A, B, L);
+  if (m > 0) {
+    DevBuf<i64> len(m);
+    k_row_len<<<grid_for(m, 256), 256, 0, stream()>>>(m, C->ptr.p, len.p);
+    CF_LAUNCHED();
+    spgemm_numeric(A, B, row_scale, *C, maxb, L, len.p);
   }
   return C;
 }

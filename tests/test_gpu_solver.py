@@ -317,3 +317,41 @@ def test_amg_large_diagonal_coarsest(cf):
     assert h.n_levels() == 1
     r = np.random.default_rng(3).standard_normal(n)
     assert np.array_equal(h.v_cycle(r), r / d)
+
+
+def test_u_amg_3d_bit_exact(cf, orc):
+    """u-block hierarchy of a 3d Jacobian (16^3 mesh, rigid-body near-nullspace): the products run
+    through the row-group SpGEMM (rows of one node / one aggregate share their pattern) and must
+    reproduce the oracle's level operators bit for bit."""
+    P, O = cf.Problem(3, 10.0, 8, 1), orc.Problem(3, 10.0, 8, 1)
+    rng = np.random.default_rng(21)
+    x = np.zeros(P.n_total)
+    x[:P.n_u] = 1e-3 * rng.uniform(-1, 1, P.n_u)
+    x[P.n_u:] = rng.uniform(0.2, 1.0, P.n_phi)
+    pt = rng.uniform(0.2, 1.0, P.n_phi)
+    mat = cf.Material()
+    reg = cf.resolve_regularization(P, mat, cf.slit_band_edge(P, mat))
+    cs = cf.build_constraints(P)
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    u = J.M_uu
+    node = np.repeat(np.arange(P.n_vertices, dtype=np.int32), 3)
+    B = cf.rigid_body_modes(P, cs)
+    h = cf.build_amg(cf.CsrMatrix(u.rows, u.cols, u.ptr, u.col, u.val), node, B)
+    ho = orc.Amg(orc.Csr(u.rows, u.cols, u.ptr, u.col, u.val), node, B)
+    _assert_amg_equal(h, ho)
+    r = rng.uniform(-1, 1, P.n_u)
+    assert np.array_equal(h.v_cycle(r), ho.vcycle(r))
+
+
+def test_amg_grouped_spgemm_everywhere(cf):
+    """CF_SPGEMM_GROUP_ALL=1 sends every product the row-group kernel can take through it (tiny
+    matrices, single-row groups, runs chunked at 6 rows); the AMG parity tests must still pass."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CF_SPGEMM_GROUP_ALL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(root, "tests", "test_gpu_solver.py"),
+                        "-k", "amg and not everywhere or block_prec or penny"], env=env, capture_output=True, text=True,
+                       timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
