@@ -998,6 +998,43 @@ __global__ void k_dense_solve(int n, const double* __restrict__ a, const int* __
   }
 }
 
+// Shared-memory variant for small coarsest systems (n <= DENSE_SM_MAX): the factors are staged in
+// shared memory; the forward substitution runs column by column over all threads (each x_i still
+// receives its updates in ascending j with the same operands, so it is bitwise the row form above);
+// the backward substitution is the same serial loop, reading shared memory.
+constexpr int DENSE_SM_MAX = 128;
+__global__ void __launch_bounds__(256) k_dense_solve_sm(int n, const double* __restrict__ a,
+                                                        const int* __restrict__ piv, const double* __restrict__ b,
+                                                        double* __restrict__ x) {
+  extern __shared__ double dsm[];
+  double* A = dsm;      // n * n, column-major
+  double* X = dsm + n * n;
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) A[t] = a[t];
+  for (int t = threadIdx.x; t < n; t += blockDim.x) X[t] = b[t];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < n; ++k)
+      if (piv[k] != k) {
+        const double t = X[k];
+        X[k] = X[piv[k]];
+        X[piv[k]] = t;
+      }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double xj = X[j];
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) X[i] -= A[j * n + i] * xj;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int i = n - 1; i >= 0; --i) {
+      double xi = X[i];
+      for (int j = i + 1; j < n; ++j) xi -= A[j * n + i] * X[j];
+      X[i] = xi / A[i * n + i];
+    }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += blockDim.x) x[t] = X[t];
+}
+
 // ------------------------------------------------------------------ V-cycle pieces
 // x = w * (d .* b)
 __global__ void k_jacobi0(i64 n, double w, const double* __restrict__ d, const double* __restrict__ b,
@@ -1098,7 +1135,18 @@ void DenseLu::solve(const double* b, double* x) const {
     CF_LAUNCHED();
     return;
   }
-  k_dense_solve<<<1, 32, 0, stream()>>>(int(n), lu.p, piv.p, b, x);
+  if (n <= DENSE_SM_MAX) {
+    const size_t sm = size_t(n) * (n + 1) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      CF_CUDA(cudaFuncSetAttribute(k_dense_solve_sm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(size_t(DENSE_SM_MAX) * (DENSE_SM_MAX + 1) * sizeof(double))));
+      attr = true;
+    }
+    k_dense_solve_sm<<<1, 256, sm, stream()>>>(int(n), lu.p, piv.p, b, x);
+  } else {
+    k_dense_solve<<<1, 32, 0, stream()>>>(int(n), lu.p, piv.p, b, x);
+  }
   CF_LAUNCHED();
 }
 
