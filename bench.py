@@ -331,10 +331,30 @@ def vcycle_leg(cf, P, mat, reg, x_final, phi_old, stream):
     for name, h, n in (("u", hu, P.n_u), ("phi", hp, P.n_phi)):
         r = torch.randn(n, dtype=torch.float64, device=x_final.device)
         h.v_cycle(r)
-        out[name + "_ms"] = time_events(lambda: h.v_cycle(r), 10, stream)
+        ms = time_events(lambda: h.v_cycle(r), 10, stream)
+        nb = vcycle_bytes(h, stencil_level0=(name == "u"))
+        out[name + "_ms"] = ms
         out[name + "_levels"] = h.n_levels()
-    out["note"] = "one V-cycle application (zero initial guess, 1+1 damped Jacobi sweeps per level, dense LU on the coarsest)"
+        out[name + "_bytes"] = nb
+        out[name + "_gbs"] = nb / ms / 1e6
+    out["note"] = ("one V-cycle application (zero initial guess, 1+1 damped Jacobi sweeps per level, dense LU on the "
+                   "coarsest); bytes = per level 2 A applies (residual and post-sweep, fused with their vector "
+                   "updates) + R + P in their storage formats + 56 B per row of vector traffic")
     return out
+
+
+def vcycle_bytes(h, stencil_level0):
+    """Algorithmic bytes of one V-cycle: per non-coarsest level 2 SpMV(A) (the residual b - A x and the
+    fused post-smoothing sweep), SpMV(R), SpMV(P) with their x/y vectors, plus 56 B per row (pre-sweep
+    reads b, D^-1 and writes x: 24 B; the residual reads b, the prolongation reads x, the post-sweep
+    reads b and D^-1: 32 B)."""
+    tot = 0
+    for lev in range(h.n_levels() - 1):
+        i = h.level_info(lev)
+        n, nc = i["rows"], i["coarse"]
+        fa = stencil_bytes if (stencil_level0 and lev == 0) else csr_bytes
+        tot += 2 * fa(n, n, i["nnz_A"]) + csr_bytes(n, nc, i["nnz_P"]) + csr_bytes(nc, n, i["nnz_P"]) + 56 * n
+    return tot
 
 
 def rebuild_probe():

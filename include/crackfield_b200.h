@@ -200,6 +200,10 @@ int cf_amg_level_info(cf_amg h, int level, int64_t* info8, double* lambda, doubl
 int cf_amg_level_aggregates(cf_amg h, int level, int32_t* agg_of_node);
 /* Level operator (which 0: A, 1: P) as CSR. */
 int cf_amg_level_export(cf_amg h, int level, int which, int64_t* rowptr, int32_t* col, double* val);
+/* Tuning hook (not a reference interface): y = M x for a level operator (which 0: A, 1: P,
+ * 2: R = P^T) with an explicit kernel variant as in cf_tune_spmv (unroll 200 + U: the persistent
+ * pointer-prefetching kernel); threads_per_row 0 takes the production dispatch. */
+int cf_tune_level_spmv(cf_amg h, int level, int which, int threads_per_row, int unroll, const double* x, double* y);
 int cf_amg_destroy(cf_amg h);
 
 /* ------------------------------------------------------------------ block preconditioner */

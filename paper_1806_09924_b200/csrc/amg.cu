@@ -1456,8 +1456,12 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
   return h;
 }
 
-// linsolve.cpp:295-312, zero initial guess
+// linsolve.cpp:295-312, zero initial guess.  The residual r = b - A x and the post-smoothing sweep
+// x + w D^-1 (b - A x) are fused into the SpMV's row epilogue (SpmvEpi), the prolongation
+// x + P x_c lands in the level's scratch vector so the fused sweep can read it while writing x;
+// the same IEEE operations as the separate kernels (CF_VCYCLE_UNFUSED=1 runs those).
 void Amg::vcycle(const double* r, double* x) const {
+  static const bool unfused = std::getenv("CF_VCYCLE_UNFUSED") != nullptr;
   const double* b = r;
   for (size_t l = 0; l < levels.size(); ++l) {
     const AmgLevel& L = *levels[l];
@@ -1471,8 +1475,15 @@ void Amg::vcycle(const double* r, double* x) const {
       k_jacobi_upd<<<grid_for(n, 256), 256, 0, stream()>>>(n, w, L.inv_diag.p, b, L.tmp_r.p, xl);
       CF_LAUNCHED();
     }
-    csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
-    vsub(b, L.tmp_r.p, L.tmp_r.p, n);             // r = b - A x
+    if (unfused) {
+      csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
+      vsub(b, L.tmp_r.p, L.tmp_r.p, n);  // r = b - A x
+    } else {
+      SpmvEpi ep;
+      ep.b = b;
+      ep.mode = 1;
+      csr_spmv_epi(*L.A, xl, L.tmp_r.p, ep);  // r = b - A x
+    }
     csr_spmv_add(*L.R, L.tmp_r.p, L.tmp_b.p, nullptr);  // b_c = P^T r
     b = L.tmp_b.p;
   }
@@ -1485,8 +1496,20 @@ void Amg::vcycle(const double* r, double* x) const {
     const i64 n = L.A->rows;
     double* xl = (l == 0) ? x : levels[l - 1]->tmp_x.p;
     const double* bl = (l == 0) ? r : levels[l - 1]->tmp_b.p;
-    csr_spmv_add(*L.P, L.tmp_x.p, xl, xl);  // x += P x_c
-    for (int s = 0; s < opts.smoothing_sweeps; ++s) {
+    int s = 0;
+    if (unfused || opts.smoothing_sweeps < 1) {
+      csr_spmv_add(*L.P, L.tmp_x.p, xl, xl);  // x += P x_c
+    } else {
+      csr_spmv_add(*L.P, L.tmp_x.p, L.tmp_r.p, xl);  // t = x + P x_c
+      SpmvEpi ep;
+      ep.b = bl;
+      ep.d = L.inv_diag.p;
+      ep.w = L.jacobi_weight;
+      ep.mode = 2;
+      csr_spmv_epi(*L.A, L.tmp_r.p, xl, ep);  // x = t + w D^-1 (b - A t)
+      s = 1;
+    }
+    for (; s < opts.smoothing_sweeps; ++s) {
       csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
       k_jacobi_upd<<<grid_for(n, 256), 256, 0, stream()>>>(n, L.jacobi_weight, L.inv_diag.p, bl, L.tmp_r.p, xl);
       CF_LAUNCHED();

@@ -635,6 +635,21 @@ int cf_amg_level_export(cf_amg h, int level, int which, int64_t* rowptr, int32_t
   });
 }
 
+int cf_tune_level_spmv(cf_amg h, int level, int which, int threads_per_row, int unroll, const double* x, double* y) {
+  return guard([&] {
+    CHECK_ARG(h && x && y && level >= 0 && level < int(h->h->levels.size()) && which >= 0 && which <= 2,
+              "cf_tune_level_spmv: bad argument");
+    const AmgLevel& L = *h->h->levels[level];
+    const Csr& M = which == 0 ? *L.A : (which == 1 ? *L.P : *L.R);
+    InArg<double> xi(x, M.cols);
+    OutArg<double> yo(y, M.rows);
+    if (threads_per_row == 0) csr_spmv_add(M, xi.dev, yo.dev, nullptr);
+    else if (!csr_spmv_variant(M, threads_per_row, unroll, xi.dev, yo.dev))
+      fail(CF_ERR_INVALID_ARGUMENT, "cf_tune_level_spmv: unknown variant");
+    yo.finish();
+  });
+}
+
 int cf_amg_destroy(cf_amg h) {
   return guard([&] { delete h; });
 }

@@ -118,6 +118,16 @@ std::unique_ptr<BlockSystem> assemble_jacobian(Problem& P, const Constraints& c,
 // assemble_pattern (linsolve.cpp:417-476): BlockSparsity as CSR blocks with zero values
 std::unique_ptr<BlockSystem> assemble_pattern(const Problem& P, const Constraints& c);
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add);  // y = A x (+ add)
+// row epilogue of a fused SpMV (A square for modes 1 and 2; y must not alias x):
+//   0: y = A x (+ b)   1: y = b - A x (residual)   2: y = x + w (d (b - A x)) (one damped Jacobi sweep)
+// each mode is the same IEEE operation sequence as the SpMV followed by the separate vector kernel
+struct SpmvEpi {
+  const double* b = nullptr;
+  const double* d = nullptr;
+  double w = 0.0;
+  int mode = 0;
+};
+void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep);
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);
 bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double* y);

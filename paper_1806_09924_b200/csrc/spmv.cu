@@ -34,6 +34,12 @@ __device__ __forceinline__ double group_sum(double s) {
   return s;
 }
 
+__device__ __forceinline__ double epi_out(const SpmvEpi& ep, const double* __restrict__ x, i64 row, double s) {
+  if (ep.mode == 1) return ep.b[row] - s;
+  if (ep.mode == 2) return x[row] + ep.w * (ep.d[row] * (ep.b[row] - s));
+  return ep.b ? ep.b[row] + s : s;
+}
+
 template <int TPR>
 __device__ __forceinline__ double row_dot(const i64* __restrict__ ptr, const int* __restrict__ col,
                                           const double* __restrict__ val, const double* __restrict__ x, i64 row,
@@ -64,7 +70,7 @@ __global__ void __launch_bounds__(256) k_spmv(i64 rows, const i64* __restrict__ 
 template <int TPR, int U>
 __global__ void __launch_bounds__(256) k_spmv_b(i64 rows, const i64* __restrict__ ptr, const int* __restrict__ col,
                                                 const double* __restrict__ val, const double* __restrict__ x,
-                                                double* y, const double* add) {
+                                                double* y, SpmvEpi ep) {
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 row = t / TPR;
   const int lane = int(t % TPR);
@@ -88,7 +94,7 @@ __global__ void __launch_bounds__(256) k_spmv_b(i64 rows, const i64* __restrict_
     }
   }
   s = group_sum<TPR>(s);
-  if (row < rows && lane == 0) y[row] = add ? add[row] + s : s;
+  if (row < rows && lane == 0) y[row] = epi_out(ep, x, row, s);
 }
 
 template <int TPR, int U>
@@ -409,7 +415,7 @@ __device__ __forceinline__ double row_dot_b_emu(const i64* __restrict__ ptr, con
 template <int TPR, int PH, int U, int D>
 __global__ void __launch_bounds__(256) k_spmv_st_emu(i64 rows, const i64* __restrict__ ptr,
                                                      const double* __restrict__ val, const double* __restrict__ x,
-                                                     double* y, const double* add, StencilCols sc) {
+                                                     double* y, SpmvEpi ep, StencilCols sc) {
   __shared__ int off[StOff<D>::N];
   StOff<D>::fill(off, int(sc.nn));
   __syncthreads();
@@ -419,19 +425,22 @@ __global__ void __launch_bounds__(256) k_spmv_st_emu(i64 rows, const i64* __rest
   double s = 0.0;
   if (row < rows) s = row_dot_st_emu<TPR, PH, U, D>(ptr, val, x, row, t, sc, off);
   s = group_sum<PH>(s);
-  if (row < rows && t == 0) y[row] = add ? add[row] + s : s;
+  if (row < rows && t == 0) y[row] = epi_out(ep, x, row, s);
 }
 
 // persistent form: each 8-thread group walks rows g, g + G, ... and fetches the next row's
-// pointers before the current row's loads, so the row-pointer latency overlaps the value stream
+// pointers before the current row's loads, so the row-pointer latency overlaps the value stream.
+// The loop bound is warp-uniform (the warp's first group decides), so every lane reaches the
+// shuffles of group_sum; groups past the last row carry s = 0 and store nothing.
 __global__ void __launch_bounds__(256) k_spmv_st16p(i64 rows, const i64* __restrict__ ptr,
                                                     const double* __restrict__ val, const double* __restrict__ x,
-                                                    double* y, const double* add, StencilCols sc) {
+                                                    double* y, SpmvEpi ep, StencilCols sc) {
   __shared__ int off[StOff<3>::N];
   StOff<3>::fill(off, int(sc.nn));
   __syncthreads();
   const i64 G = (i64(gridDim.x) * blockDim.x) >> 3;
   const i64 g0 = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
+  const int gw = int((threadIdx.x & 31) >> 3);  // group within the warp
   const int t = int(threadIdx.x & 7);
   St16Regs o;
   o.init(t, int(sc.nn));
@@ -440,20 +449,70 @@ __global__ void __launch_bounds__(256) k_spmv_st16p(i64 rows, const i64* __restr
     b0 = ptr[g0];
     b1 = ptr[g0 + 1];
   }
-  for (i64 row = g0; row < rows; row += G) {
+  for (i64 row = g0; row - gw < rows; row += G) {
+    const bool act = row < rows;
     i64 n0 = 0, n1 = 0;
     if (row + G < rows) {
       n0 = ptr[row + G];
       n1 = ptr[row + G + 1];
     }
     const double* xb = nullptr;
-    double s;
-    if (st16_interior(sc, row, b1 - b0, x, xb)) s = row16_interior(val + b0, xb, t, o);
-    else s = row_dot_st_emu<16, 8, 1, 3>(ptr, val, x, row, t, sc, off);
+    double s = 0.0;
+    if (act) {
+      if (st16_interior(sc, row, b1 - b0, x, xb)) s = row16_interior(val + b0, xb, t, o);
+      else s = row_dot_st_emu<16, 8, 1, 3>(ptr, val, x, row, t, sc, off);
+    }
     s = group_sum<8>(s);
-    if (t == 0) y[row] = add ? add[row] + s : s;
+    if (act && t == 0) y[row] = epi_out(ep, x, row, s);
     b0 = n0;
     b1 = n1;
+  }
+}
+
+// Persistent CSR SpMV: TPR lanes per row, U batched (value, column) loads, rows g, g + G, ...
+// with the next row's pointers fetched ahead (the pointer -> value -> x chain otherwise costs
+// three dependent memory latencies per row).  Bitwise k_spmv_b<TPR, U> (same lanes, same order).
+template <int TPR, int U>
+__global__ void __launch_bounds__(256) k_spmv_pf(i64 rows, const i64* __restrict__ ptr, const int* __restrict__ col,
+                                                 const double* __restrict__ val, const double* __restrict__ x,
+                                                 double* y, SpmvEpi ep) {
+  constexpr int GPW = 32 / TPR;
+  const i64 G = (i64(gridDim.x) * blockDim.x) / TPR;
+  const i64 g0 = (i64(blockIdx.x) * blockDim.x + threadIdx.x) / TPR;
+  const int gw = int((threadIdx.x & 31) / TPR);
+  const int lane = int(threadIdx.x % TPR);
+  static_assert(GPW >= 1, "TPR <= 32");
+  i64 b = 0, e = 0;
+  if (g0 < rows) {
+    b = ptr[g0];
+    e = ptr[g0 + 1];
+  }
+  for (i64 row = g0; row - gw < rows; row += G) {
+    i64 nb = 0, ne = 0;
+    if (row + G < rows) {
+      nb = ptr[row + G];
+      ne = ptr[row + G + 1];
+    }
+    double s = 0.0;
+    for (i64 k0 = b + lane; k0 < e; k0 += i64(TPR) * U) {
+      double v[U], xv[U];
+      int c[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const i64 k = k0 + i64(j) * TPR;
+        const bool in = k < e;
+        v[j] = in ? ld_stream(val + k) : 0.0;
+        c[j] = in ? ld_stream(col + k) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+      for (int j = 0; j < U; ++j) s += v[j] * xv[j];
+    }
+    s = group_sum<TPR>(s);
+    if (row < rows && lane == 0) y[row] = epi_out(ep, x, row, s);
+    b = nb;
+    e = ne;
   }
 }
 
@@ -520,7 +579,7 @@ __global__ void __launch_bounds__(256) k_spmv_phi_st_emu(i64 rows, const i64* __
 // order, so the result is bitwise k_spmv_b's
 template <int TPR, int U, int D>
 __global__ void __launch_bounds__(256) k_spmv_st(i64 rows, const i64* __restrict__ ptr, const double* __restrict__ val,
-                                                 const double* __restrict__ x, double* y, const double* add,
+                                                 const double* __restrict__ x, double* y, SpmvEpi ep,
                                                  StencilCols sc) {
   __shared__ int off[StOff<D>::N];
   StOff<D>::fill(off, int(sc.nn));
@@ -531,7 +590,7 @@ __global__ void __launch_bounds__(256) k_spmv_st(i64 rows, const i64* __restrict
   double s = 0.0;
   if (row < rows) s = row_dot_st<TPR, U, D>(ptr, val, x, row, lane, sc, off);
   s = group_sum<TPR>(s);
-  if (row < rows && lane == 0) y[row] = add ? add[row] + s : s;
+  if (row < rows && lane == 0) y[row] = epi_out(ep, x, row, s);
 }
 
 template <int TPR, int U, int D>
@@ -629,26 +688,32 @@ void launch_phi(const BlockSystem& J, const double* x, double* y) {
   CF_LAUNCHED();
 }
 
-template <int TPR, int U>
-void launch_b(const Csr& A, const double* x, double* y, const double* add) {
+// PF: the persistent pointer-prefetching CSR kernel (k_spmv_pf) instead of k_spmv_b
+template <int TPR, int U, bool PF = false>
+void launch_b(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
   const int block = 256;
   const i64 threads = A.rows * TPR;
-  if (A.st.kind == 0)
-    k_spmv_b<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, add);
+  if (A.st.kind == 0 && PF) {
+    static int bps = 0;
+    if (!bps) CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_pf<TPR, U>, block, 0));
+    const int grid = int(std::min<i64>(grid_for(threads, block), i64(std::max(1, bps)) * rt().sm_count));
+    k_spmv_pf<TPR, U><<<grid, block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, ep);
+  } else if (A.st.kind == 0)
+    k_spmv_b<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, ep);
   else if (TPR == 16 && A.st.d == 3 && !st_emu_only()) {  // persistent, pointer prefetch
     static int bps = 0;
     if (!bps) CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_st16p, block, 0));
     const i64 want = grid_for(A.rows * 8, block);
     const int grid = int(std::min<i64>(want, i64(std::max(1, bps)) * rt().sm_count));
-    k_spmv_st16p<<<grid, block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, add, A.st);
+    k_spmv_st16p<<<grid, block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, ep, A.st);
   }
   else if (TPR == 16 && A.st.d == 3)  // 8 threads per row emulating the 16-lane reduction (sweep)
     k_spmv_st_emu<16, 8, 2, 3><<<grid_for(A.rows * 8, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y,
-                                                                                   add, A.st);
+                                                                                   ep, A.st);
   else if (A.st.d == 3)
-    k_spmv_st<TPR, U, 3><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, add, A.st);
+    k_spmv_st<TPR, U, 3><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, ep, A.st);
   else
-    k_spmv_st<TPR, U, 2><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, add, A.st);
+    k_spmv_st<TPR, U, 2><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, ep, A.st);
   CF_LAUNCHED();
 }
 
@@ -679,7 +744,7 @@ bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double
 #define CFB_E(P, U)                                                                                          \
   if (ph == P && u == U) {                                                                                   \
     k_spmv_st_emu<16, P, U, 3><<<grid_for(A.rows * P, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.val.p, x, y, \
-                                                                               nullptr, A.st);               \
+                                                                               SpmvEpi{}, A.st);             \
     CF_LAUNCHED();                                                                                           \
     return true;                                                                                             \
   }
@@ -687,12 +752,17 @@ bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double
 #undef CFB_E
     return false;
   }
-#define CFB_V(T, U) if (tpr == T && unroll == U) { launch_b<T, U>(A, x, y, nullptr); return true; }
+#define CFB_V(T, U) if (tpr == T && unroll == U) { launch_b<T, U>(A, x, y, SpmvEpi{}); return true; }
   CFB_V(32, 1) CFB_V(32, 2) CFB_V(32, 3) CFB_V(32, 4)
   CFB_V(16, 2) CFB_V(16, 4) CFB_V(16, 6)
   CFB_V(8, 4) CFB_V(8, 6) CFB_V(8, 11)
   CFB_V(4, 3) CFB_V(4, 4) CFB_V(4, 5)
 #undef CFB_V
+  // persistent pointer-prefetching CSR kernel: unroll = 200 + U
+#define CFB_P(T, U) if (tpr == T && unroll == 200 + U) { launch_b<T, U, true>(A, x, y, SpmvEpi{}); return true; }
+  CFB_P(32, 2) CFB_P(32, 4) CFB_P(16, 2) CFB_P(16, 4) CFB_P(16, 6) CFB_P(8, 2) CFB_P(8, 4) CFB_P(8, 6)
+  CFB_P(4, 3) CFB_P(4, 4) CFB_P(4, 5) CFB_P(4, 8)
+#undef CFB_P
   if (unroll == 0) {
     switch (tpr) {
       case 32: launch_spmv<32>(A, x, y, nullptr); return true;
@@ -706,13 +776,19 @@ bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double
 
 // Variant table from the B200 sweep (scripts/spmv_sweep.py, profiles/r01_spmv_sweep.json):
 // one batch of TPR*U slots should cover a typical row.
-void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add) {
+void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
   if (A.rows == 0) return;
   const double mean = A.mean_hint >= 0.0 ? A.mean_hint : double(A.nnz) / double(A.rows);
-  if (mean > 64) launch_b<16, 4>(A, x, y, add);
-  else if (mean > 24) launch_b<8, 4>(A, x, y, add);
-  else if (mean > 12) launch_b<4, 5>(A, x, y, add);
-  else launch_b<4, 3>(A, x, y, add);
+  if (mean > 64) launch_b<16, 4>(A, x, y, ep);
+  else if (mean > 24) launch_b<8, 4>(A, x, y, ep);
+  else if (mean > 12) launch_b<4, 5>(A, x, y, ep);
+  else launch_b<4, 3>(A, x, y, ep);
+}
+
+void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add) {
+  SpmvEpi ep;
+  ep.b = add;
+  csr_spmv_epi(A, x, y, ep);
 }
 
 void csr_spmv(const Csr& A, const double* x, double* y, double) { csr_spmv_add(A, x, y, nullptr); }
