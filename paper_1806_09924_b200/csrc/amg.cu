@@ -150,6 +150,15 @@ constexpr int SWARP_MIN = 320;  // nodes with more entries than this use the war
 // table in global memory (capacity = next pow2 >= 2 x their entry count); one thread per node
 // keeps the (row, column) accumulation order, then compacts and heap-sorts its keys.
 __device__ __forceinline__ unsigned hash_u(int k) { return unsigned(k) * 2654435761u; }
+// slot in a power-of-two table: the high bits of the Fibonacci product (the low bits collide for
+// clustered node ids); the tables are sets or per-key sums, so the slot function never changes a result
+__device__ __forceinline__ unsigned hslot_u(int k, unsigned mask) {
+#ifdef CF_LOWHASH
+  return hash_u(k) & mask;
+#else
+  return mask ? (hash_u(k) >> (32 - __popc(mask))) : 0u;
+#endif
+}
 
 __device__ void heap_sort_pairs(int* key, double* val, int n) {
   auto sift = [&](int start, int end) {
@@ -201,7 +210,7 @@ __global__ void k_strength_big(i64 nov, const int* __restrict__ list, const i64*
     for (i64 k = Ap[r]; k < Ap[r + 1]; ++k) {
       const int nj = nod[Ac[k]];
       const double a2 = Av[k] * Av[k];
-      unsigned s = hash_u(nj) & mask;
+      unsigned s = hslot_u(nj, mask);
       while (K[s] != -1 && K[s] != nj) s = (s + 1) & mask;
       if (K[s] == nj) {
         S[s] += a2;
@@ -252,7 +261,7 @@ __global__ void __launch_bounds__(SBW_WPB * 32)
         const int nj = nod[Ac[k]];
         const double x = Av[k];
         sbuf[w][lane] = x * x;
-        unsigned s = hash_u(nj) & mask;
+        unsigned s = hslot_u(nj, mask);
         for (unsigned p = 0; p < cap; ++p) {
           int cur = K[s];
           if (cur == -1) cur = atomicCAS(&K[s], -1, nj);
@@ -441,7 +450,7 @@ __global__ void k_n2_cap(i64 nov, const int* __restrict__ list, const i64* __res
 }
 
 __device__ __forceinline__ void set_insert(int* K, unsigned mask, int v) {
-  unsigned s = hash_u(v) & mask;
+  unsigned s = hslot_u(v, mask);
   while (K[s] != -1 && K[s] != v) s = (s + 1) & mask;
   K[s] = v;
 }
@@ -508,7 +517,7 @@ __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restric
   const unsigned mask = N2CAP - 1;
   bool full = false;
   auto ins = [&](int v) {
-    unsigned s = hash_u(v) & mask;
+    unsigned s = hslot_u(v, mask);
     for (int p = 0; p < N2CAP; ++p) {
       const int cur = T[s];
       if (cur == v) return;

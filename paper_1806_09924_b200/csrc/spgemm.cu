@@ -26,7 +26,17 @@ namespace {
 
 constexpr int EMPTY = -1;
 
-__device__ __forceinline__ unsigned hslot(int key, unsigned mask) { return (unsigned(key) * 2654435761u) & mask; }
+// Fibonacci hashing: the HIGH bits of the product (the low bits of key * odd only permute the
+// residues of key mod cap, so clustered keys - the coarse dofs of neighbouring aggregates -
+// collide in runs).  mask = cap - 1 with cap a power of two (-DCF_LOWHASH: the low-bit form, A/B).
+__device__ __forceinline__ unsigned hslot(int key, unsigned mask) {
+  const unsigned h = unsigned(key) * 2654435761u;
+#ifdef CF_LOWHASH
+  return h & mask;
+#else
+  return mask ? (h >> (32 - __popc(mask))) : 0u;
+#endif
+}
 
 // insert key; returns 1 if newly inserted, 0 if present, -1 if the table is full (bounded
 // probing: a full table can never hang the kernel)
