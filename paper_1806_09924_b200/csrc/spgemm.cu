@@ -618,6 +618,62 @@ constexpr int GRP_MAX = 6;  // rows per group (longer runs are chunked)
 // the entries of B row k (CB per lane), find each slot once and apply it to every row of the group.
 // Within one k the slots are distinct, so no two lanes touch one accumulator; __syncwarp orders
 // successive k.  The next k's B row and A values are loaded while the current one is applied.
+// The position loop is instantiated per group size NR (a warp-uniform switch), and the per-lane
+// entry loop stops at the row's length, so no predicated-off row or entry slots are issued.
+template <int CB, int NR>
+__device__ __forceinline__ void num_grp_rows(double* __restrict__ Acc, const int* __restrict__ T, unsigned mask,
+                                             int cap, int row0, int lane, const i64* __restrict__ ap,
+                                             const int* __restrict__ ac, const double* __restrict__ av,
+                                             const double* __restrict__ rs, const i64* __restrict__ bp,
+                                             const int* __restrict__ bc, const double* __restrict__ bv) {
+  double si[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) si[r] = rs ? rs[row0 + r] : 1.0;
+  const i64 a0 = ap[row0];
+  const int alen = int(ap[row0 + 1] - a0);
+  int ck[CB], nk[CB];
+  double cb[CB], nb[CB], ca[NR], na[NR];
+  int cn = 0, nn = 0;
+  auto load = [&](int pos, int* kc, double* kv, double* ka, int& n) {
+    const int k = ac[a0 + pos];
+    const i64 q0 = bp[k];
+    n = int(bp[k + 1] - q0);
+#pragma unroll
+    for (int t = 0; t < CB; ++t) {
+      const int e = t * 32 + lane;
+      if (e < n) {
+        kc[t] = bc[q0 + e];
+        kv[t] = bv[q0 + e];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) ka[r] = rs ? si[r] * av[a0 + i64(r) * alen + pos] : av[a0 + i64(r) * alen + pos];
+  };
+  if (alen > 0) load(0, ck, cb, ca, cn);
+  for (int pos = 0; pos < alen; ++pos) {
+    if (pos + 1 < alen) load(pos + 1, nk, nb, na, nn);
+#pragma unroll
+    for (int t = 0; t < CB; ++t) {
+      if (t * 32 >= cn) break;  // warp-uniform
+      const int e = t * 32 + lane;
+      if (e < cn) {
+        const int sl = hfind(T, mask, ck[t]);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) Acc[size_t(r) * cap + sl] += ca[r] * cb[t];
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < CB; ++t) {
+      ck[t] = nk[t];
+      cb[t] = nb[t];
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) ca[r] = na[r];
+    cn = nn;
+  }
+}
+
 template <int CB>
 __global__ void __launch_bounds__(256) k_num_grp(const int* __restrict__ glist, int ng, const int* __restrict__ heads,
                                                  const int* __restrict__ glen, int cap, int wpb,
@@ -642,52 +698,11 @@ __global__ void __launch_bounds__(256) k_num_grp(const int* __restrict__ glist, 
   const int nc = int(cp[row0 + 1] - c0);
   for (int t = lane; t < nc; t += 32) hinsert(T, mask, cc[c0 + t]);
   __syncwarp();
-  double si[GRP_MAX];
-#pragma unroll
-  for (int r = 0; r < GRP_MAX; ++r) si[r] = (r < nr && rs) ? rs[row0 + r] : 1.0;
-  const i64 a0 = ap[row0];
-  const int alen = int(ap[row0 + 1] - a0);
-  int ck[CB], nk[CB];
-  double cb[CB], nb[CB], ca[GRP_MAX], na[GRP_MAX];
-  int cn = 0, nn = 0;
-  auto load = [&](int pos, int* kc, double* kv, double* ka, int& n) {
-    const int k = ac[a0 + pos];
-    const i64 q0 = bp[k];
-    n = int(bp[k + 1] - q0);
-#pragma unroll
-    for (int t = 0; t < CB; ++t) {
-      const int e = t * 32 + lane;
-      if (e < n) {
-        kc[t] = bc[q0 + e];
-        kv[t] = bv[q0 + e];
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < GRP_MAX; ++r)
-      if (r < nr) ka[r] = rs ? si[r] * av[a0 + i64(r) * alen + pos] : av[a0 + i64(r) * alen + pos];
-  };
-  if (alen > 0) load(0, ck, cb, ca, cn);
-  for (int pos = 0; pos < alen; ++pos) {
-    if (pos + 1 < alen) load(pos + 1, nk, nb, na, nn);
-#pragma unroll
-    for (int t = 0; t < CB; ++t) {
-      const int e = t * 32 + lane;
-      if (e < cn) {
-        const int sl = hfind(T, mask, ck[t]);
-#pragma unroll
-        for (int r = 0; r < GRP_MAX; ++r)
-          if (r < nr) Acc[size_t(r) * cap + sl] += ca[r] * cb[t];
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int t = 0; t < CB; ++t) {
-      ck[t] = nk[t];
-      cb[t] = nb[t];
-    }
-#pragma unroll
-    for (int r = 0; r < GRP_MAX; ++r) ca[r] = na[r];
-    cn = nn;
+  switch (nr) {
+#define CFB_NR(R) \
+  case R: num_grp_rows<CB, R>(Acc, T, mask, cap, row0, lane, ap, ac, av, rs, bp, bc, bv); break;
+    CFB_NR(1) CFB_NR(2) CFB_NR(3) CFB_NR(4) CFB_NR(5) CFB_NR(6)
+#undef CFB_NR
   }
   for (int t = lane; t < nc; t += 32) {
     const int sl = hfind(T, mask, cc[c0 + t]);
