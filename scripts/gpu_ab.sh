@@ -1,4 +1,2 @@
-for i in 1 2; do
-timeout 600 python scripts/amg_build_ab.py 2>&1 | grep hierarchy | sed 's/^/new /'
-CF_LIB_PATH=build_ab/lib_head.so timeout 600 python scripts/amg_build_ab.py 2>&1 | grep hierarchy | sed 's/^/head /'
-done
+timeout 600 python scripts/residual_ab.py 2>&1 | grep residual
+CF_LIB_PATH=build_ab/lib_plaindiv.so timeout 600 python scripts/residual_ab.py 2>&1 | grep residual
