@@ -170,6 +170,9 @@ int cf_block_destroy(cf_block b);
 /* Tuning hook (not a reference interface): one block times a vector with an explicit kernel
  * variant (threads per row in {4,8,16,32}; unroll 0 = plain loop, else batched loads). */
 int cf_tune_spmv(cf_block b, int which, int threads_per_row, int unroll, const double* x, double* y);
+/* Test hook (not a reference interface): q[i] = a[i] / h through the residual kernel's division by
+ * the cell size (reciprocal + two Markstein corrections); must equal the IEEE quotient bit for bit. */
+int cf_test_div_by(double h, const double* a, int64_t n, double* q);
 
 /* ------------------------------------------------------------------ generic CSR operators */
 typedef struct cf_csr_s* cf_csr;   /* CsrMatrix (types.hpp:12) on the device */

@@ -126,6 +126,7 @@ SIGNATURES = [
     ("cf_block_destroy", _I, [_P]),
     ("cf_tune_spmv", _I, [_P, _I, _I, _I, _P, _P]),
     ("cf_tune_level_spmv", _I, [_P, _I, _I, _I, _I, _P, _P]),
+    ("cf_test_div_by", _I, [C.c_double, _P, C.c_int64, _P]),
     ("cf_csr_create", _I, [_L, _L, _P, _P, _P, C.POINTER(_P)]),
     ("cf_block_csr", _I, [_P, _I, C.POINTER(_P)]),
     ("cf_csr_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),

@@ -106,6 +106,38 @@ struct Coef {
 // shuffles; each lane evaluates its point's state and its contribution to every (k, a); the
 // contributions are then folded in q order (0.0 + c_0 + c_1 + ...) — exactly the reference's
 // `ru[k*d+a] += w * val` sequence over q — and lane k keeps corner k's sums.
+// a / h for the fixed cell size h > 0 (the reference divides every shape-gradient product by h,
+// model.cpp; the oracle and this kernel keep that IEEE operation).  y = RN(1/h) once per thread,
+// then q = RN(a y) refined by two Markstein corrections q += (a - q h) y (exact remainders by FMA):
+// the first leaves q faithful, the second, with y the correctly rounded reciprocal, gives the
+// correctly rounded quotient RN(a / h) (Markstein's theorem).  Zero, tiny and huge dividends
+// take the IEEE division (0 / h = 0 with a's sign).  Five dependent FP64 operations instead of the
+// division's reciprocal refinement per quotient; bitwise a / h (tests/test_gpu_assembly.py,
+// test_div_by_h_is_ieee_division).
+struct DivBy {
+  double h, y;
+  __device__ explicit DivBy(double h_) : h(h_), y(1.0 / h_) {}
+  __device__ __forceinline__ double div(double a) const {
+#ifdef CF_PLAIN_DIV
+    return a / h;
+#else
+    const double m = fabs(a);
+    if (m == 0.0) return a;
+    if (!(m >= 0x1p-900 && m <= 0x1p900)) return a / h;
+    double q = a * y;
+    double r = __fma_rn(-q, h, a);
+    q = __fma_rn(r, y, q);
+    r = __fma_rn(-q, h, a);
+    return __fma_rn(r, y, q);
+#endif
+  }
+};
+
+__global__ void k_div_by(double h, const double* __restrict__ a, i64 n, double* __restrict__ q) {
+  const DivBy dv(h);
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) q[i] = dv.div(a[i]);
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Tables* __restrict__ T, Coef cf,
                                                          const double* __restrict__ sol,
@@ -136,7 +168,7 @@ __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Table
     my_phi = sol[nu + v];
     my_pt = ptil[v];
   }
-  const double h = g.h;
+  const DivBy dv(g.h);
   double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   double gphi[3] = {0, 0, 0};
   double phi = 0.0, pt = 0.0;
@@ -153,9 +185,9 @@ __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Table
 #pragma unroll
     for (int b = 0; b < D; ++b) {
       const double Gkb = sG[q][k][b];
-      gphi[b] += phik * Gkb / h;
+      gphi[b] += dv.div(phik * Gkb);
 #pragma unroll
-      for (int a = 0; a < D; ++a) gu[a][b] += uk[a] * Gkb / h;
+      for (int a = 0; a < D; ++a) gu[a][b] += dv.div(uk[a] * Gkb);
     }
   }
   double e[3][3], sig[3][3];
@@ -189,13 +221,13 @@ __global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Table
     for (int a = 0; a < D; ++a) {
       double val = 0.0;
 #pragma unroll
-      for (int b = 0; b < D; ++b) val += gcoef * sig[a][b] * sG[q][k][b] / h;
-      val += pphi * cf.p * sG[q][k][a] / h;
+      for (int b = 0; b < D; ++b) val += dv.div(gcoef * sig[a][b] * sG[q][k][b]);
+      val += dv.div(pphi * cf.p * sG[q][k][a]);
       contrib[a] = w * val;
     }
     double vphi = ((1.0 - cf.kap) * phi * sig_ee + 2.0 * phi * cf.p * tre - cf.Gc / cf.eps * (1.0 - phi)) * sS[q][k];
 #pragma unroll
-    for (int b = 0; b < D; ++b) vphi += cf.Gc * cf.eps * gphi[b] * sG[q][k][b] / h;
+    for (int b = 0; b < D; ++b) vphi += dv.div(cf.Gc * cf.eps * gphi[b] * sG[q][k][b]);
     contrib[D] = w * vphi;
 #pragma unroll
     for (int a = 0; a <= D; ++a) {
@@ -1070,6 +1102,13 @@ std::unique_ptr<BlockSystem> assemble_pattern(const Problem& P, const Constraint
   else
     pattern_impl<3>(P, cs, *J);
   return J;
+}
+
+// test hook: q = a / h through the residual kernel's division (DivBy)
+void div_by_h(double h, const double* a, i64 n, double* q) {
+  if (n <= 0) return;
+  k_div_by<<<int(std::min<i64>(grid_for(n, 256), 148 * 16)), 256, 0, stream()>>>(h, a, n, q);
+  CF_LAUNCHED();
 }
 
 }  // namespace cfb

@@ -465,6 +465,16 @@ int cf_block_spmv(cf_block b, int which, const double* x, double* y) {
   });
 }
 
+int cf_test_div_by(double h, const double* a, int64_t n, double* q) {
+  return guard([&] {
+    CHECK_ARG(a && q && n >= 0 && h > 0.0, "cf_test_div_by: bad argument");
+    InArg<double> ai(a, n);
+    OutArg<double> qo(q, n);
+    div_by_h(h, ai.dev, n, qo.dev);
+    qo.finish();
+  });
+}
+
 int cf_tune_spmv(cf_block b, int which, int threads_per_row, int unroll, const double* x, double* y) {
   return guard([&] {
     CHECK_ARG(b && x && y && which >= 0 && which <= 2, "cf_tune_spmv: bad argument");

@@ -131,7 +131,8 @@ void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep);
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);
 bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double* y);
-bool csr_enable_stencil(Csr& A, const StencilCols& sc);  // CF_NO_STENCIL_COLS=1 disables
+bool csr_enable_stencil(Csr& A, const StencilCols& sc);
+void div_by_h(double h, const double* a, i64 n, double* q);  // test hook of the residual's a / h  // CF_NO_STENCIL_COLS=1 disables
 
 inline double mat_mu(const cf_material& m) { return m.E / (2.0 * (1.0 + m.nu)); }              // model.hpp:26
 inline double mat_lambda(const cf_material& m) {                                                  // model.hpp:27

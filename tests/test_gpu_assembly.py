@@ -287,3 +287,26 @@ def test_matrix_free_apply_equals_assembled(cf, d, n0, r, clamp):
     ref = J.spmv(0, u)
     got = cf.mf_apply_uu(P, cs, mat, reg, pt, u)
     assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("h", [20.0 / 256, 20.0 / 128, 20.0 / 2048, 20.0 / 192, 2.0 / 16, 10.0 / 40, 0.3, 1.0 / 3.0])
+def test_div_by_h_is_ieee_division(cf, h):
+    """The residual kernel divides every gradient product by the cell size h through a reciprocal
+    and two Markstein corrections (assembly.cu DivBy); it must be the IEEE quotient a / h bit for bit:
+    4M random dividends over 2^-70..2^70 of both signs, mantissas uniform, plus zeros, subnormals,
+    extreme exponents, infinities and NaN."""
+    import ctypes as C
+    from paper_1806_09924_b200._lib import check, load
+    rng = np.random.default_rng(int(h * 1e6))
+    n = 1 << 22
+    a = rng.uniform(1.0, 2.0, n) * np.exp2(rng.integers(-70, 71, n)) * rng.choice([-1.0, 1.0], n)
+    # products of shape-gradient-like factors, as in the kernel
+    a[: n // 4] = rng.normal(size=n // 4) * rng.uniform(-0.8, 0.8, n // 4)
+    special = np.array([0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, 1e-300, 1e300, 1.7976931348623157e308,
+                        np.inf, -np.inf, np.nan, 2.0 ** -900, 2.0 ** 900, h, -h, 2 * h, h / 3])
+    a[: special.size] = special
+    q = np.empty_like(a)
+    check(load().cf_test_div_by(C.c_double(h), a.ctypes.data_as(C.c_void_p), C.c_int64(n), q.ctypes.data_as(C.c_void_p)))
+    ref = a / h
+    same = (q.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(q) & np.isnan(ref))
+    assert same.all(), f"{(~same).sum()} quotients differ, e.g. a={a[~same][:3]} q={q[~same][:3]} ref={ref[~same][:3]}"
