@@ -468,10 +468,11 @@ __global__ void k_jac_count(GridDesc g, const Tables* __restrict__ T, Coef cf, c
 template <int D>
 constexpr int pair_wpb() { return 4; }
 
-template <int D>
-struct PairSmem {
+template <int D, bool UU>
+struct PairSmem {  // the M_uu integrand table only when M_uu is filled (smaller footprint, more blocks)
   static constexpr int NQ = 1 << D, NV = 1 << D, NR = D * D + D + 1;
-  double val[NQ][NV][NV][D * D];
+  static constexpr int TQ = UU ? NQ : 1, TV = UU ? NV : 1, TD = UU ? D * D : 1;
+  double val[TQ][TV][TV][TD];
   double s[NQ][NV], gp[NQ][NV][D], gg[NQ][NV][NV], w[NQ];
   double res[pair_wpb<D>()][32][NR];
 };
@@ -486,10 +487,12 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
   constexpr int S = (D == 3) ? 27 : 9, NQ = 1 << D, NV = 1 << D, NC = 1 << D, NS = QS<D>::NS, CS = NQ * NS;
   constexpr int NR = D * D + D + 1, CPR = 32 / NV, ROUNDS = (NC + CPR - 1) / CPR;
   extern __shared__ __align__(16) unsigned char smraw[];
-  PairSmem<D>& sm = *reinterpret_cast<PairSmem<D>*>(smraw);
-  for (int i = threadIdx.x; i < NQ * NV * NV * D * D; i += blockDim.x) {
-    const int ab = i % (D * D), l = (i / (D * D)) % NV, k = (i / (D * D * NV)) % NV, q = i / (D * D * NV * NV);
-    sm.val[q][k][l][ab] = T->val[q][k][l][ab / D][ab % D];
+  PairSmem<D, UU>& sm = *reinterpret_cast<PairSmem<D, UU>*>(smraw);
+  if constexpr (UU) {
+    for (int i = threadIdx.x; i < NQ * NV * NV * D * D; i += blockDim.x) {
+      const int ab = i % (D * D), l = (i / (D * D)) % NV, k = (i / (D * D * NV)) % NV, q = i / (D * D * NV * NV);
+      sm.val[q][k][l][ab] = T->val[q][k][l][ab / D][ab % D];
+    }
   }
   for (int i = threadIdx.x; i < NQ * NV; i += blockDim.x) {
     const int q = i / NV, k = i % NV;
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
           double gl[D];
 #pragma unroll
           for (int b = 0; b < D; ++b) gl[b] = sm.gp[q][l][b];
-          if (UU) {
+          if constexpr (UU) {
             const double wg = __ldg(st);
             const double* vl = sm.val[q][k][l];
 #pragma unroll
@@ -1024,7 +1027,7 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   J.pp->val.alloc(nnz[2]);
   int bps = 0;
   constexpr int FT = pair_wpb<D>() * 32;
-  const int smem = int(sizeof(PairSmem<D>));
+  const int smem = with_uu ? int(sizeof(PairSmem<D, true>)) : int(sizeof(PairSmem<D, false>));
   auto kern = with_uu ? k_jac_fill_pair<D, true> : k_jac_fill_pair<D, false>;
   CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, FT, smem));
