@@ -408,6 +408,119 @@ __global__ void __launch_bounds__(256) k_num_cta(const int* __restrict__ rowlist
   for (int t = threadIdx.x; t < nc; t += blockDim.x) cv[c0 + t] = acc[t];
 }
 
+// numeric, CTA per row for products with few, long rows (the coarse levels' P^T (A P): a few
+// hundred output rows of B rows with hundreds of entries, too few rows to occupy the GPU one warp
+// each).  As k_num_cta, with the entries of B row k+1 (E per thread) loaded while row k is applied
+// and shared memory sized to the longest output row, so several CTAs share an SM.
+template <int E>
+__global__ void __launch_bounds__(256) k_num_cta_pf(const int* __restrict__ rowlist, i64 nrows,
+                                                    const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                    const double* __restrict__ av, const double* __restrict__ rs,
+                                                    const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                    const double* __restrict__ bv, const i64* __restrict__ cp,
+                                                    const int* __restrict__ cc, double* __restrict__ cv) {
+  extern __shared__ unsigned char smraw[];
+  const i64 r = blockIdx.x;
+  if (r >= nrows) return;
+  const i64 i = rowlist ? rowlist[r] : r;
+  const i64 c0 = cp[i];
+  const int nc = int(cp[i + 1] - c0);
+  double* acc = reinterpret_cast<double*>(smraw);
+  int* cols = reinterpret_cast<int*>(acc + nc);
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+    cols[t] = cc[c0 + t];
+    acc[t] = 0.0;
+  }
+  __syncthreads();
+  const double si = rs ? rs[i] : 1.0;
+  const i64 a0 = ap[i], a1 = ap[i + 1];
+  int cb[E], nb[E];
+  double vb[E], wb[E], ca = 0.0, na = 0.0;
+  auto load = [&](i64 ka, int* kc, double* kv, double& a) {
+    const int k = ac[ka];
+    a = rs ? si * av[ka] : av[ka];
+    const i64 q0 = bp[k], q1 = bp[k + 1];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const i64 q = q0 + threadIdx.x + i64(e) * blockDim.x;
+      kc[e] = q < q1 ? bc[q] : -1;
+      kv[e] = q < q1 ? bv[q] : 0.0;
+    }
+  };
+  if (a0 < a1) load(a0, cb, vb, ca);
+  for (i64 ka = a0; ka < a1; ++ka) {
+    if (ka + 1 < a1) load(ka + 1, nb, wb, na);
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (cb[e] >= 0) {
+        const int pos = lower_bound_sm(cols, nc, cb[e]);
+        acc[pos] += ca * vb[e];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      cb[e] = nb[e];
+      vb[e] = wb[e];
+    }
+    ca = na;
+  }
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) cv[c0 + t] = acc[t];
+}
+
+// symbolic, CTA per row with one byte flag per output column (columns < FLAG_MAX): the row's B
+// rows set their flags (benign identical writes, no atomics), then MODE 0 counts them and MODE 1
+// writes the set columns in ascending order (a block scan over contiguous column ranges).
+constexpr int FLAG_MAX = 96 * 1024;
+template <int MODE>
+__global__ void __launch_bounds__(256) k_sym_flags(i64 rows, const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                   const i64* __restrict__ bp, const int* __restrict__ bc, int ncols,
+                                                   i64* __restrict__ cnt_or_ptr, int* __restrict__ ccol) {
+  extern __shared__ unsigned char flg[];
+  __shared__ int part[256];
+  const i64 i = blockIdx.x;
+  if (i >= rows) return;
+  for (int t = threadIdx.x; t < ncols; t += blockDim.x) flg[t] = 0;
+  __syncthreads();
+  for (i64 ka = ap[i]; ka < ap[i + 1]; ++ka) {
+    const int k = ac[ka];
+    for (i64 q = bp[k] + threadIdx.x; q < bp[k + 1]; q += blockDim.x) flg[bc[q]] = 1;
+  }
+  __syncthreads();
+  const int chunk = (ncols + blockDim.x - 1) / blockDim.x;
+  const int lo = min(ncols, int(threadIdx.x) * chunk), hi = min(ncols, lo + chunk);
+  int c = 0;
+  for (int t = lo; t < hi; ++t) c += flg[t];
+  part[threadIdx.x] = c;
+  __syncthreads();
+  if (MODE == 0) {
+    if (threadIdx.x == 0) {
+      int s = 0;
+      for (int t = 0; t < int(blockDim.x); ++t) s += part[t];
+      cnt_or_ptr[i] = s;
+    }
+    return;
+  }
+  // exclusive scan of the per-thread counts (256 values, one warp of partial sums)
+  if (threadIdx.x < 32) {
+    int run = 0;
+    for (int w = 0; w < 8; ++w) {
+      const int t = w * 32 + int(threadIdx.x);
+      const int v = part[t];
+      int incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (threadIdx.x >= o) incl += n;
+      }
+      part[t] = run + incl - v;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  __syncthreads();
+  i64 o = cnt_or_ptr[i] + part[threadIdx.x];
+  for (int t = lo; t < hi; ++t)
+    if (flg[t]) ccol[o++] = t;
+}
+
 // partition rows by a predicate on a per-row value (order within a bin is irrelevant: every
 // listed row is processed independently)
 __global__ void k_bin_rows(i64 rows, const i64* __restrict__ v, i64 lo, i64 hi, int* __restrict__ list,
@@ -732,7 +845,7 @@ __global__ void k_group_clen(int ng, const int* __restrict__ heads, const i64* _
 }  // namespace
 
 // pattern of C = A B (sorted columns; values allocated, not computed); L lanes per B row
-static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L) {
+static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L, i64 maxb) {
   auto C = std::make_unique<Csr>();
   C->rows = A.rows;
   C->cols = B.cols;
@@ -741,6 +854,23 @@ static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L) {
   const i64 m = A.rows;
   if (m == 0) return C;
   i64* cnt = C->ptr.p;  // row counts in place, scanned into offsets afterwards
+  // few rows into a narrow column space (coarse-level products): CTA per row, byte flags
+  static const bool no_flags = std::getenv("CF_SPGEMM_NO_FLAGS") != nullptr;
+  if (!no_flags && m <= 32768 && B.cols <= FLAG_MAX && maxb >= 64) {
+    const size_t sm = size_t(B.cols) + 16;
+    CF_CUDA(cudaFuncSetAttribute(k_sym_flags<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    k_sym_flags<0><<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), cnt, nullptr);
+    CF_LAUNCHED();
+    scan_excl(C->ptr.p, m + 1);
+    C->nnz = read_i64(C->ptr.p + m);
+    C->col.alloc(std::max<i64>(C->nnz, 1));
+    C->val.alloc(std::max<i64>(C->nnz, 1));
+    CF_CUDA(cudaFuncSetAttribute(k_sym_flags<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    k_sym_flags<1><<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
+                                                  C->col.p);
+    CF_LAUNCHED();
+    return C;
+  }
   // 1. symbolic count: all rows with products try the 512-slot tier, which also spills its
   //    unsorted unique columns (<= 384 per row) to scratch; overflow -> 2048 -> CTA tiers
   DevBuf<i64> soff(m + 1);
@@ -831,6 +961,33 @@ static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L) {
 static void spgemm_numeric(const Csr& A, const Csr& B, const double* row_scale, Csr& C, i64 maxb, int L,
                            const i64* lensel) {
   const i64 m = A.rows;
+  // few rows of long B rows (coarse-level RAP): one CTA per row, B rows prefetched
+  static const bool no_cta_pf = std::getenv("CF_SPGEMM_NO_CTA_PF") != nullptr;
+  if (!no_cta_pf && m > 0 && m <= 32768 && maxb >= 128 && maxb <= 1024) {
+    RowBin all = make_bin(m, lensel, 1, LLONG_MAX);
+    if (all.n) {
+      DevBuf<unsigned long long> mx(1);
+      mx.zero();
+      k_max_row<<<int(std::min<i64>(1024, grid_for(m, 256))), 256, 0, stream()>>>(m, C.ptr.p, mx.p);
+      CF_LAUNCHED();
+      const i64 ncmax = read_i64(reinterpret_cast<const i64*>(mx.p));
+      if (ncmax <= SYM_BIG) {
+        const size_t sm = size_t(ncmax) * (sizeof(double) + sizeof(int)) + 16;
+        auto launch = [&](auto kern) {
+          CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+          kern<<<all.n, 256, sm, stream()>>>(all.list.p, all.n, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p,
+                                             B.col.p, B.val.p, C.ptr.p, C.col.p, C.val.p);
+          CF_LAUNCHED();
+        };
+        if (maxb <= 256) launch(k_num_cta_pf<1>);
+        else if (maxb <= 512) launch(k_num_cta_pf<2>);
+        else launch(k_num_cta_pf<4>);
+        return;
+      }
+    } else {
+      return;
+    }
+  }
   RowBin f1 = make_bin(m, lensel, 0, 256);
   RowBin f2 = make_bin(m, lensel, 256, 1024);
   RowBin f3 = make_bin(m, lensel, 1024, LLONG_MAX);
@@ -926,7 +1083,7 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
       k_gather_rows<<<grid_for(i64(ng) * 32, 256), 256, 0, stream()>>>(ng, heads.p, A.ptr.p, A.col.p, Ag.ptr.p,
                                                                       Ag.col.p);
       CF_LAUNCHED();
-      auto Cg = spgemm_symbolic(Ag, B, L);
+      auto Cg = spgemm_symbolic(Ag, B, L, maxb);
       Ag.col.release();
       // expand to the rows
       auto C = std::make_unique<Csr>();
@@ -969,7 +1126,7 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
       return C;
     }
   }
-  auto C = spgemm_symbolic(A, B, L);
+  auto C = spgemm_symbolic(A, B, L, maxb);
   if (m > 0) {
     DevBuf<i64> len(m);
     k_row_len<<<grid_for(m, 256), 256, 0, stream()>>>(m, C->ptr.p, len.p);
