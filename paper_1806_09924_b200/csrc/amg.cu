@@ -1075,24 +1075,42 @@ const double* lambda_start(i64 n) {
   return p;
 }
 
+// power-iteration bookkeeping on the device: st = {lambda, done}; the first zero norm freezes
+// lambda at 1.0 (the reference returns 1.0 there), later iterations (NaN) change nothing
+__global__ void k_lambda_step(const double* __restrict__ nw, double* __restrict__ st) {
+  if (st[1] != 0.0) return;
+  if (nw[0] == 0.0) {
+    st[0] = 1.0;
+    st[1] = 1.0;
+  } else {
+    st[0] = nw[0];
+  }
+}
+
 double estimate_lambda_max(const Csr& A, const double* inv_diag) {  // linsolve.cpp:120-134
   const i64 n = A.rows;
   DevBuf<double> v(n), w(n);
-  double* s = scalar_buf(2);
+  double* s = scalar_buf(4);  // s[0]: norm; s[2], s[3]: lambda, done
   const double* v0 = lambda_start(n);
   vdot_dev(v0, v0, n, s, true);
   vdiv_dev(v0, s, v.p, n);
-  double lambda = 1.0;
+  const double init[2] = {1.0, 0.0};
+  CF_CUDA(cudaMemcpyAsync(s + 2, init, sizeof(init), cudaMemcpyHostToDevice, stream()));
+  // 15 iterations without a host round trip each (the reference's early return on a zero norm is
+  // the device flag; the values are the same IEEE sequence)
   for (int it = 0; it < 15; ++it) {
     csr_spmv_add(A, v.p, w.p, nullptr);
     vdiag_mul(inv_diag, w.p, w.p, 1.0, n);
     vdot_dev(w.p, w.p, n, s, true);
-    const double nw = read_dev(s);
-    if (nw == 0.0) return 1.0;
-    lambda = nw;
+    k_lambda_step<<<1, 1, 0, stream()>>>(s, s + 2);
+    CF_LAUNCHED();
     vdiv_dev(w.p, s, v.p, n);
   }
-  return std::max(lambda, 1e-12);
+  double st[2];
+  CF_CUDA(cudaMemcpyAsync(st, s + 2, sizeof(st), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  if (st[1] != 0.0) return 1.0;
+  return std::max(st[0], 1e-12);
 }
 
 }  // namespace
