@@ -823,6 +823,87 @@ __global__ void __launch_bounds__(256) k_num_grp(const int* __restrict__ glist, 
   }
 }
 
+// Group numeric for short B rows (<= 8 entries: the tentative prolongator of D^-1 A T): 8 lanes per
+// B row, so one step covers G = 4 consecutive A positions; slots and products are formed in
+// parallel, then the 4 position groups add in ascending k (one at a time, __syncwarp between), so
+// every accumulator sees k_num_grp's sequence.  Each slot lookup serves the NR rows of the group.
+template <int NR>
+__device__ __forceinline__ void num_grp_short_rows(double* __restrict__ Acc, const int* __restrict__ T,
+                                                   unsigned mask, int cap, int row0, int lane,
+                                                   const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                   const double* __restrict__ av, const double* __restrict__ rs,
+                                                   const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                   const double* __restrict__ bv) {
+  constexpr int L = 8, G = 32 / L;
+  const int g = lane / L, lig = lane % L;
+  double si[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) si[r] = rs ? rs[row0 + r] : 1.0;
+  const i64 a0 = ap[row0];
+  const int alen = int(ap[row0 + 1] - a0);
+  for (int p0 = 0; p0 < alen; p0 += G) {
+    const int pos = p0 + g;
+    int sl = -1;
+    double b = 0.0, a[NR];
+    if (pos < alen) {
+      const int k = ac[a0 + pos];
+      const i64 q = bp[k] + lig;
+      if (q < bp[k + 1]) {
+        const int c = bc[q];
+        b = bv[q];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) a[r] = rs ? si[r] * av[a0 + i64(r) * alen + pos] : av[a0 + i64(r) * alen + pos];
+        sl = hfind(T, mask, c);
+      }
+    }
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      if (g == gg && sl >= 0) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) Acc[size_t(r) * cap + sl] += a[r] * b;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_num_grp_short(const int* __restrict__ glist, int ng,
+                                                       const int* __restrict__ heads, const int* __restrict__ glen,
+                                                       int cap, int wpb, const i64* __restrict__ ap,
+                                                       const int* __restrict__ ac, const double* __restrict__ av,
+                                                       const double* __restrict__ rs, const i64* __restrict__ bp,
+                                                       const int* __restrict__ bc, const double* __restrict__ bv,
+                                                       const i64* __restrict__ cp, const int* __restrict__ cc,
+                                                       double* __restrict__ cv) {
+  extern __shared__ double grp_sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 gi = i64(blockIdx.x) * wpb + w;
+  if (gi >= ng) return;
+  const int grp = glist[gi];
+  const int row0 = heads[grp], nr = glen[grp];
+  double* Acc = grp_sm + size_t(w) * cap * GRP_MAX;
+  int* T = reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * GRP_MAX) + size_t(w) * cap;
+  for (int s = lane; s < cap; s += 32) T[s] = EMPTY;
+  for (int s = lane; s < cap * nr; s += 32) Acc[s] = 0.0;
+  __syncwarp();
+  const unsigned mask = unsigned(cap) - 1u;
+  const i64 c0 = cp[row0];
+  const int nc = int(cp[row0 + 1] - c0);
+  for (int t = lane; t < nc; t += 32) hinsert(T, mask, cc[c0 + t]);
+  __syncwarp();
+  switch (nr) {
+#define CFB_NR(R) \
+  case R: num_grp_short_rows<R>(Acc, T, mask, cap, row0, lane, ap, ac, av, rs, bp, bc, bv); break;
+    CFB_NR(1) CFB_NR(2) CFB_NR(3) CFB_NR(4) CFB_NR(5) CFB_NR(6)
+#undef CFB_NR
+  }
+  for (int t = lane; t < nc; t += 32) {
+    const int sl = hfind(T, mask, cc[c0 + t]);
+    for (int r = 0; r < nr; ++r) cv[c0 + i64(r) * nc + t] = Acc[size_t(r) * cap + sl];
+  }
+}
+
+// CB = 0: the short-row kernel (B rows of <= 8 entries)
 template <int CB>
 void num_grp_launch(const RowBin& b, int cap, const int* heads, const int* glen, const Csr& A, const Csr& B,
                     const double* rs, Csr& C) {
@@ -830,10 +911,11 @@ void num_grp_launch(const RowBin& b, int cap, const int* heads, const int* glen,
   const size_t per_warp = size_t(cap) * (sizeof(int) + sizeof(double) * GRP_MAX);
   const int wpb = int(std::min<size_t>(8, std::max<size_t>(1, (100u << 10) / per_warp)));
   const size_t sm = per_warp * wpb;
-  CF_CUDA(cudaFuncSetAttribute(k_num_grp<CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-  k_num_grp<CB><<<grid_for(b.n, wpb), wpb * 32, sm, stream()>>>(b.list.p, b.n, heads, glen, cap, wpb, A.ptr.p,
-                                                               A.col.p, A.val.p, rs, B.ptr.p, B.col.p, B.val.p,
-                                                               C.ptr.p, C.col.p, C.val.p);
+  auto kern = CB == 0 ? k_num_grp_short : k_num_grp<CB == 0 ? 1 : CB>;
+  CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+  kern<<<grid_for(b.n, wpb), wpb * 32, sm, stream()>>>(b.list.p, b.n, heads, glen, cap, wpb, A.ptr.p, A.col.p,
+                                                      A.val.p, rs, B.ptr.p, B.col.p, B.val.p, C.ptr.p, C.col.p,
+                                                      C.val.p);
   CF_LAUNCHED();
 }
 
@@ -1035,7 +1117,8 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   // product the grouped kernel can take (small matrices, short B rows, few shared patterns)
   static const bool no_group = std::getenv("CF_SPGEMM_NOGROUP") != nullptr;
   static const bool group_all = std::getenv("CF_SPGEMM_GROUP_ALL") != nullptr;
-  const bool try_group = group_all ? (m >= 1 && maxb >= 1) : (m >= 1024 && maxb > 16);
+  static const bool no_short = std::getenv("CF_SPGEMM_NO_SHORT_GROUP") != nullptr;  // A/B switch
+  const bool try_group = group_all ? (m >= 1 && maxb >= 1) : (m >= 1024 && (maxb > 16 || (!no_short && maxb >= 2 && maxb <= 8)));
   if (!no_group && try_group && maxb <= 256 && m < INT_MAX) {
     // row groups, chunked to GRP_MAX rows
     DevBuf<int> head(m), key(m), runstart(m);
@@ -1109,7 +1192,8 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
       const i64 lims[4] = {0, 96, 192, 384};
       for (int t = 0; t < 3; ++t) {
         RowBin b = make_bin(ng, gl.p, lims[t], lims[t + 1]);
-        if (maxb <= 32) num_grp_launch<1>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
+        if (maxb <= 8 && !no_short) num_grp_launch<0>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
+        else if (maxb <= 32) num_grp_launch<1>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
         else if (maxb <= 64) num_grp_launch<2>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
         else if (maxb <= 128) num_grp_launch<4>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
         else num_grp_launch<8>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
