@@ -491,22 +491,28 @@ __global__ void k_n2_big(i64 nov, const int* __restrict__ list, const i64* __res
 // warp per node, shared-memory hash set of N2(i) (set semantics: the insertion order is
 // irrelevant); more than 3/4 x N2CAP members -> overflow tier
 constexpr int N2CAP = 1024, N2WPB = 4;
+// mode 0 also stores up to N2UPC upper members per node in ups[i * N2UPC ...] (redo[i] = 0), so
+// mode 1 (which rebuilds the set) runs only for the nodes with more (redo[i] = 1); k_n2_compact
+// then moves the stored lists into the CSR of the dependents
+constexpr int N2UPC = 96;
 __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restrict__ sp, const int* __restrict__ si,
                                                     const i64* __restrict__ tp, const int* __restrict__ ti,
                                                     int* __restrict__ lower, i64* __restrict__ upcnt,
                                                     const i64* __restrict__ upptr, int* __restrict__ up, int mode,
-                                                    int* __restrict__ ovf) {
+                                                    int* __restrict__ ovf, int* __restrict__ ups,
+                                                    int* __restrict__ redo) {
   __shared__ int tab[N2WPB][N2CAP];
   __shared__ int cnt[N2WPB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const i64 node = i64(blockIdx.x) * N2WPB + w;
   if (node >= nn) return;
   const int i = int(node);
-  if (mode == 1 && ovf[i]) return;
+  if (mode == 1 && (ovf[i] || !redo[i])) return;
   if (sp[i + 1] == sp[i] && tp[i + 1] == tp[i]) {  // isolated node: N2(i) is empty
     if (mode == 0 && lane == 0) {
       lower[i] = 0;
       upcnt[i] = 0;
+      redo[i] = 0;
     }
     return;
   }
@@ -549,12 +555,20 @@ __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restric
     return;
   }
   if (mode == 0) {
+    __syncwarp();
+    if (lane == 0) cnt[w] = 0;
+    __syncwarp();
     int nl = 0, nu = 0;
+    int* my = ups + i64(i) * N2UPC;
     for (int s = lane; s < N2CAP; s += 32) {
       const int v = T[s];
       if (v < 0) continue;
       nl += v < i;
-      nu += v > i;
+      if (v > i) {
+        ++nu;
+        const int pos = atomicAdd(&cnt[w], 1);
+        if (pos < N2UPC) my[pos] = v;
+      }
     }
     for (int o = 16; o > 0; o >>= 1) {
       nl += __shfl_xor_sync(0xffffffffu, nl, o);
@@ -563,6 +577,7 @@ __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restric
     if (lane == 0) {
       lower[i] = nl;
       upcnt[i] = nu;
+      redo[i] = nu > N2UPC ? 1 : 0;
     }
   } else {
     __syncwarp();
@@ -576,6 +591,17 @@ __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restric
   }
 }
 
+
+// stored upper lists -> CSR of the dependents (warp per node; nodes handled by mode 1 or by the
+// global-memory tier are skipped)
+__global__ void k_n2_compact(i64 nn, const int* __restrict__ ovf, const int* __restrict__ redo,
+                             const int* __restrict__ ups, const i64* __restrict__ upptr, int* __restrict__ up) {
+  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= nn || ovf[i] || redo[i]) return;
+  const i64 b = upptr[i], n = upptr[i + 1] - b;
+  for (i64 t = lane; t < n; t += 32) up[b + t] = ups[i * N2UPC + t];
+}
 
 // ------------------------------------------------------------------ pass 1: LFMIS frontier rounds
 constexpr int UND = 0, ROOT = 1, NOTROOT = 2;
@@ -1295,8 +1321,13 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     DevBuf<i64> uptr(n_nodes + 1);
     uptr.zero();
     ovf.zero();
+    // the stored upper lists: a persistent scratch (hundreds of MB at the fine levels; allocating
+    // it per build from the caching allocator costs more than the pass it saves)
+    static DevBuf<int> ups;
+    if (ups.n < n_nodes * N2UPC) ups.alloc(n_nodes * N2UPC);
+    DevBuf<int> redo(n_nodes);
     k_n2w<<<grid_for(n_nodes, N2WPB), N2WPB * 32, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, lower.p,
-                                                                 uptr.p, nullptr, nullptr, 0, ovf.p);
+                                                                 uptr.p, nullptr, nullptr, 0, ovf.p, ups.p, redo.p);
     CF_LAUNCHED();
     OvfList big2 = make_ovf_list(n_nodes, ovf.p);
     DevBuf<i64> noff;
@@ -1319,7 +1350,9 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     const i64 nup = read_dev(uptr.p + n_nodes);
     DevBuf<int> up(std::max<i64>(nup, 1));
     k_n2w<<<grid_for(n_nodes, N2WPB), N2WPB * 32, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, nullptr,
-                                                                 nullptr, uptr.p, up.p, 1, ovf.p);
+                                                                 nullptr, uptr.p, up.p, 1, ovf.p, nullptr, redo.p);
+    CF_LAUNCHED();
+    k_n2_compact<<<grid_for(n_nodes * 32, 256), 256, 0, stream()>>>(n_nodes, ovf.p, redo.p, ups.p, uptr.p, up.p);
     CF_LAUNCHED();
     if (big2.n) {
       k_n2_big<<<grid_for(big2.n, 64), 64, 0, stream()>>>(big2.n, big2.list.p, noff.p, sptr.p, sidx.p, tptr.p, tidx.p,
