@@ -937,8 +937,10 @@ static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L, i
   if (m == 0) return C;
   i64* cnt = C->ptr.p;  // row counts in place, scanned into offsets afterwards
   // few rows into a narrow column space (coarse-level products): CTA per row, byte flags
+  // test switches: CF_SPGEMM_NO_FLAGS=1 never, CF_SPGEMM_FORCE_PATHS=1 whenever the columns fit
   static const bool no_flags = std::getenv("CF_SPGEMM_NO_FLAGS") != nullptr;
-  if (!no_flags && m <= 32768 && B.cols <= FLAG_MAX && maxb >= 64) {
+  static const bool force = std::getenv("CF_SPGEMM_FORCE_PATHS") != nullptr;
+  if (!no_flags && B.cols <= FLAG_MAX && m < INT_MAX && (force || (m <= 32768 && maxb >= 64))) {
     const size_t sm = size_t(B.cols) + 16;
     CF_CUDA(cudaFuncSetAttribute(k_sym_flags<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     k_sym_flags<0><<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), cnt, nullptr);
@@ -1045,8 +1047,9 @@ static void spgemm_numeric(const Csr& A, const Csr& B, const double* row_scale, 
   const i64 m = A.rows;
   // few rows of long B rows (coarse-level RAP): one CTA per row, B rows prefetched
   static const bool no_cta_pf = std::getenv("CF_SPGEMM_NO_CTA_PF") != nullptr;
-  if (!no_cta_pf && m > 0 && m <= 32768 && maxb >= 128 && maxb <= 1024) {
-    RowBin all = make_bin(m, lensel, 1, LLONG_MAX);
+  static const bool force = std::getenv("CF_SPGEMM_FORCE_PATHS") != nullptr;  // test switch
+  if (!no_cta_pf && m > 0 && m < INT_MAX && maxb <= 1024 && (force || (m <= 32768 && maxb >= 128))) {
+    RowBin all = make_bin(m, lensel, 0, LLONG_MAX);  // rows with >= 1 output column
     if (all.n) {
       DevBuf<unsigned long long> mx(1);
       mx.zero();

@@ -355,3 +355,23 @@ def test_amg_grouped_spgemm_everywhere(cf):
                         "-k", "amg and not everywhere or block_prec or penny"], env=env, capture_output=True, text=True,
                        timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [
+    {"CF_SPGEMM_FORCE_PATHS": "1"},
+    {"CF_SPGEMM_NO_FLAGS": "1", "CF_SPGEMM_NO_CTA_PF": "1", "CF_SPGEMM_NO_SHORT_GROUP": "1",
+     "CF_VCYCLE_UNFUSED": "1"},
+], ids=["forced-coarse-paths", "legacy-paths"])
+def test_amg_paths_forced_and_disabled(cf, env):
+    """The structure-aware SpGEMM paths (byte-flag symbolic, CTA-per-row prefetching numeric) forced
+    onto every product they can take, and, separately, every fast path switched off (generic hash
+    SpGEMM, unfused V-cycle): the oracle AMG / preconditioner / Newton parity tests must pass
+    bit for bit either way."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(root, "tests", "test_gpu_solver.py"),
+                        "-k", "amg and not everywhere and not forced or block_prec or penny"],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
