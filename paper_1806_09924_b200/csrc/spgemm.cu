@@ -763,6 +763,11 @@ __device__ __forceinline__ void num_grp_rows(double* __restrict__ Acc, const int
     for (int r = 0; r < NR; ++r) ka[r] = rs ? si[r] * av[a0 + i64(r) * alen + pos] : av[a0 + i64(r) * alen + pos];
   };
   if (alen > 0) load(0, ck, cb, ca, cn);
+  // slot of the previous position's entry t: the d rows of a mesh node (or an aggregate's coarse
+  // dofs) repeat one column pattern, so the lookup is reused when the column is the same
+  int pk[CB], ps[CB];
+#pragma unroll
+  for (int t = 0; t < CB; ++t) pk[t] = -1;
   for (int pos = 0; pos < alen; ++pos) {
     if (pos + 1 < alen) load(pos + 1, nk, nb, na, nn);
 #pragma unroll
@@ -770,7 +775,9 @@ __device__ __forceinline__ void num_grp_rows(double* __restrict__ Acc, const int
       if (t * 32 >= cn) break;  // warp-uniform
       const int e = t * 32 + lane;
       if (e < cn) {
-        const int sl = hfind(T, mask, ck[t]);
+        const int sl = ck[t] == pk[t] ? ps[t] : hfind(T, mask, ck[t]);
+        pk[t] = ck[t];
+        ps[t] = sl;
 #pragma unroll
         for (int r = 0; r < NR; ++r) Acc[size_t(r) * cap + sl] += ca[r] * cb[t];
       }
