@@ -796,7 +796,7 @@ __device__ __forceinline__ void num_grp_rows(double* __restrict__ Acc, const int
 
 template <int CB>
 __global__ void __launch_bounds__(256) k_num_grp(const int* __restrict__ glist, int ng, const int* __restrict__ heads,
-                                                 const int* __restrict__ glen, int cap, int wpb,
+                                                 const int* __restrict__ glen, int cap, int wpb, int gm,
                                                  const i64* __restrict__ ap, const int* __restrict__ ac,
                                                  const double* __restrict__ av, const double* __restrict__ rs,
                                                  const i64* __restrict__ bp, const int* __restrict__ bc,
@@ -808,8 +808,8 @@ __global__ void __launch_bounds__(256) k_num_grp(const int* __restrict__ glist, 
   if (gi >= ng) return;
   const int grp = glist[gi];
   const int row0 = heads[grp], nr = glen[grp];
-  double* Acc = grp_sm + size_t(w) * cap * GRP_MAX;  // [GRP_MAX][cap]
-  int* T = reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * GRP_MAX) + size_t(w) * cap;
+  double* Acc = grp_sm + size_t(w) * cap * gm;  // [gm][cap], gm = the longest group
+  int* T = reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * gm) + size_t(w) * cap;
   for (int s = lane; s < cap; s += 32) T[s] = EMPTY;
   for (int s = lane; s < cap * nr; s += 32) Acc[s] = 0.0;
   __syncwarp();
@@ -876,7 +876,7 @@ __device__ __forceinline__ void num_grp_short_rows(double* __restrict__ Acc, con
 
 __global__ void __launch_bounds__(256) k_num_grp_short(const int* __restrict__ glist, int ng,
                                                        const int* __restrict__ heads, const int* __restrict__ glen,
-                                                       int cap, int wpb, const i64* __restrict__ ap,
+                                                       int cap, int wpb, int gm, const i64* __restrict__ ap,
                                                        const int* __restrict__ ac, const double* __restrict__ av,
                                                        const double* __restrict__ rs, const i64* __restrict__ bp,
                                                        const int* __restrict__ bc, const double* __restrict__ bv,
@@ -888,8 +888,8 @@ __global__ void __launch_bounds__(256) k_num_grp_short(const int* __restrict__ g
   if (gi >= ng) return;
   const int grp = glist[gi];
   const int row0 = heads[grp], nr = glen[grp];
-  double* Acc = grp_sm + size_t(w) * cap * GRP_MAX;
-  int* T = reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * GRP_MAX) + size_t(w) * cap;
+  double* Acc = grp_sm + size_t(w) * cap * gm;
+  int* T = reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * gm) + size_t(w) * cap;
   for (int s = lane; s < cap; s += 32) T[s] = EMPTY;
   for (int s = lane; s < cap * nr; s += 32) Acc[s] = 0.0;
   __syncwarp();
@@ -913,17 +913,24 @@ __global__ void __launch_bounds__(256) k_num_grp_short(const int* __restrict__ g
 // CB = 0: the short-row kernel (B rows of <= 8 entries)
 template <int CB>
 void num_grp_launch(const RowBin& b, int cap, const int* heads, const int* glen, const Csr& A, const Csr& B,
-                    const double* rs, Csr& C) {
+                    const double* rs, Csr& C, int gm) {
   if (!b.n) return;
-  const size_t per_warp = size_t(cap) * (sizeof(int) + sizeof(double) * GRP_MAX);
+  const size_t per_warp = size_t(cap) * (sizeof(int) + sizeof(double) * gm);
   const int wpb = int(std::min<size_t>(8, std::max<size_t>(1, (100u << 10) / per_warp)));
   const size_t sm = per_warp * wpb;
   auto kern = CB == 0 ? k_num_grp_short : k_num_grp<CB == 0 ? 1 : CB>;
   CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-  kern<<<grid_for(b.n, wpb), wpb * 32, sm, stream()>>>(b.list.p, b.n, heads, glen, cap, wpb, A.ptr.p, A.col.p,
+  kern<<<grid_for(b.n, wpb), wpb * 32, sm, stream()>>>(b.list.p, b.n, heads, glen, cap, wpb, gm, A.ptr.p, A.col.p,
                                                       A.val.p, rs, B.ptr.p, B.col.p, B.val.p, C.ptr.p, C.col.p,
                                                       C.val.p);
   CF_LAUNCHED();
+}
+
+__global__ void k_max_int(i64 n, const int* __restrict__ v, int* __restrict__ mx) {
+  int m = 0;
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) m = max(m, v[i]);
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
 }
 
 __global__ void k_group_clen(int ng, const int* __restrict__ heads, const i64* __restrict__ cp, i64* __restrict__ out) {
@@ -1162,6 +1169,16 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
       DevBuf<int> glen(ng);
       k_group_len<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, heads.p, m, glen.p);
       CF_LAUNCHED();
+      // accumulator rows per warp = the longest group (3 on the node-structured fine level, 6 on
+      // coarse levels): the shared-memory footprint, hence the resident warps, follows it
+      int gmax = GRP_MAX;
+      {
+        DevBuf<int> mx(1);
+        mx.zero();
+        k_max_int<<<int(std::min<i64>(1024, grid_for(ng, 256))), 256, 0, stream()>>>(ng, glen.p, mx.p);
+        CF_LAUNCHED();
+        gmax = std::max(1, std::min(GRP_MAX, read_int(mx.p)));
+      }
       // symbolic on the head rows
       Csr Ag;
       Ag.rows = ng;
@@ -1202,11 +1219,11 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
       const i64 lims[4] = {0, 96, 192, 384};
       for (int t = 0; t < 3; ++t) {
         RowBin b = make_bin(ng, gl.p, lims[t], lims[t + 1]);
-        if (maxb <= 8 && !no_short) num_grp_launch<0>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
-        else if (maxb <= 32) num_grp_launch<1>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
-        else if (maxb <= 64) num_grp_launch<2>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
-        else if (maxb <= 128) num_grp_launch<4>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
-        else num_grp_launch<8>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C);
+        if (maxb <= 8 && !no_short) num_grp_launch<0>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
+        else if (maxb <= 32) num_grp_launch<1>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
+        else if (maxb <= 64) num_grp_launch<2>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
+        else if (maxb <= 128) num_grp_launch<4>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
+        else num_grp_launch<8>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
       }
       RowBin big = make_bin(ng, gl.p, 384, LLONG_MAX);
       if (big.n) {
