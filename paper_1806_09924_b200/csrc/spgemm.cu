@@ -795,7 +795,7 @@ __device__ __forceinline__ void num_grp_rows(double* __restrict__ Acc, const int
 }
 
 template <int CB>
-__global__ void __launch_bounds__(256) k_num_grp(const int* __restrict__ glist, int ng, const int* __restrict__ heads,
+__global__ void __launch_bounds__(256, CB >= 8 ? 2 : 3) k_num_grp(const int* __restrict__ glist, int ng, const int* __restrict__ heads,
                                                  const int* __restrict__ glen, int cap, int wpb, int gm,
                                                  const i64* __restrict__ ap, const int* __restrict__ ac,
                                                  const double* __restrict__ av, const double* __restrict__ rs,
