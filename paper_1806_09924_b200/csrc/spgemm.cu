@@ -1352,6 +1352,97 @@ __global__ void k_axpy_merge(i64 rows, const i64* __restrict__ tp, const int* __
   if (!mode) pp[i] = n;
 }
 
+// P = T - w D^-1 A T, warp per row: when T's pattern is contained in DAT's (A carries its
+// diagonal, so it always is for the AMG products) the merged row is DAT's pattern; lanes take DAT's
+// entries coalesced, look their column up among T's <= 32 entries (registers + shuffles) and
+// compact the kept values with a ballot.  Rows where T has a column DAT lacks are left to the
+// serial merge (flag).  The values are k_axpy_merge's expressions.
+__global__ void k_axpy_merge_w(i64 rows, const i64* __restrict__ tp, const int* __restrict__ tc,
+                               const double* __restrict__ tv, double w, const i64* __restrict__ dp,
+                               const int* __restrict__ dc, const double* __restrict__ dv, i64* __restrict__ pp,
+                               int* __restrict__ pc, double* __restrict__ pv, int mode, int* __restrict__ serial) {
+  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= rows) return;
+  const i64 a = tp[i], na = tp[i + 1] - a, b = dp[i], nb = dp[i + 1] - b;
+  if (na > 32) {  // not handled here
+    if (mode == 0 && lane == 0) serial[i] = 1;
+    return;
+  }
+  if (mode == 1 && serial[i]) return;
+  const int myc = lane < na ? tc[a + lane] : -1;
+  const double mytv = lane < na ? tv[a + lane] : 0.0;
+  int matched = 0;
+  i64 n = 0;
+  const i64 out = mode ? pp[i] : 0;
+  for (i64 base = 0; base < nb; base += 32) {
+    const i64 e = base + lane;
+    const bool in = e < nb;
+    const int c = in ? dc[b + e] : -2;
+    const double d = in ? dv[b + e] : 0.0;
+    int hit = -1;
+    for (int t = 0; t < na; ++t)
+      if (__shfl_sync(0xffffffffu, myc, t) == c) hit = t;
+    double v = 0.0;
+    const double tvh = __shfl_sync(0xffffffffu, mytv, hit < 0 ? 0 : hit);
+    if (hit >= 0) v = tvh - w * d;
+    else v = 0.0 - w * d;
+    const bool keep = in && fabs(v) > 1e-300;
+    matched += __popc(__ballot_sync(0xffffffffu, in && hit >= 0));
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (mode == 1 && keep) {
+      const i64 o = out + n + __popc(km & ((1u << lane) - 1u));
+      pc[o] = c;
+      pv[o] = v;
+    }
+    n += __popc(km);
+  }
+  if (mode == 0 && lane == 0) {
+    const bool ok = matched == na;  // every T column found in DAT: the merge is DAT's pattern
+    serial[i] = ok ? 0 : 1;
+    if (ok) pp[i] = n;
+  }
+}
+
+// the serial merge restricted to the flagged rows
+__global__ void k_axpy_merge_rows(i64 rows, const int* __restrict__ serial, const i64* __restrict__ tp,
+                                  const int* __restrict__ tc, const double* __restrict__ tv, double w,
+                                  const i64* __restrict__ dp, const int* __restrict__ dc,
+                                  const double* __restrict__ dv, i64* __restrict__ pp, int* __restrict__ pc,
+                                  double* __restrict__ pv, int mode) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= rows || !serial[i]) return;
+  i64 a = tp[i], ae = tp[i + 1], b = dp[i], be = dp[i + 1];
+  i64 out = mode ? pp[i] : 0;
+  i64 n = 0;
+  while (a < ae || b < be) {
+    int c;
+    double v;
+    if (b >= be || (a < ae && tc[a] < dc[b])) {
+      c = tc[a];
+      v = tv[a];
+      ++a;
+    } else if (a >= ae || dc[b] < tc[a]) {
+      c = dc[b];
+      v = 0.0 - w * dv[b];
+      ++b;
+    } else {
+      c = tc[a];
+      v = tv[a] - w * dv[b];
+      ++a;
+      ++b;
+    }
+    if (fabs(v) > 1e-300) {
+      if (mode) {
+        pc[out + n] = c;
+        pv[out + n] = v;
+      }
+      ++n;
+    }
+  }
+  if (!mode) pp[i] = n;
+}
+
 __global__ void k_prune(i64 rows, const i64* __restrict__ ip, const int* __restrict__ ic, const double* __restrict__ iv,
                         i64* __restrict__ op, int* __restrict__ oc, double* __restrict__ ov, int mode) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1388,9 +1479,37 @@ std::unique_ptr<Csr> csr_axpy_prune(const Csr& T, double w, const Csr& DAT) {
   P->cols = T.cols;
   P->ptr.alloc(T.rows + 1);
   P->ptr.zero();
-  k_axpy_merge<<<grid_for(T.rows, 256), 256, 0, stream()>>>(T.rows, T.ptr.p, T.col.p, T.val.p, w, DAT.ptr.p,
-                                                            DAT.col.p, DAT.val.p, P->ptr.p, nullptr, nullptr, 0);
-  CF_LAUNCHED();
+  static const bool serial_only = std::getenv("CF_AXPY_SERIAL") != nullptr;  // A/B switch
+  // warp per row pays off for rows of tens of entries (the u-block); short rows stay serial
+  if (serial_only || DAT.nnz < 16 * T.rows) {
+    k_axpy_merge<<<grid_for(T.rows, 256), 256, 0, stream()>>>(T.rows, T.ptr.p, T.col.p, T.val.p, w, DAT.ptr.p,
+                                                              DAT.col.p, DAT.val.p, P->ptr.p, nullptr, nullptr, 0);
+    CF_LAUNCHED();
+  } else {
+    // warp-per-row merge where T's pattern lies in DAT's; the serial merge for the other rows
+    DevBuf<int> serial(T.rows);
+    k_axpy_merge_w<<<grid_for(T.rows * 32, 256), 256, 0, stream()>>>(T.rows, T.ptr.p, T.col.p, T.val.p, w, DAT.ptr.p,
+                                                                     DAT.col.p, DAT.val.p, P->ptr.p, nullptr,
+                                                                     nullptr, 0, serial.p);
+    CF_LAUNCHED();
+    k_axpy_merge_rows<<<grid_for(T.rows, 256), 256, 0, stream()>>>(T.rows, serial.p, T.ptr.p, T.col.p, T.val.p, w,
+                                                                   DAT.ptr.p, DAT.col.p, DAT.val.p, P->ptr.p,
+                                                                   nullptr, nullptr, 0);
+    CF_LAUNCHED();
+    scan_excl(P->ptr.p, T.rows + 1);
+    P->nnz = read_i64(P->ptr.p + T.rows);
+    P->col.alloc(P->nnz);
+    P->val.alloc(P->nnz);
+    k_axpy_merge_w<<<grid_for(T.rows * 32, 256), 256, 0, stream()>>>(T.rows, T.ptr.p, T.col.p, T.val.p, w, DAT.ptr.p,
+                                                                     DAT.col.p, DAT.val.p, P->ptr.p, P->col.p,
+                                                                     P->val.p, 1, serial.p);
+    CF_LAUNCHED();
+    k_axpy_merge_rows<<<grid_for(T.rows, 256), 256, 0, stream()>>>(T.rows, serial.p, T.ptr.p, T.col.p, T.val.p, w,
+                                                                   DAT.ptr.p, DAT.col.p, DAT.val.p, P->ptr.p,
+                                                                   P->col.p, P->val.p, 1);
+    CF_LAUNCHED();
+    return P;
+  }
   scan_excl(P->ptr.p, T.rows + 1);
   P->nnz = read_i64(P->ptr.p + T.rows);
   P->col.alloc(P->nnz);
