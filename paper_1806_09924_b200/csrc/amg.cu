@@ -374,7 +374,7 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
                            const i64* __restrict__ Ap, const int* __restrict__ Ac, const double* __restrict__ Av,
                            const int* __restrict__ nod, const double* __restrict__ dsq, double theta,
                            i64* __restrict__ cnt, const i64* __restrict__ sptr, int* __restrict__ sidx, int mode,
-                           int* __restrict__ ovf) {
+                           int* __restrict__ ovf, int* __restrict__ stmp) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   if (mode && ovf[i]) return;  // handled by the overflow tier
@@ -425,10 +425,21 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
     const double djj = dsq[j];
     if (sqrt(sums[s]) > theta * sqrt(dii * djj)) {
       if (mode) sidx[base + n] = j;
+      else if (stmp) stmp[i64(i) * SCAP + n] = j;  // kept for k_strength_compact (n < SCAP)
       ++n;
     }
   }
   if (!mode) cnt[i] = n;
+}
+
+// the strong lists stored by the counting pass -> CSR (warp per node; overflow-tier nodes skipped)
+__global__ void k_strength_compact(i64 nn, const int* __restrict__ ovf, const int* __restrict__ stmp,
+                                   const i64* __restrict__ sptr, int* __restrict__ sidx) {
+  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= nn || ovf[i]) return;
+  const i64 b = sptr[i], n = sptr[i + 1] - b;
+  for (i64 t = lane; t < n; t += 32) sidx[b + t] = stmp[i * SCAP + t];
 }
 
 // ------------------------------------------------------------------ N2 dependency graph
@@ -1253,9 +1264,13 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     sptr.zero();
     DevBuf<int> ovf(n_nodes);
     ovf.zero();
+    // the counting pass also stores each node's strong list (persistent scratch, SCAP per node), so
+    // the fill is a compaction instead of a second pass over the matrix
+    static DevBuf<int> stmp;
+    if (stmp.n < n_nodes * SCAP) stmp.alloc(n_nodes * SCAP);
     k_strength<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, nptr.p, ndofs.p, A->ptr.p, A->col.p, A->val.p,
                                                               nod.p, dsq.p, opts.strength_threshold, sptr.p, nullptr,
-                                                              nullptr, 0, ovf.p);
+                                                              nullptr, 0, ovf.p, stmp.p);
     CF_LAUNCHED();
     // overflow tier for high-degree nodes
     OvfList big = make_ovf_list(n_nodes, ovf.p);
@@ -1292,9 +1307,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     scan_excl(sptr.p, n_nodes + 1);
     const i64 ns = read_dev(sptr.p + n_nodes);
     DevBuf<int> sidx(std::max<i64>(ns, 1));
-    k_strength<<<grid_for(n_nodes, 128), 128, 0, stream()>>>(n_nodes, nptr.p, ndofs.p, A->ptr.p, A->col.p, A->val.p,
-                                                              nod.p, dsq.p, opts.strength_threshold, nullptr, sptr.p,
-                                                              sidx.p, 1, ovf.p);
+    k_strength_compact<<<grid_for(n_nodes * 32, 256), 256, 0, stream()>>>(n_nodes, ovf.p, stmp.p, sptr.p, sidx.p);
     CF_LAUNCHED();
     if (big.n) {
       k_strength_big_emit<<<grid_for(big.n, 128), 128, 0, stream()>>>(big.n, big.list.p, boff.p, bkeys.p, bsums.p,
