@@ -642,6 +642,24 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
       __syncwarp();
     }
     (void)vmask;
+    // CSR offsets of this slot's entries: free u / phi dofs of the in-range slots before it, by a
+    // warp prefix sum over the slot lanes (lanes >= 3^d and out-of-range slots count 0)
+    int myfu = 0, myfp = 0;
+    if (slot_ok) {
+      const i64 ws = X + g.nn * (Y + g.nn * Z);
+#pragma unroll
+      for (int b = 0; b < D; ++b) myfu += flag[ws * D + b] ? 0 : 1;
+      myfp = flag[nu + ws] ? 0 : 1;
+    }
+    int incu = myfu, incp = myfp;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int tu = __shfl_up_sync(FULL, incu, o), tp = __shfl_up_sync(FULL, incp, o);
+      if (lane >= o) {
+        incu += tu;
+        incp += tp;
+      }
+    }
     if (!slot_ok) continue;
     const i64 w = X + g.nn * (Y + g.nn * Z);
     bool rowfree_u[D], colfree_u[D];
@@ -652,16 +670,7 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
     }
     const bool rowfree_p = flag[nu + v] == 0, colfree_p = flag[nu + w] == 0;
     const bool center = w == v;
-    i64 off_u = 0, off_p = 0;
-    for (int s2 = 0; s2 < s; ++s2) {
-      const int ex = s2 % 3 - 1, ey = (s2 / 3) % 3 - 1, ez = (D == 3) ? s2 / 9 - 1 : 0;
-      const i64 X2 = x + ex, Y2 = y + ey, Z2 = z + ez;
-      if (X2 < 0 || Y2 < 0 || Z2 < 0 || X2 >= g.nn || Y2 >= g.nn || Z2 >= ((D == 3) ? g.nn : 1)) continue;
-      const i64 w2 = X2 + g.nn * (Y2 + g.nn * Z2);
-#pragma unroll
-      for (int b = 0; b < D; ++b) off_u += flag[w2 * D + b] ? 0 : 1;
-      off_p += flag[nu + w2] ? 0 : 1;
-    }
+    const i64 off_u = incu - myfu, off_p = incp - myfp;
 #pragma unroll
     for (int a = 0; a < D && UU; ++a) {
       const i64 row = lv * D + a;
