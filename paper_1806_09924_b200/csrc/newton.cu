@@ -7,6 +7,7 @@
 // change count, the constraint arrays, distribute, the rigid-body near-nullspace.  Only
 // scalars (norms, counts) cross to the host per iteration.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -201,13 +202,17 @@ __global__ void k_phi_modes(Slab sl, i64 nu, const std::uint8_t* __restrict__ fl
 
 __global__ void k_feas(Slab sl, i64 nu, const double* __restrict__ x, const double* __restrict__ po, double* out) {
   const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (lv >= sl.nv()) return;
-  const i64 v = sl.v_lo + lv;
-  const double d = x[nu + v] - po[v];
-  // max via the ordered-int trick for doubles (handles negatives)
-  long long bits = __double_as_longlong(d);
-  bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
-  atomicMax(reinterpret_cast<long long*>(out), bits);
+  // max via the ordered-int trick for doubles (handles negatives); a warp maximum first, one
+  // atomic per warp (the maximum is exact in any order)
+  long long bits = LLONG_MIN;
+  if (lv < sl.nv()) {
+    const i64 v = sl.v_lo + lv;
+    const double d = x[nu + v] - po[v];
+    bits = __double_as_longlong(d);
+    bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
+  }
+  for (int o = 16; o > 0; o >>= 1) bits = max(bits, __shfl_xor_sync(0xffffffffu, bits, o));
+  if ((threadIdx.x & 31) == 0 && bits != LLONG_MIN) atomicMax(reinterpret_cast<long long*>(out), bits);
 }
 
 struct Timer {

@@ -1460,6 +1460,31 @@ __global__ void k_prune(i64 rows, const i64* __restrict__ ip, const int* __restr
   if (!mode) op[i] = n;
 }
 
+// k_prune with a warp per row (coalesced; rows of tens to hundreds of entries): kept entries are
+// compacted in order by a ballot prefix
+__global__ void k_prune_w(i64 rows, const i64* __restrict__ ip, const int* __restrict__ ic,
+                          const double* __restrict__ iv, i64* __restrict__ op, int* __restrict__ oc,
+                          double* __restrict__ ov, int mode) {
+  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= rows) return;
+  const i64 b = ip[i], e = ip[i + 1];
+  const i64 base = mode ? op[i] : 0;
+  i64 n = 0;
+  for (i64 k0 = b; k0 < e; k0 += 32) {
+    const i64 k = k0 + lane;
+    const bool keep = k < e && fabs(iv[k]) > 1e-300;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (mode && keep) {
+      const i64 o = base + n + __popc(m & ((1u << lane) - 1u));
+      oc[o] = ic[k];
+      ov[o] = iv[k];
+    }
+    n += __popc(m);
+  }
+  if (!mode && lane == 0) op[i] = n;
+}
+
 __global__ void k_diag(i64 rows, const i64* __restrict__ p, const int* __restrict__ c, const double* __restrict__ v,
                        double* __restrict__ d) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1523,14 +1548,23 @@ std::unique_ptr<Csr> csr_axpy_prune(const Csr& T, double w, const Csr& DAT) {
 void csr_prune(Csr& A) {
   DevBuf<i64> np(A.rows + 1);
   np.zero();
-  k_prune<<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, np.p, nullptr, nullptr, 0);
+  const bool warp = A.nnz >= 16 * A.rows;  // long rows: warp per row, coalesced
+  if (warp)
+    k_prune_w<<<grid_for(A.rows * 32, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, np.p, nullptr,
+                                                                nullptr, 0);
+  else
+    k_prune<<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, np.p, nullptr, nullptr, 0);
   CF_LAUNCHED();
   scan_excl(np.p, A.rows + 1);
   const i64 nnz = read_i64(np.p + A.rows);
   if (nnz == A.nnz) return;
   DevBuf<int> nc(nnz);
   DevBuf<double> nv(nnz);
-  k_prune<<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, np.p, nc.p, nv.p, 1);
+  if (warp)
+    k_prune_w<<<grid_for(A.rows * 32, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, np.p, nc.p, nv.p,
+                                                                1);
+  else
+    k_prune<<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, np.p, nc.p, nv.p, 1);
   CF_LAUNCHED();
   A.ptr = std::move(np);
   A.col = std::move(nc);
