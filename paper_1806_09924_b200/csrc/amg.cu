@@ -50,6 +50,7 @@ T read_dev(const T* p) {
   T h{};
   CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   return h;
 }
 
@@ -64,7 +65,9 @@ struct PhaseClock {
   bool on;
   cudaEvent_t last;
   int lev = 0;
+  long syncs = 0;  // host round trips at the previous mark
   PhaseClock() : on(std::getenv("CF_TIMING") != nullptr) {
+    syncs = host_sync_count();
     if (on) {
       cudaEventCreate(&last);
       cudaEventRecord(last, stream());
@@ -78,7 +81,9 @@ struct PhaseClock {
     cudaEventSynchronize(e);
     float ms = 0;
     cudaEventElapsedTime(&ms, last, e);
-    std::fprintf(stderr, "[amg L%d] %-12s %8.3f ms\n", lev, what, ms);
+    const long ns = host_sync_count();
+    std::fprintf(stderr, "[amg L%d] %-12s %8.3f ms %4ld host syncs\n", lev, what, ms, ns - syncs);
+    syncs = ns;
     cudaEventDestroy(last);
     last = e;
   }
@@ -1106,6 +1111,7 @@ const double* lambda_start(i64 n) {
   auto buf = std::make_unique<DevBuf<double>>(n);
   CF_CUDA(cudaMemcpyAsync(buf->p, h.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   const double* p = buf->p;
   if (cache.size() > 64) cache.clear();
   cache[n] = std::move(buf);
@@ -1146,6 +1152,7 @@ double estimate_lambda_max(const Csr& A, const double* inv_diag) {  // linsolve.
   double st[2];
   CF_CUDA(cudaMemcpyAsync(st, s + 2, sizeof(st), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   if (st[1] != 0.0) return 1.0;
   return std::max(st[0], 1e-12);
 }
@@ -1172,6 +1179,7 @@ void DenseLu::factor_from_csr(const Csr& A) {
     CF_CUDA(cudaMemcpyAsync(&h_off, off.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaMemcpyAsync(&h_mn, mn.p, sizeof(h_mn), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
+    ++host_sync_count();
     if (h_off) fail(CF_ERR_UNSUPPORTED, "dense LU: matrix too large for the one-CTA factorisation");
     std::memcpy(&min_abs_pivot, &h_mn, sizeof(double));
     diagonal = true;

@@ -935,6 +935,7 @@ std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64
     int hb = 0;
     CF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
+    ++host_sync_count();
     if (hb) fail(CF_ERR_INVALID_ARGUMENT, "build_constraints: active dof out of range");
   }
   return c;
@@ -1023,6 +1024,7 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   CF_CUDA(cudaMemcpyAsync(&nnz[1], J.pu->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaMemcpyAsync(&nnz[2], J.pp->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   if (with_uu) {
     J.uu->nnz = nnz[0];
     J.uu->col.alloc(nnz[0]);
@@ -1094,6 +1096,7 @@ static void pattern_impl(const Problem& P, const Constraints& cs, BlockSystem& J
     CF_CUDA(cudaMemcpyAsync(&B[b]->nnz, B[b]->ptr.p + rows[b], sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   }
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   for (int b = 0; b < 3; ++b) {
     B[b]->col.alloc(B[b]->nnz);
     B[b]->val.alloc(B[b]->nnz);

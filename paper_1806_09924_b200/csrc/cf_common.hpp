@@ -48,6 +48,11 @@ struct Runtime {
 Runtime& rt();
 void ensure_device();  // throws CF_ERR_CUDA when no device is usable (no CPU fallback)
 inline cudaStream_t stream() { return rt().stream; }
+// host round trips of the library stream (diagnostics: CF_TIMING prints them per AMG build)
+inline long& host_sync_count() {
+  static long n = 0;
+  return n;
+}
 inline void count_launch(i64 n = 1) { rt().launches += n; }
 #define CF_LAUNCHED() ::cfb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__), ::cfb::count_launch()
 

@@ -41,6 +41,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
   double bnorm = 0.0;
   CF_CUDA(cudaMemcpyAsync(&bnorm, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   if (bnorm == 0.0) {
     res.converged = true;
     return res;
@@ -80,6 +81,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     double beta = 0.0;
     CF_CUDA(cudaMemcpyAsync(&beta, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
+    ++host_sync_count();
     if (beta <= o.rtol * bnorm) {
       res.converged = true;
       res.residual = beta / bnorm;
@@ -117,6 +119,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
       }
       CF_CUDA(cudaMemcpyAsync(hcol.data(), hd.p, size_t(j + 2) * sizeof(double), cudaMemcpyDeviceToHost, stream()));
       CF_CUDA(cudaStreamSynchronize(stream()));
+      ++host_sync_count();
       for (int i = 0; i <= j + 1; ++i) Hij(i, j) = hcol[i];
       const bool happy = Hij(j + 1, j) <= 1e-14 * bnorm;
       if (!happy) vdiv_dev(w, hd.p + j + 1, w, n);
@@ -172,6 +175,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     double rn = 0.0;
     CF_CUDA(cudaMemcpyAsync(&rn, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
+    ++host_sync_count();
     res.residual = rn / bnorm;
     if (res.residual <= o.rtol) {
       res.converged = true;

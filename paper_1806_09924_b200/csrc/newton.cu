@@ -25,6 +25,7 @@ T read_dev(const T* p) {
   T h{};
   CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   return h;
 }
 
@@ -315,6 +316,7 @@ double gnorm(const Comm* cm, const double* v, i64 n) {
   double h = 0.0;
   CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   return std::sqrt(h);
 }
 
@@ -454,6 +456,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
       int hc[2];
       CF_CUDA(cudaMemcpyAsync(hc, flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream()));
       CF_CUDA(cudaStreamSynchronize(stream()));
+      ++host_sync_count();
       long long counts[2] = {hc[0], hc[1]};
       cm.sum_i64(counts, 2);
       asize = int(counts[0]);
@@ -643,6 +646,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   long long bits = 0;
   CF_CUDA(cudaMemcpyAsync(&bits, mx.p, sizeof(bits), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   cm.max_i64(&bits, 1);
   bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
   double viol;

@@ -553,12 +553,14 @@ i64 read_i64(const i64* p) {
   i64 h = 0;
   CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   return h;
 }
 int read_int(const int* p) {
   int h = 0;
   CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   return h;
 }
 
@@ -1127,6 +1129,7 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
     unsigned long long h = 0;
     CF_CUDA(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
+    ++host_sync_count();
     maxb = i64(h);
   }
   const int L = lanes_for(maxb);

@@ -208,6 +208,7 @@ double vdot(const double* x, const double* y, i64 n) {
   double h = 0.0;
   CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   return h;
 }
 
@@ -217,6 +218,7 @@ double vnorm(const double* x, i64 n) {
   double h = 0.0;
   CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
   return h;
 }
 
