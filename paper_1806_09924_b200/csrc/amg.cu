@@ -511,18 +511,34 @@ constexpr int N2CAP = 1024, N2WPB = 4;
 // mode 1 (which rebuilds the set) runs only for the nodes with more (redo[i] = 1); k_n2_compact
 // then moves the stored lists into the CSR of the dependents
 constexpr int N2UPC = 96;
-__global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restrict__ sp, const int* __restrict__ si,
-                                                    const i64* __restrict__ tp, const int* __restrict__ ti,
-                                                    int* __restrict__ lower, i64* __restrict__ upcnt,
-                                                    const i64* __restrict__ upptr, int* __restrict__ up, int mode,
-                                                    int* __restrict__ ovf, int* __restrict__ ups,
-                                                    int* __restrict__ redo) {
+// the nodes with a strong edge (either direction); isolated nodes (the dof-less coarse nodes of
+// the phi levels, active phi dofs) get their empty N2 here, so the warp kernels visit only the list
+__global__ void k_n2_nodes(i64 nn, const i64* __restrict__ sp, const i64* __restrict__ tp, int* __restrict__ lower,
+                           i64* __restrict__ upcnt, int* __restrict__ redo, int* __restrict__ list,
+                           int* __restrict__ count) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  if (sp[i + 1] == sp[i] && tp[i + 1] == tp[i]) {
+    lower[i] = 0;
+    upcnt[i] = 0;
+    redo[i] = 0;
+  } else {
+    list[atomicAdd(count, 1)] = int(i);
+  }
+}
+
+__global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const int* __restrict__ list, const i64* __restrict__ sp,
+                                                    const int* __restrict__ si, const i64* __restrict__ tp,
+                                                    const int* __restrict__ ti, int* __restrict__ lower,
+                                                    i64* __restrict__ upcnt, const i64* __restrict__ upptr,
+                                                    int* __restrict__ up, int mode, int* __restrict__ ovf,
+                                                    int* __restrict__ ups, int* __restrict__ redo) {
   __shared__ int tab[N2WPB][N2CAP];
   __shared__ int cnt[N2WPB];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const i64 node = i64(blockIdx.x) * N2WPB + w;
   if (node >= nn) return;
-  const int i = int(node);
+  const int i = list ? list[node] : int(node);
   if (mode == 1 && (ovf[i] || !redo[i])) return;
   if (sp[i + 1] == sp[i] && tp[i + 1] == tp[i]) {  // isolated node: N2(i) is empty
     if (mode == 0 && lane == 0) {
@@ -610,11 +626,14 @@ __global__ void __launch_bounds__(N2WPB * 32) k_n2w(i64 nn, const i64* __restric
 
 // stored upper lists -> CSR of the dependents (warp per node; nodes handled by mode 1 or by the
 // global-memory tier are skipped)
-__global__ void k_n2_compact(i64 nn, const int* __restrict__ ovf, const int* __restrict__ redo,
-                             const int* __restrict__ ups, const i64* __restrict__ upptr, int* __restrict__ up) {
-  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+__global__ void k_n2_compact(i64 nn, const int* __restrict__ list, const int* __restrict__ ovf,
+                             const int* __restrict__ redo, const int* __restrict__ ups, const i64* __restrict__ upptr,
+                             int* __restrict__ up) {
+  const i64 t = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (i >= nn || ovf[i] || redo[i]) return;
+  if (t >= nn) return;
+  const i64 i = list ? list[t] : t;
+  if (ovf[i] || redo[i]) return;
   const i64 b = upptr[i], n = upptr[i + 1] - b;
   for (i64 t = lane; t < n; t += 32) up[b + t] = ups[i * N2UPC + t];
 }
@@ -1346,9 +1365,15 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     // it per build from the caching allocator costs more than the pass it saves)
     static DevBuf<int> ups;
     if (ups.n < n_nodes * N2UPC) ups.alloc(n_nodes * N2UPC);
-    DevBuf<int> redo(n_nodes);
-    k_n2w<<<grid_for(n_nodes, N2WPB), N2WPB * 32, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, lower.p,
-                                                                 uptr.p, nullptr, nullptr, 0, ovf.p, ups.p, redo.p);
+    DevBuf<int> redo(n_nodes), nlist(n_nodes), ncount(1);
+    ncount.zero();
+    k_n2_nodes<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, sptr.p, tptr.p, lower.p, uptr.p, redo.p,
+                                                             nlist.p, ncount.p);
+    CF_LAUNCHED();
+    const int nl = read_dev(ncount.p);
+    if (nl > 0)
+      k_n2w<<<grid_for(nl, N2WPB), N2WPB * 32, 0, stream()>>>(nl, nlist.p, sptr.p, sidx.p, tptr.p, tidx.p, lower.p,
+                                                              uptr.p, nullptr, nullptr, 0, ovf.p, ups.p, redo.p);
     CF_LAUNCHED();
     OvfList big2 = make_ovf_list(n_nodes, ovf.p);
     DevBuf<i64> noff;
@@ -1370,11 +1395,13 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     scan_excl(uptr.p, n_nodes + 1);
     const i64 nup = read_dev(uptr.p + n_nodes);
     DevBuf<int> up(std::max<i64>(nup, 1));
-    k_n2w<<<grid_for(n_nodes, N2WPB), N2WPB * 32, 0, stream()>>>(n_nodes, sptr.p, sidx.p, tptr.p, tidx.p, nullptr,
-                                                                 nullptr, uptr.p, up.p, 1, ovf.p, nullptr, redo.p);
-    CF_LAUNCHED();
-    k_n2_compact<<<grid_for(n_nodes * 32, 256), 256, 0, stream()>>>(n_nodes, ovf.p, redo.p, ups.p, uptr.p, up.p);
-    CF_LAUNCHED();
+    if (nl > 0) {
+      k_n2w<<<grid_for(nl, N2WPB), N2WPB * 32, 0, stream()>>>(nl, nlist.p, sptr.p, sidx.p, tptr.p, tidx.p, nullptr,
+                                                              nullptr, uptr.p, up.p, 1, ovf.p, nullptr, redo.p);
+      CF_LAUNCHED();
+      k_n2_compact<<<grid_for(i64(nl) * 32, 256), 256, 0, stream()>>>(nl, nlist.p, ovf.p, redo.p, ups.p, uptr.p, up.p);
+      CF_LAUNCHED();
+    }
     if (big2.n) {
       k_n2_big<<<grid_for(big2.n, 64), 64, 0, stream()>>>(big2.n, big2.list.p, noff.p, sptr.p, sidx.p, tptr.p, tidx.p,
                                                           nkeys.p, nullptr, nullptr, uptr.p, up.p, 1);
