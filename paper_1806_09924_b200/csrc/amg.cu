@@ -438,13 +438,16 @@ __global__ void k_strength(i64 nn, const i64* __restrict__ nptr, const int* __re
 }
 
 // the strong lists stored by the counting pass -> CSR (warp per node; overflow-tier nodes skipped)
+// G lanes per node: 32 for the fine levels (tens of strong neighbours), 1 where most nodes have
+// none (the dof-less coarse nodes of the phi levels), so the launch is not a warp per empty node
+template <int G>
 __global__ void k_strength_compact(i64 nn, const int* __restrict__ ovf, const int* __restrict__ stmp,
                                    const i64* __restrict__ sptr, int* __restrict__ sidx) {
-  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) / G;
+  const int lane = threadIdx.x % G;
   if (i >= nn || ovf[i]) return;
   const i64 b = sptr[i], n = sptr[i + 1] - b;
-  for (i64 t = lane; t < n; t += 32) sidx[b + t] = stmp[i * SCAP + t];
+  for (i64 t = lane; t < n; t += G) sidx[b + t] = stmp[i * SCAP + t];
 }
 
 // ------------------------------------------------------------------ N2 dependency graph
@@ -1334,7 +1337,10 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     scan_excl(sptr.p, n_nodes + 1);
     const i64 ns = read_dev(sptr.p + n_nodes);
     DevBuf<int> sidx(std::max<i64>(ns, 1));
-    k_strength_compact<<<grid_for(n_nodes * 32, 256), 256, 0, stream()>>>(n_nodes, ovf.p, stmp.p, sptr.p, sidx.p);
+    if (ns >= 8 * n_nodes)
+      k_strength_compact<32><<<grid_for(n_nodes * 32, 256), 256, 0, stream()>>>(n_nodes, ovf.p, stmp.p, sptr.p, sidx.p);
+    else
+      k_strength_compact<1><<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, ovf.p, stmp.p, sptr.p, sidx.p);
     CF_LAUNCHED();
     if (big.n) {
       k_strength_big_emit<<<grid_for(big.n, 128), 128, 0, stream()>>>(big.n, big.list.p, boff.p, bkeys.p, bsums.p,
