@@ -644,13 +644,15 @@ __global__ void k_n2_compact(i64 nn, const int* __restrict__ list, const int* __
 // ------------------------------------------------------------------ pass 1: LFMIS frontier rounds
 constexpr int UND = 0, ROOT = 1, NOTROOT = 2;
 
-__global__ void k_lfmis_init(i64 nn, const int* __restrict__ lower, int* __restrict__ status, int* __restrict__ front,
-                             int* __restrict__ fsize) {
+// roots without dependents (isolated nodes: active phi dofs, dof-less coarse nodes) are decided
+// here and never enter a frontier (they would message nobody)
+__global__ void k_lfmis_init(i64 nn, const int* __restrict__ lower, const i64* __restrict__ up_ptr,
+                             int* __restrict__ status, int* __restrict__ front, int* __restrict__ fsize) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nn) return;
   if (lower[i] == 0) {
     status[i] = ROOT;
-    front[atomicAdd(fsize, 1)] = int(i);
+    if (up_ptr[i + 1] > up_ptr[i]) front[atomicAdd(fsize, 1)] = int(i);
   } else {
     status[i] = UND;
   }
@@ -1418,7 +1420,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     // pass 1: lexicographically-first MIS of N2 (persistent cooperative frontier kernel)
     DevBuf<int> status(n_nodes), f0(n_nodes), f1(n_nodes), sizes(3), rounds(1);
     sizes.zero();
-    k_lfmis_init<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, lower.p, status.p, f0.p, sizes.p);
+    k_lfmis_init<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, lower.p, uptr.p, status.p, f0.p, sizes.p);
     CF_LAUNCHED();
     {
       int bps = 0;
