@@ -229,10 +229,11 @@ template <int TPR, int U, int D>
 __device__ __forceinline__ double row_dot_st(const i64* __restrict__ ptr, const double* __restrict__ val,
                                              const double* __restrict__ x, i64 row, int lane, const StencilCols& sc,
                                              const int* __restrict__ off) {
-  StGeo<D> G;
-  st_geo<D>(sc, row, G);
   double s = 0.0;
   const i64 b0 = ptr[row], e = ptr[row + 1];
+  if (e == b0) return s;  // empty row (an active phi row of M_phiu): no geometry needed
+  StGeo<D> G;
+  st_geo<D>(sc, row, G);
   for (i64 k0 = b0 + lane; k0 < e; k0 += i64(TPR) * U) {
     double v[U], xv[U];
     int c[U];
