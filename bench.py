@@ -124,6 +124,12 @@ class ClockSampler:
                                           "--format=csv,noheader,nounits", "-lms", "200"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
+            # nvidia-smi's start-up (NVML initialisation) must not fall inside the timed region:
+            # wait for its first sample, then drop it, so every kept sample is taken while timing
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.02)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -411,16 +417,19 @@ def ours(args):
     l0 = cf.kernel_launches()
     reps = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]  # per-step split (no syncs)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         e0.record(s)
-        for _ in range(args.steps):
+        for k in range(args.steps):
             st, rep = step()
             reps.append(rep)
+            marks[k].record(s)
         e1.record(s)
         torch.cuda.synchronize()
     launches = cf.kernel_launches() - l0
     ms = e0.elapsed_time(e1) / args.steps
+    ms_each = [e0.elapsed_time(marks[0])] + [marks[k - 1].elapsed_time(marks[k]) for k in range(1, args.steps)]
     its = sum(len(r["iterations"]) for r in reps) / args.steps
     if world > 1:
         t = torch.tensor([ms], device=device)
@@ -481,7 +490,7 @@ def ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Sneddon state)",
         "config": dict(CONFIG if args.workload == "cfg3" else CONFIG4, parallelism="single GPU" if world == 1 else
                        f"{world} GPUs: z-slab decomposition, NCCL halo planes, restricted additive Schwarz (per-slab block AMG)"),
-        "newton_iterations_per_step": its, "ms_per_newton_iteration": ms / its,
+        "ms_each_step": ms_each, "newton_iterations_per_step": its, "ms_per_newton_iteration": ms / its,
         "gmres_iterations": [r["gmres_iterations"] for r in last["iterations"]],
         "active_set_final": last["iterations"][-1]["active_size"],
         "phase_ms_last_step": last["times_ms"], "device_mem_used_gb": (total - free) / 1e9,
