@@ -1166,8 +1166,11 @@ double estimate_lambda_max(const Csr& A, const double* inv_diag) {  // linsolve.
   // 15 iterations without a host round trip each (the reference's early return on a zero norm is
   // the device flag; the values are the same IEEE sequence)
   for (int it = 0; it < 15; ++it) {
-    csr_spmv_add(A, v.p, w.p, nullptr);
-    vdiag_mul(inv_diag, w.p, w.p, 1.0, n);
+    SpmvEpi ep;  // w = 1.0 * (D^-1 (A v)): vdiag_mul's expression in the SpMV epilogue
+    ep.d = inv_diag;
+    ep.w = 1.0;
+    ep.mode = 3;
+    csr_spmv_epi(A, v.p, w.p, ep);
     vdot_dev(w.p, w.p, n, s, true);
     k_lambda_step<<<1, 1, 0, stream()>>>(s, s + 2);
     CF_LAUNCHED();

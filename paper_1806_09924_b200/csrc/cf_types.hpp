@@ -120,6 +120,7 @@ std::unique_ptr<BlockSystem> assemble_pattern(const Problem& P, const Constraint
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add);  // y = A x (+ add)
 // row epilogue of a fused SpMV (A square for modes 1 and 2; y must not alias x):
 //   0: y = A x (+ b)   1: y = b - A x (residual)   2: y = x + w (d (b - A x)) (one damped Jacobi sweep)
+//   3: y = w (d (A x)) (the power iteration's D^-1 A x with w = 1)
 // each mode is the same IEEE operation sequence as the SpMV followed by the separate vector kernel
 struct SpmvEpi {
   const double* b = nullptr;
