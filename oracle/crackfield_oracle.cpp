@@ -12,21 +12,42 @@
 //  Pinning: the reference cannot be built here (Eigen3, doctest, CLI11 are absent;
 //  SURVEY §8c), so this restatement is pinned against the reference's own known-answer
 //  tests (model_test, linsolve_test, solver_test, fem_test, postproc_test,
-//  reference_test KATs; see tests/test_oracle_kat.py).  Eigen's internal arithmetic
-//  (vectorised reduction order in norm()/dot(), blocked PartialPivLU) is NOT
-//  reproduced bit-for-bit: every reduction here is a left-to-right sequential sum, the
-//  coarse LU is unblocked.  ColPivHouseholderQR, makeHouseholder and
-//  applyHouseholderOnTheLeft follow Eigen 3.3's published algorithm step by step.
+//  reference_test KATs; see tests/test_oracle_kat.py).  ColPivHouseholderQR,
+//  makeHouseholder and applyHouseholderOnTheLeft follow Eigen 3.3's published algorithm
+//  step by step; the coarse LU is unblocked (Eigen blocks above 16 rows).
+//
+//  Two reduction orders (orc_set_order), because Eigen's own order is not pinned by any
+//  reference test:
+//   * ORDER_PRODUCT (0, default): the product's documented deterministic order.  An SpMV
+//     row is split over TPR lanes (lane l sums entries l, l+TPR, ...; xor butterfly), TPR
+//     from the mean row length; a dot/norm is a 256-thread block tree over a fixed grid.
+//     This is NOT the reference's order: it is the order the B200 kernels use, adopted
+//     here so that the device can be checked bit for bit (same algorithm, same order).
+//   * ORDER_REFERENCE (1): the reference's arithmetic as written — every CSR row is one
+//     left-to-right sum (Eigen's RowMajor sparse x dense, linsolve.cpp:16-17,304-311),
+//     every dot/norm one sequential sum (linsolve.cpp:30,38,57,60).  The device is checked
+//     against this mode at the north-star tolerances (1e-8 solution, 1e-6 COD/TCV, +-10%
+//     Newton/GMRES counts), not bitwise.
+//  Everything else (assembly in the reference's cell order, SpGEMM as k-ascending
+//  sequential sums, QR, LU, the aggregation greedy) is the same in both modes.
+//
+//  Threads (orc_set_threads): results are bitwise independent of the thread count.  With
+//  one thread the assembly is the literal cell loop of model.cpp; with more, every row is
+//  owned by one vertex that sums its cells' contributions in the same reference cell
+//  order (tests/test_oracle_kat.py checks the two forms bit for bit).
 //
 //  Compile with -ffp-contract=off (no FMA contraction) so the element arithmetic is
 //  the reference's expression order exactly.
 // =====================================================================================
 #include <algorithm>
+#include <chrono>
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <malloc.h>
 #include <functional>
 #include <map>
 #include <memory>
@@ -88,6 +109,7 @@ struct Grid {
   i64 nc = 1, nn = 2, V = 4, ncells = 1;
   double unit = 0.0, h = 0.0, detJ = 0.0;
   std::vector<i64> cell_order;  // cells in the reference's active-cell order
+  std::vector<i64> cell_rank;   // inverse permutation: position of a cell in cell_order
 
   // mesh.hpp:73 to_physical(c) with c = i * isize, isize = kUnit >> r
   double coord(i64 i) const { return -K + double(i * (i64(1) << (16 - r))) * unit; }
@@ -143,6 +165,8 @@ static void build_cell_order(Grid& g) {
       g.cell_order[pos++] = g.cid((rx << r) + l[0], (ry << r) + l[1], (rz << r) + l[2]);
     }
   }
+  g.cell_rank.resize(g.ncells);
+  for (i64 p = 0; p < g.ncells; ++p) g.cell_rank[g.cell_order[p]] = p;
 }
 
 static Grid make_grid(int d, double K, int n0, int r) {
@@ -292,11 +316,34 @@ static Constraints build_constraints(const Grid& g, bool clamp, const std::vecto
 }
 
 // ------------------------------------------------------------------ CSR
+// Large arrays are allocated without value-initialisation (resize() leaves them untouched), so
+// the first touch happens in the parallel loops that fill them.
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = UninitAlloc<U>;
+  };
+  UninitAlloc() = default;
+  template <class U>
+  UninitAlloc(const UninitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+template <class T>
+using uvec = std::vector<T, UninitAlloc<T>>;
+
 struct Csr {
   i64 rows = 0, cols = 0;
-  std::vector<i64> ptr{0};
-  std::vector<int> col;
-  std::vector<double> val;
+  uvec<i64> ptr{0};
+  uvec<int> col;
+  uvec<double> val;
   i64 nnz() const { return i64(col.size()); }
   double coeff(i64 i, i64 j) const {
     for (i64 k = ptr[i]; k < ptr[i + 1]; ++k)
@@ -305,17 +352,38 @@ struct Csr {
   }
 };
 
-// ---- Reduction-order contract.  Eigen's own reduction order (vectorised dot/norm, sparse
-// row sums) is not pinned by any reference test, so the oracle adopts the product's documented
-// deterministic order: a row of an SpMV is split over a group of
-// TPR lanes (lane l sums entries l, l+TPR, ... sequentially; the lanes are then combined by an
-// xor butterfly), TPR chosen from the mean row length; dot products use a fixed grid of
-// 256-thread blocks (grid-stride sequential per thread, tree per block, one ordered final block).
+// ---- Reduction order (see the header): ORDER_PRODUCT = the device's documented order,
+// ORDER_REFERENCE = the reference's sequential sums.
+enum { ORDER_PRODUCT = 0, ORDER_REFERENCE = 1 };
+static int g_order = ORDER_PRODUCT;
+
+// ORC_TIMING=1: phase times on stderr (profiling of the CPU baseline only)
+static bool timing_on() {
+  static const bool on = std::getenv("ORC_TIMING") != nullptr;
+  return on;
+}
+struct PhaseTimer {
+  const char* name;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit PhaseTimer(const char* n) : name(n) {}
+  ~PhaseTimer() {
+    if (timing_on())
+      std::fprintf(stderr, "[orc] %-18s %9.1f ms\n", name,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 static int spmv_tpr(const Csr& A) {
+  if (g_order == ORDER_REFERENCE) return 1;
   const double mean = A.rows ? double(A.nnz()) / double(A.rows) : 0.0;
   return mean > 64 ? 16 : (mean > 24 ? 8 : 4);
 }
 static double row_sum_lanes(const Csr& A, i64 i, const double* x, int tpr) {
+  if (tpr == 1) {  // Eigen RowMajor sparse x dense: tmp = 0; tmp += v * x[c] in storage order
+    double s = 0.0;
+    for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) s += A.val[k] * x[A.col[k]];
+    return s;
+  }
   double lane[32];
   for (int l = 0; l < tpr; ++l) {
     double s = 0.0;
@@ -329,28 +397,50 @@ static double row_sum_lanes(const Csr& A, i64 i, const double* x, int tpr) {
   }
   return lane[0];
 }
-// Row-parallel SpMV on a persistent host thread pool (orc_set_threads; 1 = the single-threaded
-// reference).  The reference's only multi-threaded kernel is Eigen's sparse x dense product under
-// Eigen::setNbThreads (crackfield.cpp:39); every row is still summed exactly as above, so results do
-// not depend on the thread count.
+// Persistent host thread pool (orc_set_threads; 1 = the single-threaded reference).  Work is
+// split into chunks whose results never depend on the split: every floating-point sum keeps
+// its sequential order, so results are bitwise independent of the thread count.
 class RowPool {
  public:
   void resize(int n) {
     stop_all();
     n_ = std::max(1, n);
-    for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { loop(t); });
+    const int g0 = gen_;  // new workers wait for the next dispatch, not the ones already done
+    for (int t = 1; t < n_; ++t) th_.emplace_back([this, t, g0] { loop(t, g0); });
   }
   int size() const { return n_; }
   template <class F>
-  void run(i64 rows, F&& f) {  // f(lo, hi) over n_ chunks, chunk 0 on the caller
+  void run(i64 rows, F&& f) {  // f(lo, hi) over n_ static chunks, chunk 0 on the caller
     if (n_ == 1 || rows < 4096) {
       f(i64(0), rows);
       return;
     }
-    std::function<void(int)> job = [&](int t) {
+    dispatch([&](int t) {
       const i64 chunk = (rows + n_ - 1) / n_;
       f(std::min(rows, t * chunk), std::min(rows, (t + 1) * chunk));
-    };
+    });
+  }
+  // f(tid, lo, hi) over dynamically claimed chunks of `grain` items
+  template <class F>
+  void run_dyn(i64 n, i64 grain, F&& f) {
+    grain = std::max<i64>(1, grain);
+    if (n_ == 1 || n <= grain) {
+      for (i64 lo = 0; lo < n; lo += grain) f(0, lo, std::min(n, lo + grain));
+      return;
+    }
+    std::atomic<i64> next{0};
+    dispatch([&](int t) {
+      for (;;) {
+        const i64 lo = next.fetch_add(grain);
+        if (lo >= n) break;
+        f(t, lo, std::min(n, lo + grain));
+      }
+    });
+  }
+  ~RowPool() { stop_all(); }
+
+ private:
+  void dispatch(const std::function<void(int)>& job) {
     {
       std::unique_lock<std::mutex> lk(m_);
       job_ = &job;
@@ -363,13 +453,9 @@ class RowPool {
     done_.wait(lk, [&] { return pending_ == 0; });
     job_ = nullptr;
   }
-  ~RowPool() { stop_all(); }
-
- private:
-  void loop(int t) {
-    int seen = 0;
+  void loop(int t, int seen) {
     for (;;) {
-      std::function<void(int)>* job;
+      const std::function<void(int)>* job;
       {
         std::unique_lock<std::mutex> lk(m_);
         cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
@@ -394,7 +480,7 @@ class RowPool {
   }
   int n_ = 1, gen_ = 0, pending_ = 0;
   bool stop_ = false;
-  std::function<void(int)>* job_ = nullptr;
+  const std::function<void(int)>* job_ = nullptr;
   std::vector<std::thread> th_;
   std::mutex m_;
   std::condition_variable cv_, done_;
@@ -402,6 +488,21 @@ class RowPool {
 static RowPool& row_pool() {
   static RowPool p;
   return p;
+}
+// Multi-GB vectors are allocated and freed many times per Newton iteration (GMRES, V-cycles, AMG
+// products).  glibc serves blocks above 32 MB with fresh mmaps, so each allocation page-faults
+// its whole size again; keep them in the heap instead (performance only).
+static const int g_malloc_tuned = [] {
+  mallopt(M_MMAP_MAX, 0);
+  mallopt(M_TRIM_THRESHOLD, -1);
+  return 1;
+}();
+// elementwise loop i in [0, n): f(i), split over the pool (no reductions)
+template <class F>
+static void par_for(i64 n, F&& f) {
+  row_pool().run(n, [&](i64 lo, i64 hi) {
+    for (i64 i = lo; i < hi; ++i) f(i);
+  });
 }
 
 static void spmv(const Csr& A, const double* x, double* y) {  // y = A x
@@ -417,77 +518,158 @@ static void spmv_add(const Csr& A, const double* x, double* y) {  // y += A x
   });
 }
 
+// Row-chunked CSR construction: rows [0, n) are produced by `emit(i, cols, vals)` (appending
+// row i's entries) over dynamically claimed chunks, then concatenated in row order.
+template <class Emit>
+static Csr build_rows(i64 rows, i64 cols, i64 grain, Emit&& emit) {
+  Csr C;
+  C.rows = rows;
+  C.cols = cols;
+  C.ptr.assign(rows + 1, 0);
+  const i64 nch = (rows + grain - 1) / grain;
+  std::vector<std::vector<int>> ccol(nch);
+  std::vector<std::vector<double>> cval(nch);
+  row_pool().run_dyn(nch, 1, [&](int tid, i64 c0, i64 c1) {
+    for (i64 c = c0; c < c1; ++c) {
+      const i64 lo = c * grain, hi = std::min(rows, lo + grain);
+      for (i64 i = lo; i < hi; ++i) {
+        emit(tid, i, ccol[c], cval[c]);
+        C.ptr[i + 1] = i64(ccol[c].size());  // chunk-local end, fixed below
+      }
+    }
+  });
+  std::vector<i64> base(nch + 1, 0);
+  for (i64 c = 0; c < nch; ++c) base[c + 1] = base[c] + i64(ccol[c].size());
+  par_for(rows, [&](i64 i) { C.ptr[i + 1] += base[i / grain]; });
+  C.col.resize(base[nch]);
+  C.val.resize(base[nch]);
+  row_pool().run_dyn(nch, 1, [&](int, i64 c0, i64 c1) {
+    for (i64 c = c0; c < c1; ++c) {
+      std::copy(ccol[c].begin(), ccol[c].end(), C.col.begin() + base[c]);
+      std::copy(cval[c].begin(), cval[c].end(), C.val.begin() + base[c]);
+      std::vector<int>().swap(ccol[c]);
+      std::vector<double>().swap(cval[c]);
+    }
+  });
+  return C;
+}
+
 static Csr transpose(const Csr& A) {
   Csr T;
   T.rows = A.cols;
   T.cols = A.rows;
   T.ptr.assign(T.rows + 1, 0);
-  for (i64 k = 0; k < A.nnz(); ++k) T.ptr[A.col[k] + 1]++;
-  for (i64 i = 0; i < T.rows; ++i) T.ptr[i + 1] += T.ptr[i];
   T.col.resize(A.nnz());
   T.val.resize(A.nnz());
-  std::vector<i64> pos(T.ptr.begin(), T.ptr.end() - 1);
-  for (i64 i = 0; i < A.rows; ++i)
-    for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-      const i64 p = pos[A.col[k]]++;
-      T.col[p] = int(i);
-      T.val[p] = A.val[k];
+  const int nt = row_pool().size();
+  if (nt == 1 || A.rows < 4096 || double(A.cols) * nt > 4e8) {
+    for (i64 k = 0; k < A.nnz(); ++k) T.ptr[A.col[k] + 1]++;
+    for (i64 i = 0; i < T.rows; ++i) T.ptr[i + 1] += T.ptr[i];
+    std::vector<i64> pos(T.ptr.begin(), T.ptr.end() - 1);
+    for (i64 i = 0; i < A.rows; ++i)
+      for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+        const i64 p = pos[A.col[k]]++;
+        T.col[p] = int(i);
+        T.val[p] = A.val[k];
+      }
+    return T;
+  }
+  // row chunks c = 0..nt-1; output row j lists chunk 0's entries, then chunk 1's, ... (each in
+  // row order), i.e. ascending source row exactly as the serial counting sort
+  const i64 chunk = (A.rows + nt - 1) / nt;
+  std::vector<std::vector<i64>> cnt(nt, std::vector<i64>(A.cols, 0));
+  row_pool().run_dyn(nt, 1, [&](int, i64 c0, i64) {
+    auto& cc = cnt[c0];
+    for (i64 i = c0 * chunk; i < std::min(A.rows, (c0 + 1) * chunk); ++i)
+      for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) cc[A.col[k]]++;
+  });
+  for (i64 j = 0; j < A.cols; ++j) {
+    i64 run = T.ptr[j];
+    for (int c = 0; c < nt; ++c) {
+      const i64 n = cnt[c][j];
+      cnt[c][j] = run;
+      run += n;
     }
+    T.ptr[j + 1] = run;
+  }
+  row_pool().run_dyn(nt, 1, [&](int, i64 c0, i64) {
+    auto& pos = cnt[c0];
+    for (i64 i = c0 * chunk; i < std::min(A.rows, (c0 + 1) * chunk); ++i)
+      for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+        const i64 p = pos[A.col[k]]++;
+        T.col[p] = int(i);
+        T.val[p] = A.val[k];
+      }
+  });
   return T;
 }
 
 // C = A * B, Gustavson: for each row i, for k in A.row(i) ascending, for j in B.row(k):
 // C(i,j) += A(i,k) B(k,j).  Structural nonzeros are kept (no numeric pruning), columns sorted.
-static Csr spgemm(const Csr& A, const Csr& B) {
-  Csr C;
-  C.rows = A.rows;
-  C.cols = B.cols;
-  C.ptr.assign(A.rows + 1, 0);
-  std::vector<i64> marker(B.cols, -1);
-  std::vector<double> acc(B.cols, 0.0);
-  std::vector<int> cols;
-  for (i64 i = 0; i < A.rows; ++i) {
-    cols.clear();
+// Rows are independent, so the row-chunked parallel form is bitwise the serial one.
+static Csr spgemm(const Csr& A, const Csr& B, const double* row_scale = nullptr) {
+  const int nt = row_pool().size();
+  std::vector<std::vector<i64>> marker(nt);
+  std::vector<std::vector<double>> acc(nt);
+  std::vector<std::vector<int>> cols(nt);
+  return build_rows(A.rows, B.cols, 2048, [&](int t, i64 i, std::vector<int>& oc, std::vector<double>& ov) {
+    auto& mk = marker[t];
+    auto& ac = acc[t];
+    auto& cl = cols[t];
+    if (mk.empty()) {
+      mk.assign(B.cols, -1);
+      ac.assign(B.cols, 0.0);
+    }
+    cl.clear();
     for (i64 ka = A.ptr[i]; ka < A.ptr[i + 1]; ++ka) {
       const i64 k = A.col[ka];
-      const double a = A.val[ka];
+      const double a = row_scale ? row_scale[i] * A.val[ka] : A.val[ka];  // (D^-1 A)(i,k) when scaled
       for (i64 kb = B.ptr[k]; kb < B.ptr[k + 1]; ++kb) {
         const int j = B.col[kb];
-        if (marker[j] != i) {
-          marker[j] = i;
-          acc[j] = a * B.val[kb];
-          cols.push_back(j);
+        if (mk[j] != i) {
+          mk[j] = i;
+          ac[j] = a * B.val[kb];
+          cl.push_back(j);
         } else {
-          acc[j] += a * B.val[kb];
+          ac[j] += a * B.val[kb];
         }
       }
     }
-    std::sort(cols.begin(), cols.end());
-    for (int j : cols) {
-      C.col.push_back(j);
-      C.val.push_back(acc[j]);
+    std::sort(cl.begin(), cl.end());
+    for (int j : cl) {
+      oc.push_back(j);
+      ov.push_back(ac[j]);
     }
-    C.ptr[i + 1] = i64(C.col.size());
-  }
-  return C;
+  });
 }
 
 // Eigen SparseMatrix::prune(1.0, 1e-300): keep |v| > 1e-300
 static void prune(Csr& A) {
-  i64 w = 0;
-  std::vector<i64> nptr(A.rows + 1, 0);
-  for (i64 i = 0; i < A.rows; ++i) {
+  uvec<i64> cnt(A.rows + 1);
+  cnt[0] = 0;
+  par_for(A.rows, [&](i64 i) {
+    i64 c = 0;
+    for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) c += std::abs(A.val[k]) > 1e-300;
+    cnt[i + 1] = c;
+  });
+  for (i64 i = 0; i < A.rows; ++i) cnt[i + 1] += cnt[i];
+  if (cnt[A.rows] == A.nnz()) return;
+  Csr B;
+  B.rows = A.rows;
+  B.cols = A.cols;
+  B.col.resize(cnt[A.rows]);
+  B.val.resize(cnt[A.rows]);
+  par_for(A.rows, [&](i64 i) {
+    i64 w = cnt[i];
     for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
       if (std::abs(A.val[k]) > 1e-300) {
-        A.col[w] = A.col[k];
-        A.val[w] = A.val[k];
+        B.col[w] = A.col[k];
+        B.val[w] = A.val[k];
         ++w;
       }
-    nptr[i + 1] = w;
-  }
-  A.ptr = nptr;
-  A.col.resize(w);
-  A.val.resize(w);
+  });
+  B.ptr = std::move(cnt);
+  A = std::move(B);
 }
 
 // ------------------------------------------------------------------ block system (linsolve.hpp:17-28)
@@ -516,67 +698,102 @@ static void check_material(const orc_material& m) {  // model.cpp:8-17
   if (!(m.G_c > 0.0)) throw std::invalid_argument("Material: G_c must be positive");
 }
 
-static Vec assemble_residual(const Grid& g, const Constraints& cs, const orc_material& mat,
-                             const orc_regularization& reg, const double* solution, const double* phi_tilde) {
+// Element residual of one cell (the body of the cell loop, model.cpp:136-196): ru[k*d+a], rphi[k]
+static void cell_residual(const Grid& g, const QpData& qp, const orc_material& mat, const orc_regularization& reg,
+                          const double* solution, const double* phi_tilde, i64 id, double* ru, double* rphi) {
   const int d = g.d, nv = 1 << d;
   const double kap = reg.kappa, eps = reg.eps, p = mat.pressure, Gc = mat.G_c;
   const double mu = mat_mu(mat), lam = mat_lambda(mat);
-  static thread_local QpData qp2, qp3;
-  QpData& qp = (d == 2) ? qp2 : qp3;
-  if (qp.nq == 0) qp = make_qp_data(d);
   const i64 nu = g.n_u();
-  Vec R(g.n_total(), 0.0);
-  double uloc[8][3], philoc[8], ptloc[8], ru[24], rphi[8];
+  double uloc[8][3], philoc[8], ptloc[8];
   i64 verts[8];
   const double h = g.h, detJ = g.detJ;
-  for (i64 id : g.cell_order) {
-    g.cell_vertices(id, verts);
+  g.cell_vertices(id, verts);
+  for (int k = 0; k < nv; ++k) {
+    for (int a = 0; a < d; ++a) uloc[k][a] = solution[verts[k] * d + a];
+    philoc[k] = solution[nu + verts[k]];
+    ptloc[k] = phi_tilde[verts[k]];
+  }
+  for (int i = 0; i < nv * d; ++i) ru[i] = 0.0;
+  for (int i = 0; i < nv; ++i) rphi[i] = 0.0;
+  for (int q = 0; q < qp.nq; ++q) {
+    const double* s = qp.shape[q];
+    double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    double gphi[3] = {0, 0, 0};
+    double phi = 0.0, pt = 0.0;
     for (int k = 0; k < nv; ++k) {
-      for (int a = 0; a < d; ++a) uloc[k][a] = solution[verts[k] * d + a];
-      philoc[k] = solution[nu + verts[k]];
-      ptloc[k] = phi_tilde[verts[k]];
-    }
-    for (int i = 0; i < nv * d; ++i) ru[i] = 0.0;
-    for (int i = 0; i < nv; ++i) rphi[i] = 0.0;
-    for (int q = 0; q < qp.nq; ++q) {
-      const double* s = qp.shape[q];
-      double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-      double gphi[3] = {0, 0, 0};
-      double phi = 0.0, pt = 0.0;
-      for (int k = 0; k < nv; ++k) {
-        phi += s[k] * philoc[k];
-        pt += s[k] * ptloc[k];
-        for (int b = 0; b < d; ++b) {
-          gphi[b] += philoc[k] * qp.grads[q][k][b] / h;
-          for (int a = 0; a < d; ++a) gu[a][b] += uloc[k][a] * qp.grads[q][k][b] / h;
-        }
-      }
-      double e[3][3], sig[3][3];
-      for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
-      double tre = 0.0;
-      for (int a = 0; a < d; ++a) tre += e[a][a];
-      for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) sig[a][b] = 2.0 * mu * e[a][b];
-      for (int a = 0; a < d; ++a) sig[a][a] += lam * tre;
-      double sig_ee = 0.0;
-      for (int a = 0; a < d; ++a)
-        for (int b = 0; b < d; ++b) sig_ee += sig[a][b] * e[a][b];
-      const double gcoef = (1.0 - kap) * pt * pt + kap;
-      const double pphi = (mat.pressure_coupling == 0) ? pt * pt : phi * phi;
-      const double w = qp.wts[q] * detJ;
-      for (int k = 0; k < nv; ++k) {
-        for (int a = 0; a < d; ++a) {
-          double val = 0.0;
-          for (int b = 0; b < d; ++b) val += gcoef * sig[a][b] * qp.grads[q][k][b] / h;
-          val += pphi * p * qp.grads[q][k][a] / h;
-          ru[k * d + a] += w * val;
-        }
-        double vphi = ((1.0 - kap) * phi * sig_ee + 2.0 * phi * p * tre - Gc / eps * (1.0 - phi)) * s[k];
-        for (int b = 0; b < d; ++b) vphi += Gc * eps * gphi[b] * qp.grads[q][k][b] / h;
-        rphi[k] += w * vphi;
+      phi += s[k] * philoc[k];
+      pt += s[k] * ptloc[k];
+      for (int b = 0; b < d; ++b) {
+        gphi[b] += philoc[k] * qp.grads[q][k][b] / h;
+        for (int a = 0; a < d; ++a) gu[a][b] += uloc[k][a] * qp.grads[q][k][b] / h;
       }
     }
+    double e[3][3], sig[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
+    double tre = 0.0;
+    for (int a = 0; a < d; ++a) tre += e[a][a];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) sig[a][b] = 2.0 * mu * e[a][b];
+    for (int a = 0; a < d; ++a) sig[a][a] += lam * tre;
+    double sig_ee = 0.0;
+    for (int a = 0; a < d; ++a)
+      for (int b = 0; b < d; ++b) sig_ee += sig[a][b] * e[a][b];
+    const double gcoef = (1.0 - kap) * pt * pt + kap;
+    const double pphi = (mat.pressure_coupling == 0) ? pt * pt : phi * phi;
+    const double w = qp.wts[q] * detJ;
+    for (int k = 0; k < nv; ++k) {
+      for (int a = 0; a < d; ++a) {
+        double val = 0.0;
+        for (int b = 0; b < d; ++b) val += gcoef * sig[a][b] * qp.grads[q][k][b] / h;
+        val += pphi * p * qp.grads[q][k][a] / h;
+        ru[k * d + a] += w * val;
+      }
+      double vphi = ((1.0 - kap) * phi * sig_ee + 2.0 * phi * p * tre - Gc / eps * (1.0 - phi)) * s[k];
+      for (int b = 0; b < d; ++b) vphi += Gc * eps * gphi[b] * qp.grads[q][k][b] / h;
+      rphi[k] += w * vphi;
+    }
+  }
+}
+
+static const QpData& qp_data(int d) {
+  static const QpData q2 = make_qp_data(2), q3 = make_qp_data(3);
+  return d == 2 ? q2 : q3;
+}
+
+// Cells incident to a vertex, in the reference cell order, with the vertex's corner index
+struct CellRef {
+  i64 rank, id;
+  int k;
+};
+static int incident_cells(const Grid& g, i64 v, CellRef* out) {
+  i64 x, y, z;
+  g.vxyz(v, x, y, z);
+  int n = 0;
+  for (int k = 0; k < (1 << g.d); ++k) {
+    const i64 cx = x - (k & 1), cy = y - ((k >> 1) & 1), cz = z - ((k >> 2) & 1);
+    if (cx < 0 || cy < 0 || cz < 0 || cx >= g.nc || cy >= g.nc || (g.d == 3 && cz >= g.nc)) continue;
+    const i64 id = g.cid(cx, cy, cz);
+    out[n++] = CellRef{g.cell_rank[id], id, k};
+  }
+  for (int i = 1; i < n; ++i)
+    for (int j = i; j > 0 && out[j].rank < out[j - 1].rank; --j) std::swap(out[j], out[j - 1]);
+  return n;
+}
+
+// assemble_residual (model.cpp:127-202): the cell loop in the reference's cell order.
+static Vec assemble_residual_seq(const Grid& g, const Constraints& cs, const orc_material& mat,
+                                 const orc_regularization& reg, const double* solution, const double* phi_tilde) {
+  const int d = g.d, nv = 1 << d;
+  const QpData& qp = qp_data(d);
+  const i64 nu = g.n_u();
+  Vec R(g.n_total(), 0.0);
+  double ru[24], rphi[8];
+  i64 verts[8];
+  for (i64 id : g.cell_order) {
+    cell_residual(g, qp, mat, reg, solution, phi_tilde, id, ru, rphi);
+    g.cell_vertices(id, verts);
     for (int k = 0; k < nv; ++k) {  // Scatter::vector_add (model.cpp:74-80); entry-free lines drop
       for (int a = 0; a < d; ++a) {
         const i64 dof = verts[k] * d + a;
@@ -587,6 +804,46 @@ static Vec assemble_residual(const Grid& g, const Constraints& cs, const orc_mat
     }
   }
   return R;
+}
+
+// The same sums, thread-parallel: element residuals of every cell, then each dof adds its
+// cells' contributions in the reference cell order (bitwise the cell loop).
+static Vec assemble_residual_par(const Grid& g, const Constraints& cs, const orc_material& mat,
+                                 const orc_regularization& reg, const double* solution, const double* phi_tilde) {
+  const int d = g.d, nv = 1 << d, st = nv * (d + 1);
+  const QpData& qp = qp_data(d);
+  const i64 nu = g.n_u();
+  std::vector<double> el(size_t(g.ncells) * st);
+  row_pool().run_dyn(g.ncells, 1024, [&](int, i64 lo, i64 hi) {
+    for (i64 id = lo; id < hi; ++id) {
+      double* e = el.data() + size_t(id) * st;
+      cell_residual(g, qp, mat, reg, solution, phi_tilde, id, e, e + nv * d);
+    }
+  });
+  Vec R(g.n_total(), 0.0);
+  row_pool().run_dyn(g.V, 4096, [&](int, i64 lo, i64 hi) {
+    CellRef cells[8];
+    for (i64 v = lo; v < hi; ++v) {
+      const int n = incident_cells(g, v, cells);
+      for (int a = 0; a <= d; ++a) {
+        const i64 dof = (a < d) ? v * d + a : nu + v;
+        if (cs.is(dof)) continue;
+        double s = 0.0;
+        for (int c = 0; c < n; ++c) {
+          const double* e = el.data() + size_t(cells[c].id) * st;
+          s += (a < d) ? e[cells[c].k * d + a] : e[nv * d + cells[c].k];
+        }
+        R[dof] = s;
+      }
+    }
+  });
+  return R;
+}
+
+static Vec assemble_residual(const Grid& g, const Constraints& cs, const orc_material& mat,
+                             const orc_regularization& reg, const double* solution, const double* phi_tilde) {
+  return row_pool().size() > 1 ? assemble_residual_par(g, cs, mat, reg, solution, phi_tilde)
+                               : assemble_residual_seq(g, cs, mat, reg, solution, phi_tilde);
 }
 
 // Vertex neighbourhood (3^d, lexicographic = ascending vertex index)
@@ -681,9 +938,9 @@ static void drop_zero_constrained_diag(Csr& A, const Constraints& cs, i64 off) {
   A = std::move(B);
 }
 
-static BlockSystem assemble_jacobian(const Grid& g, const Constraints& cs, const orc_material& mat,
-                                     const orc_regularization& reg, const double* solution,
-                                     const double* phi_tilde) {
+static BlockSystem assemble_jacobian_seq(const Grid& g, const Constraints& cs, const orc_material& mat,
+                                         const orc_regularization& reg, const double* solution,
+                                         const double* phi_tilde) {
   const int d = g.d, nv = 1 << d;
   const double kap = reg.kappa, eps = reg.eps, p = mat.pressure, Gc = mat.G_c;
   const double mu = mat_mu(mat), lam = mat_lambda(mat);
@@ -789,6 +1046,207 @@ static BlockSystem assemble_jacobian(const Grid& g, const Constraints& cs, const
   return J;
 }
 
+// Pattern rows of one vertex (the serial build_pattern's rule): uu rows v*d+a, the pu and pp rows
+// of the phi dof; returns the entries written (cols may be null to count only).
+static void pattern_rows(const Grid& g, const Constraints& cs, i64 v, int* uu_cols, i64* uu_len, int* pu_cols,
+                         i64* pu_len, int* pp_cols, i64* pp_len) {
+  const int d = g.d;
+  const i64 nu = g.n_u();
+  i64 nb[27];
+  const int n = vertex_neighbours(g, v, nb);
+  for (int a = 0; a < d; ++a) {
+    const i64 row = v * d + a;
+    i64 c = 0;
+    if (cs.is(row)) {
+      if (uu_cols) uu_cols[c] = int(row);
+      ++c;
+    } else {
+      for (int t = 0; t < n; ++t)
+        for (int b = 0; b < d; ++b)
+          if (!cs.is(nb[t] * d + b)) {
+            if (uu_cols) uu_cols[c] = int(nb[t] * d + b);
+            ++c;
+          }
+    }
+    uu_len[a] = c;
+    if (uu_cols) uu_cols += c;
+  }
+  i64 cp = 0, cq = 0;
+  if (!cs.is(nu + v)) {
+    for (int t = 0; t < n; ++t)
+      for (int b = 0; b < d; ++b)
+        if (!cs.is(nb[t] * d + b)) {
+          if (pu_cols) pu_cols[cp] = int(nb[t] * d + b);
+          ++cp;
+        }
+    for (int t = 0; t < n; ++t)
+      if (!cs.is(nu + nb[t])) {
+        if (pp_cols) pp_cols[cq] = int(nb[t]);
+        ++cq;
+      }
+  } else {
+    if (pp_cols) pp_cols[0] = int(v);
+    cq = 1;
+  }
+  *pu_len = cp;
+  *pp_len = cq;
+}
+
+static void build_pattern_par(const Grid& g, const Constraints& cs, BlockSystem& J) {
+  const int d = g.d;
+  const i64 nu = g.n_u(), np = g.n_phi();
+  J.uu.rows = J.uu.cols = nu;
+  J.pu.rows = np;
+  J.pu.cols = nu;
+  J.pp.rows = J.pp.cols = np;
+  J.uu.ptr.assign(nu + 1, 0);
+  J.pu.ptr.assign(np + 1, 0);
+  J.pp.ptr.assign(np + 1, 0);
+  par_for(g.V, [&](i64 v) {
+    i64 ul[3], pl, ql;
+    pattern_rows(g, cs, v, nullptr, ul, nullptr, &pl, nullptr, &ql);
+    for (int a = 0; a < d; ++a) J.uu.ptr[v * d + a + 1] = ul[a];
+    J.pu.ptr[v + 1] = pl;
+    J.pp.ptr[v + 1] = ql;
+  });
+  for (i64 i = 0; i < nu; ++i) J.uu.ptr[i + 1] += J.uu.ptr[i];
+  for (i64 i = 0; i < np; ++i) {
+    J.pu.ptr[i + 1] += J.pu.ptr[i];
+    J.pp.ptr[i + 1] += J.pp.ptr[i];
+  }
+  J.uu.col.resize(J.uu.ptr[nu]);
+  J.pu.col.resize(J.pu.ptr[np]);
+  J.pp.col.resize(J.pp.ptr[np]);
+  J.uu.val.resize(J.uu.col.size());
+  J.pu.val.resize(J.pu.col.size());
+  J.pp.val.resize(J.pp.col.size());
+  par_for(g.V, [&](i64 v) {  // columns and zeroed values, first-touched by the owning thread
+    i64 ul[3], pl, ql;
+    pattern_rows(g, cs, v, J.uu.col.data() + J.uu.ptr[v * d], ul, J.pu.col.data() + J.pu.ptr[v], &pl,
+                 J.pp.col.data() + J.pp.ptr[v], &ql);
+    std::fill(J.uu.val.begin() + J.uu.ptr[v * d], J.uu.val.begin() + J.uu.ptr[(v + 1) * d], 0.0);
+    std::fill(J.pu.val.begin() + J.pu.ptr[v], J.pu.val.begin() + J.pu.ptr[v + 1], 0.0);
+    std::fill(J.pp.val.begin() + J.pp.ptr[v], J.pp.val.begin() + J.pp.ptr[v + 1], 0.0);
+  });
+}
+
+// assemble_jacobian, thread-parallel: each vertex owns its u and phi rows and adds, cell by cell in
+// the reference cell order, its corner's rows of the element matrices (the same expressions as the
+// cell loop, so every entry is the same sequence of IEEE additions).
+static BlockSystem assemble_jacobian_par(const Grid& g, const Constraints& cs, const orc_material& mat,
+                                         const orc_regularization& reg, const double* solution,
+                                         const double* phi_tilde) {
+  const int d = g.d, nv = 1 << d;
+  const double kap = reg.kappa, eps = reg.eps, p = mat.pressure, Gc = mat.G_c;
+  const double mu = mat_mu(mat), lam = mat_lambda(mat);
+  const QpData& qp = qp_data(d);
+  const i64 nu = g.n_u();
+  BlockSystem J;
+  build_pattern_par(g, cs, J);
+  const double h = g.h, detJ = g.detJ;
+  row_pool().run_dyn(g.V, 512, [&](int, i64 lo, i64 hi) {
+    CellRef cells[8];
+    double uloc[8][3], philoc[8], ptloc[8];
+    double kuu[3][24], kpu[24], kpp[8], gphys[8][3];
+    i64 verts[8], udofs[24], pdofs[8];
+    for (i64 v = lo; v < hi; ++v) {
+      const int nc = incident_cells(g, v, cells);
+      for (int ci = 0; ci < nc; ++ci) {
+        const i64 id = cells[ci].id;
+        const int k = cells[ci].k;
+        g.cell_vertices(id, verts);
+        for (int kk = 0; kk < nv; ++kk) {
+          for (int a = 0; a < d; ++a) uloc[kk][a] = solution[verts[kk] * d + a];
+          philoc[kk] = solution[nu + verts[kk]];
+          ptloc[kk] = phi_tilde[verts[kk]];
+        }
+        std::memset(kuu, 0, sizeof(kuu));
+        std::memset(kpu, 0, sizeof(kpu));
+        std::memset(kpp, 0, sizeof(kpp));
+        for (int q = 0; q < qp.nq; ++q) {
+          const double* s = qp.shape[q];
+          for (int kk = 0; kk < nv; ++kk)
+            for (int b = 0; b < 3; ++b) gphys[kk][b] = (b < d) ? qp.grads[q][kk][b] / h : 0.0;
+          double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+          double phi = 0.0, pt = 0.0;
+          for (int kk = 0; kk < nv; ++kk) {
+            phi += s[kk] * philoc[kk];
+            pt += s[kk] * ptloc[kk];
+            for (int b = 0; b < d; ++b)
+              for (int a = 0; a < d; ++a) gu[a][b] += uloc[kk][a] * gphys[kk][b];
+          }
+          double e[3][3], sig[3][3];
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
+          double tre = 0.0;
+          for (int a = 0; a < d; ++a) tre += e[a][a];
+          for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) sig[a][b] = 2.0 * mu * e[a][b];
+          for (int a = 0; a < d; ++a) sig[a][a] += lam * tre;
+          double sig_ee = 0.0;
+          for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b) sig_ee += sig[a][b] * e[a][b];
+          const double gcoef = (1.0 - kap) * pt * pt + kap;
+          const double w = qp.wts[q] * detJ;
+          for (int l = 0; l < nv; ++l) {
+            double gg = 0.0;
+            for (int b = 0; b < d; ++b) gg += gphys[k][b] * gphys[l][b];
+            for (int a = 0; a < d; ++a)
+              for (int b = 0; b < d; ++b) {
+                double val = mu * ((a == b ? gg : 0.0) + gphys[l][a] * gphys[k][b]) + lam * gphys[l][b] * gphys[k][a];
+                kuu[a][l * d + b] += w * gcoef * val;
+              }
+            for (int b = 0; b < d; ++b) {
+              double sgl = 0.0;
+              for (int c = 0; c < d; ++c) sgl += sig[b][c] * gphys[l][c];
+              kpu[l * d + b] += w * (2.0 * (1.0 - kap) * phi * sgl + 2.0 * p * phi * gphys[l][b]) * s[k];
+            }
+            kpp[l] += w * (((1.0 - kap) * sig_ee + 2.0 * p * tre + Gc / eps) * s[l] * s[k] + Gc * eps * gg);
+          }
+        }
+        for (int kk = 0; kk < nv; ++kk) {
+          for (int a = 0; a < d; ++a) udofs[kk * d + a] = verts[kk] * d + a;
+          pdofs[kk] = nu + verts[kk];
+        }
+        for (int a = 0; a < d; ++a) {
+          const i64 ri = udofs[k * d + a];
+          if (cs.is(ri)) {
+            J.uu.val[J.uu.ptr[ri]] += kuu[a][k * d + a];
+            continue;
+          }
+          for (int j = 0; j < nv * d; ++j) {
+            if (cs.is(udofs[j])) continue;
+            J.uu.val[find_slot(J.uu, ri, udofs[j])] += kuu[a][j];
+          }
+        }
+        const i64 ri = pdofs[k];
+        if (cs.is(ri)) {
+          J.pp.val[J.pp.ptr[ri - nu]] += kpp[k];
+          continue;
+        }
+        for (int j = 0; j < nv * d; ++j) {
+          if (cs.is(udofs[j])) continue;
+          J.pu.val[find_slot(J.pu, ri - nu, udofs[j])] += kpu[j];
+        }
+        for (int j = 0; j < nv; ++j) {
+          if (cs.is(pdofs[j])) continue;
+          J.pp.val[find_slot(J.pp, ri - nu, pdofs[j] - nu)] += kpp[j];
+        }
+      }
+    }
+  });
+  drop_zero_constrained_diag(J.uu, cs, 0);
+  drop_zero_constrained_diag(J.pp, cs, nu);
+  return J;
+}
+
+static BlockSystem assemble_jacobian(const Grid& g, const Constraints& cs, const orc_material& mat,
+                                     const orc_regularization& reg, const double* solution,
+                                     const double* phi_tilde) {
+  return row_pool().size() > 1 ? assemble_jacobian_par(g, cs, mat, reg, solution, phi_tilde)
+                               : assemble_jacobian_seq(g, cs, mat, reg, solution, phi_tilde);
+}
+
 // ------------------------------------------------------------------ GMRES (linsolve.cpp:21-115)
 using Op = std::function<Vec(const Vec&)>;
 struct GmresResult {
@@ -803,19 +1261,28 @@ static double tree256(double* sh) {  // in-place block tree of 256 values
     for (int t = 0; t < s; ++t) sh[t] += sh[t + s];
   return sh[0];
 }
-static double dot(const Vec& a, const Vec& b) {  // fixed block-tree order (see spmv_tpr note)
+static double dot(const Vec& a, const Vec& b) {
   const i64 n = i64(a.size());
+  if (g_order == ORDER_REFERENCE) {  // a.dot(b): one sequential sum
+    double s = 0.0;
+    for (i64 i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+  }
+  // fixed block-tree order (the device's k_dot_partial / k_final)
   const i64 nb = std::min<i64>(1024, std::max<i64>(1, (n + 4 * 256 - 1) / (4 * 256)));
   std::vector<double> part(nb);
-  double sh[256];
-  for (i64 bk = 0; bk < nb; ++bk) {
-    for (int t = 0; t < 256; ++t) {
-      double s = 0.0;
-      for (i64 i = bk * 256 + t; i < n; i += nb * 256) s += a[i] * b[i];
-      sh[t] = s;
+  row_pool().run_dyn(nb, 8, [&](int, i64 b0, i64 b1) {
+    double sh[256];
+    for (i64 bk = b0; bk < b1; ++bk) {
+      for (int t = 0; t < 256; ++t) {
+        double s = 0.0;
+        for (i64 i = bk * 256 + t; i < n; i += nb * 256) s += a[i] * b[i];
+        sh[t] = s;
+      }
+      part[bk] = tree256(sh);
     }
-    part[bk] = tree256(sh);
-  }
+  });
+  double sh[256];
   for (int t = 0; t < 256; ++t) {
     double s = 0.0;
     for (i64 bk = t; bk < nb; bk += 256) s += part[bk];
@@ -851,7 +1318,7 @@ static GmresResult gmres(const Op& op, const Op& prec, const Vec& rhs, const orc
     Vec cs(m, 0.0), sn(m, 0.0), gv(m + 1, 0.0);
     gv[0] = beta;
     V[0].resize(n);
-    for (size_t i = 0; i < n; ++i) V[0][i] = r[i] / beta;
+    par_for(i64(n), [&](i64 i) { V[0][i] = r[i] / beta; });
     int j = 0;
     bool inner_done = false;
     for (; j < m && !inner_done; ++j) {
@@ -859,14 +1326,16 @@ static GmresResult gmres(const Op& op, const Op& prec, const Vec& rhs, const orc
       for (int i = 0; i <= j; ++i) {  // MGS
         Hij(i, j) = dot(w, V[i]);
         const double hij = Hij(i, j);
-        for (size_t t = 0; t < n; ++t) w[t] -= hij * V[i][t];
+        const Vec& Vi = V[i];
+        par_for(i64(n), [&](i64 t) { w[t] -= hij * Vi[t]; });
       }
       Hij(j + 1, j) = norm(w);
       const bool happy = Hij(j + 1, j) <= 1e-14 * bnorm;
       if (!happy) {
         V[j + 1].resize(n);
         const double hn = Hij(j + 1, j);
-        for (size_t t = 0; t < n; ++t) V[j + 1][t] = w[t] / hn;
+        Vec& Vn = V[j + 1];
+        par_for(i64(n), [&](i64 t) { Vn[t] = w[t] / hn; });
       }
       for (int i = 0; i < j; ++i) {
         double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
@@ -905,16 +1374,16 @@ static GmresResult gmres(const Op& op, const Op& prec, const Vec& rhs, const orc
         }
       }
       Vec z(n, 0.0);
-      for (size_t t = 0; t < n; ++t) {  // V.leftCols(k) * y
+      par_for(i64(n), [&](i64 t) {  // V.leftCols(k) * y
         double s = 0.0;
         for (int l = 0; l < k; ++l) s += V[l][t] * y[l];
         z[t] = s;
-      }
+      });
       Vec mz = M(z);
-      for (size_t t = 0; t < n; ++t) res.x[t] += mz[t];
+      par_for(i64(n), [&](i64 t) { res.x[t] += mz[t]; });
     }
     Vec ax = op(res.x);
-    for (size_t t = 0; t < n; ++t) r[t] = rhs[t] - ax[t];
+    par_for(i64(n), [&](i64 t) { r[t] = rhs[t] - ax[t]; });
     res.residual = norm(r) / bnorm;
     if (res.residual <= o.rtol) {
       res.converged = true;
@@ -1133,15 +1602,15 @@ struct Amg {
     const double w = L.jacobi_weight;
     const i64 n = L.A.rows;
     x.assign(n, 0.0);
-    for (i64 i = 0; i < n; ++i) x[i] = w * (L.inv_diag[i] * b[i]);
+    par_for(n, [&](i64 i) { x[i] = w * (L.inv_diag[i] * b[i]); });
     Vec ax(n);
     for (int s = 1; s < opts.smoothing_sweeps; ++s) {
       spmv(L.A, x.data(), ax.data());
-      for (i64 i = 0; i < n; ++i) x[i] += w * (L.inv_diag[i] * (b[i] - ax[i]));
+      par_for(n, [&](i64 i) { x[i] += w * (L.inv_diag[i] * (b[i] - ax[i])); });
     }
     spmv(L.A, x.data(), ax.data());
     Vec r(n);
-    for (i64 i = 0; i < n; ++i) r[i] = b[i] - ax[i];
+    par_for(n, [&](i64 i) { r[i] = b[i] - ax[i]; });
     Vec bc(L.P.cols);
     spmv(L.Pt, r.data(), bc.data());
     Vec xc;
@@ -1149,7 +1618,7 @@ struct Amg {
     spmv_add(L.P, xc.data(), x.data());
     for (int s = 0; s < opts.smoothing_sweeps; ++s) {
       spmv(L.A, x.data(), ax.data());
-      for (i64 i = 0; i < n; ++i) x[i] += w * (L.inv_diag[i] * (b[i] - ax[i]));
+      par_for(n, [&](i64 i) { x[i] += w * (L.inv_diag[i] * (b[i] - ax[i])); });
     }
   }
   Vec vcycle(const Vec& r) const {
@@ -1168,11 +1637,11 @@ static double estimate_lambda_max(const Csr& A, const Vec& inv_diag) {  // linso
   double lambda = 1.0;
   for (int it = 0; it < 15; ++it) {
     spmv(A, v.data(), w.data());
-    for (i64 i = 0; i < n; ++i) w[i] = inv_diag[i] * w[i];
+    par_for(n, [&](i64 i) { w[i] = inv_diag[i] * w[i]; });
     const double nw = norm(w);
     if (nw == 0.0) return 1.0;
     lambda = nw;
-    for (i64 i = 0; i < n; ++i) v[i] = w[i] / nw;
+    par_for(n, [&](i64 i) { v[i] = w[i] / nw; });
   }
   return std::max(lambda, 1e-12);
 }
@@ -1215,11 +1684,12 @@ static Amg build_amg(const Csr& A_in, const std::vector<int>& node_in, const Den
     const i64 n = A.rows;
     if (n <= opts.coarse_size) break;
     const int n_nodes = node_of_dof.empty() ? 0 : *std::max_element(node_of_dof.begin(), node_of_dof.end()) + 1;
-    // node-block strength; blk[ni] is an ordered map ni -> sum a^2 (std::map semantics)
+    // node-block strength (linsolve.cpp:185-203); blk[ni] is an ordered map ni -> sum a^2
+    // (std::map semantics), accumulated over the node's dofs in ascending order
+    PhaseTimer t_st("amg strength");
     std::vector<std::vector<std::pair<int, double>>> blk(n_nodes);
-    for (i64 i = 0; i < n; ++i) {
-      const int ni = node_of_dof[i];
-      auto& row = blk[ni];
+    auto add_row = [&](i64 i) {
+      auto& row = blk[node_of_dof[i]];
       for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
         const int nj = node_of_dof[A.col[k]];
         const double a2 = A.val[k] * A.val[k];
@@ -1230,117 +1700,134 @@ static Amg build_amg(const Csr& A_in, const std::vector<int>& node_in, const Den
         else
           row.insert(it, {nj, a2});
       }
-    }
-    auto diag_of = [&](int i) {
-      for (auto& e : blk[i])
-        if (e.first == i) return e.second;
-      return 0.0;
     };
+    bool monotone = true;  // every node's dofs contiguous: nodes can be filled in parallel
+    for (i64 i = 1; i < n && monotone; ++i) monotone = node_of_dof[i] >= node_of_dof[i - 1];
+    if (monotone) {
+      std::vector<i64> first(n_nodes + 1, n);
+      for (i64 i = n - 1; i >= 0; --i) first[node_of_dof[i]] = i;
+      for (int ni = n_nodes - 1; ni >= 0; --ni) first[ni] = std::min(first[ni], first[ni + 1]);
+      row_pool().run_dyn(n_nodes, 4096, [&](int, i64 lo, i64 hi) {
+        for (i64 ni = lo; ni < hi; ++ni)
+          for (i64 i = first[ni]; i < first[ni + 1]; ++i) add_row(i);
+      });
+    } else {
+      for (i64 i = 0; i < n; ++i) add_row(i);
+    }
+    std::vector<double> dsq(n_nodes, 0.0);
+    par_for(n_nodes, [&](i64 i) {
+      for (auto& e : blk[i])
+        if (e.first == i) { dsq[i] = e.second; break; }
+    });
     std::vector<std::vector<int>> strong(n_nodes);
-    for (int i = 0; i < n_nodes; ++i) {
-      const double dii = std::sqrt(diag_of(i));
+    par_for(n_nodes, [&](i64 i) {
+      const double dii = std::sqrt(dsq[i]);
       for (auto& [j, s2] : blk[i]) {
         if (j == i) continue;
-        const double djj = std::sqrt(diag_of(j));
+        const double djj = std::sqrt(dsq[j]);
         if (std::sqrt(s2) > opts.strength_threshold * std::sqrt(dii * djj)) strong[i].push_back(j);
       }
-    }
-    Aggregation agg = aggregate_nodes(n_nodes, strong);
+    });
+    std::vector<std::vector<std::pair<int, double>>>().swap(blk);
+    Aggregation agg;
+    { PhaseTimer t("amg aggregate"); agg = aggregate_nodes(n_nodes, strong); }
+    std::vector<std::vector<int>>().swap(strong);
     if (agg.n_aggregates >= n_nodes && n_nodes > 1) break;
 
+    // tentative prolongator: ColPivHouseholderQR of each aggregate's nullspace rows
+    // (linsolve.cpp:205-239); aggregates are independent
     const i64 m = B.cols;
-    std::vector<std::vector<i64>> agg_dofs(agg.n_aggregates);
-    for (i64 i = 0; i < n; ++i) agg_dofs[agg.agg_of_node[node_of_dof[i]]].push_back(i);
-    std::vector<i64> agg_offset(agg.n_aggregates + 1, 0);
-    std::vector<std::vector<double>> agg_Q(agg.n_aggregates);   // dofs x rank, column-major
-    std::vector<Dense> agg_R(agg.n_aggregates);
-    for (int a = 0; a < agg.n_aggregates; ++a) {
-      const auto& dofs = agg_dofs[a];
-      const i64 rws = i64(dofs.size());
-      Dense Bg(rws, m);
-      for (i64 r = 0; r < rws; ++r)
-        for (i64 c = 0; c < m; ++c) Bg(r, c) = B(dofs[r], c);
-      ColPivQR qr;
-      qr.compute(Bg);
-      i64 rank = qr.rank(1e-10);
-      rank = std::max<i64>(0, std::min<i64>(rank, std::min<i64>(m, rws)));
-      agg_Q[a].assign(size_t(rws * rank), 0.0);
-      for (i64 c = 0; c < rank; ++c) qr.q_column(c, agg_Q[a].data() + size_t(c * rws));
-      Dense R(rank, m);
-      for (i64 i = 0; i < rank; ++i)
-        for (i64 k = i; k < m; ++k) R(i, qr.perm[k]) = qr.qr(i, k);  // (triu R) * Perm^T
-      agg_R[a] = R;
-      agg_offset[a + 1] = agg_offset[a] + rank;
+    const int na = agg.n_aggregates;
+    std::vector<i64> dptr(na + 1, 0), dofs_sorted(n), pos_in_agg(n);
+    for (i64 i = 0; i < n; ++i) dptr[agg.agg_of_node[node_of_dof[i]] + 1]++;
+    for (int a2 = 0; a2 < na; ++a2) dptr[a2 + 1] += dptr[a2];
+    {
+      std::vector<i64> fill(dptr.begin(), dptr.end() - 1);
+      for (i64 i = 0; i < n; ++i) {
+        const int a2 = agg.agg_of_node[node_of_dof[i]];
+        pos_in_agg[i] = fill[a2] - dptr[a2];
+        dofs_sorted[fill[a2]++] = i;
+      }
     }
+    std::vector<std::vector<double>> agg_Q(na);   // dofs x rank, column-major
+    std::vector<Dense> agg_R(na);
+    std::vector<i64> agg_rank(na, 0);
+    row_pool().run_dyn(na, 256, [&](int, i64 lo, i64 hi) {
+      for (i64 a2 = lo; a2 < hi; ++a2) {
+        const i64* dofs = dofs_sorted.data() + dptr[a2];
+        const i64 rws = dptr[a2 + 1] - dptr[a2];
+        Dense Bg(rws, m);
+        for (i64 r = 0; r < rws; ++r)
+          for (i64 c = 0; c < m; ++c) Bg(r, c) = B(dofs[r], c);
+        ColPivQR qr;
+        qr.compute(Bg);
+        i64 rank = qr.rank(1e-10);
+        rank = std::max<i64>(0, std::min<i64>(rank, std::min<i64>(m, rws)));
+        agg_Q[a2].assign(size_t(rws * rank), 0.0);
+        for (i64 c = 0; c < rank; ++c) qr.q_column(c, agg_Q[a2].data() + size_t(c * rws));
+        Dense R(rank, m);
+        for (i64 i = 0; i < rank; ++i)
+          for (i64 k = i; k < m; ++k) R(i, qr.perm[k]) = qr.qr(i, k);  // (triu R) * Perm^T
+        agg_R[a2] = R;
+        agg_rank[a2] = rank;
+      }
+    });
+    std::vector<i64> agg_offset(na + 1, 0);
+    for (int a2 = 0; a2 < na; ++a2) agg_offset[a2 + 1] = agg_offset[a2] + agg_rank[a2];
     const i64 nc = agg_offset.back();
     if (nc == 0 || nc >= n) break;
 
-    // T (setFromTriplets of one entry per (dof, coarse column); rows sorted by column)
-    Csr T;
-    T.rows = n;
-    T.cols = nc;
-    T.ptr.assign(n + 1, 0);
-    {
-      std::vector<std::vector<std::pair<int, double>>> rowsT(n);
-      for (int a = 0; a < agg.n_aggregates; ++a) {
-        const auto& dofs = agg_dofs[a];
-        const i64 rws = i64(dofs.size()), rank = agg_offset[a + 1] - agg_offset[a];
-        for (i64 r = 0; r < rws; ++r)
-          for (i64 c = 0; c < rank; ++c) {
-            const double q = agg_Q[a][size_t(c * rws + r)];
-            if (std::abs(q) > 1e-300) rowsT[dofs[r]].push_back({int(agg_offset[a] + c), q});
-          }
-      }
-      for (i64 i = 0; i < n; ++i) {
-        for (auto& e : rowsT[i]) {
-          T.col.push_back(e.first);
-          T.val.push_back(e.second);
+    // T (setFromTriplets of one entry per (dof, coarse column)): a dof lies in one aggregate,
+    // so its row holds that aggregate's Q row, columns ascending
+    Csr T = build_rows(n, nc, 8192, [&](int, i64 i, std::vector<int>& oc, std::vector<double>& ov) {
+      const int a2 = agg.agg_of_node[node_of_dof[i]];
+      const i64 rws = dptr[a2 + 1] - dptr[a2], r = pos_in_agg[i];
+      for (i64 c = 0; c < agg_rank[a2]; ++c) {
+        const double q = agg_Q[a2][size_t(c * rws + r)];
+        if (std::abs(q) > 1e-300) {
+          oc.push_back(int(agg_offset[a2] + c));
+          ov.push_back(q);
         }
-        T.ptr[i + 1] = i64(T.col.size());
       }
-    }
+    });
+    std::vector<std::vector<double>>().swap(agg_Q);
     Vec inv_diag(n);
-    for (i64 i = 0; i < n; ++i) {
+    par_for(n, [&](i64 i) {
       const double dv = A.coeff(i, i);
       inv_diag[i] = (dv != 0.0) ? 1.0 / dv : 0.0;
-    }
-    const double lambda = estimate_lambda_max(A, inv_diag);
+    });
+    double lambda;
+    { PhaseTimer t("amg lambda"); lambda = estimate_lambda_max(A, inv_diag); }
     const double wp = opts.prolongation_omega * 2.0 / lambda;
-    Csr DA = A;
-    for (i64 i = 0; i < n; ++i)
-      for (i64 k = A.ptr[i]; k < A.ptr[i + 1]; ++k) DA.val[k] = inv_diag[i] * A.val[k];
-    Csr DAT = spgemm(DA, T);
+    PhaseTimer t_p("amg P");
+    Csr DAT;
+    { PhaseTimer t("  DAT"); DAT = spgemm(A, T, inv_diag.data()); }  // (D^-1 A) T
     // P = T - (wp * DAT), union pattern, then prune
-    Csr P;
-    P.rows = n;
-    P.cols = nc;
-    P.ptr.assign(n + 1, 0);
-    for (i64 i = 0; i < n; ++i) {
+    Csr P = build_rows(n, nc, 8192, [&](int, i64 i, std::vector<int>& oc, std::vector<double>& ov) {
       i64 a = T.ptr[i], b = DAT.ptr[i];
       while (a < T.ptr[i + 1] || b < DAT.ptr[i + 1]) {
         if (b >= DAT.ptr[i + 1] || (a < T.ptr[i + 1] && T.col[a] < DAT.col[b])) {
-          P.col.push_back(T.col[a]);
-          P.val.push_back(T.val[a]);
+          oc.push_back(T.col[a]);
+          ov.push_back(T.val[a]);
           ++a;
         } else if (a >= T.ptr[i + 1] || DAT.col[b] < T.col[a]) {
-          P.col.push_back(DAT.col[b]);
-          P.val.push_back(0.0 - wp * DAT.val[b]);
+          oc.push_back(DAT.col[b]);
+          ov.push_back(0.0 - wp * DAT.val[b]);
           ++b;
         } else {
-          P.col.push_back(T.col[a]);
-          P.val.push_back(T.val[a] - wp * DAT.val[b]);
+          oc.push_back(T.col[a]);
+          ov.push_back(T.val[a] - wp * DAT.val[b]);
           ++a;
           ++b;
         }
       }
-      P.ptr[i + 1] = i64(P.col.size());
-    }
-    prune(P);
+    });
+    DAT = Csr();
+    T = Csr();
+    { PhaseTimer t("  prune"); prune(P); }
 
     AmgLevel level;
-    level.A = A;
-    level.P = P;
-    level.Pt = transpose(P);
+    { PhaseTimer t("  transpose"); level.Pt = transpose(P); }
     level.inv_diag = inv_diag;
     level.jacobi_weight = opts.jacobi_omega * 2.0 / lambda;
     level.n_nodes = n_nodes;
@@ -1348,16 +1835,23 @@ static Amg build_amg(const Csr& A_in, const std::vector<int>& node_in, const Den
     level.agg_of_node = agg.agg_of_node;
     level.lambda = lambda;
 
-    Csr AP = spgemm(A, P);
-    Csr Ac = spgemm(level.Pt, AP);
+    Csr Ac;
+    {
+      PhaseTimer t("amg RAP");
+      Csr AP;
+      { PhaseTimer t("  AP"); AP = spgemm(A, P); }
+      { PhaseTimer t("  PtAP"); Ac = spgemm(level.Pt, AP); }
+    }
     prune(Ac);
+    level.A = std::move(A);
+    level.P = std::move(P);
     Dense Bc(nc, m);
-    for (int a = 0; a < agg.n_aggregates; ++a)
-      for (i64 i = 0; i < agg_R[a].rows; ++i)
-        for (i64 c = 0; c < m; ++c) Bc(agg_offset[a] + i, c) = agg_R[a](i, c);
+    for (int a2 = 0; a2 < na; ++a2)
+      for (i64 i = 0; i < agg_R[a2].rows; ++i)
+        for (i64 c = 0; c < m; ++c) Bc(agg_offset[a2] + i, c) = agg_R[a2](i, c);
     std::vector<int> coarse_node(nc);
-    for (int a = 0; a < agg.n_aggregates; ++a)
-      for (i64 c = agg_offset[a]; c < agg_offset[a + 1]; ++c) coarse_node[c] = a;
+    for (int a2 = 0; a2 < na; ++a2)
+      for (i64 c = agg_offset[a2]; c < agg_offset[a2 + 1]; ++c) coarse_node[c] = a2;
     h.levels.push_back(std::move(level));
     A = std::move(Ac);
     B = std::move(Bc);
@@ -1592,52 +2086,74 @@ static std::set<i64> detect_cycles(const std::map<i64, std::vector<char>>& histo
   return out;
 }
 
+// newton_active_set_step (solver.cpp:49-188).  The active set A and the toggle history are kept
+// as flat per-vertex arrays instead of std::set / std::map: a dof's history is tracked from the
+// iteration it first enters A, backfilled with zeros to the current history length (so every
+// tracked history has the global length, and its entries before tracking are 0 = "not active"),
+// which is exactly the reference's map semantics (solver.cpp:88-102).
 static NewtonReport newton_step(State& state, const orc_material& mat, const Grid& g,
                                 const orc_regularization& reg, const orc_solver_options& opts) {
-  NewtonReport report;  // solver.cpp:49-188
+  NewtonReport report;
   const i64 nu = g.n_u(), np = g.n_phi();
   Constraints base = build_constraints(g, true, {}, {});
   Vec& x = state.solution;
   base.distribute(x);
   const Vec phi_tilde = extrapolate_phi(state);  // conforming_phi: base has no phi lines on uniform meshes
   const double c = opts.active_set_c_scale * mat.G_c / reg.eps;
-  std::set<i64> fixed;
-  std::map<i64, std::vector<char>> history;
-  std::vector<i64> candidates;
-  for (i64 v = 0; v < g.V; ++v)
-    if (!base.is(nu + v)) candidates.push_back(v);
-  std::set<i64> prev_active;
+  std::vector<char> fixed(np, 0), active(np, 0), prev_active(np, 0), tracked(np, 0), candidate(np, 0);
+  std::vector<std::vector<char>> hist;  // hist[t][v]: iteration t of the history (global length)
+  for (i64 v = 0; v < np; ++v) candidate[v] = !base.is(nu + v);
   double res0 = -1.0;
   BlockPrec prec;
   bool have_prec = false;
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
-    Vec R = assemble_residual(g, base, mat, reg, x.data(), phi_tilde.data());
+    Vec R;
+    { PhaseTimer t("residual"); R = assemble_residual(g, base, mat, reg, x.data(), phi_tilde.data()); }
+    PhaseTimer t_as("active set");
     const double active_tol = 1e-14 * c;
-    std::set<i64> active = fixed;
-    for (i64 v : candidates) {
-      const i64 dof = nu + v;
-      const double lambda = -R[dof];
-      if (c * (x[dof] - state.phi_old[v]) + lambda > active_tol) active.insert(dof);
+    par_for(np, [&](i64 v) {
+      char a = fixed[v];
+      if (!a && candidate[v]) {
+        const i64 dof = nu + v;
+        const double lambda = -R[dof];
+        a = (c * (x[dof] - state.phi_old[v]) + lambda > active_tol) ? 1 : 0;
+      }
+      active[v] = a;
+    });
+    // history: a newly tracked dof starts at the current length (zeros before), all push 1/0
+    bool any_tracked = !hist.empty();
+    for (i64 v = 0; v < np && !any_tracked; ++v) any_tracked = active[v] != 0;
+    if (any_tracked) {
+      par_for(np, [&](i64 v) {
+        if (active[v]) tracked[v] = 1;
+      });
+      hist.emplace_back(active.begin(), active.end());
+      const int L = int(hist.size()), start = std::max(0, L - opts.cycle_window);
+      par_for(np, [&](i64 v) {  // detect_cycles (solver.cpp:10-22) over the tracked dofs
+        if (!tracked[v]) return;
+        int changes = 0;
+        for (int t = start + 1; t < L; ++t)
+          if (hist[t][v] != hist[t - 1][v]) ++changes;
+        if (changes >= opts.cycle_toggles) {
+          fixed[v] = 1;
+          active[v] = 1;
+        }
+      });
     }
-    size_t hist_len = 0;
-    for (auto& [dof, bits] : history) hist_len = std::max(hist_len, bits.size());
-    for (i64 dof : active) {
-      auto& bits = history[dof];
-      bits.resize(hist_len, 0);
+    i64 n_active = 0, changes = 0;
+    for (i64 v = 0; v < np; ++v) {
+      n_active += active[v];
+      changes += (active[v] != prev_active[v]);
     }
-    for (auto& [dof, bits] : history) bits.push_back(active.count(dof) ? 1 : 0);
-    for (i64 dof : detect_cycles(history, opts.cycle_window, opts.cycle_toggles)) {
-      fixed.insert(dof);
-      active.insert(dof);
-    }
-    int changes = 0;
-    for (i64 dof : active)
-      if (!prev_active.count(dof)) ++changes;
-    for (i64 dof : prev_active)
-      if (!active.count(dof)) ++changes;
-    std::vector<i64> adofs(active.begin(), active.end());
+    std::vector<i64> adofs;
     std::vector<double> avals;
-    for (i64 dof : adofs) avals.push_back(state.phi_old[dof - nu]);
+    adofs.reserve(n_active);
+    avals.reserve(n_active);
+    for (i64 v = 0; v < np; ++v)
+      if (active[v]) {
+        adofs.push_back(nu + v);
+        avals.push_back(state.phi_old[v]);
+      }
     Constraints full = build_constraints(g, true, adofs, avals);
     Vec x_before = x;
     full.distribute(x);
@@ -1646,21 +2162,22 @@ static NewtonReport newton_step(State& state, const orc_material& mat, const Gri
     if (moved > 0.0) {
       R = assemble_residual(g, full, mat, reg, x.data(), phi_tilde.data());
     } else {
-      for (i64 dof : active) R[dof] = 0.0;
+      for (i64 dof : adofs) R[dof] = 0.0;
     }
     const double res = norm(R);
     if (res0 < 0.0) res0 = res;
-    NewtonIter rec{res, int(active.size()), changes, 0};
+    NewtonIter rec{res, int(n_active), int(changes), 0};
     const bool small = res <= std::max(opts.newton_tol * res0, opts.newton_abs_floor);
     if (changes == 0 && small) {
       report.its.push_back(rec);
       if (opts.log)
         std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=0\n", state.step, it, res,
-                    rec.active_size, changes);
+                    rec.active_size, int(changes));
       report.converged = true;
       break;
     }
-    BlockSystem J = assemble_jacobian(g, full, mat, reg, x.data(), phi_tilde.data());
+    BlockSystem J;
+    { PhaseTimer t("jacobian"); J = assemble_jacobian(g, full, mat, reg, x.data(), phi_tilde.data()); }
     if (!have_prec || !opts.freeze_preconditioner) {
       Nullspace ns;
       ns.u_modes = rigid_body_modes(g, full);
@@ -1670,11 +2187,14 @@ static NewtonReport newton_step(State& state, const orc_material& mat, const Gri
       for (i64 v = 0; v < np; ++v)
         if (full.is(nu + v)) ns.p_modes(v, 0) = 0.0;
       ns.p_node = identity_nodes(np);
+      PhaseTimer t("prec build");
+      prec = BlockPrec();  // release the previous hierarchies before building the new ones
       prec = build_prec(J, opts.prec_kind, opts.amg, &ns);
       have_prec = true;
     }
     Vec mR(R.size());
-    for (size_t i = 0; i < R.size(); ++i) mR[i] = -R[i];
+    par_for(i64(R.size()), [&](i64 i) { mR[i] = -R[i]; });
+    PhaseTimer t_gm("gmres");
     GmresResult lin = gmres([&J](const Vec& v) { return J.apply(v); },
                             [&prec](const Vec& v) { return prec.apply(v); }, mR, opts.gmres);
     if (!lin.converged && !lin.breakdown)
@@ -1683,10 +2203,10 @@ static NewtonReport newton_step(State& state, const orc_material& mat, const Gri
     report.its.push_back(rec);
     if (opts.log)
       std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=%d\n", state.step, it, res,
-                  rec.active_size, changes, lin.iterations);
+                  rec.active_size, int(changes), lin.iterations);
     Vec delta = lin.x;
     full.distribute_homogeneous(delta);
-    for (size_t i = 0; i < x.size(); ++i) x[i] += delta[i];
+    par_for(i64(x.size()), [&](i64 i) { x[i] += delta[i]; });
     if (opts.damping) {
       double scale = 1.0;
       for (int half = 0; half < 4; ++half) {
@@ -1937,6 +2457,14 @@ int orc_set_threads(int threads) {
   return 0;
 }
 int orc_get_threads(void) { return row_pool().size(); }
+// reduction order: 0 = the product's documented order (bitwise checks), 1 = the reference's
+// sequential row sums and dots (tolerance checks); see the file header
+int orc_set_order(int order) {
+  if (order != ORDER_PRODUCT && order != ORDER_REFERENCE) return -1;
+  g_order = order;
+  return 0;
+}
+int orc_get_order(void) { return g_order; }
 
 // SpMV of one block with `threads` OpenMP threads (row-parallel; each row summed sequentially,
 // so the result is independent of the thread count).  Used for the bounded CPU baseline.

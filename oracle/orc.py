@@ -103,6 +103,46 @@ def get_threads() -> int:
     return int(lib().orc_get_threads())
 
 
+ORDER_PRODUCT, ORDER_REFERENCE = 0, 1
+
+
+def set_order(order: int) -> None:
+    """Reduction order: ORDER_PRODUCT (the device's documented order; bitwise checks) or
+    ORDER_REFERENCE (the reference's sequential CSR row sums and dots; tolerance checks)."""
+    _chk(lib().orc_set_order(int(order)))
+
+
+def get_order() -> int:
+    return int(lib().orc_get_order())
+
+
+class reference_order:
+    """with orc.reference_order(): ... runs the oracle in the reference's arithmetic order."""
+
+    def __enter__(self):
+        self.prev = get_order()
+        set_order(ORDER_REFERENCE)
+        return self
+
+    def __exit__(self, *exc):
+        set_order(self.prev)
+
+
+class threads:
+    """with orc.threads(n): ... runs the oracle on n host threads (results are unchanged)."""
+
+    def __init__(self, n: int):
+        self.n = int(n)
+
+    def __enter__(self):
+        self.prev = get_threads()
+        set_threads(self.n)
+        return self
+
+    def __exit__(self, *exc):
+        set_threads(self.prev)
+
+
 def _p(a, ct=C.c_double):
     return a.ctypes.data_as(C.POINTER(ct)) if a is not None else None
 
