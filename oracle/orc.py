@@ -301,6 +301,12 @@ class Block:
         except Exception:
             pass
 
+    def nnz(self, which: int):
+        """(rows, cols, nnz) of block `which` (0 M_uu, 1 M_phiu, 2 M_phiphi)."""
+        r, c, n = C.c_int64(), C.c_int64(), C.c_int64()
+        lib().orc_block_nnz(self.h_, which, C.byref(r), C.byref(c), C.byref(n))
+        return r.value, c.value, n.value
+
     def csr(self, which: int) -> Csr:
         r, c, n = C.c_int64(), C.c_int64(), C.c_int64()
         lib().orc_block_nnz(self.h_, which, C.byref(r), C.byref(c), C.byref(n))

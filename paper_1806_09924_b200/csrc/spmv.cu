@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(256) k_spmv_phi_st16p(i64 rows, const i64* __r
   __syncthreads();
   const i64 G = (i64(gridDim.x) * blockDim.x) >> 3;
   const i64 g0 = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 3;
+  const int gw = int((threadIdx.x & 31) >> 3);  // group within the warp
   const int t = int(threadIdx.x & 7);
   St16Regs o;
   o.init(t, int(sc.nn));
@@ -536,20 +537,25 @@ __global__ void __launch_bounds__(256) k_spmv_phi_st16p(i64 rows, const i64* __r
     b0 = p1[g0];
     b1 = p1[g0 + 1];
   }
-  for (i64 row = g0; row < rows; row += G) {
+  // warp-uniform bound (as k_spmv_st16p): every lane of the warp reaches the full-mask shuffles
+  // of group_sum; groups past the last row carry zeros and store nothing
+  for (i64 row = g0; row - gw < rows; row += G) {
+    const bool act = row < rows;
     i64 n0 = 0, n1 = 0;
     if (row + G < rows) {
       n0 = p1[row + G];
       n1 = p1[row + G + 1];
     }
     const double* xb = nullptr;
-    double s1;
-    if (st16_interior(sc, row, b1 - b0, x1, xb)) s1 = row16_interior(v1 + b0, xb, t, o);
-    else s1 = row_dot_st_emu<16, 8, 1, 3>(p1, v1, x1, row, t, sc, off);
-    double s2 = row_dot_b_emu<16, 8, 2>(p2, c2, v2, x2, row, t);
+    double s1 = 0.0, s2 = 0.0;
+    if (act) {
+      if (st16_interior(sc, row, b1 - b0, x1, xb)) s1 = row16_interior(v1 + b0, xb, t, o);
+      else s1 = row_dot_st_emu<16, 8, 1, 3>(p1, v1, x1, row, t, sc, off);
+      s2 = row_dot_b_emu<16, 8, 2>(p2, c2, v2, x2, row, t);
+    }
     s1 = group_sum<8>(s1);
     s2 = group_sum<8>(s2);
-    if (t == 0) y[row] = s1 + s2;
+    if (act && t == 0) y[row] = s1 + s2;
     b0 = n0;
     b1 = n1;
   }

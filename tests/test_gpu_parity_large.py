@@ -1,0 +1,251 @@
+"""GPU parity at the sizes where the headline kernels dispatch, and against the reference's own
+arithmetic order.
+
+* >= 40^3 in 3d (48^3 and 64^3 penny cracks): the mean M_uu / M_phiu row is longer than 64
+  entries, so the block apply, the u-hierarchy's level-0 SpMVs (with their fused residual,
+  post-smoothing and power-iteration epilogues) run through the 16-lane stencil kernels
+  k_spmv_st16p / k_spmv_phi_st16p.  Everything is compared bit for bit with the oracle in the
+  product reduction order; the same Newton step with CF_NO_STENCIL_COLS=1 (CSR kernels) and
+  CF_ST_EMU=1 (the generic emulated stencil kernel) must give the identical solution.
+* config-2 family (2d 512^2, 3 load steps, GMRES(50) rtol 1e-10; step 3 extrapolates phi).
+* config 3 at its full size (128^3, 8,586,756 dofs): the first Newton iteration (residual, active
+  set, Jacobian, both AMG hierarchies, 13 GMRES iterations) bit for bit.
+* reference order (oracle ORDER_REFERENCE: sequential CSR row sums and dots, as Eigen computes
+  them, linsolve.cpp:16-17,30,38,57,60): the device result must be within the north-star
+  tolerances — solution 1e-8 relative, COD/TCV 1e-6 relative, Newton and GMRES iteration
+  counts within 10% — on config 0, the 32^3 / 64^3 penny and the 512^2 config-2 family.
+
+The oracle runs on all host cores (bitwise independent of the thread count,
+tests/test_oracle_modes.py).  The full-size config-2 (2048^2) and config-3 (all Newton
+iterations) comparisons are `slow`: they run when CF_SLOW_PARITY=1.
+"""
+import json
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+slow = pytest.mark.skipif(not os.environ.get("CF_SLOW_PARITY"), reason="set CF_SLOW_PARITY=1 (minutes of oracle time)")
+
+
+@pytest.fixture(scope="module")
+def cf():
+    import paper_1806_09924_b200 as cf
+    return cf
+
+
+@pytest.fixture(scope="module")
+def orcmt(orc):
+    prev = orc.get_threads()
+    orc.set_threads(len(os.sched_getaffinity(0)))
+    yield orc
+    orc.set_threads(prev)
+
+
+def _pair(cf, orc, d, n0, r):
+    P, O = cf.Problem(d, 10.0, n0, r), orc.Problem(d, 10.0, n0, r)
+    mat = cf.Material(eps_mode=1, eps_fixed=2 * P.h, kappa_factor=1e-12 / P.h)
+    omat = orc.material(eps_mode=1, eps_fixed=2 * P.h, kappa_factor=1e-12 / P.h)
+    reg = cf.resolve_regularization(P, mat, cf.slit_band_edge(P, mat))
+    oreg = O.resolve_regularization(omat, O.slit_band_edge(omat))
+    assert (reg.eps, reg.kappa) == (oreg.eps, oreg.kappa)
+    phi, _ = cf.initial_crack(P, mat)
+    return P, O, mat, omat, reg, oreg, phi
+
+
+def _device_run(cf, P, mat, reg, steps, gm=None, max_iter=50):
+    st = cf.make_initial_state(P, mat)
+    opts = cf.SolverOptions(newton_max_iter=max_iter)
+    if gm is not None:
+        opts.gmres = gm
+    reps = cf.solve_loading_sequence(st, mat, P, reg, opts, steps)  # a capped step ends it, unconverged
+    return reps, st.get()["solution"]
+
+
+def _oracle_run(orc, O, omat, oreg, phi, steps, gm=None, max_iter=50):
+    sol = np.zeros(O.n_total)
+    sol[O.n_u:] = phi
+    po, pp = phi.copy(), phi.copy()
+    kw = dict(newton_max_iter=max_iter)
+    if gm is not None:
+        kw["gmres"] = orc.gmres_options(rtol=gm.rtol, max_iter=gm.max_iter, restart=gm.restart)
+    reps = [O.newton_step(omat, oreg, orc.solver_options(**kw), sol, po, pp, n) for n in range(1, steps + 1)]
+    return reps, sol
+
+
+def _its(rep):
+    return np.array([[r["residual_norm"], r["active_size"], r["set_changes"], r["gmres_iterations"]]
+                     for r in rep["iterations"]])
+
+
+def _bitwise(reps, x, oreps, xo):
+    assert len(reps) == len(oreps)
+    for a, b in zip(reps, oreps):
+        assert np.array_equal(_its(a), b["iterations"]), (_its(a), b["iterations"])
+        assert a["converged"] == b["converged"]
+    assert np.array_equal(x, xo), f"max |dx| = {np.abs(x - xo).max()}"
+
+
+def _within_north_star(reps, x, oreps, xo, P=None, cf=None, O=None):
+    """solution <= 1e-8 relative, Newton and GMRES counts within 10%, TCV/COD <= 1e-6."""
+    assert len(reps) == len(oreps)
+    for a, b in zip(reps, oreps):
+        ia, ib = _its(a), b["iterations"]
+        na, nb = len(ia), len(ib)
+        assert abs(na - nb) <= max(0.1 * nb, 0), (ia, ib)
+        ga, gb = ia[:, 3].sum(), ib[:, 3].sum()
+        assert abs(ga - gb) <= 0.1 * gb, (ia, ib)
+        assert a["converged"] and b["converged"]
+        assert ia[-1, 1] == ib[-1, 1], ("final active set size", ia[-1, 1], ib[-1, 1])
+    rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
+    assert rel <= 1e-8, rel
+    if P is not None:
+        tcv, tcvo = cf.compute_tcv(P, x), O.tcv(xo)
+        assert abs(tcv - tcvo) <= 1e-6 * abs(tcvo), (tcv, tcvo)
+        st = -1.575 + 0.05 * np.arange(64) if P.dim == 2 else np.linspace(-1.5, 1.5, 31)
+        cod, codo = cf.compute_cod(P, x, st), O.cod(xo, st)
+        big = np.abs(codo) > 1e-3 * np.abs(codo).max()
+        assert np.all(np.abs(cod - codo)[big] <= 1e-6 * np.abs(codo)[big])
+    return rel
+
+
+# ------------------------------------------------------------------ 16-lane kernels at >= 40^3
+def _state48(cf, orc, P, O):
+    rng = np.random.default_rng(48)
+    x = np.zeros(P.n_total)
+    x[:P.n_u] = 1e-3 * rng.standard_normal(P.n_u)
+    x[P.n_u:] = rng.uniform(0.0, 1.0, P.n_phi)
+    pt = rng.uniform(0.0, 1.0, P.n_phi)
+    act = {int(P.n_u + v): float(x[P.n_u + v]) for v in range(0, P.n_phi, 97)}
+    cs = cf.build_constraints(P, True, act)
+    ocs = O.constraints(True, list(act.keys()), list(act.values()))
+    return x, pt, cs, ocs
+
+
+def test_48_apply_and_u_hierarchy_bitwise(cf, orcmt):
+    orc = orcmt
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orc, 3, 12, 2)  # 48^3 cells, 470,596 dofs
+    x, pt, cs, ocs = _state48(cf, orc, P, O)
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    Jo = O.jacobian(ocs, omat, oreg, x, pt)
+    for w in range(3):
+        a, b = J.csr(w), Jo.csr(w)
+        assert np.array_equal(a.ptr, b.ptr) and np.array_equal(a.col, b.col) and np.array_equal(a.val, b.val)
+    uu, pu = J.csr(0), J.csr(1)
+    assert uu.nnz / uu.rows > 64 and pu.nnz / pu.rows > 64, "16-lane dispatch (mean row > 64) expected"
+    assert J.format(0) == "stencil" and J.format(1) == "stencil"
+    assert np.array_equal(J.apply(x), Jo.apply(x))  # k_spmv_st16p + k_spmv_phi_st16p
+    node = np.repeat(np.arange(P.n_vertices, dtype=np.int32), 3)
+    B = cf.rigid_body_modes(P, cs)
+    h = cf.build_amg(cf.CsrMatrix.from_block(J, 0), node, B)  # level 0 = the stencil-format M_uu
+    ho = orc.Amg(orc.Csr(uu.rows, uu.cols, uu.ptr, uu.col, uu.val), node, B)
+    assert h.n_levels() == ho.n_levels and h.coarse_dim() == ho.coarse_dim
+    for lev in range(ho.n_levels - 1):
+        a, b = h.level_info(lev), ho.level(lev)
+        assert a["lam"] == b["lam"], (lev, a["lam"], b["lam"])  # power iteration, mode-3 epilogue
+        assert np.array_equal(h.aggregates(lev), ho.aggregates(lev))
+        for w in (0, 1):
+            m1, m2 = h.level_matrix(lev, w), ho.level_matrix(lev, w)
+            assert np.array_equal(m1.val, m2.val) and np.array_equal(m1.col, m2.col)
+    r = np.random.default_rng(5).uniform(-1, 1, P.n_u)
+    assert np.array_equal(h.v_cycle(r), ho.vcycle(r))  # residual / post-sweep epilogues (modes 1, 2)
+
+
+def test_48_newton_step_bitwise_and_kernel_switches(cf, orcmt):
+    orc = orcmt
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orc, 3, 12, 2)
+    reps, x = _device_run(cf, P, mat, reg, 1)
+    oreps, xo = _oracle_run(orc, O, omat, oreg, phi, 1)
+    _bitwise(reps, x, oreps, xo)
+    import hashlib
+    ref = hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+    for env in ({"CF_NO_STENCIL_COLS": "1"}, {"CF_ST_EMU": "1"}):
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_newton_runner.py"), "3", "12", "2", "1"],
+                             env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res = json.loads(out.stdout.strip().splitlines()[-1])
+        assert res["sha256"] == ref, env
+        assert np.array_equal(np.array(res["its"][0]), _its(reps[0]))
+        if "CF_NO_STENCIL_COLS" in env:
+            assert res["formats"][:2] == ["csr", "csr"]
+
+
+def test_64_newton_step_bitwise(cf, orcmt):
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 3, 8, 3)  # 64^3 cells, 1,098,500 dofs
+    reps, x = _device_run(cf, P, mat, reg, 1)
+    oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 1)
+    _bitwise(reps, x, oreps, xo)
+    assert reps[0]["converged"] and reps[0]["feasibility_violation"] <= 1e-10
+
+
+def test_config2_family_512_three_steps_bitwise(cf, orcmt):
+    """Config 2's schedule on 512^2 (789,507 dofs): 3 load steps, phi extrapolated at step 3,
+    GMRES(50) with rtol 1e-10."""
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 2, 8, 6)
+    gm = cf.GmresOptions(rtol=1e-10, restart=50)
+    reps, x = _device_run(cf, P, mat, reg, 3, gm)
+    oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 3, gm)
+    _bitwise(reps, x, oreps, xo)
+
+
+def test_config3_full_size_first_newton_iteration_bitwise(cf, orcmt):
+    """Config 3 (128^3, 8,586,756 dofs) at its full size: the first Newton iteration."""
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 3, 8, 4)
+    assert P.n_total == 8586756
+    reps, x = _device_run(cf, P, mat, reg, 1, max_iter=1)
+    oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 1, max_iter=1)
+    _bitwise(reps, x, oreps, xo)
+
+
+# ------------------------------------------------------------------ reference arithmetic order
+@pytest.mark.parametrize("case", ["config0", "penny32", "penny64"])
+def test_reference_order_north_star_tolerances(cf, orcmt, case):
+    d, n0, r = {"config0": (2, 8, 5), "penny32": (3, 8, 2), "penny64": (3, 8, 3)}[case]
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, d, n0, r)
+    reps, x = _device_run(cf, P, mat, reg, 1)
+    with orcmt.reference_order():
+        oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 1)
+    rel = _within_north_star(reps, x, oreps, xo, P, cf, O)
+    print(f"{case}: solution rel diff {rel:.3e}; device {_its(reps[0])[:, 3].tolist()} "
+          f"reference-order {oreps[0]['iterations'][:, 3].astype(int).tolist()}")
+
+
+def test_reference_order_config2_family(cf, orcmt):
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 2, 8, 6)
+    gm = cf.GmresOptions(rtol=1e-10, restart=50)
+    reps, x = _device_run(cf, P, mat, reg, 3, gm)
+    with orcmt.reference_order():
+        oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 3, gm)
+    _within_north_star(reps, x, oreps, xo, P, cf, O)
+
+
+# ------------------------------------------------------------------ full-size, opt-in
+@slow
+def test_config3_full_newton_step_bitwise_and_reference_order(cf, orcmt):
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 3, 8, 4)
+    reps, x = _device_run(cf, P, mat, reg, 1)
+    oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 1)
+    _bitwise(reps, x, oreps, xo)
+    with orcmt.reference_order():
+        rreps, xr = _oracle_run(orcmt, O, omat, oreg, phi, 1)
+    _within_north_star(reps, x, rreps, xr, P, cf, O)
+
+
+@slow
+def test_config2_full_size_bitwise_and_reference_order(cf, orcmt):
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 2, 8, 8)
+    assert P.n_total == 12595203
+    gm = cf.GmresOptions(rtol=1e-10, restart=50)
+    reps, x = _device_run(cf, P, mat, reg, 3, gm)
+    oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 3, gm)
+    _bitwise(reps, x, oreps, xo)
+    with orcmt.reference_order():
+        rreps, xr = _oracle_run(orcmt, O, omat, oreg, phi, 3, gm)
+    for a, b in zip(reps, rreps):
+        print("device", _its(a).tolist(), "\nreference-order", b["iterations"].tolist())
+    _within_north_star(reps, x, rreps, xr, P, cf, O)
