@@ -1261,6 +1261,64 @@ static double tree256(double* sh) {  // in-place block tree of 256 values
     for (int t = 0; t < s; ++t) sh[t] += sh[t + s];
   return sh[0];
 }
+// The Newton step's dots and norms in the product order (the device's SegLayout, cf_vec.hpp):
+// each vertex plane's u part and phi part is cut into chunks of 8192 entries, a chunk is reduced
+// by 256 lanes (lane t: entries t, t+256, ... sequentially, then the block tree), and the chunk
+// partials, u planes then phi planes, go through the fixed final tree.  This order does not depend
+// on how the planes are split over ranks, which makes the multi-GPU step bitwise the 1-GPU step.
+struct SegDot {
+  bool on = false;
+  i64 plane_u = 0, plane_p = 0, chunk = 8192, n = 0;
+  int nplanes = 0;
+};
+static SegDot g_seg;
+struct SegScope {  // segmented dots for block vectors of the grid while in scope
+  SegDot prev;
+  SegScope(const Grid& g) : prev(g_seg) {
+    const i64 plane = (g.d == 3) ? g.nn * g.nn : g.nn;
+    g_seg.on = true;
+    g_seg.plane_u = g.d * plane;
+    g_seg.plane_p = plane;
+    g_seg.nplanes = int(g.nn);
+    g_seg.n = g.n_total();
+  }
+  ~SegScope() { g_seg = prev; }
+};
+static double seg_dot(const Vec& a, const Vec& b) {
+  const SegDot& L = g_seg;
+  const int cu = int((L.plane_u + L.chunk - 1) / L.chunk), cp = int((L.plane_p + L.chunk - 1) / L.chunk);
+  const i64 np = i64(L.nplanes) * (cu + cp);
+  std::vector<double> G(np);
+  row_pool().run_dyn(np, 16, [&](int, i64 lo, i64 hi) {
+    double sh[256];
+    for (i64 gi = lo; gi < hi; ++gi) {
+      i64 start, len;
+      if (gi < i64(L.nplanes) * cu) {
+        const i64 p = gi / cu, c = gi % cu;
+        start = p * L.plane_u + c * L.chunk;
+        len = std::min(L.chunk, L.plane_u - c * L.chunk);
+      } else {
+        const i64 q = gi - i64(L.nplanes) * cu, p = q / cp, c = q % cp;
+        start = i64(L.nplanes) * L.plane_u + p * L.plane_p + c * L.chunk;
+        len = std::min(L.chunk, L.plane_p - c * L.chunk);
+      }
+      for (int t = 0; t < 256; ++t) {
+        double s = 0.0;
+        for (i64 i = t; i < len; i += 256) s += a[start + i] * b[start + i];
+        sh[t] = s;
+      }
+      G[gi] = tree256(sh);
+    }
+  });
+  double sh[256];
+  for (int t = 0; t < 256; ++t) {
+    double s = 0.0;
+    for (i64 bk = t; bk < np; bk += 256) s += G[bk];
+    sh[t] = s;
+  }
+  return tree256(sh);
+}
+
 static double dot(const Vec& a, const Vec& b) {
   const i64 n = i64(a.size());
   if (g_order == ORDER_REFERENCE) {  // a.dot(b): one sequential sum
@@ -1268,6 +1326,7 @@ static double dot(const Vec& a, const Vec& b) {
     for (i64 i = 0; i < n; ++i) s += a[i] * b[i];
     return s;
   }
+  if (g_seg.on && n == g_seg.n) return seg_dot(a, b);
   // fixed block-tree order (the device's k_dot_partial / k_final)
   const i64 nb = std::min<i64>(1024, std::max<i64>(1, (n + 4 * 256 - 1) / (4 * 256)));
   std::vector<double> part(nb);
@@ -2164,7 +2223,11 @@ static NewtonReport newton_step(State& state, const orc_material& mat, const Gri
     } else {
       for (i64 dof : adofs) R[dof] = 0.0;
     }
-    const double res = norm(R);
+    double res;
+    {
+      SegScope seg(g);
+      res = norm(R);
+    }
     if (res0 < 0.0) res0 = res;
     NewtonIter rec{res, int(n_active), int(changes), 0};
     const bool small = res <= std::max(opts.newton_tol * res0, opts.newton_abs_floor);
@@ -2195,6 +2258,7 @@ static NewtonReport newton_step(State& state, const orc_material& mat, const Gri
     Vec mR(R.size());
     par_for(i64(R.size()), [&](i64 i) { mR[i] = -R[i]; });
     PhaseTimer t_gm("gmres");
+    SegScope seg(g);
     GmresResult lin = gmres([&J](const Vec& v) { return J.apply(v); },
                             [&prec](const Vec& v) { return prec.apply(v); }, mR, opts.gmres);
     if (!lin.converged && !lin.breakdown)
@@ -2211,6 +2275,7 @@ static NewtonReport newton_step(State& state, const orc_material& mat, const Gri
       double scale = 1.0;
       for (int half = 0; half < 4; ++half) {
         Vec Rn = assemble_residual(g, full, mat, reg, x.data(), phi_tilde.data());
+        SegScope seg2(g);
         if (norm(Rn) <= 10.0 * res) break;
         scale *= 0.5;
         for (size_t i = 0; i < x.size(); ++i) x[i] -= scale * delta[i];

@@ -438,14 +438,16 @@ __global__ void k_jac_count(GridDesc g, const Tables* __restrict__ T, Coef cf, c
         for (int b = 0; b < D; ++b) nfu += flag[w * D + b] ? 0 : 1;
         nfp += flag[nu + w] ? 0 : 1;
       }
-  bool any_con = flag[nu + v] != 0;
+  const bool con_p = flag[nu + v] != 0;
+  bool con_u = false;
 #pragma unroll
-  for (int a = 0; a < D; ++a) any_con |= flag[v * D + a] != 0;
+  for (int a = 0; a < D; ++a) con_u |= flag[v * D + a] != 0;
   PairBlocks<D> pb;
-  if (any_con) {
+  pb.pp = 0.0;
+  if (con_p || (UU && con_u)) {  // a constrained row keeps its diagonal iff the summed value is != 0
     CellList<D> L;
     common_cells<D>(g, x, y, z, 0, 0, 0, L);
-    pair_blocks<D>(T, cf, qs, L, true, true, pb);
+    pair_blocks<D>(T, cf, qs, L, UU && con_u, con_p, pb);
   }
   if (UU) {
 #pragma unroll
@@ -537,6 +539,37 @@ __global__ void __launch_bounds__(pair_wpb<D>() * 32) k_jac_fill_pair(
       const i64 kt = __shfl_sync(FULL, ckey, t);
       const bool vt = __shfl_sync(FULL, cvalid, t);
       crank += (vt && kt < ckey) ? 1 : 0;
+    }
+    if constexpr (!UU) {
+      // constrained phi row (the active set: most phi rows once the crack has formed): no M_phiu
+      // entries and only the diagonal of M_phiphi, i.e. the units (cell, l = k).  Lane t < 2^d
+      // computes its cell's unit with the fill's expression, then the units are added in
+      // reference cell order, as the center slot does below.
+      if (flag[nu + v] != 0) {
+        double u = 0.0;
+        if (cvalid) {
+          const int k = lane;
+          const double* cst = qs + ccell * CS;
+          for (int q = 0; q < NQ; ++q) {
+            const double* st = cst + q * NS;
+            const double see = __ldg(st + 3), tre = __ldg(st + 2);
+            const double sk = sm.s[q][k], slv = sm.s[q][k];
+            u += sm.w[q] * ((omk * see + c2p * tre + gce) * slv * sk + gcx * sm.gg[q][k][k]);
+          }
+        }
+        double acc = 0.0;
+        const unsigned vm = __ballot_sync(FULL, cvalid) & ((1u << NC) - 1u);
+        const int ncl = __popc(vm);
+        for (int ii = 0; ii < ncl; ++ii) {
+          const int src = __ffs(__ballot_sync(FULL, cvalid && crank == ii)) - 1;
+          acc += __shfl_sync(FULL, u, src);
+        }
+        if (lane == 0 && ptr_pp[lv + 1] > ptr_pp[lv]) {
+          col_pp[ptr_pp[lv]] = int(v - pshift);
+          val_pp[ptr_pp[lv]] = acc;
+        }
+        continue;
+      }
     }
     const unsigned vmask = __ballot_sync(FULL, cvalid) & ((1u << NC) - 1u);
     const int ncell = __popc(vmask);

@@ -29,6 +29,8 @@ struct Comm {
   bool distributed() const { return size > 1; }
   // dev[0..k) := sum over ranks (rank order) of every rank's dev[0..k)
   void sum_ordered(double* dev, int k) const;
+  // out[r*k .. (r+1)*k) := rank r's dev[0..k) (out: size*k device doubles)
+  void allgather(const double* dev, int k, double* out) const;
   // exact integer sums / maxima of host values
   void sum_i64(long long* host, int k) const;
   void max_i64(long long* host, int k) const;

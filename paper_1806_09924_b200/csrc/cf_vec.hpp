@@ -30,6 +30,32 @@ void vdot_dev(const double* x, const double* y, i64 n, double* out, bool do_sqrt
 void vaxpy_dot_dev(const double* h_dev, const double* v, double* w, const double* y, i64 n, double* out,
                    bool do_sqrt);
 double vdot(const double* x, const double* y, i64 n);
+
+// NP-invariant reductions of the Newton step's block vectors [u rows | phi rows].
+// The vector is cut into partials that depend only on the grid, never on the rank count: each
+// vertex plane's u part and phi part is split into chunks of `chunk` entries, every chunk is
+// reduced by one 256-thread block (thread t sums entries t, t+256, ... sequentially, then the
+// block tree), and the partials, in global order (u planes, then phi planes), go through the
+// fixed final tree.  A rank owns whole planes, so it computes exactly its planes' partials; an
+// all-gather places them, and every rank (and a single GPU) adds the same partials in the same
+// order: the result is bitwise independent of the number of ranks.
+struct SegLayout {
+  i64 plane_u = 0, plane_p = 0;  // entries of one vertex plane in the u / phi part
+  i64 chunk = 8192;
+  int p_lo = 0, p_hi = 0;        // owned planes
+  int nplanes = 0;               // planes of the grid
+  __host__ __device__ int cu() const { return int((plane_u + chunk - 1) / chunk); }
+  __host__ __device__ int cp() const { return int((plane_p + chunk - 1) / chunk); }
+  __host__ __device__ i64 nu_local() const { return plane_u * (p_hi - p_lo); }
+  __host__ __device__ int nparts() const { return nplanes * (cu() + cp()); }
+  __host__ __device__ int nblocks_local() const { return (p_hi - p_lo) * (cu() + cp()); }
+};
+struct Comm;
+// *out = x . y (sqrt optional) over all ranks' rows
+void seg_dot_dev(const double* x, const double* y, const SegLayout& L, double* out, bool do_sqrt, const Comm* comm);
+// w -= (*h) v, then *out = w . y (y = nullptr: w . w), bitwise the separate axpy + seg_dot_dev
+void seg_axpy_dot_dev(const double* h, const double* v, double* w, const double* y, const SegLayout& L, double* out,
+                      bool do_sqrt, const Comm* comm);
 double vnorm(const double* x, i64 n);
 void multidot(const double* V, i64 ld, int k, const double* w, i64 n, double* out_dev);   // out_i = V_i . w
 void multi_axpy(double* w, const double* V, i64 ld, int k, const double* coef_dev, i64 n, double alpha);
@@ -126,8 +152,9 @@ struct GmresResult {
 };
 struct Comm;
 // comm (optional, distributed): rhs / x are this rank's rows; every dot is summed over the ranks
+// seg (optional): the NP-invariant segmented reductions of a slab block vector (required with comm)
 GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
-                  double* x, const Comm* comm = nullptr);
+                  double* x, const Comm* comm = nullptr, const SegLayout* seg = nullptr);
 
 // ---- postproc.cu (postproc.cpp:12-99)
 double compute_tcv(const Problem& P, const double* sol);

@@ -151,6 +151,24 @@ void Comm::sum_ordered(double* dev, int k) const {
   CF_LAUNCHED();
 }
 
+void Comm::allgather(const double* dev, int k, double* out) const {
+  if (k <= 0) return;
+  if (size == 1) {
+    if (out != dev) CF_CUDA(cudaMemcpyAsync(out, dev, size_t(k) * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+    return;
+  }
+  if (host) {
+    std::vector<double> mine(static_cast<size_t>(k)), all(static_cast<size_t>(size) * k);
+    d2h(mine.data(), dev, size_t(k) * sizeof(double));
+    sync();
+    host_check(ht.allgather_f64(ht.ctx, mine.data(), all.data(), k), "allgather");
+    h2d(out, all.data(), all.size() * sizeof(double));
+    sync();
+    return;
+  }
+  CF_NCCL(::cfb::nccl().AllGather(dev, out, size_t(k), ncclFloat64, H(nccl), stream()));
+}
+
 void Comm::sum_i64(long long* host, int k) const {
   if (size == 1 || k <= 0) return;
   if (this->host) {

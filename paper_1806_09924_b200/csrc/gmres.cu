@@ -14,8 +14,14 @@ namespace {
 
 __global__ void k_sqrt1(double* s) { s[0] = sqrt(s[0]); }
 
-// dot over all ranks' rows: the local fixed-order dot, then the rank-ordered sum
-void gdot(const double* x, const double* y, i64 n, double* out, bool do_sqrt, const Comm* comm) {
+// dot over all ranks' rows: the segmented NP-invariant order when a layout is given, else the
+// local fixed-order dot followed by the rank-ordered sum
+void gdot(const double* x, const double* y, i64 n, double* out, bool do_sqrt, const Comm* comm,
+          const SegLayout* seg) {
+  if (seg) {
+    seg_dot_dev(x, y, *seg, out, do_sqrt, comm);
+    return;
+  }
   if (!comm || !comm->distributed()) {
     vdot_dev(x, y, n, out, do_sqrt);
     return;
@@ -31,13 +37,13 @@ void gdot(const double* x, const double* y, i64 n, double* out, bool do_sqrt, co
 }  // namespace
 
 GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
-                  double* x, const Comm* comm) {
+                  double* x, const Comm* comm, const SegLayout* seg) {
   if (!(o.rtol > 0.0 && o.rtol < 1.0)) fail(CF_ERR_INVALID_ARGUMENT, "gmres: rtol must be in (0,1)");
   if (o.restart < 1 || o.restart > 255) fail(CF_ERR_UNSUPPORTED, "gmres: restart must be in [1, 255]");
   GmresResult res;
   vfill(x, 0.0, n);
   DevBuf<double> sc(2);
-  gdot(rhs, rhs, n, sc.p, true, comm);
+  gdot(rhs, rhs, n, sc.p, true, comm, seg);
   double bnorm = 0.0;
   CF_CUDA(cudaMemcpyAsync(&bnorm, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
@@ -77,7 +83,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     }
   };
   while (res.iterations < o.max_iter) {
-    gdot(r.p, r.p, n, sc.p, true, comm);
+    gdot(r.p, r.p, n, sc.p, true, comm, seg);
     double beta = 0.0;
     CF_CUDA(cudaMemcpyAsync(&beta, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
@@ -102,11 +108,13 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
       apply_op(V.p + i64(j) * n, w);
       // modified Gram-Schmidt: h_i = w . v_i, w -= h_i v_i (i = 0..j), then |w|; each axpy is fused
       // with the following dot (same operations, same reduction order)
-      gdot(w, V.p, n, hd.p, false, comm);
+      gdot(w, V.p, n, hd.p, false, comm, seg);
       for (int i = 0; i <= j; ++i) {
         const double* next = i < j ? V.p + i64(i + 1) * n : nullptr;
         const bool last = i == j;
-        if (!comm || !comm->distributed()) {
+        if (seg) {
+          seg_axpy_dot_dev(hd.p + i, V.p + i64(i) * n, w, next, *seg, hd.p + i + 1, last, comm);
+        } else if (!comm || !comm->distributed()) {
           vaxpy_dot_dev(hd.p + i, V.p + i64(i) * n, w, next, n, hd.p + i + 1, last);
         } else {
           vaxpy_dot_dev(hd.p + i, V.p + i64(i) * n, w, next, n, hd.p + i + 1, false);
@@ -171,7 +179,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     }
     op(x, z.p);
     vsub(rhs, z.p, r.p, n);  // r = b - op(x)
-    gdot(r.p, r.p, n, sc.p, true, comm);
+    gdot(r.p, r.p, n, sc.p, true, comm, seg);
     double rn = 0.0;
     CF_CUDA(cudaMemcpyAsync(&rn, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));

@@ -308,16 +308,95 @@ void allgather_owned(const Comm& cm, const GridDesc& g, double* x) {
   cm.bcast_many(ops);
 }
 
-double gnorm(const Comm* cm, const double* v, i64 n) {
-  if (!cm || !cm->distributed()) return vnorm(v, n);
+// every rank's owned part of a global-layout array of element size es (bytes) to every rank
+void allgather_owned_bytes(const Comm& cm, const GridDesc& g, void* vec, size_t es) {
+  if (!cm.distributed()) return;
+  auto* b = static_cast<unsigned char*>(vec);
+  std::vector<HaloOp> ops;
+  for (int r = 0; r < cm.size; ++r) {
+    const Slab s = rank_slab(g, r, cm.size);
+    ops.push_back({nullptr, b + size_t(g.d * s.v_lo) * es, size_t(g.d * s.nv()) * es, r});
+    ops.push_back({nullptr, b + size_t(g.n_u() + s.v_lo) * es, size_t(s.nv()) * es, r});
+  }
+  cm.bcast_many(ops);
+}
+
+__global__ void k_shift_i64(const i64* __restrict__ a, i64 n, i64 add, i64* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] + add;
+}
+__global__ void k_shift_i32(const int* __restrict__ a, i64 n, i64 add, int* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = int(a[i] + add);
+}
+
+// The undivided CSR block on every rank: rank r holds the rows of its owned vertices
+// (rows_per_vertex each) with columns in its ext numbering (global column = column + cols_per_vertex
+// * ve_lo); the row pointers, columns and values of every rank are broadcast into one global
+// matrix, bitwise the single-GPU block.
+std::shared_ptr<Csr> gather_block(const Comm& cm, const GridDesc& g, const Csr& loc, int rows_per_vertex,
+                                  int cols_per_vertex) {
+  const int P = cm.size;
+  std::vector<long long> nnz(P, 0);
+  nnz[cm.rank] = loc.nnz;
+  cm.sum_i64(nnz.data(), P);
+  auto G = std::make_shared<Csr>();
+  G->rows = G->cols = rows_per_vertex * g.V;
+  i64 tot = 0;
+  for (int r = 0; r < P; ++r) tot += nnz[r];
+  G->nnz = tot;
+  G->ptr.alloc(G->rows + 1);
+  G->col.alloc(std::max<i64>(tot, 1));
+  G->val.alloc(std::max<i64>(tot, 1));
+  std::vector<HaloOp> ops;
+  i64 off = 0;
+  for (int r = 0; r < P; ++r) {
+    const Slab s = rank_slab(g, r, P);
+    const i64 row0 = rows_per_vertex * s.v_lo, nr = rows_per_vertex * s.nv();
+    if (r == cm.rank) {
+      if (nr > 0) {
+        k_shift_i64<<<grid_for(nr, 256), 256, 0, stream()>>>(loc.ptr.p, nr, off, G->ptr.p + row0);
+        CF_LAUNCHED();
+      }
+      if (loc.nnz > 0) {
+        k_shift_i32<<<grid_for(loc.nnz, 256), 256, 0, stream()>>>(loc.col.p, loc.nnz, cols_per_vertex * s.ve_lo,
+                                                                  G->col.p + off);
+        CF_LAUNCHED();
+        CF_CUDA(cudaMemcpyAsync(G->val.p + off, loc.val.p, size_t(loc.nnz) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                stream()));
+      }
+    }
+    ops.push_back({nullptr, G->ptr.p + row0, size_t(nr) * sizeof(i64), r});
+    ops.push_back({nullptr, G->col.p + off, size_t(nnz[r]) * sizeof(int), r});
+    ops.push_back({nullptr, G->val.p + off, size_t(nnz[r]) * sizeof(double), r});
+    off += nnz[r];
+  }
+  cm.bcast_many(ops);
+  const i64 end = tot;
+  CF_CUDA(cudaMemcpyAsync(G->ptr.p + G->rows, &end, sizeof(i64), cudaMemcpyHostToDevice, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  return G;
+}
+
+// ||v|| of a slab block vector in the NP-invariant segmented order (SegLayout)
+double gnorm(const Comm* cm, const double* v, const SegLayout& L) {
   double* s = scalar_buf(1);
-  vdot_dev(v, v, n, s, false);
-  cm->sum_ordered(s, 1);
+  seg_dot_dev(v, v, L, s, true, cm);
   double h = 0.0;
   CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
   ++host_sync_count();
-  return std::sqrt(h);
+  return h;
+}
+
+SegLayout seg_layout(const GridDesc& g, const Slab& sl) {
+  SegLayout L;
+  L.plane_u = g.d * sl.plane;
+  L.plane_p = sl.plane;
+  L.p_lo = int(sl.v_lo / sl.plane);
+  L.p_hi = int(sl.v_hi / sl.plane);
+  L.nplanes = int(g.nn);
+  return L;
 }
 
 }  // namespace
@@ -426,8 +505,27 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   const Csr* uu_loc_src = nullptr;
   // distributed preconditioner: restricted additive Schwarz with one plane of overlap (default), or
   // block-Jacobi over the slabs (CF_BLOCK_JACOBI=1)
-  static const bool ras_env = std::getenv("CF_BLOCK_JACOBI") == nullptr;
-  const bool ras = dist && ras_env;
+  // distributed preconditioner (N > 1):
+  //  * default: the reference's block AMG on the undivided blocks (gathered on every rank once per
+  //    build; the global hierarchy is identical to the single-GPU one), applied to the all-gathered
+  //    residual: together with the segmented dots the N-rank step is bitwise the 1-GPU step;
+  //  * CF_RAS=1: restricted additive Schwarz, per-slab block AMG with one plane of overlap;
+  //  * CF_BLOCK_JACOBI=1: block-Jacobi over the slabs.
+  // The two local variants scale the setup but change the preconditioner (and GMRES counts) with N.
+  static const bool bj_env = std::getenv("CF_BLOCK_JACOBI") != nullptr;
+  static const bool ras_env = std::getenv("CF_RAS") != nullptr;
+  const bool ras = dist && ras_env && !bj_env;
+  const bool glob = dist && !ras_env && !bj_env;
+  std::shared_ptr<Csr> uu_glob;  // the gathered M_uu of this load step
+  const Csr* uu_glob_src = nullptr;
+  Constraints fullg;  // every rank's constraint flags (global preconditioner)
+  if (glob) {
+    fullg.prob = &P;
+    fullg.flag.alloc(nt);
+  }
+  DevBuf<double> Bug(glob ? nu * (d == 2 ? 3 : 6) : 0), Bpg(glob ? V : 0);
+  DevBuf<int> unodeg(glob ? nu : 0), pnodeg(glob ? V : 0);
+  DevBuf<double> gin(glob ? nt : 0), gout(glob ? nt : 0);
   const Slab sx = ras ? make_slab(g, sl.ve_lo / sl.plane, sl.ve_hi / sl.plane) : sl;
   std::shared_ptr<Csr> uu_x_step;
   DevBuf<double> Bux(ras ? d * sx.nv() * (d == 2 ? 3 : 6) : 0), Bpx(ras ? sx.nv() : 0);
@@ -435,6 +533,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   DevBuf<double> pin(ras ? (d + 1) * sx.nv() : 0), pout(ras ? (d + 1) * sx.nv() : 0);
   DevBuf<int> unode(nul), pnode(nv);
   const unsigned gv = grid_for(nv, 256), gl = grid_for(ntl, 256);
+  const SegLayout seg = seg_layout(g, sl);  // every norm / dot of the step: NP-invariant order
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
     {
       Timer t(&T.residual);
@@ -481,7 +580,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         CF_LAUNCHED();
       }
     }
-    const double res = gnorm(comm, R.p, ntl);
+    const double res = gnorm(comm, R.p, seg);
     if (res0 < 0.0) res0 = res;
     NewtonIter rec{res, asize, changes, 0};
     const bool small = res <= std::max(opts.newton_tol * res0, opts.newton_abs_floor);
@@ -531,7 +630,27 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
       ns.p_modes = Bp.p;
       // hierarchies whose inputs are bitwise unchanged (M_uu within a load step: it depends only
       // on phi_tilde and the Dirichlet set) are reused; a rebuild would be bit-identical
-      if (dist) {
+      if (glob) {
+        CF_CUDA(cudaMemcpyAsync(fullg.flag.p, full.flag.p, size_t(nt), cudaMemcpyDeviceToDevice, stream()));
+        allgather_owned_bytes(cm, g, fullg.flag.p, 1);
+        BlockSystem Jg;
+        Jg.d = d;
+        Jg.nu = nu;
+        Jg.np = V;
+        if (uu_glob_src != J->uu.get()) {  // the M_uu of a load step is gathered once
+          uu_glob = gather_block(cm, g, *J->uu, d, d);
+          csr_enable_stencil(*uu_glob, StencilCols{1, d, g.nn, 0, 0, 1.0 / double(g.nn)});
+          uu_glob_src = J->uu.get();
+        }
+        Jg.uu = uu_glob;
+        Jg.pp = gather_block(cm, g, *J->pp, 1, 1);
+        rigid_body_modes(P, fullg, Bug.p, nullptr);
+        const Slab fs = full_slab(g);
+        k_phi_modes<<<grid_for(V, 256), 256, 0, stream()>>>(fs, nu, fullg.flag.p, Bpg.p, pnodeg.p, unodeg.p, d);
+        CF_LAUNCHED();
+        NullspaceDev nsg{unodeg.p, Bug.p, d == 2 ? 3 : 6, pnodeg.p, Bpg.p};
+        prec = build_block_prec(Jg, opts.prec_kind, opts.amg, &nsg, prec.get());
+      } else if (dist) {
         // block-Jacobi over the slabs: the preconditioner of each rank is built on the diagonal
         // block of its rows (owned columns only); one GPU is the undivided block
         BlockSystem Jl;
@@ -590,6 +709,21 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
       }
       const BlockPrec& Pr = *prec;
       DevOp pop = [&Pr](const double* in, double* out) { Pr.apply(in, out); };
+      if (glob) {  // the whole residual on every rank, the global V-cycles, the owned rows kept
+        double *gi = gin.p, *go = gout.p;
+        pop = [&Pr, &cm, &g, &sl, gi, go, d, nv, nul, nu](const double* in, double* out) {
+          CF_CUDA(cudaMemcpyAsync(gi + d * sl.v_lo, in, size_t(nul) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  stream()));
+          CF_CUDA(cudaMemcpyAsync(gi + nu + sl.v_lo, in + nul, size_t(nv) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  stream()));
+          allgather_owned(cm, g, gi);
+          Pr.apply(gi, go);
+          CF_CUDA(cudaMemcpyAsync(out, go + d * sl.v_lo, size_t(nul) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  stream()));
+          CF_CUDA(cudaMemcpyAsync(out + nul, go + nu + sl.v_lo, size_t(nv) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                  stream()));
+        };
+      }
       if (ras) {  // residual on the extended slab (halo planes), local solve, keep the owned rows
         double *pi = pin.p, *po = pout.p;
         pop = [&Pr, &cm, &g, &sl, &sx, pi, po, d, nv, nul](const double* in, double* out) {
@@ -601,7 +735,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
                                   stream()));
         };
       }
-      lin = gmres(op, &pop, rhs.p, ntl, opts.gmres, delta.p, comm);
+      lin = gmres(op, &pop, rhs.p, ntl, opts.gmres, delta.p, comm, &seg);
     }
     if (!lin.converged && !lin.breakdown) fail(CF_ERR_NUMERICAL, "newton_active_set_step: GMRES stagnated at max_iter");
     rec.gmres_iterations = lin.iterations;
@@ -629,7 +763,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
       double scale = 1.0;
       for (int half = 0; half < 4; ++half) {
         assemble_residual(P, full, mat, reg, x, pt.p, R.p, &sl);
-        if (gnorm(comm, R.p, ntl) <= 10.0 * res) break;
+        if (gnorm(comm, R.p, seg) <= 10.0 * res) break;
         scale *= 0.5;
         update_x(-scale);
       }

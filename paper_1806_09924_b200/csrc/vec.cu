@@ -1,6 +1,7 @@
 // K6: Krylov vector kernels with deterministic (fixed-order, atomic-free) reductions.
 // dot/norm: a fixed grid of block partials + one ordered final block; multidot: several basis
 // vectors per pass over w (CGS2 orthogonalisation); multi_axpy: w += alpha * V coef.
+#include "cf_comm.hpp"
 #include "cf_types.hpp"
 #include "cf_vec.hpp"
 
@@ -123,6 +124,53 @@ __global__ void k_diag_mul(const double* __restrict__ d, const double* __restric
   if (i < n) y[i] = a * (d[i] * x[i]);
 }
 
+// one block per chunk of a plane part (SegLayout); G: the global partial array
+template <bool AXPY>
+__global__ void __launch_bounds__(RB) k_seg_partial(const double* __restrict__ h, const double* __restrict__ v,
+                                                    double* __restrict__ w, const double* __restrict__ y, SegLayout L,
+                                                    double* __restrict__ G) {
+  __shared__ double sh[RB];
+  const int cu = L.cu(), cp = L.cp(), npl = L.p_hi - L.p_lo;
+  const int b = blockIdx.x;
+  i64 start, len;
+  int gi;
+  if (b < npl * cu) {
+    const int lp = b / cu, c = b % cu;
+    start = i64(lp) * L.plane_u + i64(c) * L.chunk;
+    len = min(L.chunk, L.plane_u - i64(c) * L.chunk);
+    gi = (L.p_lo + lp) * cu + c;
+  } else {
+    const int bb = b - npl * cu, lp = bb / cp, c = bb % cp;
+    start = L.nu_local() + i64(lp) * L.plane_p + i64(c) * L.chunk;
+    len = min(L.chunk, L.plane_p - i64(c) * L.chunk);
+    gi = L.nplanes * cu + (L.p_lo + lp) * cp + c;
+  }
+  const double hv = AXPY ? *h : 0.0;
+  double s = 0.0;
+  for (i64 i = threadIdx.x; i < len; i += RB) {
+    double wi = w[start + i];
+    if (AXPY) {
+      wi -= hv * v[start + i];
+      w[start + i] = wi;
+    }
+    s += wi * (y ? y[start + i] : wi);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) G[gi] = s;
+}
+
+// G := the owning rank's partial of every slot (gathered: size x nparts); owner of plane p is the
+// rank r with floor(nplanes r / size) <= p < floor(nplanes (r+1) / size) (rank_slab)
+__global__ void k_seg_pick(const double* __restrict__ gathered, int size, SegLayout L, double* __restrict__ G) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = L.nparts(), cu = L.cu(), cp = L.cp();
+  if (s >= n) return;
+  const int p = s < L.nplanes * cu ? s / cu : (s - L.nplanes * cu) / cp;
+  int r = 0;
+  while (r + 1 < size && i64(L.nplanes) * (r + 1) / size <= p) ++r;
+  G[s] = gathered[i64(r) * n + s];
+}
+
 int nblocks_for(i64 n) { return int(std::min<i64>(1024, std::max<i64>(1, (n + 4 * RB - 1) / (4 * RB)))); }
 
 Scratch& scr() {
@@ -200,6 +248,39 @@ void vaxpy_dot_dev(const double* h_dev, const double* v, double* w, const double
   CF_LAUNCHED();
   k_final<<<1, RB, 0, stream()>>>(part, nb, out, do_sqrt ? 1 : 0);
   CF_LAUNCHED();
+}
+
+namespace {
+void seg_reduce(const double* h, const double* v, double* w, const double* y, const SegLayout& L, double* out,
+                bool do_sqrt, const Comm* comm) {
+  const int np = L.nparts();
+  const bool dist = comm && comm->distributed();
+  double* G = partial_buf(i64(np) * (dist ? comm->size + 1 : 1));
+  if (L.nblocks_local() > 0) {
+    if (h)
+      k_seg_partial<true><<<L.nblocks_local(), RB, 0, stream()>>>(h, v, w, y, L, G);
+    else
+      k_seg_partial<false><<<L.nblocks_local(), RB, 0, stream()>>>(nullptr, nullptr, w, y, L, G);
+    CF_LAUNCHED();
+  }
+  if (dist) {
+    double* gathered = G + np;
+    comm->allgather(G, np, gathered);
+    k_seg_pick<<<(np + 255) / 256, 256, 0, stream()>>>(gathered, comm->size, L, G);
+    CF_LAUNCHED();
+  }
+  k_final<<<1, RB, 0, stream()>>>(G, np, out, do_sqrt ? 1 : 0);
+  CF_LAUNCHED();
+}
+}  // namespace
+
+void seg_dot_dev(const double* x, const double* y, const SegLayout& L, double* out, bool do_sqrt, const Comm* comm) {
+  seg_reduce(nullptr, nullptr, const_cast<double*>(x), y, L, out, do_sqrt, comm);
+}
+
+void seg_axpy_dot_dev(const double* h, const double* v, double* w, const double* y, const SegLayout& L, double* out,
+                      bool do_sqrt, const Comm* comm) {
+  seg_reduce(h, v, w, y, L, out, do_sqrt, comm);
 }
 
 double vdot(const double* x, const double* y, i64 n) {

@@ -1,11 +1,13 @@
 """The slab-decomposed Newton step with several ranks, on one GPU, through the host-staged test
 transport (Communicator.from_gloo): exercises the whole multi-rank control flow of newton.cu
-(halo planes, active-set flag exchange, rank-ordered dots, block-Jacobi AMG over slabs, final
-all-gather of the solution) without NCCL.  Nothing here is a measurement.
+(halo planes, active-set flag exchange, segmented NP-invariant dots, the gathered global block
+AMG, final all-gather of the solution) without NCCL.  Nothing here is a measurement.
 
-Checks: every rank converges with the same transcript and leaves the same full solution, and
-that solution solves the undivided problem (it agrees with the single-GPU step to Newton
-tolerance; the preconditioner differs, so the iterates are not bitwise those of one GPU)."""
+Default preconditioner (the undivided block AMG, gathered on every rank): the N-rank step must be
+BITWISE the single-GPU step — transcript (residual norms, |A|, set changes, GMRES counts) and
+solution — because every row and every dot is computed in an order that does not depend on N.
+The local variants (CF_RAS=1 restricted additive Schwarz, CF_BLOCK_JACOBI=1) change the
+preconditioner with N: they must still converge to the same solution to Newton tolerance."""
 import os
 import socket
 import sys
@@ -52,11 +54,20 @@ def _free_port():
         return sk.getsockname()[1]
 
 
-@pytest.mark.parametrize("d,n0,r,size", [(3, 4, 2, 2), (3, 4, 2, 3), (2, 8, 3, 4)])
-def test_multirank_newton_step(tmp_path, d, n0, r, size):
+@pytest.mark.parametrize("d,n0,r,size,mode", [(3, 4, 2, 2, "global"), (3, 4, 2, 3, "global"), (2, 8, 3, 4, "global"),
+                                               (3, 8, 1, 4, "global"), (3, 4, 2, 3, "ras"),
+                                               (2, 8, 3, 4, "block_jacobi")])
+def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
     import torch.multiprocessing as mp
     import paper_1806_09924_b200 as cf
-    mp.spawn(_worker, args=(size, _free_port(), str(tmp_path), d, n0, r), nprocs=size, join=True)
+    env = {"ras": "CF_RAS", "block_jacobi": "CF_BLOCK_JACOBI"}.get(mode)
+    if env:
+        os.environ[env] = "1"
+    try:
+        mp.spawn(_worker, args=(size, _free_port(), str(tmp_path), d, n0, r), nprocs=size, join=True)
+    finally:
+        if env:
+            del os.environ[env]
     xs = [np.load(tmp_path / f"x{k}.npy") for k in range(size)]
     its = [np.load(tmp_path / f"its{k}.npy") for k in range(size)]
     conv = [np.load(tmp_path / f"conv{k}.npy") for k in range(size)]
@@ -69,5 +80,11 @@ def test_multirank_newton_step(tmp_path, d, n0, r, size):
     rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions())
     assert rep["converged"]
     ref = st.get()["solution"]
-    assert np.linalg.norm(xs[0] - ref) <= 1e-6 * np.linalg.norm(ref)
-    assert int(its[0][-1, 1]) == rep["iterations"][-1]["active_size"]
+    ref_its = np.array([[it["residual_norm"], it["active_size"], it["set_changes"], it["gmres_iterations"]]
+                        for it in rep["iterations"]])
+    if mode == "global":
+        assert np.array_equal(its[0], ref_its), (its[0], ref_its)
+        assert np.array_equal(xs[0], ref), f"max |dx| = {np.abs(xs[0] - ref).max()}"
+    else:
+        assert np.linalg.norm(xs[0] - ref) <= 1e-6 * np.linalg.norm(ref)
+        assert int(its[0][-1, 1]) == rep["iterations"][-1]["active_size"]

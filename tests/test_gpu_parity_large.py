@@ -101,7 +101,11 @@ def _within_north_star(reps, x, oreps, xo, P=None, cf=None, O=None):
         ga, gb = ia[:, 3].sum(), ib[:, 3].sum()
         assert abs(ga - gb) <= 0.1 * gb, (ia, ib)
         assert a["converged"] and b["converged"]
-        assert ia[-1, 1] == ib[-1, 1], ("final active set size", ia[-1, 1], ib[-1, 1])
+        # the active set is decided by c (phi - phi_old) + lambda > 1e-14 c (solver.cpp:86): a dof
+        # whose indicator sits within rounding of the threshold can flip when the residual's
+        # summation order changes.  Measured: config 2 (2048^2, 3.57M active) differs by 1 dof,
+        # the 512^2 family by 3 (profiles/r02_refmode_config2*.json); the solution does not move.
+        assert abs(ia[-1, 1] - ib[-1, 1]) <= max(5, 2e-5 * ib[-1, 1]), ("final active set size", ia[-1, 1], ib[-1, 1])
     rel = np.linalg.norm(x - xo) / np.linalg.norm(xo)
     assert rel <= 1e-8, rel
     if P is not None:
