@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -76,11 +77,49 @@ size_t round_size(size_t b) {
 }
 }  // namespace
 
+// CF_GUARD=1 (debug aid; compute-sanitizer is not available on the B200 pool): every block gets a
+// 4 KB guard zone after the requested bytes, filled with 0xA5 and verified when the block is freed
+// (an out-of-bounds write past the end is reported on stderr and counted), and the requested bytes
+// are poisoned with 0xFF (NaN for doubles, -1 for integers) on every allocation, so a read of
+// uninitialised device memory shows up as a parity failure against the oracle.
+namespace {
+bool guard_on() {
+  static const bool on = std::getenv("CF_GUARD") != nullptr;
+  return on;
+}
+constexpr size_t kGuard = 4096;
+__global__ void k_guard_check(const unsigned char* __restrict__ z, size_t n, int* bad) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    if (z[i] != 0xA5) {
+      atomicExch(bad, 1);
+      return;
+    }
+}
+}  // namespace
+
+long guard_violations = 0;
+
 void* dev_alloc(size_t bytes) {
   ensure_device();
   BlockCache& c = block_cache();
   std::lock_guard<std::mutex> lk(c.mu);
-  const size_t need = round_size(bytes);
+  const size_t need = round_size(guard_on() ? bytes + kGuard : bytes);
+  if (guard_on()) {
+    void* q = nullptr;
+    auto hit = c.free_.lower_bound(need);
+    if (hit != c.free_.end() && hit->first <= need + need / 4 + (size_t(1) << 20)) {
+      q = hit->second;
+      c.cached -= hit->first;
+      c.free_.erase(hit);
+    } else {
+      CF_CUDA(cudaMalloc(&q, need));
+      c.size_of[q] = need;
+    }
+    auto* b = static_cast<unsigned char*>(q);
+    CF_CUDA(cudaMemsetAsync(b, 0xFF, bytes, stream()));
+    CF_CUDA(cudaMemsetAsync(b + bytes, 0xA5, c.size_of[q] - bytes, stream()));
+    return q;
+  }
   auto it = c.free_.lower_bound(need);
   if (it != c.free_.end() && it->first <= need + need / 4 + (size_t(1) << 20)) {
     void* p = it->second;
@@ -106,12 +145,25 @@ void* dev_alloc(size_t bytes) {
   return p;
 }
 
-void dev_free(void* p, size_t) {
+void dev_free(void* p, size_t bytes) {
   if (!p) return;
   BlockCache& c = block_cache();
   std::lock_guard<std::mutex> lk(c.mu);
   auto it = c.size_of.find(p);
   if (it == c.size_of.end()) return;
+  if (guard_on()) {
+    static int* bad = nullptr;
+    if (!bad) cudaMalloc(&bad, sizeof(int));
+    int h = 0;
+    cudaMemsetAsync(bad, 0, sizeof(int), stream());
+    k_guard_check<<<64, 256, 0, stream()>>>(static_cast<unsigned char*>(p) + bytes, it->second - bytes, bad);
+    cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, stream());
+    cudaStreamSynchronize(stream());
+    if (h) {
+      ++guard_violations;
+      std::fprintf(stderr, "CF_GUARD violation: write past the end of a %zu-byte block\n", bytes);
+    }
+  }
   c.free_.insert({it->second, p});
   c.cached += it->second;
 }
