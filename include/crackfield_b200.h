@@ -185,6 +185,12 @@ int cf_csr_create(int64_t rows, int64_t cols, const int64_t* rowptr, const int32
 int cf_block_csr(cf_block b, int which, cf_csr* out);
 int cf_csr_info(cf_csr A, int64_t* rows, int64_t* cols, int64_t* nnz);
 int cf_csr_spmv(cf_csr A, const double* x, double* y);
+/* The CSR arrays of A (rowptr: rows + 1; col, val: nnz), host or device pointers. */
+int cf_csr_export(cf_csr A, int64_t* rowptr, int32_t* col, double* val);
+/* C = diag(row_scale) A B (row_scale may be NULL): Eigen's sparse x sparse product as the AMG setup
+ * uses it (linsolve.cpp:248-263: D^-1 A T, A P, P^T (A P)); sorted columns, structural zeros kept,
+ * every entry the k-ascending sequential sum (any output row length). */
+int cf_csr_spgemm(cf_csr A, cf_csr B, const double* row_scale, cf_csr* out);
 int cf_csr_destroy(cf_csr A);
 
 /* ------------------------------------------------------------------ AMG */

@@ -2569,6 +2569,25 @@ int orc_csr_create(int64_t rows, int64_t cols, const int64_t* ptr, const int32_t
   ORC_CATCH
 }
 void orc_csr_destroy(orc_csr* c) { delete c; }
+// C = diag(rs) A B (rs may be null): the AMG setup's sparse product (k-ascending Gustavson)
+int orc_csr_spgemm(orc_csr* A, orc_csr* B, const double* rs, orc_csr** out) {
+  ORC_TRY
+  if (A->A.cols != B->A.rows) throw std::invalid_argument("spgemm: inner dimensions differ");
+  *out = new orc_csr{spgemm(A->A, B->A, rs)};
+  ORC_CATCH
+}
+int orc_csr_info(orc_csr* A, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  *rows = A->A.rows;
+  *cols = A->A.cols;
+  *nnz = A->A.nnz();
+  return 0;
+}
+int orc_csr_export(orc_csr* A, int64_t* ptr, int32_t* col, double* val) {
+  std::copy(A->A.ptr.begin(), A->A.ptr.end(), ptr);
+  std::copy(A->A.col.begin(), A->A.col.end(), col);
+  std::copy(A->A.val.begin(), A->A.val.end(), val);
+  return 0;
+}
 
 int orc_amg_build(orc_csr* A, const int32_t* node_of_dof, const double* B_colmajor, int m, const orc_amg_options* o,
                   orc_amg** out) {

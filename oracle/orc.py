@@ -340,6 +340,22 @@ class CsrHandle:
             pass
 
 
+def spgemm(A: Csr, B: Csr, row_scale=None) -> Csr:
+    """C = diag(row_scale) A B (the oracle's Gustavson product, linsolve.cpp:248-263)."""
+    ha, hb = CsrHandle(A), CsrHandle(B)
+    h = C.c_void_p()
+    rs = np.ascontiguousarray(row_scale, dtype=np.float64) if row_scale is not None else None
+    _chk(lib().orc_csr_spgemm(ha.h_, hb.h_, _p(rs), C.byref(h)))
+    r, c, n = C.c_int64(), C.c_int64(), C.c_int64()
+    lib().orc_csr_info(h, C.byref(r), C.byref(c), C.byref(n))
+    ptr = np.zeros(r.value + 1, dtype=np.int64)
+    col = np.zeros(n.value, dtype=np.int32)
+    val = np.zeros(n.value)
+    lib().orc_csr_export(h, _p(ptr, C.c_int64), _p(col, C.c_int32), _p(val))
+    lib().orc_csr_destroy(h)
+    return Csr(r.value, c.value, ptr, col, val)
+
+
 class Amg:
     def __init__(self, A: Csr, node_of_dof=None, B=None, opts=None):
         self.csr = CsrHandle(A)

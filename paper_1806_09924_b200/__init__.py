@@ -504,6 +504,21 @@ class CsrMatrix:
         check(load().cf_csr_spmv(self._h, _ptr(x), _ptr(y)))
         return y
 
+    def export(self) -> Csr:
+        """Host copy (rowptr, col, val) of the device matrix."""
+        rp = np.zeros(self.rows + 1, dtype=np.int64)
+        ci = np.zeros(self.nnz, dtype=np.int32)
+        vv = np.zeros(self.nnz)
+        check(load().cf_csr_export(self._h, _ptr(rp), _ptr(ci), _ptr(vv)))
+        return Csr(self.rows, self.cols, rp, ci, vv)
+
+    def matmul(self, B: "CsrMatrix", row_scale=None) -> "CsrMatrix":
+        """C = diag(row_scale) self B (linsolve.cpp:248-263, the AMG setup's sparse products)."""
+        h = C.c_void_p()
+        rs = _as_f64(row_scale) if row_scale is not None else None
+        check(load().cf_csr_spgemm(self._h, B._h, _ptr(rs) if rs is not None else None, C.byref(h)))
+        return CsrMatrix(_handle=h)
+
 
 class AmgHierarchy:
     """AmgHierarchy (linsolve.hpp:64-85) built by build_amg on the device."""

@@ -130,6 +130,8 @@ SIGNATURES = [
     ("cf_csr_create", _I, [_L, _L, _P, _P, _P, C.POINTER(_P)]),
     ("cf_block_csr", _I, [_P, _I, C.POINTER(_P)]),
     ("cf_csr_info", _I, [_P, C.POINTER(_L), C.POINTER(_L), C.POINTER(_L)]),
+    ("cf_csr_export", _I, [_P, _P, _P, _P]),
+    ("cf_csr_spgemm", _I, [_P, _P, _P, C.POINTER(_P)]),
     ("cf_csr_spmv", _I, [_P, _P, _P]),
     ("cf_csr_destroy", _I, [_P]),
     ("cf_amg_build", _I, [_P, _P, _P, _I, C.POINTER(AmgOptions), C.POINTER(_P)]),

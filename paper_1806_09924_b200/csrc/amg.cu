@@ -1030,6 +1030,76 @@ __global__ void __launch_bounds__(1024) k_dense_lu(int n, double* a, int* piv, d
   }
 }
 
+// Multi-CTA form of k_dense_lu for coarsest matrices beyond one CTA (n > 16384; the reference
+// LU-factors a coarsest matrix of any size, linsolve.cpp:277-285): per column k a pivot search
+// (one CTA, first maximal |a_ik|), the row swap and column division, and the rank-1 update of the
+// trailing block over the whole grid.  Every entry receives its updates in ascending k with the
+// same operands, so the factors are bitwise those of the one-CTA kernel and the oracle.
+__global__ void __launch_bounds__(1024) k_lu_pivot(int n, int k, const double* __restrict__ a, int* __restrict__ piv,
+                                                   double* __restrict__ big) {
+  __shared__ double sv[1024];
+  __shared__ int si[1024];
+  double best = -1.0;
+  int bi = k;
+  for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+    const double v = fabs(a[i64(k) * n + i]);
+    if (v > best) {
+      best = v;
+      bi = i;
+    }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double o = sv[threadIdx.x + s];
+      const int oi = si[threadIdx.x + s];
+      if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = o;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    piv[k] = si[0];
+    *big = sv[0];
+  }
+}
+__global__ void k_lu_swap(int n, int k, double* __restrict__ a, const int* __restrict__ piv,
+                          const double* __restrict__ big) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = piv[k];
+  if (j >= n || *big == 0.0 || p == k) return;
+  const double t = a[i64(j) * n + k];
+  a[i64(j) * n + k] = a[i64(j) * n + p];
+  a[i64(j) * n + p] = t;
+}
+__global__ void k_lu_scale(int n, int k, double* __restrict__ a, const double* __restrict__ big) {
+  const int i = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || *big == 0.0) return;
+  a[i64(k) * n + i] /= a[i64(k) * n + k];
+}
+__global__ void k_lu_update(int n, int k, double* __restrict__ a) {
+  const int i = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = k + 1 + blockIdx.y;
+  if (i >= n) return;
+  a[i64(j) * n + i] -= a[i64(k) * n + i] * a[i64(j) * n + k];
+}
+__global__ void k_lu_minpiv(int n, const double* __restrict__ a, double* minpiv) {
+  __shared__ double sm[256];
+  double m = INFINITY;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmin(m, fabs(a[i64(i) * n + i]));
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *minpiv = sm[0];
+}
+
 // is the CSR diagonal (no off-diagonal entries)?  diag[i] = a_ii (0 when absent)
 __global__ void k_check_diag(i64 n, const i64* __restrict__ p, const int* __restrict__ c,
                              const double* __restrict__ v, double* __restrict__ diag, int* __restrict__ offdiag) {
@@ -1125,21 +1195,22 @@ __global__ void k_jacobi_upd(i64 n, double w, const double* __restrict__ d, cons
 }
 
 // power-iteration start vector v_i = 1 + 0.5 sin(1 + i) (linsolve.cpp:123): computed on the host
-// with the C library's sin (correctly rounded) and cached per length.
+// with the C library's sin (correctly rounded).  v_i does not depend on the length, so one buffer
+// holds the longest prefix seen so far and every level (of every hierarchy) reads a prefix of it.
 const double* lambda_start(i64 n) {
-  static std::unordered_map<i64, std::unique_ptr<DevBuf<double>>> cache;
-  auto it = cache.find(n);
-  if (it != cache.end()) return it->second->p;
-  std::vector<double> h(n);
-  for (i64 i = 0; i < n; ++i) h[i] = 1.0 + 0.5 * std::sin(1.0 + double(i));
-  auto buf = std::make_unique<DevBuf<double>>(n);
-  CF_CUDA(cudaMemcpyAsync(buf->p, h.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, stream()));
+  static DevBuf<double> buf;
+  static std::vector<double> host;
+  if (i64(host.size()) >= n) return buf.p;
+  const i64 old = i64(host.size());
+  const i64 cap = std::max<i64>(n, old + old / 2);
+  host.resize(cap);
+  for (i64 i = old; i < cap; ++i) host[i] = 1.0 + 0.5 * std::sin(1.0 + double(i));
+  DevBuf<double> nb(cap);
+  CF_CUDA(cudaMemcpyAsync(nb.p, host.data(), size_t(cap) * sizeof(double), cudaMemcpyHostToDevice, stream()));
   CF_CUDA(cudaStreamSynchronize(stream()));
   ++host_sync_count();
-  const double* p = buf->p;
-  if (cache.size() > 64) cache.clear();
-  cache[n] = std::move(buf);
-  return p;
+  buf = std::move(nb);
+  return buf.p;
 }
 
 // power-iteration bookkeeping on the device: st = {lambda, done}; the first zero norm freezes
@@ -1190,7 +1261,10 @@ double estimate_lambda_max(const Csr& A, const double* inv_diag) {  // linsolve.
 void DenseLu::factor_from_csr(const Csr& A) {
   n = A.rows;
   diagonal = false;
-  if (n > 16384) {
+  // CF_LU_MULTICTA_MIN (test switch): smallest n factorised by the multi-CTA kernels (default 16385)
+  static const i64 multi_min = std::getenv("CF_LU_MULTICTA_MIN") ? std::atoll(std::getenv("CF_LU_MULTICTA_MIN")) : 16385;
+  if (n >= multi_min) {
+    if (n > 65535) fail(CF_ERR_UNSUPPORTED, "dense LU: coarsest matrix above 65535 rows (n^2 doubles)");
     lu.alloc(n);
     DevBuf<int> off(1);
     off.zero();
@@ -1207,9 +1281,32 @@ void DenseLu::factor_from_csr(const Csr& A) {
     CF_CUDA(cudaMemcpyAsync(&h_mn, mn.p, sizeof(h_mn), cudaMemcpyDeviceToHost, stream()));
     CF_CUDA(cudaStreamSynchronize(stream()));
     ++host_sync_count();
-    if (h_off) fail(CF_ERR_UNSUPPORTED, "dense LU: matrix too large for the one-CTA factorisation");
-    std::memcpy(&min_abs_pivot, &h_mn, sizeof(double));
-    diagonal = true;
+    if (!h_off) {  // a diagonal coarsest matrix: the LU is the diagonal itself
+      std::memcpy(&min_abs_pivot, &h_mn, sizeof(double));
+      diagonal = true;
+      return;
+    }
+    // a general coarsest matrix beyond one CTA: the multi-CTA factorisation (n^2 doubles)
+    lu.alloc(n * n);
+    lu.zero();
+    piv.alloc(n);
+    k_dense_from_csr<<<grid_for(n, 256), 256, 0, stream()>>>(n, A.ptr.p, A.col.p, A.val.p, lu.p);
+    CF_LAUNCHED();
+    double* big = scalar_buf(2);
+    for (int k = 0; k < int(n); ++k) {
+      k_lu_pivot<<<1, 1024, 0, stream()>>>(int(n), k, lu.p, piv.p, big);
+      k_lu_swap<<<grid_for(n, 256), 256, 0, stream()>>>(int(n), k, lu.p, piv.p, big);
+      const int rem = int(n) - k - 1;
+      if (rem > 0) {
+        k_lu_scale<<<grid_for(rem, 256), 256, 0, stream()>>>(int(n), k, lu.p, big);
+        k_lu_update<<<dim3(grid_for(rem, 256), unsigned(rem)), 256, 0, stream()>>>(int(n), k, lu.p);
+      }
+      count_launch(rem > 0 ? 4 : 2);
+    }
+    CF_CUDA(cudaGetLastError());
+    k_lu_minpiv<<<1, 256, 0, stream()>>>(int(n), lu.p, big + 1);
+    CF_LAUNCHED();
+    min_abs_pivot = read_dev(big + 1);
     return;
   }
   lu.alloc(std::max<i64>(n * n, 1));

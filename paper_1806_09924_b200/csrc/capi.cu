@@ -577,6 +577,31 @@ int cf_block_csr(cf_block b, int which, cf_csr* out) {
   });
 }
 
+int cf_csr_export(cf_csr A, int64_t* rowptr, int32_t* col, double* val) {
+  return guard([&] {
+    CHECK_ARG(A, "cf_csr_export: null handle");
+    const Csr& M = *A->A;
+    if (rowptr)
+      CF_CUDA(cudaMemcpyAsync(rowptr, M.ptr.p, size_t(M.rows + 1) * sizeof(i64), cudaMemcpyDefault, stream()));
+    if (col && M.nnz)
+      CF_CUDA(cudaMemcpyAsync(col, M.col.p, size_t(M.nnz) * sizeof(int), cudaMemcpyDefault, stream()));
+    if (val && M.nnz)
+      CF_CUDA(cudaMemcpyAsync(val, M.val.p, size_t(M.nnz) * sizeof(double), cudaMemcpyDefault, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+
+int cf_csr_spgemm(cf_csr A, cf_csr B, const double* row_scale, cf_csr* out) {
+  return guard([&] {
+    CHECK_ARG(A && B && out, "cf_csr_spgemm: bad argument");
+    CHECK_ARG(A->A->cols == B->A->rows, "cf_csr_spgemm: inner dimensions differ");
+    InArg<double> rs(row_scale, A->A->rows);
+    std::shared_ptr<Csr> C(spgemm(*A->A, *B->A, rs.dev).release());
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *out = new cf_csr_s{C};
+  });
+}
+
 int cf_csr_info(cf_csr A, int64_t* rows, int64_t* cols, int64_t* nnz) {
   return guard([&] {
     CHECK_ARG(A, "cf_csr_info: null handle");

@@ -39,7 +39,7 @@ void gdot(const double* x, const double* y, i64 n, double* out, bool do_sqrt, co
 GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, const cf_gmres_options& o,
                   double* x, const Comm* comm, const SegLayout* seg) {
   if (!(o.rtol > 0.0 && o.rtol < 1.0)) fail(CF_ERR_INVALID_ARGUMENT, "gmres: rtol must be in (0,1)");
-  if (o.restart < 1 || o.restart > 255) fail(CF_ERR_UNSUPPORTED, "gmres: restart must be in [1, 255]");
+  if (o.restart < 1) fail(CF_ERR_INVALID_ARGUMENT, "gmres: restart must be >= 1");
   GmresResult res;
   vfill(x, 0.0, n);
   DevBuf<double> sc(2);

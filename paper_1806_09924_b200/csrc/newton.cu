@@ -51,7 +51,7 @@ __global__ void k_active1(Slab sl, i64 nu, double c, double tol, const double* _
                           const double* __restrict__ po, const double* __restrict__ R,
                           const std::uint8_t* __restrict__ base_flag, const std::uint8_t* __restrict__ fixed,
                           std::uint8_t* __restrict__ active, std::uint8_t* __restrict__ tracked,
-                          unsigned long long* __restrict__ hist, int* __restrict__ any_tracked, int d) {
+                          unsigned long long* __restrict__ hist, int nw, int* __restrict__ any_tracked, int d) {
   const i64 lv = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (lv >= sl.nv()) return;
   const i64 v = sl.v_lo + lv;
@@ -63,16 +63,18 @@ __global__ void k_active1(Slab sl, i64 nu, double c, double tol, const double* _
   }
   active[lv] = a ? 1 : 0;
   bool tr = tracked[lv] != 0 || a;
-  if (tr) {
+  if (tr) {  // the history is an nw-word shift register per dof, newest entry in bit 0 of word 0
     tracked[lv] = 1;
-    hist[lv] = (hist[lv] << 1) | (a ? 1ull : 0ull);
+    unsigned long long* h = hist + lv * nw;
+    for (int k = nw - 1; k > 0; --k) h[k] = (h[k] << 1) | (h[k - 1] >> 63);
+    h[0] = (h[0] << 1) | (a ? 1ull : 0ull);
     *any_tracked = 1;
   }
 }
 
 // cycle detection on the last min(len, W) entries (solver.cpp:10-22, 97-100), set changes and |A|
 __global__ void k_active2(i64 V, int len, int window, int toggles, const std::uint8_t* __restrict__ tracked,
-                          const unsigned long long* __restrict__ hist, std::uint8_t* __restrict__ fixed,
+                          const unsigned long long* __restrict__ hist, int nw, std::uint8_t* __restrict__ fixed,
                           std::uint8_t* __restrict__ active, const std::uint8_t* __restrict__ prev,
                           int* __restrict__ counts) {
   const i64 v = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -80,10 +82,15 @@ __global__ void k_active2(i64 V, int len, int window, int toggles, const std::ui
   if (tracked[v]) {
     const int w = len < window ? len : window;
     int ch = 0;
-    if (w > 1) {
-      const unsigned long long t = hist[v] ^ (hist[v] >> 1);
-      const unsigned long long mask = (w - 1 >= 64) ? ~0ull : ((1ull << (w - 1)) - 1ull);
-      ch = __popcll(t & mask);
+    if (w > 1) {  // changes between entries i and i+1, i = 0 .. w-2 (bits of h ^ (h >> 1))
+      const unsigned long long* h = hist + v * nw;
+      for (int k = 0; k < nw && 64 * k < w - 1; ++k) {
+        const unsigned long long nxt = (k + 1 < nw) ? (h[k + 1] << 63) : 0ull;
+        const unsigned long long t = h[k] ^ ((h[k] >> 1) | nxt);
+        const int bits = w - 1 - 64 * k;
+        const unsigned long long mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+        ch += __popcll(t & mask);
+      }
     }
     if (ch >= toggles) {
       fixed[v] = 1;
@@ -470,8 +477,9 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   const int d = g.d;
   const i64 nu = g.n_u(), V = g.V, nt = g.n_total();
   const i64 nv = sl.nv(), nul = d * nv, ntl = (d + 1) * nv;  // this rank's rows
-  if (opts.cycle_window < 1 || opts.cycle_window > 64)
-    fail(CF_ERR_UNSUPPORTED, "newton_active_set_step: cycle_window must be in [1, 64]");
+  // history words per dof: the last `window` entries (any window, as detect_cycles, solver.cpp:10-22;
+  // window <= 1 sees no change)
+  const int nw = std::max(1, (opts.cycle_window + 63) / 64);
   NewtonReport report;
   PhaseTimes& T = report.times;
   auto base = build_constraints(P, true, 0, nullptr, nullptr);  // solver.cpp:55
@@ -481,7 +489,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   extrapolate_phi(st, pt.p, V);
   const double c = opts.active_set_c_scale * mat.G_c / reg.eps;
   DevBuf<std::uint8_t> fixed(nv), active(nv), prev(nv), tracked(nv);
-  DevBuf<unsigned long long> hist(nv);
+  DevBuf<unsigned long long> hist(nv * nw);
   fixed.zero();
   prev.zero();
   tracked.zero();
@@ -544,12 +552,12 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
       Timer t(&T.active_set);
       flags.zero();
       k_active1<<<gv, 256, 0, stream()>>>(sl, nu, c, 1e-14 * c, x, st.phi_old.p, R.p, base->flag.p, fixed.p,
-                                          active.p, tracked.p, hist.p, flags.p + 2, d);
+                                          active.p, tracked.p, hist.p, nw, flags.p + 2, d);
       CF_LAUNCHED();
       long long any = read_dev(flags.p + 2);
       cm.max_i64(&any, 1);
       if (any) ++hist_len;
-      k_active2<<<gv, 256, 0, stream()>>>(nv, hist_len, opts.cycle_window, opts.cycle_toggles, tracked.p, hist.p,
+      k_active2<<<gv, 256, 0, stream()>>>(nv, hist_len, opts.cycle_window, opts.cycle_toggles, tracked.p, hist.p, nw,
                                           fixed.p, active.p, prev.p, flags.p);
       CF_LAUNCHED();
       int hc[2];

@@ -682,6 +682,10 @@ __global__ void k_group_len(int ng, const int* __restrict__ heads, i64 rows, int
 }
 
 // gathered head rows (pattern only)
+__global__ void k_head_len_rows(int ng, const int* __restrict__ rows, const i64* __restrict__ p, i64* __restrict__ out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < ng) out[g] = p[rows[g] + 1] - p[rows[g]];
+}
 __global__ void k_head_len(int ng, const int* __restrict__ heads, const i64* __restrict__ p, i64* __restrict__ out) {
   const i64 g = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g < ng) out[g] = p[heads[g] + 1] - p[heads[g]];
@@ -940,6 +944,139 @@ __global__ void k_group_clen(int ng, const int* __restrict__ heads, const i64* _
   if (g < ng) out[g] = cp[heads[g] + 1] - cp[heads[g]];
 }
 
+// ---- giant rows (more than GIANT output columns, beyond the 16384-slot CTA hash): sort tier.
+// The row's products are expanded in A-position order (k ascending, then B-row order), keyed by
+// (giant row, column) and stably radix-sorted; equal keys then sit in k order, and each output
+// entry is the first product followed by the others added one by one — the k-ascending
+// sequential sum of every other tier (and of Eigen's conservative product).  Any row length.
+constexpr i64 GIANT = 12288;
+
+__global__ void k_giant_len(int ng, const int* __restrict__ rows, const i64* __restrict__ ap,
+                            const int* __restrict__ ac, const i64* __restrict__ bp, i64* __restrict__ len) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int i = rows[g];
+  i64 s = 0;
+  for (i64 k = ap[i]; k < ap[i + 1]; ++k) s += bp[ac[k] + 1] - bp[ac[k]];
+  len[g] = s;
+}
+__global__ void k_giant_expand(int ng, const int* __restrict__ rows, const i64* __restrict__ ap,
+                               const int* __restrict__ ac, const double* __restrict__ av,
+                               const double* __restrict__ rs, const i64* __restrict__ bp,
+                               const int* __restrict__ bc, const double* __restrict__ bv,
+                               const i64* __restrict__ off, unsigned long long* __restrict__ key,
+                               double* __restrict__ val) {
+  const int g = blockIdx.x;
+  const int i = rows[g];
+  i64 o = off[g];
+  for (i64 ka = ap[i]; ka < ap[i + 1]; ++ka) {
+    const int k = ac[ka];
+    const double a = rs ? rs[i] * av[ka] : (av ? av[ka] : 0.0);
+    const i64 q0 = bp[k];
+    const int n = int(bp[k + 1] - q0);
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      key[o + t] = (static_cast<unsigned long long>(g) << 32) | static_cast<unsigned>(bc[q0 + t]);
+      if (val) val[o + t] = a * bv[q0 + t];
+    }
+    o += n;
+  }
+}
+__global__ void k_zero_rows(int ng, const int* __restrict__ rows, i64* __restrict__ cnt) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < ng) cnt[rows[g]] = 0;
+}
+__global__ void k_giant_heads(i64 n, const unsigned long long* __restrict__ key, int* __restrict__ head) {
+  const i64 p = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p < n) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
+}
+__global__ void k_giant_count(i64 nu, const i64* __restrict__ hpos, const unsigned long long* __restrict__ key,
+                              const int* __restrict__ rows, i64* __restrict__ cnt) {
+  const i64 u = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u < nu) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[rows[int(key[hpos[u]] >> 32)]]), 1ull);
+}
+// unique u (in (giant row, column) order) -> its place in C: ptr[row] + (u - first[g])
+__global__ void k_giant_emit(i64 nu, i64 n, const i64* __restrict__ hpos, const unsigned long long* __restrict__ key,
+                             const double* __restrict__ val, const int* __restrict__ rows,
+                             const i64* __restrict__ first, const i64* __restrict__ cptr, int* __restrict__ ccol,
+                             double* __restrict__ cval) {
+  const i64 u = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= nu) return;
+  const i64 p0 = hpos[u], p1 = (u + 1 < nu) ? hpos[u + 1] : n;
+  const unsigned long long kk = key[p0];
+  const int g = int(kk >> 32);
+  const i64 pos = cptr[rows[g]] + (u - first[g]);
+  if (ccol) ccol[pos] = int(kk & 0xffffffffull);
+  if (cval) {
+    double s = val[p0];
+    for (i64 p = p0 + 1; p < p1; ++p) s += val[p];
+    cval[pos] = s;
+  }
+}
+
+// mode 0: cnt[row] := the row's number of distinct columns; mode 1: C.col of the rows;
+// mode 2: C.val of the rows.  rows: device list of ng giant rows.
+void giant_rows(int mode, const int* rows, int ng, const Csr& A, const Csr& B, const double* rs, i64* cnt, Csr* C) {
+  if (ng <= 0) return;
+  DevBuf<i64> off(ng + 1);
+  CF_CUDA(cudaMemsetAsync(off.p + ng, 0, sizeof(i64), stream()));
+  k_giant_len<<<grid_for(ng, 128), 128, 0, stream()>>>(ng, rows, A.ptr.p, A.col.p, B.ptr.p, off.p);
+  CF_LAUNCHED();
+  scan_excl(off.p, ng + 1);
+  const i64 n = read_i64(off.p + ng);
+  DevBuf<unsigned long long> key(n), key2(n);
+  DevBuf<double> val(mode == 2 ? n : 0), val2(mode == 2 ? n : 0);
+  k_giant_expand<<<ng, 256, 0, stream()>>>(ng, rows, A.ptr.p, A.col.p, mode == 2 ? A.val.p : nullptr, rs, B.ptr.p,
+                                           B.col.p, B.val.p, off.p, key.p, mode == 2 ? val.p : nullptr);
+  CF_LAUNCHED();
+  int hi_bit = 32;
+  while ((1ll << (hi_bit - 32)) < ng) ++hi_bit;
+  {
+    size_t bytes = 0;
+    if (mode == 2) {
+      CF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, val.p, val2.p, n, 0, hi_bit, stream()));
+      DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+      CF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, val.p, val2.p, n, 0, hi_bit, stream()));
+    } else {
+      CF_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, key.p, key2.p, n, 0, hi_bit, stream()));
+      DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+      CF_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, bytes, key.p, key2.p, n, 0, hi_bit, stream()));
+    }
+    count_launch();
+  }
+  key.release();
+  DevBuf<int> head(n);
+  k_giant_heads<<<grid_for(n, 256), 256, 0, stream()>>>(n, key2.p, head.p);
+  CF_LAUNCHED();
+  DevBuf<i64> hpos(n);
+  DevBuf<i64> nsel(1);
+  {
+    size_t bytes = 0;
+    thrust::counting_iterator<i64> it(0);
+    CF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, head.p, hpos.p, nsel.p, n, stream()));
+    DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+    CF_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, head.p, hpos.p, nsel.p, n, stream()));
+    count_launch();
+  }
+  const i64 nu = read_i64(nsel.p);
+  if (mode == 0) {
+    k_zero_rows<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, rows, cnt);  // drop the overflow marks
+    CF_LAUNCHED();
+    k_giant_count<<<grid_for(nu, 256), 256, 0, stream()>>>(nu, hpos.p, key2.p, rows, cnt);
+    CF_LAUNCHED();
+    return;
+  }
+  // first unique of every giant row: exclusive prefix of the rows' lengths, in giant order
+  DevBuf<i64> first(ng + 1);
+  CF_CUDA(cudaMemsetAsync(first.p + ng, 0, sizeof(i64), stream()));
+  k_head_len_rows<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, rows, C->ptr.p, first.p);
+  CF_LAUNCHED();
+  scan_excl(first.p, ng + 1);
+  k_giant_emit<<<grid_for(nu, 256), 256, 0, stream()>>>(nu, n, hpos.p, key2.p, mode == 2 ? val2.p : nullptr, rows,
+                                                        first.p, C->ptr.p, mode == 1 ? C->col.p : nullptr,
+                                                        mode == 2 ? C->val.p : nullptr);
+  CF_LAUNCHED();
+}
+
 }  // namespace
 
 // pattern of C = A B (sorted columns; values allocated, not computed); L lanes per B row
@@ -1014,7 +1151,10 @@ static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L, i
       k_sym_cta<SYM_BIG><<<o2.n, 256, sm, stream()>>>(o2.list.p, o2.n, A.ptr.p, A.col.p, B.ptr.p, B.col.p, cnt,
                                                       nullptr, nullptr, 0, flag.p);
       CF_LAUNCHED();
-      if (read_int(flag.p)) fail(CF_ERR_UNSUPPORTED, "spgemm: an output row exceeds 12288 columns");
+      if (read_int(flag.p)) {  // rows beyond the CTA hash: the sort tier counts them exactly
+        RowBin o3 = overflow_of(o2, cnt);
+        giant_rows(0, o3.list.p, o3.n, A, B, nullptr, cnt, nullptr);
+      }
     }
   }
   scan_excl(C->ptr.p, m + 1);
@@ -1040,7 +1180,9 @@ static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L, i
     k_scatter_len<<<grid_for(o1.n, 256), 256, 0, stream()>>>(o1.list.p, o1.n, len.p, olen.p);
     CF_LAUNCHED();
     g2 = make_bin(m, olen.p, 0, 1024);
-    g3 = make_bin(m, olen.p, 1024, LLONG_MAX);
+    g3 = make_bin(m, olen.p, 1024, GIANT);
+    RowBin g4 = make_bin(m, olen.p, GIANT, LLONG_MAX);
+    giant_rows(1, g4.list.p, g4.n, A, B, nullptr, nullptr, C.get());
   }
   sym_dispatch(L, 1, g2, 2048, A, B, nullptr, C.get());
   if (g3.n) {
@@ -1091,7 +1233,11 @@ static void spgemm_numeric(const Csr& A, const Csr& B, const double* row_scale, 
   }
   RowBin f1 = make_bin(m, lensel, 0, 256);
   RowBin f2 = make_bin(m, lensel, 256, 1024);
-  RowBin f3 = make_bin(m, lensel, 1024, LLONG_MAX);
+  RowBin f3 = make_bin(m, lensel, 1024, GIANT);
+  {
+    RowBin f4 = make_bin(m, lensel, GIANT, LLONG_MAX);  // beyond the CTA hash: the sort tier
+    giant_rows(2, f4.list.p, f4.n, A, B, row_scale, nullptr, &C);
+  }
   const i64 cmax_need = (maxb + L - 1) / L;
   bool warp_ok = true;
   if (cmax_need <= 8) {
@@ -1106,7 +1252,7 @@ static void spgemm_numeric(const Csr& A, const Csr& B, const double* row_scale, 
   } else {
     warp_ok = false;
   }
-  RowBin n3 = warp_ok ? std::move(f3) : make_bin(m, lensel, 0, LLONG_MAX);
+  RowBin n3 = warp_ok ? std::move(f3) : make_bin(m, lensel, 0, GIANT);
   if (n3.n) {
     const size_t sm = size_t(SYM_BIG) * (sizeof(double) + sizeof(int));
     CF_CUDA(cudaFuncSetAttribute(k_num_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));

@@ -82,16 +82,22 @@ __global__ void __launch_bounds__(RB) k_multidot_partial(const double* __restric
   }
 }
 
+// w += alpha * sum_c coef_c V_c: one sequential sum per entry over c ascending; the coefficients
+// are staged in shared memory 256 at a time (any number of basis vectors)
 __global__ void k_multi_axpy(double* __restrict__ w, const double* __restrict__ V, i64 ld, int k,
                              const double* __restrict__ coef, i64 n, double alpha) {
   __shared__ double cs[256];
-  for (int c = threadIdx.x; c < k && c < 256; c += blockDim.x) cs[c] = coef[c];
-  __syncthreads();
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
   double s = 0.0;
-  for (int c = 0; c < k; ++c) s += cs[c] * V[c * ld + i];
-  w[i] += alpha * s;
+  for (int c0 = 0; c0 < k; c0 += 256) {
+    const int kc = min(256, k - c0);
+    __syncthreads();
+    for (int c = threadIdx.x; c < kc; c += blockDim.x) cs[c] = coef[c0 + c];
+    __syncthreads();
+    if (i < n)
+      for (int c = 0; c < kc; ++c) s += cs[c] * V[i64(c0 + c) * ld + i];
+  }
+  if (i < n) w[i] += alpha * s;
 }
 
 __global__ void k_fill(double* x, double a, i64 n) {
@@ -317,7 +323,6 @@ void multidot(const double* V, i64 ld, int k, const double* w, i64 n, double* ou
 
 void multi_axpy(double* w, const double* V, i64 ld, int k, const double* coef_dev, i64 n, double alpha) {
   if (k <= 0 || n <= 0) return;
-  if (k > 256) fail(CF_ERR_UNSUPPORTED, "multi_axpy: more than 256 basis vectors");
   k_multi_axpy<<<grid_for(n, 256), 256, 0, stream()>>>(w, V, ld, k, coef_dev, n, alpha);
   CF_LAUNCHED();
 }
