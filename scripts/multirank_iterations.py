@@ -1,8 +1,9 @@
 """Algorithmic scaling of the slab decomposition: GMRES / Newton iteration counts of one config-3
-Newton step with N ranks (restricted additive Schwarz over N z-slabs, or block-Jacobi with
-CF_BLOCK_JACOBI=1), run with N processes sharing one GPU
-through the host-staged test transport (Communicator.from_gloo).  Only the iteration counts and the
-agreement of the solutions are meaningful here — the transport is not a timing.
+Newton step with N ranks (default: the gathered global block AMG, bitwise the 1-GPU step;
+CF_RAS=1 restricted additive Schwarz over N z-slabs, CF_BLOCK_JACOBI=1 block-Jacobi), run with N
+processes sharing one GPU through the host-staged test transport (Communicator.from_gloo).  Only the
+iteration counts and the agreement of the solutions are meaningful here — the transport is not a
+timing.  The rank-0 JSON carries a SHA-256 of the full solution.
 
 usage: python scripts/multirank_iterations.py N [cfg3|cfg2]"""
 import json
@@ -30,8 +31,11 @@ def worker(rank, size, port, cfg, out):
     rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(), comm=comm)
     if rank == 0:
         x = st.get()["solution"]
+        import hashlib
         np.save(out + f"_x{size}.npy", x[::97].copy())  # a sample: the full vector exceeds the copy-back limit
         json.dump({"ranks": size, "converged": rep["converged"],
+                   "sha256": hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest(),
+                   "residuals": [it["residual_norm"] for it in rep["iterations"]],
                    "newton": len(rep["iterations"]),
                    "gmres": [it["gmres_iterations"] for it in rep["iterations"]],
                    "active": rep["iterations"][-1]["active_size"]}, open(out + f"_{size}.json", "w"))
