@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <unordered_map>
 
+#include "cf_comm.hpp"
 #include "cf_vec.hpp"
 
 namespace cg = cooperative_groups;
@@ -1677,12 +1678,21 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
 // x + P x_c lands in the level's scratch vector so the fused sweep can read it while writing x;
 // the same IEEE operations as the separate kernels (CF_VCYCLE_UNFUSED=1 runs those).
 void Amg::vcycle(const double* r, double* x) const {
+  if (!dist.empty()) {
+    vcycle_dist(r, x);
+    return;
+  }
+  vcycle_range(0, r, x);
+}
+
+// the V-cycle of levels l0.. for the right-hand side b0 of level l0, output x0 (linsolve.cpp:295-312)
+void Amg::vcycle_range(size_t l0, const double* b0, double* x0) const {
   static const bool unfused = std::getenv("CF_VCYCLE_UNFUSED") != nullptr;
-  const double* b = r;
-  for (size_t l = 0; l < levels.size(); ++l) {
+  const double* b = b0;
+  for (size_t l = l0; l < levels.size(); ++l) {
     const AmgLevel& L = *levels[l];
     const i64 n = L.A->rows;
-    double* xl = (l == 0) ? x : levels[l - 1]->tmp_x.p;
+    double* xl = (l == l0) ? x0 : levels[l - 1]->tmp_x.p;
     const double w = L.jacobi_weight;
     k_jacobi0<<<grid_for(n, 256), 256, 0, stream()>>>(n, w, L.inv_diag.p, b, xl);
     CF_LAUNCHED();
@@ -1705,13 +1715,13 @@ void Amg::vcycle(const double* r, double* x) const {
   }
   // coarsest
   const double* bc = b;
-  double* xc = levels.empty() ? x : levels.back()->tmp_x.p;
+  double* xc = (levels.size() == l0) ? x0 : levels.back()->tmp_x.p;
   coarse.solve(bc, xc);
-  for (size_t l = levels.size(); l-- > 0;) {
+  for (size_t l = levels.size(); l-- > l0;) {
     const AmgLevel& L = *levels[l];
     const i64 n = L.A->rows;
-    double* xl = (l == 0) ? x : levels[l - 1]->tmp_x.p;
-    const double* bl = (l == 0) ? r : levels[l - 1]->tmp_b.p;
+    double* xl = (l == l0) ? x0 : levels[l - 1]->tmp_x.p;
+    const double* bl = (l == l0) ? b0 : levels[l - 1]->tmp_b.p;
     int s = 0;
     if (unfused || opts.smoothing_sweeps < 1) {
       csr_spmv_add(*L.P, L.tmp_x.p, xl, xl);  // x += P x_c
@@ -1731,6 +1741,84 @@ void Amg::vcycle(const double* r, double* x) const {
       CF_LAUNCHED();
     }
   }
+}
+
+// ------------------------------------------------------------------ distributed V-cycle (§8e)
+// The hierarchy is built identically on every rank; the leading levels with at least min_rows rows
+// are then split by rows: each rank keeps row slices of A, P and R (carrying the undivided lane
+// split) and applies only its rows, the level vectors travel by in-place all-gathers, and the
+// remaining small levels run redundantly on every rank.  Every row is computed exactly as on one
+// GPU, so the V-cycle output is bitwise independent of the rank count.
+void Amg::distribute(const Comm* cm, i64 min_rows) {
+  dist.clear();
+  comm = cm;
+  if (!cm || !cm->distributed() || opts.smoothing_sweeps != 1) return;
+  static const bool unfused = std::getenv("CF_VCYCLE_UNFUSED") != nullptr;
+  if (unfused) return;
+  const int P = cm->size, r = cm->rank;
+  for (size_t l = 0; l < levels.size(); ++l) {
+    const AmgLevel& L = *levels[l];
+    const i64 n = L.A->rows, nc = L.P->cols;
+    if (n < min_rows) break;
+    DistLevel D;
+    // row chunks aligned to the stencil format's vertex rows (d rows per vertex)
+    const i64 align = L.A->st.kind == 1 ? L.A->st.d : 1;
+    D.chunk = ((n + P - 1) / P + align - 1) / align * align;
+    D.cchunk = (nc + P - 1) / P;
+    D.lo = std::min(n, r * D.chunk);
+    D.hi = std::min(n, (r + 1) * D.chunk);
+    D.clo = std::min(nc, r * D.cchunk);
+    D.chi = std::min(nc, (r + 1) * D.cchunk);
+    D.A = csr_extract_rows(*L.A, D.lo, D.hi);
+    if (L.A->st.kind == 1)
+      csr_enable_stencil(*D.A, StencilCols{1, L.A->st.d, L.A->st.nn, D.lo / L.A->st.d, 0, L.A->st.inv_nn});
+    D.P = csr_extract_rows(*L.P, D.lo, D.hi);
+    D.R = csr_extract_rows(*L.R, D.clo, D.chi);
+    D.x.alloc(P * D.chunk);
+    D.r.alloc(P * D.chunk);
+    D.bc.alloc(P * D.cchunk);
+    dist.push_back(std::move(D));
+  }
+}
+
+void Amg::vcycle_dist(const double* r, double* x) const {
+  const size_t nd = dist.size();
+  const double* b = r;
+  for (size_t l = 0; l < nd; ++l) {  // down: pre-smooth (redundant), own residual rows, own R rows
+    const AmgLevel& L = *levels[l];
+    const DistLevel& D = dist[l];
+    const i64 n = L.A->rows;
+    k_jacobi0<<<grid_for(n, 256), 256, 0, stream()>>>(n, L.jacobi_weight, L.inv_diag.p, b, D.x.p);
+    CF_LAUNCHED();
+    SpmvEpi ep;
+    ep.b = b + D.lo;
+    ep.mode = 1;
+    if (D.hi > D.lo) csr_spmv_epi(*D.A, D.x.p, D.r.p + D.lo, ep);  // r = b - A x (own rows)
+    comm->allgather_inplace(D.r.p, D.chunk);
+    if (D.chi > D.clo) csr_spmv_add(*D.R, D.r.p, D.bc.p + D.clo, nullptr);  // b_c = P^T r (own rows)
+    comm->allgather_inplace(D.bc.p, D.cchunk);
+    b = D.bc.p;
+  }
+  // the small levels and the coarsest solve: redundant on every rank
+  double* xc = levels[nd - 1]->tmp_x.p;
+  vcycle_range(nd, b, xc);
+  for (size_t l = nd; l-- > 0;) {  // up: own rows of t = x + P x_c and of the post-smoothing sweep
+    const AmgLevel& L = *levels[l];
+    const DistLevel& D = dist[l];
+    const double* bl = (l == 0) ? r : dist[l - 1].bc.p;
+    const double* xcl = (l + 1 == nd) ? levels[l]->tmp_x.p : dist[l + 1].x.p;
+    if (D.hi > D.lo) csr_spmv_add(*D.P, xcl, D.r.p + D.lo, D.x.p + D.lo);
+    comm->allgather_inplace(D.r.p, D.chunk);
+    SpmvEpi ep;
+    ep.b = bl + D.lo;
+    ep.d = L.inv_diag.p + D.lo;
+    ep.w = L.jacobi_weight;
+    ep.mode = 2;
+    ep.xoff = D.lo;
+    if (D.hi > D.lo) csr_spmv_epi(*D.A, D.r.p, D.x.p + D.lo, ep);
+    comm->allgather_inplace(D.x.p, D.chunk);
+  }
+  vcopy(x, dist[0].x.p, levels[0]->A->rows);
 }
 
 // ------------------------------------------------------------------ input identity (reuse)
@@ -1831,9 +1919,9 @@ void BlockPrec::apply(const double* r, double* z) const {  // linsolve.cpp:398-4
     // the two V-cycles are independent (separate hierarchies, work vectors and output ranges): the
     // phi cycle runs on the auxiliary stream while the u cycle runs on the library stream, so
     // the small coarse-level kernels of one overlap the other
-    static const bool serial = std::getenv("CF_SERIAL_VCYCLES") != nullptr;
+    static const bool serial_env = std::getenv("CF_SERIAL_VCYCLES") != nullptr;
     Runtime& R = rt();
-    if (serial || np == 0) {
+    if (serial_env || serial || np == 0) {
       amg_u->vcycle(r, z);
       amg_p->vcycle(r + nu, z + nu);
       return;

@@ -31,6 +31,8 @@ struct Comm {
   void sum_ordered(double* dev, int k) const;
   // out[r*k .. (r+1)*k) := rank r's dev[0..k) (out: size*k device doubles)
   void allgather(const double* dev, int k, double* out) const;
+  // buf[r*k .. (r+1)*k) := rank r's own chunk of buf, in place (buf: size*k device doubles)
+  void allgather_inplace(double* buf, i64 k) const;
   // exact integer sums / maxima of host values
   void sum_i64(long long* host, int k) const;
   void max_i64(long long* host, int k) const;

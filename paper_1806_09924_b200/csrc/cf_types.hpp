@@ -127,6 +127,7 @@ struct SpmvEpi {
   const double* d = nullptr;
   double w = 0.0;
   int mode = 0;
+  i64 xoff = 0;  // mode 2 reads x[row + xoff] (a row slice of a square matrix applied to a full x)
 };
 void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep);
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);

@@ -70,6 +70,8 @@ void csr_diagonal(const Csr& A, double* diag);  // A(i,i) or 0
 std::unique_ptr<Csr> csr_copy(const Csr& A);
 // the entries with column in [lo, hi), columns renumbered from lo (a slab's diagonal block)
 std::unique_ptr<Csr> csr_extract_cols(const Csr& A, i64 lo, i64 hi);
+// rows [lo, hi) (all columns), carrying the lane split of A (mean_hint)
+std::unique_ptr<Csr> csr_extract_rows(const Csr& A, i64 lo, i64 hi);
 
 // ---- dense LU (amg.cu): column-major n x n, unblocked partial pivoting (PartialPivLU)
 struct DenseLu {
@@ -98,8 +100,24 @@ struct AmgLevel {
   mutable DevBuf<double> tmp_r, tmp_b, tmp_x;  // V-cycle work vectors of this level
 };
 
+struct Comm;
+// A level whose rows are split over the ranks (distributed V-cycle): rank r applies
+// rows [r c, (r+1) c) of A and P and rows [r cc, (r+1) cc) of R (c, cc: chunks padded so the
+// vectors all-gather in place), every row exactly as the undivided operator computes it.
+struct DistLevel {
+  std::shared_ptr<Csr> A, P, R;
+  i64 chunk = 0, cchunk = 0, lo = 0, hi = 0, clo = 0, chi = 0;
+  mutable DevBuf<double> x, r, bc;  // padded to size x chunk (size x cchunk for bc)
+};
+
 struct Amg {
   std::vector<std::unique_ptr<AmgLevel>> levels;
+  std::vector<DistLevel> dist;  // leading levels split over the ranks (empty: single-GPU V-cycle)
+  const Comm* comm = nullptr;
+  // split the large leading levels over the ranks of cm (the hierarchy itself is replicated)
+  void distribute(const Comm* cm, i64 min_rows);
+  void vcycle_range(size_t l0, const double* b0, double* x0) const;  // levels l0.. (single GPU)
+  void vcycle_dist(const double* r, double* x) const;
   DenseLu coarse;
   cf_amg_options opts{};
   i64 n = 0;
@@ -121,6 +139,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A, const int* node_of_dof, c
 // ---- block preconditioner (linsolve.cpp:352-415)
 struct BlockPrec {
   int kind = 1;  // 0 exact, 1 amg, 2 diagonal
+  bool serial = false;  // V-cycles in sequence on the library stream (distributed hierarchies)
   i64 nu = 0, np = 0;
   std::shared_ptr<Amg> amg_u, amg_p;
   std::shared_ptr<DenseLu> lu_u, lu_p;

@@ -169,6 +169,20 @@ void Comm::allgather(const double* dev, int k, double* out) const {
   CF_NCCL(::cfb::nccl().AllGather(dev, out, size_t(k), ncclFloat64, H(nccl), stream()));
 }
 
+void Comm::allgather_inplace(double* buf, i64 k) const {
+  if (size == 1 || k <= 0) return;
+  if (host) {
+    std::vector<double> mine(static_cast<size_t>(k)), all(static_cast<size_t>(size) * k);
+    d2h(mine.data(), buf + i64(rank) * k, size_t(k) * sizeof(double));
+    sync();
+    host_check(ht.allgather_f64(ht.ctx, mine.data(), all.data(), int(k)), "allgather");
+    h2d(buf, all.data(), all.size() * sizeof(double));
+    sync();
+    return;
+  }
+  CF_NCCL(::cfb::nccl().AllGather(buf + i64(rank) * k, buf, size_t(k), ncclFloat64, H(nccl), stream()));
+}
+
 void Comm::sum_i64(long long* host, int k) const {
   if (size == 1 || k <= 0) return;
   if (this->host) {

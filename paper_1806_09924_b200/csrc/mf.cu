@@ -14,6 +14,9 @@
 // and a boundary pass forms the constrained rows.  The element arithmetic is FMA-contracted
 // (this file only): the operator is compared with the assembled apply to 1e-12 relative, not
 // bitwise (its reduction order differs from any CSR row order anyway).
+#include <cmath>
+#include <cstdlib>
+
 #include "cf_vec.hpp"
 
 namespace cfb {
@@ -197,6 +200,228 @@ __global__ void k_mf_diag(GridDesc g, const Tables* __restrict__ T, double mu, d
   }
 }
 
+// ---- single-pass 3d kernel: z-sweeping columns of 8 x 8 owned vertices --------------------------
+// A CTA owns the vertices of an 8 x 8 column segment in x-y and sweeps it along z.  Per cell layer
+// L it computes the 9 x 9 cells touching its columns (a one-cell ring in x-y is recomputed, so no
+// partial sum leaves the CTA), with u and phi_tilde of a rolling window of three vertex planes in
+// shared memory (u read as 0 on constrained columns).  Vertex plane L is complete after layers L-1
+// and L: each owned vertex adds its upper-layer corners (k = 4..7, from layer L-1) and then its
+// lower-layer corners (k = 0..3) in a fixed order and writes its rows once; constrained rows get
+// the summed element diagonal times x (the assembled block's condensation).  No global scratch,
+// no host round trip; deterministic.
+//
+// Sum factorisation of Q1 on the 2-point Gauss rule (corner k = i + 2j + 4l, point (p, q, r)):
+// du_a/dx at (p,q,r) = (1/h) sum_{j,l} N_j(q) N_l(r) [u_a(1,j,l) - u_a(0,j,l)] (likewise y, z), and
+// the test side sum_q sigma_ab d_b N_k is accumulated per direction in 2 x 2 face sums.  About 1650
+// flops per cell instead of the canonical 2688 of the point-wise form.
+constexpr int MFB = 8, MFT = MFB + 2, MFC = MFB + 1, MF_CS = 25;  // cell-output stride (odd)
+constexpr int MF_THREADS = 96;                                     // >= MFC * MFC = 81 cells per layer
+constexpr int MF_ZSEG = 48;                                        // cell layers per CTA
+
+// the 24 outputs (k*3 + a) of one cell; U(i,j,l,a) and PT(i,j,l) read the corner values
+template <class FU, class FP>
+__device__ __forceinline__ void mf_cell(FU U, FP PT, double xi0, double xi1, double mu, double lam, double kap,
+                                        double scale, double* __restrict__ o) {
+  const double N[2][2] = {{xi1, xi0}, {xi0, xi1}};  // N[point][shape]: N_0(xi_p), N_1(xi_p)
+  double Dx[3][2][2], Dy[3][2][2], Dz[3][2][2], pc[2][2][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n2 = 0; n2 < 2; ++n2) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        Dx[a][m][n2] = U(1, m, n2, a) - U(0, m, n2, a);  // (j, l)
+        Dy[a][m][n2] = U(m, 1, n2, a) - U(m, 0, n2, a);  // (i, l)
+        Dz[a][m][n2] = U(m, n2, 1, a) - U(m, n2, 0, a);  // (i, j)
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) pc[i][m][n2] = PT(i, m, n2);
+    }
+  double Tx[3][2][2], Ty[3][2][2], Tz[3][2][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+      for (int n2 = 0; n2 < 2; ++n2) Tx[a][m][n2] = Ty[a][m][n2] = Tz[a][m][n2] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        double G[3][3];  // d u_a / d x_b times h
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          G[a][0] = (N[q][0] * Dx[a][0][0] + N[q][1] * Dx[a][1][0]) * N[r][0] +
+                    (N[q][0] * Dx[a][0][1] + N[q][1] * Dx[a][1][1]) * N[r][1];
+          G[a][1] = (N[p][0] * Dy[a][0][0] + N[p][1] * Dy[a][1][0]) * N[r][0] +
+                    (N[p][0] * Dy[a][0][1] + N[p][1] * Dy[a][1][1]) * N[r][1];
+          G[a][2] = (N[p][0] * Dz[a][0][0] + N[p][1] * Dz[a][1][0]) * N[q][0] +
+                    (N[p][0] * Dz[a][0][1] + N[p][1] * Dz[a][1][1]) * N[q][1];
+        }
+        const double ph = ((N[p][0] * pc[0][0][0] + N[p][1] * pc[1][0][0]) * N[q][0] +
+                           (N[p][0] * pc[0][1][0] + N[p][1] * pc[1][1][0]) * N[q][1]) * N[r][0] +
+                          ((N[p][0] * pc[0][0][1] + N[p][1] * pc[1][0][1]) * N[q][0] +
+                           (N[p][0] * pc[0][1][1] + N[p][1] * pc[1][1][1]) * N[q][1]) * N[r][1];
+        const double gq = (1.0 - kap) * ph * ph + kap;
+        const double tr = G[0][0] + G[1][1] + G[2][2];
+        double S[3][3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) S[a][b] = gq * (mu * (G[a][b] + G[b][a]) + (a == b ? lam * tr : 0.0));
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int n2 = 0; n2 < 2; ++n2) {
+              Tx[a][m][n2] += S[a][0] * (N[q][m] * N[r][n2]);
+              Ty[a][m][n2] += S[a][1] * (N[p][m] * N[r][n2]);
+              Tz[a][m][n2] += S[a][2] * (N[p][m] * N[q][n2]);
+            }
+      }
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double vx = i ? Tx[a][j][l] : -Tx[a][j][l];
+          const double vy = j ? Ty[a][i][l] : -Ty[a][i][l];
+          const double vz = l ? Tz[a][i][j] : -Tz[a][i][j];
+          o[(i + 2 * j + 4 * l) * 3 + a] = scale * (vx + vy + vz);
+        }
+}
+
+__global__ void __launch_bounds__(MF_THREADS) k_mf_sweep(GridDesc g, const Tables* __restrict__ T, double mu,
+                                                         double lam, double kap, double xi0, double xi1,
+                                                         double scale, const double* __restrict__ x,
+                                                         const double* __restrict__ pt,
+                                                         const std::uint8_t* __restrict__ flag,
+                                                         double* __restrict__ y) {
+  constexpr int PL = MFT * MFT;           // vertices of one tile plane
+  __shared__ double su[3][PL * 3], sp[3][PL];  // vertex planes z mod 3
+  __shared__ double co[2][MFC * MFC * MF_CS];  // cell layers L mod 2
+  const int nn = int(g.nn), nc = int(g.nc);
+  const int nbx = (nn + MFB - 1) / MFB;
+  const int col = blockIdx.x % (nbx * nbx), seg = blockIdx.x / (nbx * nbx);
+  const int x0 = (col % nbx) * MFB, y0 = (col / nbx) * MFB;
+  const int zv0 = seg * MF_ZSEG, zv1 = min(nn, zv0 + MF_ZSEG);  // owned vertex planes [zv0, zv1)
+  auto load_plane = [&](int vz) {
+    const int s = ((vz % 3) + 3) % 3;
+    for (int t = threadIdx.x; t < PL; t += blockDim.x) {
+      const int vx = x0 - 1 + t % MFT, vy = y0 - 1 + t / MFT;
+      double u0 = 0.0, u1 = 0.0, u2 = 0.0, p = 0.0;
+      if (vx >= 0 && vy >= 0 && vz >= 0 && vx < nn && vy < nn && vz < nn) {
+        const i64 v = i64(vx) + i64(nn) * (i64(vy) + i64(nn) * vz);
+        u0 = flag[v * 3] ? 0.0 : x[v * 3];
+        u1 = flag[v * 3 + 1] ? 0.0 : x[v * 3 + 1];
+        u2 = flag[v * 3 + 2] ? 0.0 : x[v * 3 + 2];
+        p = pt[v];
+      }
+      su[s][t * 3] = u0;
+      su[s][t * 3 + 1] = u1;
+      su[s][t * 3 + 2] = u2;
+      sp[s][t] = p;
+    }
+  };
+  load_plane(zv0 - 1);
+  load_plane(zv0);
+  double top[3] = {0.0, 0.0, 0.0};  // this thread's vertex: the k = 4..7 corners (layer below)
+  for (int L = zv0 - 1; L < zv1; ++L) {  // cell layer L lies between vertex planes L and L + 1
+    load_plane(L + 1);
+    __syncthreads();
+    {
+      const int c = threadIdx.x;
+      if (c < MFC * MFC) {
+        double* o = co[(L + 2) & 1] + c * MF_CS;
+        const int cx = c % MFC, cy = c / MFC;
+        const int gx = x0 - 1 + cx, gy = y0 - 1 + cy;
+        if (gx < 0 || gy < 0 || L < 0 || gx >= nc || gy >= nc || L >= nc) {
+#pragma unroll
+          for (int e = 0; e < 24; ++e) o[e] = 0.0;
+        } else {
+          const int s0 = ((L % 3) + 3) % 3, s1 = (((L + 1) % 3) + 3) % 3;
+          auto U = [&](int i, int j, int l, int a) { return su[l ? s1 : s0][((cx + i) + MFT * (cy + j)) * 3 + a]; };
+          auto P = [&](int i, int j, int l) { return sp[l ? s1 : s0][(cx + i) + MFT * (cy + j)]; };
+          mf_cell(U, P, xi0, xi1, mu, lam, kap, scale, o);
+        }
+      }
+    }
+    __syncthreads();
+    // vertex plane L (if owned): k = 0..3 from layer L after the carried k = 4..7 of layer L - 1;
+    // then carry this layer's k = 4..7 for plane L + 1
+    const int t = threadIdx.x;
+    if (t < MFB * MFB) {
+      const int lx = t % MFB, ly = t / MFB;
+      const int vx = x0 + lx, vy = y0 + ly;
+      const double* cl = co[(L + 2) & 1];
+      if (L >= zv0 && vx < nn && vy < nn) {
+        double acc[3] = {top[0], top[1], top[2]};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int cx = lx + 1 - (k & 1), cy = ly + 1 - ((k >> 1) & 1);
+          const double* o = cl + (cx + MFC * cy) * MF_CS + k * 3;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) acc[a] += o[a];
+        }
+        const int vz = L;
+        const i64 v = i64(vx) + i64(nn) * (i64(vy) + i64(nn) * vz);
+        const bool con = flag[v * 3] | flag[v * 3 + 1] | flag[v * 3 + 2];
+        if (!con) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) y[v * 3 + a] = acc[a];
+        } else {  // a constrained row keeps the summed element diagonal (model.cpp:295-300): y = d x
+          double dg[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
+          for (int k = 0; k < 8; ++k) {
+            const int gx = vx - (k & 1), gy = vy - ((k >> 1) & 1), gz = vz - ((k >> 2) & 1);
+            if (gx < 0 || gy < 0 || gz < 0 || gx >= nc || gy >= nc || gz >= nc) continue;
+            const int cx = lx + 1 - (k & 1), cy = ly + 1 - ((k >> 1) & 1);
+            double pc[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const int s = (((gz + ((kk >> 2) & 1)) % 3) + 3) % 3;
+              pc[kk] = sp[s][(cx + (kk & 1)) + MFT * (cy + ((kk >> 1) & 1))];
+            }
+#pragma unroll 1
+            for (int q = 0; q < 8; ++q) {
+              double ph = 0.0;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) ph += T->s[q][kk] * pc[kk];
+              const double wg = T->w[q] * ((1.0 - kap) * ph * ph + kap);
+              double gg = 0.0;
+#pragma unroll
+              for (int b = 0; b < 3; ++b) gg += T->gp[q][k][b] * T->gp[q][k][b];
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                const double da = T->gp[q][k][a];
+                dg[a] += wg * (mu * (gg + da * da) + lam * da * da);
+              }
+            }
+          }
+#pragma unroll
+          for (int a = 0; a < 3; ++a) y[v * 3 + a] = flag[v * 3 + a] ? dg[a] * x[v * 3 + a] : acc[a];
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) top[a] = 0.0;
+#pragma unroll
+      for (int k = 4; k < 8; ++k) {
+        const int cx = lx + 1 - (k & 1), cy = ly + 1 - ((k >> 1) & 1);
+        const double* o = cl + (cx + MFC * cy) * MF_CS + k * 3;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) top[a] += o[a];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // FP64 FMA throughput probe ("measure FP64 with a DFMA loop")
 __global__ void k_dfma(double* out, int iters) {
   double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
@@ -223,6 +448,17 @@ void mf_apply_uu(Problem& P, const Constraints& cs, const cf_material& m, const 
   build_tables(P, mat_mu(m), mat_lambda(m));
   const GridDesc& g = P.g;
   const int nv = 1 << g.d;
+  static const bool two_pass_3d = std::getenv("CF_MF_TWO_PASS") != nullptr;  // A/B: the round-1 kernels
+  if (g.d == 3 && !two_pass_3d) {
+    const double mu = mat_mu(m), lam = mat_lambda(m);
+    const int nb = int((g.nn + MFB - 1) / MFB), nseg = int((g.nn + MF_ZSEG - 1) / MF_ZSEG);
+    const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
+    const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
+    k_mf_sweep<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, xi0, xi1,
+                                                            W / (g.h * g.h), x, pt, cs.flag.p, y);
+    CF_LAUNCHED();
+    return;
+  }
   static DevBuf<double> out;  // per-cell corner sums (scratch reused across applies)
   static DevBuf<int> list, cnt;
   const i64 need = g.ncells * nv * g.d;

@@ -658,6 +658,17 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         CF_LAUNCHED();
         NullspaceDev nsg{unodeg.p, Bug.p, d == 2 ? 3 : 6, pnodeg.p, Bpg.p};
         prec = build_block_prec(Jg, opts.prec_kind, opts.amg, &nsg, prec.get());
+        // the large leading levels apply by rows split over the ranks (a reused hierarchy keeps
+        // its split); the V-cycles then run in sequence on the library stream (collectives)
+        static const bool no_split = std::getenv("CF_VCYCLE_REPLICATED") != nullptr;
+        if (!no_split) {
+          // CF_VCYCLE_SPLIT_MIN (test switch): the smallest level split over the ranks
+          static const char* smin = std::getenv("CF_VCYCLE_SPLIT_MIN");
+          const i64 min_rows = smin ? std::atoll(smin) : std::max<i64>(65536, 1024 * i64(cm.size));
+          for (Amg* h : {prec->amg_u.get(), prec->amg_p.get()})
+            if (h && h->comm != &cm) h->distribute(&cm, min_rows);
+          prec->serial = true;
+        }
       } else if (dist) {
         // block-Jacobi over the slabs: the preconditioner of each rank is built on the diagonal
         // block of its rows (owned columns only); one GPU is the undivided block

@@ -1788,6 +1788,40 @@ std::unique_ptr<Csr> csr_extract_cols(const Csr& A, i64 lo, i64 hi) {
   return C;
 }
 
+namespace {
+__global__ void k_ptr_sub(const i64* __restrict__ p, i64 n, i64* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = p[i] - p[0];
+}
+}  // namespace
+
+std::unique_ptr<Csr> csr_extract_rows(const Csr& A, i64 lo, i64 hi) {
+  auto C = std::make_unique<Csr>();
+  lo = std::max<i64>(0, std::min(lo, A.rows));
+  hi = std::max(lo, std::min(hi, A.rows));
+  C->rows = hi - lo;
+  C->cols = A.cols;
+  C->ptr.alloc(C->rows + 1);
+  k_ptr_sub<<<grid_for(C->rows + 1, 256), 256, 0, stream()>>>(A.ptr.p + lo, C->rows + 1, C->ptr.p);
+  CF_LAUNCHED();
+  i64 b[2] = {0, 0};
+  CF_CUDA(cudaMemcpyAsync(&b[0], A.ptr.p + lo, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaMemcpyAsync(&b[1], A.ptr.p + hi, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  C->nnz = b[1] - b[0];
+  C->col.alloc(std::max<i64>(C->nnz, 1));
+  C->val.alloc(std::max<i64>(C->nnz, 1));
+  if (C->nnz) {
+    CF_CUDA(cudaMemcpyAsync(C->col.p, A.col.p + b[0], size_t(C->nnz) * sizeof(int), cudaMemcpyDeviceToDevice,
+                            stream()));
+    CF_CUDA(cudaMemcpyAsync(C->val.p, A.val.p + b[0], size_t(C->nnz) * sizeof(double), cudaMemcpyDeviceToDevice,
+                            stream()));
+  }
+  // the lane split of the undivided matrix, so every row reduces exactly as there
+  C->mean_hint = A.mean_hint >= 0.0 ? A.mean_hint : (A.rows ? double(A.nnz) / double(A.rows) : 0.0);
+  return C;
+}
+
 std::unique_ptr<Csr> csr_copy(const Csr& A) {
   auto C = std::make_unique<Csr>();
   C->rows = A.rows;

@@ -36,7 +36,7 @@ __device__ __forceinline__ double group_sum(double s) {
 
 __device__ __forceinline__ double epi_out(const SpmvEpi& ep, const double* __restrict__ x, i64 row, double s) {
   if (ep.mode == 1) return ep.b[row] - s;
-  if (ep.mode == 2) return x[row] + ep.w * (ep.d[row] * (ep.b[row] - s));
+  if (ep.mode == 2) return x[row + ep.xoff] + ep.w * (ep.d[row] * (ep.b[row] - s));
   if (ep.mode == 3) return ep.w * (ep.d[row] * s);  // scaled product (vdiag_mul's expression)
   return ep.b ? ep.b[row] + s : s;
 }

@@ -271,7 +271,8 @@ def test_extrapolate_phi(cf):
         assert np.array_equal(got, ref)
 
 
-@pytest.mark.parametrize("d,n0,r,clamp", [(2, 4, 2, True), (2, 3, 2, False), (3, 3, 1, True), (3, 2, 2, True)])
+@pytest.mark.parametrize("d,n0,r,clamp", [(2, 4, 2, True), (2, 3, 2, False), (3, 3, 1, True), (3, 2, 2, True),
+                                          (3, 5, 2, True), (3, 3, 2, False), (3, 9, 1, True)])
 def test_matrix_free_apply_equals_assembled(cf, d, n0, r, clamp):
     """BASELINE config 1's matrix-free operator: y = M_uu x from phi_tilde cell by cell, equal to the
     assembled block's apply (Dirichlet condensation included) to 1e-12 relative."""

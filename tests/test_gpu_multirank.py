@@ -55,19 +55,23 @@ def _free_port():
 
 
 @pytest.mark.parametrize("d,n0,r,size,mode", [(3, 4, 2, 2, "global"), (3, 4, 2, 3, "global"), (2, 8, 3, 4, "global"),
-                                               (3, 8, 1, 4, "global"), (3, 4, 2, 3, "ras"),
-                                               (2, 8, 3, 4, "block_jacobi")])
+                                               (3, 8, 1, 4, "global"), (3, 4, 2, 3, "global-replicated"),
+                                               (3, 4, 2, 3, "ras"), (2, 8, 3, 4, "block_jacobi")])
 def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
+    """global: the hierarchy's levels of >= 256 rows apply by rows split over the ranks
+    (CF_VCYCLE_SPLIT_MIN lowers the production threshold so these small grids exercise it);
+    global-replicated: every rank applies the whole V-cycle."""
     import torch.multiprocessing as mp
     import paper_1806_09924_b200 as cf
-    env = {"ras": "CF_RAS", "block_jacobi": "CF_BLOCK_JACOBI"}.get(mode)
-    if env:
-        os.environ[env] = "1"
+    env = {"ras": {"CF_RAS": "1"}, "block_jacobi": {"CF_BLOCK_JACOBI": "1"},
+           "global": {"CF_VCYCLE_SPLIT_MIN": "256"},
+           "global-replicated": {"CF_VCYCLE_REPLICATED": "1"}}[mode]
+    os.environ.update(env)
     try:
         mp.spawn(_worker, args=(size, _free_port(), str(tmp_path), d, n0, r), nprocs=size, join=True)
     finally:
-        if env:
-            del os.environ[env]
+        for k in env:
+            del os.environ[k]
     xs = [np.load(tmp_path / f"x{k}.npy") for k in range(size)]
     its = [np.load(tmp_path / f"its{k}.npy") for k in range(size)]
     conv = [np.load(tmp_path / f"conv{k}.npy") for k in range(size)]
@@ -82,7 +86,7 @@ def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
     ref = st.get()["solution"]
     ref_its = np.array([[it["residual_norm"], it["active_size"], it["set_changes"], it["gmres_iterations"]]
                         for it in rep["iterations"]])
-    if mode == "global":
+    if mode.startswith("global"):
         assert np.array_equal(its[0], ref_its), (its[0], ref_its)
         assert np.array_equal(xs[0], ref), f"max |dx| = {np.abs(xs[0] - ref).max()}"
     else:
