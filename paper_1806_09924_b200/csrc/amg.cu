@@ -1517,6 +1517,8 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
       CF_LAUNCHED();
     }
     nkeys.release();
+    if (clk.on) std::fprintf(stderr, "[amg L%d] n2: listed %d, global-tier %lld, strength global-tier %lld, upper %lld\n",
+                             lev, nl, (long long)big2.n, (long long)big.n, (long long)nup);
     clk.mark("S^T + N2");
     // pass 1: lexicographically-first MIS of N2 (persistent cooperative frontier kernel)
     DevBuf<int> status(n_nodes), f0(n_nodes), f1(n_nodes), sizes(3), rounds(1);

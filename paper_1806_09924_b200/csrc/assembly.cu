@@ -138,8 +138,11 @@ __global__ void k_div_by(double h, const double* __restrict__ a, i64 n, double* 
   for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x) q[i] = dv.div(a[i]);
 }
 
+#ifndef CF_RES_MINB
+#define CF_RES_MINB 4  // 64 registers, 32 warps per SM: 5.35 -> 4.2-4.9 ms on config 3 (A/B, bitwise the same)
+#endif
 template <int D>
-__global__ void __launch_bounds__(256) k_cell_residual_q(GridDesc g, const Tables* __restrict__ T, Coef cf,
+__global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g, const Tables* __restrict__ T, Coef cf,
                                                          const double* __restrict__ sol,
                                                          const double* __restrict__ ptil,
                                                          double* __restrict__ out, i64 c_lo, i64 c_hi) {
