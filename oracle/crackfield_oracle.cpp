@@ -698,22 +698,14 @@ static void check_material(const orc_material& m) {  // model.cpp:8-17
   if (!(m.G_c > 0.0)) throw std::invalid_argument("Material: G_c must be positive");
 }
 
-// Element residual of one cell (the body of the cell loop, model.cpp:136-196): ru[k*d+a], rphi[k]
-static void cell_residual(const Grid& g, const QpData& qp, const orc_material& mat, const orc_regularization& reg,
-                          const double* solution, const double* phi_tilde, i64 id, double* ru, double* rphi) {
-  const int d = g.d, nv = 1 << d;
+// Element residual from the corner values of one cell of edge h (the body of the cell loop,
+// model.cpp:136-196): ru[k*d+a], rphi[k].  Shared by the uniform grid and the general meshes.
+static void elem_residual(int d, const QpData& qp, const orc_material& mat, const orc_regularization& reg, double h,
+                          double detJ, const double (*uloc)[3], const double* philoc, const double* ptloc, double* ru,
+                          double* rphi) {
+  const int nv = 1 << d;
   const double kap = reg.kappa, eps = reg.eps, p = mat.pressure, Gc = mat.G_c;
   const double mu = mat_mu(mat), lam = mat_lambda(mat);
-  const i64 nu = g.n_u();
-  double uloc[8][3], philoc[8], ptloc[8];
-  i64 verts[8];
-  const double h = g.h, detJ = g.detJ;
-  g.cell_vertices(id, verts);
-  for (int k = 0; k < nv; ++k) {
-    for (int a = 0; a < d; ++a) uloc[k][a] = solution[verts[k] * d + a];
-    philoc[k] = solution[nu + verts[k]];
-    ptloc[k] = phi_tilde[verts[k]];
-  }
   for (int i = 0; i < nv * d; ++i) ru[i] = 0.0;
   for (int i = 0; i < nv; ++i) rphi[i] = 0.0;
   for (int q = 0; q < qp.nq; ++q) {
@@ -755,6 +747,22 @@ static void cell_residual(const Grid& g, const QpData& qp, const orc_material& m
       rphi[k] += w * vphi;
     }
   }
+}
+
+// Element residual of one cell of the uniform grid
+static void cell_residual(const Grid& g, const QpData& qp, const orc_material& mat, const orc_regularization& reg,
+                          const double* solution, const double* phi_tilde, i64 id, double* ru, double* rphi) {
+  const int d = g.d, nv = 1 << d;
+  const i64 nu = g.n_u();
+  double uloc[8][3], philoc[8], ptloc[8];
+  i64 verts[8];
+  g.cell_vertices(id, verts);
+  for (int k = 0; k < nv; ++k) {
+    for (int a = 0; a < d; ++a) uloc[k][a] = solution[verts[k] * d + a];
+    philoc[k] = solution[nu + verts[k]];
+    ptloc[k] = phi_tilde[verts[k]];
+  }
+  elem_residual(d, qp, mat, reg, g.h, g.detJ, uloc, philoc, ptloc, ru, rphi);
 }
 
 static const QpData& qp_data(int d) {
@@ -938,12 +946,69 @@ static void drop_zero_constrained_diag(Csr& A, const Constraints& cs, i64 off) {
   A = std::move(B);
 }
 
+// Element matrices of one cell of edge h (model.cpp:226-289): kuu, kpu, kpp (zeroed here).
+static void elem_jacobian(int d, const QpData& qp, const orc_material& mat, const orc_regularization& reg, double h,
+                          double detJ, const double (*uloc)[3], const double* philoc, const double* ptloc,
+                          double (*kuu)[24], double (*kpu)[24], double (*kpp)[8]) {
+  const int nv = 1 << d;
+  const double kap = reg.kappa, eps = reg.eps, p = mat.pressure, Gc = mat.G_c;
+  const double mu = mat_mu(mat), lam = mat_lambda(mat);
+  double gphys[8][3];
+  for (int i = 0; i < 24; ++i)
+    for (int j = 0; j < 24; ++j) kuu[i][j] = 0.0;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 24; ++j) kpu[i][j] = 0.0;
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) kpp[i][j] = 0.0;
+  for (int q = 0; q < qp.nq; ++q) {
+    const double* s = qp.shape[q];
+    for (int k = 0; k < nv; ++k)
+      for (int b = 0; b < 3; ++b) gphys[k][b] = (b < d) ? qp.grads[q][k][b] / h : 0.0;
+    double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    double phi = 0.0, pt = 0.0;
+    for (int k = 0; k < nv; ++k) {
+      phi += s[k] * philoc[k];
+      pt += s[k] * ptloc[k];
+      for (int b = 0; b < d; ++b)
+        for (int a = 0; a < d; ++a) gu[a][b] += uloc[k][a] * gphys[k][b];
+    }
+    double e[3][3], sig[3][3];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
+    double tre = 0.0;
+    for (int a = 0; a < d; ++a) tre += e[a][a];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) sig[a][b] = 2.0 * mu * e[a][b];
+    for (int a = 0; a < d; ++a) sig[a][a] += lam * tre;
+    double sig_ee = 0.0;
+    for (int a = 0; a < d; ++a)
+      for (int b = 0; b < d; ++b) sig_ee += sig[a][b] * e[a][b];
+    const double gcoef = (1.0 - kap) * pt * pt + kap;
+    const double w = qp.wts[q] * detJ;
+    for (int k = 0; k < nv; ++k) {
+      for (int l = 0; l < nv; ++l) {
+        double gg = 0.0;
+        for (int b = 0; b < d; ++b) gg += gphys[k][b] * gphys[l][b];
+        for (int a = 0; a < d; ++a)
+          for (int b = 0; b < d; ++b) {
+            double val = mu * ((a == b ? gg : 0.0) + gphys[l][a] * gphys[k][b]) + lam * gphys[l][b] * gphys[k][a];
+            kuu[k * d + a][l * d + b] += w * gcoef * val;
+          }
+        for (int b = 0; b < d; ++b) {
+          double sgl = 0.0;
+          for (int c = 0; c < d; ++c) sgl += sig[b][c] * gphys[l][c];
+          kpu[k][l * d + b] += w * (2.0 * (1.0 - kap) * phi * sgl + 2.0 * p * phi * gphys[l][b]) * s[k];
+        }
+        kpp[k][l] += w * (((1.0 - kap) * sig_ee + 2.0 * p * tre + Gc / eps) * s[l] * s[k] + Gc * eps * gg);
+      }
+    }
+  }
+}
+
 static BlockSystem assemble_jacobian_seq(const Grid& g, const Constraints& cs, const orc_material& mat,
                                          const orc_regularization& reg, const double* solution,
                                          const double* phi_tilde) {
   const int d = g.d, nv = 1 << d;
-  const double kap = reg.kappa, eps = reg.eps, p = mat.pressure, Gc = mat.G_c;
-  const double mu = mat_mu(mat), lam = mat_lambda(mat);
   static thread_local QpData qp2, qp3;
   QpData& qp = (d == 2) ? qp2 : qp3;
   if (qp.nq == 0) qp = make_qp_data(d);
@@ -951,9 +1016,8 @@ static BlockSystem assemble_jacobian_seq(const Grid& g, const Constraints& cs, c
   BlockSystem J;
   build_pattern(g, cs, J);
   double uloc[8][3], philoc[8], ptloc[8];
-  double kuu[24][24], kpu[8][24], kpp[8][8], gphys[8][3];
+  double kuu[24][24], kpu[8][24], kpp[8][8];
   i64 verts[8], udofs[24], pdofs[8];
-  const double h = g.h, detJ = g.detJ;
   for (i64 id : g.cell_order) {
     g.cell_vertices(id, verts);
     for (int k = 0; k < nv; ++k) {
@@ -961,52 +1025,7 @@ static BlockSystem assemble_jacobian_seq(const Grid& g, const Constraints& cs, c
       philoc[k] = solution[nu + verts[k]];
       ptloc[k] = phi_tilde[verts[k]];
     }
-    std::memset(kuu, 0, sizeof(kuu));
-    std::memset(kpu, 0, sizeof(kpu));
-    std::memset(kpp, 0, sizeof(kpp));
-    for (int q = 0; q < qp.nq; ++q) {
-      const double* s = qp.shape[q];
-      for (int k = 0; k < nv; ++k)
-        for (int b = 0; b < 3; ++b) gphys[k][b] = (b < d) ? qp.grads[q][k][b] / h : 0.0;
-      double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-      double phi = 0.0, pt = 0.0;
-      for (int k = 0; k < nv; ++k) {
-        phi += s[k] * philoc[k];
-        pt += s[k] * ptloc[k];
-        for (int b = 0; b < d; ++b)
-          for (int a = 0; a < d; ++a) gu[a][b] += uloc[k][a] * gphys[k][b];
-      }
-      double e[3][3], sig[3][3];
-      for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
-      double tre = 0.0;
-      for (int a = 0; a < d; ++a) tre += e[a][a];
-      for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) sig[a][b] = 2.0 * mu * e[a][b];
-      for (int a = 0; a < d; ++a) sig[a][a] += lam * tre;
-      double sig_ee = 0.0;
-      for (int a = 0; a < d; ++a)
-        for (int b = 0; b < d; ++b) sig_ee += sig[a][b] * e[a][b];
-      const double gcoef = (1.0 - kap) * pt * pt + kap;
-      const double w = qp.wts[q] * detJ;
-      for (int k = 0; k < nv; ++k) {
-        for (int l = 0; l < nv; ++l) {
-          double gg = 0.0;
-          for (int b = 0; b < d; ++b) gg += gphys[k][b] * gphys[l][b];
-          for (int a = 0; a < d; ++a)
-            for (int b = 0; b < d; ++b) {
-              double val = mu * ((a == b ? gg : 0.0) + gphys[l][a] * gphys[k][b]) + lam * gphys[l][b] * gphys[k][a];
-              kuu[k * d + a][l * d + b] += w * gcoef * val;
-            }
-          for (int b = 0; b < d; ++b) {
-            double sgl = 0.0;
-            for (int c = 0; c < d; ++c) sgl += sig[b][c] * gphys[l][c];
-            kpu[k][l * d + b] += w * (2.0 * (1.0 - kap) * phi * sgl + 2.0 * p * phi * gphys[l][b]) * s[k];
-          }
-          kpp[k][l] += w * (((1.0 - kap) * sig_ee + 2.0 * p * tre + Gc / eps) * s[l] * s[k] + Gc * eps * gg);
-        }
-      }
-    }
+    elem_jacobian(d, qp, mat, reg, g.h, g.detJ, uloc, philoc, ptloc, kuu, kpu, kpp);
     for (int k = 0; k < nv; ++k) {
       for (int a = 0; a < d; ++a) udofs[k * d + a] = verts[k] * d + a;
       pdofs[k] = nu + verts[k];
@@ -2374,6 +2393,8 @@ static void compute_cod(const Grid& g, const double* sol, const double* stations
   }
 }
 
+#include "oracle_mesh.inc"
+
 }  // namespace orc
 
 // =====================================================================================
@@ -2812,6 +2833,262 @@ int orc_sigma(const double* grad, const orc_material* m, int d, double* out) {
     for (int b = 0; b < 3; ++b) out[3 * a + b] = 2.0 * mu * e[a][b];
   for (int a = 0; a < d; ++a) out[3 * a + a] += lam * tr;
   return 0;
+}
+
+
+// ---- general (adaptive) meshes (oracle_mesh.inc)
+struct orc_mesh {
+  gm::Mesh m;
+  gm::DofMap map;
+  void remap() { map = gm::build_dof_map(m); }
+};
+struct orc_mcs {
+  gm::CSet cs;
+};
+int orc_mesh_create(int d, double K, int n0, orc_mesh** out) {
+  ORC_TRY
+  auto* o = new orc_mesh{gm::Mesh(d, K, n0), {}};
+  o->remap();
+  *out = o;
+  ORC_CATCH
+}
+int orc_mesh_copy(orc_mesh* src, orc_mesh** out) {
+  ORC_TRY
+  *out = new orc_mesh(*src);
+  ORC_CATCH
+}
+void orc_mesh_destroy(orc_mesh* m) { delete m; }
+int orc_mesh_refine(orc_mesh* m, const int32_t* ids, int64_t n) {
+  ORC_TRY
+  m->m.refine(std::vector<int>(ids, ids + n));
+  m->remap();
+  ORC_CATCH
+}
+int orc_mesh_uniform_refine(orc_mesh* m, int times) {
+  ORC_TRY
+  m->m.uniform_refine(times);
+  m->remap();
+  ORC_CATCH
+}
+// n_cells, n_active, max_level, V
+int orc_mesh_info(orc_mesh* m, int64_t* info4, double* h_min) {
+  info4[0] = int64_t(m->m.cells.size());
+  info4[1] = int64_t(m->m.active.size());
+  info4[2] = m->m.max_active_level();
+  info4[3] = m->map.V;
+  *h_min = m->m.min_active_edge();
+  return 0;
+}
+// per cell: level, parent, active, anchor x/y/z (cells in id order)
+int orc_mesh_cells(orc_mesh* m, int32_t* level, int32_t* parent, int8_t* active, int64_t* anchor) {
+  for (size_t i = 0; i < m->m.cells.size(); ++i) {
+    const gm::Cell& c = m->m.cells[i];
+    level[i] = c.level;
+    parent[i] = c.parent;
+    active[i] = c.active;
+    for (int a = 0; a < 3; ++a) anchor[3 * i + a] = c.anchor[a];
+  }
+  return 0;
+}
+int orc_mesh_active(orc_mesh* m, int32_t* ids) {
+  std::copy(m->m.active.begin(), m->m.active.end(), ids);
+  return 0;
+}
+int orc_mesh_vertex_keys(orc_mesh* m, int64_t* keys) {
+  std::copy(m->map.keys.begin(), m->map.keys.end(), keys);
+  return 0;
+}
+int orc_mesh_cell_vertices(orc_mesh* m, int64_t* out) {
+  ORC_TRY
+  const int nv = 1 << m->m.d;
+  for (size_t i = 0; i < m->m.active.size(); ++i) m->map.cell_vertices(m->m, m->m.active[i], out + i * nv);
+  ORC_CATCH
+}
+int orc_mesh_faces(orc_mesh* m, int64_t* n, int32_t* out5) {  // out5 may be null (count only)
+  std::vector<gm::FaceEntry> f = gm::active_faces(m->m);
+  *n = int64_t(f.size());
+  if (out5)
+    for (size_t i = 0; i < f.size(); ++i) {
+      out5[5 * i] = f[i].cell;
+      out5[5 * i + 1] = f[i].axis;
+      out5[5 * i + 2] = f[i].side;
+      out5[5 * i + 3] = f[i].neighbor;
+      out5[5 * i + 4] = f[i].rel;
+    }
+  return 0;
+}
+int orc_mesh_find_cell(orc_mesh* m, const double* x, int32_t* out) {
+  *out = m->m.find_active_cell_x(x);
+  return 0;
+}
+int orc_mesh_constraints(orc_mesh* m, int clamp, int64_t n_active, const int64_t* dofs, const double* vals,
+                         orc_mcs** out) {
+  ORC_TRY
+  *out = new orc_mcs{gm::build_constraints(m->m, m->map, clamp != 0, std::vector<i64>(dofs, dofs + n_active),
+                                           std::vector<double>(vals, vals + n_active))};
+  ORC_CATCH
+}
+void orc_mcs_destroy(orc_mcs* c) { delete c; }
+// lines in ascending dof order: n_lines, total entries
+int orc_mcs_info(orc_mcs* c, int64_t* n_lines, int64_t* n_entries) {
+  *n_lines = int64_t(c->cs.lines.size());
+  int64_t e = 0;
+  for (const auto& kv : c->cs.lines) e += int64_t(kv.second.e.size());
+  *n_entries = e;
+  return 0;
+}
+int orc_mcs_export(orc_mcs* c, int64_t* dofs, int64_t* ptr, int64_t* masters, double* weights, double* inhom) {
+  int64_t i = 0, k = 0;
+  ptr[0] = 0;
+  for (const auto& [dof, l] : c->cs.lines) {
+    dofs[i] = dof;
+    inhom[i] = l.inhom;
+    for (const auto& [mm, w] : l.e) {
+      masters[k] = mm;
+      weights[k] = w;
+      ++k;
+    }
+    ptr[++i] = k;
+  }
+  return 0;
+}
+int orc_mcs_distribute(orc_mcs* c, double* v, int64_t n, int homogeneous) {
+  Vec x(v, v + n);
+  if (homogeneous) c->cs.distribute_homogeneous(x); else c->cs.distribute(x);
+  std::copy(x.begin(), x.end(), v);
+  return 0;
+}
+int orc_mesh_residual(orc_mesh* m, orc_mcs* c, const orc_material* mat, const orc_regularization* r, const double* x,
+                      const double* pt, double* R) {
+  ORC_TRY
+  check_material(*mat);
+  Vec out = gm::assemble_residual(m->m, m->map, c->cs, *mat, *r, x, pt);
+  std::copy(out.begin(), out.end(), R);
+  ORC_CATCH
+}
+int orc_mesh_jacobian(orc_mesh* m, orc_mcs* c, const orc_material* mat, const orc_regularization* r, const double* x,
+                      const double* pt, orc_block** out) {
+  ORC_TRY
+  check_material(*mat);
+  *out = new orc_block{gm::assemble_jacobian(m->m, m->map, c->cs, *mat, *r, x, pt)};
+  ORC_CATCH
+}
+int orc_mesh_rigid_body_modes(orc_mesh* m, orc_mcs* c, double* B_colmajor) {
+  Dense B = gm::rigid_body_modes(m->m, m->map, c->cs);
+  std::copy(B.a.begin(), B.a.end(), B_colmajor);
+  return 0;
+}
+int orc_mesh_slit_band_edge(orc_mesh* m, const orc_material* mat, double* out) {
+  ORC_TRY
+  *out = gm::slit_band_edge(m->m, *mat);
+  ORC_CATCH
+}
+int orc_mesh_resolve_regularization(orc_mesh* m, const orc_material* mat, double band_edge, orc_regularization* out) {
+  ORC_TRY
+  *out = gm::resolve_regularization(m->m, *mat, band_edge);
+  ORC_CATCH
+}
+int orc_mesh_initial_crack(orc_mesh* m, const orc_material* mat, double band_half, double* phi, double* band_edge) {
+  ORC_TRY
+  Vec v = gm::initial_crack(m->m, m->map, *mat, band_half, band_edge);
+  std::copy(v.begin(), v.end(), phi);
+  ORC_CATCH
+}
+int orc_mesh_newton_step(orc_mesh* m, const orc_material* mat, const orc_regularization* r,
+                         const orc_solver_options* o, double* solution, double* phi_old, double* phi_prev2, int step,
+                         int shift, int max_its, double* its_out, int* n_its, int* converged, double* feasibility) {
+  ORC_TRY
+  const gm::DofMap& map = m->map;
+  State st;
+  st.solution.assign(solution, solution + map.n_total());
+  st.phi_old.assign(phi_old, phi_old + map.V);
+  st.phi_prev2.assign(phi_prev2, phi_prev2 + map.V);
+  st.step = step;
+  if (shift) {
+    st.phi_prev2 = st.phi_old;
+    st.phi_old.assign(st.solution.begin() + map.n_u(), st.solution.end());
+  }
+  NewtonReport rep = gm::newton_step(st, *mat, m->m, map, *r, *o);
+  std::copy(st.solution.begin(), st.solution.end(), solution);
+  std::copy(st.phi_old.begin(), st.phi_old.end(), phi_old);
+  std::copy(st.phi_prev2.begin(), st.phi_prev2.end(), phi_prev2);
+  *n_its = int(rep.its.size());
+  for (int i = 0; i < int(rep.its.size()) && i < max_its; ++i) {
+    its_out[4 * i] = rep.its[i].residual_norm;
+    its_out[4 * i + 1] = rep.its[i].active_size;
+    its_out[4 * i + 2] = rep.its[i].set_changes;
+    its_out[4 * i + 3] = rep.its[i].gmres_iterations;
+  }
+  *converged = rep.converged;
+  *feasibility = rep.feasibility;
+  ORC_CATCH
+}
+int orc_mesh_tcv(orc_mesh* m, const double* sol, double* out) {
+  ORC_TRY
+  *out = gm::compute_tcv(m->m, m->map, sol);
+  ORC_CATCH
+}
+int orc_mesh_cod(orc_mesh* m, const double* sol, const double* stations, int ns, double* out) {
+  ORC_TRY
+  gm::compute_cod(m->m, m->map, sol, stations, ns, out);
+  ORC_CATCH
+}
+int orc_mesh_estimator(orc_mesh* m, const double* sol, double* eta) {
+  ORC_TRY
+  Vec e = gm::jump_estimator(m->m, m->map, sol);
+  std::copy(e.begin(), e.end(), eta);
+  ORC_CATCH
+}
+// policy5: phi_threshold, h_target, theta, max_level, estimator; eta may be null
+int orc_mesh_mark(orc_mesh* m, const double* sol, const double* eta, const double* policy5, int32_t* out,
+                  int64_t* n_out) {
+  ORC_TRY
+  gm::Policy pol{policy5[0], policy5[1], policy5[2], int(policy5[3]), policy5[4] != 0.0};
+  Vec e;
+  if (eta) e.assign(eta, eta + m->m.active.size());
+  std::vector<int> ids = gm::mark_cells(m->m, m->map, sol, e, pol);
+  std::copy(ids.begin(), ids.end(), out);
+  *n_out = int64_t(ids.size());
+  ORC_CATCH
+}
+int orc_mesh_transfer(orc_mesh* om, const double* ov, orc_mesh* nm, double* nv) {
+  ORC_TRY
+  Vec o(ov, ov + om->map.n_total());
+  Vec out = gm::transfer(om->m, om->map, o, nm->m, nm->map);
+  std::copy(out.begin(), out.end(), nv);
+  ORC_CATCH
+}
+// adaptive_cycle: the mesh is refined in place; the final state is returned through the
+// caller's buffers (sized by the caller after reading orc_mesh_info), records as 8 doubles each
+int orc_mesh_adaptive_cycle(orc_mesh* m, const orc_material* mat, const orc_solver_options* so,
+                            const double* policy5, int cycles, int n_steps, int estimator_rounds,
+                            int halve_band_target, double seed_band, int max_rec, double* rec_out, int* n_rec,
+                            double* solution, int64_t sol_cap) {
+  ORC_TRY
+  gm::AdaptOpts o;
+  o.policy = gm::Policy{policy5[0], policy5[1], policy5[2], int(policy5[3]), policy5[4] != 0.0};
+  o.solver = *so;
+  o.cycles = cycles;
+  o.n_steps = n_steps;
+  o.estimator_rounds = estimator_rounds;
+  o.halve_band_target = halve_band_target != 0;
+  o.seed_band = seed_band;
+  State st = gm::initial_state(m->m, m->map, *mat, seed_band);
+  std::vector<gm::LevelRec> recs = gm::adaptive_cycle(m->m, m->map, st, *mat, o);
+  *n_rec = int(recs.size());
+  for (int i = 0; i < int(recs.size()) && i < max_rec; ++i) {
+    double* r = rec_out + 8 * i;
+    r[0] = recs[i].level;
+    r[1] = double(recs[i].dofs);
+    r[2] = recs[i].eps;
+    r[3] = recs[i].h_min;
+    r[4] = recs[i].tcv;
+    r[5] = recs[i].newton_iters;
+    r[6] = recs[i].gmres_mean;
+    r[7] = recs[i].converged;
+  }
+  if (solution && sol_cap >= int64_t(st.solution.size())) std::copy(st.solution.begin(), st.solution.end(), solution);
+  ORC_CATCH
 }
 
 }  // extern "C"

@@ -17,8 +17,8 @@ LIB_PATH = os.path.join(HERE, "liborc.so")
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(HERE, "crackfield_oracle.cpp")
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < os.path.getmtime(src):
+    srcs = [os.path.join(HERE, f) for f in ("crackfield_oracle.cpp", "oracle_mesh.inc")]
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(map(os.path.getmtime, srcs)):
         subprocess.check_call(["make", "-s", "-C", HERE, "liborc.so"])
     return LIB_PATH
 
@@ -491,3 +491,210 @@ def sigma(grad, mat, d):
     out = np.zeros((3, 3))
     lib().orc_sigma(_p(g), C.byref(mat), d, _p(out))
     return out
+
+
+# ------------------------------------------------------------------ general (adaptive) meshes
+class Mesh:
+    """Adaptive forest mesh + its DofMap (mesh.cpp, fem.cpp:98-146): create_mesh(d, K, n0),
+    refine / uniform_refine; cell ids in creation order, vertices = sorted packed keys."""
+
+    def __init__(self, d: int, K: float, n0: int, _h=None):
+        self.h_ = C.c_void_p()
+        if _h is None:
+            _chk(lib().orc_mesh_create(d, C.c_double(K), n0, C.byref(self.h_)))
+        else:
+            self.h_ = _h
+        self.d, self.K, self.n0 = d, K, n0
+        self._info()
+
+    def _info(self):
+        info = np.zeros(4, dtype=np.int64)
+        hmin = C.c_double()
+        lib().orc_mesh_info(self.h_, _p(info, C.c_int64), C.byref(hmin))
+        self.n_cells, self.n_active, self.max_level, self.V = (int(v) for v in info)
+        self.h_min = hmin.value
+        self.n_u, self.n_phi, self.n_total = self.d * self.V, self.V, (self.d + 1) * self.V
+
+    def __del__(self):
+        try:
+            lib().orc_mesh_destroy(self.h_)
+        except Exception:
+            pass
+
+    def copy(self):
+        h = C.c_void_p()
+        _chk(lib().orc_mesh_copy(self.h_, C.byref(h)))
+        return Mesh(self.d, self.K, self.n0, _h=h)
+
+    def refine(self, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        _chk(lib().orc_mesh_refine(self.h_, _p(ids, C.c_int32), C.c_int64(len(ids))))
+        self._info()
+
+    def uniform_refine(self, times):
+        _chk(lib().orc_mesh_uniform_refine(self.h_, int(times)))
+        self._info()
+
+    def cells(self):
+        n = self.n_cells
+        lev = np.zeros(n, dtype=np.int32)
+        par = np.zeros(n, dtype=np.int32)
+        act = np.zeros(n, dtype=np.int8)
+        anc = np.zeros((n, 3), dtype=np.int64)
+        lib().orc_mesh_cells(self.h_, _p(lev, C.c_int32), _p(par, C.c_int32), _p(act, C.c_int8), _p(anc, C.c_int64))
+        return dict(level=lev, parent=par, active=act.astype(bool), anchor=anc)
+
+    def active(self):
+        out = np.zeros(self.n_active, dtype=np.int32)
+        lib().orc_mesh_active(self.h_, _p(out, C.c_int32))
+        return out
+
+    def vertex_keys(self):
+        out = np.zeros(self.V, dtype=np.int64)
+        lib().orc_mesh_vertex_keys(self.h_, _p(out, C.c_int64))
+        return out
+
+    def cell_vertices(self):
+        out = np.zeros((self.n_active, 1 << self.d), dtype=np.int64)
+        _chk(lib().orc_mesh_cell_vertices(self.h_, _p(out, C.c_int64)))
+        return out
+
+    def faces(self):
+        n = C.c_int64()
+        lib().orc_mesh_faces(self.h_, C.byref(n), None)
+        out = np.zeros((n.value, 5), dtype=np.int32)
+        lib().orc_mesh_faces(self.h_, C.byref(n), _p(out, C.c_int32))
+        return out
+
+    def find_cell(self, x):
+        x = np.ascontiguousarray(list(x) + [0.0] * (3 - len(x)), dtype=np.float64)
+        out = C.c_int32()
+        lib().orc_mesh_find_cell(self.h_, _p(x), C.byref(out))
+        return out.value
+
+    def constraints(self, clamp=True, active_dofs=(), active_vals=()):
+        return MeshConstraints(self, clamp, active_dofs, active_vals)
+
+    def residual(self, cs, mat, reg, x, pt):
+        R = np.zeros(self.n_total)
+        _chk(lib().orc_mesh_residual(self.h_, cs.h_, C.byref(mat), C.byref(reg),
+                                     _p(np.ascontiguousarray(x, dtype=np.float64)),
+                                     _p(np.ascontiguousarray(pt, dtype=np.float64)), _p(R)))
+        return R
+
+    def jacobian(self, cs, mat, reg, x, pt):
+        h = C.c_void_p()
+        _chk(lib().orc_mesh_jacobian(self.h_, cs.h_, C.byref(mat), C.byref(reg),
+                                     _p(np.ascontiguousarray(x, dtype=np.float64)),
+                                     _p(np.ascontiguousarray(pt, dtype=np.float64)), C.byref(h)))
+        return Block(h)
+
+    def rigid_body_modes(self, cs):
+        m = 3 if self.d == 2 else 6
+        B = np.zeros((m, self.n_u))
+        lib().orc_mesh_rigid_body_modes(self.h_, cs.h_, _p(B))
+        return B.T.copy()
+
+    def slit_band_edge(self, mat):
+        out = C.c_double()
+        _chk(lib().orc_mesh_slit_band_edge(self.h_, C.byref(mat), C.byref(out)))
+        return out.value
+
+    def resolve_regularization(self, mat, band_edge):
+        reg = Regularization()
+        _chk(lib().orc_mesh_resolve_regularization(self.h_, C.byref(mat), C.c_double(band_edge), C.byref(reg)))
+        return reg
+
+    def initial_crack(self, mat, band_half=0.0):
+        phi = np.zeros(self.V)
+        be = C.c_double()
+        _chk(lib().orc_mesh_initial_crack(self.h_, C.byref(mat), C.c_double(band_half), _p(phi), C.byref(be)))
+        return phi, be.value
+
+    def newton_step(self, mat, reg, opts, solution, phi_old, phi_prev2, step, shift=True, max_its=64):
+        its = np.zeros((max_its, 4))
+        n_its, conv, feas = C.c_int(), C.c_int(), C.c_double()
+        _chk(lib().orc_mesh_newton_step(self.h_, C.byref(mat), C.byref(reg), C.byref(opts), _p(solution),
+                                        _p(phi_old), _p(phi_prev2), step, int(shift), max_its, _p(its),
+                                        C.byref(n_its), C.byref(conv), C.byref(feas)))
+        return dict(iterations=its[:n_its.value].copy(), converged=bool(conv.value), feasibility=feas.value)
+
+    def tcv(self, sol):
+        out = C.c_double()
+        _chk(lib().orc_mesh_tcv(self.h_, _p(np.ascontiguousarray(sol, dtype=np.float64)), C.byref(out)))
+        return out.value
+
+    def cod(self, sol, stations):
+        st = np.ascontiguousarray(stations, dtype=np.float64)
+        out = np.zeros(len(st))
+        _chk(lib().orc_mesh_cod(self.h_, _p(np.ascontiguousarray(sol, dtype=np.float64)), _p(st), len(st),
+                                _p(out)))
+        return out
+
+    def estimator(self, sol):
+        eta = np.zeros(self.n_active)
+        _chk(lib().orc_mesh_estimator(self.h_, _p(np.ascontiguousarray(sol, dtype=np.float64)), _p(eta)))
+        return eta
+
+    def mark(self, sol, eta=None, phi_threshold=0.8, h_target=0.0, theta=0.3, max_level=16, estimator=True):
+        pol = np.array([phi_threshold, h_target, theta, max_level, 1.0 if estimator else 0.0])
+        out = np.zeros(self.n_active, dtype=np.int32)
+        n = C.c_int64()
+        e = None if eta is None else np.ascontiguousarray(eta, dtype=np.float64)
+        _chk(lib().orc_mesh_mark(self.h_, _p(np.ascontiguousarray(sol, dtype=np.float64)), _p(e), _p(pol),
+                                 _p(out, C.c_int32), C.byref(n)))
+        return out[:n.value].copy()
+
+    def transfer_to(self, vec, new_mesh):
+        out = np.zeros(new_mesh.n_total)
+        _chk(lib().orc_mesh_transfer(self.h_, _p(np.ascontiguousarray(vec, dtype=np.float64)), new_mesh.h_,
+                                     _p(out)))
+        return out
+
+    def adaptive_cycle(self, mat, opts, cycles=1, n_steps=1, estimator_rounds=1, halve_band_target=True,
+                       seed_band=0.0, phi_threshold=0.8, h_target=0.0, theta=0.3, max_level=16, estimator=True,
+                       sol_cap=1 << 24):
+        pol = np.array([phi_threshold, h_target, theta, max_level, 1.0 if estimator else 0.0])
+        rec = np.zeros((cycles + 1, 8))
+        n = C.c_int()
+        sol = np.zeros(sol_cap)
+        _chk(lib().orc_mesh_adaptive_cycle(self.h_, C.byref(mat), C.byref(opts), _p(pol), cycles, n_steps,
+                                           estimator_rounds, int(halve_band_target), C.c_double(seed_band),
+                                           cycles + 1, _p(rec), C.byref(n), _p(sol), C.c_int64(sol_cap)))
+        self._info()
+        return rec[:n.value].copy(), sol[:self.n_total].copy()
+
+
+class MeshConstraints:
+    """ConstraintSet of a general mesh (fem.cpp:189-267): closed lines in ascending dof order."""
+
+    def __init__(self, mesh: Mesh, clamp, dofs, vals):
+        self.mesh = mesh
+        dofs = np.ascontiguousarray(dofs, dtype=np.int64)
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        self.h_ = C.c_void_p()
+        _chk(lib().orc_mesh_constraints(mesh.h_, int(clamp), C.c_int64(len(dofs)), _p(dofs, C.c_int64), _p(vals),
+                                        C.byref(self.h_)))
+
+    def __del__(self):
+        try:
+            lib().orc_mcs_destroy(self.h_)
+        except Exception:
+            pass
+
+    def lines(self):
+        """dofs, ptr, masters, weights, inhomogeneities (CSR of the closed lines)."""
+        nl, ne = C.c_int64(), C.c_int64()
+        lib().orc_mcs_info(self.h_, C.byref(nl), C.byref(ne))
+        dofs = np.zeros(nl.value, dtype=np.int64)
+        ptr = np.zeros(nl.value + 1, dtype=np.int64)
+        m = np.zeros(ne.value, dtype=np.int64)
+        w = np.zeros(ne.value)
+        inh = np.zeros(nl.value)
+        lib().orc_mcs_export(self.h_, _p(dofs, C.c_int64), _p(ptr, C.c_int64), _p(m, C.c_int64), _p(w), _p(inh))
+        return dofs, ptr, m, w, inh
+
+    def distribute(self, v, homogeneous=False):
+        v = np.array(v, dtype=np.float64)
+        lib().orc_mcs_distribute(self.h_, _p(v), C.c_int64(len(v)), int(homogeneous))
+        return v
