@@ -286,6 +286,88 @@ int cf_block_write_matrix_market(cf_block b, int which, const char* path);
 int cf_csr_write_matrix_market(cf_csr A, const char* path);
 int cf_write_vtk(cf_problem p, const double* solution, const double* phi_old, const char* path, int binary);
 
+/* ------------------------------------------------------------------ general (adaptive) meshes
+ * A cf_mesh is the reference's Mesh + DofMap (mesh.hpp:52-119, fem.hpp:33-74): a forest of
+ * n0^d root cells on (-K, K)^d, refined with the 2:1 face-balance closure; cell ids in creation
+ * order; vertices = sorted packed integer corner keys (the DofMap, built on the device).  The
+ * constraint / assembly / Newton / post-processing entries below mirror the uniform ones with the
+ * mesh in place of the problem; constraint sets of a mesh come from cf_mesh_constraints_build
+ * (Dirichlet clamp, hanging vertices with closed lines, active set; fem.cpp:189-267) and are
+ * accepted by cf_constraints_distribute.  States of a mesh come from cf_mesh_state_create. */
+typedef struct cf_mesh_s* cf_mesh;
+/* RefinementPolicy (adapt.hpp:12-20) */
+typedef struct {
+  double phi_threshold, h_target, theta;
+  int max_level, estimator;
+} cf_refinement_policy;
+/* AdaptiveOptions (adapt.hpp:38-55; cod_stations omitted: use cf_mesh_compute_cod per level) */
+typedef struct {
+  cf_refinement_policy policy;
+  cf_solver_options solver;
+  int cycles, n_steps, halve_band_target, estimator_rounds;
+  double seed_band;
+} cf_adaptive_options;
+/* LevelRecord (postproc.hpp:33-43) without the COD profile, plus the last report's convergence */
+typedef struct {
+  int level;
+  int64_t dofs;
+  double eps, h_min, tcv;
+  int newton_iters;
+  double gmres_mean;
+  int converged;
+} cf_level_record;
+
+int cf_mesh_create(int dim, double half_width, int n0, cf_mesh* out);       /* create_mesh (mesh.cpp:18-34) */
+int cf_mesh_copy(cf_mesh m, cf_mesh* out);
+int cf_mesh_destroy(cf_mesh m);
+int cf_mesh_refine(cf_mesh m, const int32_t* cells, int64_t n);            /* refine (mesh.cpp:203-215) */
+int cf_mesh_uniform_refine(cf_mesh m, int times);                          /* uniform_refine (mesh.cpp:217-223) */
+/* info4: n_cells, n_active, max_active_level, n_vertices; h_min = min_active_edge */
+int cf_mesh_info(cf_mesh m, int64_t info4[4], double* h_min);
+int cf_mesh_active_cells(cf_mesh m, int32_t* ids);                         /* active_cells, ascending */
+/* per cell (id order): level, parent, active, anchor (3 integer coordinates) */
+int cf_mesh_cells(cf_mesh m, int32_t* level, int32_t* parent, int8_t* active, int64_t* anchor);
+int cf_mesh_vertex_keys(cf_mesh m, int64_t* keys);                         /* DofMap numbering (fem.cpp:98-116) */
+int cf_mesh_cell_vertices(cf_mesh m, int64_t* out);                        /* per active cell, 2^d corners */
+/* active_faces (mesh.cpp:225-259): rows of 5 (cell, axis, side, neighbor or -1, rel); out5 NULL counts */
+int cf_mesh_faces(cf_mesh m, int64_t* n, int32_t* out5);
+int cf_mesh_find_cell(cf_mesh m, const double x[3], int32_t* cell);        /* find_active_cell (mesh.cpp:143-150) */
+int cf_mesh_constraints_build(cf_mesh m, int clamp_boundary, int64_t n_active, const int64_t* active_dofs,
+                              const double* active_values, cf_constraints* out);
+/* the closed lines with entries, ascending dof: counts first (dofs NULL), then CSR export */
+int cf_constraint_lines(cf_constraints c, int64_t* n_lines, int64_t* n_entries, int64_t* dofs, int64_t* ptr,
+                        int64_t* masters, double* weights, double* inhomogeneities);
+int cf_mesh_assemble_residual(cf_mesh m, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                              const double* solution, const double* phi_tilde, double* residual);
+int cf_mesh_assemble_jacobian(cf_mesh m, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                              const double* solution, const double* phi_tilde, cf_block* out);
+int cf_mesh_rigid_body_modes(cf_mesh m, cf_constraints c, double* B);
+int cf_mesh_slit_band_edge(cf_mesh m, const cf_material* mat, double* edge);
+int cf_mesh_resolve_regularization(cf_mesh m, const cf_material* mat, double band_edge, cf_regularization* out);
+int cf_mesh_initial_crack(cf_mesh m, const cf_material* mat, double band_half, double* phi, double* band_edge);
+int cf_mesh_make_initial_state(cf_mesh m, const cf_material* mat, double seed_band, cf_state* out);
+int cf_mesh_state_create(cf_mesh m, const double* solution, const double* phi_old, const double* phi_prev2, int step,
+                         cf_state* out);
+int cf_mesh_newton_active_set_step(cf_mesh m, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, cf_newton_iteration* its, int max_its, int* n_its,
+                                   int* converged, double* feasibility, cf_phase_times* times);
+int cf_mesh_solve_loading_sequence(cf_mesh m, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, int n_steps, cf_newton_iteration* its, int max_its,
+                                   int* n_its, int* converged, double* feasibility, int* steps_done);
+int cf_mesh_compute_tcv(cf_mesh m, const double* solution, double* tcv);
+int cf_mesh_compute_cod(cf_mesh m, const double* solution, const double* stations, int n_stations, double* openings);
+/* jump_estimator (adapt.cpp:16-55): eta per active cell in active order */
+int cf_mesh_jump_estimator(cf_mesh m, const double* solution, double* eta);
+/* mark_cells (adapt.cpp:57-97): eta may be NULL (no estimator field); ids ascending */
+int cf_mesh_mark_cells(cf_mesh m, const double* solution, const double* eta, const cf_refinement_policy* policy,
+                       int32_t* marked, int64_t* n_marked);
+/* transfer (fem.cpp:318-333): nodal interpolation of old_vec onto the refined mesh */
+int cf_mesh_transfer(cf_mesh old_mesh, const double* old_vec, cf_mesh new_mesh, double* new_vec);
+/* adaptive_cycle (adapt.cpp:122-190): the mesh is refined in place and the state replaced by the
+ * final level's; records[max_records] */
+int cf_mesh_adaptive_cycle(cf_mesh m, cf_state s, cf_material* mat, const cf_adaptive_options* opts,
+                           cf_level_record* records, int max_records, int* n_records);
+
 /* ------------------------------------------------------------------ multi-GPU
  * One process per GPU.  Rank 0 makes an id, the launcher broadcasts it (e.g. over
  * torch.distributed), every rank creates its communicator on its current CUDA device.  The _comm

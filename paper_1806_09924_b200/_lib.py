@@ -67,6 +67,17 @@ class GmresOptions(C.Structure):
         super().__init__(**d)
 
 
+class RefinementPolicy(C.Structure):
+    """adapt.hpp:12-20."""
+    _fields_ = [("phi_threshold", C.c_double), ("h_target", C.c_double), ("theta", C.c_double),
+                ("max_level", C.c_int), ("estimator", C.c_int)]
+
+    def __init__(self, **kw):
+        d = dict(phi_threshold=0.8, h_target=0.0, theta=0.3, max_level=16, estimator=1)
+        d.update(kw)
+        super().__init__(**d)
+
+
 class SolverOptions(C.Structure):
     """solver.hpp:13-26 (prec_kind 0 exact, 1 amg, 2 diagonal)."""
     _fields_ = [("newton_tol", C.c_double), ("newton_abs_floor", C.c_double), ("newton_max_iter", C.c_int),
@@ -80,6 +91,23 @@ class SolverOptions(C.Structure):
                  gmres=GmresOptions(), amg=AmgOptions())
         d.update(kw)
         super().__init__(**d)
+
+
+class AdaptiveOptions(C.Structure):
+    """adapt.hpp:38-55 (cod_stations: compute_cod per level)."""
+    _fields_ = [("policy", RefinementPolicy), ("solver", SolverOptions), ("cycles", C.c_int), ("n_steps", C.c_int),
+                ("halve_band_target", C.c_int), ("estimator_rounds", C.c_int), ("seed_band", C.c_double)]
+
+    def __init__(self, **kw):
+        d = dict(policy=RefinementPolicy(), solver=SolverOptions(), cycles=0, n_steps=1, halve_band_target=1,
+                 estimator_rounds=1, seed_band=0.0)
+        d.update(kw)
+        super().__init__(**d)
+
+
+class LevelRecordC(C.Structure):
+    _fields_ = [("level", C.c_int), ("dofs", C.c_int64), ("eps", C.c_double), ("h_min", C.c_double),
+                ("tcv", C.c_double), ("newton_iters", C.c_int), ("gmres_mean", C.c_double), ("converged", C.c_int)]
 
 
 _lib = None
@@ -163,6 +191,41 @@ SIGNATURES = [
     ("cf_block_write_matrix_market", _I, [_P, _I, C.c_char_p]),
     ("cf_csr_write_matrix_market", _I, [_P, C.c_char_p]),
     ("cf_write_vtk", _I, [_P, _P, _P, C.c_char_p, _I]),
+    ("cf_mesh_create", _I, [_I, _D, _I, C.POINTER(_P)]),
+    ("cf_mesh_copy", _I, [_P, C.POINTER(_P)]),
+    ("cf_mesh_destroy", _I, [_P]),
+    ("cf_mesh_refine", _I, [_P, _P, _L]),
+    ("cf_mesh_uniform_refine", _I, [_P, _I]),
+    ("cf_mesh_info", _I, [_P, _P, C.POINTER(_D)]),
+    ("cf_mesh_active_cells", _I, [_P, _P]),
+    ("cf_mesh_cells", _I, [_P, _P, _P, _P, _P]),
+    ("cf_mesh_vertex_keys", _I, [_P, _P]),
+    ("cf_mesh_cell_vertices", _I, [_P, _P]),
+    ("cf_mesh_faces", _I, [_P, C.POINTER(_L), _P]),
+    ("cf_mesh_find_cell", _I, [_P, _P, C.POINTER(C.c_int32)]),
+    ("cf_mesh_constraints_build", _I, [_P, _I, _L, _P, _P, C.POINTER(_P)]),
+    ("cf_constraint_lines", _I, [_P, C.POINTER(_L), C.POINTER(_L), _P, _P, _P, _P, _P]),
+    ("cf_mesh_assemble_residual", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P, _P]),
+    ("cf_mesh_assemble_jacobian", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization), _P, _P,
+                                       C.POINTER(_P)]),
+    ("cf_mesh_rigid_body_modes", _I, [_P, _P, _P]),
+    ("cf_mesh_slit_band_edge", _I, [_P, C.POINTER(Material), C.POINTER(_D)]),
+    ("cf_mesh_resolve_regularization", _I, [_P, C.POINTER(Material), _D, C.POINTER(Regularization)]),
+    ("cf_mesh_initial_crack", _I, [_P, C.POINTER(Material), _D, _P, C.POINTER(_D)]),
+    ("cf_mesh_make_initial_state", _I, [_P, C.POINTER(Material), _D, C.POINTER(_P)]),
+    ("cf_mesh_state_create", _I, [_P, _P, _P, _P, _I, C.POINTER(_P)]),
+    ("cf_mesh_newton_active_set_step", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
+                                            C.POINTER(SolverOptions), _P, _I, C.POINTER(_I), C.POINTER(_I),
+                                            C.POINTER(_D), _P]),
+    ("cf_mesh_solve_loading_sequence", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
+                                            C.POINTER(SolverOptions), _I, _P, _I, _P, _P, _P, C.POINTER(_I)]),
+    ("cf_mesh_compute_tcv", _I, [_P, _P, C.POINTER(_D)]),
+    ("cf_mesh_compute_cod", _I, [_P, _P, _P, _I, _P]),
+    ("cf_mesh_jump_estimator", _I, [_P, _P, _P]),
+    ("cf_mesh_mark_cells", _I, [_P, _P, _P, C.POINTER(RefinementPolicy), _P, C.POINTER(_L)]),
+    ("cf_mesh_transfer", _I, [_P, _P, _P, _P]),
+    ("cf_mesh_adaptive_cycle", _I, [_P, _P, C.POINTER(Material), C.POINTER(AdaptiveOptions), _P, _I,
+                                    C.POINTER(_I)]),
     ("cf_comm_unique_id", _I, [_P]),
     ("cf_comm_create", _I, [_P, _I, _I, C.POINTER(_P)]),
     ("cf_comm_create_host", _I, [_I, _I, _P, C.POINTER(_P)]),

@@ -901,10 +901,10 @@ Problem* make_problem(int d, double K, int n0, int r) {
 }
 
 // q1_shape / cell_rule (fem.cpp:53-96) and the elasticity integrand table (model.cpp:270-276).
-void build_tables(Problem& P, double mu, double lam) {
-  if (P.val_ready && P.mu == mu && P.lam == lam) return;
-  const int d = P.g.d, nv = 1 << d, nq = 1 << d;
-  Tables& T = P.host_tab;
+// Quadrature / Q1 tables of a cell of edge h (fem.cpp:53-96; model.cpp:111-123, 245-247, 274-275),
+// computed with the reference's expressions (no FMA contraction in this file)
+void fill_tables(Tables& T, int d, double h, double detJ, double mu, double lam) {
+  const int nv = 1 << d, nq = 1 << d;
   std::memset(&T, 0, sizeof(T));
   const double a1 = 1.0 / std::sqrt(3.0);
   const double x1[2] = {-a1, a1}, w1[2] = {1.0, 1.0};
@@ -918,7 +918,7 @@ void build_tables(Problem& P, double mu, double lam) {
       xi[a] = 0.5 * (x1[i] + 1.0);
       wt *= 0.5 * w1[i];
     }
-    T.w[q] = wt * P.g.detJ;
+    T.w[q] = wt * detJ;
     for (int k = 0; k < nv; ++k) {
       double v = 1.0;
       for (int a = 0; a < d; ++a) v *= (k & (1 << a)) ? xi[a] : 1.0 - xi[a];
@@ -930,7 +930,7 @@ void build_tables(Problem& P, double mu, double lam) {
           gr *= (k & (1 << b)) ? xi[b] : 1.0 - xi[b];
         }
         T.G[q][k][a] = gr;
-        T.gp[q][k][a] = gr / P.g.h;
+        T.gp[q][k][a] = gr / h;
       }
     }
     for (int k = 0; k < nv; ++k)
@@ -944,7 +944,12 @@ void build_tables(Problem& P, double mu, double lam) {
                 mu * ((a == b ? gg : 0.0) + T.gp[q][l][a] * T.gp[q][k][b]) + lam * T.gp[q][l][b] * T.gp[q][k][a];
       }
   }
-  CF_CUDA(cudaMemcpyAsync(P.tab.p, &T, sizeof(Tables), cudaMemcpyHostToDevice, stream()));
+}
+
+void build_tables(Problem& P, double mu, double lam) {
+  if (P.val_ready && P.mu == mu && P.lam == lam) return;
+  fill_tables(P.host_tab, P.g.d, P.g.h, P.g.detJ, mu, lam);
+  CF_CUDA(cudaMemcpyAsync(P.tab.p, &P.host_tab, sizeof(Tables), cudaMemcpyHostToDevice, stream()));
   P.mu = mu;
   P.lam = lam;
   P.val_ready = true;
@@ -978,9 +983,10 @@ std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64
 }
 
 void distribute(const Constraints& c, double* v, bool homogeneous) {
-  const i64 nt = c.prob->g.n_total();
+  const i64 nt = c.flag.n;
   k_distribute<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, c.flag.p, c.inhom.p, v, homogeneous ? 1 : 0);
   CF_LAUNCHED();
+  distribute_lines(c, v, homogeneous);  // general meshes: the hanging lines (masters are unconstrained)
 }
 
 Slab make_slab(const GridDesc& g, i64 p_lo, i64 p_hi) {

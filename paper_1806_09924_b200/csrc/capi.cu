@@ -9,6 +9,7 @@
 #include <unordered_map>
 
 #include "cf_comm.hpp"
+#include "cf_mesh.hpp"
 #include "cf_types.hpp"
 #include "cf_vec.hpp"
 
@@ -27,6 +28,10 @@ struct cf_prec_s {
 struct cf_state_s {
   cfb::State st;
   cf_problem prob;
+  cf_mesh mesh = nullptr;  // a general-mesh state (prob == nullptr)
+};
+struct cf_mesh_s {
+  std::unique_ptr<cfb::MeshDisc> m;
 };
 struct cf_constraints_s {
   std::unique_ptr<cfb::Constraints> c;
@@ -287,7 +292,7 @@ int cf_constraints_destroy(cf_constraints c) {
 int cf_constraints_distribute(cf_constraints c, double* v, int homogeneous) {
   return guard([&] {
     CHECK_ARG(c && v, "cf_constraints_distribute: null argument");
-    OutArg<double> out(v, c->owner->p->g.n_total(), true);
+    OutArg<double> out(v, c->c->flag.n, true);
     distribute(*c->c, out.dev, homogeneous != 0);
     out.finish();
   });
@@ -941,7 +946,7 @@ int cf_state_get(cf_state s, double* solution, double* phi_old, double* phi_prev
 int cf_extrapolate_phi(cf_state s, double* phi_tilde) {
   return guard([&] {
     CHECK_ARG(s && phi_tilde, "cf_extrapolate_phi: null argument");
-    const i64 V = s->prob->p->g.V;
+    const i64 V = s->st.phi_old.n;
     OutArg<double> out(phi_tilde, V);
     extrapolate_phi(s->st, out.dev, V);
     out.finish();
@@ -1103,6 +1108,438 @@ int cf_solve_loading_sequence_comm(cf_problem p, cf_state s, const cf_material* 
     CHECK_ARG(p && s && mat && reg && opts && comm, "cf_solve_loading_sequence_comm: null argument");
     loading_sequence(p, s, mat, reg, opts, comm->c.get(), n_steps, its, max_its, n_its, converged, feasibility,
                      steps_done);
+  });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ general meshes
+static MeshDisc& M(cf_mesh m) { return *m->m; }
+
+static void mesh_loading_sequence(MeshDisc& m, State& st, const cf_material& mat, const cf_regularization& reg,
+                                  const cf_solver_options& opts, int n_steps, std::vector<NewtonReport>& reps) {
+  if (n_steps < 1) fail(CF_ERR_INVALID_ARGUMENT, "solve_loading_sequence: n_steps must be >= 1");
+  for (int n = 1; n <= n_steps; ++n) {  // solver.cpp:190-204
+    CF_CUDA(cudaMemcpyAsync(st.phi_prev2.p, st.phi_old.p, size_t(m.V) * sizeof(double), cudaMemcpyDeviceToDevice,
+                            stream()));
+    CF_CUDA(cudaMemcpyAsync(st.phi_old.p, st.solution.p + m.n_u(), size_t(m.V) * sizeof(double),
+                            cudaMemcpyDeviceToDevice, stream()));
+    st.step = n;
+    reps.push_back(mesh_newton_step(m, st, mat, reg, opts));
+    if (!reps.back().converged) break;
+  }
+}
+
+// make_initial_state on a mesh (solver.cpp:24-35): u = 0, phi = phi_old = phi_prev2 = seed
+static void mesh_initial_state(MeshDisc& m, const cf_material& mat, double seed_band, State& st) {
+  const std::vector<double> phi = mesh_initial_crack(m, mat, seed_band, nullptr);
+  st.solution.alloc(m.n_total());
+  st.phi_old.alloc(m.V);
+  st.phi_prev2.alloc(m.V);
+  st.solution.zero();
+  CF_CUDA(cudaMemcpyAsync(st.solution.p + m.n_u(), phi.data(), size_t(m.V) * sizeof(double), cudaMemcpyHostToDevice,
+                          stream()));
+  CF_CUDA(cudaMemcpyAsync(st.phi_old.p, phi.data(), size_t(m.V) * sizeof(double), cudaMemcpyHostToDevice, stream()));
+  CF_CUDA(cudaMemcpyAsync(st.phi_prev2.p, phi.data(), size_t(m.V) * sizeof(double), cudaMemcpyHostToDevice,
+                          stream()));
+  st.step = 0;
+  CF_CUDA(cudaStreamSynchronize(stream()));
+}
+
+// adaptive_cycle (adapt.cpp:122-190)
+static std::vector<cf_level_record> mesh_adaptive_cycle(MeshDisc& m, State& st, const cf_material& mat,
+                                                        const cf_adaptive_options& o) {
+  if (o.cycles < 0) fail(CF_ERR_INVALID_ARGUMENT, "adaptive_cycle: cycles must be >= 0");
+  cf_refinement_policy pol = o.policy;
+  double seed_band = o.seed_band;
+  if (seed_band <= 0.0 && !o.halve_band_target) seed_band = mesh_slit_band_edge(m, mat);
+  std::vector<cf_level_record> out;
+  for (int cycle = 0; cycle <= o.cycles; ++cycle) {
+    const cf_regularization reg = mesh_resolve_regularization(m, mat, mesh_slit_band_edge(m, mat));
+    std::vector<NewtonReport> reps;
+    mesh_loading_sequence(m, st, mat, reg, o.solver, o.n_steps, reps);
+    const NewtonReport& last = reps.back();
+    cf_level_record r{};
+    r.level = cycle;
+    r.dofs = m.n_total();
+    r.eps = reg.eps;
+    r.h_min = m.level_edge(m.max_level);
+    r.tcv = std::abs(mesh_compute_tcv(m, st.solution.p));
+    r.newton_iters = int(last.its.size());
+    int tot = 0;
+    for (const auto& it : last.its) tot += it.gmres_iterations;
+    r.gmres_mean = last.its.empty() ? 0.0 : double(tot) / double(last.its.size());
+    r.converged = last.converged;
+    out.push_back(r);
+    if (!last.converged || cycle == o.cycles) break;
+    if (o.halve_band_target) pol.h_target = 0.5 * mesh_slit_band_edge(m, mat);
+    for (int pass = 0; pass < std::max(1, o.estimator_rounds); ++pass) {
+      if (pass > 0) {
+        const cf_regularization r2 = mesh_resolve_regularization(m, mat, mesh_slit_band_edge(m, mat));
+        std::vector<NewtonReport> rp;
+        mesh_loading_sequence(m, st, mat, r2, o.solver, o.n_steps, rp);
+        if (!rp.back().converged) break;
+      }
+      DevBuf<double> eta;
+      if (pol.estimator) {
+        eta.alloc(m.nact);
+        mesh_jump_estimator(m, st.solution.p, eta.p);
+        mesh_mask_band_eta(m, st.solution.p, eta.p, pol);
+      }
+      std::vector<int> marked = mesh_mark_cells(m, st.solution.p, pol.estimator ? eta.p : nullptr, pol);
+      if (marked.empty()) break;
+      for (int round = 0; round < 10 && !marked.empty(); ++round) {
+        std::unique_ptr<MeshDisc> old = mesh_copy(m);
+        mesh_refine(m, marked);
+        // move_state (adapt.cpp:101-118): u transferred, phi / phi_old / history re-seeded
+        DevBuf<double> moved(m.n_total());
+        mesh_transfer(*old, st.solution.p, m, moved.p);
+        State next;
+        mesh_initial_state(m, mat, seed_band, next);
+        CF_CUDA(cudaMemcpyAsync(next.solution.p, moved.p, size_t(m.n_u()) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                stream()));
+        st.solution = std::move(next.solution);
+        st.phi_old = std::move(next.phi_old);
+        st.phi_prev2 = std::move(next.phi_prev2);
+        st.step = 0;
+        cf_refinement_policy band_only = pol;
+        band_only.estimator = 0;
+        marked = mesh_mark_cells(m, st.solution.p, nullptr, band_only);
+      }
+    }
+  }
+  return out;
+}
+
+extern "C" {
+
+int cf_mesh_create(int dim, double half_width, int n0, cf_mesh* out) {
+  return guard([&] {
+    CHECK_ARG(out, "cf_mesh_create: null argument");
+    *out = new cf_mesh_s{std::unique_ptr<MeshDisc>(mesh_create(dim, half_width, n0))};
+  });
+}
+int cf_mesh_copy(cf_mesh m, cf_mesh* out) {
+  return guard([&] {
+    CHECK_ARG(m && out, "cf_mesh_copy: null argument");
+    *out = new cf_mesh_s{mesh_copy(M(m))};
+  });
+}
+int cf_mesh_destroy(cf_mesh m) {
+  return guard([&] { delete m; });
+}
+int cf_mesh_refine(cf_mesh m, const int32_t* cells, int64_t n) {
+  return guard([&] {
+    CHECK_ARG(m && (n == 0 || cells) && n >= 0, "cf_mesh_refine: bad argument");
+    mesh_refine(M(m), std::vector<int>(cells, cells + n));
+  });
+}
+int cf_mesh_uniform_refine(cf_mesh m, int times) {
+  return guard([&] {
+    CHECK_ARG(m, "cf_mesh_uniform_refine: null mesh");
+    mesh_uniform_refine(M(m), times);
+  });
+}
+int cf_mesh_info(cf_mesh m, int64_t info4[4], double* h_min) {
+  return guard([&] {
+    CHECK_ARG(m && info4, "cf_mesh_info: null argument");
+    const MeshDisc& d = M(m);
+    info4[0] = int64_t(d.cells.size());
+    info4[1] = d.nact;
+    info4[2] = d.max_level;
+    info4[3] = d.V;
+    if (h_min) *h_min = d.level_edge(d.max_level);
+  });
+}
+int cf_mesh_active_cells(cf_mesh m, int32_t* ids) {
+  return guard([&] {
+    CHECK_ARG(m && ids, "cf_mesh_active_cells: null argument");
+    std::copy(M(m).active.begin(), M(m).active.end(), ids);
+  });
+}
+int cf_mesh_cells(cf_mesh m, int32_t* level, int32_t* parent, int8_t* active, int64_t* anchor) {
+  return guard([&] {
+    CHECK_ARG(m, "cf_mesh_cells: null mesh");
+    const MeshDisc& d = M(m);
+    for (size_t i = 0; i < d.cells.size(); ++i) {
+      if (level) level[i] = d.cells[i].level;
+      if (parent) parent[i] = d.cells[i].parent;
+      if (active) active[i] = d.cells[i].active;
+      if (anchor)
+        for (int a = 0; a < 3; ++a) anchor[3 * i + a] = d.cells[i].anchor[a];
+    }
+  });
+}
+int cf_mesh_vertex_keys(cf_mesh m, int64_t* keys) {
+  return guard([&] {
+    CHECK_ARG(m && keys, "cf_mesh_vertex_keys: null argument");
+    CF_CUDA(cudaMemcpyAsync(keys, M(m).vkey.p, size_t(M(m).V) * sizeof(int64_t), cudaMemcpyDefault, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+int cf_mesh_cell_vertices(cf_mesh m, int64_t* out) {
+  return guard([&] {
+    CHECK_ARG(m && out, "cf_mesh_cell_vertices: null argument");
+    const MeshDisc& d = M(m);
+    const i64 n = d.nact * (i64(1) << d.d);
+    std::vector<int> cv(size_t(std::max<i64>(n, 0)));
+    CF_CUDA(cudaMemcpyAsync(cv.data(), d.cvert.p, size_t(n) * sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    for (i64 i = 0; i < n; ++i) out[i] = cv[size_t(i)];
+  });
+}
+int cf_mesh_faces(cf_mesh m, int64_t* n, int32_t* out5) {
+  return guard([&] {
+    CHECK_ARG(m && n, "cf_mesh_faces: null argument");
+    const std::vector<int> f = mesh_faces(M(m));
+    *n = int64_t(f.size() / 5);
+    if (out5) std::copy(f.begin(), f.end(), out5);
+  });
+}
+int cf_mesh_find_cell(cf_mesh m, const double x[3], int32_t* cell) {
+  return guard([&] {
+    CHECK_ARG(m && x && cell, "cf_mesh_find_cell: null argument");
+    *cell = mesh_find_cell(M(m), x);
+  });
+}
+int cf_mesh_constraints_build(cf_mesh m, int clamp_boundary, int64_t n_active, const int64_t* active_dofs,
+                              const double* active_values, cf_constraints* out) {
+  return guard([&] {
+    CHECK_ARG(m && out, "cf_mesh_constraints_build: null argument");
+    CHECK_ARG(n_active >= 0, "cf_mesh_constraints_build: negative active count");
+    CHECK_ARG(n_active == 0 || (active_dofs && active_values), "cf_mesh_constraints_build: null active arrays");
+    InArg<i64> dofs(reinterpret_cast<const i64*>(active_dofs), n_active);
+    InArg<double> vals(active_values, n_active);
+    auto c = mesh_build_constraints(M(m), clamp_boundary != 0, n_active, dofs.dev, vals.dev);
+    *out = new cf_constraints_s{std::move(c), nullptr};
+  });
+}
+int cf_constraint_lines(cf_constraints c, int64_t* n_lines, int64_t* n_entries, int64_t* dofs, int64_t* ptr,
+                        int64_t* masters, double* weights, double* inhomogeneities) {
+  return guard([&] {
+    CHECK_ARG(c && n_lines && n_entries, "cf_constraint_lines: null argument");
+    const Constraints& cs = *c->c;
+    *n_lines = cs.n_lines;
+    std::vector<i64> lp(size_t(cs.n_lines + 1), 0);
+    if (cs.n_lines)
+      CF_CUDA(cudaMemcpyAsync(lp.data(), cs.line_ptr.p, lp.size() * sizeof(i64), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *n_entries = lp.back();
+    if (!dofs) return;
+    std::vector<int> ld(size_t(cs.n_lines)), lm(size_t(lp.back()));
+    std::vector<double> lw(size_t(lp.back())), inh(size_t(cs.flag.n));
+    if (cs.n_lines) {
+      CF_CUDA(cudaMemcpyAsync(ld.data(), cs.line_dof.p, ld.size() * sizeof(int), cudaMemcpyDeviceToHost, stream()));
+      if (!lm.empty()) {
+        CF_CUDA(cudaMemcpyAsync(lm.data(), cs.line_m.p, lm.size() * sizeof(int), cudaMemcpyDeviceToHost, stream()));
+        CF_CUDA(cudaMemcpyAsync(lw.data(), cs.line_w.p, lw.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                stream()));
+      }
+    }
+    CF_CUDA(cudaMemcpyAsync(inh.data(), cs.inhom.p, inh.size() * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    for (i64 i = 0; i < cs.n_lines; ++i) {
+      dofs[i] = ld[size_t(i)];
+      if (ptr) ptr[i] = lp[size_t(i)];
+      if (inhomogeneities) inhomogeneities[i] = inh[size_t(ld[size_t(i)])];
+    }
+    if (ptr) ptr[cs.n_lines] = lp.back();
+    for (i64 k = 0; k < lp.back(); ++k) {
+      if (masters) masters[k] = lm[size_t(k)];
+      if (weights) weights[k] = lw[size_t(k)];
+    }
+  });
+}
+int cf_mesh_assemble_residual(cf_mesh m, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                              const double* solution, const double* phi_tilde, double* residual) {
+  return guard([&] {
+    CHECK_ARG(m && c && mat && reg && solution && phi_tilde && residual, "cf_mesh_assemble_residual: null argument");
+    MeshDisc& d = M(m);
+    InArg<double> x(solution, d.n_total());
+    InArg<double> pt(phi_tilde, d.V);
+    OutArg<double> out(residual, d.n_total());
+    mesh_assemble_residual(d, *c->c, *c->c, *mat, *reg, x.dev, pt.dev, out.dev);
+    out.finish();
+  });
+}
+int cf_mesh_assemble_jacobian(cf_mesh m, cf_constraints c, const cf_material* mat, const cf_regularization* reg,
+                              const double* solution, const double* phi_tilde, cf_block* out) {
+  return guard([&] {
+    CHECK_ARG(m && c && mat && reg && solution && phi_tilde && out, "cf_mesh_assemble_jacobian: null argument");
+    MeshDisc& d = M(m);
+    InArg<double> x(solution, d.n_total());
+    InArg<double> pt(phi_tilde, d.V);
+    auto J = mesh_assemble_jacobian(d, *c->c, *c->c, *mat, *reg, x.dev, pt.dev);
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *out = new cf_block_s{std::move(J)};
+  });
+}
+int cf_mesh_rigid_body_modes(cf_mesh m, cf_constraints c, double* B) {
+  return guard([&] {
+    CHECK_ARG(m && c && B, "cf_mesh_rigid_body_modes: null argument");
+    MeshDisc& d = M(m);
+    OutArg<double> out(B, d.n_u() * (d.d == 2 ? 3 : 6));
+    mesh_rigid_body_modes(d, *c->c, out.dev);
+    out.finish();
+  });
+}
+int cf_mesh_slit_band_edge(cf_mesh m, const cf_material* mat, double* edge) {
+  return guard([&] {
+    CHECK_ARG(m && mat && edge, "cf_mesh_slit_band_edge: null argument");
+    *edge = mesh_slit_band_edge(M(m), *mat);
+  });
+}
+int cf_mesh_resolve_regularization(cf_mesh m, const cf_material* mat, double band_edge, cf_regularization* out) {
+  return guard([&] {
+    CHECK_ARG(m && mat && out, "cf_mesh_resolve_regularization: null argument");
+    *out = mesh_resolve_regularization(M(m), *mat, band_edge);
+  });
+}
+int cf_mesh_initial_crack(cf_mesh m, const cf_material* mat, double band_half, double* phi, double* band_edge) {
+  return guard([&] {
+    CHECK_ARG(m && mat && phi, "cf_mesh_initial_crack: null argument");
+    const std::vector<double> v = mesh_initial_crack(M(m), *mat, band_half, band_edge);
+    OutArg<double> out(phi, M(m).V);
+    CF_CUDA(cudaMemcpyAsync(out.dev, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, stream()));
+    out.finish();
+    CF_CUDA(cudaStreamSynchronize(stream()));
+  });
+}
+int cf_mesh_state_create(cf_mesh m, const double* solution, const double* phi_old, const double* phi_prev2, int step,
+                         cf_state* out) {
+  return guard([&] {
+    CHECK_ARG(m && out, "cf_mesh_state_create: null argument");
+    MeshDisc& d = M(m);
+    auto* s = new cf_state_s;
+    s->prob = nullptr;
+    s->mesh = m;
+    s->st.solution.alloc(d.n_total());
+    s->st.phi_old.alloc(d.V);
+    s->st.phi_prev2.alloc(d.V);
+    auto put = [&](DevBuf<double>& b, const double* src) {
+      if (src)
+        CF_CUDA(cudaMemcpyAsync(b.p, src, size_t(b.n) * sizeof(double), cudaMemcpyDefault, stream()));
+      else
+        b.zero();
+    };
+    put(s->st.solution, solution);
+    put(s->st.phi_old, phi_old);
+    put(s->st.phi_prev2, phi_prev2);
+    s->st.step = step;
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    *out = s;
+  });
+}
+int cf_mesh_make_initial_state(cf_mesh m, const cf_material* mat, double seed_band, cf_state* out) {
+  return guard([&] {
+    CHECK_ARG(m && mat && out, "cf_mesh_make_initial_state: null argument");
+    auto* s = new cf_state_s;
+    s->prob = nullptr;
+    s->mesh = m;
+    try {
+      mesh_initial_state(M(m), *mat, seed_band, s->st);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+int cf_mesh_newton_active_set_step(cf_mesh m, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, cf_newton_iteration* its, int max_its, int* n_its,
+                                   int* converged, double* feasibility, cf_phase_times* times) {
+  return guard([&] {
+    CHECK_ARG(m && s && mat && reg && opts, "cf_mesh_newton_active_set_step: null argument");
+    CHECK_ARG(s->st.solution.n == M(m).n_total(), "cf_mesh_newton_active_set_step: state of another mesh");
+    validate_material(*mat);
+    cudaEvent_t a, b;
+    CF_CUDA(cudaEventCreate(&a));
+    CF_CUDA(cudaEventCreate(&b));
+    CF_CUDA(cudaEventRecord(a, stream()));
+    NewtonReport r = mesh_newton_step(M(m), s->st, *mat, *reg, *opts);
+    CF_CUDA(cudaEventRecord(b, stream()));
+    CF_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    fill_report(r, its, max_its, n_its, converged, feasibility);
+    if (times)
+      *times = cf_phase_times{r.times.residual, r.times.active_set, r.times.jacobian, r.times.amg_setup,
+                              r.times.gmres, double(ms)};
+  });
+}
+int cf_mesh_solve_loading_sequence(cf_mesh m, cf_state s, const cf_material* mat, const cf_regularization* reg,
+                                   const cf_solver_options* opts, int n_steps, cf_newton_iteration* its, int max_its,
+                                   int* n_its, int* converged, double* feasibility, int* steps_done) {
+  return guard([&] {
+    CHECK_ARG(m && s && mat && reg && opts, "cf_mesh_solve_loading_sequence: null argument");
+    validate_material(*mat);
+    std::vector<NewtonReport> reps;
+    mesh_loading_sequence(M(m), s->st, *mat, *reg, *opts, n_steps, reps);
+    int off = 0;
+    for (size_t n = 0; n < reps.size(); ++n) {
+      int k = 0;
+      fill_report(reps[n], its ? its + off : nullptr, std::max(0, max_its - off), &k,
+                  converged ? converged + n : nullptr, feasibility ? feasibility + n : nullptr);
+      if (n_its) n_its[n] = k;
+      off += std::min(k, std::max(0, max_its - off));
+    }
+    if (steps_done) *steps_done = int(reps.size());
+  });
+}
+int cf_mesh_compute_tcv(cf_mesh m, const double* solution, double* tcv) {
+  return guard([&] {
+    CHECK_ARG(m && solution && tcv, "cf_mesh_compute_tcv: null argument");
+    InArg<double> x(solution, M(m).n_total());
+    *tcv = mesh_compute_tcv(M(m), x.dev);
+  });
+}
+int cf_mesh_compute_cod(cf_mesh m, const double* solution, const double* stations, int n_stations, double* openings) {
+  return guard([&] {
+    CHECK_ARG(m && solution && (n_stations == 0 || (stations && openings)), "cf_mesh_compute_cod: null argument");
+    InArg<double> x(solution, M(m).n_total());
+    mesh_compute_cod(M(m), x.dev, stations, n_stations, openings);
+  });
+}
+int cf_mesh_jump_estimator(cf_mesh m, const double* solution, double* eta) {
+  return guard([&] {
+    CHECK_ARG(m && solution && eta, "cf_mesh_jump_estimator: null argument");
+    InArg<double> x(solution, M(m).n_total());
+    OutArg<double> out(eta, M(m).nact);
+    mesh_jump_estimator(M(m), x.dev, out.dev);
+    out.finish();
+  });
+}
+int cf_mesh_mark_cells(cf_mesh m, const double* solution, const double* eta, const cf_refinement_policy* policy,
+                       int32_t* marked, int64_t* n_marked) {
+  return guard([&] {
+    CHECK_ARG(m && solution && policy && marked && n_marked, "cf_mesh_mark_cells: null argument");
+    InArg<double> x(solution, M(m).n_total());
+    InArg<double> e(eta, eta ? M(m).nact : 0);
+    const std::vector<int> ids = mesh_mark_cells(M(m), x.dev, eta ? e.dev : nullptr, *policy);
+    std::copy(ids.begin(), ids.end(), marked);
+    *n_marked = int64_t(ids.size());
+  });
+}
+int cf_mesh_transfer(cf_mesh old_mesh, const double* old_vec, cf_mesh new_mesh, double* new_vec) {
+  return guard([&] {
+    CHECK_ARG(old_mesh && old_vec && new_mesh && new_vec, "cf_mesh_transfer: null argument");
+    InArg<double> x(old_vec, M(old_mesh).n_total());
+    OutArg<double> out(new_vec, M(new_mesh).n_total());
+    mesh_transfer(M(old_mesh), x.dev, M(new_mesh), out.dev);
+    out.finish();
+  });
+}
+int cf_mesh_adaptive_cycle(cf_mesh m, cf_state s, cf_material* mat, const cf_adaptive_options* opts,
+                           cf_level_record* records, int max_records, int* n_records) {
+  return guard([&] {
+    CHECK_ARG(m && s && mat && opts, "cf_mesh_adaptive_cycle: null argument");
+    validate_material(*mat);
+    CHECK_ARG(s->st.solution.n == M(m).n_total(), "cf_mesh_adaptive_cycle: state of another mesh");
+    const std::vector<cf_level_record> r = mesh_adaptive_cycle(M(m), s->st, *mat, *opts);
+    if (n_records) *n_records = int(r.size());
+    for (int i = 0; i < int(r.size()) && i < max_records && records; ++i) records[i] = r[size_t(i)];
   });
 }
 

@@ -64,6 +64,16 @@ struct Constraints {
   DevBuf<std::uint8_t> flag;  // per dof
   DevBuf<double> inhom;       // per dof (phi_old on the active set, 0 elsewhere)
   i64 count = 0;
+  // lines with entries (hanging vertices of a general mesh, closed: every master is unconstrained):
+  // dof line_dof[i] = inhom + sum of line_w * x[line_m] over [line_ptr[i], line_ptr[i+1]), in the
+  // reference's entry order (fem.cpp:229-247)
+  i64 n_lines = 0;
+  DevBuf<int> line_dof;
+  DevBuf<i64> line_ptr;
+  DevBuf<int> line_m;
+  DevBuf<double> line_w;
+  const void* mesh = nullptr;  // the MeshDisc of a general-mesh set (nullptr: uniform grid)
+  std::uint64_t uid = 0;       // identity of a general-mesh set (its assembly plans are cached by it)
 };
 
 // Stencil-implicit columns of the uniform-grid blocks M_uu / M_phiu when the Dirichlet clamp is the
@@ -102,6 +112,8 @@ struct BlockSystem {
 // ---- host helpers implemented in the .cu files
 Problem* make_problem(int d, double K, int n0, int r);
 void build_tables(Problem& P, double mu, double lam);
+void fill_tables(Tables& T, int d, double h, double detJ, double mu, double lam);
+void distribute_lines(const Constraints& c, double* v, bool homogeneous);  // mesh.cu
 std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64 n_active,
                                                const i64* dofs_dev, const double* vals_dev);
 void distribute(const Constraints& c, double* v_dev, bool homogeneous);

@@ -14,6 +14,7 @@
 #include <cstring>
 
 #include "cf_comm.hpp"
+#include "cf_mesh.hpp"
 #include "cf_vec.hpp"
 
 namespace cfb {
@@ -806,6 +807,189 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   std::memcpy(&viol, &bits, sizeof(viol));
   report.feasibility = std::max(0.0, viol);  // solver.cpp:183-186 starts from viol = 0
   allgather_owned(cm, g, x);  // every rank leaves with the full solution
+  return report;
+}
+
+// ------------------------------------------------------------------ general meshes
+namespace {
+__global__ void k_any_diff(i64 n, const double* __restrict__ a, const double* __restrict__ b, int* flag) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && fabs(a[i] - b[i]) > 0.0) *flag = 1;
+}
+}  // namespace
+
+// newton_active_set_step (solver.cpp:49-188) on a general mesh, single GPU.  Same control flow
+// and device kernels as the uniform step; the mesh pieces are the plan-based assembly (base
+// plans, masked by the full set), the constraint lines (conforming phi_tilde, distribute) and the
+// flat segmented reduction order (each block cut into 8192-entry chunks, oracle_mesh.inc SegFlat).
+NewtonReport mesh_newton_step(MeshDisc& m, State& st, const cf_material& mat, const cf_regularization& reg,
+                              const cf_solver_options& opts) {
+  const int d = m.d;
+  const i64 nu = m.n_u(), V = m.V, nt = m.n_total();
+  Slab sl;
+  sl.v_lo = 0;
+  sl.v_hi = V;
+  sl.ve_lo = 0;
+  sl.ve_hi = V;
+  sl.c_lo = 0;
+  sl.c_hi = m.nact;
+  sl.plane = V;
+  const int nw = std::max(1, (opts.cycle_window + 63) / 64);
+  NewtonReport report;
+  PhaseTimes& T = report.times;
+  auto base = mesh_build_constraints(m, true, 0, nullptr, nullptr);  // solver.cpp:55
+  double* x = st.solution.p;
+  distribute(*base, x, false);
+  DevBuf<double> ptfull(nt);  // conforming_phi (solver.cpp:40-47): phi_tilde distributed by the base set
+  ptfull.zero();
+  extrapolate_phi(st, ptfull.p + nu, V);
+  distribute(*base, ptfull.p, false);
+  const double* pt = ptfull.p + nu;
+  const double c = opts.active_set_c_scale * mat.G_c / reg.eps;
+  DevBuf<std::uint8_t> fixed(V), active(V), prev(V), tracked(V);
+  DevBuf<unsigned long long> hist(V * nw);
+  fixed.zero();
+  prev.zero();
+  tracked.zero();
+  hist.zero();
+  DevBuf<int> flags(4);
+  DevBuf<double> R(nt), rhs(nt), delta(nt), xb(nt);
+  int hist_len = 0;
+  double res0 = -1.0;
+  std::unique_ptr<BlockPrec> prec;
+  Constraints full;
+  full.mesh = &m;
+  full.flag.alloc(nt);
+  full.inhom.alloc(nt);
+  CF_CUDA(cudaMemcpyAsync(full.flag.p, base->flag.p, size_t(nt), cudaMemcpyDeviceToDevice, stream()));
+  CF_CUDA(cudaMemcpyAsync(full.inhom.p, base->inhom.p, size_t(nt) * sizeof(double), cudaMemcpyDeviceToDevice,
+                          stream()));
+  DevBuf<double> Bu(nu * (d == 2 ? 3 : 6)), Bp(V);
+  DevBuf<int> unode(nu), pnode(V);
+  const unsigned gv = grid_for(V, 256), gl = grid_for(nt, 256);
+  SegLayout seg;
+  seg.plane_u = nu;
+  seg.plane_p = V;
+  seg.p_lo = 0;
+  seg.p_hi = 1;
+  seg.nplanes = 1;
+  for (int it = 1; it <= opts.newton_max_iter; ++it) {
+    {
+      Timer t(&T.residual);
+      mesh_assemble_residual(m, *base, *base, mat, reg, x, pt, R.p);
+    }
+    int changes = 0, asize = 0;
+    {
+      Timer t(&T.active_set);
+      flags.zero();
+      k_active1<<<gv, 256, 0, stream()>>>(sl, nu, c, 1e-14 * c, x, st.phi_old.p, R.p, base->flag.p, fixed.p,
+                                          active.p, tracked.p, hist.p, nw, flags.p + 2, d);
+      CF_LAUNCHED();
+      if (read_dev(flags.p + 2)) ++hist_len;
+      k_active2<<<gv, 256, 0, stream()>>>(V, hist_len, opts.cycle_window, opts.cycle_toggles, tracked.p, hist.p, nw,
+                                          fixed.p, active.p, prev.p, flags.p);
+      CF_LAUNCHED();
+      int hc[2];
+      CF_CUDA(cudaMemcpyAsync(hc, flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream()));
+      CF_CUDA(cudaStreamSynchronize(stream()));
+      ++host_sync_count();
+      asize = hc[0];
+      changes = hc[1];
+      k_full_constraints<<<gv, 256, 0, stream()>>>(sl, nu, base->flag.p, base->inhom.p, active.p, st.phi_old.p,
+                                                   full.flag.p, full.inhom.p);
+      CF_LAUNCHED();
+      mesh_full_lines(*base, full);
+      CF_CUDA(cudaMemcpyAsync(xb.p, x, size_t(nt) * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
+      distribute(full, x, false);
+      CF_CUDA(cudaMemsetAsync(flags.p + 3, 0, sizeof(int), stream()));
+      k_any_diff<<<gl, 256, 0, stream()>>>(nt, x, xb.p, flags.p + 3);
+      CF_LAUNCHED();
+    }
+    const int moved = read_dev(flags.p + 3);
+    {
+      Timer t(&T.residual);
+      if (moved) {
+        mesh_assemble_residual(m, *base, full, mat, reg, x, pt, R.p);
+      } else {
+        k_zero_active<<<gv, 256, 0, stream()>>>(V, nu, active.p, R.p);
+        CF_LAUNCHED();
+      }
+    }
+    const double res = gnorm(nullptr, R.p, seg);
+    if (res0 < 0.0) res0 = res;
+    NewtonIter rec{res, asize, changes, 0};
+    const bool small = res <= std::max(opts.newton_tol * res0, opts.newton_abs_floor);
+    if (changes == 0 && small) {
+      report.its.push_back(rec);
+      if (opts.log)
+        std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=0\n", st.step, it, res, asize,
+                    changes);
+      report.converged = true;
+      break;
+    }
+    std::unique_ptr<BlockSystem> J;
+    {
+      Timer t(&T.jacobian);
+      J = mesh_assemble_jacobian(m, *base, full, mat, reg, x, pt);
+    }
+    if (!prec || !opts.freeze_preconditioner) {
+      Timer t(&T.amg_setup);
+      NullspaceDev ns;
+      mesh_rigid_body_modes(m, full, Bu.p);
+      k_phi_modes<<<gv, 256, 0, stream()>>>(sl, nu, full.flag.p, Bp.p, pnode.p, unode.p, d);
+      CF_LAUNCHED();
+      ns.u_node = unode.p;
+      ns.u_modes = Bu.p;
+      ns.m_u = d == 2 ? 3 : 6;
+      ns.p_node = pnode.p;
+      ns.p_modes = Bp.p;
+      prec = build_block_prec(*J, opts.prec_kind, opts.amg, &ns, prec.get());
+    }
+    GmresResult lin;
+    {
+      Timer t(&T.gmres);
+      k_neg<<<gl, 256, 0, stream()>>>(nt, R.p, rhs.p);
+      CF_LAUNCHED();
+      const BlockSystem& Jr = *J;
+      DevOp op = [&Jr](const double* in, double* out) { block_apply(Jr, in, out); };
+      const BlockPrec& Pr = *prec;
+      DevOp pop = [&Pr](const double* in, double* out) { Pr.apply(in, out); };
+      lin = gmres(op, &pop, rhs.p, nt, opts.gmres, delta.p, nullptr, &seg);
+    }
+    if (!lin.converged && !lin.breakdown) fail(CF_ERR_NUMERICAL, "newton_active_set_step: GMRES stagnated at max_iter");
+    rec.gmres_iterations = lin.iterations;
+    report.its.push_back(rec);
+    if (opts.log)
+      std::printf("newton step=%d it=%d res=%.6e active=%d changed=%d gmres=%d\n", st.step, it, res, asize, changes,
+                  lin.iterations);
+    distribute(full, delta.p, true);
+    vaxpy(1.0, delta.p, x, nt);
+    if (opts.damping) {
+      double scale = 1.0;
+      for (int half = 0; half < 4; ++half) {
+        mesh_assemble_residual(m, *base, full, mat, reg, x, pt, R.p);
+        if (gnorm(nullptr, R.p, seg) <= 10.0 * res) break;
+        scale *= 0.5;
+        vaxpy(-scale, delta.p, x, nt);
+      }
+    }
+    CF_CUDA(cudaMemcpyAsync(prev.p, active.p, size_t(V), cudaMemcpyDeviceToDevice, stream()));
+  }
+  DevBuf<double> mx(1);
+  {
+    const long long lowest = 0x8000000000000000LL;
+    CF_CUDA(cudaMemcpyAsync(mx.p, &lowest, sizeof(lowest), cudaMemcpyHostToDevice, stream()));
+  }
+  k_feas<<<gv, 256, 0, stream()>>>(sl, nu, x, st.phi_old.p, mx.p);
+  CF_LAUNCHED();
+  long long bits = 0;
+  CF_CUDA(cudaMemcpyAsync(&bits, mx.p, sizeof(bits), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
+  bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
+  double viol;
+  std::memcpy(&viol, &bits, sizeof(viol));
+  report.feasibility = std::max(0.0, viol);
   return report;
 }
 
