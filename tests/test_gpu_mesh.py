@@ -18,7 +18,7 @@ def cm():
     return m
 
 
-def twin(orc, cm, d, K, n0, rounds, seed, frac=3):
+def twin(orc, cm, d, K, n0, rounds, seed, frac):
     """The same refinement sequence on the device mesh and on the oracle mesh."""
     M = cm.create_mesh(d, K, n0)
     O = orc.Mesh(d, K, n0)
@@ -39,12 +39,15 @@ def rand_state(M, rng, phi_lo=0.0):
     return x
 
 
-CASES = [(2, 1.0, 2, 3, 11), (2, 5.0, 4, 3, 12), (3, 1.0, 2, 2, 13)]
+# (d, K, n0, rounds, seed, frac): random refinement sequences (each active cell marked with
+# probability 1/frac per round); the 3d seed-0 case has chained hanging lines (a vertex hanging on a
+# hanging vertex across a 2-level edge jump: closed weights 1/8, 3/8, 3/4, five masters)
+CASES = [(2, 1.0, 2, 3, 11, 3), (2, 5.0, 4, 4, 12, 3), (3, 1.0, 2, 2, 13, 3), (3, 1.0, 2, 3, 0, 4)]
 
 
-@pytest.mark.parametrize("d,K,n0,rounds,seed", CASES)
-def test_mesh_topology(orc, cm, d, K, n0, rounds, seed):
-    M, O = twin(orc, cm, d, K, n0, rounds, seed)
+@pytest.mark.parametrize("d,K,n0,rounds,seed,frac", CASES)
+def test_mesh_topology(orc, cm, d, K, n0, rounds, seed, frac):
+    M, O = twin(orc, cm, d, K, n0, rounds, seed, frac)
     assert (M.n_cells, M.n_active, M.max_level, M.n_vertices) == (O.n_cells, O.n_active, O.max_level, O.V)
     c1, c2 = M.cells(), O.cells()
     for k in ("level", "parent", "active", "anchor"):
@@ -58,10 +61,10 @@ def test_mesh_topology(orc, cm, d, K, n0, rounds, seed):
         assert M.find_active_cell(x[:d]) == O.find_cell(x[:d])
 
 
-@pytest.mark.parametrize("d,K,n0,rounds,seed", CASES)
+@pytest.mark.parametrize("d,K,n0,rounds,seed,frac", CASES)
 @pytest.mark.parametrize("clamp", [True, False])
-def test_constraint_lines_and_distribute(orc, cm, d, K, n0, rounds, seed, clamp):
-    M, O = twin(orc, cm, d, K, n0, rounds, seed)
+def test_constraint_lines_and_distribute(orc, cm, d, K, n0, rounds, seed, frac, clamp):
+    M, O = twin(orc, cm, d, K, n0, rounds, seed, frac)
     rng = np.random.default_rng(seed + 1)
     act = sorted(set(int(v) for v in rng.integers(0, M.n_vertices, M.n_vertices // 6)))
     adofs = [M.n_u + v for v in act]
@@ -84,10 +87,10 @@ def test_constraint_lines_and_distribute(orc, cm, d, K, n0, rounds, seed, clamp)
     assert np.array_equal(dc.distribute_homogeneous(v.copy()), oc.distribute(v, homogeneous=True))
 
 
-@pytest.mark.parametrize("d,K,n0,rounds,seed", CASES)
-def test_assembly_bitwise(orc, cm, d, K, n0, rounds, seed):
+@pytest.mark.parametrize("d,K,n0,rounds,seed,frac", CASES)
+def test_assembly_bitwise(orc, cm, d, K, n0, rounds, seed, frac):
     import paper_1806_09924_b200 as cf
-    M, O = twin(orc, cm, d, K, n0, rounds, seed)
+    M, O = twin(orc, cm, d, K, n0, rounds, seed, frac)
     rng = np.random.default_rng(seed + 2)
     x = rand_state(M, rng)
     pt = rng.uniform(0, 1, M.n_vertices)
@@ -131,7 +134,7 @@ def sneddon_twin(orc, cm, d, K, n0, r, extra):
     return M, O
 
 
-@pytest.mark.parametrize("d,K,n0,r,extra", [(2, 5.0, 10, 0, 2), (3, 4.0, 4, 1, 1)])
+@pytest.mark.parametrize("d,K,n0,r,extra", [(2, 5.0, 10, 0, 2), (3, 4.0, 4, 1, 1), (2, 10.0, 8, 3, 3)])
 def test_newton_step_bitwise(orc, cm, d, K, n0, r, extra):
     import paper_1806_09924_b200 as cf
     M, O = sneddon_twin(orc, cm, d, K, n0, r, extra)
@@ -160,9 +163,9 @@ def test_newton_step_bitwise(orc, cm, d, K, n0, r, extra):
     assert np.allclose(cm.compute_cod(M, got, stations), O.cod(sol, stations), rtol=1e-12, atol=1e-18)
 
 
-@pytest.mark.parametrize("d,K,n0,rounds,seed", CASES)
-def test_estimator_marking_transfer_bitwise(orc, cm, d, K, n0, rounds, seed):
-    M, O = twin(orc, cm, d, K, n0, rounds, seed)
+@pytest.mark.parametrize("d,K,n0,rounds,seed,frac", CASES)
+def test_estimator_marking_transfer_bitwise(orc, cm, d, K, n0, rounds, seed, frac):
+    M, O = twin(orc, cm, d, K, n0, rounds, seed, frac)
     rng = np.random.default_rng(seed + 3)
     x = rand_state(M, rng)
     x = O.constraints(True).distribute(x)
@@ -199,3 +202,14 @@ def test_adaptive_cycle_matches_oracle(orc, cm):
         assert r["tcv"] == pytest.approx(o[4], rel=1e-12)
     assert M.n_total == O.n_total
     assert np.array_equal(st.get()["solution"], osol)
+
+
+def test_chained_lines_present(orc):
+    """The seed-0 3d case really has chained hanging lines (so the closure is exercised)."""
+    O = orc.Mesh(3, 1.0, 2)
+    rng = np.random.default_rng(0)
+    for _ in range(3):
+        act = O.active()
+        O.refine([int(c) for c in act if rng.integers(4) == 0] or [int(act[0])])
+    dd, p, m, w, inh = O.constraints(False).lines()
+    assert {0.125, 0.375}.issubset(set(w.tolist())) and max(p[1:] - p[:-1]) > 4
