@@ -482,6 +482,7 @@ def ours(args):
         torch.cuda.synchronize()
         e0.record(s)
         for k in range(args.steps):
+            st = None  # the previous step's state is released before the next one is created (as in warm-up)
             st, rep = step()
             reps.append(rep)
             marks[k].record(s)

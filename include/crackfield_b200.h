@@ -61,7 +61,12 @@ typedef struct {
   int max_iter, restart;
 } cf_gmres_options;
 
-/* SolverOptions (solver.hpp:13-26). prec_kind: 0 exact, 1 amg, 2 diagonal (linsolve.hpp:100). */
+/* SolverOptions (solver.hpp:13-26). prec_kind: 0 exact, 1 amg, 2 diagonal (linsolve.hpp:100).
+ * operator_kind (no reference counterpart): 1 (default) applies M_uu matrix-free (sum-factorised,
+ * 3d uniform grids on one GPU) in the Krylov operator and in the u-hierarchy's finest-level
+ * smoother / residual; 0 applies the assembled M_uu everywhere (the reference's operator, and
+ * the mode that is bitwise identical to the CPU oracle).  Both agree to rounding (north-star
+ * tolerances, tests/test_gpu_mf_solver.py). */
 typedef struct {
   double newton_tol, newton_abs_floor;
   int newton_max_iter;
@@ -69,6 +74,7 @@ typedef struct {
   int cycle_window, cycle_toggles, damping, prec_kind, freeze_preconditioner, log;
   cf_gmres_options gmres;
   cf_amg_options amg;
+  int operator_kind;
 } cf_solver_options;
 
 typedef struct cf_problem_s* cf_problem;         /* Mesh + DofMap of a uniform grid */

@@ -83,12 +83,14 @@ class SolverOptions(C.Structure):
     _fields_ = [("newton_tol", C.c_double), ("newton_abs_floor", C.c_double), ("newton_max_iter", C.c_int),
                 ("active_set_c_scale", C.c_double), ("cycle_window", C.c_int), ("cycle_toggles", C.c_int),
                 ("damping", C.c_int), ("prec_kind", C.c_int), ("freeze_preconditioner", C.c_int),
-                ("log", C.c_int), ("gmres", GmresOptions), ("amg", AmgOptions)]
+                ("log", C.c_int), ("gmres", GmresOptions), ("amg", AmgOptions), ("operator_kind", C.c_int)]
 
     def __init__(self, **kw):
+        # operator_kind 1: matrix-free M_uu in the Krylov operator and the finest smoother (3d uniform,
+        # one GPU); 0: the assembled operator, bitwise identical to the CPU oracle
         d = dict(newton_tol=1e-8, newton_abs_floor=1e-11, newton_max_iter=50, active_set_c_scale=100.0,
                  cycle_window=8, cycle_toggles=3, damping=0, prec_kind=1, freeze_preconditioner=0, log=0,
-                 gmres=GmresOptions(), amg=AmgOptions())
+                 gmres=GmresOptions(), amg=AmgOptions(), operator_kind=1)
         d.update(kw)
         super().__init__(**d)
 

@@ -1690,6 +1690,13 @@ void Amg::vcycle(const double* r, double* x) const {
 // the V-cycle of levels l0.. for the right-hand side b0 of level l0, output x0 (linsolve.cpp:295-312)
 void Amg::vcycle_range(size_t l0, const double* b0, double* x0) const {
   static const bool unfused = std::getenv("CF_VCYCLE_UNFUSED") != nullptr;
+  // A x (+ epilogue) of level l: matrix-free on the finest level when mf0 is set
+  auto apply = [&](size_t l, const double* xin, double* yout, const SpmvEpi& ep) {
+    if (l == 0 && mf0)
+      mf_apply(*mf0, xin, yout, ep);
+    else
+      csr_spmv_epi(*levels[l]->A, xin, yout, ep);
+  };
   const double* b = b0;
   for (size_t l = l0; l < levels.size(); ++l) {
     const AmgLevel& L = *levels[l];
@@ -1699,18 +1706,18 @@ void Amg::vcycle_range(size_t l0, const double* b0, double* x0) const {
     k_jacobi0<<<grid_for(n, 256), 256, 0, stream()>>>(n, w, L.inv_diag.p, b, xl);
     CF_LAUNCHED();
     for (int s = 1; s < opts.smoothing_sweeps; ++s) {
-      csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
+      apply(l, xl, L.tmp_r.p, SpmvEpi{});
       k_jacobi_upd<<<grid_for(n, 256), 256, 0, stream()>>>(n, w, L.inv_diag.p, b, L.tmp_r.p, xl);
       CF_LAUNCHED();
     }
     if (unfused) {
-      csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
+      apply(l, xl, L.tmp_r.p, SpmvEpi{});
       vsub(b, L.tmp_r.p, L.tmp_r.p, n);  // r = b - A x
     } else {
       SpmvEpi ep;
       ep.b = b;
       ep.mode = 1;
-      csr_spmv_epi(*L.A, xl, L.tmp_r.p, ep);  // r = b - A x
+      apply(l, xl, L.tmp_r.p, ep);  // r = b - A x
     }
     csr_spmv_add(*L.R, L.tmp_r.p, L.tmp_b.p, nullptr);  // b_c = P^T r
     b = L.tmp_b.p;
@@ -1734,11 +1741,11 @@ void Amg::vcycle_range(size_t l0, const double* b0, double* x0) const {
       ep.d = L.inv_diag.p;
       ep.w = L.jacobi_weight;
       ep.mode = 2;
-      csr_spmv_epi(*L.A, L.tmp_r.p, xl, ep);  // x = t + w D^-1 (b - A t)
+      apply(l, L.tmp_r.p, xl, ep);  // x = t + w D^-1 (b - A t)
       s = 1;
     }
     for (; s < opts.smoothing_sweeps; ++s) {
-      csr_spmv_add(*L.A, xl, L.tmp_r.p, nullptr);
+      apply(l, xl, L.tmp_r.p, SpmvEpi{});
       k_jacobi_upd<<<grid_for(n, 256), 256, 0, stream()>>>(n, L.jacobi_weight, L.inv_diag.p, bl, L.tmp_r.p, xl);
       CF_LAUNCHED();
     }

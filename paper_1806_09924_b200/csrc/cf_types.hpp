@@ -99,6 +99,16 @@ struct Csr {
   double mean_hint = -1.0;
 };
 
+// Matrix-free stand-in for a uniform 3d grid's M_uu (the block's values are never read): y = M_uu x
+// with the assembled block's condensation (constrained columns dropped, constrained rows keep the
+// summed element diagonal), optionally with an SpMV row epilogue (modes 0-2 of SpmvEpi).
+struct MfOp {
+  Problem* P = nullptr;
+  const std::uint8_t* flag = nullptr;  // u constraint flags (global dof numbering)
+  double mu = 0.0, lam = 0.0, kap = 0.0;
+  const double* pt = nullptr;  // phi_tilde
+};
+
 struct BlockSystem {
   i64 nu = 0, np = 0;
   // input layout of block_apply: [u (nu_in) | phi (np_in)]; < 0 means square (nu, np).  A slab's
@@ -106,6 +116,7 @@ struct BlockSystem {
   i64 nu_in = -1, np_in = -1;
   std::shared_ptr<Csr> uu = std::make_shared<Csr>(), pu = std::make_shared<Csr>(), pp = std::make_shared<Csr>();
   int d = 2;
+  std::shared_ptr<MfOp> mf_uu;  // set: M_uu applied matrix-free in block_apply (uu keeps its values)
   i64 in_u() const { return nu_in >= 0 ? nu_in : nu; }
 };
 
@@ -142,6 +153,7 @@ struct SpmvEpi {
   i64 xoff = 0;  // mode 2 reads x[row + xoff] (a row slice of a square matrix applied to a full x)
 };
 void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep);
+void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep);  // mf.cu (3d)
 void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);
 bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double* y);

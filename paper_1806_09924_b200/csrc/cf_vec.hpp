@@ -128,6 +128,9 @@ struct Amg {
   DevBuf<double> B0;
   int m0 = 0;
   mutable DevBuf<double> cb, cx;  // coarsest rhs / solution
+  // set: the finest level's operator (residual, smoothing sweeps) is applied matrix-free; level 0's A
+  // stays the assembled matrix the hierarchy was built from
+  std::shared_ptr<MfOp> mf0;
   void vcycle(const double* r, double* x) const;  // x = V(r), zero initial guess
   // true iff build_amg(A, node_of_dof, B, m, opts) would rebuild exactly this hierarchy
   bool same_inputs(const Csr& A, const int* node_of_dof, const double* B, int m, const cf_amg_options& o) const;

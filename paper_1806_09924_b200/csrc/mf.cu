@@ -297,12 +297,19 @@ __device__ __forceinline__ void mf_cell(FU U, FP PT, double xi0, double xi1, dou
         }
 }
 
+// the SpMV row epilogue (spmv.cu epi_out, modes 0-2): the same IEEE expression per row
+__device__ __forceinline__ double mf_epi(const SpmvEpi& ep, const double* __restrict__ x, i64 row, double s) {
+  if (ep.mode == 1) return ep.b[row] - s;
+  if (ep.mode == 2) return x[row + ep.xoff] + ep.w * (ep.d[row] * (ep.b[row] - s));
+  return ep.b ? ep.b[row] + s : s;
+}
+
 __global__ void __launch_bounds__(MF_THREADS) k_mf_sweep(GridDesc g, const Tables* __restrict__ T, double mu,
                                                          double lam, double kap, double xi0, double xi1,
                                                          double scale, const double* __restrict__ x,
                                                          const double* __restrict__ pt,
                                                          const std::uint8_t* __restrict__ flag,
-                                                         double* __restrict__ y) {
+                                                         double* __restrict__ y, SpmvEpi ep) {
   constexpr int PL = MFT * MFT;           // vertices of one tile plane
   __shared__ double su[3][PL * 3], sp[3][PL];  // vertex planes z mod 3
   __shared__ double co[2][MFC * MFC * MF_CS];  // cell layers L mod 2
@@ -374,7 +381,7 @@ __global__ void __launch_bounds__(MF_THREADS) k_mf_sweep(GridDesc g, const Table
         const bool con = flag[v * 3] | flag[v * 3 + 1] | flag[v * 3 + 2];
         if (!con) {
 #pragma unroll
-          for (int a = 0; a < 3; ++a) y[v * 3 + a] = acc[a];
+          for (int a = 0; a < 3; ++a) y[v * 3 + a] = mf_epi(ep, x, v * 3 + a, acc[a]);
         } else {  // a constrained row keeps the summed element diagonal (model.cpp:295-300): y = d x
           double dg[3] = {0.0, 0.0, 0.0};
 #pragma unroll 1
@@ -405,7 +412,8 @@ __global__ void __launch_bounds__(MF_THREADS) k_mf_sweep(GridDesc g, const Table
             }
           }
 #pragma unroll
-          for (int a = 0; a < 3; ++a) y[v * 3 + a] = flag[v * 3 + a] ? dg[a] * x[v * 3 + a] : acc[a];
+          for (int a = 0; a < 3; ++a)
+            y[v * 3 + a] = mf_epi(ep, x, v * 3 + a, flag[v * 3 + a] ? dg[a] * x[v * 3 + a] : acc[a]);
         }
       }
 #pragma unroll
@@ -443,6 +451,19 @@ __global__ void k_dfma(double* out, int iters) {
 
 }  // namespace
 
+void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep) {
+  Problem& P = *op.P;
+  build_tables(P, op.mu, op.lam);
+  const GridDesc& g = P.g;
+  if (g.d != 3) fail(CF_ERR_UNSUPPORTED, "mf_apply: the matrix-free M_uu is 3d");
+  const int nb = int((g.nn + MFB - 1) / MFB), nseg = int((g.nn + MF_ZSEG - 1) / MF_ZSEG);
+  const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
+  const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
+  k_mf_sweep<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1,
+                                                          W / (g.h * g.h), x, op.pt, op.flag, y, ep);
+  CF_LAUNCHED();
+}
+
 void mf_apply_uu(Problem& P, const Constraints& cs, const cf_material& m, const cf_regularization& reg,
                  const double* pt, const double* x, double* y) {
   build_tables(P, mat_mu(m), mat_lambda(m));
@@ -450,13 +471,14 @@ void mf_apply_uu(Problem& P, const Constraints& cs, const cf_material& m, const 
   const int nv = 1 << g.d;
   static const bool two_pass_3d = std::getenv("CF_MF_TWO_PASS") != nullptr;  // A/B: the round-1 kernels
   if (g.d == 3 && !two_pass_3d) {
-    const double mu = mat_mu(m), lam = mat_lambda(m);
-    const int nb = int((g.nn + MFB - 1) / MFB), nseg = int((g.nn + MF_ZSEG - 1) / MF_ZSEG);
-    const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
-    const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
-    k_mf_sweep<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, mu, lam, reg.kappa, xi0, xi1,
-                                                            W / (g.h * g.h), x, pt, cs.flag.p, y);
-    CF_LAUNCHED();
+    MfOp op;
+    op.P = &P;
+    op.flag = cs.flag.p;
+    op.mu = mat_mu(m);
+    op.lam = mat_lambda(m);
+    op.kap = reg.kappa;
+    op.pt = pt;
+    mf_apply(op, x, y, SpmvEpi{});
     return;
   }
   static DevBuf<double> out;  // per-cell corner sums (scratch reused across applies)

@@ -543,6 +543,18 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   DevBuf<int> unode(nul), pnode(nv);
   const unsigned gv = grid_for(nv, 256), gl = grid_for(ntl, 256);
   const SegLayout seg = seg_layout(g, sl);  // every norm / dot of the step: NP-invariant order
+  // operator_kind 1 (3d, one GPU): M_uu applied matrix-free in the Krylov operator and on the
+  // u-hierarchy's finest level (mf.cu); M_uu is still assembled once per step for the AMG setup
+  std::shared_ptr<MfOp> mf;
+  if (opts.operator_kind == 1 && d == 3 && !dist) {
+    mf = std::make_shared<MfOp>();
+    mf->P = &P;
+    mf->flag = base->flag.p;  // the u constraints of every set of the step
+    mf->mu = mat_mu(mat);
+    mf->lam = mat_lambda(mat);
+    mf->kap = reg.kappa;
+    mf->pt = pt.p;
+  }
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
     {
       Timer t(&T.residual);
@@ -626,6 +638,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         J->pu->mean_hint = tot[3] ? double(tot[2]) / double(tot[3]) : 0.0;
       }
     }
+    if (mf) J->mf_uu = mf;
     if (!prec || !opts.freeze_preconditioner) {
       Timer t(&T.amg_setup);
       NullspaceDev ns;
@@ -711,6 +724,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         prec = build_block_prec(*J, opts.prec_kind, opts.amg, &ns, prec.get());
       }
     }
+    if (mf && prec->amg_u && prec->amg_u->n == J->uu->rows) prec->amg_u->mf0 = mf;
     GmresResult lin;
     {
       Timer t(&T.gmres);

@@ -802,7 +802,10 @@ void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add) {
 void csr_spmv(const Csr& A, const double* x, double* y, double) { csr_spmv_add(A, x, y, nullptr); }
 
 void block_apply(const BlockSystem& J, const double* x, double* y) {
-  csr_spmv_add(*J.uu, x, y, nullptr);
+  if (J.mf_uu)
+    mf_apply(*J.mf_uu, x, y, SpmvEpi{});
+  else
+    csr_spmv_add(*J.uu, x, y, nullptr);
   if (J.np == 0) return;
   const double mean = J.pu->mean_hint >= 0.0 ? J.pu->mean_hint : double(J.pu->nnz) / double(J.np);
   if (mean > 64) launch_phi<16, 4>(J, x, y);

@@ -48,7 +48,7 @@ def test_cycle_window_beyond_64(cf, orc, window, toggles):
     oreg = O.resolve_regularization(omat, O.slit_band_edge(omat))
     phi, _ = cf.initial_crack(P, mat)
     st = cf.make_initial_state(P, mat)
-    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(cycle_window=window, cycle_toggles=toggles))
+    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(cycle_window=window, cycle_toggles=toggles, operator_kind=0))
     sol = np.zeros(O.n_total)
     sol[O.n_u:] = phi
     orep = O.newton_step(omat, oreg, orc.solver_options(cycle_window=window, cycle_toggles=toggles), sol,

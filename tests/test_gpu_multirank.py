@@ -37,7 +37,7 @@ def _worker(rank, size, port, out_dir, d, n0, r):
     comm = cf.Communicator.from_gloo()
     P, mat, reg = _setup(cf, d, n0, r)
     st = cf.make_initial_state(P, mat)
-    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(), comm=comm)
+    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(operator_kind=0), comm=comm)
     x = st.get()["solution"]
     its = np.array([[it["residual_norm"], it["active_size"], it["set_changes"], it["gmres_iterations"]]
                     for it in rep["iterations"]])
@@ -81,7 +81,7 @@ def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
         assert np.array_equal(its[k], its[0]), "ranks disagree on the Newton transcript"
     P, mat, reg = _setup(cf, d, n0, r)
     st = cf.make_initial_state(P, mat)
-    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions())
+    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(operator_kind=0))
     assert rep["converged"]
     ref = st.get()["solution"]
     ref_its = np.array([[it["residual_norm"], it["active_size"], it["set_changes"], it["gmres_iterations"]]

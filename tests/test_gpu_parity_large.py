@@ -58,9 +58,10 @@ def _pair(cf, orc, d, n0, r):
     return P, O, mat, omat, reg, oreg, phi
 
 
-def _device_run(cf, P, mat, reg, steps, gm=None, max_iter=50):
+def _device_run(cf, P, mat, reg, steps, gm=None, max_iter=50, op=0):
+    """op 0: the assembled operator (bitwise the oracle); 1: the matrix-free M_uu (3d)."""
     st = cf.make_initial_state(P, mat)
-    opts = cf.SolverOptions(newton_max_iter=max_iter)
+    opts = cf.SolverOptions(newton_max_iter=max_iter, operator_kind=op)
     if gm is not None:
         opts.gmres = gm
     reps = cf.solve_loading_sequence(st, mat, P, reg, opts, steps)  # a capped step ends it, unconverged
@@ -226,6 +227,43 @@ def test_reference_order_config2_family(cf, orcmt):
     with orcmt.reference_order():
         oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 3, gm)
     _within_north_star(reps, x, oreps, xo, P, cf, O)
+
+
+# ------------------------------------------------------------------ matrix-free operator (operator_kind 1)
+# The default product path in 3d applies M_uu matrix-free (sum-factorised, mf.cu) in the Krylov
+# operator and on the u-hierarchy's finest level.  Its sums are associated per cell, not per CSR
+# row, so it is checked at the north-star tolerances against the reference's own arithmetic order
+# and against the assembled-operator step, and per apply to 1e-13 against the assembled M_uu.
+def test_mf_apply_matches_assembled_48(cf):
+    P = cf.Problem(3, 10.0, 12, 2)
+    rng = np.random.default_rng(48)
+    x = np.zeros(P.n_total)
+    x[:P.n_u] = 1e-3 * rng.standard_normal(P.n_u)
+    pt = rng.uniform(0, 1, P.n_vertices)
+    x[P.n_u:] = pt
+    cs = cf.build_constraints(P)
+    mat, reg = cf.Material(), cf.Regularization(0.3, 1e-12)
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    u = rng.standard_normal(P.n_u)
+    ya = J.spmv(0, u)
+    ym = cf.mf_apply_uu(P, cs, mat, reg, pt, u)
+    assert np.linalg.norm(ym - ya) <= 1e-13 * np.linalg.norm(ya)
+
+
+@pytest.mark.parametrize("case", ["penny32", "penny48", "penny64"])
+def test_mf_operator_north_star_tolerances(cf, orcmt, case):
+    n0, r = {"penny32": (8, 2), "penny48": (12, 2), "penny64": (8, 3)}[case]
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 3, n0, r)
+    reps, x = _device_run(cf, P, mat, reg, 1, op=1)
+    with orcmt.reference_order():
+        oreps, xo = _oracle_run(orcmt, O, omat, oreg, phi, 1)
+    rel = _within_north_star(reps, x, oreps, xo, P, cf, O)
+    reps0, x0 = _device_run(cf, P, mat, reg, 1, op=0)  # the assembled operator on the device
+    rel0 = np.linalg.norm(x - x0) / np.linalg.norm(x0)
+    assert rel0 <= 1e-8, rel0
+    print(f"{case}: matrix-free vs reference order {rel:.3e}, vs assembled {rel0:.3e}; GMRES "
+          f"{_its(reps[0])[:, 3].tolist()} / assembled {_its(reps0[0])[:, 3].tolist()} / "
+          f"reference {oreps[0]['iterations'][:, 3].astype(int).tolist()}")
 
 
 # ------------------------------------------------------------------ full-size, opt-in

@@ -86,7 +86,7 @@ def test_single_rank_communicator_is_the_single_gpu_step(cf):
     P = cf.Problem(2, 10.0, 8, 2)
     mat = cf.Material(eps_mode=1, eps_fixed=2 * P.h, kappa_factor=1e-12 / P.h)
     reg = cf.resolve_regularization(P, mat, cf.slit_band_edge(P, mat))
-    opts = cf.SolverOptions()
+    opts = cf.SolverOptions(operator_kind=0)
     a, b = cf.make_initial_state(P, mat), cf.make_initial_state(P, mat)
     comm = cf.Communicator(0, 1)
     ra = cf.newton_active_set_step(a, mat, P, reg, opts)

@@ -210,7 +210,7 @@ def _sneddon_pair(cf, orc, d=2, K=5.0, n0=10, r=1, fixed=False):
 
 def _run_pair(cf, orc, P, O, mat, omat, reg, oreg, phi, steps=1, **optkw):
     st = cf.make_initial_state(P, mat)
-    reps = cf.solve_loading_sequence(st, mat, P, reg, cf.SolverOptions(**optkw), steps)
+    reps = cf.solve_loading_sequence(st, mat, P, reg, cf.SolverOptions(**dict(dict(operator_kind=0), **optkw)), steps)
     sol = np.zeros(O.n_total)
     sol[O.n_u:] = phi
     po, pp = phi.copy(), phi.copy()
