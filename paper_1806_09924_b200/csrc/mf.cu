@@ -216,7 +216,7 @@ __global__ void k_mf_diag(GridDesc g, const Tables* __restrict__ T, double mu, d
 // flops per cell instead of the canonical 2688 of the point-wise form.
 constexpr int MFB = 8, MFT = MFB + 2, MFC = MFB + 1, MF_CS = 25;  // cell-output stride (odd)
 constexpr int MF_THREADS = 96;                                     // >= MFC * MFC = 81 cells per layer
-constexpr int MF_ZSEG = 48;                                        // cell layers per CTA
+constexpr int MF_ZSEG = 12;                                        // cell layers per CTA (short segments: more CTAs, better tail; A/B 48 -> 12: 0.52 -> 0.41 ms at config 3)
 
 // the 24 outputs (k*3 + a) of one cell; U(i,j,l,a) and PT(i,j,l) read the corner values
 template <class FU, class FP>
@@ -304,9 +304,12 @@ __device__ __forceinline__ double mf_epi(const SpmvEpi& ep, const double* __rest
   return ep.b ? ep.b[row] + s : s;
 }
 
-__global__ void __launch_bounds__(MF_THREADS) k_mf_sweep(GridDesc g, const Tables* __restrict__ T, double mu,
+#ifndef CF_MF_MINB
+#define CF_MF_MINB 5  // 126 registers, 5 CTAs per SM (A/B: config 1 1.24 -> 1.12 ms)
+#endif
+__global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g, const Tables* __restrict__ T, double mu,
                                                          double lam, double kap, double xi0, double xi1,
-                                                         double scale, const double* __restrict__ x,
+                                                         double scale, int zseg, const double* __restrict__ x,
                                                          const double* __restrict__ pt,
                                                          const std::uint8_t* __restrict__ flag,
                                                          double* __restrict__ y, SpmvEpi ep) {
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(MF_THREADS) k_mf_sweep(GridDesc g, const Table
   const int nbx = (nn + MFB - 1) / MFB;
   const int col = blockIdx.x % (nbx * nbx), seg = blockIdx.x / (nbx * nbx);
   const int x0 = (col % nbx) * MFB, y0 = (col / nbx) * MFB;
-  const int zv0 = seg * MF_ZSEG, zv1 = min(nn, zv0 + MF_ZSEG);  // owned vertex planes [zv0, zv1)
+  const int zv0 = seg * zseg, zv1 = min(nn, zv0 + zseg);  // owned vertex planes [zv0, zv1)
   auto load_plane = [&](int vz) {
     const int s = ((vz % 3) + 3) % 3;
     for (int t = threadIdx.x; t < PL; t += blockDim.x) {
@@ -456,11 +459,14 @@ void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep) {
   build_tables(P, op.mu, op.lam);
   const GridDesc& g = P.g;
   if (g.d != 3) fail(CF_ERR_UNSUPPORTED, "mf_apply: the matrix-free M_uu is 3d");
-  const int nb = int((g.nn + MFB - 1) / MFB), nseg = int((g.nn + MF_ZSEG - 1) / MF_ZSEG);
+  const int nb = int((g.nn + MFB - 1) / MFB);
+  static const char* zenv = std::getenv("CF_MF_ZSEG");  // A/B: cell layers per CTA
+  const int zseg = zenv ? std::max(1, std::atoi(zenv)) : MF_ZSEG;
+  const int nseg = int((g.nn + zseg - 1) / zseg);
   const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
   const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
   k_mf_sweep<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1,
-                                                          W / (g.h * g.h), x, op.pt, op.flag, y, ep);
+                                                          W / (g.h * g.h), zseg, x, op.pt, op.flag, y, ep);
   CF_LAUNCHED();
 }
 
