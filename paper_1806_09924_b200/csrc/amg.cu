@@ -1791,6 +1791,20 @@ void Amg::distribute(const Comm* cm, i64 min_rows) {
 }
 
 void Amg::vcycle_dist(const double* r, double* x) const {
+  // own rows of level l's A (x global): matrix-free on the finest level when mf0 is set (the rows
+  // of the vertices [lo/d, hi/d), bitwise the rows of the undivided matrix-free apply)
+  auto dist_apply = [&](size_t l, const DistLevel& D, const double* xin, double* yout, const SpmvEpi& ep) {
+    if (l == 0 && mf0) {
+      MfOp op = *mf0;
+      const i64 dd = mf0->P->g.d;
+      op.x_off = 0;
+      op.y_lo = D.lo / dd;
+      op.y_hi = D.hi / dd;
+      mf_apply(op, xin, yout, ep);
+    } else {
+      csr_spmv_epi(*D.A, xin, yout, ep);
+    }
+  };
   const size_t nd = dist.size();
   const double* b = r;
   for (size_t l = 0; l < nd; ++l) {  // down: pre-smooth (redundant), own residual rows, own R rows
@@ -1802,7 +1816,7 @@ void Amg::vcycle_dist(const double* r, double* x) const {
     SpmvEpi ep;
     ep.b = b + D.lo;
     ep.mode = 1;
-    if (D.hi > D.lo) csr_spmv_epi(*D.A, D.x.p, D.r.p + D.lo, ep);  // r = b - A x (own rows)
+    if (D.hi > D.lo) dist_apply(l, D, D.x.p, D.r.p + D.lo, ep);  // r = b - A x (own rows)
     comm->allgather_inplace(D.r.p, D.chunk);
     if (D.chi > D.clo) csr_spmv_add(*D.R, D.r.p, D.bc.p + D.clo, nullptr);  // b_c = P^T r (own rows)
     comm->allgather_inplace(D.bc.p, D.cchunk);
@@ -1824,7 +1838,7 @@ void Amg::vcycle_dist(const double* r, double* x) const {
     ep.w = L.jacobi_weight;
     ep.mode = 2;
     ep.xoff = D.lo;
-    if (D.hi > D.lo) csr_spmv_epi(*D.A, D.r.p, D.x.p + D.lo, ep);
+    if (D.hi > D.lo) dist_apply(l, D, D.r.p, D.x.p + D.lo, ep);
     comm->allgather_inplace(D.x.p, D.chunk);
   }
   vcopy(x, dist[0].x.p, levels[0]->A->rows);

@@ -106,7 +106,10 @@ struct MfOp {
   Problem* P = nullptr;
   const std::uint8_t* flag = nullptr;  // u constraint flags (global dof numbering)
   double mu = 0.0, lam = 0.0, kap = 0.0;
-  const double* pt = nullptr;  // phi_tilde
+  const double* pt = nullptr;  // phi_tilde (global vertex numbering)
+  // rows of the vertices [y_lo, y_hi) (all when y_hi < 0), written at local row (v - y_lo) d + a;
+  // x holds the vertices from x_off on (a slab's ext range, or the global vector)
+  i64 x_off = 0, y_lo = 0, y_hi = -1;
 };
 
 struct BlockSystem {

@@ -309,7 +309,8 @@ __device__ __forceinline__ double mf_epi(const SpmvEpi& ep, const double* __rest
 #endif
 __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g, const Tables* __restrict__ T, double mu,
                                                          double lam, double kap, double xi0, double xi1,
-                                                         double scale, int zseg, const double* __restrict__ x,
+                                                         double scale, int zseg, int pz_lo, int pz_hi, i64 x_off,
+                                                         i64 y_lo, i64 y_hi, const double* __restrict__ x,
                                                          const double* __restrict__ pt,
                                                          const std::uint8_t* __restrict__ flag,
                                                          double* __restrict__ y, SpmvEpi ep) {
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g,
   const int nbx = (nn + MFB - 1) / MFB;
   const int col = blockIdx.x % (nbx * nbx), seg = blockIdx.x / (nbx * nbx);
   const int x0 = (col % nbx) * MFB, y0 = (col / nbx) * MFB;
-  const int zv0 = seg * zseg, zv1 = min(nn, zv0 + zseg);  // owned vertex planes [zv0, zv1)
+  const int zv0 = pz_lo + seg * zseg, zv1 = min(pz_hi, zv0 + zseg);  // owned vertex planes [zv0, zv1)
   auto load_plane = [&](int vz) {
     const int s = ((vz % 3) + 3) % 3;
     for (int t = threadIdx.x; t < PL; t += blockDim.x) {
@@ -328,9 +329,10 @@ __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g,
       double u0 = 0.0, u1 = 0.0, u2 = 0.0, p = 0.0;
       if (vx >= 0 && vy >= 0 && vz >= 0 && vx < nn && vy < nn && vz < nn) {
         const i64 v = i64(vx) + i64(nn) * (i64(vy) + i64(nn) * vz);
-        u0 = flag[v * 3] ? 0.0 : x[v * 3];
-        u1 = flag[v * 3 + 1] ? 0.0 : x[v * 3 + 1];
-        u2 = flag[v * 3 + 2] ? 0.0 : x[v * 3 + 2];
+        const i64 xv = (v - x_off) * 3;
+        u0 = flag[v * 3] ? 0.0 : x[xv];
+        u1 = flag[v * 3 + 1] ? 0.0 : x[xv + 1];
+        u2 = flag[v * 3 + 2] ? 0.0 : x[xv + 2];
         p = pt[v];
       }
       su[s][t * 3] = u0;
@@ -370,7 +372,8 @@ __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g,
       const int lx = t % MFB, ly = t / MFB;
       const int vx = x0 + lx, vy = y0 + ly;
       const double* cl = co[(L + 2) & 1];
-      if (L >= zv0 && vx < nn && vy < nn) {
+      const i64 vglob = i64(vx) + i64(nn) * (i64(vy) + i64(nn) * L);
+      if (L >= zv0 && vx < nn && vy < nn && vglob >= y_lo && vglob < y_hi) {
         double acc[3] = {top[0], top[1], top[2]};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -380,11 +383,11 @@ __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g,
           for (int a = 0; a < 3; ++a) acc[a] += o[a];
         }
         const int vz = L;
-        const i64 v = i64(vx) + i64(nn) * (i64(vy) + i64(nn) * vz);
+        const i64 v = vglob, r0 = (v - y_lo) * 3;
         const bool con = flag[v * 3] | flag[v * 3 + 1] | flag[v * 3 + 2];
         if (!con) {
 #pragma unroll
-          for (int a = 0; a < 3; ++a) y[v * 3 + a] = mf_epi(ep, x, v * 3 + a, acc[a]);
+          for (int a = 0; a < 3; ++a) y[r0 + a] = mf_epi(ep, x, r0 + a, acc[a]);
         } else {  // a constrained row keeps the summed element diagonal (model.cpp:295-300): y = d x
           double dg[3] = {0.0, 0.0, 0.0};
 #pragma unroll 1
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g,
           }
 #pragma unroll
           for (int a = 0; a < 3; ++a)
-            y[v * 3 + a] = mf_epi(ep, x, v * 3 + a, flag[v * 3 + a] ? dg[a] * x[v * 3 + a] : acc[a]);
+            y[r0 + a] = mf_epi(ep, x, r0 + a, flag[v * 3 + a] ? dg[a] * x[(v - x_off) * 3 + a] : acc[a]);
         }
       }
 #pragma unroll
@@ -462,11 +465,16 @@ void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep) {
   const int nb = int((g.nn + MFB - 1) / MFB);
   static const char* zenv = std::getenv("CF_MF_ZSEG");  // A/B: cell layers per CTA
   const int zseg = zenv ? std::max(1, std::atoi(zenv)) : MF_ZSEG;
-  const int nseg = int((g.nn + zseg - 1) / zseg);
+  const i64 plane = g.nn * g.nn;
+  const i64 y_lo = op.y_lo, y_hi = op.y_hi < 0 ? g.V : op.y_hi;
+  if (y_hi <= y_lo) return;
+  const int pz_lo = int(y_lo / plane), pz_hi = int((y_hi - 1) / plane) + 1;
+  const int nseg = (pz_hi - pz_lo + zseg - 1) / zseg;
   const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
   const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
   k_mf_sweep<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1,
-                                                          W / (g.h * g.h), zseg, x, op.pt, op.flag, y, ep);
+                                                          W / (g.h * g.h), zseg, pz_lo, pz_hi, op.x_off, y_lo, y_hi,
+                                                          x, op.pt, op.flag, y, ep);
   CF_LAUNCHED();
 }
 

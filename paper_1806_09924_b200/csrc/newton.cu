@@ -545,8 +545,10 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   const SegLayout seg = seg_layout(g, sl);  // every norm / dot of the step: NP-invariant order
   // operator_kind 1 (3d, one GPU): M_uu applied matrix-free in the Krylov operator and on the
   // u-hierarchy's finest level (mf.cu); M_uu is still assembled once per step for the AMG setup
-  std::shared_ptr<MfOp> mf;
-  if (opts.operator_kind == 1 && d == 3 && !dist) {
+  // N > 1 (the gathered global AMG): each rank applies its slab's rows (x on the ext planes) and its
+  // V-cycle row chunk of level 0 matrix-free, bitwise the rows of the 1-GPU apply
+  std::shared_ptr<MfOp> mf, mf_slab;
+  if (opts.operator_kind == 1 && d == 3 && (!dist || glob)) {
     mf = std::make_shared<MfOp>();
     mf->P = &P;
     mf->flag = base->flag.p;  // the u constraints of every set of the step
@@ -554,6 +556,10 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
     mf->lam = mat_lambda(mat);
     mf->kap = reg.kappa;
     mf->pt = pt.p;
+    mf_slab = std::make_shared<MfOp>(*mf);
+    mf_slab->x_off = sl.ve_lo;
+    mf_slab->y_lo = sl.v_lo;
+    mf_slab->y_hi = sl.v_hi;
   }
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
     {
@@ -638,7 +644,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         J->pu->mean_hint = tot[3] ? double(tot[2]) / double(tot[3]) : 0.0;
       }
     }
-    if (mf) J->mf_uu = mf;
+    if (mf) J->mf_uu = mf_slab;
     if (!prec || !opts.freeze_preconditioner) {
       Timer t(&T.amg_setup);
       NullspaceDev ns;
@@ -724,7 +730,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         prec = build_block_prec(*J, opts.prec_kind, opts.amg, &ns, prec.get());
       }
     }
-    if (mf && prec->amg_u && prec->amg_u->n == J->uu->rows) prec->amg_u->mf0 = mf;
+    if (mf && prec->amg_u && prec->amg_u->n == nu) prec->amg_u->mf0 = mf;
     GmresResult lin;
     {
       Timer t(&T.gmres);

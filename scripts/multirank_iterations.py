@@ -28,7 +28,7 @@ def worker(rank, size, port, cfg, out):
     c = bench.CFG3 if cfg == "cfg3" else dict(dim=2, half_width=10.0, n0=8, refinements=8)
     P, mat, reg = bench.sneddon_setup(cf, c)
     st = cf.make_initial_state(P, mat)
-    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(operator_kind=0), comm=comm)
+    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(), comm=comm)
     if rank == 0:
         x = st.get()["solution"]
         import hashlib

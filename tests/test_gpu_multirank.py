@@ -37,7 +37,8 @@ def _worker(rank, size, port, out_dir, d, n0, r):
     comm = cf.Communicator.from_gloo()
     P, mat, reg = _setup(cf, d, n0, r)
     st = cf.make_initial_state(P, mat)
-    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(operator_kind=0), comm=comm)
+    opk = int(os.environ.get("CF_TEST_OPKIND", "0"))
+    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(operator_kind=opk), comm=comm)
     x = st.get()["solution"]
     its = np.array([[it["residual_norm"], it["active_size"], it["set_changes"], it["gmres_iterations"]]
                     for it in rep["iterations"]])
@@ -55,6 +56,8 @@ def _free_port():
 
 
 @pytest.mark.parametrize("d,n0,r,size,mode", [(3, 4, 2, 2, "global"), (3, 4, 2, 3, "global"), (2, 8, 3, 4, "global"),
+                                               (3, 4, 2, 2, "global-mf"), (3, 4, 2, 3, "global-mf"),
+                                               (3, 8, 1, 4, "global-mf"), (3, 4, 2, 3, "global-replicated-mf"),
                                                (3, 8, 1, 4, "global"), (3, 4, 2, 3, "global-replicated"),
                                                (3, 4, 2, 3, "ras"), (2, 8, 3, 4, "block_jacobi")])
 def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
@@ -65,6 +68,9 @@ def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
     import paper_1806_09924_b200 as cf
     env = {"ras": {"CF_RAS": "1"}, "block_jacobi": {"CF_BLOCK_JACOBI": "1"},
            "global": {"CF_VCYCLE_SPLIT_MIN": "256"},
+           # the default matrix-free M_uu (operator_kind 1): slab rows and level-0 row chunks
+           "global-mf": {"CF_VCYCLE_SPLIT_MIN": "256", "CF_TEST_OPKIND": "1"},
+           "global-replicated-mf": {"CF_VCYCLE_REPLICATED": "1", "CF_TEST_OPKIND": "1"},
            "global-replicated": {"CF_VCYCLE_REPLICATED": "1"}}[mode]
     os.environ.update(env)
     try:
@@ -81,7 +87,7 @@ def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
         assert np.array_equal(its[k], its[0]), "ranks disagree on the Newton transcript"
     P, mat, reg = _setup(cf, d, n0, r)
     st = cf.make_initial_state(P, mat)
-    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(operator_kind=0))
+    rep = cf.newton_active_set_step(st, mat, P, reg, cf.SolverOptions(operator_kind=int(env.get("CF_TEST_OPKIND", "0"))))
     assert rep["converged"]
     ref = st.get()["solution"]
     ref_its = np.array([[it["residual_norm"], it["active_size"], it["set_changes"], it["gmres_iterations"]]
