@@ -527,7 +527,14 @@ class AmgHierarchy:
         self.A = A
         self.opts = opts or AmgOptions()
         self._h = C.c_void_p()
-        if node_of_dof is not None:
+        if node_of_dof is not None and _is_torch(node_of_dof):  # device arrays: no staging copies
+            import torch
+            nod = node_of_dof.to(torch.int32).contiguous()
+            B = near_nullspace.to(torch.float64)
+            m = 1 if B.dim() == 1 else B.shape[1]
+            Bf = B.t().contiguous().reshape(-1) if B.dim() == 2 else B.contiguous()
+            check(load().cf_amg_build(A._h, _ptr(nod), _ptr(Bf), m, C.byref(self.opts), C.byref(self._h)))
+        elif node_of_dof is not None:
             nod = np.ascontiguousarray(node_of_dof, dtype=np.int32)
             B = np.asfortranarray(near_nullspace, dtype=np.float64)
             m = 1 if B.ndim == 1 else B.shape[1]

@@ -145,7 +145,8 @@ template <int D>
 __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g, const Tables* __restrict__ T, Coef cf,
                                                          const double* __restrict__ sol,
                                                          const double* __restrict__ ptil,
-                                                         double* __restrict__ out, i64 c_lo, i64 c_hi) {
+                                                         double* __restrict__ out, i64 c_lo, i64 c_hi,
+                                                         const int* __restrict__ list, int nlist) {
   constexpr int NV = 1 << D, NQ = 1 << D;
   __shared__ double sG[NQ][NV][D], sS[NQ][NV], sW[NQ];
   for (int i = threadIdx.x; i < NQ * NV; i += blockDim.x) {
@@ -156,9 +157,10 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
   if (threadIdx.x < NQ) sW[threadIdx.x] = T->w[threadIdx.x];
   __syncthreads();
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  const i64 c = c_lo + t / NQ;
+  // list: only the listed cells (offsets from c_lo) are recomputed (assemble_residual_moved)
+  const bool valid = list ? t / NQ < nlist : c_lo + t / NQ < c_hi;
+  const i64 c = list ? (valid ? c_lo + list[t / NQ] : c_lo) : c_lo + t / NQ;
   const int q = int(t % NQ);
-  const bool valid = c < c_hi;
   const i64 cc = valid ? c : c_lo;
   const i64 cx = cc % g.nc, cy = (cc / g.nc) % g.nc, cz = (D == 3) ? cc / (g.nc * g.nc) : 0;
   const i64 nu = g.n_u();
@@ -245,6 +247,23 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
 #pragma unroll
     for (int a = 0; a <= D; ++a) o[a] = keep[a];
   }
+}
+
+// cells of [c_lo, c_hi) with a corner whose dofs changed (x vs x_before): their offsets, any order
+template <int D>
+__global__ void k_moved_cells(GridDesc g, i64 c_lo, i64 c_hi, const double* __restrict__ x,
+                              const double* __restrict__ xb, int* __restrict__ list, int* __restrict__ count) {
+  const i64 c = c_lo + i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= c_hi) return;
+  const i64 cx = c % g.nc, cy = (c / g.nc) % g.nc, cz = (D == 3) ? c / (g.nc * g.nc) : 0;
+  const i64 nu = g.n_u();
+  bool moved = false;
+  for (int k = 0; k < (1 << D) && !moved; ++k) {
+    const i64 v = (cx + (k & 1)) + g.nn * ((cy + ((k >> 1) & 1)) + g.nn * (cz + ((k >> 2) & 1)));
+    for (int a = 0; a < D; ++a) moved = moved || x[v * D + a] != xb[v * D + a];
+    moved = moved || x[nu + v] != xb[nu + v];
+  }
+  if (moved) list[atomicAdd(count, 1)] = int(c - c_lo);
 }
 
 // K1b: vertex gather with condensation (Scatter::vector_add, model.cpp:74-80; entry-free lines drop).
@@ -1004,27 +1023,75 @@ Slab make_slab(const GridDesc& g, i64 p_lo, i64 p_hi) {
 }
 
 void assemble_residual(Problem& P, const Constraints& cs, const cf_material& m, const cf_regularization& reg,
-                       const double* x, const double* pt, double* R, const Slab* slab) {
+                       const double* x, const double* pt, double* R, const Slab* slab, ResidualCache* cache) {
   build_tables(P, mat_mu(m), mat_lambda(m));
   const Coef cf = make_coef(P, m, reg);
   const GridDesc& g = P.g;
   const Slab sl = slab ? *slab : full_slab(g);
   const int nv = 1 << g.d;
   const i64 nc = sl.c_hi - sl.c_lo;
-  DevBuf<double> cellres(nc * nv * (g.d + 1));
+  DevBuf<double> local;
+  DevBuf<double>& cellres = cache ? cache->cellres : local;
+  if (cellres.n != nc * nv * (g.d + 1)) cellres.alloc(nc * nv * (g.d + 1));
   if (g.d == 2) {
     k_cell_residual_q<2><<<grid_for(nc * 4, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p, sl.c_lo,
-                                                                      sl.c_hi);
+                                                                      sl.c_hi, nullptr, 0);
     CF_LAUNCHED();
     k_vertex_residual<2><<<grid_for(sl.nv(), 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R, sl);
     CF_LAUNCHED();
   } else {
     k_cell_residual_q<3><<<grid_for(nc * 8, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cellres.p, sl.c_lo,
-                                                                      sl.c_hi);
+                                                                      sl.c_hi, nullptr, 0);
     CF_LAUNCHED();
     k_vertex_residual<3><<<grid_for(sl.nv(), 256), 256, 0, stream()>>>(g, cellres.p, cs.flag.p, R, sl);
     CF_LAUNCHED();
   }
+  if (cache) {
+    cache->c_lo = sl.c_lo;
+    cache->c_hi = sl.c_hi;
+    cache->valid = true;
+  }
+}
+
+void assemble_residual_moved(Problem& P, const Constraints& cs, const cf_material& m, const cf_regularization& reg,
+                             const double* x, const double* x_before, const double* pt, double* R,
+                             const Slab* slab, ResidualCache& cache) {
+  const GridDesc& g = P.g;
+  const Slab sl = slab ? *slab : full_slab(g);
+  if (!cache.valid || cache.c_lo != sl.c_lo || cache.c_hi != sl.c_hi) {
+    assemble_residual(P, cs, m, reg, x, pt, R, slab, &cache);
+    return;
+  }
+  build_tables(P, mat_mu(m), mat_lambda(m));
+  const Coef cf = make_coef(P, m, reg);
+  const i64 nc = sl.c_hi - sl.c_lo;
+  if (cache.list.n < nc) cache.list.alloc(nc);
+  if (!cache.count.n) cache.count.alloc(1);
+  cache.count.zero();
+  int n = 0;
+  if (g.d == 2) {
+    k_moved_cells<2><<<grid_for(nc, 256), 256, 0, stream()>>>(g, sl.c_lo, sl.c_hi, x, x_before, cache.list.p,
+                                                              cache.count.p);
+  } else {
+    k_moved_cells<3><<<grid_for(nc, 256), 256, 0, stream()>>>(g, sl.c_lo, sl.c_hi, x, x_before, cache.list.p,
+                                                              cache.count.p);
+  }
+  CF_LAUNCHED();
+  CF_CUDA(cudaMemcpyAsync(&n, cache.count.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  ++host_sync_count();
+  if (g.d == 2) {
+    if (n)
+      k_cell_residual_q<2><<<grid_for(i64(n) * 4, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cache.cellres.p,
+                                                                            sl.c_lo, sl.c_hi, cache.list.p, n);
+    k_vertex_residual<2><<<grid_for(sl.nv(), 256), 256, 0, stream()>>>(g, cache.cellres.p, cs.flag.p, R, sl);
+  } else {
+    if (n)
+      k_cell_residual_q<3><<<grid_for(i64(n) * 8, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cache.cellres.p,
+                                                                            sl.c_lo, sl.c_hi, cache.list.p, n);
+    k_vertex_residual<3><<<grid_for(sl.nv(), 256), 256, 0, stream()>>>(g, cache.cellres.p, cs.flag.p, R, sl);
+  }
+  CF_LAUNCHED();
 }
 
 template <int D>

@@ -132,8 +132,25 @@ std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64
                                                const i64* dofs_dev, const double* vals_dev);
 void distribute(const Constraints& c, double* v_dev, bool homogeneous);
 // x, pt: global-length vectors (valid on the slab's ext range).  R: local layout of the slab.
+// cache (optional): keeps the per-cell element residuals of the call, so that a following
+// assemble_residual_moved (same problem, material, phi_tilde and slab) recomputes only the cells
+// touching the vertices whose dofs changed; bitwise the full assembly (each element residual is a
+// function of its own corners only)
+struct ResidualCache {
+  DevBuf<double> cellres;
+  DevBuf<int> list, count;
+  DevBuf<std::uint8_t> moved;
+  i64 c_lo = 0, c_hi = 0;
+  bool valid = false;
+};
 void assemble_residual(Problem& P, const Constraints& c, const cf_material& m, const cf_regularization& reg,
-                       const double* x, const double* pt, double* R, const Slab* slab = nullptr);
+                       const double* x, const double* pt, double* R, const Slab* slab = nullptr,
+                       ResidualCache* cache = nullptr);
+// x_before: x of the cached call (global layout); only the cells with a corner whose dofs differ
+// between x_before and x are recomputed, then every owned row is gathered with c's flags
+void assemble_residual_moved(Problem& P, const Constraints& c, const cf_material& m, const cf_regularization& reg,
+                             const double* x, const double* x_before, const double* pt, double* R,
+                             const Slab* slab, ResidualCache& cache);
 // rows of the slab's owned vertices; columns in the slab's ext numbering.  reuse_uu: an M_uu of
 // the same phi_tilde, slab and Dirichlet set (M_uu depends on nothing else, model.cpp:268-276),
 // taken as is instead of being recomputed.

@@ -497,6 +497,8 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   hist.zero();
   DevBuf<int> flags(4);
   DevBuf<double> R(ntl), rhs(ntl), delta(ntl);
+  DevBuf<double> xb(nt);    // x before the active-set distribute (the moved cells)
+  ResidualCache rcache;     // element residuals of the iteration's first assembly
   DevBuf<double> ext(dist ? (d + 1) * sl.ne() : 0);  // GMRES operator input with ghost planes
   int hist_len = 0;
   double res0 = -1.0;
@@ -564,7 +566,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   for (int it = 1; it <= opts.newton_max_iter; ++it) {
     {
       Timer t(&T.residual);
-      assemble_residual(P, *base, mat, reg, x, pt.p, R.p, &sl);
+      assemble_residual(P, *base, mat, reg, x, pt.p, R.p, &sl, &rcache);
     }
     int changes = 0, asize = 0;
     {
@@ -591,6 +593,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
                                                    full.flag.p, full.inhom.p);
       CF_LAUNCHED();
       halo_global(cm, g, sl, full.flag.p, 1, false, true);  // neighbours' active phi columns
+      CF_CUDA(cudaMemcpyAsync(xb.p, x, size_t(nt) * sizeof(double), cudaMemcpyDeviceToDevice, stream()));
       CF_CUDA(cudaMemsetAsync(flags.p + 3, 0, sizeof(int), stream()));
       k_distribute_moved<<<gl, 256, 0, stream()>>>(sl, d, nu, full.flag.p, full.inhom.p, x, flags.p + 3);
       CF_LAUNCHED();
@@ -600,8 +603,8 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
     cm.max_i64(&moved, 1);
     {
       Timer t(&T.residual);
-      if (moved) {
-        assemble_residual(P, full, mat, reg, x, pt.p, R.p, &sl);
+      if (moved) {  // only the cells touching moved dofs are recomputed (bitwise the full assembly)
+        assemble_residual_moved(P, full, mat, reg, x, xb.p, pt.p, R.p, &sl, rcache);
       } else {
         k_zero_active<<<gv, 256, 0, stream()>>>(nv, nul, active.p, R.p);
         CF_LAUNCHED();

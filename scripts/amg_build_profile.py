@@ -33,7 +33,7 @@ cases = {
 which = sys.argv[1:] or ["phi", "u"]
 for name in which:
     A, nod, B = cases[name]
-    nod_d = torch.from_numpy(nod).cuda()
+    nod_d = torch.from_numpy(nod).cuda()  # device arrays: the build times exclude staging copies
     B_d = torch.from_numpy(np.ascontiguousarray(B)).cuda()
     for _ in range(2):
         h = cf.build_amg(A, nod_d, B_d)
