@@ -366,6 +366,79 @@ __global__ void __launch_bounds__(128) k_cell_qpstate(GridDesc g, const Tables* 
   }
 }
 
+// the same states, one thread per (cell, point): the 2^d lanes of a cell load one corner each and
+// exchange them with shuffles (as K1a); every state is the serial kernel's expression sequence
+template <int D>
+__global__ void __launch_bounds__(256) k_cell_qpstate_q(GridDesc g, const Tables* __restrict__ T, Coef cf,
+                                                        const double* __restrict__ sol,
+                                                        const double* __restrict__ ptil, double* __restrict__ out,
+                                                        i64 c_lo, i64 c_hi) {
+  constexpr int NV = 1 << D, NQ = 1 << D, NS = QS<D>::NS;
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 c = c_lo + t / NQ;
+  const int q = int(t % NQ);
+  const bool valid = c < c_hi;
+  const i64 cc = valid ? c : c_lo;
+  const i64 cx = cc % g.nc, cy = (cc / g.nc) % g.nc, cz = (D == 3) ? cc / (g.nc * g.nc) : 0;
+  const i64 nu = g.n_u();
+  double my_u[D], my_phi, my_pt;
+  {
+    const int k = q;
+    const i64 v = (cx + (k & 1)) + g.nn * ((cy + ((k >> 1) & 1)) + g.nn * (cz + ((k >> 2) & 1)));
+#pragma unroll
+    for (int a = 0; a < D; ++a) my_u[a] = sol[v * D + a];
+    my_phi = sol[nu + v];
+    my_pt = ptil[v];
+  }
+  double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double phi = 0.0, pt = 0.0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const double sk = T->s[q][k];
+    phi += sk * __shfl_sync(0xffffffffu, my_phi, k, NQ);
+    pt += sk * __shfl_sync(0xffffffffu, my_pt, k, NQ);
+    double uk[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) uk[a] = __shfl_sync(0xffffffffu, my_u[a], k, NQ);
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+#pragma unroll
+      for (int a = 0; a < D; ++a) gu[a][b] += uk[a] * T->gp[q][k][b];
+  }
+  double e[3][3], sig[3][3];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) e[a][b] = 0.5 * (gu[a][b] + gu[b][a]);
+  double tre = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) tre += e[a][a];
+  const double two_mu = 2.0 * cf.mu;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) sig[a][b] = two_mu * e[a][b];
+#pragma unroll
+  for (int a = 0; a < D; ++a) sig[a][a] += cf.lam * tre;
+  double sig_ee = 0.0;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) sig_ee += sig[a][b] * e[a][b];
+  const double gcoef = (1.0 - cf.kap) * pt * pt + cf.kap;
+  const double w = T->w[q];
+  if (!valid) return;
+  double* o = out + (c - c_lo) * (NQ * NS) + q * NS;
+  o[0] = w * gcoef;
+  o[1] = phi;
+  o[2] = tre;
+  o[3] = sig_ee;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) o[4 + a * D + b] = sig[a][b];
+}
+
 // Element-matrix entries coupling row vertex v (local k) and column vertex w (local l),
 // summed over their common cells in reference order (kuu/kpu/kpp of model.cpp:268-285).
 template <int D>
@@ -1101,7 +1174,12 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   constexpr int NQ = 1 << D, NS = QS<D>::NS;
   const i64 ncl = sl.c_hi - sl.c_lo;
   DevBuf<double> qs(ncl * NQ * NS);
-  k_cell_qpstate<D><<<grid_for(ncl, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p, sl.c_lo, sl.c_hi);
+  static const bool serial_qs = std::getenv("CF_QPSTATE_SERIAL") != nullptr;  // A/B: one thread per cell
+  if (serial_qs)
+    k_cell_qpstate<D><<<grid_for(ncl, 128), 128, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p, sl.c_lo, sl.c_hi);
+  else
+    k_cell_qpstate_q<D><<<grid_for(ncl * (1 << D), 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, qs.p, sl.c_lo,
+                                                                              sl.c_hi);
   CF_LAUNCHED();
   const i64 nu = D * sl.nv(), np = sl.nv();
   J.pu->rows = np;
