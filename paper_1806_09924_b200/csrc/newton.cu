@@ -699,7 +699,11 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
         Jl.d = d;
         if (ras) {
           // restricted additive Schwarz: the block of the owned planes plus one plane of overlap
-          // on each side (rows assembled for the extended slab, columns cut to it)
+          // on each side (rows assembled for the extended slab, columns cut to it).  The overlap
+          // rows read x and the constraint flags two planes beyond the owned ones, where the
+          // one-plane halo is not current: every rank's owned planes are all-gathered first.
+          allgather_owned(cm, g, x);
+          allgather_owned_bytes(cm, g, full.flag.p, 1);
           auto Jx = assemble_jacobian(P, full, mat, reg, x, pt.p, &sx, uu_x_step);
           if (!uu_x_step) uu_x_step = Jx->uu;
           const i64 lo = sx.v_lo - sx.ve_lo, nx = sx.nv();
