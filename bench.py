@@ -321,9 +321,15 @@ def operator_leg(cf, device, stream, applies=20):
     """Config 1: assembled M_uu apply (CSR SpMV), inputs resident in HBM."""
     import torch
     P, cs, mat, reg, x, pt = config1_inputs(cf, device=device)
-    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
     nu = P.n_u
-    u = x[:nu].contiguous()
+    u0 = x[:nu].contiguous()
+    # the matrix-free equivalent first (BASELINE config 1): same operator from phi_tilde, cell by cell
+    y_mf = torch.empty_like(u0)
+    for _ in range(3):
+        cf.mf_apply_uu(P, cs, mat, reg, pt, u0, out=y_mf)
+    ms_mf = time_events(lambda: cf.mf_apply_uu(P, cs, mat, reg, pt, u0, out=y_mf), applies, stream)
+    J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+    u = u0
     del x
     y = torch.empty(nu, dtype=torch.float64, device=u.device)
     fmt = J.format(0)
@@ -333,10 +339,6 @@ def operator_leg(cf, device, stream, applies=20):
     for _ in range(3):
         J.spmv(0, u, out=y)
     ms = time_events(lambda: J.spmv(0, u, out=y), applies, stream)
-    # the matrix-free equivalent (BASELINE config 1): same operator from phi_tilde, cell by cell
-    y_mf = torch.empty_like(y)
-    cf.mf_apply_uu(P, cs, mat, reg, pt, u, out=y_mf)
-    ms_mf = time_events(lambda: cf.mf_apply_uu(P, cs, mat, reg, pt, u, out=y_mf), applies, stream)
     rel_mf = float(torch.linalg.norm(y_mf - y) / torch.linalg.norm(y))
     fp64 = cf.fp64_peak_tflops()
     ncells = P.n_cells
@@ -405,9 +407,18 @@ def vcycle_leg(cf, P, mat, reg, x_final, phi_old, stream):
         out[name + "_levels"] = h.n_levels()
         out[name + "_bytes"] = nb
         out[name + "_gbs"] = nb / ms / 1e6
+    # the u-cycle as the Newton step runs it (operator_kind 1): the finest level's residual and
+    # smoothing sweep matrix-free; its bytes exclude the two level-0 A applies (FP64-bound)
+    if P.dim == 3:
+        hu.set_matrix_free(P, cs, mat, reg, phi_old)
+        r = torch.randn(P.n_u, dtype=torch.float64, device=x_final.device)
+        hu.v_cycle(r)
+        ms = time_events(lambda: hu.v_cycle(r), 10, stream)
+        out["u_ms_matrix_free"] = ms
     out["note"] = ("one V-cycle application (zero initial guess, 1+1 damped Jacobi sweeps per level, dense LU on the "
                    "coarsest); bytes = per level 2 A applies (residual and post-sweep, fused with their vector "
-                   "updates) + R + P in their storage formats + 56 B per row of vector traffic")
+                   "updates) + R + P in their storage formats + 56 B per row of vector traffic; u_ms_matrix_free: "
+                   "the same u-cycle with the finest level's two A applies matrix-free, as the Newton step runs it")
     return out
 
 
@@ -502,6 +513,10 @@ def ours(args):
     last = reps[-1]
     free, total = torch.cuda.mem_get_info()
 
+    # the converged solution (V-cycle leg), then the last device state is released so the e2e step
+    # allocates like a timed step does
+    x_final = st.get()["solution"]
+    st = None
     # e2e: through the C ABI with pinned host buffers (H2D of the state, Newton step, D2H of the
     # whole state back into pinned host memory)
     import ctypes as C
@@ -547,7 +562,7 @@ def ours(args):
     vcyc = None
     if rank == 0 and world == 1:
         try:
-            vcyc = vcycle_leg(cf, P, mat, reg, torch.from_numpy(st.get()["solution"]).to(device), po0, s)
+            vcyc = vcycle_leg(cf, P, mat, reg, torch.from_numpy(x_final).to(device), po0, s)
         except Exception as ex:  # reported, never fatal
             vcyc = {"error": str(ex)[:200]}
     if world > 1:

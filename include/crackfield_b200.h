@@ -209,6 +209,10 @@ int cf_amg_build(cf_csr A, const int32_t* node_of_dof, const double* B, int m, c
 int cf_amg_vcycle(cf_amg h, const double* r, double* x);
 /* n_levels() and coarse_dim() (linsolve.hpp:67-68). */
 int cf_amg_info(cf_amg h, int* n_levels, int64_t* coarse_dim);
+/* the hierarchy's finest level applied matrix-free in its V-cycles (residual, smoothing), as in the
+ * Newton step with operator_kind 1: h must be a u-block hierarchy of the 3d problem p */
+int cf_amg_set_matrix_free(cf_amg h, cf_problem p, cf_constraints c, const cf_material* mat,
+                           const cf_regularization* reg, const double* phi_tilde);
 /* Diagnostics of one non-coarsest level: info8 = {rows(A), nnz(A), nnz(P), cols(P), n_nodes,
  * n_aggregates, strong edges, LFMIS rounds}; lambda_max and the Jacobi weight. */
 int cf_amg_level_info(cf_amg h, int level, int64_t* info8, double* lambda, double* jacobi_weight);

@@ -559,6 +559,11 @@ class AmgHierarchy:
     def coarse_dim(self):
         return self._coarse
 
+    def set_matrix_free(self, prob, constraints, mat, reg, phi_tilde):
+        """Apply the finest level (a 3d u-block) matrix-free in the V-cycles (operator_kind 1)."""
+        pt = _as_f64(phi_tilde)
+        check(load().cf_amg_set_matrix_free(self._h, prob._h, constraints._h, C.byref(mat), C.byref(reg), _ptr(pt)))
+
     def v_cycle(self, r):
         r = _as_f64(r)
         x = _empty_like_kind(r, self.A.rows)

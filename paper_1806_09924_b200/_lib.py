@@ -171,6 +171,7 @@ SIGNATURES = [
     ("cf_amg_level_aggregates", _I, [_P, _I, _P]),
     ("cf_amg_level_export", _I, [_P, _I, _I, _P, _P, _P]),
     ("cf_amg_destroy", _I, [_P]),
+    ("cf_amg_set_matrix_free", _I, [_P, _P, _P, C.POINTER(Material), C.POINTER(Regularization), _P]),
     ("cf_prec_build", _I, [_P, _I, C.POINTER(AmgOptions), _P, _P, C.POINTER(_P)]),
     ("cf_prec_apply", _I, [_P, _P, _P]),
     ("cf_prec_destroy", _I, [_P]),

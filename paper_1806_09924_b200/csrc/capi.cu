@@ -21,6 +21,8 @@ struct cf_csr_s {
 };
 struct cf_amg_s {
   std::unique_ptr<cfb::Amg> h;
+  cfb::DevBuf<double> mf_pt;         // cf_amg_set_matrix_free: copies of phi_tilde and the flags
+  cfb::DevBuf<std::uint8_t> mf_flag;
 };
 struct cf_prec_s {
   std::unique_ptr<cfb::BlockPrec> p;
@@ -675,6 +677,29 @@ int cf_amg_vcycle(cf_amg h, const double* r, double* x) {
     OutArg<double> xo(x, h->h->n);
     h->h->vcycle(ri.dev, xo.dev);
     xo.finish();
+  });
+}
+
+int cf_amg_set_matrix_free(cf_amg h, cf_problem p, cf_constraints c, const cf_material* mat,
+                           const cf_regularization* reg, const double* phi_tilde) {
+  return guard([&] {
+    CHECK_ARG(h && p && c && mat && reg && phi_tilde, "cf_amg_set_matrix_free: null argument");
+    const GridDesc& g = p->p->g;
+    CHECK_ARG(g.d == 3, "cf_amg_set_matrix_free: the matrix-free M_uu is 3d");
+    CHECK_ARG(h->h->n == g.n_u(), "cf_amg_set_matrix_free: the hierarchy is not a u-block hierarchy of this problem");
+    h->mf_pt.alloc(g.V);
+    h->mf_flag.alloc(g.n_total());
+    CF_CUDA(cudaMemcpyAsync(h->mf_pt.p, phi_tilde, size_t(g.V) * sizeof(double), cudaMemcpyDefault, stream()));
+    CF_CUDA(cudaMemcpyAsync(h->mf_flag.p, c->c->flag.p, size_t(g.n_total()), cudaMemcpyDeviceToDevice, stream()));
+    auto op = std::make_shared<MfOp>();
+    op->P = p->p;
+    op->flag = h->mf_flag.p;
+    op->mu = mat_mu(*mat);
+    op->lam = mat_lambda(*mat);
+    op->kap = reg->kappa;
+    op->pt = h->mf_pt.p;
+    h->h->mf0 = op;
+    CF_CUDA(cudaStreamSynchronize(stream()));
   });
 }
 
