@@ -78,6 +78,9 @@ struct MeshDisc {
   Plan res;          // residual: slot = dof
   Plan uu, pu, pp;   // Jacobian entries
   Plan self;         // dof -> its own (cell, local dof) incidences (constrained diagonals)
+  // the base constraint set of the Newton step (Dirichlet clamp + hanging lines), kept with its
+  // plans across load steps until the mesh changes
+  std::unique_ptr<Constraints> base_cache;
   i64 n_u() const { return d * V; }
   i64 n_total() const { return (d + 1) * V; }
   DevForest forest() const {

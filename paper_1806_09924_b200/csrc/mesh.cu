@@ -292,6 +292,7 @@ void upload(MeshDisc& m) {
   CF_LAUNCHED();
   m.plans_ready = false;
   m.tab_mu = m.tab_lam = -1.0;
+  m.base_cache.reset();
 }
 
 // ------------------------------------------------------------------ constraints (fem.cpp:189-267)

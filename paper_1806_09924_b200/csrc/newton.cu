@@ -864,7 +864,8 @@ NewtonReport mesh_newton_step(MeshDisc& m, State& st, const cf_material& mat, co
   const int nw = std::max(1, (opts.cycle_window + 63) / 64);
   NewtonReport report;
   PhaseTimes& T = report.times;
-  auto base = mesh_build_constraints(m, true, 0, nullptr, nullptr);  // solver.cpp:55
+  if (!m.base_cache) m.base_cache = mesh_build_constraints(m, true, 0, nullptr, nullptr);  // solver.cpp:55
+  const Constraints* base = m.base_cache.get();
   double* x = st.solution.p;
   distribute(*base, x, false);
   DevBuf<double> ptfull(nt);  // conforming_phi (solver.cpp:40-47): phi_tilde distributed by the base set
