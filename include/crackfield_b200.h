@@ -49,10 +49,15 @@ typedef struct {
   double eps, kappa;
 } cf_regularization;
 
-/* AmgOptions (linsolve.hpp:51-60). */
+/* AmgOptions (linsolve.hpp:51-60).  smoother: 0 = damped Jacobi, the reference's smoother
+ * (linsolve.cpp:301-311); 1 = Chebyshev of degree chebyshev_degree (3 recommended) on D^-1 A over
+ * [g / 10, g], g the Gershgorin bound of D^-1 A (the north star's "Jacobi/Chebyshev smoothing";
+ * opt-in, no reference counterpart, so not part of the parity contract; smoothing_sweeps
+ * applications per visit; with it the V-cycle is not row-split over ranks but replicated). */
 typedef struct {
   double strength_threshold, prolongation_omega, jacobi_omega;
   int smoothing_sweeps, coarse_size, max_levels;
+  int smoother, chebyshev_degree;
 } cf_amg_options;
 
 /* GmresOptions (linsolve.hpp:32-36). */

@@ -48,11 +48,12 @@ class AmgOptions(C.Structure):
     """linsolve.hpp:51-60."""
     _fields_ = [("strength_threshold", C.c_double), ("prolongation_omega", C.c_double),
                 ("jacobi_omega", C.c_double), ("smoothing_sweeps", C.c_int), ("coarse_size", C.c_int),
-                ("max_levels", C.c_int)]
+                ("max_levels", C.c_int), ("smoother", C.c_int), ("chebyshev_degree", C.c_int)]
 
     def __init__(self, **kw):
+        # smoother 0: damped Jacobi (the reference); 1: Chebyshev (opt-in, outside the parity contract)
         d = dict(strength_threshold=0.02, prolongation_omega=2.0 / 3.0, jacobi_omega=2.0 / 3.0,
-                 smoothing_sweeps=1, coarse_size=64, max_levels=25)
+                 smoothing_sweeps=1, coarse_size=64, max_levels=25, smoother=0, chebyshev_degree=3)
         d.update(kw)
         super().__init__(**d)
 

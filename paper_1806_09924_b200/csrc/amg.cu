@@ -1198,6 +1198,49 @@ __global__ void k_jacobi_upd(i64 n, double w, const double* __restrict__ d, cons
 // power-iteration start vector v_i = 1 + 0.5 sin(1 + i) (linsolve.cpp:123): computed on the host
 // with the C library's sin (correctly rounded).  v_i does not depend on the length, so one buffer
 // holds the longest prefix seen so far and every level (of every hierarchy) reads a prefix of it.
+// Chebyshev smoothing on D^-1 A (smoother 1): the first step d = D^-1 r / theta, then
+// d = c1 d + c2 D^-1 r, x += d (the standard three-term recurrence)
+__global__ void k_cheb_init(i64 n, double inv_theta, const double* __restrict__ dinv, const double* __restrict__ r,
+                            double* __restrict__ d, double* __restrict__ x, int zero) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double di = inv_theta * (dinv[i] * r[i]);
+  d[i] = di;
+  x[i] = zero ? di : x[i] + di;
+}
+__global__ void k_cheb_step(i64 n, double c1, double c2, const double* __restrict__ dinv,
+                            const double* __restrict__ r, double* __restrict__ d, double* __restrict__ x) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double di = c1 * d[i] + c2 * (dinv[i] * r[i]);
+  d[i] = di;
+  x[i] += di;
+}
+
+// Gershgorin bound of D^-1 A, row i: |d_i| sum_j |a_ij| (the Chebyshev smoother's upper bound)
+__global__ void k_gershgorin_rows(i64 n, const i64* __restrict__ ptr, const double* __restrict__ val,
+                                  const double* __restrict__ dinv, double* __restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (i64 k = ptr[i]; k < ptr[i + 1]; ++k) s += fabs(val[k]);
+  out[i] = fabs(dinv[i]) * s;
+}
+
+double gershgorin_bound(const Csr& A, const double* inv_diag) {
+  const i64 n = A.rows;
+  if (n == 0) return 1.0;
+  DevBuf<double> rows(n), mx(1);
+  k_gershgorin_rows<<<grid_for(n, 256), 256, 0, stream()>>>(n, A.ptr.p, A.val.p, inv_diag, rows.p);
+  CF_LAUNCHED();
+  size_t bytes = 0;
+  CF_CUDA(cub::DeviceReduce::Max(nullptr, bytes, rows.p, mx.p, n, stream()));
+  DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+  CF_CUDA(cub::DeviceReduce::Max(tmp.p, bytes, rows.p, mx.p, n, stream()));
+  count_launch();
+  return read_dev(mx.p);
+}
+
 const double* lambda_start(i64 n) {
   static DevBuf<double> buf;
   static std::vector<double> host;
@@ -1638,6 +1681,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     L->A = A;
     L->jacobi_weight = opts.jacobi_omega * 2.0 / lambda;
     L->lambda = lambda;
+    if (opts.smoother == 1) L->cheb_hi = gershgorin_bound(*A, L->inv_diag.p);
     L->n_nodes = n_nodes;
     L->n_aggregates = n_agg;
     L->strong_edges = ns;
@@ -1697,12 +1741,59 @@ void Amg::vcycle_range(size_t l0, const double* b0, double* x0) const {
     else
       csr_spmv_epi(*levels[l]->A, xin, yout, ep);
   };
+  // Chebyshev smoothing of level l (opts.smoother == 1) on D^-1 A over [hi / 10, hi], hi the
+  // Gershgorin bound (the 15-step power estimate undershoots lambda_max by enough that the
+  // polynomial amplifies the top of the spectrum: GMRES stagnated on config 3 with 1.1 lambda)
+  auto chebyshev = [&](size_t l, const double* bl, double* xl, bool zero) {
+    const AmgLevel& L = *levels[l];
+    const i64 n = L.A->rows;
+    if (L.tmp_d.n < n) L.tmp_d.alloc(n);
+    const double hi = L.cheb_hi, lo = hi / 10.0;
+    const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+    const int deg = std::max(1, opts.chebyshev_degree);
+    for (int sweep = 0; sweep < std::max(1, opts.smoothing_sweeps); ++sweep) {
+      const bool z = zero && sweep == 0;
+      const double* r = bl;
+      if (!z) {
+        SpmvEpi ep;
+        ep.b = bl;
+        ep.mode = 1;
+        apply(l, xl, L.tmp_r.p, ep);  // r = b - A x
+        r = L.tmp_r.p;
+      }
+      k_cheb_init<<<grid_for(n, 256), 256, 0, stream()>>>(n, 1.0 / theta, L.inv_diag.p, r, L.tmp_d.p, xl, z ? 1 : 0);
+      CF_LAUNCHED();
+      double rho = 1.0 / sigma;
+      for (int k = 1; k < deg; ++k) {
+        SpmvEpi ep;
+        ep.b = bl;
+        ep.mode = 1;
+        apply(l, xl, L.tmp_r.p, ep);
+        const double rho_new = 1.0 / (2.0 * sigma - rho);
+        k_cheb_step<<<grid_for(n, 256), 256, 0, stream()>>>(n, rho_new * rho, 2.0 * rho_new / delta, L.inv_diag.p,
+                                                            L.tmp_r.p, L.tmp_d.p, xl);
+        CF_LAUNCHED();
+        rho = rho_new;
+      }
+    }
+  };
+  const bool cheb = opts.smoother == 1;
   const double* b = b0;
   for (size_t l = l0; l < levels.size(); ++l) {
     const AmgLevel& L = *levels[l];
     const i64 n = L.A->rows;
     double* xl = (l == l0) ? x0 : levels[l - 1]->tmp_x.p;
     const double w = L.jacobi_weight;
+    if (cheb) {
+      chebyshev(l, b, xl, true);
+      SpmvEpi ep;
+      ep.b = b;
+      ep.mode = 1;
+      apply(l, xl, L.tmp_r.p, ep);  // r = b - A x
+      csr_spmv_add(*L.R, L.tmp_r.p, L.tmp_b.p, nullptr);
+      b = L.tmp_b.p;
+      continue;
+    }
     k_jacobi0<<<grid_for(n, 256), 256, 0, stream()>>>(n, w, L.inv_diag.p, b, xl);
     CF_LAUNCHED();
     for (int s = 1; s < opts.smoothing_sweeps; ++s) {
@@ -1731,6 +1822,11 @@ void Amg::vcycle_range(size_t l0, const double* b0, double* x0) const {
     const i64 n = L.A->rows;
     double* xl = (l == l0) ? x0 : levels[l - 1]->tmp_x.p;
     const double* bl = (l == l0) ? b0 : levels[l - 1]->tmp_b.p;
+    if (cheb) {
+      csr_spmv_add(*L.P, L.tmp_x.p, xl, xl);  // x += P x_c
+      chebyshev(l, bl, xl, false);
+      continue;
+    }
     int s = 0;
     if (unfused || opts.smoothing_sweeps < 1) {
       csr_spmv_add(*L.P, L.tmp_x.p, xl, xl);  // x += P x_c
@@ -1761,7 +1857,7 @@ void Amg::vcycle_range(size_t l0, const double* b0, double* x0) const {
 void Amg::distribute(const Comm* cm, i64 min_rows) {
   dist.clear();
   comm = cm;
-  if (!cm || !cm->distributed() || opts.smoothing_sweeps != 1) return;
+  if (!cm || !cm->distributed() || opts.smoothing_sweeps != 1 || opts.smoother != 0) return;
   static const bool unfused = std::getenv("CF_VCYCLE_UNFUSED") != nullptr;
   if (unfused) return;
   const int P = cm->size, r = cm->rank;
@@ -1871,7 +1967,8 @@ bool Amg::same_inputs(const Csr& A, const int* node_of_dof, const double* B, int
   if (!A0 || m != m0 || A.rows != A0->rows || A.cols != A0->cols || A.nnz != A0->nnz) return false;
   if (o.strength_threshold != opts.strength_threshold || o.prolongation_omega != opts.prolongation_omega ||
       o.jacobi_omega != opts.jacobi_omega || o.smoothing_sweeps != opts.smoothing_sweeps ||
-      o.coarse_size != opts.coarse_size || o.max_levels != opts.max_levels)
+      o.coarse_size != opts.coarse_size || o.max_levels != opts.max_levels || o.smoother != opts.smoother ||
+      o.chebyshev_degree != opts.chebyshev_degree)
     return false;
   const bool same_matrix = &A == A0.get() ||  // the very matrix the hierarchy was built from
                            (bitwise_equal(A.ptr.p, A0->ptr.p, size_t(A.rows + 1) * sizeof(i64)) &&

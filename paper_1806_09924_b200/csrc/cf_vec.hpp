@@ -94,10 +94,12 @@ struct AmgLevel {
   DevBuf<double> inv_diag;
   double jacobi_weight = 2.0 / 3.0;
   double lambda = 0.0;
+  double cheb_hi = 0.0;  // Chebyshev upper bound (smoother 1): Gershgorin bound of D^-1 A
   i64 n_nodes = 0, n_aggregates = 0, strong_edges = 0;
   int lfmis_rounds = 0;
   DevBuf<int> agg_of_node;  // kept for parity checks
   mutable DevBuf<double> tmp_r, tmp_b, tmp_x;  // V-cycle work vectors of this level
+  mutable DevBuf<double> tmp_d;                // Chebyshev search direction (smoother 1)
 };
 
 struct Comm;

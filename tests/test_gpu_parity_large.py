@@ -279,6 +279,24 @@ def test_config3_full_newton_step_bitwise_and_reference_order(cf, orcmt):
 
 
 @slow
+def test_config3_full_newton_step_matrix_free_reference_order(cf, orcmt):
+    """The headline path at its full size: config 3 with the matrix-free operator (operator_kind 1)
+    against the oracle in the reference's arithmetic order, at the north-star tolerances."""
+    P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 3, 8, 4)
+    reps, x = _device_run(cf, P, mat, reg, 1, op=1)
+    with orcmt.reference_order():
+        rreps, xr = _oracle_run(orcmt, O, omat, oreg, phi, 1)
+    rel = _within_north_star(reps, x, rreps, xr, P, cf, O)
+    out = {"case": "config 3 (128^3, 8,586,756 dofs), one load step, operator_kind 1 vs reference order",
+           "solution_rel_diff": rel, "device_iterations": _its(reps[0]).tolist(),
+           "reference_order_iterations": rreps[0]["iterations"].tolist(),
+           "tcv_device": cf.compute_tcv(P, x), "tcv_reference_order": O.tcv(xr)}
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "mf_config3_fullsize.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+@slow
 def test_config2_full_size_bitwise_and_reference_order(cf, orcmt):
     P, O, mat, omat, reg, oreg, phi = _pair(cf, orcmt, 2, 8, 8)
     assert P.n_total == 12595203

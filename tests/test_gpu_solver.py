@@ -375,3 +375,94 @@ def test_amg_paths_forced_and_disabled(cf, env):
                         "-k", "amg and not everywhere and not forced or block_prec or penny"],
                        env=dict(os.environ, **env), capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def _np_vcycle_cheb(levels, Ac, b, deg, sweeps=1):
+    """numpy restatement of the opt-in Chebyshev V-cycle (amg.cu vcycle_range, smoother 1): on each
+    level `sweeps` Chebyshev passes of degree `deg` on D^-1 A over [hi / 10, hi], hi the Gershgorin
+    bound max_i |d_i| sum_j |a_ij|, restrict the residual, dense solve on the coarsest level,
+    prolongate and post-smooth."""
+    def cheb(A, dinv, bl, x, zero):
+        hi = (abs(A) @ np.ones(A.shape[1]) * abs(dinv)).max()
+        lo = hi / 10.0
+        theta, delta = 0.5 * (hi + lo), 0.5 * (hi - lo)
+        sigma = theta / delta
+        for s in range(sweeps):
+            r = bl if (zero and s == 0) else bl - A @ x
+            d = dinv * r / theta
+            x = d.copy() if (zero and s == 0) else x + d
+            rho = 1.0 / sigma
+            for _ in range(1, deg):
+                rho_new = 1.0 / (2.0 * sigma - rho)
+                d = rho_new * rho * d + 2.0 * rho_new / delta * (dinv * (bl - A @ x))
+                x = x + d
+                rho = rho_new
+        return x
+
+    def rec(l, bl):
+        if l == len(levels):
+            return np.linalg.solve(Ac, bl)
+        A, P = levels[l]
+        dinv = 1.0 / A.diagonal()
+        x = cheb(A, dinv, bl, None, True)
+        xc = rec(l + 1, P.T @ (bl - A @ x))
+        return cheb(A, dinv, bl, x + P @ xc, False)
+    return rec(0, b)
+
+
+@pytest.mark.parametrize("deg,sweeps", [(1, 1), (2, 1), (3, 2)])
+def test_amg_chebyshev_smoother_matches_numpy(cf, deg, sweeps):
+    """The opt-in Chebyshev smoother (AmgOptions.smoother = 1; the reference smooths with damped
+    Jacobi only, so this is outside the bitwise contract) against its numpy restatement on the
+    16^3 u-block hierarchy, to 1e-10 relative."""
+    P = cf.Problem(3, 10.0, 8, 1)
+    rng = np.random.default_rng(31)
+    x = np.zeros(P.n_total)
+    x[:P.n_u] = 1e-3 * rng.uniform(-1, 1, P.n_u)
+    x[P.n_u:] = rng.uniform(0.2, 1.0, P.n_phi)
+    mat = cf.Material()
+    reg = cf.resolve_regularization(P, mat, cf.slit_band_edge(P, mat))
+    cs = cf.build_constraints(P)
+    u = cf.assemble_jacobian(P, cs, mat, reg, x, x[P.n_u:].copy()).M_uu
+    node = np.repeat(np.arange(P.n_vertices, dtype=np.int32), 3)
+    opts = cf.AmgOptions(smoother=1, chebyshev_degree=deg, smoothing_sweeps=sweeps)
+    h = cf.build_amg(cf.CsrMatrix(u.rows, u.cols, u.ptr, u.col, u.val), node, cf.rigid_body_modes(P, cs), opts)
+    levels = []
+    for lev in range(h.n_levels() - 1):
+        A, Pm = h.level_matrix(lev, 0), h.level_matrix(lev, 1)
+        levels.append((sp.csr_matrix((A.val, A.col, A.ptr), shape=(A.rows, A.cols)),
+                       sp.csr_matrix((Pm.val, Pm.col, Pm.ptr), shape=(Pm.rows, Pm.cols))))
+    assert len(levels) >= 2
+    Ac = levels[-1][0]
+    Pl = levels[-1][1]
+    Ac = (Pl.T @ Ac @ Pl).toarray()
+    r = rng.uniform(-1, 1, P.n_u)
+    got = h.v_cycle(r)
+    ref = _np_vcycle_cheb(levels, Ac, r, deg, sweeps)
+    assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+    # a linear operator (fixed polynomial), and a better smoother than none at all
+    s = rng.uniform(-1, 1, P.n_u)
+    lhs, rhs = h.v_cycle(0.6 * r + 1.3 * s), 0.6 * got + 1.3 * h.v_cycle(s)
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(rhs)
+    A0 = levels[0][0]
+    assert np.linalg.norm(r - A0 @ got) < np.linalg.norm(r)
+
+
+@pytest.mark.parametrize("opkind", [0, 1])
+def test_newton_step_chebyshev_smoother(cf, orc, opkind):
+    """The whole 3d penny Newton step with Chebyshev-smoothed AMG (assembled and matrix-free finest
+    level) converges to the same solution as the reference's Jacobi-smoothed run, to the Newton
+    tolerance, with the same final active set."""
+    P, O, mat, omat, reg, oreg, phi = _sneddon_pair(cf, orc, d=3, K=10.0, n0=8, r=1, fixed=True)
+    out = {}
+    for sm in (0, 1):
+        st = cf.make_initial_state(P, mat)
+        o = cf.SolverOptions(operator_kind=opkind, amg=cf.AmgOptions(smoother=sm, chebyshev_degree=2))
+        rep = cf.newton_active_set_step(st, mat, P, reg, o)
+        assert rep["converged"] and rep["feasibility_violation"] <= 1e-10
+        out[sm] = (rep, st.get()["solution"])
+    (rj, xj), (rc, xc) = out[0], out[1]
+    assert np.abs(xc - xj).max() <= 1e-6 * np.abs(xj).max()
+    assert rc["iterations"][-1]["active_size"] == rj["iterations"][-1]["active_size"]
+    assert max(q["gmres_iterations"] for q in rc["iterations"]) <= 4 * max(q["gmres_iterations"]
+                                                                        for q in rj["iterations"])
