@@ -667,6 +667,11 @@ __global__ void k_same_prev(i64 rows, const i64* __restrict__ p, const int* __re
   if (lane == 0) head[i] = same ? 0 : 1;
 }
 
+__global__ void k_not_head(i64 rows, const int* __restrict__ head, unsigned char* __restrict__ same) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < rows) same[i] = head[i] ? 0 : 1;
+}
+
 // run start of each row: max over j <= i of (head[j] ? j : 0) via a max-scan of these keys
 __global__ void k_head_key(i64 rows, const int* __restrict__ head, int* __restrict__ key) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -800,6 +805,193 @@ __device__ __forceinline__ void num_grp_rows(double* __restrict__ Acc, const int
   }
 }
 
+// Runs of B rows: consecutive A positions k, k+1, .. (the d dofs of one mesh node, or the coarse
+// dofs of one aggregate) whose B rows repeat one column pattern (bsame[k + j]: row k + j has row
+// k + j - 1's columns) are applied together, up to MR rows per step: the lane of entry e loads its
+// column once and the m values (the rows are contiguous, row k + j at bp[k] + j n), finds the slot
+// once and adds the m products to each accumulator in ascending k — per C(i,j) the same
+// k-ascending sequence of IEEE additions as one position at a time (any split of the positions
+// into runs gives it), with a third of the steps, slot lookups and shared-memory updates.
+// The positions are taken in windows of 32: lane p loads position base + p's column k, B-row
+// offset and length and the group's A values there in one round, so a run's step waits only on its
+// own B entries; the runs of a window are the ballot of run starts (chain starts, and every MR-th
+// link of a chain).  B rows longer than 32 entries are taken 32 CH entries per load round.
+template <int NR, int MR, int CH>
+__device__ __forceinline__ void num_grp_runs(double* __restrict__ Acc, const int* __restrict__ T, unsigned mask,
+                                             int cap, int row0, int lane, const i64* __restrict__ ap,
+                                             const int* __restrict__ ac, const double* __restrict__ av,
+                                             const double* __restrict__ rs, const i64* __restrict__ bp,
+                                             const int* __restrict__ bc, const double* __restrict__ bv,
+                                             const unsigned char* __restrict__ bsame, double* __restrict__ wa,
+                                             i64* __restrict__ wq, int* __restrict__ wn) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const i64 a0 = ap[row0];
+  const int alen = int(ap[row0 + 1] - a0);
+  for (int base = 0; base < alen; base += 32) {
+    // the window's positions: B-row offsets and lengths and the group's A values, in shared memory
+    const int p = base + lane;
+    const bool in = p < alen;
+    int k = -1;
+    if (in) {
+      k = ac[a0 + p];
+      const i64 q0 = bp[k];
+      wq[lane] = q0;
+      wn[lane] = int(bp[k + 1] - q0);
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        wa[r * 32 + lane] = rs ? rs[row0 + r] * av[a0 + i64(r) * alen + p] : av[a0 + i64(r) * alen + p];
+    }
+    const int kprev = __shfl_up_sync(FULL, k, 1);
+    const bool link = in && lane > 0 && k == kprev + 1 && bsame[k];
+    const unsigned lm = __ballot_sync(FULL, link);
+    const unsigned nl = ~lm & __ballot_sync(FULL, in);
+    const int cs = 31 - __clz(nl & (FULL >> (31 - lane)));  // chain start (lane 0 is never a link)
+    unsigned starts = __ballot_sync(FULL, in && (lane - cs) % MR == 0);
+    __syncwarp();
+    // software pipeline over the window's runs: the first 32 entries of the next run are loaded
+    // while the current run is applied (longer rows: the rest is taken CH chunks per round)
+    auto run_len = [&](int st) {
+      return st < 31 ? 1 + min(MR - 1, __ffs(~(lm >> (st + 1))) - 1) : 1;
+    };
+    auto load0 = [&](int st, int m, int& col, double* b) {
+      const i64 rq = wq[st];
+      const int rn = wn[st];
+      if (lane < rn) {
+        col = bc[rq + lane];
+#pragma unroll
+        for (int j = 0; j < MR; ++j)
+          if (j < m) b[j] = bv[rq + i64(j) * rn + lane];
+      }
+    };
+    int pcol = 0;
+    double pb[MR];
+    int st = -1, m = 1;
+    if (starts) {
+      st = __ffs(starts) - 1;
+      starts &= starts - 1;
+      m = run_len(st);
+      load0(st, m, pcol, pb);
+    }
+    while (st >= 0) {
+      const i64 rq = wq[st];
+      const int rn = wn[st];
+      double ca[MR][NR];
+#pragma unroll
+      for (int j = 0; j < MR; ++j)
+        if (j < m) {
+#pragma unroll
+          for (int r = 0; r < NR; ++r) ca[j][r] = wa[r * 32 + st + j];
+        }
+      const int ccol = pcol;
+      double cb[MR];
+#pragma unroll
+      for (int j = 0; j < MR; ++j) cb[j] = pb[j];
+      const int cm = m;
+      // next run of the window: start its loads now
+      st = -1;
+      if (starts) {
+        st = __ffs(starts) - 1;
+        starts &= starts - 1;
+        m = run_len(st);
+        load0(st, m, pcol, pb);
+      }
+      if (lane < rn) {
+        const int sl = hfind(T, mask, ccol);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          double acc = Acc[size_t(r) * cap + sl];
+#pragma unroll
+          for (int j = 0; j < MR; ++j)
+            if (j < cm) acc += ca[j][r] * cb[j];
+          Acc[size_t(r) * cap + sl] = acc;
+        }
+      }
+      for (int c0 = 32; c0 < rn; c0 += 32 * CH) {
+        int col[CH];
+        double b[CH][MR];
+#pragma unroll
+        for (int h = 0; h < CH; ++h) {
+          const int e = c0 + h * 32 + lane;
+          if (e < rn) {
+            col[h] = bc[rq + e];
+#pragma unroll
+            for (int j = 0; j < MR; ++j)
+              if (j < cm) b[h][j] = bv[rq + i64(j) * rn + e];
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < CH; ++h) {
+          const int e = c0 + h * 32 + lane;
+          if (e < rn) {
+            const int sl = hfind(T, mask, col[h]);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+              double acc = Acc[size_t(r) * cap + sl];
+#pragma unroll
+              for (int j = 0; j < MR; ++j)
+                if (j < cm) acc += ca[j][r] * b[h][j];
+              Acc[size_t(r) * cap + sl] = acc;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncwarp();
+  }
+}
+
+// per-warp window scratch of the run kernel (after the hash tables): A values, B-row offsets, lengths
+#ifndef CF_RUN_MINB
+#define CF_RUN_MINB 4
+#endif
+#ifndef CF_RUN_MINB6
+#define CF_RUN_MINB6 2
+#endif
+constexpr size_t RUN_WIN_BYTES = size_t(GRP_MAX) * 32 * sizeof(double) + 32 * sizeof(i64) + 32 * sizeof(int);
+
+template <int NRMAX, int CH>
+__global__ void __launch_bounds__(256, NRMAX <= 3 ? CF_RUN_MINB : CF_RUN_MINB6) k_num_grp_run(const int* __restrict__ glist, int ng, const int* __restrict__ heads,
+                                                 const int* __restrict__ glen, int cap, int wpb, int gm,
+                                                 const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                 const double* __restrict__ av, const double* __restrict__ rs,
+                                                 const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                 const double* __restrict__ bv, const unsigned char* __restrict__ bsame,
+                                                 const i64* __restrict__ cp, const int* __restrict__ cc,
+                                                 double* __restrict__ cv) {
+  extern __shared__ double grp_sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 gi = i64(blockIdx.x) * wpb + w;
+  if (gi >= ng) return;
+  const int grp = glist[gi];
+  const int row0 = heads[grp], nr = glen[grp];
+  double* Acc = grp_sm + size_t(w) * cap * gm;
+  int* T = reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * gm) + size_t(w) * cap;
+  for (int s = lane; s < cap; s += 32) T[s] = EMPTY;
+  for (int s = lane; s < cap * nr; s += 32) Acc[s] = 0.0;
+  __syncwarp();
+  const unsigned mask = unsigned(cap) - 1u;
+  const i64 c0 = cp[row0];
+  const int nc = int(cp[row0 + 1] - c0);
+  for (int t = lane; t < nc; t += 32) hinsert(T, mask, cc[c0 + t]);
+  unsigned char* win = reinterpret_cast<unsigned char*>(reinterpret_cast<int*>(grp_sm + size_t(wpb) * cap * gm) +
+                                                        size_t(wpb) * cap) + size_t(w) * RUN_WIN_BYTES;
+  double* wa = reinterpret_cast<double*>(win);
+  i64* wq = reinterpret_cast<i64*>(win + size_t(GRP_MAX) * 32 * sizeof(double));
+  int* wn = reinterpret_cast<int*>(win + size_t(GRP_MAX) * 32 * sizeof(double) + 32 * sizeof(i64));
+  __syncwarp();
+  switch (nr) {
+#define CFB_NR(R) \
+  case R: if (R <= NRMAX) num_grp_runs<R <= NRMAX ? R : 1, 3, CH>(Acc, T, mask, cap, row0, lane, ap, ac, av, rs, bp, bc, bv, bsame, wa, wq, wn); break;
+    CFB_NR(1) CFB_NR(2) CFB_NR(3) CFB_NR(4) CFB_NR(5) CFB_NR(6)
+#undef CFB_NR
+  }
+  for (int t = lane; t < nc; t += 32) {
+    const int sl = hfind(T, mask, cc[c0 + t]);
+    for (int r = 0; r < nr; ++r) cv[c0 + i64(r) * nc + t] = Acc[size_t(r) * cap + sl];
+  }
+}
+
 template <int CB>
 __global__ void __launch_bounds__(256, CB >= 8 ? 2 : 3) k_num_grp(const int* __restrict__ glist, int ng, const int* __restrict__ heads,
                                                  const int* __restrict__ glen, int cap, int wpb, int gm,
@@ -916,14 +1108,26 @@ __global__ void __launch_bounds__(256) k_num_grp_short(const int* __restrict__ g
   }
 }
 
-// CB = 0: the short-row kernel (B rows of <= 8 entries)
+// CB = 0: the short-row kernel (B rows of <= 8 entries); bsame: the run kernel
 template <int CB>
 void num_grp_launch(const RowBin& b, int cap, const int* heads, const int* glen, const Csr& A, const Csr& B,
-                    const double* rs, Csr& C, int gm) {
+                    const double* rs, Csr& C, int gm, const unsigned char* bsame = nullptr) {
   if (!b.n) return;
   const size_t per_warp = size_t(cap) * (sizeof(int) + sizeof(double) * gm);
   const int wpb = int(std::min<size_t>(8, std::max<size_t>(1, (100u << 10) / per_warp)));
   const size_t sm = per_warp * wpb;
+  if (bsame) {
+    const size_t per_warp_r = per_warp + RUN_WIN_BYTES;
+    const int wpb = int(std::min<size_t>(8, std::max<size_t>(1, (100u << 10) / per_warp_r)));
+    const size_t sm = per_warp_r * wpb;
+    auto rk = gm <= 3 ? k_num_grp_run<3, 1> : k_num_grp_run<6, 1>;
+    CF_CUDA(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    rk<<<grid_for(b.n, wpb), wpb * 32, sm, stream()>>>(b.list.p, b.n, heads, glen, cap, wpb, gm, A.ptr.p, A.col.p,
+                                                      A.val.p, rs, B.ptr.p, B.col.p, B.val.p, bsame, C.ptr.p,
+                                                      C.col.p, C.val.p);
+    CF_LAUNCHED();
+    return;
+  }
   auto kern = CB == 0 ? k_num_grp_short : k_num_grp<CB == 0 ? 1 : CB>;
   CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
   kern<<<grid_for(b.n, wpb), wpb * 32, sm, stream()>>>(b.list.p, b.n, heads, glen, cap, wpb, gm, A.ptr.p, A.col.p,
@@ -1366,13 +1570,26 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
       CF_LAUNCHED();
       const int caps[3] = {128, 256, 512};
       const i64 lims[4] = {0, 96, 192, 384};
+      // runs of B rows with one pattern (CF_SPGEMM_NO_RUNS=1: one position at a time; A/B switch)
+      static const bool no_runs = std::getenv("CF_SPGEMM_NO_RUNS") != nullptr;
+      DevBuf<unsigned char> bsame;
+      static const bool short_runs = std::getenv("CF_SPGEMM_SHORT_RUNS") != nullptr;  // A/B switch
+      if (!no_runs && (short_runs || !(maxb <= 8 && !no_short)) && B.rows > 1) {
+        DevBuf<int> bh(B.rows);
+        k_same_prev<<<grid_for(B.rows * 32, 256), 256, 0, stream()>>>(B.rows, B.ptr.p, B.col.p, bh.p);
+        CF_LAUNCHED();
+        bsame.alloc(B.rows);
+        k_not_head<<<grid_for(B.rows, 256), 256, 0, stream()>>>(B.rows, bh.p, bsame.p);
+        CF_LAUNCHED();
+      }
+      const unsigned char* bs = bsame.n ? bsame.p : nullptr;
       for (int t = 0; t < 3; ++t) {
         RowBin b = make_bin(ng, gl.p, lims[t], lims[t + 1]);
-        if (maxb <= 8 && !no_short) num_grp_launch<0>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
-        else if (maxb <= 32) num_grp_launch<1>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
-        else if (maxb <= 64) num_grp_launch<2>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
-        else if (maxb <= 128) num_grp_launch<4>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
-        else num_grp_launch<8>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax);
+        if (maxb <= 8 && !no_short) num_grp_launch<0>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax, bs);
+        else if (maxb <= 32) num_grp_launch<1>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax, bs);
+        else if (maxb <= 64) num_grp_launch<2>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax, bs);
+        else if (maxb <= 128) num_grp_launch<4>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax, bs);
+        else num_grp_launch<8>(b, caps[t], heads.p, glen.p, A, B, row_scale, *C, gmax, bs);
       }
       RowBin big = make_bin(ng, gl.p, 384, LLONG_MAX);
       if (big.n) {
