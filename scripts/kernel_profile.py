@@ -34,7 +34,7 @@ rows.sort(reverse=True)
 tot = sum(r[0] for r in rows)
 print(json.dumps(rep["times_ms"]))
 print(f"total kernel time {tot:.1f} ms over {sum(r[1] for r in rows)} launches")
-for t, c, k in rows[:40]:
+for t, c, k in rows[:int(os.environ.get("TOPN", "40"))]:
     print(f"{t:9.2f} ms {100 * t / tot:5.1f}% {c:7d}  {k[:110]}")
 os.makedirs("gpurun_out", exist_ok=True)
 with open(f"gpurun_out/kernels_{name}.json", "w") as f:
