@@ -88,8 +88,19 @@ struct StencilCols {
   double inv_nn = 0.0;
 };
 
+// Runs of consecutive rows with one column pattern (the dofs of a mesh node, the coarse dofs of an
+// aggregate), chunked to <= gmax rows: group g is rows heads[g] .. heads[g] + len[g] - 1, stored
+// contiguously with equal lengths.  Set on the AMG level operators (A of levels >= 1, P, R), where
+// the SpMV reads each group's column indices and x entries once for all its rows.
+struct RowGroups {
+  DevBuf<int> heads, len;
+  i64 n = 0;
+  int gmax = 1;
+};
+
 struct Csr {
   i64 rows = 0, cols = 0, nnz = 0;
+  std::shared_ptr<RowGroups> grp;  // optional (SpMV only; the pattern must not change while set)
   StencilCols st;
   DevBuf<i64> ptr;
   DevBuf<int> col;

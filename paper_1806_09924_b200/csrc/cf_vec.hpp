@@ -63,6 +63,9 @@ void multi_axpy(double* w, const double* V, i64 ld, int k, const double* coef_de
 // ---- spgemm.cu: CSR utilities (deterministic)
 std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale = nullptr);  // diag(s) A B
 std::unique_ptr<Csr> transpose(const Csr& A);
+// row groups of A (runs of equal-pattern rows, <= gmax rows each); null when they would not pay
+// (fewer than 4/3 rows per group on average, or short rows)
+std::shared_ptr<RowGroups> csr_row_groups(const Csr& A, int gmax);
 // P = T - w * DAT (union pattern), entries with |v| <= 1e-300 removed
 std::unique_ptr<Csr> csr_axpy_prune(const Csr& T, double w, const Csr& DAT);
 void csr_prune(Csr& A);  // in place (Eigen prune(1.0, 1e-300))

@@ -1613,6 +1613,48 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   return C;
 }
 
+std::shared_ptr<RowGroups> csr_row_groups(const Csr& A, int gmax) {
+  const i64 m = A.rows;
+  if (m < 1024 || m >= INT_MAX || A.nnz < 8 * m || gmax < 2) return nullptr;
+  DevBuf<int> head(m), key(m), runstart(m);
+  k_same_prev<<<grid_for(m * 32, 256), 256, 0, stream()>>>(m, A.ptr.p, A.col.p, head.p);
+  CF_LAUNCHED();
+  k_head_key<<<grid_for(m, 256), 256, 0, stream()>>>(m, head.p, key.p);
+  CF_LAUNCHED();
+  {
+    size_t bytes = 0;
+    CF_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, key.p, runstart.p, cub::Max(), m, stream()));
+    DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+    CF_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, bytes, key.p, runstart.p, cub::Max(), m, stream()));
+    count_launch();
+  }
+  k_chunk_heads<<<grid_for(m, 256), 256, 0, stream()>>>(m, runstart.p, gmax, head.p);
+  CF_LAUNCHED();
+  auto g = std::make_shared<RowGroups>();
+  g->heads.alloc(m);
+  DevBuf<int> nsel(1);
+  {
+    size_t bytes = 0;
+    thrust::counting_iterator<int> it(0);
+    CF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, head.p, g->heads.p, nsel.p, m, stream()));
+    DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+    CF_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, head.p, g->heads.p, nsel.p, m, stream()));
+    count_launch();
+  }
+  const int ng = read_int(nsel.p);
+  if (double(ng) * 4.0 > double(m) * 3.0) return nullptr;
+  g->n = ng;
+  g->len.alloc(ng);
+  k_group_len<<<grid_for(ng, 256), 256, 0, stream()>>>(ng, g->heads.p, m, g->len.p);
+  CF_LAUNCHED();
+  DevBuf<int> mx(1);
+  mx.zero();
+  k_max_int<<<int(std::min<i64>(1024, grid_for(ng, 256))), 256, 0, stream()>>>(ng, g->len.p, mx.p);
+  CF_LAUNCHED();
+  g->gmax = read_int(mx.p);
+  return g;
+}
+
 // ------------------------------------------------------------------ transpose (stable)
 namespace {
 __global__ void k_iota64(i64 n, i64* out) {

@@ -98,6 +98,64 @@ __global__ void __launch_bounds__(256) k_spmv_b(i64 rows, const i64* __restrict_
   if (row < rows && lane == 0) y[row] = epi_out(ep, x, row, s);
 }
 
+// k_spmv_b over row groups (RowGroups): TPR lanes per group, each lane loads a column index and
+// its x entry once and applies them to every row of the group; per row the lane's partial sum
+// runs over the same entries in the same order as k_spmv_b's, and the TPR-lane reduction and
+// epilogue are the same, so each y[row] is bitwise k_spmv_b's.
+template <int TPR, int U, int GM>
+__global__ void __launch_bounds__(256) k_spmv_grp(i64 ng, const int* __restrict__ heads,
+                                                  const int* __restrict__ glen, const i64* __restrict__ ptr,
+                                                  const int* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ x, double* y, SpmvEpi ep) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 gi = t / TPR;
+  const int lane = int(t % TPR);
+  double s[GM];
+#pragma unroll
+  for (int r = 0; r < GM; ++r) s[r] = 0.0;
+  i64 h = 0;
+  int g = 0;
+  if (gi < ng) {
+    h = heads[gi];
+    g = glen[gi];
+    const i64 b0 = ptr[h];
+    const i64 n = ptr[h + 1] - b0;
+    for (i64 k0 = lane; k0 < n; k0 += i64(TPR) * U) {
+      // every load of the step is issued before the first product (in-order issue would otherwise
+      // stall each row's value loads behind the previous row's x gathers)
+      double xv[U], v[GM][U];
+      int c[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const i64 e = k0 + i64(j) * TPR;
+        c[j] = e < n ? ld_stream(col + b0 + e) : -1;
+      }
+#pragma unroll
+      for (int r = 0; r < GM; ++r)
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          const i64 e = k0 + i64(j) * TPR;
+          v[r][j] = (r < g && e < n) ? ld_stream(val + b0 + i64(r) * n + e) : 0.0;
+        }
+#pragma unroll
+      for (int j = 0; j < U; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+      for (int r = 0; r < GM; ++r)
+        if (r < g) {
+#pragma unroll
+          for (int j = 0; j < U; ++j) s[r] += v[r][j] * xv[j];
+        }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < GM; ++r) s[r] = group_sum<TPR>(s[r]);
+  if (gi < ng && lane == 0) {
+#pragma unroll
+    for (int r = 0; r < GM; ++r)
+      if (r < g) y[h + r] = epi_out(ep, x, h + r, s[r]);
+  }
+}
+
 template <int TPR, int U>
 __device__ __forceinline__ double row_dot_b(const i64* __restrict__ ptr, const int* __restrict__ col,
                                             const double* __restrict__ val, const double* __restrict__ x, i64 row,
@@ -784,9 +842,31 @@ bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double
 
 // Variant table from the B200 sweep (scripts/spmv_sweep.py, profiles/r01_spmv_sweep.json):
 // one batch of TPR*U slots should cover a typical row.
+template <int TPR, int U>
+void launch_grp(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
+  const RowGroups& G = *A.grp;
+  const i64 threads = G.n * TPR;
+  if (G.gmax <= 3)
+    k_spmv_grp<TPR, U, 3><<<grid_for(threads, 256), 256, 0, stream()>>>(G.n, G.heads.p, G.len.p, A.ptr.p, A.col.p,
+                                                                        A.val.p, x, y, ep);
+  else
+    k_spmv_grp<TPR, U, 6><<<grid_for(threads, 256), 256, 0, stream()>>>(G.n, G.heads.p, G.len.p, A.ptr.p, A.col.p,
+                                                                        A.val.p, x, y, ep);
+  CF_LAUNCHED();
+}
+
 void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
   if (A.rows == 0) return;
   const double mean = A.mean_hint >= 0.0 ? A.mean_hint : double(A.nnz) / double(A.rows);
+  // row groups (AMG level operators): CF_SPMV_NO_GROUPS=1 reads them row by row (A/B switch)
+  static const bool no_groups = std::getenv("CF_SPMV_NO_GROUPS") != nullptr;
+  if (A.grp && A.grp->gmax <= 6 && A.st.kind == 0 && !no_groups) {
+    if (mean > 64) launch_grp<16, 4>(A, x, y, ep);
+    else if (mean > 24) launch_grp<8, 4>(A, x, y, ep);
+    else if (mean > 12) launch_grp<4, 5>(A, x, y, ep);
+    else launch_grp<4, 3>(A, x, y, ep);
+    return;
+  }
   if (mean > 64) launch_b<16, 4>(A, x, y, ep);
   else if (mean > 24) launch_b<8, 4>(A, x, y, ep);
   else if (mean > 12) launch_b<4, 5>(A, x, y, ep);
