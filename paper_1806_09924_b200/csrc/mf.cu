@@ -436,6 +436,176 @@ __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g,
   }
 }
 
+// k_mf_sweep with the vertex planes staged by cp.async two layers ahead: a ring of four planes
+// (the layer's two, the one the constrained rows of the previous vertex plane read, the one in
+// flight), u of constrained components zeroed by the thread that copied it once its copy landed
+// (flags held in registers meanwhile), one cell-output buffer.  The cell arithmetic and every
+// sum are k_mf_sweep's, so the output is bitwise the same.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = unsigned(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep_async(GridDesc g, const Tables* __restrict__ T, double mu,
+                                                         double lam, double kap, double xi0, double xi1,
+                                                         double scale, int zseg, int pz_lo, int pz_hi, i64 x_off,
+                                                         i64 y_lo, i64 y_hi, const double* __restrict__ x,
+                                                         const double* __restrict__ pt,
+                                                         const std::uint8_t* __restrict__ flag,
+                                                         double* __restrict__ y, SpmvEpi ep) {
+  constexpr int PL = MFT * MFT;           // vertices of one tile plane
+  constexpr int VPT = (PL + MF_THREADS - 1) / MF_THREADS;  // plane vertices per thread (2)
+  __shared__ double su[4][PL * 3], sp[4][PL];  // vertex planes z mod 4
+  __shared__ double co[MFC * MFC * MF_CS];     // the layer's cell outputs
+  const int nn = int(g.nn), nc = int(g.nc);
+  const int nbx = (nn + MFB - 1) / MFB;
+  const int col = blockIdx.x % (nbx * nbx), seg = blockIdx.x / (nbx * nbx);
+  const int x0 = (col % nbx) * MFB, y0 = (col / nbx) * MFB;
+  const int zv0 = pz_lo + seg * zseg, zv1 = min(pz_hi, zv0 + zseg);  // owned vertex planes [zv0, zv1)
+  // copy plane vz into its slot; returns this thread's constrained-component bits (3 per vertex)
+  struct Fl {
+    std::uint8_t b[VPT * 3];
+  };
+  auto issue = [&](int vz) {
+    const int sl = vz & 3;
+    Fl fm;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int t = threadIdx.x + q * MF_THREADS;
+      if (t < PL) {
+        const int vx = x0 - 1 + t % MFT, vy = y0 - 1 + t / MFT;
+        const bool in = vx >= 0 && vy >= 0 && vz >= 0 && vx < nn && vy < nn && vz < nn;
+        const i64 v = in ? i64(vx) + i64(nn) * (i64(vy) + i64(nn) * vz) : 0;
+        const double* xs = in ? x + (v - x_off) * 3 : x;
+        cp_async8(&su[sl][t * 3], xs, in);
+        cp_async8(&su[sl][t * 3 + 1], in ? xs + 1 : x, in);
+        cp_async8(&su[sl][t * 3 + 2], in ? xs + 2 : x, in);
+        cp_async8(&sp[sl][t], in ? pt + v : pt, in);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) fm.b[3 * q + a] = in ? flag[v * 3 + a] : std::uint8_t(0);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) fm.b[3 * q + a] = 0;
+      }
+    }
+    cp_async_commit();
+    return fm;
+  };
+  // after this thread's copy of plane vz landed: zero its constrained u components
+  auto mask = [&](int vz, const Fl& fm) {
+    const int sl = vz & 3;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int t = threadIdx.x + q * MF_THREADS;
+      if (t < PL) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          if (fm.b[3 * q + a]) su[sl][t * 3 + a] = 0.0;
+      }
+    }
+  };
+  const Fl f0 = issue(zv0 - 1);  // plane L
+  Fl f1 = issue(zv0);            // plane L + 1
+  double top[3] = {0.0, 0.0, 0.0};  // this thread's vertex: the k = 4..7 corners (layer below)
+  for (int L = zv0 - 1; L < zv1; ++L) {  // cell layer L lies between vertex planes L and L + 1
+    cp_async_wait<0>();  // plane L + 1 landed (this thread's part)
+    if (L == zv0 - 1) mask(L, f0);
+    mask(L + 1, f1);
+    // one barrier publishes plane L + 1 and retires layer L - 1's vertex phase (the last reader
+    // of plane L - 2's slot and of the cell outputs), so plane L + 2 goes in flight behind it
+    __syncthreads();
+    Fl f2 = {};
+    if (L + 2 <= zv1) f2 = issue(L + 2);
+    {
+      const int c = threadIdx.x;
+      if (c < MFC * MFC) {
+        double* o = co + c * MF_CS;
+        const int cx = c % MFC, cy = c / MFC;
+        const int gx = x0 - 1 + cx, gy = y0 - 1 + cy;
+        if (gx < 0 || gy < 0 || L < 0 || gx >= nc || gy >= nc || L >= nc) {
+#pragma unroll
+          for (int e = 0; e < 24; ++e) o[e] = 0.0;
+        } else {
+          const int s0 = L & 3, s1 = (L + 1) & 3;
+          auto U = [&](int i, int j, int l, int a) { return su[l ? s1 : s0][((cx + i) + MFT * (cy + j)) * 3 + a]; };
+          auto P = [&](int i, int j, int l) { return sp[l ? s1 : s0][(cx + i) + MFT * (cy + j)]; };
+          mf_cell(U, P, xi0, xi1, mu, lam, kap, scale, o);
+        }
+      }
+    }
+    __syncthreads();
+    // vertex plane L (if owned): k = 0..3 from layer L after the carried k = 4..7 of layer L - 1;
+    // then carry this layer's k = 4..7 for plane L + 1
+    const int t = threadIdx.x;
+    if (t < MFB * MFB) {
+      const int lx = t % MFB, ly = t / MFB;
+      const int vx = x0 + lx, vy = y0 + ly;
+      const double* cl = co;
+      const i64 vglob = i64(vx) + i64(nn) * (i64(vy) + i64(nn) * L);
+      if (L >= zv0 && vx < nn && vy < nn && vglob >= y_lo && vglob < y_hi) {
+        double acc[3] = {top[0], top[1], top[2]};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int cx = lx + 1 - (k & 1), cy = ly + 1 - ((k >> 1) & 1);
+          const double* o = cl + (cx + MFC * cy) * MF_CS + k * 3;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) acc[a] += o[a];
+        }
+        const int vz = L;
+        const i64 v = vglob, r0 = (v - y_lo) * 3;
+        const bool con = flag[v * 3] | flag[v * 3 + 1] | flag[v * 3 + 2];
+        if (!con) {
+#pragma unroll
+          for (int a = 0; a < 3; ++a) y[r0 + a] = mf_epi(ep, x, r0 + a, acc[a]);
+        } else {  // a constrained row keeps the summed element diagonal (model.cpp:295-300): y = d x
+          double dg[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
+          for (int k = 0; k < 8; ++k) {
+            const int gx = vx - (k & 1), gy = vy - ((k >> 1) & 1), gz = vz - ((k >> 2) & 1);
+            if (gx < 0 || gy < 0 || gz < 0 || gx >= nc || gy >= nc || gz >= nc) continue;
+            const int cx = lx + 1 - (k & 1), cy = ly + 1 - ((k >> 1) & 1);
+            double pc[8];
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) pc[kk] = sp[(gz + ((kk >> 2) & 1)) & 3][(cx + (kk & 1)) + MFT * (cy + ((kk >> 1) & 1))];
+#pragma unroll 1
+            for (int q = 0; q < 8; ++q) {
+              double ph = 0.0;
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) ph += T->s[q][kk] * pc[kk];
+              const double wg = T->w[q] * ((1.0 - kap) * ph * ph + kap);
+              double gg = 0.0;
+#pragma unroll
+              for (int b = 0; b < 3; ++b) gg += T->gp[q][k][b] * T->gp[q][k][b];
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                const double da = T->gp[q][k][a];
+                dg[a] += wg * (mu * (gg + da * da) + lam * da * da);
+              }
+            }
+          }
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+            y[r0 + a] = mf_epi(ep, x, r0 + a, flag[v * 3 + a] ? dg[a] * x[(v - x_off) * 3 + a] : acc[a]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) top[a] = 0.0;
+#pragma unroll
+      for (int k = 4; k < 8; ++k) {
+        const int cx = lx + 1 - (k & 1), cy = ly + 1 - ((k >> 1) & 1);
+        const double* o = cl + (cx + MFC * cy) * MF_CS + k * 3;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) top[a] += o[a];
+      }
+    }
+    f1 = f2;
+  }
+  cp_async_wait<0>();
+}
+
 // FP64 FMA throughput probe ("measure FP64 with a DFMA loop")
 __global__ void k_dfma(double* out, int iters) {
   double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
@@ -472,9 +642,11 @@ void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep) {
   const int nseg = (pz_hi - pz_lo + zseg - 1) / zseg;
   const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
   const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
-  k_mf_sweep<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1,
-                                                          W / (g.h * g.h), zseg, pz_lo, pz_hi, op.x_off, y_lo, y_hi,
-                                                          x, op.pt, op.flag, y, ep);
+  static const bool sync_loads = std::getenv("CF_MF_SYNC_LOADS") != nullptr;  // A/B: plain plane loads
+  auto kern = sync_loads ? k_mf_sweep : k_mf_sweep_async;
+  kern<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1,
+                                                    W / (g.h * g.h), zseg, pz_lo, pz_hi, op.x_off, y_lo, y_hi,
+                                                    x, op.pt, op.flag, y, ep);
   CF_LAUNCHED();
 }
 
