@@ -1527,6 +1527,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
       k_n2w<<<grid_for(nl, N2WPB), N2WPB * 32, 0, stream()>>>(nl, nlist.p, sptr.p, sidx.p, tptr.p, tidx.p, lower.p,
                                                               uptr.p, nullptr, nullptr, 0, ovf.p, ups.p, redo.p);
     CF_LAUNCHED();
+    clk.mark("S^T + N2 count");
     OvfList big2 = make_ovf_list(n_nodes, ovf.p);
     DevBuf<i64> noff;
     DevBuf<int> nkeys;
@@ -1560,8 +1561,14 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
       CF_LAUNCHED();
     }
     nkeys.release();
-    if (clk.on) std::fprintf(stderr, "[amg L%d] n2: listed %d, global-tier %lld, strength global-tier %lld, upper %lld\n",
-                             lev, nl, (long long)big2.n, (long long)big.n, (long long)nup);
+    if (clk.on) {
+      std::vector<int> rd(n_nodes);
+      if (n_nodes) CF_CUDA(cudaMemcpy(rd.data(), redo.p, size_t(n_nodes) * sizeof(int), cudaMemcpyDeviceToHost));
+      long long nredo = 0;
+      for (int v : rd) nredo += v != 0;
+      std::fprintf(stderr, "[amg L%d] n2: listed %d, global-tier %lld, strength global-tier %lld, upper %lld, redo %lld\n",
+                   lev, nl, (long long)big2.n, (long long)big.n, (long long)nup, nredo);
+    }
     clk.mark("S^T + N2");
     // pass 1: lexicographically-first MIS of N2 (persistent cooperative frontier kernel)
     DevBuf<int> status(n_nodes), f0(n_nodes), f1(n_nodes), sizes(3), rounds(1);

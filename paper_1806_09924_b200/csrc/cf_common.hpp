@@ -48,6 +48,33 @@ struct Runtime {
 Runtime& rt();
 void ensure_device();  // throws CF_ERR_CUDA when no device is usable (no CPU fallback)
 inline cudaStream_t stream() { return rt().stream; }
+// Enqueue f's kernels on the auxiliary stream, forked from the library stream at this point (f
+// must not allocate: the caching allocator relies on one stream order); aux_join() makes the
+// library stream wait for them.  Independent outputs only: the results are those of running f
+// in sequence.
+template <class F>
+void on_aux(F&& f) {
+  Runtime& R = rt();
+  if (!R.aux) {
+    CF_CUDA(cudaStreamCreateWithFlags(&R.aux, cudaStreamNonBlocking));
+    CF_CUDA(cudaEventCreateWithFlags(&R.ev_fork, cudaEventDisableTiming));
+    CF_CUDA(cudaEventCreateWithFlags(&R.ev_join, cudaEventDisableTiming));
+  }
+  const cudaStream_t main = R.stream;
+  CF_CUDA(cudaEventRecord(R.ev_fork, main));
+  CF_CUDA(cudaStreamWaitEvent(R.aux, R.ev_fork, 0));
+  R.stream = R.aux;
+  try {
+    f();
+  } catch (...) {
+    R.stream = main;
+    throw;
+  }
+  R.stream = main;
+  CF_CUDA(cudaEventRecord(R.ev_join, R.aux));
+}
+inline void aux_join() { CF_CUDA(cudaStreamWaitEvent(rt().stream, rt().ev_join, 0)); }
+
 // host round trips of the library stream (diagnostics: CF_TIMING prints them per AMG build)
 inline long& host_sync_count() {
   static long n = 0;

@@ -22,7 +22,7 @@ def main():
     mat = cf.Material(eps_mode=1, eps_fixed=2 * P.h, kappa_factor=1e-12 / P.h)
     reg = cf.resolve_regularization(P, mat, cf.slit_band_edge(P, mat))
     st = cf.make_initial_state(P, mat)
-    reps = cf.solve_loading_sequence(st, mat, P, reg, cf.SolverOptions(gmres=gm, operator_kind=0), steps)
+    reps = cf.solve_loading_sequence(st, mat, P, reg, cf.SolverOptions(gmres=gm, operator_kind=int(os.environ.get("CF_RUNNER_OPKIND", "0"))), steps)
     x = np.ascontiguousarray(st.get()["solution"])
     its = [[[i["residual_norm"], i["active_size"], i["set_changes"], i["gmres_iterations"]] for i in rp["iterations"]]
            for rp in reps]
