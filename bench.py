@@ -363,7 +363,7 @@ def operator_leg(cf, device, stream, applies=20):
     peak, src = peak_hbm()
     gbs = nb / (ms * 1e-3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_spmv_st_cfg1_ncu.json" if fmt == "stencil" else "r01_spmv_cfg1_ncu.json")
+    tp = os.path.join(ROOT, "profiles", "r02_spmv_st16t_cfg1_ncu.json" if fmt == "stencil" else "r01_spmv_cfg1_ncu.json")
     if os.path.exists(tp):
         tj = json.load(open(tp))
         if tj.get("format", "csr") == fmt:  # only a capture of the kernel measured here
@@ -379,7 +379,7 @@ def operator_leg(cf, device, stream, applies=20):
     torch.cuda.empty_cache()
     return res, {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                  "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
-                 "kernel": ("k_spmv_st16p (stencil-implicit columns, M_uu of config 1)" if fmt == "stencil"
+                 "kernel": ("k_spmv_st16t (TMA-fed value/x ring, stencil-implicit columns, M_uu of config 1)" if fmt == "stencil"
                             else "k_spmv_b<16,4> (CSR SpMV, M_uu of config 1)"), "bytes_per_launch": nb,
                  "ms_per_launch": ms, "peak_source": src}
 

@@ -22,9 +22,7 @@ template <class T>
 std::vector<T> dl(const T* p, i64 n) {
   std::vector<T> h(size_t(std::max<i64>(n, 0)));
   if (n > 0) {
-    CF_CUDA(cudaMemcpyAsync(h.data(), p, size_t(n) * sizeof(T), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    ++host_sync_count();
+    read_small(h.data(), p, size_t(n) * sizeof(T));
   }
   return h;
 }

@@ -49,9 +49,7 @@ void scan_excl(T* data, i64 n_plus_1) {
 template <class T>
 T read_dev(const T* p) {
   T h{};
-  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, p, sizeof(T));
   return h;
 }
 
@@ -941,6 +939,55 @@ __global__ void k_build_Bc(i64 na, int m, const i64* __restrict__ aptr, const in
   }
 }
 
+// ---- empty coarse nodes (DESIGN.md §4 K7) --------------------------------------------------------
+// A level's nodes are the previous level's aggregates, and an aggregate whose near-nullspace block
+// has rank 0 (every constrained phi dof is one) carries no coarse dof: in the reference it is an
+// isolated node and seeds its own, again empty, aggregate in pass 1 (linsolve.cpp:146-154).  The
+// build runs on the non-empty nodes only (ascending order kept, so every aggregate keeps its place
+// among the others) and restores the reference numbering for what it reports: nodes counted with
+// the empty ones, pass-1 aggregates numbered over all roots by ascending node id.
+__global__ void k_nonempty_flags(i64 na, const int* __restrict__ rank, int* __restrict__ f) {
+  const i64 a = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a < na) f[a] = rank[a] > 0 ? 1 : 0;
+}
+// compact id -> reference id of the next level's nodes (aorig: this level's compact -> reference
+// aggregate ids, null = identity)
+__global__ void k_compact_orig(i64 na, const int* __restrict__ rank, const int* __restrict__ cid,
+                               const int* __restrict__ aorig, int* __restrict__ orig_next) {
+  const i64 a = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a < na && rank[a] > 0) orig_next[cid[a]] = aorig ? aorig[a] : int(a);
+}
+__global__ void k_renumber(i64 n, const int* __restrict__ cid, int* __restrict__ node) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) node[i] = cid[node[i]];
+}
+__global__ void k_fill_ones(i64 n, int* __restrict__ f) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = 1;
+}
+// root flags over the reference node numbering (empty nodes are roots) and each pass-1 aggregate's root
+__global__ void k_root_scatter(i64 nn, const int* __restrict__ status, const int* __restrict__ rootid,
+                               const int* __restrict__ orig, int* __restrict__ rflag, int* __restrict__ root_of_agg) {
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= nn) return;
+  const bool root = status[c] == ROOT;
+  rflag[orig[c]] = root ? 1 : 0;
+  if (root) root_of_agg[rootid[c]] = int(c);
+}
+// reference id of compact aggregate a: pass-1 aggregates by their root's rank among all roots,
+// pass-3 singletons after all pass-1 aggregates
+__global__ void k_agg_orig(i64 na, int n1, const int* __restrict__ root_of_agg, const int* __restrict__ orig,
+                           const int* __restrict__ rid, i64 nn_orig, int* __restrict__ aorig) {
+  const i64 a = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= na) return;
+  aorig[a] = a < n1 ? rid[orig[root_of_agg[a]]] : rid[nn_orig] + int(a - n1);
+}
+__global__ void k_agg_full(i64 nn, const int* __restrict__ agg, const int* __restrict__ orig,
+                           const int* __restrict__ aorig, int* __restrict__ agg_full) {
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < nn) agg_full[orig[c]] = aorig[agg[c]];
+}
+
 __global__ void k_inv_diag(i64 n, double* d) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) d[i] = d[i] != 0.0 ? 1.0 / d[i] : 0.0;
@@ -1292,9 +1339,7 @@ double estimate_lambda_max(const Csr& A, const double* inv_diag) {  // linsolve.
     vdiv_dev(w.p, s, v.p, n);
   }
   double st[2];
-  CF_CUDA(cudaMemcpyAsync(st, s + 2, sizeof(st), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(st, s + 2, sizeof(st));
   if (st[1] != 0.0) return 1.0;
   return std::max(st[0], 1e-12);
 }
@@ -1322,9 +1367,7 @@ void DenseLu::factor_from_csr(const Csr& A) {
     int h_off = 0;
     unsigned long long h_mn = 0;
     CF_CUDA(cudaMemcpyAsync(&h_off, off.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaMemcpyAsync(&h_mn, mn.p, sizeof(h_mn), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    ++host_sync_count();
+    read_small(&h_mn, mn.p, sizeof(h_mn));
     if (!h_off) {  // a diagonal coarsest matrix: the LU is the diagonal itself
       std::memcpy(&min_abs_pivot, &h_mn, sizeof(double));
       diagonal = true;
@@ -1413,6 +1456,9 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
   }
   DevBuf<int> err(1);
   PhaseClock clk;
+  // compact -> reference node ids of the current level (empty: identity, no empty nodes)
+  DevBuf<int> orig_of_c;
+  static const bool no_compact = std::getenv("CF_AMG_NO_COMPACT") != nullptr;  // A/B switch
   for (int lev = 0; lev < opts.max_levels; ++lev) {
     clk.lev = lev;
     const i64 n = A->rows;
@@ -1427,6 +1473,12 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
       CF_CUDA(cub::DeviceReduce::Max(tmp.p, bytes, nod.p, mx.p, n, stream()));
       count_launch();
       n_nodes = i64(read_dev(mx.p)) + 1;
+    }
+    // the reference's node count includes the empty nodes below the last non-empty one
+    i64 n_nodes_ref = n_nodes;
+    if (orig_of_c.n > 0) {
+      n_nodes_ref = i64(read_dev(orig_of_c.p + n_nodes - 1)) + 1;
+      if (n_nodes_ref == n_nodes) orig_of_c.release();  // no empty node: identity
     }
     // strength graph S (ascending neighbour lists)
     DevBuf<i64> nptr;
@@ -1605,13 +1657,22 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     k_claim<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, status.p, rootid.p, sptr.p, sidx.p, agg1.p);
     CF_LAUNCHED();
     // pass 2 (ordered fix point) and pass 3 (new singletons, ascending)
-    DevBuf<int> p2(n_nodes), changed(1);
+    // (a sweep that changes nothing leaves every later sweep without effect, so sweeps run in
+    // batches of P2B with one flag each and one host round trip per batch)
+    constexpr int P2B = 4;
+    DevBuf<int> p2(n_nodes), changed(P2B);
     CF_CUDA(cudaMemsetAsync(p2.p, 0xff, size_t(n_nodes) * sizeof(int), stream()));
-    for (int guard = 0;; ++guard) {
+    for (i64 guard = 0;; guard += P2B) {
       changed.zero();
-      k_pass2<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, sptr.p, sidx.p, agg1.p, p2.p, changed.p);
-      CF_LAUNCHED();
-      if (!read_dev(changed.p)) break;
+      for (int b = 0; b < P2B; ++b) {
+        k_pass2<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, sptr.p, sidx.p, agg1.p, p2.p, changed.p + b);
+        CF_LAUNCHED();
+      }
+      int hc[P2B];
+      read_small(hc, changed.p, sizeof(hc));
+      bool done = false;
+      for (int b = 0; b < P2B; ++b) done = done || hc[b] == 0;
+      if (done) break;
       if (guard > n_nodes + 2) fail(CF_ERR_LOGIC, "build_amg: pass-2 resolution did not converge");
     }
     DevBuf<int> p3(n_nodes + 1), agg(n_nodes);
@@ -1623,7 +1684,28 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     k_final_agg<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, agg1.p, p2.p, p3.p, n1, agg.p);
     CF_LAUNCHED();
     const i64 n_agg = i64(n1) + n3;
-    if (n_agg >= n_nodes && n_nodes > 1) break;  // no coarsening possible (linsolve.cpp:203)
+    if (n_agg >= n_nodes && n_nodes_ref > 1) break;  // no coarsening possible (linsolve.cpp:203)
+    // reference numbering of the aggregates when empty nodes were left out
+    DevBuf<int> aorig, agg_ref;
+    if (orig_of_c.n > 0) {
+      DevBuf<int> rid(n_nodes_ref + 1), root_of_agg(std::max(n1, 1));
+      k_fill_ones<<<grid_for(n_nodes_ref, 256), 256, 0, stream()>>>(n_nodes_ref, rid.p);
+      CF_LAUNCHED();
+      CF_CUDA(cudaMemsetAsync(rid.p + n_nodes_ref, 0, sizeof(int), stream()));
+      k_root_scatter<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, status.p, rootid.p, orig_of_c.p, rid.p,
+                                                                   root_of_agg.p);
+      CF_LAUNCHED();
+      scan_excl(rid.p, n_nodes_ref + 1);  // rid[i]: roots below i; rid[n_nodes_ref]: all pass-1 aggregates
+      aorig.alloc(n_agg);
+      k_agg_orig<<<grid_for(n_agg, 256), 256, 0, stream()>>>(n_agg, n1, root_of_agg.p, orig_of_c.p, rid.p,
+                                                             n_nodes_ref, aorig.p);
+      CF_LAUNCHED();
+      agg_ref.alloc(n_nodes_ref);
+      CF_CUDA(cudaMemcpyAsync(agg_ref.p, rid.p, size_t(n_nodes_ref) * sizeof(int), cudaMemcpyDeviceToDevice,
+                              stream()));  // an empty node's aggregate: its rank among the roots
+      k_agg_full<<<grid_for(n_nodes, 256), 256, 0, stream()>>>(n_nodes, agg.p, orig_of_c.p, aorig.p, agg_ref.p);
+      CF_LAUNCHED();
+    }
 
     clk.mark("pass 2/3");
     // tentative prolongator: per-aggregate QR of the near-nullspace rows
@@ -1698,11 +1780,11 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     L->jacobi_weight = opts.jacobi_omega * 2.0 / lambda;
     L->lambda = lambda;
     if (opts.smoother == 1) L->cheb_hi = gershgorin_bound(*A, L->inv_diag.p);
-    L->n_nodes = n_nodes;
-    L->n_aggregates = n_agg;
+    L->n_nodes = n_nodes_ref;
+    L->n_aggregates = n_agg + (n_nodes_ref - n_nodes);  // every empty node is its own aggregate
     L->strong_edges = ns;
     L->lfmis_rounds = read_dev(rounds.p);
-    L->agg_of_node = std::move(agg);
+    L->agg_of_node = orig_of_c.n > 0 ? std::move(agg_ref) : std::move(agg);
     // Galerkin coarse operator Ac = P^T (A P), pruned; coarse nullspace and node ids
     auto AP = spgemm(*A, *L->P);
     clk.mark("spgemm AP");
@@ -1715,6 +1797,20 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     k_build_Bc<<<grid_for(n_agg, 256), 256, 0, stream()>>>(n_agg, m, aptr.p, rank.p, rank64.p, W.p, perm.p, nc, Bc.p,
                                                            cnode.p);
     CF_LAUNCHED();
+    // next level's nodes: the aggregates that carry coarse dofs, renumbered in order
+    if (!no_compact) {
+      DevBuf<int> cid(n_agg + 1), orig_next(n_agg);
+      k_nonempty_flags<<<grid_for(n_agg, 256), 256, 0, stream()>>>(n_agg, rank.p, cid.p);
+      CF_LAUNCHED();
+      CF_CUDA(cudaMemsetAsync(cid.p + n_agg, 0, sizeof(int), stream()));
+      scan_excl(cid.p, n_agg + 1);
+      k_compact_orig<<<grid_for(n_agg, 256), 256, 0, stream()>>>(n_agg, rank.p, cid.p, aorig.n > 0 ? aorig.p : nullptr,
+                                                                 orig_next.p);
+      CF_LAUNCHED();
+      k_renumber<<<grid_for(nc, 256), 256, 0, stream()>>>(nc, cid.p, cnode.p);
+      CF_LAUNCHED();
+      orig_of_c = std::move(orig_next);
+    }
     L->tmp_r.alloc(n);
     L->tmp_b.alloc(nc);
     L->tmp_x.alloc(nc);

@@ -1066,9 +1066,7 @@ std::unique_ptr<Constraints> build_constraints(const Problem& P, bool clamp, i64
     k_normalise_flags<<<grid_for(nt, 256), 256, 0, stream()>>>(nt, c->flag.p);
     CF_LAUNCHED();
     int hb = 0;
-    CF_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    ++host_sync_count();
+    read_small(&hb, bad.p, sizeof(int));
     if (hb) fail(CF_ERR_INVALID_ARGUMENT, "build_constraints: active dof out of range");
   }
   return c;
@@ -1150,9 +1148,7 @@ void assemble_residual_moved(Problem& P, const Constraints& cs, const cf_materia
                                                               cache.count.p);
   }
   CF_LAUNCHED();
-  CF_CUDA(cudaMemcpyAsync(&n, cache.count.p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&n, cache.count.p, sizeof(int));
   if (g.d == 2) {
     if (n)
       k_cell_residual_q<2><<<grid_for(i64(n) * 4, 256), 256, 0, stream()>>>(g, P.tab.p, cf, x, pt, cache.cellres.p,
@@ -1209,9 +1205,7 @@ static void jacobian_impl(Problem& P, const Constraints& cs, const Coef& cf, con
   i64 nnz[3] = {0, 0, 0};
   if (with_uu) CF_CUDA(cudaMemcpyAsync(&nnz[0], J.uu->ptr.p + nu, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
   CF_CUDA(cudaMemcpyAsync(&nnz[1], J.pu->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaMemcpyAsync(&nnz[2], J.pp->ptr.p + np, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&nnz[2], J.pp->ptr.p + np, sizeof(i64));
   if (with_uu) {
     J.uu->nnz = nnz[0];
     J.uu->col.alloc(nnz[0]);

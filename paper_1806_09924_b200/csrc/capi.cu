@@ -177,6 +177,23 @@ void dev_free(void* p, size_t bytes) {
 
 size_t dev_cached_bytes() { return block_cache().cached; }
 
+void read_small(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kSlot = 4096;
+  static void* slot = nullptr;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  ++host_sync_count();
+  if (bytes > kSlot) {
+    CF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream()));
+    CF_CUDA(cudaStreamSynchronize(stream()));
+    return;
+  }
+  if (!slot) CF_CUDA(cudaHostAlloc(&slot, kSlot, cudaHostAllocDefault));
+  CF_CUDA(cudaMemcpyAsync(slot, src, bytes, cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  std::memcpy(dst, slot, bytes);
+}
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;

@@ -80,6 +80,10 @@ inline long& host_sync_count() {
   static long n = 0;
   return n;
 }
+// Small device -> host read, ordered on the library stream and complete on return: the bytes go
+// through a pinned staging slot (a pageable destination makes the driver stage and block inside
+// cudaMemcpyAsync, about twice the latency of a pinned copy + stream sync).  Counts one host sync.
+void read_small(void* dst, const void* src, size_t bytes);
 inline void count_launch(i64 n = 1) { rt().launches += n; }
 #define CF_LAUNCHED() ::cfb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__), ::cfb::count_launch()
 

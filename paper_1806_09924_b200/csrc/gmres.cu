@@ -45,9 +45,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
   DevBuf<double> sc(2);
   gdot(rhs, rhs, n, sc.p, true, comm, seg);
   double bnorm = 0.0;
-  CF_CUDA(cudaMemcpyAsync(&bnorm, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&bnorm, sc.p, sizeof(double));
   if (bnorm == 0.0) {
     res.converged = true;
     return res;
@@ -85,9 +83,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
   while (res.iterations < o.max_iter) {
     gdot(r.p, r.p, n, sc.p, true, comm, seg);
     double beta = 0.0;
-    CF_CUDA(cudaMemcpyAsync(&beta, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    ++host_sync_count();
+    read_small(&beta, sc.p, sizeof(double));
     if (beta <= o.rtol * bnorm) {
       res.converged = true;
       res.residual = beta / bnorm;
@@ -125,9 +121,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
           }
         }
       }
-      CF_CUDA(cudaMemcpyAsync(hcol.data(), hd.p, size_t(j + 2) * sizeof(double), cudaMemcpyDeviceToHost, stream()));
-      CF_CUDA(cudaStreamSynchronize(stream()));
-      ++host_sync_count();
+      read_small(hcol.data(), hd.p, size_t(j + 2) * sizeof(double));
       for (int i = 0; i <= j + 1; ++i) Hij(i, j) = hcol[i];
       const bool happy = Hij(j + 1, j) <= 1e-14 * bnorm;
       if (!happy) vdiv_dev(w, hd.p + j + 1, w, n);
@@ -181,9 +175,7 @@ GmresResult gmres(const DevOp& op, const DevOp* prec, const double* rhs, i64 n, 
     vsub(rhs, z.p, r.p, n);  // r = b - op(x)
     gdot(r.p, r.p, n, sc.p, true, comm, seg);
     double rn = 0.0;
-    CF_CUDA(cudaMemcpyAsync(&rn, sc.p, sizeof(double), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    ++host_sync_count();
+    read_small(&rn, sc.p, sizeof(double));
     res.residual = rn / bnorm;
     if (res.residual <= o.rtol) {
       res.converged = true;

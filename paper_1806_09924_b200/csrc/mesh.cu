@@ -30,9 +30,7 @@ namespace {
 template <class T>
 T read1(const T* p) {
   T h{};
-  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, p, sizeof(T));
   return h;
 }
 
@@ -40,9 +38,7 @@ template <class T>
 std::vector<T> to_host(const T* p, i64 n) {
   std::vector<T> h(size_t(std::max<i64>(n, 0)));
   if (n > 0) {
-    CF_CUDA(cudaMemcpyAsync(h.data(), p, size_t(n) * sizeof(T), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    ++host_sync_count();
+    read_small(h.data(), p, size_t(n) * sizeof(T));
   }
   return h;
 }

@@ -22,9 +22,7 @@ namespace {
 template <class T>
 T read1(const T* p) {
   T h{};
-  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, p, sizeof(T));
   return h;
 }
 

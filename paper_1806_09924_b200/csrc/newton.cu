@@ -24,9 +24,7 @@ namespace {
 template <class T>
 T read_dev(const T* p) {
   T h{};
-  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(T), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, p, sizeof(T));
   return h;
 }
 
@@ -391,9 +389,7 @@ double gnorm(const Comm* cm, const double* v, const SegLayout& L) {
   double* s = scalar_buf(1);
   seg_dot_dev(v, v, L, s, true, cm);
   double h = 0.0;
-  CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, s, sizeof(double));
   return h;
 }
 
@@ -582,9 +578,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
                                           fixed.p, active.p, prev.p, flags.p);
       CF_LAUNCHED();
       int hc[2];
-      CF_CUDA(cudaMemcpyAsync(hc, flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream()));
-      CF_CUDA(cudaStreamSynchronize(stream()));
-      ++host_sync_count();
+      read_small(hc, flags.p, 2 * sizeof(int));
       long long counts[2] = {hc[0], hc[1]};
       cm.sum_i64(counts, 2);
       asize = int(counts[0]);
@@ -825,9 +819,7 @@ NewtonReport newton_active_set_step(Problem& P, State& st, const cf_material& ma
   k_feas<<<gv, 256, 0, stream()>>>(sl, nu, x, st.phi_old.p, mx.p);
   CF_LAUNCHED();
   long long bits = 0;
-  CF_CUDA(cudaMemcpyAsync(&bits, mx.p, sizeof(bits), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&bits, mx.p, sizeof(bits));
   cm.max_i64(&bits, 1);
   bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
   double viol;
@@ -918,9 +910,7 @@ NewtonReport mesh_newton_step(MeshDisc& m, State& st, const cf_material& mat, co
                                           fixed.p, active.p, prev.p, flags.p);
       CF_LAUNCHED();
       int hc[2];
-      CF_CUDA(cudaMemcpyAsync(hc, flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream()));
-      CF_CUDA(cudaStreamSynchronize(stream()));
-      ++host_sync_count();
+      read_small(hc, flags.p, 2 * sizeof(int));
       asize = hc[0];
       changes = hc[1];
       k_full_constraints<<<gv, 256, 0, stream()>>>(sl, nu, base->flag.p, base->inhom.p, active.p, st.phi_old.p,
@@ -1011,9 +1001,7 @@ NewtonReport mesh_newton_step(MeshDisc& m, State& st, const cf_material& mat, co
   k_feas<<<gv, 256, 0, stream()>>>(sl, nu, x, st.phi_old.p, mx.p);
   CF_LAUNCHED();
   long long bits = 0;
-  CF_CUDA(cudaMemcpyAsync(&bits, mx.p, sizeof(bits), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&bits, mx.p, sizeof(bits));
   bits = bits >= 0 ? bits : (bits ^ 0x7fffffffffffffffLL);
   double viol;
   std::memcpy(&viol, &bits, sizeof(viol));

@@ -551,16 +551,12 @@ void scan_excl(T* data, i64 n_plus_1) {
 
 i64 read_i64(const i64* p) {
   i64 h = 0;
-  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(i64), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, p, sizeof(i64));
   return h;
 }
 int read_int(const int* p) {
   int h = 0;
-  CF_CUDA(cudaMemcpyAsync(&h, p, sizeof(int), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, p, sizeof(int));
   return h;
 }
 
@@ -593,6 +589,7 @@ RowBin overflow_of(const RowBin& in, const i64* cnt) {
 }
 
 constexpr int SYM_BIG = 16384;
+constexpr i64 SMALL_ROWS = 16384, SMALL_COLS = 8192;  // the one-round-trip path of spgemm()
 
 // lanes per A entry in the warp kernels, from the longest B row
 // 8 lanes (4 A entries in flight per step, <= 16 independent B loads per lane) unless B rows are
@@ -1477,12 +1474,49 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
     k_max_row<<<int(std::min<i64>(1024, grid_for(B.rows, 256))), 256, 0, stream()>>>(B.rows, B.ptr.p, mx.p);
     CF_LAUNCHED();
     unsigned long long h = 0;
-    CF_CUDA(cudaMemcpyAsync(&h, mx.p, sizeof(h), cudaMemcpyDeviceToHost, stream()));
-    CF_CUDA(cudaStreamSynchronize(stream()));
-    ++host_sync_count();
+    read_small(&h, mx.p, sizeof(h));
     maxb = i64(h);
   }
   const int L = lanes_for(maxb);
+  // Small products (the coarse levels of every hierarchy, eight phi-hierarchies per Newton step):
+  // the tiered paths below cost 13-15 host round trips per product to size their row bins, which
+  // is all the time such a product takes.  One CTA per row instead, byte-flag symbolic and
+  // prefetching numeric over all rows with shared memory for B.cols columns: one round trip (nnz).
+  // Same per-entry summation order as every other path (CF_SPGEMM_NO_SMALL=1: tiered paths).
+  static const bool no_small = std::getenv("CF_SPGEMM_NO_SMALL") != nullptr;
+  if (!no_small && m > 0 && m <= SMALL_ROWS && B.cols <= SMALL_COLS && maxb >= 1 && maxb <= 1024) {
+    auto C = std::make_unique<Csr>();
+    C->rows = m;
+    C->cols = B.cols;
+    C->ptr.alloc(m + 1);
+    CF_CUDA(cudaMemsetAsync(C->ptr.p + m, 0, sizeof(i64), stream()));
+    const size_t smf = size_t(B.cols) + 16;
+    CF_CUDA(cudaFuncSetAttribute(k_sym_flags<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf)));
+    k_sym_flags<0><<<int(m), 256, smf, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
+                                                   nullptr);
+    CF_LAUNCHED();
+    scan_excl(C->ptr.p, m + 1);
+    C->nnz = read_i64(C->ptr.p + m);
+    C->col.alloc(std::max<i64>(C->nnz, 1));
+    C->val.alloc(std::max<i64>(C->nnz, 1));
+    CF_CUDA(cudaFuncSetAttribute(k_sym_flags<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf)));
+    k_sym_flags<1><<<int(m), 256, smf, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
+                                                   C->col.p);
+    CF_LAUNCHED();
+    if (C->nnz > 0) {
+      const size_t sm = size_t(B.cols) * (sizeof(double) + sizeof(int)) + 16;
+      auto launch = [&](auto kern) {
+        CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        kern<<<int(m), 256, sm, stream()>>>(nullptr, m, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p, B.col.p,
+                                            B.val.p, C->ptr.p, C->col.p, C->val.p);
+        CF_LAUNCHED();
+      };
+      if (maxb <= 256) launch(k_num_cta_pf<1>);
+      else if (maxb <= 512) launch(k_num_cta_pf<2>);
+      else launch(k_num_cta_pf<4>);
+    }
+    return C;
+  }
   // A/B and test switches: CF_SPGEMM_NOGROUP=1 row-wise only; CF_SPGEMM_GROUP_ALL=1 groups every
   // product the grouped kernel can take (small matrices, short B rows, few shared patterns)
   static const bool no_group = std::getenv("CF_SPGEMM_NOGROUP") != nullptr;

@@ -8,6 +8,7 @@
 // persistent 8-thread row groups carrying the 16 logical lanes, interior fast path);
 // k_spmv_st_emu (general emulated form: tuning sweeps, CF_ST_EMU=1).  Every variant produces
 // bitwise the TPR-lane reduction of the contract.
+#include <cstdint>
 #include <cstdlib>
 
 #include "cf_types.hpp"
@@ -529,6 +530,284 @@ __global__ void __launch_bounds__(256) k_spmv_st16p(i64 rows, const i64* __restr
   }
 }
 
+// ---- TMA-fed form of k_spmv_st16p (the 3d M_uu production kernel) ------------------------------
+// One producer warp feeds a ring of S shared-memory stages with 1d bulk copies (cp.async.bulk,
+// completion counted on an mbarrier): per tile of T16_ROWS consecutive rows the contiguous slice of
+// val (8 B per stored entry, 98% of the bytes) and the nine contiguous x segments (3 y-lines x 3
+// z-planes around the tile's vertices) that its interior rows read, so neither the bytes in flight
+// nor the x gathers depend on consumer registers, occupancy or L1/L2 round trips.  The eight
+// consumer warps keep k_spmv_st16p's arithmetic exactly (8 threads per row carrying the 16 logical
+// lanes, interior fast path, the same products in the same order), reading values and x from
+// shared memory; boundary and clamp rows take x from global memory as before.  Bitwise
+// k_spmv_st16p (scripts/st16t_ab.py, and the 48^3 / 64^3 oracle parity tests run through it).
+constexpr int T16_ROWS = 32;                 // rows per tile: one per consumer group
+constexpr int T16_VCAP = T16_ROWS * 81 + 2;  // doubles per stage (+2: 16-byte alignment slack)
+constexpr int T16_XSEG = 46;                 // doubles per x segment: 3 (12 + 2) vertices + alignment, even
+struct T16Stage {
+  double val[T16_VCAP];
+  double xs[9 * T16_XSEG];
+  i64 ptr[T16_ROWS + 1];
+  i64 base;  // index in val[] of the stage's first double (even)
+};
+static_assert(sizeof(T16Stage) % 16 == 0 && (T16_VCAP * 8) % 16 == 0 && (T16_XSEG % 2) == 0, "stage alignment");
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return unsigned(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "W16T_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra D16T_%=;\n"
+      "bra W16T_%=;\n"
+      "D16T_%=:\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// 1d bulk copy global -> shared (both 16-byte aligned, size a multiple of 16)
+template <bool EVICT_FIRST>
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  if (EVICT_FIRST) {  // the value stream is read once: keep x and the vectors in L2 instead
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+        : "memory");
+  } else {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+  }
+}
+
+// shared-memory x offsets of thread t's entries of an interior row, relative to the row's vertex:
+// entry e = 3 n + b with neighbour n = dx + 3 dy + 9 dz lies in segment q = dy + 3 dz at
+// 3 dx + b (+ 3 (v - v0) + the segment's alignment parity, added per row)
+struct St16Sm {
+  int a[6], b[5];
+  unsigned fmask;  // bit j (a[j]) / bit 6 + j (b[j]): the entry's segment parity differs from segment 4's
+  __device__ static int off(int e) {
+    const int n = e / 3, c = e - 3 * n;
+    return (n / 3) * T16_XSEG + 3 * (n % 3) + c;
+  }
+  __device__ static unsigned par(int e, int nn_odd) {
+    const int n = e / 3, dy = (n / 3) % 3, dz = n / 9;
+    return unsigned(nn_odd & (dy + dz) & 1);
+  }
+  __device__ void init(int t, int nn) {
+    fmask = 0;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      a[j] = off(t + 16 * j);
+      b[j] = off(t + 8 + 16 * j);
+      fmask |= par(t + 16 * j, nn & 1) << j;
+      fmask |= par(t + 8 + 16 * j, nn & 1) << (6 + j);
+    }
+    a[5] = off(80);
+    fmask |= par(80, nn & 1) << 5;
+  }
+};
+
+// row16_interior with values and x in shared memory (xs: the stage's segments; vb = 3 (v - v0);
+// m: the tile's parity mask over this thread's entries)
+__device__ __forceinline__ double row16_interior_sm(const double* vrow, const double* xs, int vb, unsigned m, int t,
+                                                    const St16Sm& o) {
+  double va[6], vbv[5], xa[6], xv[5];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    va[j] = vrow[t + 16 * j];
+    vbv[j] = vrow[t + 8 + 16 * j];
+  }
+  va[5] = (t == 0) ? vrow[80] : 0.0;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    xa[j] = xs[o.a[j] + vb + int((m >> j) & 1u)];
+    xv[j] = xs[o.b[j] + vb + int((m >> (6 + j)) & 1u)];
+  }
+  xa[5] = (t == 0) ? xs[o.a[5] + vb + int((m >> 5) & 1u)] : 0.0;
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    sa += va[j] * xa[j];
+    sb += vbv[j] * xv[j];
+  }
+  sa += va[5] * xa[5];
+  return sa + sb;
+}
+
+// row_dot_st_emu<16, 8, 1, 3> with the row's values in shared memory (boundary and clamp rows)
+__device__ __forceinline__ double row16_general_sm(const double* vrow, int len, const double* __restrict__ x, i64 row,
+                                                   int t, const StencilCols& sc, const int* __restrict__ off) {
+  StGeo<3> G;
+  st_geo<3>(sc, row, G);
+  double s0 = 0.0, s1 = 0.0;
+  for (int base = 0; base < len; base += 16) {
+    const int k0 = base + t, k1 = base + t + 8;
+    const bool in0 = k0 < len, in1 = k1 < len;
+    const double v0 = in0 ? vrow[k0] : 0.0, v1 = in1 ? vrow[k1] : 0.0;
+    const int c0 = !in0 ? -1 : (G.interior ? G.colbase + off[k0] : st_col<3>(G, k0));
+    const int c1 = !in1 ? -1 : (G.interior ? G.colbase + off[k1] : st_col<3>(G, k1));
+    const double x0 = c0 >= 0 ? __ldg(x + c0) : 0.0, x1 = c1 >= 0 ? __ldg(x + c1) : 0.0;
+    s0 += v0 * x0;
+    s1 += v1 * x1;
+  }
+  return s0 + s1;
+}
+
+// interior test on the vertex coordinates of a u row (all 27 neighbours free)
+__device__ __forceinline__ bool st16_interior_v(const StencilCols& sc, unsigned v) {
+  const unsigned nn = unsigned(sc.nn);
+  auto divn = [&](unsigned t) {
+    unsigned q = unsigned(double(t) * sc.inv_nn);
+    if (q * nn > t) --q;
+    else if ((q + 1) * nn <= t) ++q;
+    return q;
+  };
+  const unsigned vy = divn(v), vz = divn(vy);
+  const unsigned xx = v - vy * nn, yy = vy - vz * nn, zz = vz;
+  const unsigned lo = 2u, hi = nn - 3u;
+  return !(xx < lo || xx > hi || yy < lo || yy > hi || zz < lo || zz > hi);
+}
+
+// rows are u dofs (sc.kind == 1); ncols = length of x
+template <int S, int MINB>
+__global__ void __launch_bounds__(288, MINB) k_spmv_st16t(i64 rows, i64 nnz, i64 ncols, const i64* __restrict__ ptr,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x, double* y, SpmvEpi ep,
+                                                          StencilCols sc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T16Stage* st = reinterpret_cast<T16Stage*>(smem_raw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(T16Stage) * S);
+  unsigned long long* empty = full + S;
+  int* off = reinterpret_cast<int*>(empty + S);
+  StOff<3>::fill(off, int(sc.nn));
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);   // the producer's arrive (+ the copies' bytes)
+      mbar_init(empty + i, 8);  // one arrive per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const i64 ntiles = (rows + T16_ROWS - 1) / T16_ROWS;
+  const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  const i64 nn = sc.nn;
+  if (warp == 8) {
+    // ---- producer warp: the tile's row pointers by plain loads (one tile ahead), its value slice
+    // by one bulk copy (lane 0) and its nine x segments by one bulk copy each (lanes 1..9)
+    i64 tile = blockIdx.x;
+    i64 pa = 0, pb = 0;
+    auto load_ptrs = [&](i64 tl) {
+      const i64 r0 = tl * T16_ROWS;
+      const int nr = int(min(i64(T16_ROWS), rows - r0));
+      pa = lane <= nr ? ptr[r0 + lane] : 0;
+      pb = (lane == 0 && nr == 32) ? ptr[r0 + 32] : 0;
+    };
+    if (tile < ntiles) load_ptrs(tile);
+    for (unsigned it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+      const int s = int(it % S);
+      const unsigned ph = (it / S) & 1u;
+      const i64 r0 = tile * T16_ROWS;
+      const int nr = int(min(i64(T16_ROWS), rows - r0));
+      const i64 ca = pa, cb = pb;
+      if (tile + gridDim.x < ntiles) load_ptrs(tile + gridDim.x);
+      mbar_wait(empty + s, ph ^ 1u);
+      T16Stage& T = st[s];
+      if (lane <= nr) T.ptr[lane] = ca;
+      if (lane == 0 && nr == 32) T.ptr[32] = cb;
+      const i64 first = __shfl_sync(0xffffffffu, ca, 0);
+      const i64 last = nr == 32 ? __shfl_sync(0xffffffffu, cb, 0) : __shfl_sync(0xffffffffu, ca, nr);
+      // lane 0: doubles [a0, a0 + cnt) of val, an even count from an even index; the array's odd
+      // last double is fetched by a plain load instead of reading past the end
+      const void* src = nullptr;
+      void* dst = nullptr;
+      i64 cnt = 0;
+      if (lane == 0) {
+        const i64 a0 = first & ~i64(1);
+        cnt = last - a0;
+        const bool tail = (cnt & 1) && last == nnz;
+        cnt += (cnt & 1) ? (tail ? -1 : 1) : 0;
+        T.base = a0;
+        if (tail) T.val[cnt] = val[last - 1];
+        src = val + a0;
+        dst = T.val;
+      } else if (lane <= 9) {
+        // segment q = dy + 3 dz: x entries of vertices v0 - 1 .. v1 + 1 shifted by (dy - 1) nn + (dz - 1) nn^2,
+        // widened to even bounds and clamped to x (interior rows never reach a clamped part)
+        const int q = lane - 1;
+        const i64 v0 = sc.v_lo + r0 / 3, v1 = sc.v_lo + (r0 + nr - 1) / 3;
+        const i64 sh = i64(q % 3 - 1) * nn + i64(q / 3 - 1) * nn * nn;
+        const i64 s0 = 3 * (v0 - 1 + sh) - sc.shift, s1 = 3 * (v1 + 2 + sh) - sc.shift;  // [s0, s1)
+        const i64 a = s0 & ~i64(1);
+        const i64 lo = max(a, i64(0)), hi = min((s1 + 1) & ~i64(1), ncols & ~i64(1));
+        if (hi > lo) {
+          cnt = hi - lo;
+          src = x + lo;
+          dst = T.xs + q * T16_XSEG + (lo - a);
+        }
+      }
+      unsigned bytes = unsigned(cnt * 8), total = bytes;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o, 16);
+      __syncwarp();  // the stage's pointer stores are ordered before lane 0's releasing arrive
+      if (lane == 0) {
+        if (total > 0) mbar_arrive_tx(full + s, total);
+        else mbar_arrive(full + s);
+      }
+      __syncwarp();
+      if (bytes > 0) {
+        if (lane == 0) bulk_g2s<true>(dst, src, bytes, full + s);
+        else bulk_g2s<false>(dst, src, bytes, full + s);
+      }
+    }
+    return;
+  }
+  // ---- consumers: group g of the CTA owns row g of every tile
+  const int g = int(threadIdx.x >> 3), t = int(threadIdx.x & 7);
+  St16Sm o;
+  o.init(t, int(nn));
+  unsigned it = 0;
+  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = int(it % S);
+    const unsigned ph = (it / S) & 1u;
+    const i64 r0 = tile * T16_ROWS;
+    const i64 row = r0 + g;
+    const bool act = row < rows;
+    const unsigned lv0 = unsigned(r0) / 3u, lv = unsigned(row) / 3u;
+    const bool inter = act && st16_interior_v(sc, unsigned(sc.v_lo) + lv);
+    // parity of segment 4's first entry 3 (v0 - 1) - shift; the others differ by fmask
+    const unsigned p0 = unsigned(3 * (i64(sc.v_lo) + lv0 - 1) - sc.shift) & 1u;
+    const unsigned m = p0 ? ~o.fmask : o.fmask;
+    mbar_wait(full + s, ph);
+    const T16Stage& T = st[s];
+    double sum = 0.0;
+    if (act) {
+      const i64 b0 = T.ptr[g], b1 = T.ptr[g + 1];
+      const double* vrow = T.val + (b0 - T.base);
+      const int len = int(b1 - b0);
+      if (inter && len == 81) sum = row16_interior_sm(vrow, T.xs, 3 * int(lv - lv0), m, t, o);
+      else sum = row16_general_sm(vrow, len, x, row, t, sc, off);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+    sum = group_sum<8>(sum);
+    if (act && t == 0) y[row] = epi_out(ep, x, row, sum);
+  }
+}
+
 // Persistent CSR SpMV: TPR lanes per row, U batched (value, column) loads, rows g, g + G, ...
 // with the next row's pointers fetched ahead (the pointer -> value -> x chain otherwise costs
 // three dependent memory latencies per row).  Bitwise k_spmv_b<TPR, U> (same lanes, same order).
@@ -754,6 +1033,34 @@ void launch_phi(const BlockSystem& J, const double* x, double* y) {
   CF_LAUNCHED();
 }
 
+// stages of the TMA value ring (0: use k_spmv_st16p); CF_ST16T_STAGES=2|3|4 for A/B runs (4, 3, 2 CTAs per SM)
+int st16t_stages() {
+  static const int s = [] {
+    if (std::getenv("CF_NO_ST16T")) return 0;
+    const char* e = std::getenv("CF_ST16T_STAGES");
+    // measured on config 1 (scripts/st16t_ab.py): 2 stages x 4 CTAs/SM 2.355 ms, 3 x 3 2.410 ms,
+    // 4 x 2 2.729 ms (k_spmv_st16p: 2.73 ms): consumer warps per SM matter more than ring depth
+    const int v = e ? std::atoi(e) : 2;
+    return (v == 3 || v == 4) ? v : 2;
+  }();
+  return s;
+}
+
+template <int S, int MINB>
+void launch_st16t(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
+  constexpr int smem = int(sizeof(T16Stage)) * S + 2 * S * 8 + StOff<3>::N * 4;
+  static int bps = 0;
+  if (!bps) {
+    CF_CUDA(cudaFuncSetAttribute(k_spmv_st16t<S, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_st16t<S, MINB>, 288, smem));
+    if (bps < 1) fail(CF_ERR_CUDA, "k_spmv_st16t: no resident block");
+  }
+  const i64 ntiles = (A.rows + T16_ROWS - 1) / T16_ROWS;
+  const int grid = int(std::min<i64>(ntiles, i64(bps) * rt().sm_count));
+  k_spmv_st16t<S, MINB><<<grid, 288, smem, stream()>>>(A.rows, A.nnz, A.cols, A.ptr.p, A.val.p, x, y, ep, A.st);
+  CF_LAUNCHED();
+}
+
 // PF: the persistent pointer-prefetching CSR kernel (k_spmv_pf) instead of k_spmv_b
 template <int TPR, int U, bool PF = false>
 void launch_b(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
@@ -766,6 +1073,15 @@ void launch_b(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
     k_spmv_pf<TPR, U><<<grid, block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, ep);
   } else if (A.st.kind == 0)
     k_spmv_b<TPR, U><<<grid_for(threads, block), block, 0, stream()>>>(A.rows, A.ptr.p, A.col.p, A.val.p, x, y, ep);
+  else if (TPR == 16 && A.st.d == 3 && A.st.kind == 1 && !st_emu_only() && st16t_stages() > 0 &&
+           ((reinterpret_cast<uintptr_t>(A.val.p) | reinterpret_cast<uintptr_t>(x)) & 15) == 0) {
+    // TMA-fed value and x ring (CF_NO_ST16T=1: k_spmv_st16p; CF_ST16T_STAGES: A/B runs)
+    const int S = st16t_stages();
+    if (S == 2) launch_st16t<2, 4>(A, x, y, ep);
+    else if (S == 4) launch_st16t<4, 2>(A, x, y, ep);
+    else launch_st16t<3, 3>(A, x, y, ep);
+    return;
+  }
   else if (TPR == 16 && A.st.d == 3 && !st_emu_only()) {  // persistent, pointer prefetch
     static int bps = 0;
     if (!bps) CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_st16p, block, 0));

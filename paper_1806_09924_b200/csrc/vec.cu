@@ -293,9 +293,7 @@ double vdot(const double* x, const double* y, i64 n) {
   double* s = scalar_buf(1);
   vdot_dev(x, y, n, s, false);
   double h = 0.0;
-  CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, s, sizeof(double));
   return h;
 }
 
@@ -303,9 +301,7 @@ double vnorm(const double* x, i64 n) {
   double* s = scalar_buf(1);
   vdot_dev(x, x, n, s, true);
   double h = 0.0;
-  CF_CUDA(cudaMemcpyAsync(&h, s, sizeof(double), cudaMemcpyDeviceToHost, stream()));
-  CF_CUDA(cudaStreamSynchronize(stream()));
-  ++host_sync_count();
+  read_small(&h, s, sizeof(double));
   return h;
 }
 

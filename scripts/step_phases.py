@@ -7,15 +7,16 @@ import sys
 
 if len(sys.argv) > 2 and sys.argv[1] == "--parse":
     lines = open(sys.argv[2]).read().split("@@STEP2@@")[1].splitlines()
+    # the first hierarchy built in a step is M_uu's, the others are M_phiphi's (one per Newton iteration)
     kind, acc, nb = None, collections.defaultdict(float), collections.Counter()
     for ln in lines:
-        m = re.match(r"\[amg L(\d+)\] nodes (\d+)", ln)
-        if m and m.group(1) == "0":
-            kind = "u" if int(m.group(2)) * 3 > 5_000_000 else "phi"
-            nb[kind] += 1
         m = re.match(r"\[amg L(\d+)\] (.+?)\s+([\d.]+) ms", ln)
-        if m and kind:
-            acc[(kind, "L" + m.group(1), m.group(2).strip())] += float(m.group(3))
+        if not m:
+            continue
+        if m.group(1) == "0" and m.group(2).strip() == "strength":
+            kind = "u" if not nb else "phi"
+            nb[kind] += 1
+        acc[(kind, "L" + m.group(1), m.group(2).strip())] += float(m.group(3))
     print("builds", dict(nb))
     for k in sorted(acc):
         print(f"{k[0]:4s} {k[1]:3s} {k[2]:14s} {acc[k]:9.2f} ms")

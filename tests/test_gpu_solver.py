@@ -126,6 +126,36 @@ def test_amg_laplacian_parity_and_mesh_independence(cf, orc):  # linsolve_test.c
     assert its[1] <= 1.5 * its[0] and its[0] <= 1.5 * its[1]
 
 
+def test_amg_empty_coarse_nodes_reference_numbering(cf, orc):
+    """A phi-like block: most rows constrained (identity rows with a zero near-nullspace entry), so
+    most level-0 aggregates carry no coarse dof and are empty nodes of every coarser level.  The
+    device build leaves them out (amg.cu, "empty coarse nodes") and must still report the
+    reference's node counts, aggregate counts and aggregate ids (linsolve.cpp:146-154: an empty
+    node seeds its own aggregate in pass 1), and produce the same operators and V-cycle."""
+    rng = np.random.default_rng(23)
+    for nv, keep in ((97, 0.25), (129, 0.6)):
+        A = _q1_laplacian(nv).tolil()
+        n = nv * nv
+        con = rng.uniform(0, 1, n) > keep
+        # constrained rows and columns become identity (Scatter condensation of a Dirichlet value)
+        A = A.tocsr()
+        D = sp.diags((~con).astype(float))
+        A = (D @ A @ D + sp.diags(con.astype(float))).tocsr()
+        A.eliminate_zeros()
+        A.sort_indices()
+        B = (~con).astype(float).reshape(n, 1)
+        nod = np.arange(n, dtype=np.int32)
+        opts = cf.AmgOptions(coarse_size=16)
+        h = cf.build_amg(cf.CsrMatrix.from_scipy(A), nod, B, opts)
+        ho = orc.Amg(orc.Csr.from_scipy(A), nod, B, orc.amg_options(coarse_size=16))
+        assert ho.n_levels >= 3
+        # the case must contain empty nodes below the last non-empty one on a coarse level
+        assert any(ho.level(l)["n_aggregates"] > ho.level(l)["coarse"] for l in range(1, ho.n_levels - 1))
+        _assert_amg_equal(h, ho)
+        r = rng.uniform(-1, 1, n)
+        assert np.array_equal(h.v_cycle(r), ho.vcycle(r))
+
+
 def test_gmres_identity_spd_and_validation(cf, orc):  # linsolve_test.cpp:194-217
     I = cf.CsrMatrix.from_scipy(sp.identity(20, format="csr"))
     b = np.linspace(1.0, 20.0, 20)
