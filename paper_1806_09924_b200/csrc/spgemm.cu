@@ -521,6 +521,156 @@ __global__ void __launch_bounds__(256) k_sym_flags(i64 rows, const i64* __restri
     if (flg[t]) ccol[o++] = t;
 }
 
+// ---- staged CTA-per-row kernels of the small-product path --------------------------------------
+// k_sym_flags / k_num_cta_pf walk a row's A entries one after the other, each a dependent global
+// round trip (column -> B row pointers -> B row), so a row of R with 800 entries takes ~1 ms
+// whatever the GPU (56 such launches were 31 ms of the config-3 step).  Here the row's (A entry,
+// B entry) products are flattened: a chunk of up to 256 A entries loads its B row ranges at once,
+// a block scan numbers the products, and every thread fetches products f, f + 256, ... (all loads
+// independent).  The symbolic pass sets their flags; the numeric pass stages product and output
+// slot in shared memory and then adds them A entry by A entry (one barrier each, shared memory
+// only), which is the order of every other numeric kernel.
+constexpr int ST_CH = 2048;  // staged products per sub-chunk (>= the longest B row of the path, 1024)
+
+// exclusive block scan of one int per thread (256 threads); returns the total; off[256] in smem
+__device__ __forceinline__ int block_scan_256(int v, int* off, int* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  int base = 0, tot = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int x = wsum[i];
+    if (i < w) base += x;
+    tot += x;
+  }
+  off[threadIdx.x] = base + incl - v;
+  if (threadIdx.x == 255) off[256] = tot;
+  __syncthreads();
+  return tot;
+}
+// last e in [0, n) with off[e] <= f (off ascending, off[0] = 0)
+__device__ __forceinline__ int seg_of(const int* off, int n, int f) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= f) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_sym_flags_st(i64 rows, const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                      const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                      int ncols, i64* __restrict__ cnt_or_ptr,
+                                                      int* __restrict__ ccol) {
+  extern __shared__ unsigned char flg[];
+  __shared__ int off[257], wsum[8];
+  __shared__ i64 q0s[256];
+  const i64 i = blockIdx.x;
+  if (i >= rows) return;
+  for (int t = threadIdx.x; t < ncols; t += blockDim.x) flg[t] = 0;
+  const i64 a0 = ap[i], a1 = ap[i + 1];
+  for (i64 base = a0; base < a1; base += 256) {
+    const i64 ka = base + threadIdx.x;
+    int len = 0;
+    if (ka < a1) {
+      const int k = ac[ka];
+      const i64 q0 = bp[k];
+      len = int(bp[k + 1] - q0);
+      q0s[threadIdx.x] = q0;
+    }
+    const int tot = block_scan_256(len, off, wsum);  // (its barriers also order the flag zeroing)
+    const int ne = int(min(i64(256), a1 - base));
+    for (int f = threadIdx.x; f < tot; f += 256) {
+      const int e = seg_of(off, ne, f);
+      flg[bc[q0s[e] + (f - off[e])]] = 1;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  const int chunk = (ncols + blockDim.x - 1) / blockDim.x;
+  const int lo = min(ncols, int(threadIdx.x) * chunk), hi = min(ncols, lo + chunk);
+  int c = 0;
+  for (int t = lo; t < hi; ++t) c += flg[t];
+  const int tot = block_scan_256(c, off, wsum);
+  if (MODE == 0) {
+    if (threadIdx.x == 0) cnt_or_ptr[i] = tot;
+    return;
+  }
+  i64 o = cnt_or_ptr[i] + off[threadIdx.x];
+  for (int t = lo; t < hi; ++t)
+    if (flg[t]) ccol[o++] = t;
+}
+
+__global__ void __launch_bounds__(256) k_num_cta_st(i64 nrows, const i64* __restrict__ ap, const int* __restrict__ ac,
+                                                    const double* __restrict__ av, const double* __restrict__ rs,
+                                                    const i64* __restrict__ bp, const int* __restrict__ bc,
+                                                    const double* __restrict__ bv, const i64* __restrict__ cp,
+                                                    const int* __restrict__ cc, double* __restrict__ cv) {
+  extern __shared__ unsigned char smraw[];
+  __shared__ int off[257], wsum[8];
+  __shared__ i64 q0s[256];
+  __shared__ double as[256];
+  const i64 i = blockIdx.x;
+  if (i >= nrows) return;
+  const i64 c0 = cp[i];
+  const int nc = int(cp[i + 1] - c0);
+  double* prod = reinterpret_cast<double*>(smraw);
+  double* acc = prod + ST_CH;
+  int* cols = reinterpret_cast<int*>(acc + nc);
+  int* pos = cols + nc;
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+    cols[t] = cc[c0 + t];
+    acc[t] = 0.0;
+  }
+  const double si = rs ? rs[i] : 1.0;
+  const i64 a0 = ap[i], a1 = ap[i + 1];
+  for (i64 base = a0; base < a1; base += 256) {
+    const i64 ka = base + threadIdx.x;
+    int len = 0;
+    if (ka < a1) {
+      const int k = ac[ka];
+      const i64 q0 = bp[k];
+      len = int(bp[k + 1] - q0);
+      q0s[threadIdx.x] = q0;
+      as[threadIdx.x] = rs ? si * av[ka] : av[ka];
+    }
+    block_scan_256(len, off, wsum);  // (its barriers also order the cols / acc initialisation)
+    const int ne = int(min(i64(256), a1 - base));
+    // sub-chunks of whole A entries with at most ST_CH products
+    for (int e_lo = 0; e_lo < ne;) {
+      const int f0 = off[e_lo];
+      int e_hi = seg_of(off, ne + 1, f0 + ST_CH);  // last e with off[e] <= f0 + ST_CH
+      if (e_hi <= e_lo) e_hi = e_lo + 1;            // (a single B row never exceeds ST_CH)
+      const int f1 = off[e_hi];
+      for (int f = f0 + int(threadIdx.x); f < f1; f += 256) {
+        const int e = e_lo + seg_of(off + e_lo, e_hi - e_lo, f);
+        const i64 kb = q0s[e] + (f - off[e]);
+        prod[f - f0] = as[e] * bv[kb];
+        pos[f - f0] = lower_bound_sm(cols, nc, bc[kb]);
+      }
+      __syncthreads();
+      for (int e = e_lo; e < e_hi; ++e) {
+        const int b = off[e] - f0, n = off[e + 1] - off[e];
+        if (n == 0) continue;
+        for (int t = threadIdx.x; t < n; t += 256) acc[pos[b + t]] += prod[b + t];
+        __syncthreads();
+      }
+      e_lo = e_hi;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) cv[c0 + t] = acc[t];
+}
+
 // partition rows by a predicate on a per-row value (order within a bin is irrelevant: every
 // listed row is processed independently)
 __global__ void k_bin_rows(i64 rows, const i64* __restrict__ v, i64 lo, i64 hi, int* __restrict__ list,
@@ -1491,29 +1641,26 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
     C->ptr.alloc(m + 1);
     CF_CUDA(cudaMemsetAsync(C->ptr.p + m, 0, sizeof(i64), stream()));
     const size_t smf = size_t(B.cols) + 16;
-    CF_CUDA(cudaFuncSetAttribute(k_sym_flags<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf)));
-    k_sym_flags<0><<<int(m), 256, smf, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
-                                                   nullptr);
+    CF_CUDA(cudaFuncSetAttribute(k_sym_flags_st<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf)));
+    k_sym_flags_st<0><<<int(m), 256, smf, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
+                                                      nullptr);
     CF_LAUNCHED();
     scan_excl(C->ptr.p, m + 1);
     C->nnz = read_i64(C->ptr.p + m);
     C->col.alloc(std::max<i64>(C->nnz, 1));
     C->val.alloc(std::max<i64>(C->nnz, 1));
-    CF_CUDA(cudaFuncSetAttribute(k_sym_flags<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf)));
-    k_sym_flags<1><<<int(m), 256, smf, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
-                                                   C->col.p);
+    CF_CUDA(cudaFuncSetAttribute(k_sym_flags_st<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smf)));
+    k_sym_flags_st<1><<<int(m), 256, smf, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
+                                                      C->col.p);
     CF_LAUNCHED();
     if (C->nnz > 0) {
-      const size_t sm = size_t(B.cols) * (sizeof(double) + sizeof(int)) + 16;
-      auto launch = [&](auto kern) {
-        CF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        kern<<<int(m), 256, sm, stream()>>>(nullptr, m, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p, B.col.p,
-                                            B.val.p, C->ptr.p, C->col.p, C->val.p);
-        CF_LAUNCHED();
-      };
-      if (maxb <= 256) launch(k_num_cta_pf<1>);
-      else if (maxb <= 512) launch(k_num_cta_pf<2>);
-      else launch(k_num_cta_pf<4>);
+      // products + slots of a sub-chunk, accumulators and sorted columns of the longest possible row
+      const size_t sm = size_t(ST_CH) * (sizeof(double) + sizeof(int)) +
+                        size_t(B.cols) * (sizeof(double) + sizeof(int)) + 16;
+      CF_CUDA(cudaFuncSetAttribute(k_num_cta_st, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      k_num_cta_st<<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p, B.col.p, B.val.p,
+                                                  C->ptr.p, C->col.p, C->val.p);
+      CF_LAUNCHED();
     }
     return C;
   }

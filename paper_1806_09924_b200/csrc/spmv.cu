@@ -808,6 +808,167 @@ __global__ void __launch_bounds__(288, MINB) k_spmv_st16t(i64 rows, i64 nnz, i64
   }
 }
 
+// ---- TMA-fed CSR SpMV for long matrices with short rows (the level-0 prolongator) ---------------
+// k_spmv_b's per-row chain (row pointers -> values / columns -> x) is three dependent memory
+// latencies for ~26 entries, and the bytes in flight are bounded by the resident warps (P of the
+// config-3 u-hierarchy: 61% of the HBM peak).  Here a producer warp streams the contiguous val and
+// col slices of a tile of BT_ROWS consecutive rows into a ring of S shared-memory stages by bulk
+// copies (as k_spmv_st16t); the consumers keep k_spmv_b<TPR, U>'s lanes, batches and summation
+// order, reading values and columns from shared memory, so only the x gathers touch global memory.
+// A tile with more than BT_CAP entries is read from global memory by the same code path (direct).
+// Bitwise k_spmv_b<TPR, U>.
+constexpr int BT_ROWS = 64;
+constexpr int BT_CAP = 3072;  // entries per stage
+struct BtStage {
+  double val[BT_CAP + 2];
+  int col[BT_CAP + 4];
+  i64 ptr[BT_ROWS + 2];  // + 1 pad: 16-byte stage size
+  i64 vbase, cbase;  // first staged index of val (even) and col (multiple of 4); vbase < 0: direct tile
+};
+static_assert(sizeof(BtStage) % 16 == 0 && ((BT_CAP + 2) * 8) % 16 == 0 && ((BT_CAP + 4) * 4) % 16 == 0,
+              "stage alignment");
+
+template <int TPR, int U, int S, int MINB>
+__global__ void __launch_bounds__(288, MINB) k_spmv_bt(i64 rows, i64 nnz, const i64* __restrict__ ptr,
+                                                       const int* __restrict__ col, const double* __restrict__ val,
+                                                       const double* __restrict__ x, double* y, SpmvEpi ep) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  BtStage* st = reinterpret_cast<BtStage*>(smem_raw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(BtStage) * S);
+  unsigned long long* empty = full + S;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const i64 ntiles = (rows + BT_ROWS - 1) / BT_ROWS;
+  const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  if (warp == 8) {
+    // ---- producer: row pointers one tile ahead (lanes 0..31 hold entries lane, lane + 32; lane 0 also 64)
+    i64 tile = blockIdx.x;
+    i64 pa = 0, pb = 0, pc = 0;
+    auto load_ptrs = [&](i64 tl) {
+      const i64 r0 = tl * BT_ROWS;
+      const int nr = int(min(i64(BT_ROWS), rows - r0));
+      pa = lane <= nr ? ptr[r0 + lane] : 0;
+      pb = lane + 32 <= nr ? ptr[r0 + 32 + lane] : 0;
+      pc = (lane == 0 && nr == 64) ? ptr[r0 + 64] : 0;
+    };
+    if (tile < ntiles) load_ptrs(tile);
+    for (unsigned it = 0; tile < ntiles; tile += gridDim.x, ++it) {
+      const int s = int(it % S);
+      const unsigned ph = (it / S) & 1u;
+      const i64 r0 = tile * BT_ROWS;
+      const int nr = int(min(i64(BT_ROWS), rows - r0));
+      const i64 ca = pa, cb = pb, cc = pc;
+      if (tile + gridDim.x < ntiles) load_ptrs(tile + gridDim.x);
+      mbar_wait(empty + s, ph ^ 1u);
+      BtStage& T = st[s];
+      if (lane <= nr) T.ptr[lane] = ca;
+      if (lane + 32 <= nr) T.ptr[lane + 32] = cb;
+      if (lane == 0 && nr == 64) T.ptr[64] = cc;
+      const i64 first = __shfl_sync(0xffffffffu, ca, 0);
+      const i64 last = nr == 64 ? __shfl_sync(0xffffffffu, cc, 0)
+                                : (nr >= 32 ? __shfl_sync(0xffffffffu, cb, nr - 32) : __shfl_sync(0xffffffffu, ca, nr));
+      const bool direct = last - first > BT_CAP;
+      unsigned vbytes = 0, cbytes = 0;
+      const i64 v0 = first & ~i64(1), c0 = first & ~i64(3);
+      if (lane == 0) {
+        T.vbase = direct ? -1 : v0;
+        T.cbase = c0;
+        if (!direct) {
+          // whole 16-byte units; what would reach past the arrays' end comes by plain loads
+          i64 vc = last - v0, ccn = last - c0;
+          if (vc & 1) {
+            if (last == nnz) {
+              T.val[vc - 1] = val[last - 1];
+              --vc;
+            } else {
+              ++vc;
+            }
+          }
+          if (ccn & 3) {
+            if (last + 3 >= nnz) {  // the rounded-up copy could pass the end of col
+              const i64 fl = ccn & ~i64(3);
+              for (i64 k = fl; k < ccn; ++k) T.col[k] = col[c0 + k];
+              ccn = fl;
+            } else {
+              ccn = (ccn + 3) & ~i64(3);
+            }
+          }
+          vbytes = unsigned(vc * 8);
+          cbytes = unsigned(ccn * 4);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (vbytes + cbytes > 0) {
+          mbar_arrive_tx(full + s, vbytes + cbytes);
+          if (vbytes) bulk_g2s<true>(T.val, val + v0, vbytes, full + s);
+          if (cbytes) bulk_g2s<true>(T.col, col + c0, cbytes, full + s);
+        } else {
+          mbar_arrive(full + s);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers: k_spmv_b<TPR, U> rows and lanes
+  constexpr int RPP = 256 / TPR;  // rows per pass
+  const int g = int(threadIdx.x) / TPR, l = int(threadIdx.x) % TPR;
+  unsigned it = 0;
+  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = int(it % S);
+    const unsigned ph = (it / S) & 1u;
+    const i64 r0 = tile * BT_ROWS;
+    mbar_wait(full + s, ph);
+    const BtStage& T = st[s];
+    const i64 vbase = T.vbase, cbase = T.cbase;
+    double sum[BT_ROWS / RPP];
+#pragma unroll
+    for (int p = 0; p < BT_ROWS / RPP; ++p) {
+      const int rl = p * RPP + g;
+      const i64 row = r0 + rl;
+      double acc = 0.0;
+      if (row < rows) {
+        const i64 b0 = T.ptr[rl], e = T.ptr[rl + 1];
+        for (i64 k0 = b0 + l; k0 < e; k0 += i64(TPR) * U) {
+          double v[U], xv[U];
+          int c[U];
+#pragma unroll
+          for (int j = 0; j < U; ++j) {
+            const i64 k = k0 + i64(j) * TPR;
+            const bool in = k < e;
+            if (vbase >= 0) {
+              v[j] = in ? T.val[k - vbase] : 0.0;
+              c[j] = in ? T.col[k - cbase] : -1;
+            } else {
+              v[j] = in ? ld_stream(val + k) : 0.0;
+              c[j] = in ? ld_stream(col + k) : -1;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < U; ++j) xv[j] = c[j] >= 0 ? __ldg(x + c[j]) : 0.0;
+#pragma unroll
+          for (int j = 0; j < U; ++j) acc += v[j] * xv[j];
+        }
+      }
+      sum[p] = acc;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+#pragma unroll
+    for (int p = 0; p < BT_ROWS / RPP; ++p) {
+      const i64 row = r0 + p * RPP + g;
+      const double sr = group_sum<TPR>(sum[p]);
+      if (row < rows && l == 0) y[row] = epi_out(ep, x, row, sr);
+    }
+  }
+}
+
 // Persistent CSR SpMV: TPR lanes per row, U batched (value, column) loads, rows g, g + G, ...
 // with the next row's pointers fetched ahead (the pointer -> value -> x chain otherwise costs
 // three dependent memory latencies per row).  Bitwise k_spmv_b<TPR, U> (same lanes, same order).
@@ -1061,6 +1222,29 @@ void launch_st16t(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
   CF_LAUNCHED();
 }
 
+// TMA-fed CSR SpMV (k_spmv_bt) for long short-row matrices; CF_NO_SPMV_BT=1: k_spmv_b (A/B switch)
+bool spmv_bt_ok(const Csr& A) {
+  static const bool off = std::getenv("CF_NO_SPMV_BT") != nullptr;
+  return !off && A.st.kind == 0 && A.rows >= 262144 &&
+         ((reinterpret_cast<uintptr_t>(A.val.p) | reinterpret_cast<uintptr_t>(A.col.p)) & 15) == 0;
+}
+
+template <int TPR, int U>
+void launch_bt(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
+  constexpr int S = 2, MINB = 3;
+  constexpr int smem = int(sizeof(BtStage)) * S + 2 * S * 8;
+  static int bps = 0;
+  if (!bps) {
+    CF_CUDA(cudaFuncSetAttribute(k_spmv_bt<TPR, U, S, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_bt<TPR, U, S, MINB>, 288, smem));
+    if (bps < 1) fail(CF_ERR_CUDA, "k_spmv_bt: no resident block");
+  }
+  const i64 ntiles = (A.rows + BT_ROWS - 1) / BT_ROWS;
+  const int grid = int(std::min<i64>(ntiles, i64(bps) * rt().sm_count));
+  k_spmv_bt<TPR, U, S, MINB><<<grid, 288, smem, stream()>>>(A.rows, A.nnz, A.ptr.p, A.col.p, A.val.p, x, y, ep);
+  CF_LAUNCHED();
+}
+
 // PF: the persistent pointer-prefetching CSR kernel (k_spmv_pf) instead of k_spmv_b
 template <int TPR, int U, bool PF = false>
 void launch_b(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
@@ -1184,9 +1368,13 @@ void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
     return;
   }
   if (mean > 64) launch_b<16, 4>(A, x, y, ep);
-  else if (mean > 24) launch_b<8, 4>(A, x, y, ep);
-  else if (mean > 12) launch_b<4, 5>(A, x, y, ep);
-  else launch_b<4, 3>(A, x, y, ep);
+  else if (mean > 24) {
+    if (spmv_bt_ok(A)) launch_bt<8, 4>(A, x, y, ep);
+    else launch_b<8, 4>(A, x, y, ep);
+  } else if (mean > 12) {
+    if (spmv_bt_ok(A)) launch_bt<4, 5>(A, x, y, ep);
+    else launch_b<4, 5>(A, x, y, ep);
+  } else launch_b<4, 3>(A, x, y, ep);
 }
 
 void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add) {
