@@ -1634,7 +1634,11 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
   // prefetching numeric over all rows with shared memory for B.cols columns: one round trip (nnz).
   // Same per-entry summation order as every other path (CF_SPGEMM_NO_SMALL=1: tiered paths).
   static const bool no_small = std::getenv("CF_SPGEMM_NO_SMALL") != nullptr;
-  if (!no_small && m > 0 && m <= SMALL_ROWS && B.cols <= SMALL_COLS && maxb >= 1 && maxb <= 1024) {
+  static const i64 small_rows = [] {  // CF_SPGEMM_SMALL_ROWS: A/B override of the row limit
+    const char* e = std::getenv("CF_SPGEMM_SMALL_ROWS");
+    return e ? i64(std::atoll(e)) : SMALL_ROWS;
+  }();
+  if (!no_small && m > 0 && m <= small_rows && B.cols <= SMALL_COLS && maxb >= 1 && maxb <= 1024) {
     auto C = std::make_unique<Csr>();
     C->rows = m;
     C->cols = B.cols;
