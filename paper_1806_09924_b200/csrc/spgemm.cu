@@ -609,7 +609,8 @@ __global__ void __launch_bounds__(256) k_sym_flags_st(i64 rows, const i64* __res
     if (flg[t]) ccol[o++] = t;
 }
 
-__global__ void __launch_bounds__(256) k_num_cta_st(i64 nrows, const i64* __restrict__ ap, const int* __restrict__ ac,
+__global__ void __launch_bounds__(256) k_num_cta_st(const int* __restrict__ rowlist, i64 nrows,
+                                                    const i64* __restrict__ ap, const int* __restrict__ ac,
                                                     const double* __restrict__ av, const double* __restrict__ rs,
                                                     const i64* __restrict__ bp, const int* __restrict__ bc,
                                                     const double* __restrict__ bv, const i64* __restrict__ cp,
@@ -618,8 +619,8 @@ __global__ void __launch_bounds__(256) k_num_cta_st(i64 nrows, const i64* __rest
   __shared__ int off[257], wsum[8];
   __shared__ i64 q0s[256];
   __shared__ double as[256];
-  const i64 i = blockIdx.x;
-  if (i >= nrows) return;
+  if (i64(blockIdx.x) >= nrows) return;
+  const i64 i = rowlist ? rowlist[blockIdx.x] : i64(blockIdx.x);
   const i64 c0 = cp[i];
   const int nc = int(cp[i + 1] - c0);
   double* prod = reinterpret_cast<double*>(smraw);
@@ -1446,6 +1447,22 @@ static std::unique_ptr<Csr> spgemm_symbolic(const Csr& A, const Csr& B, int L, i
   static const bool force = std::getenv("CF_SPGEMM_FORCE_PATHS") != nullptr;
   if (!no_flags && B.cols <= FLAG_MAX && m < INT_MAX && (force || (m <= 32768 && maxb >= 64))) {
     const size_t sm = size_t(B.cols) + 16;
+    static const bool no_staged = std::getenv("CF_SPGEMM_NO_STAGED") != nullptr;
+    if (!no_staged) {
+      CF_CUDA(cudaFuncSetAttribute(k_sym_flags_st<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      k_sym_flags_st<0><<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), cnt,
+                                                       nullptr);
+      CF_LAUNCHED();
+      scan_excl(C->ptr.p, m + 1);
+      C->nnz = read_i64(C->ptr.p + m);
+      C->col.alloc(std::max<i64>(C->nnz, 1));
+      C->val.alloc(std::max<i64>(C->nnz, 1));
+      CF_CUDA(cudaFuncSetAttribute(k_sym_flags_st<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      k_sym_flags_st<1><<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), C->ptr.p,
+                                                       C->col.p);
+      CF_LAUNCHED();
+      return C;
+    }
     CF_CUDA(cudaFuncSetAttribute(k_sym_flags<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
     k_sym_flags<0><<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, B.ptr.p, B.col.p, int(B.cols), cnt, nullptr);
     CF_LAUNCHED();
@@ -1573,6 +1590,17 @@ static void spgemm_numeric(const Csr& A, const Csr& B, const double* row_scale, 
                                              B.col.p, B.val.p, C.ptr.p, C.col.p, C.val.p);
           CF_LAUNCHED();
         };
+        // staged form (all B-row loads of 256 A entries in flight at once) when its sub-chunk
+        // buffers fit beside the row's accumulators; CF_SPGEMM_NO_STAGED=1: the prefetching kernel
+        static const bool no_staged = std::getenv("CF_SPGEMM_NO_STAGED") != nullptr;
+        const size_t sms = sm + size_t(ST_CH) * (sizeof(double) + sizeof(int));
+        if (!no_staged && sms <= size_t(200) * 1024) {
+          CF_CUDA(cudaFuncSetAttribute(k_num_cta_st, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sms)));
+          k_num_cta_st<<<all.n, 256, sms, stream()>>>(all.list.p, all.n, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p,
+                                                      B.col.p, B.val.p, C.ptr.p, C.col.p, C.val.p);
+          CF_LAUNCHED();
+          return;
+        }
         if (maxb <= 256) launch(k_num_cta_pf<1>);
         else if (maxb <= 512) launch(k_num_cta_pf<2>);
         else launch(k_num_cta_pf<4>);
@@ -1662,7 +1690,8 @@ std::unique_ptr<Csr> spgemm(const Csr& A, const Csr& B, const double* row_scale)
       const size_t sm = size_t(ST_CH) * (sizeof(double) + sizeof(int)) +
                         size_t(B.cols) * (sizeof(double) + sizeof(int)) + 16;
       CF_CUDA(cudaFuncSetAttribute(k_num_cta_st, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      k_num_cta_st<<<int(m), 256, sm, stream()>>>(m, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p, B.col.p, B.val.p,
+      k_num_cta_st<<<int(m), 256, sm, stream()>>>(nullptr, m, A.ptr.p, A.col.p, A.val.p, row_scale, B.ptr.p, B.col.p,
+                                                  B.val.p,
                                                   C->ptr.p, C->col.p, C->val.p);
       CF_LAUNCHED();
     }
