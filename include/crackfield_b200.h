@@ -408,6 +408,11 @@ int cf_comm_create_host(int rank, int size, const cf_host_transport* transport, 
 int cf_comm_unique_id(uint8_t id[128]);
 int cf_comm_create(const uint8_t id[128], int rank, int size, cf_comm* out);
 int cf_comm_info(cf_comm c, int* rank, int* size);
+/* Runs every NCCL entry point the decomposed step uses (id, init, all-gather in and out of place,
+ * int64 sum / max all-reduce, broadcast, grouped broadcasts, grouped send / receive, destroy) on a
+ * one-rank communicator on the current device and checks the results; *failed_checks = 0 when all
+ * hold.  What a single-GPU box can verify of the NCCL transport. */
+int cf_comm_selftest(int* failed_checks);
 int cf_comm_destroy(cf_comm c);
 int cf_newton_active_set_step_comm(cf_problem p, cf_state s, const cf_material* mat, const cf_regularization* reg,
                                    const cf_solver_options* opts, cf_comm comm, cf_newton_iteration* its,

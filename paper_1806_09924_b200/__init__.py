@@ -374,6 +374,14 @@ class Communicator:
         check(load().cf_comm_unique_id(buf))
         return bytes(buf)
 
+    @staticmethod
+    def nccl_selftest() -> int:
+        """Every NCCL entry point of the decomposed step on a one-rank communicator on the current
+        device (cf_comm_selftest); returns the number of failed checks (0 = all hold)."""
+        bad = C.c_int(-1)
+        check(load().cf_comm_selftest(C.byref(bad)))
+        return bad.value
+
     @classmethod
     def from_torch_distributed(cls, group=None) -> "Communicator":
         import torch.distributed as dist

@@ -234,6 +234,7 @@ SIGNATURES = [
     ("cf_comm_create", _I, [_P, _I, _I, C.POINTER(_P)]),
     ("cf_comm_create_host", _I, [_I, _I, _P, C.POINTER(_P)]),
     ("cf_comm_info", _I, [_P, C.POINTER(_I), C.POINTER(_I)]),
+    ("cf_comm_selftest", _I, [C.POINTER(_I)]),
     ("cf_comm_destroy", _I, [_P]),
     ("cf_newton_active_set_step_comm", _I, [_P, _P, C.POINTER(Material), C.POINTER(Regularization),
                                             C.POINTER(SolverOptions), _P, _P, _I, C.POINTER(_I), C.POINTER(_I),

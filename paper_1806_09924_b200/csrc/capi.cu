@@ -1042,6 +1042,14 @@ int cf_comm_unique_id(uint8_t id[128]) {
   });
 }
 
+int cf_comm_selftest(int* failed_checks) {
+  return guard([&] {
+    CHECK_ARG(failed_checks, "cf_comm_selftest: null argument");
+    ensure_device();
+    *failed_checks = comm_selftest();
+  });
+}
+
 int cf_comm_create_host(int rank, int size, const cf_host_transport* transport, cf_comm* out) {
   return guard([&] {
     CHECK_ARG(out && transport, "cf_comm_create_host: null argument");

@@ -45,6 +45,7 @@ struct Comm {
 };
 
 void comm_unique_id(unsigned char out[128]);
+int comm_selftest();  // every NCCL entry point on a one-rank communicator; failed checks
 std::unique_ptr<Comm> comm_create(const unsigned char id[128], int rank, int size);
 std::unique_ptr<Comm> comm_create_host(int rank, int size, const cf_host_transport& t);
 

@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -101,6 +102,54 @@ std::unique_ptr<Comm> comm_create(const unsigned char id_bytes[128], int rank, i
     c->nccl = h;
   }
   return c;
+}
+
+// Every NCCL entry point the decomposed step uses, executed on a one-rank communicator on the
+// library stream and checked on the host (a single-GPU box cannot run two NCCL ranks, so this is
+// what can be exercised there: loading libnccl, the symbol table, the id / init / destroy
+// sequence, all-gather in and out of place, int64 sum / max all-reduce, broadcast, grouped
+// broadcasts and a grouped send / receive to self).  Returns the number of failed checks.
+int comm_selftest() {
+  const NcclApi& api = nccl();
+  ncclUniqueId id;
+  CF_NCCL(api.GetUniqueId(&id));
+  ncclComm_t h = nullptr;
+  CF_NCCL(api.CommInitRank(&h, 1, id, 0));
+  int bad = 0;
+  constexpr int K = 1000;
+  std::vector<double> a(K), b(K, -1.0);
+  for (int i = 0; i < K; ++i) a[i] = 0.5 * i + 0.25;
+  DevBuf<double> da(K), db(K), dc(K);
+  CF_CUDA(cudaMemcpyAsync(da.p, a.data(), K * sizeof(double), cudaMemcpyHostToDevice, stream()));
+  CF_NCCL(api.AllGather(da.p, db.p, size_t(K), ncclFloat64, h, stream()));  // out of place
+  CF_NCCL(api.AllGather(db.p, db.p, size_t(K), ncclFloat64, h, stream()));  // in place (rank 0's chunk)
+  CF_CUDA(cudaMemcpyAsync(b.data(), db.p, K * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  bad += std::memcmp(a.data(), b.data(), K * sizeof(double)) != 0;
+  long long iv[3] = {7, -3, 1LL << 40}, io[3] = {0, 0, 0};
+  DevBuf<long long> di(3);
+  CF_CUDA(cudaMemcpyAsync(di.p, iv, sizeof(iv), cudaMemcpyHostToDevice, stream()));
+  CF_NCCL(api.AllReduce(di.p, di.p, 3, ncclInt64, ncclSum, h, stream()));
+  CF_NCCL(api.AllReduce(di.p, di.p, 3, ncclInt64, ncclMax, h, stream()));
+  CF_CUDA(cudaMemcpyAsync(io, di.p, sizeof(io), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  bad += std::memcmp(iv, io, sizeof(iv)) != 0;
+  CF_NCCL(api.Broadcast(da.p, da.p, K * sizeof(double), ncclUint8, 0, h, stream()));
+  CF_NCCL(api.GroupStart());
+  CF_NCCL(api.Broadcast(da.p, da.p, K * sizeof(double), ncclUint8, 0, h, stream()));
+  CF_NCCL(api.Broadcast(db.p, db.p, K * sizeof(double), ncclUint8, 0, h, stream()));
+  CF_NCCL(api.GroupEnd());
+  CF_CUDA(cudaMemsetAsync(dc.p, 0, K * sizeof(double), stream()));
+  CF_NCCL(api.GroupStart());  // the halo exchange's pattern, with this rank as its own neighbour
+  CF_NCCL(api.Send(da.p, K * sizeof(double), ncclUint8, 0, h, stream()));
+  CF_NCCL(api.Recv(dc.p, K * sizeof(double), ncclUint8, 0, h, stream()));
+  CF_NCCL(api.GroupEnd());
+  std::fill(b.begin(), b.end(), -1.0);
+  CF_CUDA(cudaMemcpyAsync(b.data(), dc.p, K * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  CF_CUDA(cudaStreamSynchronize(stream()));
+  bad += std::memcmp(a.data(), b.data(), K * sizeof(double)) != 0;
+  CF_NCCL(api.CommDestroy(h));
+  return bad;
 }
 
 std::unique_ptr<Comm> comm_create_host(int rank, int size, const cf_host_transport& t) {

@@ -214,8 +214,11 @@ __global__ void k_mf_diag(GridDesc g, const Tables* __restrict__ T, double mu, d
 // du_a/dx at (p,q,r) = (1/h) sum_{j,l} N_j(q) N_l(r) [u_a(1,j,l) - u_a(0,j,l)] (likewise y, z), and
 // the test side sum_q sigma_ab d_b N_k is accumulated per direction in 2 x 2 face sums.  About 1650
 // flops per cell instead of the canonical 2688 of the point-wise form.
-constexpr int MFB = 8, MFT = MFB + 2, MFC = MFB + 1, MF_CS = 25;  // cell-output stride (odd)
-constexpr int MF_THREADS = 96;                                     // >= MFC * MFC = 81 cells per layer
+#ifndef CF_MFB
+#define CF_MFB 8  // owned vertices per tile side (A/B builds: -DCF_MFB=7|10|15 with a matching CF_MF_MINB)
+#endif
+constexpr int MFB = CF_MFB, MFT = MFB + 2, MFC = MFB + 1, MF_CS = 25;  // cell-output stride (odd)
+constexpr int MF_THREADS = (MFC * MFC + 31) / 32 * 32;                 // >= MFC * MFC cells per layer
 constexpr int MF_ZSEG = 12;                                        // cell layers per CTA (short segments: more CTAs, better tail; A/B 48 -> 12: 0.52 -> 0.41 ms at config 3)
 
 // the 24 outputs (k*3 + a) of one cell; U(i,j,l,a) and PT(i,j,l) read the corner values
@@ -307,6 +310,7 @@ __device__ __forceinline__ double mf_epi(const SpmvEpi& ep, const double* __rest
 #ifndef CF_MF_MINB
 #define CF_MF_MINB 5  // 126 registers, 5 CTAs per SM (A/B: config 1 1.24 -> 1.12 ms)
 #endif
+#if CF_MFB <= 8  // (its two cell-output buffers exceed the static shared-memory limit for larger tiles)
 __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g, const Tables* __restrict__ T, double mu,
                                                          double lam, double kap, double xi0, double xi1,
                                                          double scale, int zseg, int pz_lo, int pz_hi, i64 x_off,
@@ -436,6 +440,8 @@ __global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep(GridDesc g,
   }
 }
 
+#endif
+
 // k_mf_sweep with the vertex planes staged by cp.async two layers ahead: a ring of four planes
 // (the layer's two, the one the constrained rows of the previous vertex plane read, the one in
 // flight), u of constrained components zeroed by the thread that copied it once its copy landed
@@ -449,13 +455,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(MF_THREADS, CF_MF_MINB) k_mf_sweep_async(GridDesc g, const Tables* __restrict__ T, double mu,
+// TB: owned vertices per tile side (cells per layer (TB + 1)^2: 7 -> 2 full warps, 8 -> 3 warps
+// at 84%, 10 -> 4 warps at 95%; the output does not depend on it)
+constexpr int mf_threads(int tb) { return ((tb + 1) * (tb + 1) + 31) / 32 * 32; }
+template <int TB, int MINB>
+__global__ void __launch_bounds__(mf_threads(TB), MINB) k_mf_sweep_async(GridDesc g, const Tables* __restrict__ T, double mu,
                                                          double lam, double kap, double xi0, double xi1,
                                                          double scale, int zseg, int pz_lo, int pz_hi, i64 x_off,
                                                          i64 y_lo, i64 y_hi, const double* __restrict__ x,
                                                          const double* __restrict__ pt,
                                                          const std::uint8_t* __restrict__ flag,
                                                          double* __restrict__ y, SpmvEpi ep) {
+  constexpr int MFB = TB, MFT = MFB + 2, MFC = MFB + 1, MF_THREADS = mf_threads(TB);  // (shadow the file-scope tile)
   constexpr int PL = MFT * MFT;           // vertices of one tile plane
   constexpr int VPT = (PL + MF_THREADS - 1) / MF_THREADS;  // plane vertices per thread (2)
   __shared__ double su[4][PL * 3], sp[4][PL];  // vertex planes z mod 4
@@ -632,7 +643,25 @@ void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep) {
   build_tables(P, op.mu, op.lam);
   const GridDesc& g = P.g;
   if (g.d != 3) fail(CF_ERR_UNSUPPORTED, "mf_apply: the matrix-free M_uu is 3d");
-  const int nb = int((g.nn + MFB - 1) / MFB);
+  // tile side by the cell-warp count of a sweep, tiles^2 x warps per tile layer (measured order on
+  // 129^3: 10 < 7 < 8 = 0.330 / 0.343 / 0.351 ms, on 193^3: 7 < 10 < 8 = 0.851 / 0.875 / 0.941 ms,
+  // both as the count predicts); CF_MF_TILE=7|8|10 forces one (A/B)
+  static const int forced = [] {
+    const char* e = std::getenv("CF_MF_TILE");
+    return e ? std::atoi(e) : 0;
+  }();
+  int tb = forced;
+  if (tb != 7 && tb != 8 && tb != 10) {
+    i64 best = -1;
+    for (int c : {10, 7, 8}) {
+      const i64 t = (g.nn + c - 1) / c, cost = t * t * (mf_threads(c) / 32);
+      if (best < 0 || cost < best) {
+        best = cost;
+        tb = c;
+      }
+    }
+  }
+  const int nb = int((g.nn + tb - 1) / tb);
   static const char* zenv = std::getenv("CF_MF_ZSEG");  // A/B: cell layers per CTA
   const int zseg = zenv ? std::max(1, std::atoi(zenv)) : MF_ZSEG;
   const i64 plane = g.nn * g.nn;
@@ -643,10 +672,24 @@ void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep) {
   const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
   const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
   static const bool sync_loads = std::getenv("CF_MF_SYNC_LOADS") != nullptr;  // A/B: plain plane loads
-  auto kern = sync_loads ? k_mf_sweep : k_mf_sweep_async;
-  kern<<<nb * nb * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1,
-                                                    W / (g.h * g.h), zseg, pz_lo, pz_hi, op.x_off, y_lo, y_hi,
-                                                    x, op.pt, op.flag, y, ep);
+  auto launch = [&](auto kern, int threads) {
+    kern<<<nb * nb * nseg, threads, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1, W / (g.h * g.h), zseg,
+                                                   pz_lo, pz_hi, op.x_off, y_lo, y_hi, x, op.pt, op.flag, y, ep);
+  };
+#if CF_MFB <= 8
+  if (sync_loads) {
+    const int nb8 = int((g.nn + MFB - 1) / MFB);
+    k_mf_sweep<<<nb8 * nb8 * nseg, MF_THREADS, 0, stream()>>>(g, P.tab.p, op.mu, op.lam, op.kap, xi0, xi1,
+                                                             W / (g.h * g.h), zseg, pz_lo, pz_hi, op.x_off, y_lo,
+                                                             y_hi, x, op.pt, op.flag, y, ep);
+    CF_LAUNCHED();
+    return;
+  }
+#endif
+  (void)sync_loads;
+  if (tb == 7) launch(k_mf_sweep_async<7, 8>, mf_threads(7));
+  else if (tb == 10) launch(k_mf_sweep_async<10, 4>, mf_threads(10));
+  else launch(k_mf_sweep_async<8, CF_MF_MINB>, mf_threads(8));
   CF_LAUNCHED();
 }
 

@@ -56,3 +56,28 @@ def test_no_cpu_fallback_without_device(lib):
     import paper_1806_09924_b200 as cf
     with pytest.raises(RuntimeError, match="no CUDA device"):
         cf.Problem(2, 1.0, 2, 0)
+
+
+def test_production_spmv_kernels_use_tma_bulk_copies(lib):
+    """The sm_100a object of spmv.cu (the production M_uu SpMV k_spmv_st16t and the prolongator
+    SpMV k_spmv_bt) must contain the bulk-copy and mbarrier instructions their design rests on:
+    UBLKCP.S.G (cp.async.bulk global -> shared) and SYNCS.ARRIVE.TRANS64 / SYNCS.PHASECHK (mbarrier
+    expect-tx arrive and try_wait), the SASS mnemonics /opt/skills/guides/B200_PROFILING.md names."""
+    import shutil
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not on PATH")
+    obj = os.path.join(ROOT, "paper_1806_09924_b200", "csrc", "spmv.o")
+    target = obj if os.path.exists(obj) else lib.LIB_PATH
+    sass = subprocess.check_output(["cuobjdump", "-sass", target], text=True)
+    funcs = re.split(r"\n\s*Function : ", sass)
+    by_kernel = {}
+    for f in funcs[1:]:
+        name = f.split("\n", 1)[0]
+        for k in ("k_spmv_st16t", "k_spmv_bt"):
+            if k in name:
+                by_kernel.setdefault(k, "")
+                by_kernel[k] += f
+    assert set(by_kernel) == {"k_spmv_st16t", "k_spmv_bt"}, sorted(by_kernel)
+    for k, body in by_kernel.items():
+        assert "UBLKCP.S.G" in body, k
+        assert "SYNCS.ARRIVE.TRANS64" in body and "SYNCS.PHASECHK.TRANS64.TRYWAIT" in body, k

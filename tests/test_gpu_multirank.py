@@ -98,3 +98,13 @@ def test_multirank_newton_step(tmp_path, d, n0, r, size, mode):
     else:
         assert np.linalg.norm(xs[0] - ref) <= 1e-6 * np.linalg.norm(ref)
         assert int(its[0][-1, 1]) == rep["iterations"][-1]["active_size"]
+
+
+def test_nccl_transport_selftest_one_rank():
+    """The NCCL transport itself (comm.cu): libnccl loaded from the process, the symbol table, id /
+    init / destroy, all-gather in and out of place, int64 sum / max all-reduce, broadcast, grouped
+    broadcasts and a grouped send / receive, each executed on a one-rank communicator on the
+    library stream and checked on the host.  (Two NCCL ranks cannot share this box's one GPU; the
+    multi-rank control flow above runs through the host transport.)"""
+    import paper_1806_09924_b200 as cf
+    assert cf.Communicator.nccl_selftest() == 0
