@@ -663,11 +663,19 @@ void mf_apply(const MfOp& op, const double* x, double* y, const SpmvEpi& ep) {
   }
   const int nb = int((g.nn + tb - 1) / tb);
   static const char* zenv = std::getenv("CF_MF_ZSEG");  // A/B: cell layers per CTA
-  const int zseg = zenv ? std::max(1, std::atoi(zenv)) : MF_ZSEG;
   const i64 plane = g.nn * g.nn;
   const i64 y_lo = op.y_lo, y_hi = op.y_hi < 0 ? g.V : op.y_hi;
   if (y_hi <= y_lo) return;
   const int pz_lo = int(y_lo / plane), pz_hi = int((y_hi - 1) / plane) + 1;
+  // vertex planes per CTA: each segment repeats one cell layer, but the sweep needs ~7 waves of
+  // CTAs to balance (measured, 129^3 with 10-wide tiles: 5 planes 0.308 ms, 8 0.321, 12 0.330,
+  // 16 0.371; 193^3 with 7-wide tiles: 7 0.842, 11 0.836, 12 0.851, 16 0.870)
+  int zseg = MF_ZSEG;
+  if (zenv) zseg = std::max(1, std::atoi(zenv));
+  else {
+    const i64 slots = i64(rt().sm_count) * (tb == 7 ? 8 : tb == 10 ? 4 : CF_MF_MINB);
+    zseg = int(std::min<i64>(11, std::max<i64>(5, i64(pz_hi - pz_lo) * nb * nb / (7 * slots))));
+  }
   const int nseg = (pz_hi - pz_lo + zseg - 1) / zseg;
   const double xi0 = 0.5 * (1.0 - 1.0 / std::sqrt(3.0)), xi1 = 0.5 * (1.0 + 1.0 / std::sqrt(3.0));
   const double W = g.detJ / 8.0;  // 2-point Gauss weight (1/2)^3 times h^3
