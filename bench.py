@@ -346,7 +346,7 @@ def operator_leg(cf, device, stream, applies=20):
     mf = {"ms_per_apply": ms_mf, "gflops": flops / (ms_mf * 1e-3) / 1e9, "fp64_peak_tflops_measured": fp64,
           "frac_of_fp64_peak": flops / (ms_mf * 1e-3) / 1e12 / fp64, "rel_err_vs_assembled": rel_mf,
           "min_bytes": 8 * (2 * nu + P.n_vertices),
-          "note": "single-pass z-sweep (k_mf_sweep: 8x8 vertex columns per CTA, 12 cell layers, one thread per "
+          "note": "single-pass z-sweep (k_mf_sweep_async: 7x7 / 8x8 / 10x10 vertex columns per CTA chosen per grid, 5-11 vertex planes per CTA, one thread per "
                   "cell, sum-factorised ~1,650 flops), FMA-contracted element math, compared with the assembled "
                   "apply to rounding; flops = canonical 2,688 per cell. The same kernel is the Newton step's "
                   "Krylov operator and finest-level smoother in 3d (operator_kind 1)"}

@@ -817,24 +817,25 @@ __global__ void __launch_bounds__(288, MINB) k_spmv_st16t(i64 rows, i64 nnz, i64
 // order, reading values and columns from shared memory, so only the x gathers touch global memory.
 // A tile with more than BT_CAP entries is read from global memory by the same code path (direct).
 // Bitwise k_spmv_b<TPR, U>.
-constexpr int BT_ROWS = 64;
-constexpr int BT_CAP = 3072;  // entries per stage
+template <int ROWS, int CAP>
 struct BtStage {
-  double val[BT_CAP + 2];
-  int col[BT_CAP + 4];
-  i64 ptr[BT_ROWS + 2];  // + 1 pad: 16-byte stage size
-  i64 vbase, cbase;  // first staged index of val (even) and col (multiple of 4); vbase < 0: direct tile
+  double val[CAP + 2];
+  int col[CAP + 4];
+  i64 ptr[ROWS + 2];  // + 1 pad: 16-byte stage size
+  i64 vbase, cbase;   // first staged index of val (even) and col (multiple of 4); vbase < 0: direct tile
 };
-static_assert(sizeof(BtStage) % 16 == 0 && ((BT_CAP + 2) * 8) % 16 == 0 && ((BT_CAP + 4) * 4) % 16 == 0,
-              "stage alignment");
 
-template <int TPR, int U, int S, int MINB>
+template <int TPR, int U, int S, int MINB, int BT_ROWS, int BT_CAP>
 __global__ void __launch_bounds__(288, MINB) k_spmv_bt(i64 rows, i64 nnz, const i64* __restrict__ ptr,
                                                        const int* __restrict__ col, const double* __restrict__ val,
                                                        const double* __restrict__ x, double* y, SpmvEpi ep) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  BtStage* st = reinterpret_cast<BtStage*>(smem_raw);
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(BtStage) * S);
+  using Stage = BtStage<BT_ROWS, BT_CAP>;
+  static_assert(sizeof(Stage) % 16 == 0 && ((BT_CAP + 2) * 8) % 16 == 0 && ((BT_CAP + 4) * 4) % 16 == 0 &&
+                    (BT_ROWS == 32 || BT_ROWS == 64) && BT_ROWS % (256 / TPR) == 0,
+                "stage layout");
+  Stage* st = reinterpret_cast<Stage*>(smem_raw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + sizeof(Stage) * S);
   unsigned long long* empty = full + S;
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -854,7 +855,7 @@ __global__ void __launch_bounds__(288, MINB) k_spmv_bt(i64 rows, i64 nnz, const 
       const i64 r0 = tl * BT_ROWS;
       const int nr = int(min(i64(BT_ROWS), rows - r0));
       pa = lane <= nr ? ptr[r0 + lane] : 0;
-      pb = lane + 32 <= nr ? ptr[r0 + 32 + lane] : 0;
+      pb = lane + 32 <= nr ? ptr[r0 + 32 + lane] : 0;  // (BT_ROWS == 32: lane 0 only, entry 32)
       pc = (lane == 0 && nr == 64) ? ptr[r0 + 64] : 0;
     };
     if (tile < ntiles) load_ptrs(tile);
@@ -866,7 +867,7 @@ __global__ void __launch_bounds__(288, MINB) k_spmv_bt(i64 rows, i64 nnz, const 
       const i64 ca = pa, cb = pb, cc = pc;
       if (tile + gridDim.x < ntiles) load_ptrs(tile + gridDim.x);
       mbar_wait(empty + s, ph ^ 1u);
-      BtStage& T = st[s];
+      Stage& T = st[s];
       if (lane <= nr) T.ptr[lane] = ca;
       if (lane + 32 <= nr) T.ptr[lane + 32] = cb;
       if (lane == 0 && nr == 64) T.ptr[64] = cc;
@@ -925,7 +926,7 @@ __global__ void __launch_bounds__(288, MINB) k_spmv_bt(i64 rows, i64 nnz, const 
     const unsigned ph = (it / S) & 1u;
     const i64 r0 = tile * BT_ROWS;
     mbar_wait(full + s, ph);
-    const BtStage& T = st[s];
+    const Stage& T = st[s];
     const i64 vbase = T.vbase, cbase = T.cbase;
     double sum[BT_ROWS / RPP];
 #pragma unroll
@@ -1229,20 +1230,36 @@ bool spmv_bt_ok(const Csr& A) {
          ((reinterpret_cast<uintptr_t>(A.val.p) | reinterpret_cast<uintptr_t>(A.col.p)) & 15) == 0;
 }
 
-template <int TPR, int U>
-void launch_bt(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
-  constexpr int S = 2, MINB = 3;
-  constexpr int smem = int(sizeof(BtStage)) * S + 2 * S * 8;
+template <int TPR, int U, int S, int MINB, int ROWS, int CAP>
+void launch_bt_cfg(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
+  constexpr int smem = int(sizeof(BtStage<ROWS, CAP>)) * S + 2 * S * 8;
   static int bps = 0;
   if (!bps) {
-    CF_CUDA(cudaFuncSetAttribute(k_spmv_bt<TPR, U, S, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_bt<TPR, U, S, MINB>, 288, smem));
+    CF_CUDA(cudaFuncSetAttribute(k_spmv_bt<TPR, U, S, MINB, ROWS, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+    CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_spmv_bt<TPR, U, S, MINB, ROWS, CAP>, 288, smem));
     if (bps < 1) fail(CF_ERR_CUDA, "k_spmv_bt: no resident block");
   }
-  const i64 ntiles = (A.rows + BT_ROWS - 1) / BT_ROWS;
+  const i64 ntiles = (A.rows + ROWS - 1) / ROWS;
   const int grid = int(std::min<i64>(ntiles, i64(bps) * rt().sm_count));
-  k_spmv_bt<TPR, U, S, MINB><<<grid, 288, smem, stream()>>>(A.rows, A.nnz, A.ptr.p, A.col.p, A.val.p, x, y, ep);
+  k_spmv_bt<TPR, U, S, MINB, ROWS, CAP><<<grid, 288, smem, stream()>>>(A.rows, A.nnz, A.ptr.p, A.col.p, A.val.p, x, y,
+                                                                       ep);
   CF_LAUNCHED();
+}
+
+// ring shape: CF_SPMV_BT_CFG=0..3 (A/B runs); default 0
+template <int TPR, int U>
+void launch_bt(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
+  static const int cfg = [] {
+    const char* e = std::getenv("CF_SPMV_BT_CFG");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (cfg == 1) return launch_bt_cfg<TPR, U, 2, 4, 64, 2048>(A, x, y, ep);  // 4 CTAs/SM, 2 x 25 KB
+  if constexpr (TPR == 8) {  // 32-row tiles: one pass of 32 rows
+    if (cfg == 2) return launch_bt_cfg<TPR, U, 3, 4, 32, 1024>(A, x, y, ep);  // 4 CTAs/SM, 3 x 12.6 KB
+    if (cfg == 3) return launch_bt_cfg<TPR, U, 4, 4, 32, 1024>(A, x, y, ep);  // 4 CTAs/SM, 4 x 12.6 KB
+  }
+  launch_bt_cfg<TPR, U, 2, 3, 64, 3072>(A, x, y, ep);  // 3 CTAs/SM, 2 x 37 KB
 }
 
 // PF: the persistent pointer-prefetching CSR kernel (k_spmv_pf) instead of k_spmv_b
