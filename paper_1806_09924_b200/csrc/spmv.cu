@@ -1247,18 +1247,24 @@ void launch_bt_cfg(const Csr& A, const double* x, double* y, const SpmvEpi& ep) 
   CF_LAUNCHED();
 }
 
-// ring shape: CF_SPMV_BT_CFG=0..3 (A/B runs); default 0
+// ring shape: CF_SPMV_BT_CFG=0..6 (A/B runs).  Config-3 level-0 P alone / the whole u V-cycle:
+// 0: 0.426 / 2.959 ms, 1: 0.740 / 3.176 (tiles beyond 2048 entries fall to the direct path),
+// 2: 0.495 / 2.963, 3: 0.719 / 3.251, 4: 0.434 / 2.879, 5: 0.470 / 2.991, 6: 0.540 / 3.275;
+// default 4 for 8 lanes per row (32-row tiles, 4 CTAs per SM), 0 for 4 lanes
 template <int TPR, int U>
 void launch_bt(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
   static const int cfg = [] {
     const char* e = std::getenv("CF_SPMV_BT_CFG");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : (TPR == 8 ? 4 : 0);
   }();
   if (cfg == 1) return launch_bt_cfg<TPR, U, 2, 4, 64, 2048>(A, x, y, ep);  // 4 CTAs/SM, 2 x 25 KB
   if constexpr (TPR == 8) {  // 32-row tiles: one pass of 32 rows
     if (cfg == 2) return launch_bt_cfg<TPR, U, 3, 4, 32, 1024>(A, x, y, ep);  // 4 CTAs/SM, 3 x 12.6 KB
     if (cfg == 3) return launch_bt_cfg<TPR, U, 4, 4, 32, 1024>(A, x, y, ep);  // 4 CTAs/SM, 4 x 12.6 KB
+    if (cfg == 4) return launch_bt_cfg<TPR, U, 2, 4, 32, 2048>(A, x, y, ep);  // 4 CTAs/SM, 2 x 25 KB
+    if (cfg == 5) return launch_bt_cfg<TPR, U, 3, 3, 32, 2048>(A, x, y, ep);  // 3 CTAs/SM, 3 x 25 KB
   }
+  if (cfg == 6) return launch_bt_cfg<TPR, U, 2, 2, 64, 4096>(A, x, y, ep);  // 2 CTAs/SM, 2 x 49 KB
   launch_bt_cfg<TPR, U, 2, 3, 64, 3072>(A, x, y, ep);  // 3 CTAs/SM, 2 x 37 KB
 }
 
