@@ -161,6 +161,33 @@ def test_48_apply_and_u_hierarchy_bitwise(cf, orcmt):
     assert np.array_equal(h.v_cycle(r), ho.vcycle(r))  # residual / post-sweep epilogues (modes 1, 2)
 
 
+def test_48_tma_spmv_equals_register_path_at_every_alignment(cf, orcmt):
+    """k_spmv_st16t (bulk copies of 16-byte units into the stage ring) against k_spmv_st16p, which the
+    dispatch falls back to when x is not 16-byte aligned: the same M_uu applied to the same vector
+    held at an aligned and at an 8-byte-offset device address must agree bit for bit, and with the
+    oracle; sizes whose row count, nnz and vertex parities differ exercise the tile, tail and
+    x-segment alignment cases (nn = 41, 45, 49)."""
+    import torch
+    orc = orcmt
+    for n0, r in ((10, 2), (11, 2), (12, 2)):
+        P, O, mat, omat, reg, oreg, phi = _pair(cf, orc, 3, n0, r)
+        x, pt, cs, ocs = _state48(cf, orc, P, O)
+        J = cf.assemble_jacobian(P, cs, mat, reg, x, pt)
+        assert J.format(0) == "stencil" and J.csr(0).nnz / P.n_u > 64
+        u = torch.from_numpy(x[:P.n_u].copy()).cuda()
+        buf = torch.zeros(P.n_u + 1, dtype=torch.float64, device="cuda")
+        off = buf[1:]
+        off.copy_(u)
+        assert u.data_ptr() % 16 == 0 and off.data_ptr() % 16 == 8
+        ya = J.spmv(0, u)
+        yb = J.spmv(0, off)
+        assert torch.equal(ya, yb)
+        Jo = O.jacobian(ocs, omat, oreg, x, pt)
+        yo = np.zeros(P.n_u)
+        Jo.spmv(0, np.ascontiguousarray(x[:P.n_u]), yo)
+        assert np.array_equal(ya.cpu().numpy(), yo)
+
+
 def test_48_newton_step_bitwise_and_kernel_switches(cf, orcmt):
     orc = orcmt
     P, O, mat, omat, reg, oreg, phi = _pair(cf, orc, 3, 12, 2)
