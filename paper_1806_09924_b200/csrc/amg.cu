@@ -1630,7 +1630,11 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     {
       int bps = 0;
       CF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_lfmis, 256, 0));
-      const int grid = std::max(1, std::min(bps, 4)) * rt().sm_count;
+      static const int bps_cap = [] {  // CF_LFMIS_BPS: blocks per SM of the cooperative grid (A/B)
+        const char* e = std::getenv("CF_LFMIS_BPS");
+        return e ? std::max(1, std::atoi(e)) : 4;
+      }();
+      const int grid = std::max(1, std::min(bps, bps_cap)) * rt().sm_count;
       const i64* a1 = uptr.p;
       const int* a2 = up.p;
       int* a3 = lower.p;  // consumed as the pending-dependency counter

@@ -132,6 +132,11 @@ struct BlockSystem {
   int d = 2;
   std::shared_ptr<MfOp> mf_uu;  // set: M_uu applied matrix-free in block_apply (uu keeps its values)
   i64 in_u() const { return nu_in >= 0 ? nu_in : nu; }
+  // phi rows split for block_apply (spmv.cu, built on first use): rows with a non-empty M_phiu row or
+  // more than one M_phiphi entry ("heavy", ascending) and the rest (active phi dofs: one diagonal entry)
+  mutable DevBuf<int> phi_heavy;
+  mutable DevBuf<std::uint8_t> phi_heavy_flag;
+  mutable i64 n_phi_heavy = -1;  // -1: not classified yet
 };
 
 // ---- host helpers implemented in the .cu files

@@ -8,6 +8,10 @@
 // persistent 8-thread row groups carrying the 16 logical lanes, interior fast path);
 // k_spmv_st_emu (general emulated form: tuning sweeps, CF_ST_EMU=1).  Every variant produces
 // bitwise the TPR-lane reduction of the contract.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <climits>
 #include <cstdint>
 #include <cstdlib>
 
@@ -1122,6 +1126,62 @@ __global__ void __launch_bounds__(256) k_spmv_phi_st(i64 rows, const i64* __rest
   if (row < rows && lane == 0) y[row] = s1 + s2;
 }
 
+// ---- phi rows split by weight -------------------------------------------------------------------
+// Late in a Newton step four phi dofs in five are active: their M_phiu row is empty and their
+// M_phiphi row is the diagonal entry, while a free row carries 81 + 27 entries.  One kernel over all
+// rows keeps mostly empty row groups in flight (the 4-lane dispatch reached 2 TB/s); the heavy rows
+// run from an ascending list with the same lanes, batches and sums, the light rows one thread each
+// with the sum the lanes would form (lane 0's single product, the other lanes and both butterflies
+// adding +0.0).  Bitwise k_spmv_phi_st.
+__global__ void k_phi_heavy_flags(i64 rows, const i64* __restrict__ p1, const i64* __restrict__ p2,
+                                  std::uint8_t* __restrict__ f) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < rows) f[r] = (p1[r + 1] > p1[r] || p2[r + 1] - p2[r] > 1) ? 1 : 0;
+}
+
+template <int TPR, int U, int D>
+__global__ void __launch_bounds__(256) k_spmv_phi_st_list(i64 nlist, const int* __restrict__ list,
+                                                          const i64* __restrict__ p1, const double* __restrict__ v1,
+                                                          const double* __restrict__ x1, StencilCols sc,
+                                                          const i64* __restrict__ p2, const int* __restrict__ c2,
+                                                          const double* __restrict__ v2, const double* __restrict__ x2,
+                                                          double* __restrict__ y) {
+  __shared__ int off[StOff<D>::N];
+  StOff<D>::fill(off, int(sc.nn));
+  __syncthreads();
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 li = t / TPR;
+  const int lane = int(t % TPR);
+  double s1 = 0.0, s2 = 0.0;
+  i64 row = 0;
+  if (li < nlist) {
+    row = list[li];
+    s1 = row_dot_st<TPR, U, D>(p1, v1, x1, row, lane, sc, off);
+    s2 = row_dot_b<TPR, U>(p2, c2, v2, x2, row, lane);
+  }
+  s1 = group_sum<TPR>(s1);
+  s2 = group_sum<TPR>(s2);
+  if (li < nlist && lane == 0) y[row] = s1 + s2;
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(256) k_spmv_phi_light(i64 rows, const std::uint8_t* __restrict__ heavy,
+                                                        const i64* __restrict__ p2, const int* __restrict__ c2,
+                                                        const double* __restrict__ v2, const double* __restrict__ x2,
+                                                        double* __restrict__ y) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows || heavy[r]) return;
+  const i64 k = p2[r];
+  double s1 = 0.0, s2 = 0.0;
+  if (p2[r + 1] > k) s2 += ld_stream(v2 + k) * __ldg(x2 + ld_stream(c2 + k));  // lane 0's sum
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) {  // the butterflies: the other lanes hold +0.0
+    s1 += 0.0;
+    s2 += 0.0;
+  }
+  y[r] = s1 + s2;
+}
+
 // every stored column equals the computed one and the row has the stencil's length (0 or 1 on
 // clamp rows, 0 allowed on constrained phi rows); 8 threads per row read the columns coalesced
 template <int D>
@@ -1180,6 +1240,16 @@ void launch_phi(const BlockSystem& J, const double* x, double* y) {
     else if (TPR == 16 && A.st.d == 3)
       k_spmv_phi_st_emu<16, 8, 2, 3><<<grid_for(J.np * 8, block), block, 0, stream()>>>(
           J.np, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p, x + J.in_u(), y + J.nu);
+    else if (A.st.d == 3 && J.n_phi_heavy >= 0 && 2 * J.n_phi_heavy <= J.np) {  // heavy list + light rows
+      if (J.n_phi_heavy > 0) {
+        k_spmv_phi_st_list<TPR, U, 3><<<grid_for(J.n_phi_heavy * TPR, block), block, 0, stream()>>>(
+            J.n_phi_heavy, J.phi_heavy.p, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p, x + J.in_u(),
+            y + J.nu);
+        CF_LAUNCHED();
+      }
+      k_spmv_phi_light<TPR><<<grid_for(J.np, block), block, 0, stream()>>>(J.np, J.phi_heavy_flag.p, B.ptr.p, B.col.p,
+                                                                           B.val.p, x + J.in_u(), y + J.nu);
+    }
     else if (A.st.d == 3)
       k_spmv_phi_st<TPR, U, 3><<<grid_for(threads, block), block, 0, stream()>>>(
           J.np, A.ptr.p, A.val.p, x, A.st, B.ptr.p, B.col.p, B.val.p, x + J.in_u(), y + J.nu);
@@ -1408,12 +1478,48 @@ void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add) {
 
 void csr_spmv(const Csr& A, const double* x, double* y, double) { csr_spmv_add(A, x, y, nullptr); }
 
+// classify the phi rows once per Jacobian (on the library stream: it allocates and reads a count back)
+static void phi_split(const BlockSystem& J) {
+  if (J.n_phi_heavy >= 0) return;
+  static const bool off = std::getenv("CF_NO_PHI_SPLIT") != nullptr;  // A/B switch
+  if (off || J.np == 0 || J.pu->st.kind == 0 || J.pu->st.d != 3 || J.np >= INT_MAX) {
+    J.n_phi_heavy = J.np + 1;  // never split
+    return;
+  }
+  J.phi_heavy_flag.alloc(J.np);
+  k_phi_heavy_flags<<<grid_for(J.np, 256), 256, 0, stream()>>>(J.np, J.pu->ptr.p, J.pp->ptr.p, J.phi_heavy_flag.p);
+  CF_LAUNCHED();
+  J.phi_heavy.alloc(J.np);
+  DevBuf<int> nsel(1);
+  size_t bytes = 0;
+  thrust::counting_iterator<int> it(0);
+  CF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, J.phi_heavy_flag.p, J.phi_heavy.p, nsel.p, int(J.np),
+                                     stream()));
+  DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+  CF_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, J.phi_heavy_flag.p, J.phi_heavy.p, nsel.p, int(J.np),
+                                     stream()));
+  count_launch();
+  int h = 0;
+  read_small(&h, nsel.p, sizeof(int));
+  J.n_phi_heavy = h;
+}
+
 void block_apply(const BlockSystem& J, const double* x, double* y) {
+  if (J.np > 0) phi_split(J);
   auto phi_rows = [&] {
     const double mean = J.pu->mean_hint >= 0.0 ? J.pu->mean_hint : double(J.pu->nnz) / double(J.np);
     if (mean > 64) launch_phi<16, 4>(J, x, y);
     else if (mean > 24) launch_phi<8, 4>(J, x, y);
-    else launch_phi<4, 5>(J, x, y);
+    else {
+      // batch depth of the 4-lane dispatch (CF_PHI_U=5|11|21, A/B; the summation order does not depend on it)
+      static const int pu = [] {
+        const char* e = std::getenv("CF_PHI_U");
+        return e ? std::atoi(e) : 5;
+      }();
+      if (pu == 11) launch_phi<4, 11>(J, x, y);
+      else if (pu == 21) launch_phi<4, 21>(J, x, y);
+      else launch_phi<4, 5>(J, x, y);
+    }
   };
   if (J.mf_uu) {
     // the phi rows (latency-bound gathers) run on the auxiliary stream beside the FP64-bound
