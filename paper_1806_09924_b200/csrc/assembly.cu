@@ -141,7 +141,7 @@ __global__ void k_div_by(double h, const double* __restrict__ a, i64 n, double* 
 #ifndef CF_RES_MINB
 #define CF_RES_MINB 4  // 64 registers, 32 warps per SM: 5.35 -> 4.2-4.9 ms on config 3 (A/B, bitwise the same)
 #endif
-template <int D>
+template <int D, bool SMX = true>
 __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g, const Tables* __restrict__ T, Coef cf,
                                                          const double* __restrict__ sol,
                                                          const double* __restrict__ ptil,
@@ -218,10 +218,7 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
   const double gcoef = (1.0 - cf.kap) * pt * pt + cf.kap;
   const double pphi = (cf.coupling == 0) ? pt * pt : phi * phi;
   const double w = sW[q];
-  double keep[D + 1];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double contrib[D + 1];
+  auto contribs = [&](int k, double (&contrib)[D + 1]) {
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       double val = 0.0;
@@ -234,6 +231,47 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
 #pragma unroll
     for (int b = 0; b < D; ++b) vphi += dv.div(cf.Gc * cf.eps * gphi[b] * sG[q][k][b]);
     contrib[D] = w * vphi;
+  };
+  if constexpr (D == 3 && SMX) {
+    // 3d: the q-ordered fold through shared memory instead of 8 x 4 x 8 double shuffles per thread
+    // (the shuffle pipe cost as much as the FP64 pipe): the corners go in two halves of four; lane q
+    // stores its contributions [k][a][q], then lane (k', h) of the cell sums components 2h, 2h + 1
+    // of corner k' over q = 0..7 in order (0.0 + c_0 + c_1 + ...: the same sums) and writes them
+    constexpr int XC = 4 * 4 * 9 + 8;  // doubles per cell: [corner of the half][component][q (+1)] (+8: banks)
+    __shared__ double sXf[(256 / 8) * XC];
+    double* sXc = sXf + (int(threadIdx.x) >> 3) * XC;
+    auto X = [&](int kk, int a, int qq) -> double& { return sXc[(kk * 4 + a) * 9 + qq]; };
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        double contrib[D + 1];
+        contribs(half * 4 + kk, contrib);
+#pragma unroll
+        for (int a = 0; a <= D; ++a) X(kk, a, q) = contrib[a];
+      }
+      __syncwarp();
+      const int kq = q & 3, h = q >> 2;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < NQ; ++qq) {
+        s0 += X(kq, 2 * h, qq);
+        s1 += X(kq, 2 * h + 1, qq);
+      }
+      if (valid) {
+        double* o = out + (c - c_lo) * (NV * (D + 1)) + (half * 4 + kq) * (D + 1) + 2 * h;
+        o[0] = s0;
+        o[1] = s1;
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  double keep[D + 1];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double contrib[D + 1];
+    contribs(k, contrib);
 #pragma unroll
     for (int a = 0; a <= D; ++a) {
       double s = 0.0;
