@@ -412,6 +412,17 @@ __global__ void __launch_bounds__(256) k_cell_qpstate_q(GridDesc g, const Tables
                                                         const double* __restrict__ ptil, double* __restrict__ out,
                                                         i64 c_lo, i64 c_hi) {
   constexpr int NV = 1 << D, NQ = 1 << D, NS = QS<D>::NS;
+  // element tables and the cell's corner values through shared memory: the kernel is bound by the
+  // memory-instruction pipe (table loads, 2 x 5 x 2^d shuffles and the state stores per thread), not
+  // by arithmetic; a corner value is stored once and read by the cell's lanes as a broadcast
+  __shared__ double sS[NQ][NV], sG[NQ][NV][D], sW[NQ];
+  __shared__ double sC[256 / NQ][NV][D + 2];
+  for (int i = threadIdx.x; i < NQ * NV; i += blockDim.x) {
+    const int qq = i / NV, k = i % NV;
+    sS[qq][k] = T->s[qq][k];
+    for (int b = 0; b < D; ++b) sG[qq][k][b] = T->gp[qq][k][b];
+  }
+  if (threadIdx.x < NQ) sW[threadIdx.x] = T->w[threadIdx.x];
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   const i64 c = c_lo + t / NQ;
   const int q = int(t % NQ);
@@ -428,20 +439,29 @@ __global__ void __launch_bounds__(256) k_cell_qpstate_q(GridDesc g, const Tables
     my_phi = sol[nu + v];
     my_pt = ptil[v];
   }
+  {
+    double* mine = sC[threadIdx.x / NQ][q];
+#pragma unroll
+    for (int a = 0; a < D; ++a) mine[a] = my_u[a];
+    mine[D] = my_phi;
+    mine[D + 1] = my_pt;
+  }
+  __syncthreads();  // tables and corner values
   double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   double phi = 0.0, pt = 0.0;
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    const double sk = T->s[q][k];
-    phi += sk * __shfl_sync(0xffffffffu, my_phi, k, NQ);
-    pt += sk * __shfl_sync(0xffffffffu, my_pt, k, NQ);
+    const double* ck = sC[threadIdx.x / NQ][k];
+    const double sk = sS[q][k];
+    phi += sk * ck[D];
+    pt += sk * ck[D + 1];
     double uk[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) uk[a] = __shfl_sync(0xffffffffu, my_u[a], k, NQ);
+    for (int a = 0; a < D; ++a) uk[a] = ck[a];
 #pragma unroll
     for (int b = 0; b < D; ++b)
 #pragma unroll
-      for (int a = 0; a < D; ++a) gu[a][b] += uk[a] * T->gp[q][k][b];
+      for (int a = 0; a < D; ++a) gu[a][b] += uk[a] * sG[q][k][b];
   }
   double e[3][3], sig[3][3];
 #pragma unroll
@@ -464,7 +484,7 @@ __global__ void __launch_bounds__(256) k_cell_qpstate_q(GridDesc g, const Tables
 #pragma unroll
     for (int b = 0; b < D; ++b) sig_ee += sig[a][b] * e[a][b];
   const double gcoef = (1.0 - cf.kap) * pt * pt + cf.kap;
-  const double w = T->w[q];
+  const double w = sW[q];
   if (!valid) return;
   double* o = out + (c - c_lo) * (NQ * NS) + q * NS;
   o[0] = w * gcoef;
