@@ -155,6 +155,11 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
     for (int b = 0; b < D; ++b) sG[qq][k][b] = T->G[qq][k][b];
   }
   if (threadIdx.x < NQ) sW[threadIdx.x] = T->w[threadIdx.x];
+  // 3d: per-cell exchange buffer (corner values first, then the fold of the contributions)
+  constexpr bool SM3 = D == 3 && SMX;
+  constexpr int XC = 4 * 4 * 9 + 8;  // doubles per cell: [corner of the half][component][q (+1)] (+8: banks)
+  __shared__ double sXf[SM3 ? (256 / 8) * XC : 1];
+  double* sXc = sXf + (SM3 ? (int(threadIdx.x) >> 3) * XC : 0);
   __syncthreads();
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   // list: only the listed cells (offsets from c_lo) are recomputed (assemble_residual_moved)
@@ -177,13 +182,27 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
   double gu[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
   double gphi[3] = {0, 0, 0};
   double phi = 0.0, pt = 0.0;
+  if constexpr (SM3) {  // corner q's values, read back by the cell's lanes as broadcasts
+#pragma unroll
+    for (int a = 0; a < D; ++a) sXc[q * (D + 2) + a] = my_u[a];
+    sXc[q * (D + 2) + D] = my_phi;
+    sXc[q * (D + 2) + D + 1] = my_pt;
+    __syncwarp();
+  }
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    double uk[D];
+    double uk[D], phik, ptk;
+    if constexpr (SM3) {
 #pragma unroll
-    for (int a = 0; a < D; ++a) uk[a] = __shfl_sync(0xffffffffu, my_u[a], k, NQ);
-    const double phik = __shfl_sync(0xffffffffu, my_phi, k, NQ);
-    const double ptk = __shfl_sync(0xffffffffu, my_pt, k, NQ);
+      for (int a = 0; a < D; ++a) uk[a] = sXc[k * (D + 2) + a];
+      phik = sXc[k * (D + 2) + D];
+      ptk = sXc[k * (D + 2) + D + 1];
+    } else {
+#pragma unroll
+      for (int a = 0; a < D; ++a) uk[a] = __shfl_sync(0xffffffffu, my_u[a], k, NQ);
+      phik = __shfl_sync(0xffffffffu, my_phi, k, NQ);
+      ptk = __shfl_sync(0xffffffffu, my_pt, k, NQ);
+    }
     const double sk = sS[q][k];
     phi += sk * phik;
     pt += sk * ptk;
@@ -237,9 +256,7 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
     // (the shuffle pipe cost as much as the FP64 pipe): the corners go in two halves of four; lane q
     // stores its contributions [k][a][q], then lane (k', h) of the cell sums components 2h, 2h + 1
     // of corner k' over q = 0..7 in order (0.0 + c_0 + c_1 + ...: the same sums) and writes them
-    constexpr int XC = 4 * 4 * 9 + 8;  // doubles per cell: [corner of the half][component][q (+1)] (+8: banks)
-    __shared__ double sXf[(256 / 8) * XC];
-    double* sXc = sXf + (int(threadIdx.x) >> 3) * XC;
+    __syncwarp();  // the corner values above have been read
     auto X = [&](int kk, int a, int qq) -> double& { return sXc[(kk * 4 + a) * 9 + qq]; };
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
