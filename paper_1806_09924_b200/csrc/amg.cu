@@ -1445,6 +1445,9 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
   h->nod0.alloc(A0->rows);
   h->B0.alloc(A0->rows * m);
   std::shared_ptr<Csr> A = A0;
+  // a level-0 operator most of whose rows are a lone diagonal (the phi block's active rows): its
+  // SpMVs (power iteration, residual and smoothing sweeps) run the heavy rows from a list
+  if (m == 1 && !A0->split) csr_enable_row_split(*A0);
   DevBuf<int> nod(A->rows);
   DevBuf<double> B(A->rows * m);
   if (A->rows) {
@@ -1774,6 +1777,7 @@ std::unique_ptr<Amg> build_amg(std::shared_ptr<Csr> A0, const int* node_of_dof, 
     // pattern in A, P and R); on level 0 the row-wise kernel wins (3x the threads in flight: P
     // 0.53 vs 0.58 ms, R 0.34 vs 0.36 ms on config 3), on level 1 the groups do (A 0.117 vs
     // 0.143, P 0.041 vs 0.047, R 0.043 vs 0.051 ms)
+    if (lev == 0 && m == 1) csr_enable_row_split(*L->P);  // (mostly empty rows: the active phi dofs)
     if (lev > 0) {
       L->P->grp = csr_row_groups(*L->P, 6);
       L->R->grp = csr_row_groups(*L->R, 6);

@@ -282,25 +282,25 @@ __global__ void __launch_bounds__(256, CF_RES_MINB) k_cell_residual_q(GridDesc g
       }
       __syncwarp();
     }
-    return;
-  }
-  double keep[D + 1];
+  } else {
+    double keep[D + 1];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double contrib[D + 1];
-    contribs(k, contrib);
+    for (int k = 0; k < NV; ++k) {
+      double contrib[D + 1];
+      contribs(k, contrib);
 #pragma unroll
-    for (int a = 0; a <= D; ++a) {
-      double s = 0.0;
+      for (int a = 0; a <= D; ++a) {
+        double s = 0.0;
 #pragma unroll
-      for (int qq = 0; qq < NQ; ++qq) s += __shfl_sync(0xffffffffu, contrib[a], qq, NQ);
-      if (q == k) keep[a] = s;
+        for (int qq = 0; qq < NQ; ++qq) s += __shfl_sync(0xffffffffu, contrib[a], qq, NQ);
+        if (q == k) keep[a] = s;
+      }
     }
-  }
-  if (valid) {
-    double* o = out + (c - c_lo) * (NV * (D + 1)) + q * (D + 1);
+    if (valid) {
+      double* o = out + (c - c_lo) * (NV * (D + 1)) + q * (D + 1);
 #pragma unroll
-    for (int a = 0; a <= D; ++a) o[a] = keep[a];
+      for (int a = 0; a <= D; ++a) o[a] = keep[a];
+    }
   }
 }
 

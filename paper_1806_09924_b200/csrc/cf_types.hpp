@@ -98,9 +98,19 @@ struct RowGroups {
   int gmax = 1;
 };
 
+// Rows with at most one entry (constrained dofs: the diagonal) apart from the rest (ascending list):
+// set on a level-0 operator most of whose rows are such (the phi block late in a Newton step), where
+// the SpMV runs the heavy rows from the list and the light rows one thread each.
+struct RowSplit {
+  DevBuf<int> heavy;
+  DevBuf<std::uint8_t> flag;
+  i64 n_heavy = 0;
+};
+
 struct Csr {
   i64 rows = 0, cols = 0, nnz = 0;
   std::shared_ptr<RowGroups> grp;  // optional (SpMV only; the pattern must not change while set)
+  std::shared_ptr<RowSplit> split;  // optional (SpMV only; the pattern must not change while set)
   StencilCols st;
   DevBuf<i64> ptr;
   DevBuf<int> col;
@@ -194,6 +204,7 @@ void csr_spmv(const Csr& A, const double* x, double* y, double unused = 0.0);
 void block_apply(const BlockSystem& J, const double* x, double* y);
 bool csr_spmv_variant(const Csr& A, int tpr, int unroll, const double* x, double* y);
 bool csr_enable_stencil(Csr& A, const StencilCols& sc);
+void csr_enable_row_split(Csr& A);  // sets A.split when at least half of a long matrix's rows hold <= 1 entry
 void div_by_h(double h, const double* a, i64 n, double* q);  // test hook of the residual's a / h  // CF_NO_STENCIL_COLS=1 disables
 
 inline double mat_mu(const cf_material& m) { return m.E / (2.0 * (1.0 + m.nu)); }              // model.hpp:26

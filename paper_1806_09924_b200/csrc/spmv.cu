@@ -1126,6 +1126,48 @@ __global__ void __launch_bounds__(256) k_spmv_phi_st(i64 rows, const i64* __rest
   if (row < rows && lane == 0) y[row] = s1 + s2;
 }
 
+// ---- CSR rows split by weight (RowSplit) -------------------------------------------------------
+// k_spmv_b<TPR, U> over the listed rows, and one thread per remaining row (<= 1 entry) forming the
+// sum the lanes would (lane 0's single product added to +0.0, the other lanes and the butterflies
+// adding +0.0) before the same epilogue.  Bitwise k_spmv_b<TPR, U>.
+__global__ void k_row_heavy_flags(i64 rows, const i64* __restrict__ ptr, std::uint8_t* __restrict__ f) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < rows) f[r] = ptr[r + 1] - ptr[r] > 1 ? 1 : 0;
+}
+
+template <int TPR, int U>
+__global__ void __launch_bounds__(256) k_spmv_b_list(i64 nlist, const int* __restrict__ list,
+                                                     const i64* __restrict__ ptr, const int* __restrict__ col,
+                                                     const double* __restrict__ val, const double* __restrict__ x,
+                                                     double* y, SpmvEpi ep) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 li = t / TPR;
+  const int lane = int(t % TPR);
+  double s = 0.0;
+  i64 row = 0;
+  if (li < nlist) {
+    row = list[li];
+    s = row_dot_b<TPR, U>(ptr, col, val, x, row, lane);
+  }
+  s = group_sum<TPR>(s);
+  if (li < nlist && lane == 0) y[row] = epi_out(ep, x, row, s);
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(256) k_spmv_b_light(i64 rows, const std::uint8_t* __restrict__ heavy,
+                                                      const i64* __restrict__ ptr, const int* __restrict__ col,
+                                                      const double* __restrict__ val, const double* __restrict__ x,
+                                                      double* y, SpmvEpi ep) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows || heavy[r]) return;
+  const i64 k = ptr[r];
+  double s = 0.0;
+  if (ptr[r + 1] > k) s += ld_stream(val + k) * __ldg(x + ld_stream(col + k));
+#pragma unroll
+  for (int o = TPR / 2; o > 0; o >>= 1) s += 0.0;
+  y[r] = epi_out(ep, x, r, s);
+}
+
 // ---- phi rows split by weight -------------------------------------------------------------------
 // Late in a Newton step four phi dofs in five are active: their M_phiu row is empty and their
 // M_phiphi row is the diagonal entry, while a free row carries 81 + 27 entries.  One kernel over all
@@ -1460,6 +1502,17 @@ void csr_spmv_epi(const Csr& A, const double* x, double* y, const SpmvEpi& ep) {
     else launch_grp<4, 3>(A, x, y, ep);
     return;
   }
+  if (A.split && A.st.kind == 0 && mean <= 12) {  // the <4, 3> dispatch over heavy and light rows
+    const RowSplit& S = *A.split;
+    if (S.n_heavy > 0) {
+      k_spmv_b_list<4, 3><<<grid_for(S.n_heavy * 4, 256), 256, 0, stream()>>>(S.n_heavy, S.heavy.p, A.ptr.p, A.col.p,
+                                                                              A.val.p, x, y, ep);
+      CF_LAUNCHED();
+    }
+    k_spmv_b_light<4><<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, S.flag.p, A.ptr.p, A.col.p, A.val.p, x, y, ep);
+    CF_LAUNCHED();
+    return;
+  }
   if (mean > 64) launch_b<16, 4>(A, x, y, ep);
   else if (mean > 24) {
     if (spmv_bt_ok(A)) launch_bt<8, 4>(A, x, y, ep);
@@ -1477,6 +1530,28 @@ void csr_spmv_add(const Csr& A, const double* x, double* y, const double* add) {
 }
 
 void csr_spmv(const Csr& A, const double* x, double* y, double) { csr_spmv_add(A, x, y, nullptr); }
+
+void csr_enable_row_split(Csr& A) {
+  A.split.reset();
+  static const bool off = std::getenv("CF_NO_ROW_SPLIT") != nullptr;  // A/B switch
+  if (off || A.rows < 262144 || A.rows >= INT_MAX || A.st.kind != 0 || A.grp) return;
+  auto S = std::make_shared<RowSplit>();
+  S->flag.alloc(A.rows);
+  k_row_heavy_flags<<<grid_for(A.rows, 256), 256, 0, stream()>>>(A.rows, A.ptr.p, S->flag.p);
+  CF_LAUNCHED();
+  S->heavy.alloc(A.rows);
+  DevBuf<int> nsel(1);
+  size_t bytes = 0;
+  thrust::counting_iterator<int> it(0);
+  CF_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, S->flag.p, S->heavy.p, nsel.p, int(A.rows), stream()));
+  DevBuf<unsigned char> tmp{static_cast<i64>(bytes)};
+  CF_CUDA(cub::DeviceSelect::Flagged(tmp.p, bytes, it, S->flag.p, S->heavy.p, nsel.p, int(A.rows), stream()));
+  count_launch();
+  int h = 0;
+  read_small(&h, nsel.p, sizeof(int));
+  S->n_heavy = h;
+  if (2 * S->n_heavy <= A.rows) A.split = S;
+}
 
 // classify the phi rows once per Jacobian (on the library stream: it allocates and reads a count back)
 static void phi_split(const BlockSystem& J) {
